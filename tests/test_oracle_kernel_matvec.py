@@ -1,0 +1,176 @@
+"""Pins for the oracle's kernel entries, cell list and matvec (CPU only).
+
+Each check ties the oracle to something other than itself: SPEC worked
+examples, closed forms (Poisson summation of the lattice Gaussian), brute-force
+membership scans in numpy, integer lattice counts, and the S:333 tail bound.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import rbf_workloads as W
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "lattice_constants.json")))
+
+
+# --------------------------------------------------------------- kernel (Eq.12)
+
+def test_phi_worked_examples():
+    # sigma=0.01, r=0 -> 1/(2 pi 1e-4); r = 2 sigma -> phi(0) e^-2
+    assert O.phi(0.01, 0.0) == pytest.approx(GOLD["phi_sigma001_r0"], rel=2e-16 * 4)
+    assert O.phi(0.01, 4e-4) == pytest.approx(GOLD["phi_sigma001_r2sigma"], rel=1e-11)
+    # closed form of the normalisation for other sigma
+    for s in (0.3, 1e-3, 7.8125e-4):
+        assert O.phi(s, 0.0) == pytest.approx(1.0 / (2.0 * math.pi * s * s), rel=1e-15)
+
+
+def test_phi_decay_and_cutoff_round_trip():
+    s = 0.025
+    vals = [O.phi(s, (k * 0.1 * s) ** 2) for k in range(80)]
+    assert all(a > b for a, b in zip(vals, vals[1:]))
+    for t in (math.exp(-2.0), math.exp(-8.0), 1e-6, 0.5):
+        r = O.cutoff_radius(s, t)
+        assert O.phi(s, r * r) / O.phi(s, 0.0) == pytest.approx(t, rel=1e-12)
+    assert O.cutoff_radius(s, math.exp(-2.0)) == pytest.approx(2 * s, rel=1e-14)
+    assert O.cutoff_radius(s, math.exp(-8.0)) == pytest.approx(4 * s, rel=1e-14)
+
+
+def test_gaussian_integrates_to_one():
+    # Riemann sum of phi on a fine lattice (h = sigma/3) = 1 up to the Poisson alias
+    s = 1.0
+    h = s / 3.0
+    m = np.arange(-60, 61) * h
+    X, Y = np.meshgrid(m, m)
+    total = sum(O.phi(s, float(r2)) for r2 in (X * X + Y * Y).ravel()[::1]) * h * h
+    assert total == pytest.approx(1.0, abs=1e-13)
+
+
+# ----------------------------------------------------------------- cell list
+
+def _brute_cells(xy, box, cell):
+    ncx, ncy = O.grid_dims(box, cell)
+    cx = np.clip(np.floor((xy[:, 0] - box[0]) / cell), 0, ncx - 1).astype(np.int64)
+    cy = np.clip(np.floor((xy[:, 1] - box[1]) / cell), 0, ncy - 1).astype(np.int64)
+    return cy * ncx + cx, ncx, ncy
+
+
+@pytest.mark.parametrize("wl", [W.make_lattice(24), W.make_lattice(40, jitter_frac=0.1, seed=7),
+                                W.make_clustered(3000, seed=11)])
+def test_cell_list_partition_and_membership(wl):
+    key, perm, start = O.cell_list(wl.xy, wl.box, wl.cell)
+    bkey, ncx, ncy = _brute_cells(wl.xy, wl.box, wl.cell)
+    assert np.array_equal(key, bkey)
+    assert start[0] == 0 and start[-1] == wl.n and np.all(np.diff(start) >= 0)
+    assert np.array_equal(np.sort(perm), np.arange(wl.n))  # partition: each point once
+    for c in range(ncx * ncy):
+        members = perm[start[c]:start[c + 1]]
+        assert np.all(bkey[members] == c)
+        assert np.all(np.diff(members) > 0)  # stable: ascending caller index
+
+
+def test_cell_counts_cfg1_and_ragged():
+    wl = W.config(1)
+    _, _, start = O.cell_list(wl.xy, wl.box, wl.cell)
+    assert O.grid_dims(wl.box, wl.cell) == (20, 20)
+    assert np.all(np.diff(start) == 25)
+    # 24x24 lattice: 24/5 = 4.8 -> 5 cells per axis, last column 4 points wide
+    wl = W.make_lattice(24)
+    _, _, start = O.cell_list(wl.xy, wl.box, wl.cell)
+    cnt = np.diff(start).reshape(5, 5)
+    assert cnt[0, 0] == 25 and cnt[0, 4] == 20 and cnt[4, 0] == 20 and cnt[4, 4] == 16
+
+
+# ----------------------------------------------------------------- matvec
+
+def _theta2(h, s):
+    """Poisson summation: h^2 sum_{m in Z^2} G_s(mh) = (sum_k exp(-2 pi^2 s^2 k^2/h^2))^2."""
+    th = 1.0 + 2.0 * sum(math.exp(-2.0 * math.pi ** 2 * s * s * k * k / (h * h)) for k in range(1, 6))
+    return th * th
+
+
+def test_constant_field_exact_and_cutoff():
+    wl = W.config(1)
+    h = wl.meta["h"]
+    centre = [50 * 100 + 50, 45 * 100 + 55, 60 * 100 + 40]  # >= 0.8 from the edge (32 sigma)
+    ones = np.ones(wl.n)
+    y_ex = O.matvec_brute(wl.xy, ones, wl.sigma, None, rows=centre)
+    y_ct = O.matvec_brute(wl.xy, ones, wl.sigma, wl.rc, rows=centre)
+    alpha = _theta2(h, wl.sigma) - 1.0
+    assert alpha == pytest.approx(GOLD["alias_alpha"], rel=1e-6)  # two independent derivations
+    for v in h * h * y_ex:
+        assert v - 1.0 == pytest.approx(alpha, abs=2e-15)
+    for v in h * h * y_ct:
+        assert v - 1.0 == pytest.approx(alpha - GOLD["tail_t"], abs=2e-15)
+
+
+def test_pairs_per_point_lattice():
+    wl = W.config(1)
+    assert O.count_pairs(wl.xy, wl.rc, wl.box, wl.cell) == GOLD["cfg1_pairs"]
+    m = np.arange(-10, 11)
+    M1, M2 = np.meshgrid(m, m)
+    assert int(np.sum(M1 ** 2 + M2 ** 2 < 56.25)) == GOLD["interior_pairs_per_point"]
+    # exact count for an n x n lattice: sum over offsets m with |m|^2 < 56.25 of
+    # (n - |m1|)(n - |m2|) ordered pairs; pairs per point -> 177 as n grows (O(N))
+    inside = (M1 ** 2 + M2 ** 2) < 56.25
+    for n in (100, 200):
+        wl2 = W.make_lattice(n)
+        expect = int(np.sum(((n - np.abs(M1)) * (n - np.abs(M2)))[inside]))
+        assert O.count_pairs(wl2.xy, wl2.rc, wl2.box, wl2.cell) == expect
+
+
+def test_unit_vector_column():
+    # x = e_j -> y_i = phi(|x_i - x_j|^2) inside the cutoff, exactly 0 outside
+    wl = W.make_lattice(30, jitter_frac=0.1, seed=3)
+    j = 437
+    e = np.zeros(wl.n)
+    e[j] = 1.0
+    y = O.matvec_brute(wl.xy, e, wl.sigma, wl.rc)
+    d = wl.xy - wl.xy[j]
+    r2 = d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]
+    inside = r2 < wl.rc ** 2
+    assert np.all(y[~inside] == 0.0)
+    expect = np.exp(-r2[inside] / (2 * wl.sigma ** 2)) / (2 * math.pi * wl.sigma ** 2)
+    assert np.allclose(y[inside], expect, rtol=1e-14, atol=0)
+
+
+@pytest.mark.parametrize("wl", [W.make_lattice(33, jitter_frac=0.1, seed=5),
+                                W.make_clustered(2500, seed=9)])
+def test_cells_matches_brute_symmetry_linearity(wl):
+    rng = np.random.default_rng(0)
+    u, w = rng.standard_normal(wl.n), rng.standard_normal(wl.n)
+    yb = O.matvec_brute(wl.xy, w, wl.sigma, wl.rc)
+    yc = O.matvec_cells(wl.xy, w, wl.sigma, wl.rc, wl.box, wl.cell)
+    assert np.linalg.norm(yb - yc) / np.linalg.norm(yb) < 1e-14
+    Au = O.matvec_brute(wl.xy, u, wl.sigma, wl.rc)
+    assert np.dot(u, yb) == pytest.approx(np.dot(Au, w), rel=1e-12)
+    ylin = O.matvec_brute(wl.xy, 2.0 * u - 3.0 * w, wl.sigma, wl.rc)
+    assert np.linalg.norm(ylin - (2.0 * Au - 3.0 * yb)) / np.linalg.norm(ylin) < 1e-13
+    assert np.all(O.matvec_brute(wl.xy, np.zeros(wl.n), wl.sigma, wl.rc) == 0.0)
+
+
+def test_truncation_tail_bound():
+    # |y_exact - y_cut|_i <= ||w||_inf * neglected_row_mass(i)
+    wl = W.make_clustered(1500, seed=4)
+    rng = np.random.default_rng(1)
+    w = rng.uniform(-1, 1, wl.n)
+    rows = np.arange(wl.n)
+    ye = O.matvec_brute(wl.xy, w, wl.sigma, None)
+    yc = O.matvec_brute(wl.xy, w, wl.sigma, wl.rc)
+    mass = O.neglected_row_mass(wl.xy, wl.sigma, wl.rc, rows)
+    assert np.all(np.abs(ye - yc) <= np.max(np.abs(w)) * mass * (1 + 1e-12) + 1e-300)
+    # and the mass is below the continuum tail exp(-rc^2/2sigma^2) times the point density bound
+    assert np.all(mass >= 0.0)
+
+
+def test_dense_assembly_symmetric_spd():
+    wl = W.make_lattice(12, jitter_frac=0.1, seed=1)
+    A = O.assemble_dense(wl.xy, wl.sigma, wl.rc)
+    assert np.array_equal(A, A.T)
+    np.linalg.cholesky(A)
+    Ae = O.assemble_dense(wl.xy, wl.sigma, None)
+    assert np.array_equal(Ae, Ae.T)
+    assert np.all(Ae >= A)

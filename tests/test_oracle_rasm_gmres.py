@@ -1,0 +1,235 @@
+"""Pins for the oracle's RASM preconditioner, dense factorizations, GMRES and
+full solve (CPU only).
+
+The RASM pin builds Eq.(11) M^-1 = sum_i R~_i^T A_i^-1 R_i literally from 0/1
+restriction matrices found by a brute-force membership scan in numpy
+(SPEC S:392); the solve pins are the dense direct solve and the deconvolution
+closed form G_sigma * G_tau = G_s ([D3]).
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import rbf_workloads as W
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "lattice_constants.json")))
+
+
+def _cells(xy, box, cell):
+    ncx, ncy = O.grid_dims(box, cell)
+    cx = np.clip(np.floor((xy[:, 0] - box[0]) / cell), 0, ncx - 1).astype(np.int64)
+    cy = np.clip(np.floor((xy[:, 1] - box[1]) / cell), 0, ncy - 1).astype(np.int64)
+    return cx, cy, ncx, ncy
+
+
+def _explicit_minv(xy, sigma, rc, box, cell, rings, variant="rasm"):
+    """Eq.(5),(9),(11) with explicit 0/1 matrices (N small)."""
+    n = xy.shape[0]
+    d = xy[:, None, :] - xy[None, :, :]
+    r2 = d[..., 0] ** 2 + d[..., 1] ** 2
+    A = np.where(r2 < rc * rc, np.exp(-r2 / (2 * sigma * sigma)) / (2 * math.pi * sigma * sigma), 0.0)
+    cx, cy, ncx, ncy = _cells(xy, box, cell)
+    Minv = np.zeros((n, n))
+    for c in range(ncx * ncy):
+        ccx, ccy = c % ncx, c // ncx
+        own = np.nonzero((cx == ccx) & (cy == ccy))[0]
+        if own.size == 0:
+            continue
+        ov = np.nonzero((np.abs(cx - ccx) <= rings) & (np.abs(cy - ccy) <= rings))[0]
+        R = np.zeros((ov.size, n)); R[np.arange(ov.size), ov] = 1.0
+        Ai = R @ A @ R.T
+        if variant == "rasm":
+            Rt = np.zeros((ov.size, n))
+            for q, j in enumerate(ov):
+                if j in set(own.tolist()):
+                    Rt[q, j] = 1.0
+        else:
+            Rt = R
+        Minv += Rt.T @ np.linalg.inv(Ai) @ R
+    return Minv, A
+
+
+@pytest.mark.parametrize("wl,rings", [(W.make_lattice(14, jitter_frac=0.1, seed=3), 1),
+                                      (W.make_lattice(17), 1),
+                                      (W.make_lattice(15, jitter_frac=0.3, seed=2), 1),
+                                      (W.make_lattice(14), 0)])
+def test_rasm_equals_explicit_eq11(wl, rings):
+    Minv, _ = _explicit_minv(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, rings)
+    P = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, rings)
+    assert P.status == 0
+    rng = np.random.default_rng(4)
+    for _ in range(3):
+        r = rng.standard_normal(wl.n)
+        z = P.apply(r)
+        ref = Minv @ r
+        assert np.linalg.norm(z - ref) / np.linalg.norm(ref) < 1e-11
+    P.close()
+
+
+def test_asm_equals_explicit_eq8():
+    wl = W.make_lattice(14, jitter_frac=0.1, seed=8)
+    Minv, _ = _explicit_minv(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, 1, variant="asm")
+    P = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, 1)
+    r = np.random.default_rng(5).standard_normal(wl.n)
+    ref = Minv @ r
+    assert np.linalg.norm(P.apply(r, "asm") - ref) / np.linalg.norm(ref) < 1e-11
+
+
+def test_single_subdomain_is_exact_inverse():
+    # Eq.(11) with p = 1, R = R~ = I: M^-1 = A_rc^-1
+    wl = W.make_lattice(12, jitter_frac=0.1, seed=6)
+    P = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, 4.0, 0)
+    assert P.nsub == 1
+    A = O.assemble_dense(wl.xy, wl.sigma, wl.rc)
+    r = np.random.default_rng(7).standard_normal(wl.n)
+    ref = np.linalg.solve(A, r)
+    assert np.linalg.norm(P.apply(r) - ref) / np.linalg.norm(ref) < 1e-10
+
+
+def test_rasm_partition_property_and_index_sets():
+    wl = W.make_lattice(30, jitter_frac=0.1, seed=1)
+    P = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, 1)
+    cx, cy, ncx, ncy = _cells(wl.xy, wl.box, wl.cell)
+    rng = np.random.default_rng(2)
+    r = rng.standard_normal(wl.n)
+    z = P.apply(r)
+    nonempty = [c for c in range(ncx * ncy) if np.any((cx == c % ncx) & (cy == c // ncx))]
+    assert P.nsub == len(nonempty)
+    for s in (0, 7, P.nsub - 1):
+        c = nonempty[s]
+        ov, own_pos = P.subdomain(s)
+        # R_c: 3x3 block row-major, ascending caller index within each cell
+        expect = []
+        for by in range(c // ncx - 1, c // ncx + 2):
+            for bx in range(c % ncx - 1, c % ncx + 2):
+                if 0 <= bx < ncx and 0 <= by < ncy:
+                    expect += list(np.nonzero((cx == bx) & (cy == by))[0])
+        assert list(ov) == expect
+        own = ov[own_pos]
+        assert set(own.tolist()) == set(np.nonzero((cx == c % ncx) & (cy == c // ncx))[0].tolist())
+        # z on own(c) depends only on r on Omega_c: perturb the rest
+        r2 = r + rng.standard_normal(wl.n)
+        r2[ov] = r[ov]
+        z2 = P.apply(r2)
+        assert np.array_equal(z[own], z2[own])
+    P.close()
+
+
+def test_dense_factor_examples_and_lu_fallback():
+    x, lu = O.dense_factor_solve(np.diag([2.0, 3.0]), np.array([2.0, 3.0]))
+    assert not lu and np.allclose(x, [1.0, 1.0], rtol=0, atol=1e-15)
+    x, lu = O.dense_factor_solve(np.eye(3), np.array([1.0, -2.0, 5.0]))
+    assert np.array_equal(x, [1.0, -2.0, 5.0])
+    # symmetric indefinite -> Cholesky breaks down -> LU with partial pivoting
+    A = np.array([[1.0, 2.0, 0.0], [2.0, 1.0, 1.0], [0.0, 1.0, 3.0]])
+    b = np.array([1.0, 0.0, -1.0])
+    x, lu = O.dense_factor_solve(A, b)
+    assert lu and np.allclose(A @ x, b, rtol=0, atol=1e-14)
+    rng = np.random.default_rng(3)
+    G = rng.standard_normal((20, 20))
+    A = G @ G.T + 20 * np.eye(20)
+    b = rng.standard_normal(20)
+    x, lu = O.dense_factor_solve(A, b)
+    assert not lu and np.linalg.norm(A @ x - b) / np.linalg.norm(b) < 1e-12
+    with pytest.raises(ArithmeticError):
+        O.dense_factor_solve(np.zeros((2, 2)), np.ones(2))
+
+
+# ----------------------------------------------------------------- GMRES (Q12)
+
+def test_gmres_identity_one_iteration():
+    b = np.random.default_rng(0).standard_normal(40)
+    res = O.gmres(O.op_identity(40), O.op_identity(40), b)
+    assert res.iterations == 1 and res.converged
+    assert np.allclose(res.x, b, rtol=1e-15, atol=0)
+
+
+def test_gmres_zero_rhs():
+    res = O.gmres(O.op_identity(10), O.op_identity(10), np.zeros(10))
+    assert res.iterations == 0 and res.converged and np.all(res.x == 0)
+
+
+def test_gmres_spd_vs_dense_and_invariants():
+    rng = np.random.default_rng(1)
+    G = rng.standard_normal((50, 50))
+    A = G @ G.T + 5 * np.eye(50)
+    b = rng.standard_normal(50)
+    res = O.gmres(O.op_dense(A), O.op_identity(50), b, restart=60, rtol=1e-14)
+    ref = np.linalg.solve(A, b)
+    assert res.converged
+    assert np.linalg.norm(res.x - ref) / np.linalg.norm(ref) < 1e-10
+    # recurrence residual non-increasing inside a cycle
+    assert np.all(np.diff(res.history) <= 1e-15)
+    # restarted run: orthonormal Krylov basis of the last cycle
+    res = O.gmres(O.op_dense(A), O.op_identity(50), b, restart=12, rtol=1e-12, keep_basis=True)
+    V = res.basis
+    G2 = V @ V.T
+    assert np.max(np.abs(G2 - np.eye(V.shape[0]))) < 1e-8
+    assert res.restarts >= 1 and res.converged
+    assert np.linalg.norm(A @ res.x - b) / np.linalg.norm(b) < 1e-9
+
+
+def test_gmres_exact_inverse_pc_two_iterations():
+    # Q19: with M = A^-1, M^-1 A = I up to eps*kappa -> <= 2 iterations
+    rng = np.random.default_rng(2)
+    G = rng.standard_normal((30, 30))
+    A = G @ G.T + np.eye(30)
+    res = O.gmres(O.op_dense(A), O.op_dense(np.linalg.inv(A)), rng.standard_normal(30), rtol=1e-13)
+    assert res.converged and res.iterations <= 2
+
+
+def test_gmres_not_converged_status():
+    rng = np.random.default_rng(3)
+    A = np.diag(np.linspace(1.0, 1e4, 200))
+    res = O.gmres(O.op_dense(A), O.op_identity(200), rng.standard_normal(200), restart=5,
+                  max_iters=7, rtol=1e-14)
+    assert not res.converged and res.status == O.ORC_NOT_CONVERGED and res.iterations == 7
+
+
+# ----------------------------------------------------------------- full solve
+
+@pytest.fixture(scope="module")
+def cfg1_solution():
+    wl = W.config(1)
+    res = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, rtol=wl.tol)
+    lam = O.dense_solve(wl.xy, wl.f, wl.sigma, wl.rc)
+    return wl, res, lam
+
+
+def test_cfg1_solve_vs_dense_direct(cfg1_solution):
+    wl, res, lam = cfg1_solution
+    assert res.converged
+    assert abs(res.iterations - GOLD["cfg1_iterations_model"]) <= 2
+    assert np.linalg.norm(res.x - lam) / np.linalg.norm(lam) < 1e-9  # [D3]: 1.6e-10
+    assert res.resid_true < 1e-10
+    # interpolation conditions at the data (Eq.(2))
+    s = O.matvec_brute(wl.xy, res.x, wl.sigma, wl.rc)
+    assert np.linalg.norm(s - wl.f) / np.linalg.norm(wl.f) < 1e-10
+
+
+def test_cfg1_deconvolution_closed_form(cfg1_solution):
+    # G_sigma * G_tau = G_s (tau^2 = s^2 - sigma^2): lambda_j ~ h^2 G_tau(x_j) / (1 + alpha - t)
+    wl, res, lam = cfg1_solution
+    h, s2 = wl.meta["h"], wl.meta["s2"]
+    tau2 = s2 - wl.sigma ** 2
+    r2 = np.sum(wl.xy ** 2, axis=1)
+    closed = h * h * np.exp(-r2 / (2 * tau2)) / (2 * math.pi * tau2)
+    closed /= 1.0 + GOLD["alias_alpha"] - GOLD["tail_t"]
+    inner = np.max(np.abs(wl.xy), axis=1) <= 0.4
+    dev = np.max(np.abs(res.x[inner] - closed[inner])) / np.max(np.abs(res.x))
+    assert dev < 3 * GOLD["cfg1_closed_form_dev_x04"]
+
+
+def test_mesh_independent_iterations():
+    # the iteration count does not change with N at fixed ratios
+    its = []
+    for n in (40, 80):
+        wl = W.make_lattice(n, rhs="gauss", s2=0.05)
+        res = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, rtol=1e-13)
+        assert res.converged
+        its.append(res.iterations)
+    assert abs(its[0] - its[1]) <= 3
