@@ -1,0 +1,202 @@
+/*
+ * rbf.h -- C ABI of librbf.so, the B200 (sm_100a) hot path of PetRBF
+ * (Yokota, Barba, Knepley, "PetRBF -- A parallel O(N) algorithm for radial
+ * basis function interpolation", arXiv 0909.5413; PAPER.md line numbers are
+ * cited as P:<line>).
+ *
+ * The library solves the Gaussian RBF interpolation problem of Eqs.(1)-(4)
+ * without polynomial part (the Gaussian is positive definite,
+ * P:81):   A_rc lambda = f,   A_ij = exp(-|x_i-x_j|^2/(2 sigma^2))/(2 pi sigma^2)
+ * (Eq.(12)) truncated to pairs with |x_i-x_j| < rc (reading
+ * Q1 of DESIGN.md), by GMRES left-preconditioned with the restricted
+ * additive Schwarz method M^-1 = sum_i R~_i^T A_i^-1 R_i (Eq.(11)),
+ * one subdomain per cell of a uniform cell grid, overlap = rings of
+ * neighbouring cells (reading Q9).
+ *
+ * Conventions (all entry points):
+ *  - Every pointer argument named *_dev is DEVICE memory of the current CUDA
+ *    device; *_host is host memory.  The caller owns every buffer it passes and
+ *    keeps it alive until the stream work that uses it has completed.
+ *  - All device work is enqueued on `stream` (a cudaStream_t passed as void*,
+ *    NULL = legacy default stream); calls that return results to the host
+ *    (reports, counts) synchronise that stream.
+ *  - Vectors are RANK-LOCAL and in LIBRARY (cell-sorted) ORDER: entry s of a
+ *    local vector belongs to caller point rbf_local_index()[s].  A single-GPU
+ *    run has one rank owning all N points.
+ *  - fp64 throughout.  N < 2^31.  A context is not thread-safe.
+ *  - Return value: RBF_OK (0) on success, RBF_NOT_CONVERGED (2) when a solve
+ *    stopped at max_iters (the last iterate is returned), or a
+ *    negative error code; rbf_last_error() then holds a thread-local message.
+ *    There is no CPU fallback: without a usable CUDA device every call fails
+ *    with RBF_ECUDA.
+ */
+#ifndef RBF_H
+#define RBF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rbf_ctx rbf_ctx; /* opaque, owned by the library */
+
+enum {
+  RBF_OK = 0,
+  RBF_NOT_CONVERGED = 2,
+  RBF_EINVAL = -1,      /* invalid argument (message names it)                    */
+  RBF_ENOMEM = -2,      /* device allocation failed                                */
+  RBF_ECUDA = -3,       /* CUDA runtime error                                      */
+  RBF_ENCCL = -4,       /* NCCL error                                              */
+  RBF_EFACTOR = -5,     /* zero pivot even after the LU fallback; message names the cell */
+  RBF_ENUMERIC = -6,    /* NaN/Inf produced                                        */
+  RBF_EUNSUPPORTED = -7 /* valid input this build does not handle (message says why) */
+};
+
+/* Geometry and kernel parameters (readings Q1, Q5, Q9).
+ *  sigma          Gaussian width, > 0 (Eq.(12)).
+ *  cell           cell side c > 0; cells tile the box from (x0, y0):
+ *                 ncx = ceil((x1-x0)/c), ncy = ceil((y1-y0)/c);
+ *                 cell of a point: cx = clamp(floor((x-x0)/c), 0, ncx-1), same for y;
+ *                 cells are numbered key = cy*ncx + cx (row-major).
+ *  rc             per-pair cutoff radius > 0: pair (i,j) enters A_rc iff
+ *                 fma(dx,dx,dy*dy) < rc*rc (reading Q1).
+ *  overlap_rings  >= 0: Omega_c = the (2r+1)^2 block of cells around cell c,
+ *                 clipped to the grid (reading Q9); 0 = block Jacobi.
+ *  x0,y0,x1,y1    domain box; every point must satisfy x0 <= x <= x1, y0 <= y <= y1. */
+typedef struct {
+  double sigma;
+  double cell;
+  double rc;
+  int32_t overlap_rings;
+  int32_t reserved0;
+  double x0, y0, x1, y1;
+} rbf_params;
+
+/* Domain decomposition into strips of cell rows.
+ *  rank, nranks   this process's strip and the strip count (1 <= nranks).
+ *  comm           RBF_COMM_NCCL: halos/reductions go through an NCCL communicator
+ *                 created from nccl_id (one process per GPU; the caller selects the
+ *                 device first).  RBF_COMM_NONE: "virtual strip" -- the context owns
+ *                 strip `rank` of `nranks` but never communicates; only the *_ext
+ *                 entry points (caller-supplied halos) are usable.
+ *  nccl_id        from rbf_get_nccl_id() on rank 0, broadcast by the caller. */
+enum { RBF_COMM_NONE = 0, RBF_COMM_NCCL = 1 };
+typedef struct {
+  int32_t rank;
+  int32_t nranks;
+  int32_t comm;
+  int32_t reserved0;
+  unsigned char nccl_id[128];
+} rbf_dist;
+
+/* GMRES parameters (reading Q12).
+ *  restart    m >= 1 (30).      max_iters  >= 1 (1000).
+ *  rtol, atol >= 0: stop when the recurrence residual |g_{k+1}| <= max(rtol*||M^-1 f||, atol).
+ *  timing     nonzero: record per-phase CUDA-event times into the report (adds events). */
+typedef struct {
+  int32_t restart;
+  int32_t max_iters;
+  double rtol;
+  double atol;
+  int32_t timing;
+  int32_t reserved0;
+} rbf_gmres_params;
+
+/* Solve report.  Residuals are relative: resid_est = |g|/||M^-1 f|| (recurrence),
+ * resid_precond = ||M^-1(f - A lambda)||/||M^-1 f||, resid_true = ||f - A lambda||/||f||.
+ * Phase times (ms, when timing != 0) follow the paper's breakdown.
+ * history: optional caller array (host) of history_cap doubles receiving resid_est
+ * after each iteration; history_len = entries written. */
+typedef struct {
+  int32_t iterations;
+  int32_t converged;
+  int32_t restarts;
+  int32_t status;
+  double resid_est, resid_precond, resid_true, beta0;
+  double ms_setup, ms_matmult, ms_pcapply, ms_orth, ms_total;
+  int64_t n_pairs;      /* in-cutoff pairs of this rank's rows (filled by rbf_count_pairs) */
+  int64_t n_cells;      /* non-empty owned cells = subdomains of this rank */
+  int64_t bytes_device; /* device bytes held by the context */
+  double *history;
+  int32_t history_cap;
+  int32_t history_len;
+} rbf_report;
+
+/* NCCL unique id for a multi-GPU context (call on rank 0 only). */
+int rbf_get_nccl_id(unsigned char out[128]);
+
+/* Build the cell list, choose this rank's strip, and set up the
+ * RASM preconditioner: per non-empty owned cell assemble A_c = R_c A_rc R_c^T,
+ * factor it (Cholesky; LU with partial pivoting on breakdown, reading Q11)
+ * and store the rows of A_c^-1 belonging to the cell's own points (PCSetUp).
+ *  xy_dev  N x 2 interleaved fp64 (x0,y0,x1,y1,...) in caller order; every rank
+ *          passes the full, identical point set.  Copied; may be freed afterwards.
+ *  dist    NULL = single GPU.
+ * Errors: EINVAL (n < 1, non-finite or out-of-box points, bad params, strips
+ * thinner than the halo), ENOMEM, EFACTOR, ECUDA, ENCCL, EUNSUPPORTED (a
+ * subdomain larger than this build's local-solve limit). */
+int rbf_setup(rbf_ctx **ctx, const double *xy_dev, int64_t n, const rbf_params *p,
+              const rbf_dist *dist, void *stream);
+
+/* Rank-local sizes: owned points, and the extended range (owned + halo rows). */
+int64_t rbf_local_count(const rbf_ctx *ctx);
+int64_t rbf_ext_count(const rbf_ctx *ctx);
+/* Position of this rank's owned / extended points in the GLOBAL sorted order:
+ * out[0] = ext_lo, out[1] = own_lo, out[2] = own_hi, out[3] = ext_hi. */
+int rbf_ranges(const rbf_ctx *ctx, int64_t out[4]);
+/* idx_dev[s] (int64, rbf_local_count entries) = caller index of local entry s. */
+int rbf_local_index(const rbf_ctx *ctx, int64_t *idx_dev, void *stream);
+/* Global cell list export (tests): perm_dev (int64, N) = caller index of global sorted
+ * entry s; cell_start_dev (int64, ncx*ncy+1).  dims_host[0..1] = ncx, ncy. */
+int rbf_cell_list(const rbf_ctx *ctx, int64_t *perm_dev, int64_t *cell_start_dev,
+                  int64_t dims_host[2], void *stream);
+/* Permute a caller-order vector (N entries, device) into this rank's local order,
+ * and back (scatter writes only this rank's entries). */
+int rbf_to_local(const rbf_ctx *ctx, const double *v_caller_dev, double *v_loc_dev, void *stream);
+int rbf_from_local(const rbf_ctx *ctx, const double *v_loc_dev, double *v_caller_dev, void *stream);
+
+/* y = A_rc w on this rank's points (MatMult): halo exchange of w
+ * (ceil(rc/c) cell rows from each strip neighbour) then the cutoff matvec. */
+int rbf_matvec(rbf_ctx *ctx, const double *w_loc_dev, double *y_loc_dev, void *stream);
+/* z = M^-1 r (PCApply / MatSolve, Eq.(10)-(11)): halo exchange of r
+ * (overlap_rings rows), then z[own(c)] = (A_c^-1 R_c r)[own(c)] for every cell. */
+int rbf_rasm_apply(rbf_ctx *ctx, const double *r_loc_dev, double *z_loc_dev, void *stream);
+/* Same two operators with the halo supplied by the caller: w_ext_dev holds
+ * rbf_ext_count() entries = global sorted entries [ext_lo, ext_hi). */
+int rbf_matvec_ext(rbf_ctx *ctx, const double *w_ext_dev, double *y_loc_dev, void *stream);
+int rbf_rasm_apply_ext(rbf_ctx *ctx, const double *r_ext_dev, double *z_loc_dev, void *stream);
+
+/* Solve A_rc lambda = f (KSPSolve): left-preconditioned restarted
+ * GMRES(m) with modified Gram-Schmidt and Givens rotations, x0 = 0 (reading Q12).
+ * f_loc_dev, lambda_loc_dev: rank-local, library order.  rep may be NULL.
+ * A zero right-hand side returns lambda = 0 after 0 iterations. */
+int rbf_solve(rbf_ctx *ctx, const double *f_loc_dev, const rbf_gmres_params *g,
+              double *lambda_loc_dev, rbf_report *rep, void *stream);
+
+/* One-call interpolation with HOST buffers in caller order (single GPU):
+ * copies xy/f to the device, rbf_setup, rbf_solve, copies lambda back. */
+int rbf_interpolate_host(const double *xy_host, const double *f_host, int64_t n,
+                         const rbf_params *p, const rbf_gmres_params *g,
+                         double *lambda_host, rbf_report *rep, void *stream);
+
+/* In-cutoff pair count of this rank's rows (for Gpairs/s; synchronises). */
+int rbf_count_pairs(rbf_ctx *ctx, int64_t *n_pairs, void *stream);
+
+/* Deterministic local dot product and norm (GMRES building blocks, exported for
+ * tests): *out_host = <a, b> over this rank's entries, summed in a fixed order. */
+int rbf_dot(rbf_ctx *ctx, const double *a_dev, const double *b_dev, double *out_host, void *stream);
+
+/* Strip planner (host only, no GPU): cell-row boundaries row_bounds[0..nranks]
+ * for ncy rows with row_counts[r] points, balanced by cumulative count, each
+ * strip at least min_rows rows.  Returns EINVAL if impossible. */
+int rbf_plan_strips(const int64_t *row_counts, int64_t ncy, int32_t nranks, int64_t min_rows,
+                    int64_t *row_bounds);
+
+const char *rbf_last_error(void);
+void rbf_destroy(rbf_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RBF_H */

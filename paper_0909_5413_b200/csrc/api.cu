@@ -1,0 +1,384 @@
+// api.cu -- the C ABI of librbf.so (include/rbf.h): context lifecycle, validation,
+// strip planning, and the thin wrappers around the kernels.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+namespace rbf {
+
+static thread_local std::string g_err;
+
+void set_error(const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+long long n_loc(const rbf_ctx *c) { return c->s.own_hi - c->s.own_lo; }
+long long n_ext(const rbf_ctx *c) { return c->s.ext_hi - c->s.ext_lo; }
+int owned_cells(const rbf_ctx *c) { return (c->s.row_hi - c->s.row_lo) * c->g.ncx; }
+
+// Stream-ordered allocations from the device's default memory pool.  The pool keeps
+// freed memory (release threshold = max), so repeated setup/solve cycles do not
+// return memory to the driver between steps.
+int dalloc(rbf_ctx *c, void **p, size_t bytes, cudaStream_t s) {
+  static bool pool_configured = false;
+  if (!pool_configured) {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_configured = true;
+  }
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMallocAsync(p, bytes, s);
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    set_error("device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? RBF_ENOMEM : RBF_ECUDA;
+  }
+  if (c) c->bytes += (long long)bytes;
+  return RBF_OK;
+}
+
+void dfree(void *p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);
+}
+
+int gather_positions(rbf_ctx *c, const double *xy, cudaStream_t s);  // cells.cu
+
+static int plan_strips(const long long *counts, long long ncy, int P, long long min_rows,
+                       long long *b) {
+  long long N = 0;
+  for (long long r = 0; r < ncy; ++r) N += counts[r];
+  if (P < 1 || (long long)P * min_rows > ncy) {
+    set_error("cannot cut %lld cell rows into %d strips of >= %lld rows", ncy, P, min_rows);
+    return RBF_EINVAL;
+  }
+  b[0] = 0;
+  b[P] = ncy;
+  long long cum = 0, r = 0;
+  for (int g = 1; g < P; ++g) {
+    const long long target = (N * g + P / 2) / P;
+    while (r < ncy && cum + counts[r] <= target) cum += counts[r++];
+    // choose the closer of r and r+1
+    if (r < ncy && (target - cum) > (cum + counts[r] - target)) cum += counts[r++];
+    b[g] = r;
+  }
+  for (int g = 1; g < P; ++g)
+    if (b[g] < b[g - 1] + min_rows) b[g] = b[g - 1] + min_rows;
+  for (int g = P - 1; g >= 1; --g)
+    if (b[g] > b[g + 1] - min_rows) b[g] = b[g + 1] - min_rows;
+  for (int g = 0; g < P; ++g)
+    if (b[g + 1] - b[g] < min_rows) {
+      set_error("strip %d has fewer than %lld cell rows", g, min_rows);
+      return RBF_EINVAL;
+    }
+  return RBF_OK;
+}
+
+static int validate(const rbf_params *p, long long n) {
+  if (!p) { set_error("params is NULL"); return RBF_EINVAL; }
+  if (n < 1 || n > 0x7fffffffLL) { set_error("n = %lld outside [1, 2^31)", n); return RBF_EINVAL; }
+  if (!(p->sigma > 0.0) || !std::isfinite(p->sigma)) { set_error("sigma must be > 0"); return RBF_EINVAL; }
+  if (!(p->cell > 0.0) || !std::isfinite(p->cell)) { set_error("cell must be > 0"); return RBF_EINVAL; }
+  if (!(p->rc > 0.0) || !std::isfinite(p->rc)) { set_error("rc must be > 0"); return RBF_EINVAL; }
+  if (p->overlap_rings < 0 || p->overlap_rings > 7) {
+    set_error("overlap_rings must be in [0, 7]");
+    return RBF_EINVAL;
+  }
+  if (!(p->x1 > p->x0) || !(p->y1 > p->y0) || !std::isfinite(p->x0) || !std::isfinite(p->x1) ||
+      !std::isfinite(p->y0) || !std::isfinite(p->y1)) {
+    set_error("box must satisfy x0 < x1, y0 < y1 (finite)");
+    return RBF_EINVAL;
+  }
+  double ncx = std::ceil((p->x1 - p->x0) / p->cell), ncy = std::ceil((p->y1 - p->y0) / p->cell);
+  if (ncx * ncy > 1.5e9) { set_error("too many cells (%g x %g)", ncx, ncy); return RBF_EINVAL; }
+  return RBF_OK;
+}
+
+}  // namespace rbf
+
+using namespace rbf;
+
+extern "C" {
+
+const char *rbf_last_error(void) { return g_err.c_str(); }
+
+int rbf_get_nccl_id(unsigned char out[128]) {
+  if (!out) { set_error("out is NULL"); return RBF_EINVAL; }
+  ncclUniqueId id;
+  RBF_NCCL_TRY(ncclGetUniqueId(&id));
+  memcpy(out, id.internal, 128);
+  return RBF_OK;
+}
+
+int rbf_plan_strips(const int64_t *row_counts, int64_t ncy, int32_t nranks, int64_t min_rows,
+                    int64_t *row_bounds) {
+  if (!row_counts || !row_bounds || ncy < 1) { set_error("bad arguments"); return RBF_EINVAL; }
+  return plan_strips((const long long *)row_counts, ncy, nranks, min_rows, (long long *)row_bounds);
+}
+
+void rbf_destroy(rbf_ctx *c) {
+  if (!c) return;
+  cudaStream_t s = c->last_stream;
+  dfree(c->cell_start, s);
+  dfree(c->perm, s);
+  dfree(c->xy_ext, s);
+  dfree(c->x_off, s);
+  dfree(c->X, s);
+  dfree(c->w_ext, s);
+  dfree(c->V, s);
+  dfree(c->t1, s);
+  dfree(c->t2, s);
+  dfree(c->red_part, s);
+  dfree(c->red_count, s);
+  dfree(c->dscal, s);
+  if (c->hpin) cudaFreeHost(c->hpin);
+  comm_destroy(c);
+  delete c;
+}
+
+int rbf_setup(rbf_ctx **out, const double *xy, int64_t n, const rbf_params *p, const rbf_dist *d,
+              void *stream) {
+  if (!out || !xy) { set_error("rbf_setup: NULL argument"); return RBF_EINVAL; }
+  *out = nullptr;
+  RBF_TRY(validate(p, n));
+  int ndev = 0;
+  (void)cudaGetLastError();  // clear a stale non-sticky error from earlier calls
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+    set_error("rbf_setup: no CUDA device (this library has no CPU fallback)");
+    return RBF_ECUDA;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  rbf_ctx *c = new rbf_ctx();
+  c->last_stream = s;
+  c->p = *p;
+  c->n = n;
+  if (d) {
+    if (d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks ||
+        (d->comm != RBF_COMM_NONE && d->comm != RBF_COMM_NCCL)) {
+      set_error("rbf_setup: bad rbf_dist (rank %d of %d, comm %d)", d->rank, d->nranks, d->comm);
+      delete c;
+      return RBF_EINVAL;
+    }
+    c->rank = d->rank;
+    c->nranks = d->nranks;
+    c->comm_mode = d->comm;
+  }
+  Geom &g = c->g;
+  g.x0 = p->x0; g.y0 = p->y0; g.x1 = p->x1; g.y1 = p->y1;
+  g.cell = p->cell;
+  g.rc2 = p->rc * p->rc;
+  g.neg_inv_2s2 = -1.0 / (2.0 * p->sigma * p->sigma);
+  g.norm = 1.0 / (2.0 * M_PI * p->sigma * p->sigma);
+  g.ncx = (int)std::ceil((p->x1 - p->x0) / p->cell);
+  g.ncy = (int)std::ceil((p->y1 - p->y0) / p->cell);
+  if (g.ncx < 1) g.ncx = 1;
+  if (g.ncy < 1) g.ncy = 1;
+  g.kh = (int)std::ceil(p->rc / p->cell * (1.0 + 1e-12));
+  g.rings = p->overlap_rings;
+  int st = build_cell_list(c, xy, s);
+  if (st != RBF_OK) { rbf_destroy(c); return st; }
+  // strips of cell rows, balanced by point count; each strip >= halo depth rows
+  const int depth = g.kh > g.rings ? g.kh : g.rings;
+  std::vector<long long> counts(g.ncy), bounds(c->nranks + 1);
+  for (int r = 0; r < g.ncy; ++r) counts[r] = c->row_start[r + 1] - c->row_start[r];
+  st = plan_strips(counts.data(), g.ncy, c->nranks, c->nranks > 1 ? depth : 1, bounds.data());
+  if (st != RBF_OK) { rbf_destroy(c); return st; }
+  Strip &S = c->s;
+  S.row_lo = (int)bounds[c->rank];
+  S.row_hi = (int)bounds[c->rank + 1];
+  S.ext_row_lo = S.row_lo - depth < 0 ? 0 : S.row_lo - depth;
+  S.ext_row_hi = S.row_hi + depth > g.ncy ? g.ncy : S.row_hi + depth;
+  S.own_lo = c->row_start[S.row_lo];
+  S.own_hi = c->row_start[S.row_hi];
+  S.ext_lo = c->row_start[S.ext_row_lo];
+  S.ext_hi = c->row_start[S.ext_row_hi];
+  auto halo = [&](int dd, Halo *h) {
+    // below (rank-1)
+    int lo = S.row_lo - dd < 0 ? 0 : S.row_lo - dd;
+    h[0].recv_off = c->row_start[lo] - S.ext_lo;
+    h[0].recv_cnt = c->row_start[S.row_lo] - c->row_start[lo];
+    int hi = S.row_lo + dd > S.row_hi ? S.row_hi : S.row_lo + dd;
+    h[0].send_off = 0;
+    h[0].send_cnt = (c->rank > 0) ? c->row_start[hi] - c->row_start[S.row_lo] : 0;
+    if (c->rank == 0) h[0].recv_cnt = 0;
+    // above (rank+1)
+    int hi2 = S.row_hi + dd > g.ncy ? g.ncy : S.row_hi + dd;
+    h[1].recv_off = c->row_start[S.row_hi] - S.ext_lo;
+    h[1].recv_cnt = (c->rank < c->nranks - 1) ? c->row_start[hi2] - c->row_start[S.row_hi] : 0;
+    int lo2 = S.row_hi - dd < S.row_lo ? S.row_lo : S.row_hi - dd;
+    h[1].send_off = c->row_start[lo2] - S.own_lo;
+    h[1].send_cnt = (c->rank < c->nranks - 1) ? c->row_start[S.row_hi] - c->row_start[lo2] : 0;
+  };
+  halo(g.kh, c->halo_mv);
+  halo(g.rings, c->halo_pc);
+  st = gather_positions(c, xy, s);
+  if (st == RBF_OK && c->nranks > 1)
+    st = dalloc(c, (void **)&c->w_ext, sizeof(double) * (size_t)(n_ext(c) > 0 ? n_ext(c) : 1), s);
+  if (st == RBF_OK) st = comm_init(c, d);
+  if (st == RBF_OK) st = rasm_setup(c, s);
+  if (st != RBF_OK) { rbf_destroy(c); return st; }
+  *out = c;
+  return RBF_OK;
+}
+
+int64_t rbf_local_count(const rbf_ctx *c) { return c ? n_loc(c) : -1; }
+int64_t rbf_ext_count(const rbf_ctx *c) { return c ? n_ext(c) : -1; }
+
+int rbf_ranges(const rbf_ctx *c, int64_t o[4]) {
+  if (!c || !o) { set_error("NULL argument"); return RBF_EINVAL; }
+  o[0] = c->s.ext_lo; o[1] = c->s.own_lo; o[2] = c->s.own_hi; o[3] = c->s.ext_hi;
+  return RBF_OK;
+}
+
+int rbf_local_index(const rbf_ctx *c, int64_t *idx, void *stream) {
+  if (!c || !idx) { set_error("NULL argument"); return RBF_EINVAL; }
+  return launch_local_index(c, idx, (cudaStream_t)stream);
+}
+
+__global__ void k_i32_to_i64(const int *a, long long n, int64_t *b) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t < n) b[t] = a[t];
+}
+
+int rbf_cell_list(const rbf_ctx *c, int64_t *perm, int64_t *cs, int64_t dims[2], void *stream) {
+  if (!c) { set_error("NULL ctx"); return RBF_EINVAL; }
+  cudaStream_t s = (cudaStream_t)stream;
+  long long nc = (long long)c->g.ncx * c->g.ncy + 1;
+  if (perm) k_i32_to_i64<<<(int)((c->n + 255) / 256), 256, 0, s>>>(c->perm, c->n, perm);
+  if (cs) k_i32_to_i64<<<(int)((nc + 255) / 256), 256, 0, s>>>(c->cell_start, nc, cs);
+  RBF_CUDA_TRY(cudaGetLastError());
+  if (dims) { dims[0] = c->g.ncx; dims[1] = c->g.ncy; }
+  return RBF_OK;
+}
+
+int rbf_to_local(const rbf_ctx *c, const double *vc, double *vl, void *stream) {
+  if (!c || !vc || !vl) { set_error("NULL argument"); return RBF_EINVAL; }
+  return launch_to_local(c, vc, vl, (cudaStream_t)stream);
+}
+
+int rbf_from_local(const rbf_ctx *c, const double *vl, double *vc, void *stream) {
+  if (!c || !vc || !vl) { set_error("NULL argument"); return RBF_EINVAL; }
+  return launch_from_local(c, vl, vc, (cudaStream_t)stream);
+}
+
+int rbf_matvec(rbf_ctx *c, const double *w, double *y, void *stream) {
+  if (!c || !w || !y) { set_error("NULL argument"); return RBF_EINVAL; }
+  cudaStream_t s = (cudaStream_t)stream;
+  const double *src = w;
+  if (c->nranks > 1) {
+    RBF_TRY(halo_exchange(c, w, c->w_ext, true, s));
+    src = c->w_ext;
+  }
+  return launch_matvec(c, src, y, s);
+}
+
+int rbf_rasm_apply(rbf_ctx *c, const double *r, double *z, void *stream) {
+  if (!c || !r || !z) { set_error("NULL argument"); return RBF_EINVAL; }
+  cudaStream_t s = (cudaStream_t)stream;
+  const double *src = r;
+  if (c->nranks > 1) {
+    RBF_TRY(halo_exchange(c, r, c->w_ext, false, s));
+    src = c->w_ext;
+  }
+  return launch_rasm_apply(c, src, z, s);
+}
+
+int rbf_matvec_ext(rbf_ctx *c, const double *w_ext, double *y, void *stream) {
+  if (!c || !w_ext || !y) { set_error("NULL argument"); return RBF_EINVAL; }
+  return launch_matvec(c, w_ext, y, (cudaStream_t)stream);
+}
+
+int rbf_rasm_apply_ext(rbf_ctx *c, const double *r_ext, double *z, void *stream) {
+  if (!c || !r_ext || !z) { set_error("NULL argument"); return RBF_EINVAL; }
+  return launch_rasm_apply(c, r_ext, z, (cudaStream_t)stream);
+}
+
+int rbf_solve(rbf_ctx *c, const double *f, const rbf_gmres_params *g, double *lam, rbf_report *rep,
+              void *stream) {
+  if (!c || !f || !g || !lam) { set_error("rbf_solve: NULL argument"); return RBF_EINVAL; }
+  if (g->restart < 1 || g->max_iters < 1 || !(g->rtol >= 0.0) || !(g->atol >= 0.0)) {
+    set_error("rbf_solve: restart >= 1, max_iters >= 1, rtol >= 0, atol >= 0 required");
+    return RBF_EINVAL;
+  }
+  if (c->nranks > 1 && c->comm_mode != RBF_COMM_NCCL) {
+    set_error("rbf_solve: virtual strip contexts cannot solve (no communicator)");
+    return RBF_EUNSUPPORTED;
+  }
+  c->last_stream = (cudaStream_t)stream;
+  int st = solve_gmres(c, f, g, lam, rep, (cudaStream_t)stream);
+  if (rep) {
+    rep->n_cells = c->nsub;
+    rep->bytes_device = c->bytes;
+  }
+  return st;
+}
+
+int rbf_count_pairs(rbf_ctx *c, int64_t *np, void *stream) {
+  if (!c || !np) { set_error("NULL argument"); return RBF_EINVAL; }
+  long long v = 0;
+  RBF_TRY(count_pairs(c, &v, (cudaStream_t)stream));
+  *np = v;
+  return RBF_OK;
+}
+
+int rbf_dot(rbf_ctx *c, const double *a, const double *b, double *out, void *stream) {
+  if (!c || !a || !b || !out) { set_error("NULL argument"); return RBF_EINVAL; }
+  return dot_host(c, a, b, out, (cudaStream_t)stream);
+}
+
+int rbf_interpolate_host(const double *xy_h, const double *f_h, int64_t n, const rbf_params *p,
+                         const rbf_gmres_params *g, double *lam_h, rbf_report *rep, void *stream) {
+  if (!xy_h || !f_h || !lam_h || !g) { set_error("rbf_interpolate_host: NULL argument"); return RBF_EINVAL; }
+  RBF_TRY(validate(p, n));
+  cudaStream_t s = (cudaStream_t)stream;
+  double *xy = nullptr, *fc = nullptr, *fl = nullptr, *ll = nullptr;
+  RBF_TRY(dalloc(nullptr, (void **)&xy, sizeof(double) * 2 * (size_t)n, s));
+  RBF_TRY(dalloc(nullptr, (void **)&fc, sizeof(double) * (size_t)n, s));
+  RBF_TRY(dalloc(nullptr, (void **)&fl, sizeof(double) * (size_t)n, s));
+  RBF_TRY(dalloc(nullptr, (void **)&ll, sizeof(double) * (size_t)n, s));
+  int st = RBF_OK;
+  rbf_ctx *c = nullptr;
+  do {
+    if (cudaMemcpyAsync(xy, xy_h, sizeof(double) * 2 * (size_t)n, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(fc, f_h, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+      set_error("rbf_interpolate_host: host-to-device copy failed");
+      st = RBF_ECUDA;
+      break;
+    }
+    st = rbf_setup(&c, xy, n, p, nullptr, stream);
+    if (st != RBF_OK) break;
+    st = launch_to_local(c, fc, fl, s);
+    if (st != RBF_OK) break;
+    st = rbf_solve(c, fl, g, ll, rep, stream);
+    if (st < 0) break;
+    int st2 = launch_from_local(c, ll, fc, s);
+    if (st2 != RBF_OK) { st = st2; break; }
+    if (cudaMemcpyAsync(lam_h, fc, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+      set_error("rbf_interpolate_host: device-to-host copy failed");
+      st = RBF_ECUDA;
+      break;
+    }
+  } while (0);
+  if (c) rbf_destroy(c);
+  dfree(xy, s);
+  dfree(fc, s);
+  dfree(fl, s);
+  dfree(ll, s);
+  return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,440 @@
+// krylov.cu -- restarted GMRES(m), left preconditioned with RASM, modified
+// Gram-Schmidt, Givens rotations (
+// SPEC S:264-284; reading Q12).
+//
+// Vector work is fused into streaming kernels: MGS step j of iteration k is ONE
+// pass  w <- w - h_{j-1,k} v_{j-1};  partial <w, v_j>  (the coefficient is read
+// from device memory, no host round trip), the last step also forms ||w||^2.
+// Reductions use a fixed grid and a fixed-shape tree, so the sums are
+// deterministic; across ranks the per-rank partials are all-gathered and summed in
+// rank order (reading Q14).  The Hessenberg column, Givens rotations and the
+// residual estimate live on the device; the host reads back one scalar per
+// iteration to decide convergence.
+#include <cmath>
+
+#include "common.cuh"
+
+namespace rbf {
+
+// Device scalar area layout (doubles), for restart m and P ranks.
+struct Scal {
+  int m, P;
+  __host__ __device__ long long hloc() const { return 0; }                  // [m+2]
+  __host__ __device__ long long hall() const { return m + 2; }              // [(m+2) P]
+  __host__ __device__ long long H() const { return hall() + (long long)(m + 2) * P; }  // [(m+1) m]
+  __host__ __device__ long long cs() const { return H() + (long long)(m + 1) * m; }
+  __host__ __device__ long long sn() const { return cs() + m; }
+  __host__ __device__ long long g() const { return sn() + m; }              // [m+1]
+  __host__ __device__ long long y() const { return g() + m + 1; }           // [m]
+  __host__ __device__ long long out() const { return y() + m; }             // [4]: |g|, hn, beta
+  __host__ __device__ long long total() const { return out() + 4; }
+};
+
+__device__ __forceinline__ double sum_ranks(const double *hall, int slot, int P) {
+  double s = 0.0;
+  for (int r = 0; r < P; ++r) s += hall[(long long)slot * P + r];
+  return s;
+}
+
+// Fixed-shape block reduction (deterministic).
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (warp == 0) {
+    t = (lane < (int)(blockDim.x >> 5)) ? sh[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  }
+  return t;  // valid in thread 0
+}
+
+// Grid-level finish: every block writes its partial; the last block to arrive sums
+// the partials in block order and writes *out.
+__device__ __forceinline__ void grid_finish(double partial, double *blk, unsigned *count,
+                                            double *out) {
+  __shared__ bool last;
+  __shared__ double sh[32];
+  if (threadIdx.x == 0) {
+    blk[blockIdx.x] = partial;
+    __threadfence();
+    unsigned t = atomicAdd(count, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double v = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) v += ((volatile double *)blk)[b];
+  v = block_sum(v, sh);
+  if (threadIdx.x == 0) {
+    *out = v;
+    *count = 0u;
+  }
+}
+
+// w <- w - (sum_r coef[r]) x  (if coef != null);  out = <w, v>   (v may alias w)
+__global__ __launch_bounds__(kRedThreads) void k_axpy_dot(const double *__restrict__ coef, int P,
+                                                          double *w, const double *__restrict__ x,
+                                                          const double *v, long long n,
+                                                          double *__restrict__ blk,
+                                                          unsigned *__restrict__ count,
+                                                          double *__restrict__ out) {
+  __shared__ double sh[32];
+  double a = 0.0;
+  if (coef) {
+    for (int r = 0; r < P; ++r) a += coef[r];
+  }
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    double wi = w[i];
+    if (coef) {
+      wi = fma(-a, x[i], wi);
+      w[i] = wi;
+    }
+    acc = fma(wi, v[i], acc);
+  }
+  double bs = block_sum(acc, sh);
+  grid_finish(bs, blk, count, out);
+}
+
+__global__ void k_scale_by_norm(double *__restrict__ w, long long n, const double *__restrict__ nrm2,
+                                int P) {
+  double h = sqrt(sum_ranks(nrm2, 0, P));
+  if (h == 0.0) return;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
+    w[i] = w[i] / h;
+}
+
+__global__ void k_sub(const double *__restrict__ f, double *__restrict__ t, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
+    t[i] = f[i] - t[i];
+}
+
+// Start of a cycle: g = (beta, 0, ...), beta = sqrt(sum_r nrm2[r]).
+__global__ void k_cycle_init(double *S, Scal L, const double *nrm2) {  // nrm2 = slot 0
+  double beta = sqrt(sum_ranks(nrm2, 0, L.P));
+  for (int i = 0; i <= L.m; ++i) S[L.g() + i] = 0.0;
+  S[L.g()] = beta;
+  S[L.out() + 2] = beta;
+}
+
+// Column k of H from the all-gathered MGS results, previous rotations, new rotation,
+// g update (Saad's GMRES with Givens; oracle orc_gmres follows the same steps).
+__global__ void k_givens(double *S, Scal L, const double *hall, int k) {
+  const int m = L.m;
+  double *H = S + L.H();
+  double *cs = S + L.cs(), *sn = S + L.sn(), *g = S + L.g();
+  for (int j = 0; j <= k; ++j) H[(long long)j * m + k] = sum_ranks(hall, j, L.P);
+  const double hn = sqrt(sum_ranks(hall, k + 1, L.P));
+  H[(long long)(k + 1) * m + k] = hn;
+  for (int j = 0; j < k; ++j) {
+    double a = H[(long long)j * m + k], c = H[(long long)(j + 1) * m + k];
+    H[(long long)j * m + k] = cs[j] * a + sn[j] * c;
+    H[(long long)(j + 1) * m + k] = -sn[j] * a + cs[j] * c;
+  }
+  double a = H[(long long)k * m + k], c = H[(long long)(k + 1) * m + k];
+  double den = hypot(a, c);
+  cs[k] = a / den;
+  sn[k] = c / den;
+  H[(long long)k * m + k] = den;
+  H[(long long)(k + 1) * m + k] = 0.0;
+  g[k + 1] = -sn[k] * g[k];
+  g[k] = cs[k] * g[k];
+  S[L.out() + 0] = fabs(g[k + 1]);
+  S[L.out() + 1] = hn;
+}
+
+// y = H(0:kend, 0:kend)^-1 g(0:kend)
+__global__ void k_backsolve(double *S, Scal L, int kend) {
+  const int m = L.m;
+  const double *H = S + L.H(), *g = S + L.g();
+  double *y = S + L.y();
+  for (int i = kend - 1; i >= 0; --i) {
+    double s = g[i];
+    for (int j = i + 1; j < kend; ++j) s -= H[(long long)i * m + j] * y[j];
+    y[i] = s / H[(long long)i * m + i];
+  }
+}
+
+// x += sum_{j < kend} y_j V_j   (one streaming pass)
+__global__ void k_update_x(double *__restrict__ x, const double *__restrict__ V, long long ldv,
+                           const double *__restrict__ S, Scal L, int kend, long long n) {
+  const double *y = S + L.y();
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    double xi = x[i];
+    for (int j = 0; j < kend; ++j) xi += y[j] * V[j * ldv + i];
+    x[i] = xi;
+  }
+}
+
+// ---------------------------------------------------------------------------
+
+struct Op {
+  rbf_ctx *c;
+  cudaStream_t s;
+  // y = A w (halo of w first)
+  int matvec(const double *w, double *y) {
+    const double *src = w;
+    if (c->nranks > 1) {
+      RBF_TRY(halo_exchange(c, w, c->w_ext, true, s));
+      src = c->w_ext;
+    }
+    return launch_matvec(c, src, y, s);
+  }
+  int pc(const double *r, double *z) {
+    const double *src = r;
+    if (c->nranks > 1) {
+      RBF_TRY(halo_exchange(c, r, c->w_ext, false, s));
+      src = c->w_ext;
+    }
+    return launch_rasm_apply(c, src, z, s);
+  }
+};
+
+static int ensure_workspace(rbf_ctx *c, int m, cudaStream_t s) {
+  const long long n = n_loc(c);
+  if (c->V && c->V_m >= m) return RBF_OK;
+  if (c->V) dfree(c->V, s);
+  if (c->dscal) dfree(c->dscal, s);
+  c->V = nullptr;
+  c->dscal = nullptr;
+  RBF_TRY(dalloc(c, (void **)&c->V, sizeof(double) * (size_t)(m + 1) * (size_t)(n > 0 ? n : 1), s));
+  Scal L{m, c->nranks};
+  RBF_TRY(dalloc(c, (void **)&c->dscal, sizeof(double) * (size_t)L.total(), s));
+  RBF_CUDA_TRY(cudaMemsetAsync(c->dscal, 0, sizeof(double) * (size_t)L.total(), s));
+  c->V_m = m;
+  if (!c->t1) RBF_TRY(dalloc(c, (void **)&c->t1, sizeof(double) * (size_t)(n > 0 ? n : 1), s));
+  if (!c->t2) RBF_TRY(dalloc(c, (void **)&c->t2, sizeof(double) * (size_t)(n > 0 ? n : 1), s));
+  if (!c->red_part) RBF_TRY(dalloc(c, (void **)&c->red_part, sizeof(double) * kRedBlocks, s));
+  if (!c->red_count) {
+    RBF_TRY(dalloc(c, (void **)&c->red_count, sizeof(unsigned), s));
+    RBF_CUDA_TRY(cudaMemsetAsync(c->red_count, 0, sizeof(unsigned), s));
+  }
+  if (!c->hpin) RBF_CUDA_TRY(cudaMallocHost((void **)&c->hpin, sizeof(double) * 64));
+  return RBF_OK;
+}
+
+static int grid_for(long long n) {
+  long long b = (n + kRedThreads - 1) / kRedThreads;
+  return (int)(b < kRedBlocks ? (b > 0 ? b : 1) : kRedBlocks);
+}
+
+// out_dev = this rank's partial <a, b> (optionally after w -= coef*x)
+static int axpy_dot(rbf_ctx *c, const double *coef, double *w, const double *x, const double *v,
+                    double *out_dev, cudaStream_t s) {
+  const long long n = n_loc(c);
+  k_axpy_dot<<<grid_for(n), kRedThreads, 0, s>>>(coef, c->nranks, w, x, v, n, c->red_part,
+                                                  c->red_count, out_dev);
+  RBF_CUDA_TRY(cudaGetLastError());
+  return RBF_OK;
+}
+
+// Reduce a scalar slot across ranks: hloc[slot] -> hall[slot*P ...]
+static int reduce_slot(rbf_ctx *c, const Scal &L, int slot, cudaStream_t s) {
+  if (c->nranks <= 1) return RBF_OK;
+  return allgather_scalars(c, c->dscal + L.hloc() + slot, c->dscal + L.hall() + (long long)slot * L.P,
+                           1, s);
+}
+
+static const double *hall_slot(rbf_ctx *c, const Scal &L, int slot) {
+  return c->nranks <= 1 ? c->dscal + L.hloc() + slot : c->dscal + L.hall() + (long long)slot * L.P;
+}
+
+static int read_scalars(rbf_ctx *c, const double *src, int count, cudaStream_t s) {
+  RBF_CUDA_TRY(cudaMemcpyAsync(c->hpin, src, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  return RBF_OK;
+}
+
+// Global <a, b> (summed over ranks in rank order) to the host.
+static int global_dot(rbf_ctx *c, const Scal &L, const double *a, const double *b, double *out,
+                      cudaStream_t s) {
+  RBF_TRY(axpy_dot(c, nullptr, const_cast<double *>(a), nullptr, b, c->dscal + L.hloc(), s));
+  RBF_TRY(reduce_slot(c, L, 0, s));
+  RBF_TRY(read_scalars(c, hall_slot(c, L, 0), c->nranks, s));
+  double t = 0.0;
+  for (int r = 0; r < c->nranks; ++r) t += c->hpin[r];
+  *out = t;
+  return RBF_OK;
+}
+
+int dot_host(rbf_ctx *c, const double *a, const double *b, double *out, cudaStream_t s) {
+  RBF_TRY(ensure_workspace(c, c->V_m > 0 ? c->V_m : 1, s));
+  Scal L{c->V_m, c->nranks};
+  return global_dot(c, L, a, b, out, s);
+}
+
+struct PhaseTimer {
+  bool on = false;
+  cudaEvent_t e[4]{};
+  double mv = 0, pc = 0, orth = 0;
+  int init(bool enable) {
+    on = enable;
+    if (!on) return RBF_OK;
+    for (auto &x : e) RBF_CUDA_TRY(cudaEventCreate(&x));
+    return RBF_OK;
+  }
+  void rec(int i, cudaStream_t s) {
+    if (on) cudaEventRecord(e[i], s);
+  }
+  void accumulate() {  // after a stream sync
+    if (!on) return;
+    float a = 0, b = 0, d = 0;
+    cudaEventElapsedTime(&a, e[0], e[1]);
+    cudaEventElapsedTime(&b, e[1], e[2]);
+    cudaEventElapsedTime(&d, e[2], e[3]);
+    mv += a;
+    pc += b;
+    orth += d;
+  }
+  ~PhaseTimer() {
+    if (on)
+      for (auto &x : e) cudaEventDestroy(x);
+  }
+};
+
+int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double *x,
+                rbf_report *rep, cudaStream_t s) {
+  const int m = gp->restart;
+  const long long n = n_loc(c);
+  RBF_TRY(ensure_workspace(c, m, s));
+  Scal L{m, c->nranks};
+  Op op{c, s};
+  double *V = c->V;
+  const long long ldv = n;
+  PhaseTimer pt;
+  RBF_TRY(pt.init(gp->timing != 0));
+  cudaEvent_t t_begin = nullptr, t_end = nullptr;
+  if (gp->timing) {
+    RBF_CUDA_TRY(cudaEventCreate(&t_begin));
+    RBF_CUDA_TRY(cudaEventCreate(&t_end));
+    RBF_CUDA_TRY(cudaEventRecord(t_begin, s));
+  }
+  const int blocks = grid_for(n);
+
+  RBF_CUDA_TRY(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)n, s));
+  // beta0 = ||M^-1 f||  (x0 = 0)
+  RBF_TRY(op.pc(f, V));
+  double beta0sq = 0.0;
+  RBF_TRY(global_dot(c, L, V, V, &beta0sq, s));
+  const double beta0 = std::sqrt(beta0sq);
+  int it = 0, restarts = 0, converged = 0, status = RBF_OK, hist_len = 0;
+  double resid_est = 0.0;
+  if (beta0 == 0.0) {
+    converged = 1;
+  } else {
+    const double tol = std::fmax(gp->rtol * beta0, gp->atol);
+    for (;;) {
+      // V0 holds the unscaled preconditioned residual; its ||.||^2 is in slot 0
+      k_cycle_init<<<1, 1, 0, s>>>(c->dscal, L, hall_slot(c, L, 0));
+      k_scale_by_norm<<<blocks, kRedThreads, 0, s>>>(V, n, hall_slot(c, L, 0), L.P);
+      RBF_CUDA_TRY(cudaGetLastError());
+      int kend = 0;
+      bool done = false;
+      for (int k = 0; k < m; ++k) {
+        double *vk = V + (long long)k * ldv;
+        double *w = V + (long long)(k + 1) * ldv;
+        pt.rec(0, s);
+        RBF_TRY(op.matvec(vk, c->t1));
+        pt.rec(1, s);
+        RBF_TRY(op.pc(c->t1, w));
+        pt.rec(2, s);
+        for (int j = 0; j <= k; ++j) {  // modified Gram-Schmidt, fused
+          const double *coef = (j > 0) ? hall_slot(c, L, j - 1) : nullptr;
+          const double *xprev = (j > 0) ? V + (long long)(j - 1) * ldv : nullptr;
+          RBF_TRY(axpy_dot(c, coef, w, xprev, V + (long long)j * ldv, c->dscal + L.hloc() + j, s));
+          RBF_TRY(reduce_slot(c, L, j, s));
+        }
+        RBF_TRY(axpy_dot(c, hall_slot(c, L, k), w, vk, w, c->dscal + L.hloc() + k + 1, s));
+        RBF_TRY(reduce_slot(c, L, k + 1, s));
+        k_givens<<<1, 1, 0, s>>>(c->dscal, L, hall_slot(c, L, 0), k);
+        k_scale_by_norm<<<blocks, kRedThreads, 0, s>>>(w, n, hall_slot(c, L, k + 1), L.P);
+        RBF_CUDA_TRY(cudaGetLastError());
+        pt.rec(3, s);
+        RBF_TRY(read_scalars(c, c->dscal + L.out(), 2, s));
+        pt.accumulate();
+        const double gabs = c->hpin[0], hn = c->hpin[1];
+        ++it;
+        resid_est = gabs / beta0;
+        if (rep && rep->history && hist_len < rep->history_cap) rep->history[hist_len++] = resid_est;
+        kend = k + 1;
+        if (!std::isfinite(gabs) || !std::isfinite(hn)) {
+          status = RBF_ENUMERIC;
+          done = true;
+          break;
+        }
+        if (gabs <= tol || hn == 0.0) {
+          converged = 1;
+          done = true;
+          break;
+        }
+        if (it >= gp->max_iters) {
+          done = true;
+          break;
+        }
+      }
+      k_backsolve<<<1, 1, 0, s>>>(c->dscal, L, kend);
+      k_update_x<<<blocks, kRedThreads, 0, s>>>(x, V, ldv, c->dscal, L, kend, n);
+      RBF_CUDA_TRY(cudaGetLastError());
+      if (done) break;
+      // restart: V0 = M^-1 (f - A x), explicitly
+      RBF_TRY(op.matvec(x, c->t1));
+      k_sub<<<blocks, kRedThreads, 0, s>>>(f, c->t1, n);
+      RBF_TRY(op.pc(c->t1, V));
+      double bsq = 0.0;
+      RBF_TRY(global_dot(c, L, V, V, &bsq, s));
+      ++restarts;
+      const double beta = std::sqrt(bsq);
+      if (beta <= tol) {
+        converged = 1;
+        resid_est = beta / beta0;
+        break;
+      }
+    }
+  }
+  double ms_total = 0.0;
+  if (gp->timing) {
+    RBF_CUDA_TRY(cudaEventRecord(t_end, s));
+    RBF_CUDA_TRY(cudaEventSynchronize(t_end));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t_begin, t_end);
+    ms_total = ms;
+    cudaEventDestroy(t_begin);
+    cudaEventDestroy(t_end);
+  }
+  if (rep) {
+    // explicit residuals (not part of the timed solve)
+    double fsq = 0.0, rsq = 0.0, psq = 0.0;
+    RBF_TRY(global_dot(c, L, f, f, &fsq, s));
+    RBF_TRY(op.matvec(x, c->t1));
+    k_sub<<<blocks, kRedThreads, 0, s>>>(f, c->t1, n);
+    RBF_TRY(global_dot(c, L, c->t1, c->t1, &rsq, s));
+    RBF_TRY(op.pc(c->t1, c->t2));
+    RBF_TRY(global_dot(c, L, c->t2, c->t2, &psq, s));
+    rep->iterations = it;
+    rep->converged = converged;
+    rep->restarts = restarts;
+    rep->beta0 = beta0;
+    rep->resid_est = resid_est;
+    rep->resid_true = fsq > 0 ? std::sqrt(rsq / fsq) : 0.0;
+    rep->resid_precond = beta0 > 0 ? std::sqrt(psq) / beta0 : 0.0;
+    rep->history_len = hist_len;
+    rep->ms_matmult = pt.mv;
+    rep->ms_pcapply = pt.pc;
+    rep->ms_orth = pt.orth;
+    rep->ms_total = ms_total;
+  }
+  if (status == RBF_OK && !converged) status = RBF_NOT_CONVERGED;
+  if (rep) rep->status = status;
+  return status;
+}
+
+}  // namespace rbf

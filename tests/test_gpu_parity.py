@@ -1,0 +1,265 @@
+"""GPU parity: the CUDA path (through the C ABI of librbf.so) against the oracle
+on the same seeded inputs.  Tolerances:
+  cell list      bit-exact perm and cell_start
+  matvec         <= 1e-12 relative L2 (BASELINE.json north_star)
+  RASM apply     <= 1e-10 relative L2 (reading Q11: explicit inverse rows vs triangular solves)
+  solve          same stopping rule; iterations within +-2; true residuals <= 1e-10;
+                 weights within 1e-8 relative L2 (reading Q17)
+  strips         per-point matvec/RASM results bitwise identical for any strip count (Q20)
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import rbf_workloads as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - the gpu marker keeps this off CPU runs
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_0909_5413_b200 as P  # noqa: E402
+
+
+def ctx_for(wl, rings=None, **kw):
+    xy = torch.from_numpy(wl.xy).cuda()
+    return P.Context(xy, wl.sigma, wl.cell, wl.rc, wl.rings if rings is None else rings, wl.box, **kw)
+
+
+def to_caller(ctx, v_loc):
+    idx = ctx.local_index().cpu().numpy()
+    out = np.zeros(ctx.n)
+    out[idx] = v_loc.cpu().numpy()
+    return out
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+SMALL = [W.config(1), W.make_lattice(24), W.make_lattice(40, jitter_frac=0.1, seed=7),
+         W.make_lattice(37, jitter_frac=0.3, seed=3), W.make_clustered(3000, seed=11)]
+IDS = ["cfg1", "ragged24", "jitter40", "jitter37", "clustered3000"]
+
+
+@pytest.mark.parametrize("wl", SMALL, ids=IDS)
+def test_cell_list_bit_exact(wl):
+    key, perm, start = O.cell_list(wl.xy, wl.box, wl.cell)
+    with ctx_for(wl, rings=0) as c:
+        gperm, gstart, dims = c.cell_list()
+        assert dims == O.grid_dims(wl.box, wl.cell)
+        assert np.array_equal(gperm.cpu().numpy(), perm)
+        assert np.array_equal(gstart.cpu().numpy(), start)
+        assert np.array_equal(c.local_index().cpu().numpy(), perm)
+
+
+@pytest.mark.parametrize("wl", SMALL, ids=IDS)
+def test_matvec_parity(wl):
+    rng = np.random.default_rng(12)
+    w = rng.standard_normal(wl.n)
+    ref = O.matvec_brute(wl.xy, w, wl.sigma, wl.rc)
+    with ctx_for(wl, rings=0) as c:
+        y = c.matvec(c.to_local(torch.from_numpy(w).cuda()))
+        got = to_caller(c, y)
+    assert rel(got, ref) <= 1e-12
+    # w == 1 on cfg1 interior: the constant-field value of the oracle pin
+    if wl.name == "cfg1":
+        with ctx_for(wl, rings=0) as c:
+            y = to_caller(c, c.matvec(torch.ones(wl.n, dtype=torch.float64, device="cuda")))
+        ref1 = O.matvec_brute(wl.xy, np.ones(wl.n), wl.sigma, wl.rc)
+        assert np.max(np.abs(y - ref1) / ref1) < 1e-14
+
+
+@pytest.mark.parametrize("wl", SMALL[:4], ids=IDS[:4])
+def test_rasm_apply_parity(wl):
+    rng = np.random.default_rng(13)
+    r = rng.standard_normal(wl.n)
+    Pc = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, 1)
+    ref = Pc.apply(r)
+    Pc.close()
+    with ctx_for(wl) as c:
+        z = to_caller(c, c.rasm_apply(c.to_local(torch.from_numpy(r).cuda())))
+    assert rel(z, ref) <= 1e-10
+
+
+def test_rasm_block_jacobi_parity():
+    wl = W.make_lattice(30, jitter_frac=0.1, seed=2)
+    r = np.random.default_rng(3).standard_normal(wl.n)
+    Pc = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, 0)
+    ref = Pc.apply(r)
+    with ctx_for(wl, rings=0) as c:
+        z = to_caller(c, c.rasm_apply(c.to_local(torch.from_numpy(r).cuda())))
+    assert rel(z, ref) <= 1e-10
+
+
+@pytest.fixture(scope="module")
+def cfg1_oracle():
+    wl = W.config(1)
+    return wl, O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, rtol=wl.tol)
+
+
+def test_solve_parity_cfg1(cfg1_oracle):
+    wl, ref = cfg1_oracle
+    with ctx_for(wl) as c:
+        lam, rep = c.solve(c.to_local(torch.from_numpy(wl.f).cuda()), rtol=wl.tol)
+        lam = to_caller(c, lam)
+    assert rep.converged and rep.status == 0
+    assert abs(rep.iterations - ref.iterations) <= 2
+    assert rep.resid_true <= 1e-10 and ref.resid_true <= 1e-10
+    assert rel(lam, ref.x) <= 1e-8
+    n = min(len(rep.history), len(ref.history))
+    h1, h2 = rep.history[:n], ref.history[:n]
+    big = h2 > 1e-9
+    assert np.all(np.abs(h1[big] - h2[big]) <= 1e-6 * h2[big])
+    # interpolation conditions through the oracle's own operator (Eq.(2))
+    s = O.matvec_brute(wl.xy, lam, wl.sigma, wl.rc)
+    assert rel(s, wl.f) <= 1e-10
+
+
+def test_interpolate_host_matches_context(cfg1_oracle):
+    wl, ref = cfg1_oracle
+    lam, rep = P.interpolate_host(wl.xy, wl.f, wl.sigma, wl.cell, wl.rc, 1, wl.box, rtol=wl.tol)
+    assert rep.converged and abs(rep.iterations - ref.iterations) <= 2
+    assert rel(lam, ref.x) <= 1e-8
+
+
+def test_solve_parity_jittered_restarts():
+    wl = W.make_lattice(64, jitter_frac=0.1, seed=2, rhs="gauss", s2=0.02)
+    ref = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, rtol=1e-13)
+    with ctx_for(wl) as c:
+        lam, rep = c.solve(c.to_local(torch.from_numpy(wl.f).cuda()), rtol=1e-13)
+        lam = to_caller(c, lam)
+    assert rep.converged and ref.converged
+    assert abs(rep.iterations - ref.iterations) <= 2
+    assert rep.resid_true <= 1e-10
+    assert rel(lam, ref.x) <= 1e-8
+
+
+# ------------------------------------------------------------------ edge cases
+
+def test_zero_rhs_and_not_converged():
+    wl = W.make_lattice(30)
+    with ctx_for(wl) as c:
+        lam, rep = c.solve(torch.zeros(c.n_local, dtype=torch.float64, device="cuda"))
+        assert rep.iterations == 0 and rep.converged and float(lam.abs().max()) == 0.0
+        f = c.to_local(torch.from_numpy(wl.f).cuda())
+        lam, rep = c.solve(f, max_iters=3, rtol=1e-15)
+        assert rep.status == P.rbf.RBF_NOT_CONVERGED and rep.iterations == 3 and not rep.converged
+
+
+def test_single_point_and_single_cell():
+    xy = np.array([[0.1, -0.2]])
+    wl = W.Workload("one", xy, np.array([2.0]), 0.05, 0.3, 0.2)
+    with ctx_for(wl) as c:
+        y = c.matvec(torch.tensor([3.0], dtype=torch.float64, device="cuda"))
+        assert float(y[0]) == pytest.approx(3.0 / (2 * np.pi * 0.05 ** 2), rel=1e-15)
+        lam, rep = c.solve(torch.tensor([2.0], dtype=torch.float64, device="cuda"))
+        assert float(lam[0]) == pytest.approx(2.0 * 2 * np.pi * 0.05 ** 2, rel=1e-13)
+    # all points in one cell: RASM is the exact inverse -> <= 2 iterations (Q19)
+    wl = W.make_lattice(12, jitter_frac=0.1, seed=1)
+    wl.cell = 4.0
+    with ctx_for(wl) as c:
+        _, rep = c.solve(c.to_local(torch.from_numpy(wl.f).cuda()))
+        assert rep.converged and rep.iterations <= 2
+
+
+def test_invalid_arguments():
+    wl = W.make_lattice(10)
+    xy = torch.from_numpy(wl.xy).cuda()
+    with pytest.raises(P.RbfError) as e:
+        P.Context(xy, -1.0, wl.cell, wl.rc)
+    assert e.value.code == -1
+    bad = wl.xy.copy()
+    bad[5, 0] = 1.5
+    with pytest.raises(P.RbfError) as e:
+        P.Context(torch.from_numpy(bad).cuda(), wl.sigma, wl.cell, wl.rc)
+    assert e.value.code == -1 and "point 5" in str(e.value)
+    bad[5, 0] = np.nan
+    with pytest.raises(P.RbfError):
+        P.Context(torch.from_numpy(bad).cuda(), wl.sigma, wl.cell, wl.rc)
+    with ctx_for(wl) as c:
+        with pytest.raises(P.RbfError):
+            c.solve(c.to_local(torch.from_numpy(wl.f).cuda()), restart=0)
+
+
+# ------------------------------------------------------------------ strips (Q20)
+
+@pytest.mark.parametrize("nranks", [2, 3, 4])
+def test_virtual_strips_bitwise(nranks):
+    wl = W.make_lattice(60, jitter_frac=0.1, seed=5)  # 12 cell rows, halo 2 rows
+    rng = np.random.default_rng(1)
+    w = rng.standard_normal(wl.n)
+    xy = torch.from_numpy(wl.xy).cuda()
+    with ctx_for(wl) as c1:
+        ws = c1.to_local(torch.from_numpy(w).cuda())  # global sorted order
+        y1 = c1.matvec(ws).cpu().numpy()
+        z1 = c1.rasm_apply(ws).cpu().numpy()
+    ys, zs = [], []
+    for g in range(nranks):
+        with P.Context(xy, wl.sigma, wl.cell, wl.rc, 1, wl.box, rank=g, nranks=nranks) as c:
+            ext = ws[c.ext_lo:c.ext_hi].contiguous()
+            ys.append(c.matvec_ext(ext).cpu().numpy())
+            zs.append(c.rasm_apply_ext(ext).cpu().numpy())
+            assert c.n_local == c.own_hi - c.own_lo
+            with pytest.raises(P.RbfError):
+                c.matvec(ws[c.own_lo:c.own_hi].contiguous())  # no communicator
+    assert np.array_equal(np.concatenate(ys), y1)
+    assert np.array_equal(np.concatenate(zs), z1)
+
+
+# ------------------------------------------------------------------ full size (bench config)
+
+@pytest.fixture(scope="module")
+def cfg2():
+    return W.config(2)
+
+
+def test_cfg2_matvec_sampled_rows(cfg2):
+    wl = cfg2
+    rng = np.random.default_rng(7)
+    w = rng.standard_normal(wl.n)
+    rows = np.concatenate([[0, wl.n - 1, 1023, wl.n - 1024], rng.choice(wl.n, 400, replace=False)])
+    ref = O.matvec_brute(wl.xy, w, wl.sigma, wl.rc, rows=rows)
+    with ctx_for(wl, rings=0) as c:
+        got = to_caller(c, c.matvec(c.to_local(torch.from_numpy(w).cuda())))
+        assert c.count_pairs() == O.count_pairs(wl.xy, wl.rc, wl.box, wl.cell)
+    assert rel(got[rows], ref) <= 1e-12
+
+
+def test_cfg2_rasm_sampled_cells(cfg2):
+    """z[own(c)] = (A_c^-1 r[Omega_c])[own(c)] for sampled cells, A_c assembled by the
+    oracle and solved densely (Eq.(10))."""
+    wl = cfg2
+    key, perm, start = O.cell_list(wl.xy, wl.box, wl.cell)
+    ncx, ncy = O.grid_dims(wl.box, wl.cell)
+    rng = np.random.default_rng(8)
+    r = rng.standard_normal(wl.n)
+    with ctx_for(wl) as c:
+        z = to_caller(c, c.rasm_apply(c.to_local(torch.from_numpy(r).cuda())))
+    cells = [0, ncx - 1, ncx * ncy - 1, ncx * (ncy // 2) + ncx // 2] + list(rng.choice(ncx * ncy, 12))
+    for cc in cells:
+        cx, cy = cc % ncx, cc // ncx
+        ov = []
+        for by in range(max(cy - 1, 0), min(cy + 1, ncy - 1) + 1):
+            for bx in range(max(cx - 1, 0), min(cx + 1, ncx - 1) + 1):
+                b = by * ncx + bx
+                ov += list(perm[start[b]:start[b + 1]])
+        ov = np.array(ov)
+        own = perm[start[cc]:start[cc + 1]]
+        Ac = O.assemble_dense(wl.xy[ov], wl.sigma, wl.rc)
+        sol, _ = O.dense_factor_solve(Ac, r[ov])
+        pos = {j: q for q, j in enumerate(ov)}
+        ref = np.array([sol[pos[j]] for j in own])
+        assert rel(z[own], ref) <= 1e-10
+
+
+def test_cfg2_solve_true_residual(cfg2):
+    wl = cfg2
+    with ctx_for(wl) as c:
+        lam, rep = c.solve(c.to_local(torch.from_numpy(wl.f).cuda()), rtol=wl.tol)
+        lam = to_caller(c, lam)
+    assert rep.converged
+    assert 40 <= rep.iterations <= 150  # [D4]: 73 on a 256^2 jittered model
+    s = O.matvec_cells(wl.xy, lam, wl.sigma, wl.rc, wl.box, wl.cell)
+    assert rel(s, wl.f) <= 1e-10
