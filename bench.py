@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""Benchmark of the PetRBF hot path on B200 (contract: README/DESIGN.md "Bench").
+
+One step = one full interpolation solve of BASELINE.json configs[1] (cfg2: 1,048,576
+jittered lattice points, h/sigma = 0.8, rc = 6 sigma, cell = 4 sigma, GMRES(30) +
+RASM, tol 1e-13): rbf_setup (cell list + RASM setup) + rbf_solve, inputs resident in
+HBM.  metric/unit follow BASELINE.json: solve time (s, lower is better) plus the
+matvec Gpairs/s and the FP64-peak fractions.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl reference]
+
+Multi-GPU: launched by torchrun, one rank per GPU; strips of cell rows with NCCL
+halos/all-gathers (strong scaling: total work fixed).  --impl reference times the
+oracle (plain C, host cores) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import rbf_workloads as W  # noqa: E402
+
+METRIC = "fp64 GMRES+RASM solve time and matvec Gpairs/s at 1/2/4/8 B200, % FP64 peak"
+FP64_PEAK_TFLOPS = 33.96  # measured DFMA peak on this pool's B200 (profiles/r01_fp64_peak.json)
+FLOP_PER_PAIR = 38        # algorithmic flops per in-cutoff pair
+SAMPLE_SIDE = 256         # oracle sample: 256^2 points of the same recipe
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------------------- clocks
+class Clocks:
+    def __init__(self, gpu_index: int):
+        self.path = f"/tmp/rbf_clocks_{os.getpid()}.csv"
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        rows = []
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        load = [x for x in sm if mx and x > 0.5 * max(mx)] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[3 + k] == "Active"})
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------------------- reference arm
+def oracle_sample(cfg: int):
+    """The oracle on a bounded sample of the workload: the same recipe on a
+    SAMPLE_SIDE^2 lattice (same h/sigma, cell/sigma, rc/sigma, jitter, rhs)."""
+    import oracle as O
+
+    full = W.config(cfg)
+    if cfg == 2:
+        wl = W.make_lattice(SAMPLE_SIDE, jitter_frac=0.1, seed=2, rhs="gauss", s2=0.02)
+    elif cfg == 1:
+        wl = full
+    else:
+        wl = W.make_lattice(SAMPLE_SIDE, rhs="gauss", s2=0.02)
+    t0 = time.perf_counter()
+    res = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, rtol=full.tol)
+    dt = time.perf_counter() - t0
+    scale = full.n / wl.n  # O(N) time per solve
+    return dt, scale, res, wl, full
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    times = []
+    res = wl = full = None
+    scale = 1.0
+    for i in range(args.warmup + args.steps):
+        dt, scale, res, wl, full = oracle_sample(args.config)
+        if i >= args.warmup:
+            times.append(dt * scale)
+    v = statistics.mean(times)
+    sample = (f"oracle solve of a {wl.n}-point sample ({wl.name}, same recipe) in "
+              f"{v / scale:.2f} s, {res.iterations} iterations; x{scale:.1f} linear-in-N "
+              f"extrapolation to {full.name} (N={full.n})")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": full.name, "N": full.n},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+def run_ours(args, rank, world):
+    import torch
+    import torch.distributed as dist
+
+    import paper_0909_5413_b200 as P
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream()
+    wl = W.config(args.config)
+    xy_h = torch.from_numpy(wl.xy)
+    f_h = torch.from_numpy(wl.f)
+    xy = xy_h.cuda()
+    f = f_h.cuda()
+    nccl_id = None
+    if world > 1:
+        obj = [P.get_nccl_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    kw = dict(rank=rank, nranks=world, comm="nccl", nccl_id=nccl_id) if world > 1 else {}
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+
+    def step(timing=False):
+        c = P.Context(xy, wl.sigma, wl.cell, wl.rc, wl.rings, wl.box, **kw)
+        fl = c.to_local(f)
+        lam, rep = c.solve(fl, rtol=wl.tol, timing=timing)
+        return c, lam, rep
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (also: facts for the roofline)
+    for _ in range(args.warmup):
+        c, lam, rep = step()
+        info = c.info()
+        c.close()
+    barrier()
+    # timed region: K steps, each bracketed by CUDA events; L2 flushed between steps
+    clocks = Clocks(dev)
+    launches0 = P.launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    reps = []
+    barrier()
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        ev[k][0].record(stream)
+        c, lam, rep = step(timing=True)
+        ev[k][1].record(stream)
+        reps.append(rep)
+        c.close()
+    barrier()
+    launches = P.launch_count() - launches0
+    clk = clocks.stop()
+    ms = [a.elapsed_time(b) for a, b in ev]
+    t_local = sum(ms)
+    t = torch.tensor([t_local], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / args.steps
+
+    # ---- per-kernel measurements for the roofline (same stream, after the timed region)
+    c = P.Context(xy, wl.sigma, wl.cell, wl.rc, wl.rings, wl.box, **kw)
+    info = c.info()
+    n_pairs_local = c.count_pairs()
+    w = torch.randn(c.n_local, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(w)
+
+    def time_op(fn, reps_=20):
+        fn()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps_):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / reps_
+
+    mv_ms = time_op(lambda: c.matvec(w, y))
+    pc_ms = time_op(lambda: c.rasm_apply(w, y))
+    c.close()
+    n_loc = c.n_local
+    iters = statistics.mean(r.iterations for r in reps)
+    # phase shares inside the timed steps (library CUDA events on the launching stream)
+    mv_live = statistics.mean(r.ms_matmult for r in reps)
+    pc_live = statistics.mean(r.ms_pcapply for r in reps)
+    orth_live = statistics.mean(r.ms_orth for r in reps)
+    # matvec launches per solve: one per iteration + one per restart + 0 (beta0 uses PC only)
+    mv_launches = statistics.mean(r.iterations + r.restarts for r in reps)
+    pc_launches = statistics.mean(r.iterations + r.restarts + 1 for r in reps)
+    x_bytes = 8 * info["x_doubles"]
+    pc_alg_bytes = x_bytes + 16 * n_loc          # X streamed once + u read + z written
+    mv_alg_flops = FLOP_PER_PAIR * n_pairs_local
+    hbm_peak, hbm_src = peaks()
+    pc_per_launch_ms = pc_live / max(iters, 1)   # live: phase time / launches in the phase
+    mv_per_launch_ms = mv_live / max(iters, 1)
+    pc_gbs = pc_alg_bytes / (pc_per_launch_ms * 1e-3) / 1e9
+    mv_tflops = mv_alg_flops / (mv_per_launch_ms * 1e-3) / 1e12
+    shares = {"matvec": mv_live, "rasm_apply": pc_live, "orth": orth_live}
+    dom = max(("matvec", "rasm_apply"), key=lambda k: shares[k])
+    if dom == "rasm_apply":
+        roof = {"kernel": "k_rasm_apply", "bound": "hbm", "achieved": pc_gbs, "peak": hbm_peak,
+                "unit": "GB/s", "frac": pc_gbs / hbm_peak, "traffic": None,
+                "peak_source": hbm_src, "alg_bytes_per_launch": pc_alg_bytes,
+                "ms_per_launch": pc_per_launch_ms}
+    else:
+        roof = {"kernel": "k_matvec", "bound": "alu", "achieved": mv_tflops,
+                "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": mv_tflops / FP64_PEAK_TFLOPS,
+                "traffic": None, "peak_source": "measured DFMA microbenchmark",
+                "alg_flops_per_launch": mv_alg_flops, "ms_per_launch": mv_per_launch_ms}
+    gpairs = n_pairs_local / (mv_ms * 1e-3) / 1e9
+    if world > 1:
+        tot = torch.tensor([float(n_pairs_local)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tot)
+        mvt = torch.tensor([mv_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(mvt, op=dist.ReduceOp.MAX)
+        gpairs = float(tot.item()) / (float(mvt.item()) * 1e-3) / 1e9
+
+    # ---- e2e: host buffers through the public C ABI (rbf_interpolate_host), N=1
+    e2e = None
+    if world == 1:
+        xy_pin = xy_h.pin_memory().numpy()
+        f_pin = f_h.pin_memory().numpy()
+        e2e_ms = []
+        for k in range(max(1, min(args.steps, 3)) + 1):
+            flush.fill_(float(k))
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            lam_h, rep_h = P.interpolate_host(xy_pin, f_pin, wl.sigma, wl.cell, wl.rc, wl.rings,
+                                              wl.box, rtol=wl.tol)
+            torch.cuda.synchronize()
+            if k > 0:
+                e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        e2e = {"value": statistics.mean(e2e_ms) / 1e3, "unit": "s",
+               "h2d_bytes_per_step": int(xy_pin.nbytes + f_pin.nbytes),
+               "d2h_bytes_per_step": int(lam_h.nbytes),
+               "api": "rbf_interpolate_host (pinned host xy, f -> host lambda)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        os.environ["OMP_NUM_THREADS"] = str(cores)
+        dt, scale, res, swl, full = oracle_sample(args.config)
+        cpu = {"value": dt * scale, "unit": "s", "cores": cores, "kind": "oracle",
+               "sample": f"oracle solve of {swl.n} points ({swl.name}, same recipe) took "
+                         f"{dt:.2f} s ({res.iterations} it); x{scale:.1f} linear-in-N "
+                         f"extrapolation to {full.name}"}
+
+    if rank == 0:
+        r0 = reps[0]
+        line = {
+            "metric": METRIC, "value": ms_per_step / 1e3, "unit": "s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": wl.name, "N": wl.n, "desc": W.CONFIG_DESCRIPTIONS[args.config],
+                       "parallelism": f"strips{world}", "l2": "flushed (256 MiB write) between steps",
+                       "step": "rbf_setup (cell list + RASM setup) + rbf_solve, inputs in HBM"},
+            "iterations": iters, "restarts": r0.restarts, "resid_est": r0.resid_est,
+            "resid_true": r0.resid_true, "resid_precond": r0.resid_precond,
+            "phase_ms": {"matvec": mv_live, "rasm_apply": pc_live, "orth": orth_live,
+                         "solve_total": statistics.mean(r.ms_total for r in reps),
+                         "setup_and_other": ms_per_step - statistics.mean(r.ms_total for r in reps)},
+            "matvec_gpairs_s": gpairs,
+            "matvec_ms": mv_ms, "rasm_apply_ms": pc_ms,
+            "matvec_fp64_frac_useful": gpairs * 1e9 * FLOP_PER_PAIR / (FP64_PEAK_TFLOPS * 1e12),
+            "rasm_apply_gbs": pc_alg_bytes / (pc_ms * 1e-3) / 1e9,
+            "roofline": roof, "clocks": clk, "gpu_launches": int(launches),
+            "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+    run_ours(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

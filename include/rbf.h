@@ -193,6 +193,15 @@ int rbf_dot(rbf_ctx *ctx, const double *a_dev, const double *b_dev, double *out_
 int rbf_plan_strips(const int64_t *row_counts, int64_t ncy, int32_t nranks, int64_t min_rows,
                     int64_t *row_bounds);
 
+/* Context facts: out[0] = doubles stored in the X blocks (RASM apply streams
+ * 8*out[0] bytes per application), out[1] = subdomains, out[2] = largest
+ * |Omega_c|, out[3] = largest |own(c)|, out[4] = subdomains solved by the
+ * global-memory LU path, out[5..6] = ncx, ncy, out[7] = device bytes held. */
+int rbf_info(const rbf_ctx *ctx, int64_t out[8]);
+
+/* Number of kernel launches this library has issued so far (process-wide). */
+int64_t rbf_launch_count(void);
+
 const char *rbf_last_error(void);
 void rbf_destroy(rbf_ctx *ctx);
 

@@ -2,6 +2,7 @@
 // strip planning, and the thin wrappers around the kernels.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstring>
@@ -12,6 +13,9 @@
 namespace rbf {
 
 static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+
+void count_launch(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
 void set_error(const char *fmt, ...) {
   char buf[1024];
@@ -114,6 +118,21 @@ using namespace rbf;
 extern "C" {
 
 const char *rbf_last_error(void) { return g_err.c_str(); }
+
+int64_t rbf_launch_count(void) { return g_launches.load(); }
+
+int rbf_info(const rbf_ctx *c, int64_t out[8]) {
+  if (!c || !out) { set_error("NULL argument"); return RBF_EINVAL; }
+  out[0] = c->x_count;
+  out[1] = c->nsub;
+  out[2] = c->max_ov;
+  out[3] = c->max_own;
+  out[4] = c->n_lu;
+  out[5] = c->g.ncx;
+  out[6] = c->g.ncy;
+  out[7] = c->bytes;
+  return RBF_OK;
+}
 
 int rbf_get_nccl_id(unsigned char out[128]) {
   if (!out) { set_error("out is NULL"); return RBF_EINVAL; }
@@ -257,8 +276,8 @@ int rbf_cell_list(const rbf_ctx *c, int64_t *perm, int64_t *cs, int64_t dims[2],
   if (!c) { set_error("NULL ctx"); return RBF_EINVAL; }
   cudaStream_t s = (cudaStream_t)stream;
   long long nc = (long long)c->g.ncx * c->g.ncy + 1;
-  if (perm) k_i32_to_i64<<<(int)((c->n + 255) / 256), 256, 0, s>>>(c->perm, c->n, perm);
-  if (cs) k_i32_to_i64<<<(int)((nc + 255) / 256), 256, 0, s>>>(c->cell_start, nc, cs);
+  if (perm) k_i32_to_i64<<<(int)((c->n + 255) / 256), 256, 0, s>>>(c->perm, c->n, perm); count_launch(1);
+  if (cs) k_i32_to_i64<<<(int)((nc + 255) / 256), 256, 0, s>>>(c->cell_start, nc, cs); count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
   if (dims) { dims[0] = c->g.ncx; dims[1] = c->g.ncy; }
   return RBF_OK;

@@ -89,7 +89,7 @@ int build_cell_list(rbf_ctx *c, const double *xy, cudaStream_t s) {
   RBF_TRY(dalloc(c, (void **)&c->cell_start, sizeof(int) * ((size_t)ncells + 1), s));
   int init_bad = 0x7fffffff;
   RBF_CUDA_TRY(cudaMemcpyAsync(bad, &init_bad, sizeof(int), cudaMemcpyHostToDevice, s));
-  k_cell_keys<<<blocks_for(n, 256), 256, 0, s>>>(xy, n, c->g, keys, vals, bad);
+  k_cell_keys<<<blocks_for(n, 256), 256, 0, s>>>(xy, n, c->g, keys, vals, bad); count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
   int end_bit = 1;
   while ((1LL << end_bit) < (long long)ncells) ++end_bit;
@@ -100,12 +100,13 @@ int build_cell_list(rbf_ctx *c, const double *xy, cudaStream_t s) {
   RBF_TRY(dalloc(c, &tmp, tmp_bytes, s));
   RBF_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, skeys, vals, c->perm, n, 0,
                                                end_bit, s));
-  k_cell_start<<<blocks_for(n, 256), 256, 0, s>>>(skeys, n, ncells, c->cell_start);
+  count_launch(1 + (end_bit + 7) / 8);  // onesweep: histogram + one pass per 8-bit digit
+  k_cell_start<<<blocks_for(n, 256), 256, 0, s>>>(skeys, n, ncells, c->cell_start); count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
   // row starts (host copy drives the strip plan and the halo ranges)
   long long *rs = nullptr;
   RBF_TRY(dalloc(c, (void **)&rs, sizeof(long long) * (c->g.ncy + 1), s));
-  k_row_start<<<blocks_for(c->g.ncy + 1, 256), 256, 0, s>>>(c->cell_start, c->g.ncx, c->g.ncy, rs);
+  k_row_start<<<blocks_for(c->g.ncy + 1, 256), 256, 0, s>>>(c->cell_start, c->g.ncx, c->g.ncy, rs); count_launch(1);
   c->row_start.assign(c->g.ncy + 1, 0);
   int hbad = 0;
   RBF_CUDA_TRY(cudaMemcpyAsync(c->row_start.data(), rs, sizeof(long long) * (c->g.ncy + 1),
@@ -130,7 +131,7 @@ int gather_positions(rbf_ctx *c, const double *xy, cudaStream_t s) {
   long long cnt = c->s.ext_hi - c->s.ext_lo;
   RBF_TRY(dalloc(c, (void **)&c->xy_ext, sizeof(double2) * (size_t)(cnt > 0 ? cnt : 1), s));
   if (cnt > 0) {
-    k_gather_xy<<<blocks_for(cnt, 256), 256, 0, s>>>(xy, c->perm, c->s.ext_lo, cnt, c->xy_ext);
+    k_gather_xy<<<blocks_for(cnt, 256), 256, 0, s>>>(xy, c->perm, c->s.ext_lo, cnt, c->xy_ext); count_launch(1);
     RBF_CUDA_TRY(cudaGetLastError());
   }
   return RBF_OK;
@@ -138,21 +139,30 @@ int gather_positions(rbf_ctx *c, const double *xy, cudaStream_t s) {
 
 int launch_to_local(const rbf_ctx *c, const double *vc, double *vl, cudaStream_t s) {
   long long cnt = n_loc(c);
-  if (cnt > 0) k_to_local<<<blocks_for(cnt, 256), 256, 0, s>>>(vc, c->perm, c->s.own_lo, cnt, vl);
+  if (cnt > 0) {
+    k_to_local<<<blocks_for(cnt, 256), 256, 0, s>>>(vc, c->perm, c->s.own_lo, cnt, vl);
+    count_launch(1);
+  }
   RBF_CUDA_TRY(cudaGetLastError());
   return RBF_OK;
 }
 
 int launch_from_local(const rbf_ctx *c, const double *vl, double *vc, cudaStream_t s) {
   long long cnt = n_loc(c);
-  if (cnt > 0) k_from_local<<<blocks_for(cnt, 256), 256, 0, s>>>(vl, c->perm, c->s.own_lo, cnt, vc);
+  if (cnt > 0) {
+    k_from_local<<<blocks_for(cnt, 256), 256, 0, s>>>(vl, c->perm, c->s.own_lo, cnt, vc);
+    count_launch(1);
+  }
   RBF_CUDA_TRY(cudaGetLastError());
   return RBF_OK;
 }
 
 int launch_local_index(const rbf_ctx *c, int64_t *idx, cudaStream_t s) {
   long long cnt = n_loc(c);
-  if (cnt > 0) k_local_index<<<blocks_for(cnt, 256), 256, 0, s>>>(c->perm, c->s.own_lo, cnt, idx);
+  if (cnt > 0) {
+    k_local_index<<<blocks_for(cnt, 256), 256, 0, s>>>(c->perm, c->s.own_lo, cnt, idx);
+    count_launch(1);
+  }
   RBF_CUDA_TRY(cudaGetLastError());
   return RBF_OK;
 }
@@ -187,7 +197,7 @@ int count_pairs(rbf_ctx *c, long long *out, cudaStream_t s) {
   RBF_TRY(dalloc(c, (void **)&d, sizeof(unsigned long long), s));
   RBF_CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(unsigned long long), s));
   int nc = owned_cells(c);
-  if (nc > 0) k_count_pairs<<<nc, 64, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, d);
+  if (nc > 0) k_count_pairs<<<nc, 64, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, d); count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
   RBF_CUDA_TRY(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
   RBF_CUDA_TRY(cudaStreamSynchronize(s));

@@ -14,6 +14,7 @@
 namespace rbf {
 
 void set_error(const char *fmt, ...);
+void count_launch(int k);  // kernel launches issued by this library (rbf_launch_count)
 
 #define RBF_CUDA_TRY(call)                                                               \
   do {                                                                                   \

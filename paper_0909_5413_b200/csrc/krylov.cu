@@ -232,7 +232,7 @@ static int axpy_dot(rbf_ctx *c, const double *coef, double *w, const double *x, 
                     double *out_dev, cudaStream_t s) {
   const long long n = n_loc(c);
   k_axpy_dot<<<grid_for(n), kRedThreads, 0, s>>>(coef, c->nranks, w, x, v, n, c->red_part,
-                                                  c->red_count, out_dev);
+                                                  c->red_count, out_dev); count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
   return RBF_OK;
 }
@@ -334,8 +334,8 @@ int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double 
     const double tol = std::fmax(gp->rtol * beta0, gp->atol);
     for (;;) {
       // V0 holds the unscaled preconditioned residual; its ||.||^2 is in slot 0
-      k_cycle_init<<<1, 1, 0, s>>>(c->dscal, L, hall_slot(c, L, 0));
-      k_scale_by_norm<<<blocks, kRedThreads, 0, s>>>(V, n, hall_slot(c, L, 0), L.P);
+      k_cycle_init<<<1, 1, 0, s>>>(c->dscal, L, hall_slot(c, L, 0)); count_launch(1);
+      k_scale_by_norm<<<blocks, kRedThreads, 0, s>>>(V, n, hall_slot(c, L, 0), L.P); count_launch(1);
       RBF_CUDA_TRY(cudaGetLastError());
       int kend = 0;
       bool done = false;
@@ -355,8 +355,8 @@ int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double 
         }
         RBF_TRY(axpy_dot(c, hall_slot(c, L, k), w, vk, w, c->dscal + L.hloc() + k + 1, s));
         RBF_TRY(reduce_slot(c, L, k + 1, s));
-        k_givens<<<1, 1, 0, s>>>(c->dscal, L, hall_slot(c, L, 0), k);
-        k_scale_by_norm<<<blocks, kRedThreads, 0, s>>>(w, n, hall_slot(c, L, k + 1), L.P);
+        k_givens<<<1, 1, 0, s>>>(c->dscal, L, hall_slot(c, L, 0), k); count_launch(1);
+        k_scale_by_norm<<<blocks, kRedThreads, 0, s>>>(w, n, hall_slot(c, L, k + 1), L.P); count_launch(1);
         RBF_CUDA_TRY(cudaGetLastError());
         pt.rec(3, s);
         RBF_TRY(read_scalars(c, c->dscal + L.out(), 2, s));
@@ -381,13 +381,13 @@ int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double 
           break;
         }
       }
-      k_backsolve<<<1, 1, 0, s>>>(c->dscal, L, kend);
-      k_update_x<<<blocks, kRedThreads, 0, s>>>(x, V, ldv, c->dscal, L, kend, n);
+      k_backsolve<<<1, 1, 0, s>>>(c->dscal, L, kend); count_launch(1);
+      k_update_x<<<blocks, kRedThreads, 0, s>>>(x, V, ldv, c->dscal, L, kend, n); count_launch(1);
       RBF_CUDA_TRY(cudaGetLastError());
       if (done) break;
       // restart: V0 = M^-1 (f - A x), explicitly
       RBF_TRY(op.matvec(x, c->t1));
-      k_sub<<<blocks, kRedThreads, 0, s>>>(f, c->t1, n);
+      k_sub<<<blocks, kRedThreads, 0, s>>>(f, c->t1, n); count_launch(1);
       RBF_TRY(op.pc(c->t1, V));
       double bsq = 0.0;
       RBF_TRY(global_dot(c, L, V, V, &bsq, s));
@@ -415,7 +415,7 @@ int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double 
     double fsq = 0.0, rsq = 0.0, psq = 0.0;
     RBF_TRY(global_dot(c, L, f, f, &fsq, s));
     RBF_TRY(op.matvec(x, c->t1));
-    k_sub<<<blocks, kRedThreads, 0, s>>>(f, c->t1, n);
+    k_sub<<<blocks, kRedThreads, 0, s>>>(f, c->t1, n); count_launch(1);
     RBF_TRY(global_dot(c, L, c->t1, c->t1, &rsq, s));
     RBF_TRY(op.pc(c->t1, c->t2));
     RBF_TRY(global_dot(c, L, c->t2, c->t2, &psq, s));

@@ -48,7 +48,7 @@ int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStre
   if (nc <= 0) return RBF_OK;
   int blocks = (nc + kMvWarps - 1) / kMvWarps;
   k_matvec_v1<<<blocks, 32 * kMvWarps, 0, s>>>(c->g, c->s, c->xy_ext, w_ext, c->cell_start, nc,
-                                               y_loc);
+                                               y_loc); count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
   return RBF_OK;
 }

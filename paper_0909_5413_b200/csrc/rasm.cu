@@ -409,13 +409,14 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
   RBF_TRY(dalloc(c, (void **)&glist, sizeof(int) * (ncl > 0 ? ncl : 1), s));
   RBF_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * 8, s));
   k_rasm_sizes<<<(ncl + 1 + 255) / 256, 256, 0, s>>>(c->g, c->s, c->cell_start, ncl, smem_limit,
-                                                     sizes, cnt, glist);
+                                                     sizes, cnt, glist); count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
   size_t tmp_bytes = 0;
   RBF_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, sizes, c->x_off, ncl + 1, s));
   void *tmp = nullptr;
   RBF_TRY(dalloc(c, &tmp, tmp_bytes, s));
   RBF_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, sizes, c->x_off, ncl + 1, s));
+  count_launch(2);  // init + scan
   int hc[8];
   long long total = 0;
   RBF_CUDA_TRY(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
@@ -434,7 +435,7 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
     RBF_CUDA_TRY(cudaFuncSetAttribute(k_rasm_setup, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
     k_rasm_setup<<<ncl, kRsThreads, smem, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off,
-                                               c->X, smem, cnt, glist);
+                                               c->X, smem, cnt, glist); count_launch(1);
     RBF_CUDA_TRY(cudaGetLastError());
     RBF_CUDA_TRY(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
     RBF_CUDA_TRY(cudaStreamSynchronize(s));
@@ -455,7 +456,7 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
     for (int first = 0; first < nglobal; first += (int)batch) {
       int count = nglobal - first < batch ? nglobal - first : (int)batch;
       k_rasm_setup_lu<<<count, kLuThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off,
-                                                   c->X, glist, first, count, ws, stride, fail);
+                                                   c->X, glist, first, count, ws, stride, fail); count_launch(1);
       RBF_CUDA_TRY(cudaGetLastError());
     }
     RBF_CUDA_TRY(cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -478,7 +479,7 @@ int launch_rasm_apply(const rbf_ctx *c, const double *r_ext, double *z_loc, cuda
   if (ncl <= 0 || c->nsub == 0) return RBF_OK;
   size_t smem = sizeof(double) * (size_t)c->max_ov;
   k_rasm_apply_v1<<<ncl, kRaThreads, smem, s>>>(c->g, c->s, c->cell_start, c->x_off, c->X, r_ext,
-                                                z_loc);
+                                                z_loc); count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
   return RBF_OK;
 }

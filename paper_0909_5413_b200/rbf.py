@@ -55,7 +55,7 @@ EXPORTS = ["rbf_get_nccl_id", "rbf_setup", "rbf_local_count", "rbf_ext_count", "
            "rbf_local_index", "rbf_cell_list", "rbf_to_local", "rbf_from_local", "rbf_matvec",
            "rbf_rasm_apply", "rbf_matvec_ext", "rbf_rasm_apply_ext", "rbf_solve",
            "rbf_interpolate_host", "rbf_count_pairs", "rbf_dot", "rbf_plan_strips",
-           "rbf_last_error", "rbf_destroy"]
+           "rbf_last_error", "rbf_destroy", "rbf_info", "rbf_launch_count"]
 
 _lib = None
 
@@ -89,6 +89,8 @@ def lib() -> C.CDLL:
             "rbf_dot": (C.c_int, [p, p, p, p, p]),
             "rbf_plan_strips": (C.c_int, [p, i64, i32, i64, p]),
             "rbf_last_error": (C.c_char_p, []),
+            "rbf_info": (C.c_int, [p, p]),
+            "rbf_launch_count": (i64, []),
             "rbf_destroy": (None, [p]),
         }
         for name, (res, args) in sigs.items():
@@ -118,6 +120,11 @@ def _stream(stream):
 
 def make_params(sigma, cell, rc, rings=1, box=(-1.0, -1.0, 1.0, 1.0)) -> Params:
     return Params(float(sigma), float(cell), float(rc), int(rings), 0, *map(float, box))
+
+
+def launch_count() -> int:
+    """Kernel launches issued by librbf.so so far (process-wide)."""
+    return int(lib().rbf_launch_count())
 
 
 def get_nccl_id() -> bytes:
@@ -259,6 +266,12 @@ class Context:
         r = _report(rep, hist)
         r.status = code
         return lam, r
+
+    def info(self) -> dict:
+        o = np.zeros(8, dtype=np.int64)
+        _check(lib().rbf_info(self._h, o.ctypes.data_as(C.c_void_p)))
+        keys = ["x_doubles", "nsub", "max_ov", "max_own", "n_lu", "ncx", "ncy", "bytes_device"]
+        return {k: int(v) for k, v in zip(keys, o)}
 
     def count_pairs(self) -> int:
         v = C.c_int64()
