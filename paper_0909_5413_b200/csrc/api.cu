@@ -97,6 +97,10 @@ static int validate(const rbf_params *p, long long n) {
   if (!(p->sigma > 0.0) || !std::isfinite(p->sigma)) { set_error("sigma must be > 0"); return RBF_EINVAL; }
   if (!(p->cell > 0.0) || !std::isfinite(p->cell)) { set_error("cell must be > 0"); return RBF_EINVAL; }
   if (!(p->rc > 0.0) || !std::isfinite(p->rc)) { set_error("rc must be > 0"); return RBF_EINVAL; }
+  if (p->rc > 37.0 * p->sigma) {  // exp(-rc^2/2sigma^2) < 1e-297: the kernels assume this
+    set_error("rc must be <= 37 sigma (entries beyond are below fp64 range)");
+    return RBF_EINVAL;
+  }
   if (p->overlap_rings < 0 || p->overlap_rings > 7) {
     set_error("overlap_rings must be in [0, 7]");
     return RBF_EINVAL;
@@ -154,7 +158,13 @@ void rbf_destroy(rbf_ctx *c) {
   dfree(c->cell_start, s);
   dfree(c->perm, s);
   dfree(c->xy_ext, s);
+  dfree(c->xyf_ext, s);
   dfree(c->x_off, s);
+  dfree(c->chunk_first, s);
+  dfree(c->chunk_cell, s);
+  dfree(c->chunk_len, s);
+  dfree(c->chunk_off, s);
+  dfree(c->nlist, s);
   dfree(c->X, s);
   dfree(c->w_ext, s);
   dfree(c->V, s);
@@ -244,6 +254,7 @@ int rbf_setup(rbf_ctx **out, const double *xy, int64_t n, const rbf_params *p, c
   halo(g.kh, c->halo_mv);
   halo(g.rings, c->halo_pc);
   st = gather_positions(c, xy, s);
+  if (st == RBF_OK) st = build_nlist(c, s);
   if (st == RBF_OK && c->nranks > 1)
     st = dalloc(c, (void **)&c->w_ext, sizeof(double) * (size_t)(n_ext(c) > 0 ? n_ext(c) : 1), s);
   if (st == RBF_OK) st = comm_init(c, d);

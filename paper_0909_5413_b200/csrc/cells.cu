@@ -42,12 +42,25 @@ __global__ void k_cell_start(const int *__restrict__ skeys, int n, int ncells,
     for (int k = k1 + 1; k <= ncells; ++k) cell_start[k] = n;
 }
 
-__global__ void k_gather_xy(const double *__restrict__ xy, const int *__restrict__ perm,
-                            long long lo, long long cnt, double2 *__restrict__ out) {
+// Sorted positions (fp64) and, for the matvec's conservative fp32 prefilter, the
+// position relative to the point's own cell origin in fp32.
+__global__ void k_gather_xy(const double *__restrict__ xy, const int *__restrict__ perm, Geom g,
+                            long long lo, long long cnt, double2 *__restrict__ out,
+                            float2 *__restrict__ outf) {
   long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= cnt) return;
   long long i = perm[lo + t];
-  out[t] = make_double2(xy[2 * i], xy[2 * i + 1]);
+  const double x = xy[2 * i], y = xy[2 * i + 1];
+  out[t] = make_double2(x, y);
+  const int cx = cell_coord(x, g.x0, g.cell, g.ncx), cy = cell_coord(y, g.y0, g.cell, g.ncy);
+  outf[t] = make_float2((float)(x - (g.x0 + cx * g.cell)), (float)(y - (g.y0 + cy * g.cell)));
+}
+
+__global__ void k_max_cell(const int *__restrict__ cell_start, int ncells, int *__restrict__ out) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  int v = (k < ncells) ? cell_start[k + 1] - cell_start[k] : 0;
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0 && v > 0) atomicMax(out, v);
 }
 
 __global__ void k_row_start(const int *__restrict__ cell_start, int ncx, int ncy,
@@ -84,7 +97,8 @@ int build_cell_list(rbf_ctx *c, const double *xy, cudaStream_t s) {
   RBF_TRY(dalloc(c, (void **)&keys, sizeof(int) * n, s));
   RBF_TRY(dalloc(c, (void **)&vals, sizeof(int) * n, s));
   RBF_TRY(dalloc(c, (void **)&skeys, sizeof(int) * n, s));
-  RBF_TRY(dalloc(c, (void **)&bad, sizeof(int), s));
+  RBF_TRY(dalloc(c, (void **)&bad, sizeof(int) * 2, s));
+  RBF_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int) * 2, s));
   RBF_TRY(dalloc(c, (void **)&c->perm, sizeof(int) * n, s));
   RBF_TRY(dalloc(c, (void **)&c->cell_start, sizeof(int) * ((size_t)ncells + 1), s));
   int init_bad = 0x7fffffff;
@@ -107,12 +121,17 @@ int build_cell_list(rbf_ctx *c, const double *xy, cudaStream_t s) {
   long long *rs = nullptr;
   RBF_TRY(dalloc(c, (void **)&rs, sizeof(long long) * (c->g.ncy + 1), s));
   k_row_start<<<blocks_for(c->g.ncy + 1, 256), 256, 0, s>>>(c->cell_start, c->g.ncx, c->g.ncy, rs); count_launch(1);
+  k_max_cell<<<blocks_for(ncells, 256), 256, 0, s>>>(c->cell_start, ncells, bad + 1);
+  count_launch(1);
+  int hmax = 0;
   c->row_start.assign(c->g.ncy + 1, 0);
   int hbad = 0;
   RBF_CUDA_TRY(cudaMemcpyAsync(c->row_start.data(), rs, sizeof(long long) * (c->g.ncy + 1),
                                cudaMemcpyDeviceToHost, s));
   RBF_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaMemcpyAsync(&hmax, bad + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
   RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  c->max_cell = hmax;
   dfree(tmp, s);
   dfree(keys, s);
   dfree(vals, s);
@@ -130,8 +149,11 @@ int build_cell_list(rbf_ctx *c, const double *xy, cudaStream_t s) {
 int gather_positions(rbf_ctx *c, const double *xy, cudaStream_t s) {
   long long cnt = c->s.ext_hi - c->s.ext_lo;
   RBF_TRY(dalloc(c, (void **)&c->xy_ext, sizeof(double2) * (size_t)(cnt > 0 ? cnt : 1), s));
+  RBF_TRY(dalloc(c, (void **)&c->xyf_ext, sizeof(float2) * (size_t)(cnt > 0 ? cnt : 1), s));
   if (cnt > 0) {
-    k_gather_xy<<<blocks_for(cnt, 256), 256, 0, s>>>(xy, c->perm, c->s.ext_lo, cnt, c->xy_ext); count_launch(1);
+    k_gather_xy<<<blocks_for(cnt, 256), 256, 0, s>>>(xy, c->perm, c->g, c->s.ext_lo, cnt, c->xy_ext,
+                                                     c->xyf_ext);
+    count_launch(1);
     RBF_CUDA_TRY(cudaGetLastError());
   }
   return RBF_OK;
@@ -197,7 +219,10 @@ int count_pairs(rbf_ctx *c, long long *out, cudaStream_t s) {
   RBF_TRY(dalloc(c, (void **)&d, sizeof(unsigned long long), s));
   RBF_CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(unsigned long long), s));
   int nc = owned_cells(c);
-  if (nc > 0) k_count_pairs<<<nc, 64, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, d); count_launch(1);
+  if (nc > 0) {
+    k_count_pairs<<<nc, 64, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, d);
+    count_launch(1);
+  }
   RBF_CUDA_TRY(cudaGetLastError());
   RBF_CUDA_TRY(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
   RBF_CUDA_TRY(cudaStreamSynchronize(s));

@@ -68,6 +68,53 @@ struct Halo {  // one direction of a halo exchange, in element offsets
   long long recv_off, recv_cnt;  // relative to the ext vector
 };
 
+
+// exp(x) for x <= 0 on the FP64 pipe with a 64-entry table (reading Q15: <= 2 ulp;
+// measured max 1 ulp against CUDA exp() over [-18.5, 0], tools/micro.cu):
+//   k = round(64 x / ln2),  r = x - k ln2/64 (Cody-Waite, ln2/64 = L_HI + L_LO,
+//   L_HI with 32 trailing zero bits so k*L_HI is exact),  |r| <= ln2/128,
+//   exp(x) = 2^(k>>6) * T[k & 63] * (1 + r + r^2/2 + ... + r^5/120).
+// 10 FP64 instructions + one cached table load, vs ~22 for exp().  x < -707 returns 0
+// (the true value is below 1e-307).
+static __device__ const double kExp2Tab64[64] = {
+1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284,
+1.0442737824274138, 1.0556451783605572, 1.0671404006768237, 1.0787607977571199,
+1.0905077326652577, 1.102382583307841, 1.1143867425958924, 1.1265216186082418,
+1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812,
+1.189207115002721, 1.202156731452703, 1.215247359980469, 1.22848053610687,
+1.241857812073484, 1.255380757024691, 1.2690509571917332, 1.2828700160787783,
+1.2968395546510096, 1.3109612115247644, 1.3252366431597413, 1.339667524053303,
+1.3542555469368927, 1.3690024229745905, 1.383909881963832, 1.3989796725383112,
+1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647,
+1.4768261459394993, 1.4929077282912648, 1.5091644275934228, 1.5255981507445384,
+1.5422108254079407, 1.559004400237837, 1.5759808451078865, 1.593142151342267,
+1.6104903319492543, 1.6280274218573478, 1.645755478153965, 1.6636765803267364,
+1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062,
+1.7562521603732995, 1.7753764925265212, 1.7947090750031072, 1.8142521755003989,
+1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656,
+1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951};
+
+__device__ __forceinline__ double exp_neg(double x) {
+  const double kMagic = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer shifter
+  const double kInvL = 92.33248261689366;    // 64 / ln2
+  const double kLHi = 0.010830417275428772;  // ln2/64, high part (32 trailing zero bits)
+  const double kLLo = 7.420820373486988e-09; // ln2/64 - kLHi
+  if (x < -707.0) return 0.0;
+  const double t = fma(x, kInvL, kMagic);
+  const double kd = t - kMagic;
+  const int k = __double2loint(t);
+  double r = fma(kd, -kLHi, x);
+  r = fma(kd, -kLLo, r);
+  double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  p = fma(r, p, 1.0 / 6.0);
+  p = fma(r, p, 0.5);
+  p = fma(r, p, 1.0);
+  p = r * p;
+  const double T = __ldg(&kExp2Tab64[k & 63]);
+  const double e = fma(T, p, T);
+  return __hiloint2double(__double2hiint(e) + ((k >> 6) << 20), __double2loint(e));
+}
+
 }  // namespace rbf
 
 struct rbf_ctx {
@@ -84,11 +131,21 @@ struct rbf_ctx {
   int *cell_start = nullptr;   // ncx*ncy+1
   int *perm = nullptr;         // N: caller index of global sorted entry
   double2 *xy_ext = nullptr;   // positions of the ext range, sorted
+  float2 *xyf_ext = nullptr;   // fp32 positions relative to each point's cell origin (matvec prefilter)
   // RASM
   long long *x_off = nullptr;  // per owned cell (ncx * owned rows + 1), in doubles
   double *X = nullptr;         // rows of A_c^-1 for own(c), row-major, ld = n_ov rounded up to even
   long long x_count = 0;
   int max_ov = 0, max_own = 0, nsub = 0, n_lu = 0;
+  int max_cell = 0;            // largest cell population (all cells of the ext range)
+  // matvec neighbour list (ELL of 32-bit entries in groups of 4, chunks of 32 targets)
+  int nchunks = 0;
+  int *chunk_first = nullptr;  // per owned cell (+1): first chunk
+  int *chunk_cell = nullptr;   // per chunk: owned cell index
+  int *chunk_len = nullptr;    // per chunk: list length (max over its lanes)
+  long long *chunk_off = nullptr;  // per chunk (+1): first entry
+  int *nlist = nullptr;           // source index (ext-relative sorted order), -1 = padding
+  long long nlist_entries = 0;
   // workspaces
   double *w_ext = nullptr;     // n_ext (multi-rank only)
   double *V = nullptr;         // (restart+1) x n_loc Krylov basis
@@ -120,6 +177,7 @@ int launch_from_local(const rbf_ctx *c, const double *v_loc, double *v_caller, c
 int launch_local_index(const rbf_ctx *c, int64_t *idx, cudaStream_t s);
 
 // matvec.cu
+int build_nlist(rbf_ctx *c, cudaStream_t s);
 int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStream_t s);
 
 // rasm.cu

@@ -17,13 +17,13 @@
 // cell that streams X once per GMRES iteration (HBM-bound).  Every output entry
 // is written by exactly one cell (partition property): no atomics.
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 #include "common.cuh"
 
 namespace rbf {
 
 constexpr int kMaxRuns = 15;   // rings <= 7
-constexpr int kRsThreads = 256;
 constexpr int kRaThreads = 128;
 
 struct Runs {
@@ -59,34 +59,77 @@ __device__ __forceinline__ int nat_to_global(const Runs &R, int q) {
   return R.lo[r] + q;
 }
 
-__device__ __forceinline__ long long tri(int i) { return (long long)i * (i + 1) / 2; }
+// ---------------------------------------------------------------------------
+// Shared-memory tile layout of one subdomain matrix (tensor-core setup).
+//
+// Factor order: the block's other points [0, n0), padding to n0p = ceil8(n0), the
+// cell's own points [n0p, n0p + n1), padding to N = n0p + n1p.  Padding unknowns
+// are decoupled identity rows/columns, so they change nothing (their pivots are 1).
+// The lower triangle is stored as 8x8 tiles, tile (it, jt) (jt <= it) at
+// ((it (it+1))/2 + jt) * 64 doubles, row-major with an XOR swizzle of the column
+// (c ^ 4*((r>>1)&1)) so that the DMMA fragment loads (8 rows x 4 columns) and the
+// 16-byte accumulator stores are bank-conflict free.
+// ---------------------------------------------------------------------------
+constexpr int kTcThreads = 512;
+constexpr int kTcWarps = kTcThreads / 32;
+constexpr int kTcMaxTiles = 29;  // N <= 232: 435 tiles = 222,720 B of shared memory
 
-// flat index f of a lower triangle (row a >= col b) -> (a, b)
-__device__ __forceinline__ void tri_index(int f, int &a, int &b) {
-  a = (int)((sqrtf(8.0f * (float)f + 1.0f) - 1.0f) * 0.5f);
-  while ((long long)a * (a + 1) / 2 > f) --a;
-  while ((long long)(a + 1) * (a + 2) / 2 <= f) ++a;
-  b = f - a * (a + 1) / 2;
-}
+__device__ __forceinline__ int toff(int it, int jt) { return ((it * (it + 1)) / 2 + jt) * 64; }
+__device__ __forceinline__ int swz(int r, int c) { return r * 8 + (c ^ (((r >> 1) & 1) << 2)); }
 
-// Shared-memory layout for one subdomain of n points, n_own own points.
-struct SetupSmem {
-  size_t off_B, off_pos, off_gidx, total;
-  __host__ __device__ SetupSmem(int n, int n_own) {
-    size_t a = (size_t)n * (n + 1) / 2 * sizeof(double);
-    off_B = a;
-    size_t b = off_B + (size_t)n_own * n_own * sizeof(double);
-    off_pos = (b + 15) & ~(size_t)15;
-    off_gidx = off_pos + (size_t)n * sizeof(double2);
-    total = off_gidx + (size_t)n * sizeof(int);
+struct TileShape {
+  int n, n0, n1, n0p, n1p, N, T, T0, T1;
+  __host__ __device__ TileShape(int n_ov, int n_own) {
+    n = n_ov;
+    n1 = n_own;
+    n0 = n_ov - n_own;
+    n0p = (n0 + 7) & ~7;
+    n1p = (n1 + 7) & ~7;
+    N = n0p + n1p;
+    T = N / 8;
+    T0 = n0p / 8;
+    T1 = n1p / 8;
+  }
+  __host__ __device__ bool fits_tc() const { return T <= kTcMaxTiles && n1p <= 32; }
+  __host__ __device__ size_t smem_bytes() const {
+    return ((size_t)T * (T + 1) / 2 * 64 + (size_t)T * 8) * 8 + (size_t)N * sizeof(double2);
   }
 };
 
-// Per owned cell: X block size, maxima, and the list of cells whose factor does
-// not fit in shared memory (they go to the global-memory LU kernel).
+// D += A * B, one 8x8x4 fp64 tensor-core MMA (DMMA on sm_100a).
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Fragment offsets inside a swizzled tile (lane l): A[m][k] = X[m][k] and
+// B[k][n] = X[n][k] use "rowk"; B[k][n] = X[k][n] and A[m][k] = X[k][m] use "colk".
+__device__ __forceinline__ int frag_rowk(int lane, int h) { return swz(lane >> 2, 4 * h + (lane & 3)); }
+__device__ __forceinline__ int frag_colk(int lane, int h) { return swz(4 * h + (lane & 3), lane >> 2); }
+__device__ __forceinline__ int frag_acc(int lane) { return swz(lane >> 2, 2 * (lane & 3)); }
+
+// factor index p -> global sorted index (or -1 for a padding unknown)
+__device__ __forceinline__ int fac_to_global(const Runs &R, const TileShape &S, int p) {
+  int q;
+  if (p < S.n0) q = (p < R.own_nat_lo) ? p : p + S.n1;
+  else if (p >= S.n0p && p < S.n0p + S.n1) q = R.own_nat_lo + (p - S.n0p);
+  else return -1;
+  return nat_to_global(R, q);
+}
+
+// natural column q -> factor index
+__device__ __forceinline__ int nat_to_fac(const Runs &R, const TileShape &S, int q) {
+  if (q < R.own_nat_lo) return q;
+  if (q < R.own_nat_lo + S.n1) return S.n0p + (q - R.own_nat_lo);
+  return q - S.n1;
+}
+
+// Per owned cell: X block size, maxima, and the list of cells that the tensor-core
+// kernel cannot take (they go to the global-memory LU kernel).
 __global__ void k_rasm_sizes(Geom g, Strip st, const int *__restrict__ cell_start, int ncl,
-                             size_t smem_limit, long long *__restrict__ sizes,
-                             int *__restrict__ maxes, int *__restrict__ glist) {
+                             long long *__restrict__ sizes, int *__restrict__ maxes,
+                             int *__restrict__ glist) {
   int cl = blockIdx.x * blockDim.x + threadIdx.x;
   if (cl >= ncl) {
     if (cl == ncl) sizes[cl] = 0;
@@ -101,148 +144,344 @@ __global__ void k_rasm_sizes(Geom g, Strip st, const int *__restrict__ cell_star
     atomicMax(&maxes[0], R.n_ov);
     atomicMax(&maxes[1], R.n_own);
     atomicAdd(&maxes[2], 1);
-    if (SetupSmem(R.n_ov, R.n_own).total > smem_limit) glist[atomicAdd(&maxes[3], 1)] = cl;
+    TileShape S(R.n_ov, R.n_own);
+    if (!S.fits_tc()) glist[atomicAdd(&maxes[3], 1)] = cl;
+    else atomicMax(&maxes[4], S.T);
   }
 }
 
-__global__ __launch_bounds__(kRsThreads) void k_rasm_setup(
+// One CTA per cell.  Left-looking blocked Cholesky A_c = L L^T on 8x8 tiles with the
+// products on the fp64 tensor cores (DMMA 8x8x4), software-pipelined so that the
+// serial 8x8 diagonal factorization of column j (one warp) overlaps the
+// accumulation of column j+1 (the other warps); then
+//   W = L21 L11^-1 (backward tile sweep, one warp per own tile row),
+//   S^-1 = (L22 L22^T)^-1 (the Schur complement's inverse, concurrently on the other warps),
+//   X_c = S^-1 [-W, I]  (the rows of A_c^-1 for own(c), Eq.(9)-(11)),
+// written to HBM in natural column order.
+constexpr int kAccWarps = kTcWarps - 2;  // warps 14, 15 alternate as diagonal warps
+
+struct AccSet {
+  double a0, a1, b0, b1;  // two independent DMMA chains (even / odd kt)
+  __device__ __forceinline__ void zero() { a0 = a1 = b0 = b1 = 0.0; }
+};
+
+// acc += sum_{kt in [k0, k1)} L(it, kt) L(jt, kt)^T
+__device__ __forceinline__ void acc_range(AccSet &A, const double *sm, int it, int jt, int k0,
+                                          int k1, int lane) {
+  const double *Li = sm + toff(it, 0), *Lj = sm + toff(jt, 0);
+  const int f0 = frag_rowk(lane, 0), f1 = frag_rowk(lane, 1);
+  int kt = k0;
+  for (; kt + 1 < k1; kt += 2) {
+    dmma(A.a0, A.a1, Li[kt * 64 + f0], Lj[kt * 64 + f0]);
+    dmma(A.b0, A.b1, Li[(kt + 1) * 64 + f0], Lj[(kt + 1) * 64 + f0]);
+    dmma(A.a0, A.a1, Li[kt * 64 + f1], Lj[kt * 64 + f1]);
+    dmma(A.b0, A.b1, Li[(kt + 1) * 64 + f1], Lj[(kt + 1) * 64 + f1]);
+  }
+  if (kt < k1) {
+    dmma(A.a0, A.a1, Li[kt * 64 + f0], Lj[kt * 64 + f0]);
+    dmma(A.a0, A.a1, Li[kt * 64 + f1], Lj[kt * 64 + f1]);
+  }
+}
+
+// C(it, jt) = A(it, jt) - acc, stored in place (accumulator layout)
+__device__ __forceinline__ void acc_finish(const AccSet &A, double *sm, int it, int jt, int lane) {
+  double2 *cp = reinterpret_cast<double2 *>(sm + toff(it, jt) + frag_acc(lane));
+  double2 cv = *cp;
+  cv.x -= A.a0 + A.b0;
+  cv.y -= A.a1 + A.b1;
+  *cp = cv;
+}
+
+// 8x8 Cholesky of the diagonal tile j in place (lanes 0..7 = rows) plus its inverse:
+// lower part = L_d, upper part (r < c) = Linv[c][r], rdiag = 1 / diag(L_d).
+__device__ __forceinline__ bool diag_factor(double *sm, double *rdiag, int j, int lane) {
+  double *D = sm + toff(j, j);
+  double a[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) a[c] = (lane < 8) ? D[swz(lane, c)] : 1.0;
+  bool bad = false;
+  double rinv = 1.0;  // 1 / L[lane][lane]
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double akk = __shfl_sync(0xffffffffu, a[k], k);
+    bad |= !(akk > 0.0);
+    const double il = rsqrt(akk);  // 1 / l_kk
+    const double lik = (lane == k) ? akk * il : a[k] * il;
+    if (lane == k) rinv = il;
+    a[k] = (lane >= k) ? lik : 0.0;
+#pragma unroll
+    for (int jj = k + 1; jj < 8; ++jj) {
+      const double ljk = __shfl_sync(0xffffffffu, lik, jj);
+      if (lane >= jj) a[jj] = fma(-lik, ljk, a[jj]);
+    }
+  }
+  // Linv column `lane`: x = L^-1 e_lane by forward substitution
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    double sacc = (lane == i) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) sacc = fma(-__shfl_sync(0xffffffffu, a[k], i), x[k], sacc);
+    x[i] = sacc * __shfl_sync(0xffffffffu, rinv, i);
+  }
+  if (lane < 8) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) D[swz(lane, c)] = (c <= lane) ? a[c] : x[c];
+    rdiag[j * 8 + lane] = rinv;
+  }
+  return bad;
+}
+
+__global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
     Geom g, Strip st, const double2 *__restrict__ xy, const int *__restrict__ cell_start,
-    const long long *__restrict__ x_off, double *__restrict__ X, size_t smem_limit,
-    int *__restrict__ counts, int *__restrict__ glist) {
-  extern __shared__ __align__(16) unsigned char smem[];
+    const long long *__restrict__ x_off, double *__restrict__ X, int *__restrict__ counts,
+    int *__restrict__ glist) {
+  extern __shared__ __align__(16) double sm[];
   __shared__ Runs R;
-  const int tid = threadIdx.x, T = blockDim.x;
+  __shared__ int s_fail;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int cl = blockIdx.x;
   const int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
-  if (tid == 0) block_runs(g, cell_start, cx, cy, R);
-  __syncthreads();
-  const int n = R.n_ov, n_own = R.n_own, n0 = n - n_own;
-  if (n_own == 0) return;
-  const int own_nat = R.own_nat_lo;
-  SetupSmem L(n, n_own);
-  if (L.total > smem_limit) return;  // handled by k_rasm_setup_lu
-  double *A = reinterpret_cast<double *>(smem);
-  double *B = reinterpret_cast<double *>(smem + L.off_B);
-  double2 *pos = reinterpret_cast<double2 *>(smem + L.off_pos);
-
-  // factor order p -> natural order q: own(c) moved to the end
-  for (int p = tid; p < n; p += T) {
-    int q = (p < n0) ? (p < own_nat ? p : p + n_own) : own_nat + (p - n0);
-    pos[p] = xy[nat_to_global(R, q) - st.ext_lo];
+  if (tid == 0) {
+    block_runs(g, cell_start, cx, cy, R);
+    s_fail = 0;
   }
   __syncthreads();
-  // A_c = R_c A_rc R_c^T, packed lower triangle (reading Q10)
-  {
-    const int warp = tid >> 5, lane = tid & 31, nw = T >> 5;
-    for (int i = warp; i < n; i += nw) {
-      const double2 pi = pos[i];
-      for (int j = lane; j <= i; j += 32) {
-        const double2 pj = pos[j];
-        const double dx = pi.x - pj.x, dy = pi.y - pj.y;
+  if (R.n_own == 0) return;
+  const TileShape S(R.n_ov, R.n_own);
+  if (!S.fits_tc()) return;  // handled by k_rasm_setup_lu
+  const int T = S.T, T0 = S.T0, T1 = S.T1, N = S.N;
+  double *rdiag = sm + T * (T + 1) / 2 * 64;
+  double2 *pos = reinterpret_cast<double2 *>(rdiag + T * 8);
+
+  // ---- positions in factor order, then A_c = R_c A_rc R_c^T (reading Q10)
+  for (int p = tid; p < N; p += kTcThreads) {
+    const int gi = fac_to_global(R, S, p);
+    pos[p] = (gi >= 0) ? xy[gi - st.ext_lo] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  const int ntiles = T * (T + 1) / 2;
+  for (int t = warp; t < ntiles; t += kTcWarps) {
+    int it = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+    while (it * (it + 1) / 2 > t) --it;
+    while ((it + 1) * (it + 2) / 2 <= t) ++it;
+    const int jt = t - it * (it + 1) / 2;
+    const int r = lane >> 2, c0 = 2 * (lane & 3);
+    const int pi = it * 8 + r;
+    const bool padi = (pi >= S.n0 && pi < S.n0p) || pi >= S.n0p + S.n1;
+    const double2 xi = pos[pi];
+    double v[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int pj = jt * 8 + c0 + u;
+      const bool padj = (pj >= S.n0 && pj < S.n0p) || pj >= S.n0p + S.n1;
+      if (padi || padj) {
+        v[u] = (pi == pj) ? 1.0 : 0.0;
+      } else {
+        const double2 xj = pos[pj];
+        const double dx = xi.x - xj.x, dy = xi.y - xj.y;
         const double r2 = fma(dx, dx, dy * dy);
-        A[tri(i) + j] = (r2 < g.rc2) ? exp(r2 * g.neg_inv_2s2) * g.norm : 0.0;
+        v[u] = (r2 < g.rc2) ? exp_neg(r2 * g.neg_inv_2s2) * g.norm : 0.0;
       }
     }
+    *reinterpret_cast<double2 *>(&sm[toff(it, jt) + swz(r, c0)]) = make_double2(v[0], v[1]);
   }
-  for (int t = tid; t < n_own * n_own; t += T) B[t] = ((t / n_own) == (t % n_own)) ? 1.0 : 0.0;
   __syncthreads();
 
-  // Right-looking Cholesky, one barrier per column: step k updates the trailing
-  // triangle with a_ik a_jk / d_k (column k still unscaled) and finalises
-  // column k-1 (not read in step k).
-  bool failed = false;
-  double l_prev_inv = 0.0;
-  for (int k = 0; k < n; ++k) {
-    const double d = A[tri(k) + k];
-    if (!(d > 0.0)) { failed = true; break; }  // uniform: every thread reads the same d
-    const double inv_d = 1.0 / d;
-    const int m = n - 1 - k;
-    const int nt = m * (m + 1) / 2;
-    if (nt > 0) {
-      int a, b;
-      tri_index(tid, a, b);
-      for (int f = tid; f < nt; f += T) {
-        const int i = k + 1 + a, j = k + 1 + b;
-        A[tri(i) + j] -= A[tri(i) + k] * A[tri(j) + k] * inv_d;
-        b += T;
-        while (b > a) { b -= a + 1; ++a; }
+  // ---- software-pipelined left-looking Cholesky over tile columns
+  AccSet acc[2];
+  acc[0].zero();
+  acc[1].zero();
+  for (int j = 0; j < T; ++j) {
+    const int dw = kAccWarps + (j & 1);  // diagonal warp of column j
+    if (warp < kAccWarps) {
+      // step 1: finish column j (tiles it > j) with the kt = j-1 term
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int it = j + 1 + warp + kAccWarps * m;
+        if (it < T) {
+          if (j >= 1) acc_range(acc[m], sm, it, j, j - 1, j, lane);
+          acc_finish(acc[m], sm, it, j, lane);
+        }
+      }
+      // step 2: accumulate column j+1 (tiles it > j+1) over kt < j
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int it = j + 2 + warp + kAccWarps * m;
+        acc[m].zero();
+        if (it < T && j + 1 < T) acc_range(acc[m], sm, it, j + 1, 0, j, lane);
+      }
+    } else if (warp == dw) {
+      // finish the diagonal tile (its sum over kt < j-1 was accumulated last step)
+      if (j >= 1) acc_range(acc[0], sm, j, j, j - 1, j, lane);
+      acc_finish(acc[0], sm, j, j, lane);
+      __syncwarp();
+      if (diag_factor(sm, rdiag, j, lane) && lane == 0) s_fail = 1;
+    } else if (j + 1 < T) {
+      // the other diagonal warp accumulates the next diagonal tile over kt < j
+      acc[0].zero();
+      acc_range(acc[0], sm, j + 1, j + 1, 0, j, lane);
+    }
+    __syncthreads();
+    if (s_fail) break;  // uniform
+    // step 4: panel L(it, j) = C(it, j) L_d^-T  (B[k][n] = Linv[n][k])
+    if (warp < kAccWarps) {
+      const double *D = sm + toff(j, j);
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int it = j + 1 + warp + kAccWarps * m;
+        if (it < T) {
+          double *Ct = sm + toff(it, j);
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int k = 4 * h + (lane & 3), n = lane >> 2;
+            const double bv = (n > k) ? D[swz(k, n)] : (n == k ? rdiag[j * 8 + k] : 0.0);
+            dmma(d0, d1, Ct[frag_rowk(lane, h)], bv);
+          }
+          __syncwarp();
+          *reinterpret_cast<double2 *>(Ct + frag_acc(lane)) = make_double2(d0, d1);
+        }
       }
     }
-    if (k > 0) {  // finalise column k-1
-      for (int i = k + tid; i < n; i += T) A[tri(i) + k - 1] *= l_prev_inv;
-      if (tid == 0) A[tri(k - 1) + k - 1] = 1.0 / l_prev_inv;
-    }
-    const double l = sqrt(d);
-    l_prev_inv = 1.0 / l;
     __syncthreads();
   }
-  if (failed) {  // Cholesky broke down: redo this cell with LU (reading Q11)
+  if (s_fail) {  // Cholesky broke down: redo this cell with LU (reading Q11)
     if (tid == 0) glist[atomicAdd(&counts[3], 1)] = cl;
     return;
   }
-  if (tid == 0) A[tri(n - 1) + n - 1] = 1.0 / l_prev_inv;
-  __syncthreads();
 
-  // W = L21 L11^-1 in place over L21 (rows n0.., cols ..n0), column j finished at
-  // step j and scaled one step later.
-  for (int j = n0 - 1; j >= 0; --j) {
-    const double inv = 1.0 / A[tri(j) + j];
-    const int nt = n_own * j;
-    for (int f = tid; f < nt; f += T) {
-      const int r = f / j, kk = f - r * j;
-      const long long row = tri(n0 + r);
-      A[row + kk] -= A[row + j] * inv * A[tri(j) + kk];
-    }
-    if (j + 1 < n0) {
-      const double inv1 = 1.0 / A[tri(j + 1) + j + 1];
-      for (int r = tid; r < n_own; r += T) A[tri(n0 + r) + j + 1] *= inv1;
-    }
-    __syncthreads();
-  }
-  if (n0 > 0) {
-    const double inv0 = 1.0 / A[0];
-    for (int r = tid; r < n_own; r += T) A[tri(n0 + r) + 0] *= inv0;
-  }
-  __syncthreads();
-
-  // Columns of S^-1 [-W, I]: per column, L22 y = b then L22^T x = y.
-  for (int p = tid; p < n; p += T) {
-    // column storage: W part in A (row n0+r, col p), identity part in B (row r, col p-n0)
-    const bool wpart = p < n0;
-    const long long bcol = p - n0;
-    auto colp = [&](int r) -> double & {
-      return wpart ? A[tri(n0 + r) + p] : B[(long long)r * n_own + bcol];
-    };
-    for (int r = 0; r < n_own; ++r) {
-      double s = wpart ? -colp(r) : colp(r);
-      const long long row = tri(n0 + r) + n0;
-      for (int c2 = 0; c2 < r; ++c2) s -= A[row + c2] * colp(c2);
-      colp(r) = s / A[row + r];
-    }
-    for (int r = n_own - 1; r >= 0; --r) {
-      double s = colp(r);
-      for (int c2 = r + 1; c2 < n_own; ++c2) s -= A[tri(n0 + c2) + n0 + r] * colp(c2);
-      colp(r) = s / A[tri(n0 + r) + n0 + r];
-    }
-  }
-  __syncthreads();
-
-  // X_c[o][q] (natural column order), ld = n rounded up to even
-  const long long ld = (n + 1) & ~1;
-  double *Xc = X + x_off[cl];
-  for (int o = 0; o < n_own; ++o) {
-    for (int q = tid; q < ld; q += T) {
-      double v = 0.0;
-      if (q < n) {
-        int p;
-        if (q < own_nat) p = q;
-        else if (q < own_nat + n_own) p = n0 + (q - own_nat);
-        else p = q - n_own;
-        v = (p < n0) ? A[tri(n0 + o) + p] : B[(long long)o * n_own + (p - n0)];
+  // ---- W = L21 L11^-1 (warps 0..T1-1, one own tile row each, right to left) and
+  //      S^-1 = L22^-T L22^-1 (the other warps; lane = row, one column at a time)
+  double sinv[4];
+  if (warp < T1) {
+    const int it = T0 + warp;
+    double *Wrow = sm + toff(it, 0);
+    for (int jt = T0 - 1; jt >= 0; --jt) {
+      AccSet A, B;  // four independent DMMA chains
+      A.zero();
+      B.zero();
+      int kt = jt + 1;
+      const int f0 = frag_rowk(lane, 0), f1 = frag_rowk(lane, 1);
+      const int g0 = frag_colk(lane, 0), g1 = frag_colk(lane, 1);
+      for (; kt + 1 < T0; kt += 2) {
+        const double *Lk = sm + toff(kt, jt), *Lk1 = sm + toff(kt + 1, jt);
+        dmma(A.a0, A.a1, Wrow[kt * 64 + f0], Lk[g0]);
+        dmma(A.b0, A.b1, Wrow[(kt + 1) * 64 + f0], Lk1[g0]);
+        dmma(B.a0, B.a1, Wrow[kt * 64 + f1], Lk[g1]);
+        dmma(B.b0, B.b1, Wrow[(kt + 1) * 64 + f1], Lk1[g1]);
       }
-      Xc[o * ld + q] = v;
+      if (kt < T0) {
+        const double *Lk = sm + toff(kt, jt);
+        dmma(A.a0, A.a1, Wrow[kt * 64 + f0], Lk[g0]);
+        dmma(B.a0, B.a1, Wrow[kt * 64 + f1], Lk[g1]);
+      }
+      A.a0 += B.a0;
+      A.a1 += B.a1;
+      A.b0 += B.b0;
+      A.b1 += B.b1;
+      acc_finish(A, sm, it, jt, lane);
+      __syncwarp();
+      // W(it, jt) = C L_d^-1   (B[k][n] = Linv[k][n])
+      const double *D = sm + toff(jt, jt);
+      double *Ct = Wrow + jt * 64;
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int k = 4 * h + (lane & 3), n = lane >> 2;
+        const double bv = (k > n) ? D[swz(n, k)] : (k == n ? rdiag[jt * 8 + k] : 0.0);
+        dmma(d0, d1, Ct[frag_rowk(lane, h)], bv);
+      }
+      __syncwarp();
+      *reinterpret_cast<double2 *>(Ct + frag_acc(lane)) = make_double2(d0, d1);
+      __syncwarp();
+    }
+  } else {
+    auto L22 = [&](int i, int j) -> double {
+      return sm[toff(T0 + (i >> 3), T0 + (j >> 3)) + swz(i & 7, j & 7)];
+    };
+    const int n1p = S.n1p;
+    const int nsw = kTcWarps - T1;  // warps solving for columns of S^-1
+    const double rd = (lane < n1p) ? rdiag[T0 * 8 + lane] : 1.0;  // 1 / L22[lane][lane]
+    // this warp's columns c = warp - T1 + sl * nsw, all advanced together (ILP)
+    double acc1[4], yv[4];
+#pragma unroll
+    for (int sl = 0; sl < 4; ++sl) {
+      const int c = warp - T1 + sl * nsw;
+      acc1[sl] = (lane == c) ? 1.0 : 0.0;
+      yv[sl] = 0.0;
+    }
+    for (int i = 0; i < n1p; ++i) {  // L22 y = e_c
+      const double lli = (lane > i && lane < n1p) ? L22(lane, i) : 0.0;
+#pragma unroll
+      for (int sl = 0; sl < 4; ++sl) {
+        if (lane == i) yv[sl] = acc1[sl] * rd;
+        const double yi = __shfl_sync(0xffffffffu, yv[sl], i);
+        acc1[sl] = fma(-lli, yi, acc1[sl]);
+      }
+    }
+#pragma unroll
+    for (int sl = 0; sl < 4; ++sl) {
+      acc1[sl] = yv[sl];
+      sinv[sl] = 0.0;
+    }
+    for (int i = n1p - 1; i >= 0; --i) {  // L22^T x = y
+      const double lil = (lane < i) ? L22(i, lane) : 0.0;
+#pragma unroll
+      for (int sl = 0; sl < 4; ++sl) {
+        if (lane == i) sinv[sl] = acc1[sl] * rd;
+        const double xi = __shfl_sync(0xffffffffu, sinv[sl], i);
+        acc1[sl] = fma(-lil, xi, acc1[sl]);
+      }
     }
   }
+  __syncthreads();
+  if (warp >= T1) {  // S^-1 (symmetric) -> lower half of the L22 tiles
+#pragma unroll
+    for (int sl = 0; sl < 4; ++sl) {
+      const int c = warp - T1 + sl * (kTcWarps - T1);
+      if (c < S.n1p && lane >= c && lane < S.n1p)
+        sm[toff(T0 + (lane >> 3), T0 + (c >> 3)) + swz(lane & 7, c & 7)] = sinv[sl];
+    }
+  }
+  __syncthreads();
+
+  // ---- X_c = S^-1 [-W, I] in natural column order, ld = n rounded up to even.
+  // X_other = -S^-1 W straight from the DMMA accumulators; X_own = S^-1.
+  const int n = S.n;
+  const int ld = (n + 1) & ~1;
+  double *Xc = X + x_off[cl];
+  for (int task = warp; task < T1 * T0; task += kTcWarps) {
+    const int ot = task / T0, jt = task - ot * T0;
+    double d0 = 0.0, d1 = 0.0;
+    for (int kt = 0; kt < T1; ++kt) {
+      // A = S^-1 tile (ot, kt): only the lower triangle of S^-1 is stored (the upper
+      // half of diagonal tiles still holds the L^-1 scratch), so read (k, m) above it.
+      const bool lower = kt <= ot;
+      const double *At = lower ? sm + toff(T0 + ot, T0 + kt) : sm + toff(T0 + kt, T0 + ot);
+      const double *Bt = sm + toff(T0 + kt, jt);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int m = lane >> 2, k = 4 * h + (lane & 3);
+        const bool below = (kt < ot) || (kt == ot && k <= m);
+        const double av = below ? At[swz(m, k)] : At[swz(k, m)];
+        dmma(d0, d1, av, Bt[frag_colk(lane, h)]);
+      }
+    }
+    const int o = ot * 8 + (lane >> 2);
+    const int p0 = jt * 8 + 2 * (lane & 3);
+    if (o < S.n1) {
+      if (p0 < S.n0) Xc[o * ld + (p0 < R.own_nat_lo ? p0 : p0 + S.n1)] = -d0;
+      if (p0 + 1 < S.n0) Xc[o * ld + (p0 + 1 < R.own_nat_lo ? p0 + 1 : p0 + 1 + S.n1)] = -d1;
+    }
+  }
+  for (int t = tid; t < S.n1 * S.n1; t += kTcThreads) {
+    const int o = t / S.n1, j = t - o * S.n1;
+    const int i1 = o >= j ? o : j, j1 = o >= j ? j : o;
+    Xc[o * ld + R.own_nat_lo + j] = sm[toff(T0 + (i1 >> 3), T0 + (j1 >> 3)) + swz(i1 & 7, j1 & 7)];
+  }
+  if (ld != n)
+    for (int o = tid; o < S.n1; o += kTcThreads) Xc[o * ld + n] = 0.0;
 }
 
 // Global-memory local solve for subdomains whose factor does not fit in shared
@@ -368,25 +607,57 @@ __global__ __launch_bounds__(kLuThreads) void k_rasm_setup_lu(
   }
 }
 
-__global__ __launch_bounds__(kRaThreads) void k_rasm_apply_v1(
+// z[own(c)] = X_c u[Omega_c]: one CTA per cell; u[Omega_c] gathered into shared
+// memory once, then each warp streams whole rows of X_c with 16-byte loads (rows are
+// 16-byte aligned: ld even, block offsets even), 4 loads in flight per lane.
+// Direct-load variant: one CTA per cell.  Each warp issues the 16-byte loads of its
+// first X row BEFORE the u[Omega_c] gather, and the next row's loads before the
+// current row's reduction, so the HBM stream never waits on the gather.
+__global__ __launch_bounds__(kRaThreads) void k_rasm_apply(
     Geom g, Strip st, const int *__restrict__ cell_start, const long long *__restrict__ x_off,
     const double *__restrict__ X, const double *__restrict__ u, double *__restrict__ z) {
   extern __shared__ double su[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int cl = blockIdx.x;
   const int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
+  const int key = cy * g.ncx + cx;
+  const int o0 = cell_start[key], n_own = cell_start[key + 1] - o0;
+  if (n_own == 0) return;
+  const long long nel = x_off[cl + 1] - x_off[cl];
+  const int ld = (int)(nel / n_own), h = ld >> 1;
+  const double2 *Xc = reinterpret_cast<const double2 *>(X + x_off[cl]);
+  auto load4 = [&](int o, int c0, double2 *xv) {
+    const double2 *row = Xc + (long long)o * h + c0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = lane + 32 * k;
+      xv[k] = (o < n_own && c0 + j < h) ? __ldcs(row + j) : make_double2(0.0, 0.0);
+    }
+  };
+  double2 xv[4];
+  load4(warp, 0, xv);  // in flight during the gather below
   Runs R;
   block_runs(g, cell_start, cx, cy, R);
-  if (R.n_own == 0) return;
   const int n = R.n_ov;
-  for (int q = tid; q < n; q += kRaThreads) su[q] = u[nat_to_global(R, q) - st.ext_lo];
+  for (int q = tid; q < ld; q += kRaThreads) su[q] = (q < n) ? u[nat_to_global(R, q) - st.ext_lo] : 0.0;
   __syncthreads();
-  const long long ld = (n + 1) & ~1;
-  const double *Xc = X + x_off[cl];
-  const int o0 = cell_start[cy * g.ncx + cx];
-  for (int o = warp; o < R.n_own; o += kRaThreads / 32) {
-    double acc = 0.0;
-    for (int q = lane; q < n; q += 32) acc = fma(Xc[o * ld + q], su[q], acc);
+  const double2 *u2 = reinterpret_cast<const double2 *>(su);
+  for (int o = warp; o < n_own; o += kRaThreads / 32) {
+    double acc = 0.0, acc2 = 0.0;
+    for (int c0 = 0; c0 < h; c0 += 128) {
+      if (c0 > 0) load4(o, c0, xv);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = c0 + lane + 32 * k;
+        if (j < h) {
+          const double2 uv = u2[j];
+          acc = fma(xv[k].x, uv.x, acc);
+          acc2 = fma(xv[k].y, uv.y, acc2);
+        }
+      }
+    }
+    load4(o + kRaThreads / 32, 0, xv);  // next row of this warp
+    acc += acc2;
 #pragma unroll
     for (int sh = 16; sh > 0; sh >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, sh);
     if (lane == 0) z[o0 + o - st.own_lo] = acc;
@@ -395,12 +666,6 @@ __global__ __launch_bounds__(kRaThreads) void k_rasm_apply_v1(
 
 int rasm_setup(rbf_ctx *c, cudaStream_t s) {
   const int ncl = owned_cells(c);
-  int dev = 0, smem_optin = 0;
-  RBF_CUDA_TRY(cudaGetDevice(&dev));
-  RBF_CUDA_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  cudaFuncAttributes fa;
-  RBF_CUDA_TRY(cudaFuncGetAttributes(&fa, k_rasm_setup));
-  const size_t smem_limit = (size_t)smem_optin - fa.sharedSizeBytes;  // dynamic part
   long long *sizes = nullptr;
   int *cnt = nullptr, *glist = nullptr;
   RBF_TRY(dalloc(c, (void **)&sizes, sizeof(long long) * (ncl + 1), s));
@@ -408,8 +673,9 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
   RBF_TRY(dalloc(c, (void **)&cnt, sizeof(int) * 8, s));
   RBF_TRY(dalloc(c, (void **)&glist, sizeof(int) * (ncl > 0 ? ncl : 1), s));
   RBF_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * 8, s));
-  k_rasm_sizes<<<(ncl + 1 + 255) / 256, 256, 0, s>>>(c->g, c->s, c->cell_start, ncl, smem_limit,
-                                                     sizes, cnt, glist); count_launch(1);
+  k_rasm_sizes<<<(ncl + 1 + 255) / 256, 256, 0, s>>>(c->g, c->s, c->cell_start, ncl, sizes, cnt,
+                                                     glist);
+  count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
   size_t tmp_bytes = 0;
   RBF_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, sizes, c->x_off, ncl + 1, s));
@@ -429,13 +695,15 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
   c->nsub = hc[2];
   c->x_count = total;
   RBF_TRY(dalloc(c, (void **)&c->X, sizeof(double) * (size_t)(total > 0 ? total : 2), s));
-  if (ncl > 0 && c->nsub > 0 && hc[3] < c->nsub) {
-    SetupSmem L(c->max_ov, c->max_own);
-    size_t smem = L.total < smem_limit ? L.total : smem_limit;
-    RBF_CUDA_TRY(cudaFuncSetAttribute(k_rasm_setup, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (ncl > 0 && c->nsub > hc[3]) {
+    const int Tmax = hc[4];
+    const size_t smem = ((size_t)Tmax * (Tmax + 1) / 2 * 64 + (size_t)Tmax * 8) * 8 +
+                        (size_t)Tmax * 8 * sizeof(double2);
+    RBF_CUDA_TRY(cudaFuncSetAttribute(k_rasm_setup_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
-    k_rasm_setup<<<ncl, kRsThreads, smem, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off,
-                                               c->X, smem, cnt, glist); count_launch(1);
+    k_rasm_setup_tc<<<ncl, kTcThreads, smem, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off,
+                                                  c->X, cnt, glist);
+    count_launch(1);
     RBF_CUDA_TRY(cudaGetLastError());
     RBF_CUDA_TRY(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
     RBF_CUDA_TRY(cudaStreamSynchronize(s));
@@ -474,12 +742,161 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
   return RBF_OK;
 }
 
+// ---------------------------------------------------------------------------
+// RASM apply, TMA version: a persistent CTA walks its cells; each cell's X block
+// (contiguous, n_own x ld doubles, 16-byte aligned) is fetched by one
+// cp.async.bulk (TMA, SASS UBLKCP) into a shared-memory stage signalled by an
+// mbarrier, double-buffered so the next cell's block streams in from HBM while
+// the current one is multiplied out of shared memory.  Blocks larger than a stage
+// (very dense cells) are streamed with plain 16-byte loads instead.
+// ---------------------------------------------------------------------------
+constexpr int kTmaThreads = 256;
+constexpr int kTmaStageBytes = 48 * 1024;
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned bytes,
+                                            unsigned long long *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__global__ __launch_bounds__(kTmaThreads) void k_rasm_apply_tma(
+    Geom g, Strip st, const int *__restrict__ cell_start, const long long *__restrict__ x_off,
+    const double *__restrict__ X, int ncl, int max_ov, const double *__restrict__ u,
+    double *__restrict__ z) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) unsigned long long bar[2];
+  double *stage[2] = {reinterpret_cast<double *>(smem),
+                      reinterpret_cast<double *>(smem + kTmaStageBytes)};
+  double *su = reinterpret_cast<double *>(smem + 2 * kTmaStageBytes);  // max_ov + 2 doubles
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  unsigned phase[2] = {0u, 0u};
+  auto block_bytes = [&](int cl) -> long long { return 8 * (x_off[cl + 1] - x_off[cl]); };
+  auto issue = [&](int cl, int sidx) {
+    const long long nb = block_bytes(cl);
+    if (nb > 0 && nb <= kTmaStageBytes) {
+      mbar_expect_tx(&bar[sidx], (unsigned)nb);
+      tma_load_1d(stage[sidx], X + x_off[cl], (unsigned)nb, &bar[sidx]);
+    }
+  };
+  int cl = blockIdx.x;
+  if (tid == 0 && cl < ncl) issue(cl, 0);
+  for (int it = 0; cl < ncl; ++it, cl += gridDim.x) {
+    const int sidx = it & 1;
+    const int nxt = cl + gridDim.x;
+    if (tid == 0 && nxt < ncl) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(nxt, sidx ^ 1);
+    }
+    const int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
+    Runs R;
+    block_runs(g, cell_start, cx, cy, R);
+    const long long nb = block_bytes(cl);
+    if (R.n_own > 0) {
+      const int n = R.n_ov;
+      const int ld = (n + 1) & ~1;
+      for (int q = tid; q < ld; q += kTmaThreads)
+        su[q] = (q < n) ? u[nat_to_global(R, q) - st.ext_lo] : 0.0;
+      const double2 *Xc;
+      if (nb <= kTmaStageBytes) {
+        mbar_wait(&bar[sidx], phase[sidx]);
+        phase[sidx] ^= 1u;
+        Xc = reinterpret_cast<const double2 *>(stage[sidx]);
+      } else {
+        Xc = reinterpret_cast<const double2 *>(X + x_off[cl]);
+      }
+      __syncthreads();
+      const double2 *u2 = reinterpret_cast<const double2 *>(su);
+      const int h = ld >> 1;
+      const int o0 = cell_start[cy * g.ncx + cx];
+      for (int o = warp; o < R.n_own; o += kTmaThreads / 32) {
+        const double2 *row = Xc + (long long)o * h;
+        double acc = 0.0, acc2 = 0.0;
+#pragma unroll 4
+        for (int j = lane; j < h; j += 32) {
+          const double2 xv = row[j];
+          const double2 uv = u2[j];
+          acc = fma(xv.x, uv.x, acc);
+          acc2 = fma(xv.y, uv.y, acc2);
+        }
+        acc += acc2;
+#pragma unroll
+        for (int sh = 16; sh > 0; sh >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, sh);
+        if (lane == 0) z[o0 + o - st.own_lo] = acc;
+      }
+    }
+    __syncthreads();  // stage sidx and su free for reuse
+  }
+  (void)max_ov;
+}
+
 int launch_rasm_apply(const rbf_ctx *c, const double *r_ext, double *z_loc, cudaStream_t s) {
   const int ncl = owned_cells(c);
   if (ncl <= 0 || c->nsub == 0) return RBF_OK;
-  size_t smem = sizeof(double) * (size_t)c->max_ov;
-  k_rasm_apply_v1<<<ncl, kRaThreads, smem, s>>>(c->g, c->s, c->cell_start, c->x_off, c->X, r_ext,
-                                                z_loc); count_launch(1);
+  static int use_tma = -1;
+  if (use_tma < 0) {
+    const char *e = getenv("RBF_APPLY_TMA");
+    use_tma = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (!use_tma) {
+    const size_t smem = sizeof(double) * (size_t)(c->max_ov + 2);
+    static size_t attr_d = 48 * 1024;
+    if (smem > attr_d) {
+      RBF_CUDA_TRY(cudaFuncSetAttribute(k_rasm_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+      attr_d = smem;
+    }
+    k_rasm_apply<<<ncl, kRaThreads, smem, s>>>(c->g, c->s, c->cell_start, c->x_off, c->X, r_ext,
+                                               z_loc);
+    count_launch(1);
+    RBF_CUDA_TRY(cudaGetLastError());
+    return RBF_OK;
+  }
+  const size_t smem = 2 * (size_t)kTmaStageBytes + sizeof(double) * (size_t)(c->max_ov + 2);
+  static size_t attr_bytes = 0;  // opt-in dynamic shared memory set so far
+  if (smem > attr_bytes) {
+    RBF_CUDA_TRY(cudaFuncSetAttribute(k_rasm_apply_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    attr_bytes = smem;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int per_sm = smem <= 113 * 1024 ? 2 : 1;
+  const int grid = ncl < sms * per_sm ? ncl : sms * per_sm;
+  k_rasm_apply_tma<<<grid, kTmaThreads, smem, s>>>(c->g, c->s, c->cell_start, c->x_off, c->X, ncl,
+                                                   c->max_ov, r_ext, z_loc);
+  count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
   return RBF_OK;
 }
