@@ -54,7 +54,7 @@ class Clocks:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
                                       stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
@@ -168,11 +168,11 @@ def run_ours(args, rank, world):
         c.close()
     barrier()
     # timed region: K steps, each bracketed by CUDA events; L2 flushed between steps
-    clocks = Clocks(dev)
+    clocks = Clocks(dev) if not os.environ.get("RBF_BENCH_NO_CLOCKS") else None
     launches0 = P.launch_count()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    reps = []
+    reps, setups = [], []
     barrier()
     for k in range(args.steps):
         flush.fill_(float(k))
@@ -180,10 +180,11 @@ def run_ours(args, rank, world):
         c, lam, rep = step(timing=True)
         ev[k][1].record(stream)
         reps.append(rep)
+        setups.append(c.setup_times())
         c.close()
     barrier()
     launches = P.launch_count() - launches0
-    clk = clocks.stop()
+    clk = clocks.stop() if clocks else {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["not sampled"]}
     ms = [a.elapsed_time(b) for a, b in ev]
     t_local = sum(ms)
     t = torch.tensor([t_local], dtype=torch.float64, device="cuda")
@@ -291,6 +292,7 @@ def run_ours(args, rank, world):
                        "step": "rbf_setup (cell list + RASM setup) + rbf_solve, inputs in HBM"},
             "iterations": iters, "restarts": r0.restarts, "resid_est": r0.resid_est,
             "resid_true": r0.resid_true, "resid_precond": r0.resid_precond,
+            "setup_ms": {k: statistics.mean(sd[k] for sd in setups) for k in setups[0]},
             "phase_ms": {"matvec": mv_live, "rasm_apply": pc_live, "orth": orth_live,
                          "solve_total": statistics.mean(r.ms_total for r in reps),
                          "setup_and_other": ms_per_step - statistics.mean(r.ms_total for r in reps)},

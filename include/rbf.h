@@ -199,6 +199,11 @@ int rbf_plan_strips(const int64_t *row_counts, int64_t ncy, int32_t nranks, int6
  * global-memory LU path, out[5..6] = ncx, ncy, out[7] = device bytes held. */
 int rbf_info(const rbf_ctx *ctx, int64_t out[8]);
 
+/* Device time (ms, CUDA events) of rbf_setup's phases for this context:
+ * out[0] = cell list, out[1] = positions + matvec neighbour list,
+ * out[2] = RASM setup (assemble + factor + X), out[3] = whole rbf_setup. */
+int rbf_setup_times(const rbf_ctx *ctx, double out[4]);
+
 /* Number of kernel launches this library has issued so far (process-wide). */
 int64_t rbf_launch_count(void);
 

@@ -125,6 +125,15 @@ const char *rbf_last_error(void) { return g_err.c_str(); }
 
 int64_t rbf_launch_count(void) { return g_launches.load(); }
 
+/* debug: per-CTA clock64 phase stamps of the RASM setup kernel (RBF_PROBE builds) */
+int rbf_debug_probe(int64_t *out) { return rbf::probe_read((long long *)out); }
+
+int rbf_setup_times(const rbf_ctx *c, double out[4]) {
+  if (!c || !out) { set_error("NULL argument"); return RBF_EINVAL; }
+  for (int i = 0; i < 4; ++i) out[i] = c->setup_ms[i];
+  return RBF_OK;
+}
+
 int rbf_info(const rbf_ctx *c, int64_t out[8]) {
   if (!c || !out) { set_error("NULL argument"); return RBF_EINVAL; }
   out[0] = c->x_count;
@@ -173,6 +182,8 @@ void rbf_destroy(rbf_ctx *c) {
   dfree(c->red_part, s);
   dfree(c->red_count, s);
   dfree(c->dscal, s);
+  dfree(c->ar_part, s);
+  dfree(c->ar_bar, s);
   if (c->hpin) cudaFreeHost(c->hpin);
   comm_destroy(c);
   delete c;
@@ -217,7 +228,11 @@ int rbf_setup(rbf_ctx **out, const double *xy, int64_t n, const rbf_params *p, c
   if (g.ncy < 1) g.ncy = 1;
   g.kh = (int)std::ceil(p->rc / p->cell * (1.0 + 1e-12));
   g.rings = p->overlap_rings;
+  cudaEvent_t ev[4];
+  for (auto &e : ev) cudaEventCreate(&e);
+  cudaEventRecord(ev[0], s);
   int st = build_cell_list(c, xy, s);
+  cudaEventRecord(ev[1], s);
   if (st != RBF_OK) { rbf_destroy(c); return st; }
   // strips of cell rows, balanced by point count; each strip >= halo depth rows
   const int depth = g.kh > g.rings ? g.kh : g.rings;
@@ -255,10 +270,24 @@ int rbf_setup(rbf_ctx **out, const double *xy, int64_t n, const rbf_params *p, c
   halo(g.rings, c->halo_pc);
   st = gather_positions(c, xy, s);
   if (st == RBF_OK) st = build_nlist(c, s);
+  cudaEventRecord(ev[2], s);
   if (st == RBF_OK && c->nranks > 1)
     st = dalloc(c, (void **)&c->w_ext, sizeof(double) * (size_t)(n_ext(c) > 0 ? n_ext(c) : 1), s);
   if (st == RBF_OK) st = comm_init(c, d);
   if (st == RBF_OK) st = rasm_setup(c, s);
+  cudaEventRecord(ev[3], s);
+  if (st == RBF_OK && cudaEventSynchronize(ev[3]) == cudaSuccess) {
+    float a = 0, b = 0, d = 0, t = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    cudaEventElapsedTime(&d, ev[2], ev[3]);
+    cudaEventElapsedTime(&t, ev[0], ev[3]);
+    c->setup_ms[0] = a;
+    c->setup_ms[1] = b;
+    c->setup_ms[2] = d;
+    c->setup_ms[3] = t;
+  }
+  for (auto &e : ev) cudaEventDestroy(e);
   if (st != RBF_OK) { rbf_destroy(c); return st; }
   *out = c;
   return RBF_OK;

@@ -154,8 +154,13 @@ struct rbf_ctx {
   double *red_part = nullptr;  // kRedBlocks
   unsigned *red_count = nullptr;
   double *dscal = nullptr;     // device scalars (see krylov.cu)
-  double *hpin = nullptr;      // pinned host scalars
+  double *hpin = nullptr;      // pinned, mapped host scalars: [0..2] GMRES mailbox, [8..] readbacks
+  double *hpin_dev = nullptr;  // device alias of hpin
+  int ar_grid = 0;             // CTAs of the fused single-rank Arnoldi kernel (0 = unused)
+  double *ar_part = nullptr;   // its per-CTA partial sums
+  unsigned *ar_bar = nullptr;  // its grid barrier (count, generation)
   long long bytes = 0;
+  double setup_ms[4] = {0, 0, 0, 0};
   cudaStream_t last_stream = nullptr;
 };
 
@@ -182,6 +187,7 @@ int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStre
 
 // rasm.cu
 int rasm_setup(rbf_ctx *c, cudaStream_t s);
+int probe_read(long long *out);  // RBF_PROBE builds only
 int launch_rasm_apply(const rbf_ctx *c, const double *r_ext, double *z_loc, cudaStream_t s);
 
 // comm.cu

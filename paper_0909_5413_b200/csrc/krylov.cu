@@ -11,6 +11,7 @@
 // residual estimate live on the device; the host reads back one scalar per
 // iteration to decide convergence.
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -127,7 +128,7 @@ __global__ void k_cycle_init(double *S, Scal L, const double *nrm2) {  // nrm2 =
 
 // Column k of H from the all-gathered MGS results, previous rotations, new rotation,
 // g update (Saad's GMRES with Givens; oracle orc_gmres follows the same steps).
-__global__ void k_givens(double *S, Scal L, const double *hall, int k) {
+__device__ void givens_step(double *S, const Scal &L, const double *hall, int k) {
   const int m = L.m;
   double *H = S + L.H();
   double *cs = S + L.cs(), *sn = S + L.sn(), *g = S + L.g();
@@ -149,6 +150,129 @@ __global__ void k_givens(double *S, Scal L, const double *hall, int k) {
   g[k] = cs[k] * g[k];
   S[L.out() + 0] = fabs(g[k + 1]);
   S[L.out() + 1] = hn;
+}
+
+// Host-mapped mailbox: the iteration's residual estimate and a sequence number the
+// host polls without any CUDA call (no stream synchronisation per iteration).
+struct Mailbox {
+  double gabs, hn;
+  long long seq;
+};
+
+__device__ __forceinline__ void post_mailbox(Mailbox *mb, const double *S, const Scal &L, long long seq) {
+  volatile Mailbox *v = mb;
+  v->gabs = S[L.out() + 0];
+  v->hn = S[L.out() + 1];
+  __threadfence_system();
+  v->seq = seq;
+}
+
+__global__ void k_givens(double *S, Scal L, const double *hall, int k, Mailbox *mb, long long seq) {
+  givens_step(S, L, hall, k);
+  post_mailbox(mb, S, L, seq);
+}
+
+// ---------------------------------------------------------------------------
+// Single-rank Arnoldi step in ONE cooperative launch: w = V[k+1] stays in
+// registers while all k+1 MGS projections, the norm, the scaling and the Givens
+// update run, separated by a software grid barrier (all CTAs co-resident by the
+// cooperative launch).  Each projection reads only v_j (8 B/element) instead of
+// w, v_{j-1}, v_j and a write of w.  Per-CTA partial sums are combined by every
+// CTA in CTA order: deterministic.
+// ---------------------------------------------------------------------------
+constexpr int kArThreads = 1024;
+constexpr int kArE = 8;  // elements per thread held in registers
+
+__device__ __forceinline__ void grid_sync(unsigned *bar, unsigned nb) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned *vgen = bar + 1;
+    const unsigned gen = *vgen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nb - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*vgen == gen) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double block_sum_ar(double v, double *sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double t = (threadIdx.x < kArThreads / 32) ? sh[threadIdx.x] : 0.0;
+  if (warp == 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) sh[32] = t;
+  }
+  __syncthreads();
+  return sh[32];
+}
+
+__global__ __launch_bounds__(kArThreads, 1) void k_arnoldi_fused(double *V, long long ldv, long long n,
+                                                              int k, double *S, Scal L,
+                                                              double *part, unsigned *bar,
+                                                              Mailbox *mb, long long seq) {
+  __shared__ double sh[33];
+  const unsigned G = gridDim.x;
+  const long long chunk = (n + G - 1) / G;
+  const long long base = (long long)blockIdx.x * chunk;
+  const long long end = base + chunk < n ? base + chunk : n;
+  double *wv = V + (long long)(k + 1) * ldv;
+  double w[kArE];
+#pragma unroll
+  for (int e = 0; e < kArE; ++e) {
+    const long long i = base + threadIdx.x + (long long)e * kArThreads;
+    w[e] = i < end ? wv[i] : 0.0;
+  }
+  for (int j = 0; j <= k + 1; ++j) {
+    double acc = 0.0;
+    const double *vj = V + (long long)j * ldv;
+    if (j <= k) {
+#pragma unroll
+      for (int e = 0; e < kArE; ++e) {
+        const long long i = base + threadIdx.x + (long long)e * kArThreads;
+        if (i < end) acc = fma(w[e], vj[i], acc);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < kArE; ++e) acc = fma(w[e], w[e], acc);
+    }
+    const double bs = block_sum_ar(acc, sh);
+    if (threadIdx.x == 0) part[(long long)j * G + blockIdx.x] = bs;
+    grid_sync(bar, G);
+    double t = 0.0;
+    for (unsigned b = threadIdx.x; b < G; b += kArThreads) t += ((volatile double *)part)[(long long)j * G + b];
+    const double h = block_sum_ar(t, sh);
+    if (blockIdx.x == 0 && threadIdx.x == 0) S[L.hloc() + j] = h;
+    if (j <= k) {  // v_j re-read: this CTA's slice was just streamed, so it hits L1/L2
+#pragma unroll
+      for (int e = 0; e < kArE; ++e) {
+        const long long i = base + threadIdx.x + (long long)e * kArThreads;
+        if (i < end) w[e] = fma(-h, vj[i], w[e]);
+      }
+    } else {
+      const double hn = sqrt(h);
+#pragma unroll
+      for (int e = 0; e < kArE; ++e) {
+        const long long i = base + threadIdx.x + (long long)e * kArThreads;
+        if (i < end) wv[i] = (hn != 0.0) ? w[e] / hn : w[e];
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    givens_step(S, L, S + L.hloc(), k);
+    post_mailbox(mb, S, L, seq);
+  }
 }
 
 // y = H(0:kend, 0:kend)^-1 g(0:kend)
@@ -218,7 +342,26 @@ static int ensure_workspace(rbf_ctx *c, int m, cudaStream_t s) {
     RBF_TRY(dalloc(c, (void **)&c->red_count, sizeof(unsigned), s));
     RBF_CUDA_TRY(cudaMemsetAsync(c->red_count, 0, sizeof(unsigned), s));
   }
-  if (!c->hpin) RBF_CUDA_TRY(cudaMallocHost((void **)&c->hpin, sizeof(double) * 64));
+  if (!c->hpin) {
+    RBF_CUDA_TRY(cudaHostAlloc((void **)&c->hpin, sizeof(double) * (16 + c->nranks), cudaHostAllocMapped));
+    RBF_CUDA_TRY(cudaHostGetDevicePointer((void **)&c->hpin_dev, c->hpin, 0));
+  }
+  if (c->nranks == 1 && !c->ar_part) {
+    int dev = 0, sms = 0, per_sm = 0;
+    RBF_CUDA_TRY(cudaGetDevice(&dev));
+    RBF_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    RBF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_arnoldi_fused, kArThreads, 0));
+    int coop = 0;
+    RBF_CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+    c->ar_grid = (coop && per_sm > 0) ? sms * (per_sm < 2 ? per_sm : 2) : 0;
+    if (getenv("RBF_NO_FUSED_ARNOLDI")) c->ar_grid = 0;
+    if (c->ar_grid > 0 && (long long)c->ar_grid * kArThreads * kArE < n) c->ar_grid = 0;
+    if (c->ar_grid > 0) {
+      RBF_TRY(dalloc(c, (void **)&c->ar_part, sizeof(double) * (size_t)(m + 2) * c->ar_grid, s));
+      RBF_TRY(dalloc(c, (void **)&c->ar_bar, sizeof(unsigned) * 2, s));
+      RBF_CUDA_TRY(cudaMemsetAsync(c->ar_bar, 0, sizeof(unsigned) * 2, s));
+    }
+  }
   return RBF_OK;
 }
 
@@ -249,7 +392,7 @@ static const double *hall_slot(rbf_ctx *c, const Scal &L, int slot) {
 }
 
 static int read_scalars(rbf_ctx *c, const double *src, int count, cudaStream_t s) {
-  RBF_CUDA_TRY(cudaMemcpyAsync(c->hpin, src, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaMemcpyAsync(c->hpin + 8, src, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
   RBF_CUDA_TRY(cudaStreamSynchronize(s));
   return RBF_OK;
 }
@@ -261,7 +404,7 @@ static int global_dot(rbf_ctx *c, const Scal &L, const double *a, const double *
   RBF_TRY(reduce_slot(c, L, 0, s));
   RBF_TRY(read_scalars(c, hall_slot(c, L, 0), c->nranks, s));
   double t = 0.0;
-  for (int r = 0; r < c->nranks; ++r) t += c->hpin[r];
+  for (int r = 0; r < c->nranks; ++r) t += c->hpin[8 + r];
   *out = t;
   return RBF_OK;
 }
@@ -272,34 +415,63 @@ int dot_host(rbf_ctx *c, const double *a, const double *b, double *out, cudaStre
   return global_dot(c, L, a, b, out, s);
 }
 
-struct PhaseTimer {
+struct PhaseTimer {  // rotating event sets; a set is read only when it is surely complete
+  static constexpr int kSets = 4;
   bool on = false;
-  cudaEvent_t e[4]{};
+  cudaEvent_t e[kSets][4]{};
   double mv = 0, pc = 0, orth = 0;
   int init(bool enable) {
     on = enable;
     if (!on) return RBF_OK;
-    for (auto &x : e) RBF_CUDA_TRY(cudaEventCreate(&x));
+    for (auto &set : e)
+      for (auto &x : set) RBF_CUDA_TRY(cudaEventCreate(&x));
     return RBF_OK;
   }
-  void rec(int i, cudaStream_t s) {
-    if (on) cudaEventRecord(e[i], s);
+  void rec(long long seq, int i, cudaStream_t s) {
+    if (on) cudaEventRecord(e[seq % kSets][i], s);
   }
-  void accumulate() {  // after a stream sync
-    if (!on) return;
+  // add the phase times of Arnoldi step `seq` (its events must be complete or
+  // `wait` must be set)
+  void accumulate(long long seq, bool wait) {
+    if (!on || seq < 1) return;
+    auto &set = e[seq % kSets];
+    if (wait) cudaEventSynchronize(set[3]);
     float a = 0, b = 0, d = 0;
-    cudaEventElapsedTime(&a, e[0], e[1]);
-    cudaEventElapsedTime(&b, e[1], e[2]);
-    cudaEventElapsedTime(&d, e[2], e[3]);
+    cudaEventElapsedTime(&a, set[0], set[1]);
+    cudaEventElapsedTime(&b, set[1], set[2]);
+    cudaEventElapsedTime(&d, set[2], set[3]);
     mv += a;
     pc += b;
     orth += d;
   }
   ~PhaseTimer() {
     if (on)
-      for (auto &x : e) cudaEventDestroy(x);
+      for (auto &set : e)
+        for (auto &x : set) cudaEventDestroy(x);
   }
 };
+
+// Spin on the mailbox until iteration `seq` has posted (no CUDA API call in the
+// fast path; the stream is queried now and then to surface errors).
+static int wait_mailbox(rbf_ctx *c, long long seq, cudaStream_t s, double *gabs, double *hn) {
+  volatile Mailbox *mb = reinterpret_cast<volatile Mailbox *>(c->hpin);
+  for (long long spin = 0; mb->seq < seq; ++spin) {
+    if ((spin & 0xfff) == 0xfff) {
+      cudaError_t e = cudaStreamQuery(s);
+      if (e != cudaSuccess && e != cudaErrorNotReady) {
+        set_error("GMRES iteration failed: %s", cudaGetErrorString(e));
+        return RBF_ECUDA;
+      }
+      if (e == cudaSuccess && mb->seq < seq) {  // stream drained but no post: cannot happen
+        set_error("GMRES mailbox: iteration %lld never posted", seq);
+        return RBF_ECUDA;
+      }
+    }
+  }
+  *gabs = mb->gabs;
+  *hn = mb->hn;
+  return RBF_OK;
+}
 
 int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double *x,
                 rbf_report *rep, cudaStream_t s) {
@@ -332,6 +504,8 @@ int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double 
     converged = 1;
   } else {
     const double tol = std::fmax(gp->rtol * beta0, gp->atol);
+    long long seq_enq = 0, seq_base = 0;  // Arnoldi steps enqueued; steps before this cycle
+    reinterpret_cast<volatile Mailbox *>(c->hpin)->seq = 0;
     for (;;) {
       // V0 holds the unscaled preconditioned residual; its ||.||^2 is in slot 0
       k_cycle_init<<<1, 1, 0, s>>>(c->dscal, L, hall_slot(c, L, 0)); count_launch(1);
@@ -339,29 +513,55 @@ int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double 
       RBF_CUDA_TRY(cudaGetLastError());
       int kend = 0;
       bool done = false;
-      for (int k = 0; k < m; ++k) {
+      // enqueue Arnoldi step k (matvec, preconditioner, orthogonalisation, Givens)
+      auto enqueue = [&](int k) -> int {
         double *vk = V + (long long)k * ldv;
         double *w = V + (long long)(k + 1) * ldv;
-        pt.rec(0, s);
+        const long long seq = ++seq_enq;
+        pt.rec(seq, 0, s);
         RBF_TRY(op.matvec(vk, c->t1));
-        pt.rec(1, s);
+        pt.rec(seq, 1, s);
         RBF_TRY(op.pc(c->t1, w));
-        pt.rec(2, s);
-        for (int j = 0; j <= k; ++j) {  // modified Gram-Schmidt, fused
-          const double *coef = (j > 0) ? hall_slot(c, L, j - 1) : nullptr;
-          const double *xprev = (j > 0) ? V + (long long)(j - 1) * ldv : nullptr;
-          RBF_TRY(axpy_dot(c, coef, w, xprev, V + (long long)j * ldv, c->dscal + L.hloc() + j, s));
-          RBF_TRY(reduce_slot(c, L, j, s));
+        pt.rec(seq, 2, s);
+        Mailbox *mb = reinterpret_cast<Mailbox *>(c->hpin_dev);
+        if (c->ar_grid > 0) {
+          // single rank: MGS + norm + scale + Givens in one cooperative launch
+          double *Sp = c->dscal;
+          double *part = c->ar_part;
+          unsigned *bar = c->ar_bar;
+          long long ldv_ = ldv, n_ = n, seq_ = seq;
+          int k_ = k;
+          void *args[] = {&V, &ldv_, &n_, &k_, &Sp, &L, &part, &bar, &mb, &seq_};
+          RBF_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_arnoldi_fused, c->ar_grid,
+                                                   kArThreads, args, 0, s));
+          count_launch(1);
+        } else {
+          for (int j = 0; j <= k; ++j) {  // modified Gram-Schmidt, fused axpy + dot
+            const double *coef = (j > 0) ? hall_slot(c, L, j - 1) : nullptr;
+            const double *xprev = (j > 0) ? V + (long long)(j - 1) * ldv : nullptr;
+            RBF_TRY(axpy_dot(c, coef, w, xprev, V + (long long)j * ldv, c->dscal + L.hloc() + j, s));
+            RBF_TRY(reduce_slot(c, L, j, s));
+          }
+          RBF_TRY(axpy_dot(c, hall_slot(c, L, k), w, vk, w, c->dscal + L.hloc() + k + 1, s));
+          RBF_TRY(reduce_slot(c, L, k + 1, s));
+          k_givens<<<1, 1, 0, s>>>(c->dscal, L, hall_slot(c, L, 0), k, mb, seq);
+          count_launch(1);
+          k_scale_by_norm<<<blocks, kRedThreads, 0, s>>>(w, n, hall_slot(c, L, k + 1), L.P);
+          count_launch(1);
         }
-        RBF_TRY(axpy_dot(c, hall_slot(c, L, k), w, vk, w, c->dscal + L.hloc() + k + 1, s));
-        RBF_TRY(reduce_slot(c, L, k + 1, s));
-        k_givens<<<1, 1, 0, s>>>(c->dscal, L, hall_slot(c, L, 0), k); count_launch(1);
-        k_scale_by_norm<<<blocks, kRedThreads, 0, s>>>(w, n, hall_slot(c, L, k + 1), L.P); count_launch(1);
         RBF_CUDA_TRY(cudaGetLastError());
-        pt.rec(3, s);
-        RBF_TRY(read_scalars(c, c->dscal + L.out(), 2, s));
-        pt.accumulate();
-        const double gabs = c->hpin[0], hn = c->hpin[1];
+        pt.rec(seq, 3, s);
+        return RBF_OK;
+      };
+      // One-iteration lookahead: step k+1 is enqueued before the host waits for
+      // step k's residual.  If step k converges, step k+1's writes (V[k+2], H column
+      // k+1, g[k+1..k+2]) are outside what the solution update reads.
+      RBF_TRY(enqueue(0));
+      for (int k = 0; k < m; ++k) {
+        if (k + 1 < m && it + 1 < gp->max_iters) RBF_TRY(enqueue(k + 1));
+        double gabs = 0.0, hn = 0.0;
+        RBF_TRY(wait_mailbox(c, seq_base + k + 1, s, &gabs, &hn));
+        if (k >= 1) pt.accumulate(seq_base + k, false);  // previous step: events complete
         ++it;
         resid_est = gabs / beta0;
         if (rep && rep->history && hist_len < rep->history_cap) rep->history[hist_len++] = resid_est;
@@ -381,6 +581,8 @@ int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double 
           break;
         }
       }
+      if (kend >= 1) pt.accumulate(seq_base + kend, true);  // last step of the cycle
+      seq_base = seq_enq;
       k_backsolve<<<1, 1, 0, s>>>(c->dscal, L, kend); count_launch(1);
       k_update_x<<<blocks, kRedThreads, 0, s>>>(x, V, ldv, c->dscal, L, kend, n); count_launch(1);
       RBF_CUDA_TRY(cudaGetLastError());

@@ -160,6 +160,28 @@ __global__ void k_rasm_sizes(Geom g, Strip st, const int *__restrict__ cell_star
 // written to HBM in natural column order.
 constexpr int kAccWarps = kTcWarps - 2;  // warps 14, 15 alternate as diagonal warps
 
+#ifdef RBF_PROBE
+__device__ long long g_probe[64][8];
+__device__ long long g_trace[65536][3];  // per CTA: smid, globaltimer at entry, at exit
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int smid() {
+  int r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+#define TRACE(i) \
+  if (threadIdx.x == 0 && blockIdx.x < 65536) { g_trace[blockIdx.x][0] = smid(); g_trace[blockIdx.x][i] = gtimer(); }
+#define PROBE(i) \
+  if (threadIdx.x == 0 && blockIdx.x < 64) g_probe[blockIdx.x][i] = clock64();
+#else
+#define PROBE(i)
+#define TRACE(i)
+#endif
+
 struct AccSet {
   double a0, a1, b0, b1;  // two independent DMMA chains (even / odd kt)
   __device__ __forceinline__ void zero() { a0 = a1 = b0 = b1 = 0.0; }
@@ -236,6 +258,7 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
     Geom g, Strip st, const double2 *__restrict__ xy, const int *__restrict__ cell_start,
     const long long *__restrict__ x_off, double *__restrict__ X, int *__restrict__ counts,
     int *__restrict__ glist) {
+  TRACE(1)
   extern __shared__ __align__(16) double sm[];
   __shared__ Runs R;
   __shared__ int s_fail;
@@ -251,6 +274,7 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
   const TileShape S(R.n_ov, R.n_own);
   if (!S.fits_tc()) return;  // handled by k_rasm_setup_lu
   const int T = S.T, T0 = S.T0, T1 = S.T1, N = S.N;
+  PROBE(0)
   double *rdiag = sm + T * (T + 1) / 2 * 64;
   double2 *pos = reinterpret_cast<double2 *>(rdiag + T * 8);
 
@@ -288,6 +312,7 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
   }
   __syncthreads();
 
+  PROBE(1)
   // ---- software-pipelined left-looking Cholesky over tile columns
   AccSet acc[2];
   acc[0].zero();
@@ -351,6 +376,7 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
     return;
   }
 
+  PROBE(2)
   // ---- W = L21 L11^-1 (warps 0..T1-1, one own tile row each, right to left) and
   //      S^-1 = L22^-T L22^-1 (the other warps; lane = row, one column at a time)
   double sinv[4];
@@ -446,6 +472,7 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
   }
   __syncthreads();
 
+  PROBE(3)
   // ---- X_c = S^-1 [-W, I] in natural column order, ld = n rounded up to even.
   // X_other = -S^-1 W straight from the DMMA accumulators; X_own = S^-1.
   const int n = S.n;
@@ -482,6 +509,9 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
   }
   if (ld != n)
     for (int o = tid; o < S.n1; o += kTcThreads) Xc[o * ld + n] = 0.0;
+  __syncthreads();
+  PROBE(4)
+  TRACE(2)
 }
 
 // Global-memory local solve for subdomains whose factor does not fit in shared
@@ -662,6 +692,18 @@ __global__ __launch_bounds__(kRaThreads) void k_rasm_apply(
     for (int sh = 16; sh > 0; sh >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, sh);
     if (lane == 0) z[o0 + o - st.own_lo] = acc;
   }
+}
+
+int probe_read(long long *out) {
+#ifdef RBF_PROBE
+  RBF_CUDA_TRY(cudaMemcpyFromSymbol(out, g_probe, sizeof(long long) * 64 * 8));
+  RBF_CUDA_TRY(cudaMemcpyFromSymbol(out + 64 * 8, g_trace, sizeof(long long) * 65536 * 3));
+  return RBF_OK;
+#else
+  (void)out;
+  set_error("built without RBF_PROBE");
+  return RBF_EUNSUPPORTED;
+#endif
 }
 
 int rasm_setup(rbf_ctx *c, cudaStream_t s) {

@@ -55,7 +55,7 @@ EXPORTS = ["rbf_get_nccl_id", "rbf_setup", "rbf_local_count", "rbf_ext_count", "
            "rbf_local_index", "rbf_cell_list", "rbf_to_local", "rbf_from_local", "rbf_matvec",
            "rbf_rasm_apply", "rbf_matvec_ext", "rbf_rasm_apply_ext", "rbf_solve",
            "rbf_interpolate_host", "rbf_count_pairs", "rbf_dot", "rbf_plan_strips",
-           "rbf_last_error", "rbf_destroy", "rbf_info", "rbf_launch_count"]
+           "rbf_last_error", "rbf_destroy", "rbf_info", "rbf_launch_count", "rbf_setup_times"]
 
 _lib = None
 
@@ -91,6 +91,7 @@ def lib() -> C.CDLL:
             "rbf_last_error": (C.c_char_p, []),
             "rbf_info": (C.c_int, [p, p]),
             "rbf_launch_count": (i64, []),
+            "rbf_setup_times": (C.c_int, [p, p]),
             "rbf_destroy": (None, [p]),
         }
         for name, (res, args) in sigs.items():
@@ -272,6 +273,11 @@ class Context:
         _check(lib().rbf_info(self._h, o.ctypes.data_as(C.c_void_p)))
         keys = ["x_doubles", "nsub", "max_ov", "max_own", "n_lu", "ncx", "ncy", "bytes_device"]
         return {k: int(v) for k, v in zip(keys, o)}
+
+    def setup_times(self) -> dict:
+        o = np.zeros(4, dtype=np.float64)
+        _check(lib().rbf_setup_times(self._h, o.ctypes.data_as(C.c_void_p)))
+        return dict(zip(["cell_list", "nlist", "rasm", "total"], map(float, o)))
 
     def count_pairs(self) -> int:
         v = C.c_int64()

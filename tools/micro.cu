@@ -29,6 +29,19 @@ __global__ void k_dmma(double *out, int iters) {
   if (s == 1.2345) out[0] = s;
 }
 
+// latency: one warp, dependent DMMA chain; and dependent DFMA chain
+__global__ void k_lat(double *out, long long *cyc, int iters) {
+  double c0 = 1.0, c1 = 0.5, a = 1.0 + threadIdx.x * 1e-9, b = 0.999999;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) dmma(c0, c1, a, b);
+  long long t1 = clock64();
+  double x = c0;
+  for (int i = 0; i < iters; ++i) x = fma(x, b, a);
+  long long t2 = clock64();
+  if (threadIdx.x == 0) { cyc[0] = t1 - t0; cyc[1] = t2 - t1; }
+  if (c0 + c1 + x == 1.2345) out[0] = 1;
+}
+
 __constant__ double c_tab[64];
 
 // exp(x) = 2^(k/64) (1 + p(r)),  k = round(64 x / ln2), r = x - k ln2/64
@@ -103,6 +116,10 @@ int main() {
   printf("{\"dmma_tflops\": %.3f", best);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) printf(", \"dmma_err\": \"%s\"", cudaGetErrorString(err));
+  long long *dc; cudaMalloc(&dc, 16);
+  k_lat<<<1, 32>>>(d, dc, 1000);
+  long long hc[2]; cudaMemcpy(hc, dc, 16, cudaMemcpyDeviceToHost);
+  printf(", \"dmma_latency_cyc\": %.1f, \"dfma_latency_cyc\": %.1f", hc[0] / 1000.0, hc[1] / 1000.0);
   // exp table
   double h[64];
   for (int j = 0; j < 64; ++j) h[j] = exp2((double)j / 64.0);
