@@ -207,6 +207,16 @@ int rbf_setup_times(const rbf_ctx *ctx, double out[4]);
 /* Number of kernel launches this library has issued so far (process-wide). */
 int64_t rbf_launch_count(void);
 
+/* Halo plan (host only, no GPU) used by rbf_setup for strip `rank`: row_start[r] =
+ * global sorted position of the first point of cell row r (ncy+1 entries),
+ * row_bounds from rbf_plan_strips, kh = ceil(rc/c) matvec halo rows, rings = RASM
+ * overlap rings.  out = {ext_lo, own_lo, own_hi, ext_hi,
+ *   below: send_off, send_cnt, recv_off, recv_cnt,   above: same four}
+ * for the matvec halo (send offsets relative to the owned vector, receive offsets
+ * relative to the extended vector [ext_lo, ext_hi)). */
+int rbf_plan_halo(const int64_t *row_start, int64_t ncy, const int64_t *row_bounds, int32_t nranks,
+                  int32_t rank, int32_t kh, int32_t rings, int64_t out[12]);
+
 const char *rbf_last_error(void);
 void rbf_destroy(rbf_ctx *ctx);
 

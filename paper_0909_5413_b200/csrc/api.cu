@@ -91,6 +91,40 @@ static int plan_strips(const long long *counts, long long ncy, int P, long long 
   return RBF_OK;
 }
 
+// Strip `rank` of the cell-row partition `bounds` and its halos.  row_start[r] is
+// the global sorted position of the first point of cell row r (ncy+1 entries).
+// depth = rows of the extended range; kh / rings = matvec / RASM halo rows.
+// Halo [0] is exchanged with rank-1 (below), [1] with rank+1 (above); send offsets
+// are relative to the owned vector, receive offsets to the extended vector.
+static void plan_strip(const long long *row_start, int ncy, const long long *bounds, int nranks,
+                       int rank, int depth, int kh, int rings, Strip &S, Halo *hmv, Halo *hpc) {
+  S.row_lo = (int)bounds[rank];
+  S.row_hi = (int)bounds[rank + 1];
+  S.ext_row_lo = S.row_lo - depth < 0 ? 0 : S.row_lo - depth;
+  S.ext_row_hi = S.row_hi + depth > ncy ? ncy : S.row_hi + depth;
+  S.own_lo = row_start[S.row_lo];
+  S.own_hi = row_start[S.row_hi];
+  S.ext_lo = row_start[S.ext_row_lo];
+  S.ext_hi = row_start[S.ext_row_hi];
+  auto halo = [&](int dd, Halo *h) {
+    const bool below = rank > 0, above = rank < nranks - 1;
+    const int lo = S.row_lo - dd < 0 ? 0 : S.row_lo - dd;
+    const int hi = S.row_lo + dd > S.row_hi ? S.row_hi : S.row_lo + dd;
+    h[0].recv_off = row_start[lo] - S.ext_lo;
+    h[0].recv_cnt = below ? row_start[S.row_lo] - row_start[lo] : 0;
+    h[0].send_off = 0;
+    h[0].send_cnt = below ? row_start[hi] - row_start[S.row_lo] : 0;
+    const int hi2 = S.row_hi + dd > ncy ? ncy : S.row_hi + dd;
+    const int lo2 = S.row_hi - dd < S.row_lo ? S.row_lo : S.row_hi - dd;
+    h[1].recv_off = row_start[S.row_hi] - S.ext_lo;
+    h[1].recv_cnt = above ? row_start[hi2] - row_start[S.row_hi] : 0;
+    h[1].send_off = row_start[lo2] - S.own_lo;
+    h[1].send_cnt = above ? row_start[S.row_hi] - row_start[lo2] : 0;
+  };
+  halo(kh, hmv);
+  halo(rings, hpc);
+}
+
 static int validate(const rbf_params *p, long long n) {
   if (!p) { set_error("params is NULL"); return RBF_EINVAL; }
   if (n < 1 || n > 0x7fffffffLL) { set_error("n = %lld outside [1, 2^31)", n); return RBF_EINVAL; }
@@ -159,6 +193,25 @@ int rbf_plan_strips(const int64_t *row_counts, int64_t ncy, int32_t nranks, int6
                     int64_t *row_bounds) {
   if (!row_counts || !row_bounds || ncy < 1) { set_error("bad arguments"); return RBF_EINVAL; }
   return plan_strips((const long long *)row_counts, ncy, nranks, min_rows, (long long *)row_bounds);
+}
+
+int rbf_plan_halo(const int64_t *row_start, int64_t ncy, const int64_t *row_bounds, int32_t nranks,
+                  int32_t rank, int32_t kh, int32_t rings, int64_t out[12]) {
+  if (!row_start || !row_bounds || !out || ncy < 1 || nranks < 1 || rank < 0 || rank >= nranks ||
+      kh < 0 || rings < 0) {
+    set_error("rbf_plan_halo: bad arguments");
+    return RBF_EINVAL;
+  }
+  Strip S;
+  Halo hmv[2], hpc[2];
+  const int depth = kh > rings ? kh : rings;
+  plan_strip((const long long *)row_start, (int)ncy, (const long long *)row_bounds, nranks, rank,
+             depth, kh, rings, S, hmv, hpc);
+  const long long v[12] = {S.ext_lo, S.own_lo, S.own_hi, S.ext_hi,
+                           hmv[0].send_off, hmv[0].send_cnt, hmv[0].recv_off, hmv[0].recv_cnt,
+                           hmv[1].send_off, hmv[1].send_cnt, hmv[1].recv_off, hmv[1].recv_cnt};
+  for (int i = 0; i < 12; ++i) out[i] = v[i];
+  return RBF_OK;
 }
 
 void rbf_destroy(rbf_ctx *c) {
@@ -240,34 +293,8 @@ int rbf_setup(rbf_ctx **out, const double *xy, int64_t n, const rbf_params *p, c
   for (int r = 0; r < g.ncy; ++r) counts[r] = c->row_start[r + 1] - c->row_start[r];
   st = plan_strips(counts.data(), g.ncy, c->nranks, c->nranks > 1 ? depth : 1, bounds.data());
   if (st != RBF_OK) { rbf_destroy(c); return st; }
-  Strip &S = c->s;
-  S.row_lo = (int)bounds[c->rank];
-  S.row_hi = (int)bounds[c->rank + 1];
-  S.ext_row_lo = S.row_lo - depth < 0 ? 0 : S.row_lo - depth;
-  S.ext_row_hi = S.row_hi + depth > g.ncy ? g.ncy : S.row_hi + depth;
-  S.own_lo = c->row_start[S.row_lo];
-  S.own_hi = c->row_start[S.row_hi];
-  S.ext_lo = c->row_start[S.ext_row_lo];
-  S.ext_hi = c->row_start[S.ext_row_hi];
-  auto halo = [&](int dd, Halo *h) {
-    // below (rank-1)
-    int lo = S.row_lo - dd < 0 ? 0 : S.row_lo - dd;
-    h[0].recv_off = c->row_start[lo] - S.ext_lo;
-    h[0].recv_cnt = c->row_start[S.row_lo] - c->row_start[lo];
-    int hi = S.row_lo + dd > S.row_hi ? S.row_hi : S.row_lo + dd;
-    h[0].send_off = 0;
-    h[0].send_cnt = (c->rank > 0) ? c->row_start[hi] - c->row_start[S.row_lo] : 0;
-    if (c->rank == 0) h[0].recv_cnt = 0;
-    // above (rank+1)
-    int hi2 = S.row_hi + dd > g.ncy ? g.ncy : S.row_hi + dd;
-    h[1].recv_off = c->row_start[S.row_hi] - S.ext_lo;
-    h[1].recv_cnt = (c->rank < c->nranks - 1) ? c->row_start[hi2] - c->row_start[S.row_hi] : 0;
-    int lo2 = S.row_hi - dd < S.row_lo ? S.row_lo : S.row_hi - dd;
-    h[1].send_off = c->row_start[lo2] - S.own_lo;
-    h[1].send_cnt = (c->rank < c->nranks - 1) ? c->row_start[S.row_hi] - c->row_start[lo2] : 0;
-  };
-  halo(g.kh, c->halo_mv);
-  halo(g.rings, c->halo_pc);
+  plan_strip(c->row_start.data(), g.ncy, bounds.data(), c->nranks, c->rank, depth, g.kh, g.rings,
+             c->s, c->halo_mv, c->halo_pc);
   st = gather_positions(c, xy, s);
   if (st == RBF_OK) st = build_nlist(c, s);
   cudaEventRecord(ev[2], s);

@@ -55,7 +55,8 @@ EXPORTS = ["rbf_get_nccl_id", "rbf_setup", "rbf_local_count", "rbf_ext_count", "
            "rbf_local_index", "rbf_cell_list", "rbf_to_local", "rbf_from_local", "rbf_matvec",
            "rbf_rasm_apply", "rbf_matvec_ext", "rbf_rasm_apply_ext", "rbf_solve",
            "rbf_interpolate_host", "rbf_count_pairs", "rbf_dot", "rbf_plan_strips",
-           "rbf_last_error", "rbf_destroy", "rbf_info", "rbf_launch_count", "rbf_setup_times"]
+           "rbf_last_error", "rbf_destroy", "rbf_info", "rbf_launch_count", "rbf_setup_times",
+           "rbf_plan_halo"]
 
 _lib = None
 
@@ -92,6 +93,7 @@ def lib() -> C.CDLL:
             "rbf_info": (C.c_int, [p, p]),
             "rbf_launch_count": (i64, []),
             "rbf_setup_times": (C.c_int, [p, p]),
+            "rbf_plan_halo": (C.c_int, [p, i64, p, i32, i32, i32, i32, p]),
             "rbf_destroy": (None, [p]),
         }
         for name, (res, args) in sigs.items():
@@ -141,6 +143,20 @@ def plan_strips(row_counts, nranks: int, min_rows: int) -> np.ndarray:
     _check(lib().rbf_plan_strips(rc.ctypes.data_as(C.c_void_p), rc.shape[0], int(nranks),
                                  int(min_rows), out.ctypes.data_as(C.c_void_p)))
     return out
+
+
+def plan_halo(row_start, row_bounds, rank: int, kh: int, rings: int) -> dict:
+    """Host-only halo plan of strip `rank` (the one rbf_setup uses)."""
+    rs = np.ascontiguousarray(row_start, dtype=np.int64)
+    rb = np.ascontiguousarray(row_bounds, dtype=np.int64)
+    out = np.zeros(12, dtype=np.int64)
+    _check(lib().rbf_plan_halo(rs.ctypes.data_as(C.c_void_p), rs.shape[0] - 1,
+                               rb.ctypes.data_as(C.c_void_p), rb.shape[0] - 1, int(rank), int(kh),
+                               int(rings), out.ctypes.data_as(C.c_void_p)))
+    keys = ["ext_lo", "own_lo", "own_hi", "ext_hi",
+            "below_send_off", "below_send_cnt", "below_recv_off", "below_recv_cnt",
+            "above_send_off", "above_send_cnt", "above_recv_off", "above_recv_cnt"]
+    return {k: int(v) for k, v in zip(keys, out)}
 
 
 @dataclass
