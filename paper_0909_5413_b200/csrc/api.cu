@@ -220,10 +220,8 @@ void rbf_destroy(rbf_ctx *c) {
   dfree(c->cell_start, s);
   dfree(c->perm, s);
   dfree(c->xy_ext, s);
-  dfree(c->xyf_ext, s);
   dfree(c->x_off, s);
-  dfree(c->chunk_first, s);
-  dfree(c->chunk_cell, s);
+  dfree(c->rec, s);
   dfree(c->chunk_len, s);
   dfree(c->chunk_off, s);
   dfree(c->nlist, s);
@@ -274,6 +272,8 @@ int rbf_setup(rbf_ctx **out, const double *xy, int64_t n, const rbf_params *p, c
   g.cell = p->cell;
   g.rc2 = p->rc * p->rc;
   g.neg_inv_2s2 = -1.0 / (2.0 * p->sigma * p->sigma);
+  g.esc = -1.0 / (2.0 * M_LN2 * p->sigma * p->sigma);
+  g.esc64 = 64.0 * g.esc;
   g.norm = 1.0 / (2.0 * M_PI * p->sigma * p->sigma);
   g.ncx = (int)std::ceil((p->x1 - p->x0) / p->cell);
   g.ncy = (int)std::ceil((p->y1 - p->y0) / p->cell);

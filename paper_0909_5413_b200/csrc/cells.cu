@@ -42,18 +42,13 @@ __global__ void k_cell_start(const int *__restrict__ skeys, int n, int ncells,
     for (int k = k1 + 1; k <= ncells; ++k) cell_start[k] = n;
 }
 
-// Sorted positions (fp64) and, for the matvec's conservative fp32 prefilter, the
-// position relative to the point's own cell origin in fp32.
-__global__ void k_gather_xy(const double *__restrict__ xy, const int *__restrict__ perm, Geom g,
-                            long long lo, long long cnt, double2 *__restrict__ out,
-                            float2 *__restrict__ outf) {
+// Sorted positions (fp64, double2).
+__global__ void k_gather_xy(const double *__restrict__ xy, const int *__restrict__ perm,
+                            long long lo, long long cnt, double2 *__restrict__ out) {
   long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= cnt) return;
   long long i = perm[lo + t];
-  const double x = xy[2 * i], y = xy[2 * i + 1];
-  out[t] = make_double2(x, y);
-  const int cx = cell_coord(x, g.x0, g.cell, g.ncx), cy = cell_coord(y, g.y0, g.cell, g.ncy);
-  outf[t] = make_float2((float)(x - (g.x0 + cx * g.cell)), (float)(y - (g.y0 + cy * g.cell)));
+  out[t] = make_double2(xy[2 * i], xy[2 * i + 1]);
 }
 
 __global__ void k_max_cell(const int *__restrict__ cell_start, int ncells, int *__restrict__ out) {
@@ -149,10 +144,8 @@ int build_cell_list(rbf_ctx *c, const double *xy, cudaStream_t s) {
 int gather_positions(rbf_ctx *c, const double *xy, cudaStream_t s) {
   long long cnt = c->s.ext_hi - c->s.ext_lo;
   RBF_TRY(dalloc(c, (void **)&c->xy_ext, sizeof(double2) * (size_t)(cnt > 0 ? cnt : 1), s));
-  RBF_TRY(dalloc(c, (void **)&c->xyf_ext, sizeof(float2) * (size_t)(cnt > 0 ? cnt : 1), s));
   if (cnt > 0) {
-    k_gather_xy<<<blocks_for(cnt, 256), 256, 0, s>>>(xy, c->perm, c->g, c->s.ext_lo, cnt, c->xy_ext,
-                                                     c->xyf_ext);
+    k_gather_xy<<<blocks_for(cnt, 256), 256, 0, s>>>(xy, c->perm, c->s.ext_lo, cnt, c->xy_ext);
     count_launch(1);
     RBF_CUDA_TRY(cudaGetLastError());
   }

@@ -47,6 +47,8 @@ struct Geom {
   double x0, y0, x1, y1, cell;
   double rc2;          // rc*rc, computed once on the host (reading Q1)
   double neg_inv_2s2;  // -1 / (2 sigma^2)
+  double esc;          // -log2(e) / (2 sigma^2): matvec exp argument in powers of 2
+  double esc64;        // 64 * esc (table variant)
   double norm;         // 1 / (2 pi sigma^2), hoisted out of the pair sum (reading Q2)
   int ncx, ncy;
   int kh;              // matvec search rings = ceil(rc/c), bumped on near-integral rc/c
@@ -131,20 +133,21 @@ struct rbf_ctx {
   int *cell_start = nullptr;   // ncx*ncy+1
   int *perm = nullptr;         // N: caller index of global sorted entry
   double2 *xy_ext = nullptr;   // positions of the ext range, sorted
-  float2 *xyf_ext = nullptr;   // fp32 positions relative to each point's cell origin (matvec prefilter)
   // RASM
   long long *x_off = nullptr;  // per owned cell (ncx * owned rows + 1), in doubles
   double *X = nullptr;         // rows of A_c^-1 for own(c), row-major, ld = n_ov rounded up to even
   long long x_count = 0;
   int max_ov = 0, max_own = 0, nsub = 0, n_lu = 0;
   int max_cell = 0;            // largest cell population (all cells of the ext range)
-  // matvec neighbour list (ELL of 32-bit entries in groups of 4, chunks of 32 targets)
+  // matvec: packed source records {x, y, w, 0} (ext range) and the neighbour list
+  // (ELL of 32-bit entries in groups of 4, chunks of 32 consecutive owned targets)
+  double4 *rec = nullptr;
+  int mv_exp = 1;              // exp variant (1: polynomial, 0: replicated 64-entry table)
+  int mv_g = 2;                // targets per lane (union lists with per-target mask bits)
   int nchunks = 0;
-  int *chunk_first = nullptr;  // per owned cell (+1): first chunk
-  int *chunk_cell = nullptr;   // per chunk: owned cell index
-  int *chunk_len = nullptr;    // per chunk: list length (max over its lanes)
+  int *chunk_len = nullptr;    // per chunk: list length (max over its lanes, multiple of 4)
   long long *chunk_off = nullptr;  // per chunk (+1): first entry
-  int *nlist = nullptr;           // source index (ext-relative sorted order), -1 = padding
+  unsigned *nlist = nullptr;      // source index (ext-relative sorted order) | target mask bits
   long long nlist_entries = 0;
   // workspaces
   double *w_ext = nullptr;     // n_ext (multi-rank only)

@@ -152,15 +152,20 @@ __device__ void givens_step(double *S, const Scal &L, const double *hall, int k)
   S[L.out() + 1] = hn;
 }
 
-// Host-mapped mailbox: the iteration's residual estimate and a sequence number the
-// host polls without any CUDA call (no stream synchronisation per iteration).
+// Host-mapped mailbox ring: each Arnoldi step posts its residual estimate and its
+// sequence number to slot seq % kMbSlots; the host polls that slot without any CUDA
+// call (no stream synchronisation per iteration).  A ring, not a single slot: with
+// the one-step lookahead, step k+1 may post before the host has read step k.
 struct Mailbox {
   double gabs, hn;
   long long seq;
 };
+constexpr int kMbSlots = 4;
+constexpr int kHpinScal = 16;  // hpin[kHpinScal...] : scalar read-backs (after the ring)
+static_assert(sizeof(Mailbox) * kMbSlots <= sizeof(double) * kHpinScal, "mailbox ring overlaps");
 
-__device__ __forceinline__ void post_mailbox(Mailbox *mb, const double *S, const Scal &L, long long seq) {
-  volatile Mailbox *v = mb;
+__device__ __forceinline__ void post_mailbox(Mailbox *ring, const double *S, const Scal &L, long long seq) {
+  volatile Mailbox *v = ring + (seq % kMbSlots);
   v->gabs = S[L.out() + 0];
   v->hn = S[L.out() + 1];
   __threadfence_system();
@@ -343,7 +348,7 @@ static int ensure_workspace(rbf_ctx *c, int m, cudaStream_t s) {
     RBF_CUDA_TRY(cudaMemsetAsync(c->red_count, 0, sizeof(unsigned), s));
   }
   if (!c->hpin) {
-    RBF_CUDA_TRY(cudaHostAlloc((void **)&c->hpin, sizeof(double) * (16 + c->nranks), cudaHostAllocMapped));
+    RBF_CUDA_TRY(cudaHostAlloc((void **)&c->hpin, sizeof(double) * (kHpinScal + 8 + c->nranks), cudaHostAllocMapped));
     RBF_CUDA_TRY(cudaHostGetDevicePointer((void **)&c->hpin_dev, c->hpin, 0));
   }
   if (c->nranks == 1 && !c->ar_part) {
@@ -392,7 +397,7 @@ static const double *hall_slot(rbf_ctx *c, const Scal &L, int slot) {
 }
 
 static int read_scalars(rbf_ctx *c, const double *src, int count, cudaStream_t s) {
-  RBF_CUDA_TRY(cudaMemcpyAsync(c->hpin + 8, src, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaMemcpyAsync(c->hpin + kHpinScal, src, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
   RBF_CUDA_TRY(cudaStreamSynchronize(s));
   return RBF_OK;
 }
@@ -404,7 +409,7 @@ static int global_dot(rbf_ctx *c, const Scal &L, const double *a, const double *
   RBF_TRY(reduce_slot(c, L, 0, s));
   RBF_TRY(read_scalars(c, hall_slot(c, L, 0), c->nranks, s));
   double t = 0.0;
-  for (int r = 0; r < c->nranks; ++r) t += c->hpin[8 + r];
+  for (int r = 0; r < c->nranks; ++r) t += c->hpin[kHpinScal + r];
   *out = t;
   return RBF_OK;
 }
@@ -454,15 +459,15 @@ struct PhaseTimer {  // rotating event sets; a set is read only when it is surel
 // Spin on the mailbox until iteration `seq` has posted (no CUDA API call in the
 // fast path; the stream is queried now and then to surface errors).
 static int wait_mailbox(rbf_ctx *c, long long seq, cudaStream_t s, double *gabs, double *hn) {
-  volatile Mailbox *mb = reinterpret_cast<volatile Mailbox *>(c->hpin);
-  for (long long spin = 0; mb->seq < seq; ++spin) {
+  volatile Mailbox *mb = reinterpret_cast<volatile Mailbox *>(c->hpin) + (seq % kMbSlots);
+  for (long long spin = 0; mb->seq != seq; ++spin) {
     if ((spin & 0xfff) == 0xfff) {
       cudaError_t e = cudaStreamQuery(s);
       if (e != cudaSuccess && e != cudaErrorNotReady) {
         set_error("GMRES iteration failed: %s", cudaGetErrorString(e));
         return RBF_ECUDA;
       }
-      if (e == cudaSuccess && mb->seq < seq) {  // stream drained but no post: cannot happen
+      if (e == cudaSuccess && mb->seq != seq) {  // stream drained but no post: cannot happen
         set_error("GMRES mailbox: iteration %lld never posted", seq);
         return RBF_ECUDA;
       }
@@ -505,7 +510,7 @@ int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double 
   } else {
     const double tol = std::fmax(gp->rtol * beta0, gp->atol);
     long long seq_enq = 0, seq_base = 0;  // Arnoldi steps enqueued; steps before this cycle
-    reinterpret_cast<volatile Mailbox *>(c->hpin)->seq = 0;
+    for (int i = 0; i < kMbSlots; ++i) reinterpret_cast<volatile Mailbox *>(c->hpin)[i].seq = -1;
     for (;;) {
       // V0 holds the unscaled preconditioned residual; its ||.||^2 is in slot 0
       k_cycle_init<<<1, 1, 0, s>>>(c->dscal, L, hall_slot(c, L, 0)); count_launch(1);

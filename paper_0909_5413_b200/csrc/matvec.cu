@@ -8,198 +8,285 @@
 // The truncated operator is applied matrix-free in its VALUES (every entry is
 // recomputed, "without actually storing the matrix"), but its sparsity
 // pattern -- which of the stencil's sources lie within rc of each target -- is
-// found once in rbf_setup (exact fp64 test) and kept as an ELLPACK-style list of
-// 32-bit source indices, 4 bytes per in-cutoff pair (O(N) storage).  A matvec then
-// spends its FP64 pipe only on in-cutoff pairs: one warp per chunk of <= 32 targets
-// of a cell, lanes walk their own lists in lock step (coalesced list loads, gathers
-// of the sources from L1/L2), table-driven exp on the FP64 pipe.
+// found once in rbf_setup (the exact fp64 test of reading Q1) and kept as an
+// ELLPACK-style list of 32-bit source indices, 4 bytes per in-cutoff pair (O(N)
+// storage).  A matvec then spends its FP64 pipe only on in-cutoff pairs.
 //
-// The per-target summation order is the stencil order (rows, then sorted order),
-// independent of the strip decomposition: results are deterministic and bitwise
-// identical for any number of strips (reading Q20).
+// Layout (B200): one warp per chunk of 32 CONSECUTIVE targets (sorted order; chunks
+// ignore cell boundaries, so all 32 lanes carry work), lanes walk their own lists in
+// lock step, 4 entries per coalesced 16-byte load.  The sources are gathered from a
+// packed record array {x, y, w, 0} -- ONE 256-bit load (LDG.E.ENL2.256) per pair --
+// whose w slot is refreshed by k_pack_w before each matvec.  The L1 data pipe, not
+// the FP64 pipe, is what a gather-based matvec saturates first (ncu, profiles/), so
+// every byte through L1 counts: 32 B per pair for the record, 4 B for the index.
+//
+// exp() runs on the FP64 pipe with no table (EXPV 1): k = round(-r2 log2e/(2s^2)),
+// f = -r2 log2e/(2 s^2) - k in [-1/2, 1/2] (one fma from the exact product), 2^f by
+// a degree-11 polynomial (<= ~1 ulp, reading Q15), 2^k by an integer add to the
+// exponent field.  EXPV 0 is the table variant (64 entries, replicated per lane in
+// shared memory so each LDS.64 is conflict-free).
+//
+// Padding entries point at the target itself (a finite term) and are masked by a
+// predicated accumulate, so the per-target sum is exactly the sum over its list in
+// stencil order (rows, then sorted order): deterministic and bitwise identical for
+// any strip decomposition (reading Q20).
 #include <cub/cub.cuh>
+
+#include <cstdlib>
 
 #include "common.cuh"
 
 namespace rbf {
 
-constexpr int kMvWarps = 4;  // target chunks per CTA
+constexpr int kMvWarps = 8;  // target chunks per CTA
 constexpr int kMvThreads = 32 * kMvWarps;
-constexpr int kPad = -1;
 
-// exp_neg()'s constants in the constant bank, so the DFMAs read them as c[][]
-// operands instead of re-materialising 64-bit immediates in every iteration.
-__constant__ double kExpC[8] = {6755399441055744.0,   92.33248261689366,
-                                -0.010830417275428772, -7.420820373486988e-09,
-                                1.0 / 120.0,           1.0 / 24.0,
-                                1.0 / 6.0,             0.5};
+// 2^f = 1 + f P(f) on [-1/2, 1/2], P of degree 10 (Chebyshev-node fit, max error
+// ~1 ulp; tools/ derivation in DESIGN.md §6), highest coefficient first.
+__constant__ double kExp2P[11] = {4.4549605981865186e-10, 7.072585949269223e-09,
+                                  1.0178062445845774e-07, 1.321544258792169e-06,
+                                  1.525273382983612e-05,  0.0001540353044173605,
+                                  0.0013333558146416936,  0.009618129107606888,
+                                  0.0555041086648216,     0.24022650695910097,
+                                  0.6931471805599453};
+// e^{f ln2/64} - 1 = f (a1 + a2 f + ... + a5 f^4), a_i = (ln2/64)^i / i!
+__constant__ double kExp64A[5] = {1.2417843701716925e-12, 5.732851688640402e-10,
+                                  2.1173137155464776e-07, 5.86490495505617e-05,
+                                  0.010830424696249145};
 
-__device__ __forceinline__ double exp_neg_smem(double x, const double *tab) {
-  // exp_neg() without the underflow guard (rbf_setup requires rc <= 37 sigma, so
-  // every in-range argument is > -685) and with the table in shared memory.
-  const double t = fma(x, kExpC[1], kExpC[0]);
-  const double kd = t - kExpC[0];
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer shifter
+
+// exp(-r2/(2 sigma^2)) for 0 <= r2 < rc^2 (rc <= 37 sigma, so the result is a normal
+// number > 2^-990 and no underflow guard is needed).  esc = -log2(e)/(2 sigma^2).
+__device__ __forceinline__ double gauss_exp2(double r2, double esc) {
+  const double t = fma(r2, esc, kMagic);
+  const double kd = t - kMagic;
   const int k = __double2loint(t);
-  double r = fma(kd, kExpC[2], x);
-  r = fma(kd, kExpC[3], r);
-  double p = fma(r, kExpC[4], kExpC[5]);
-  p = fma(r, p, kExpC[6]);
-  p = fma(r, p, kExpC[7]);
-  p = fma(r, p, 1.0);
-  p = r * p;
-  const double T = tab[k & 63];
+  const double f = fma(r2, esc, -kd);  // exact product, one rounding: |f| <= 1/2
+  double p = kExp2P[0];
+#pragma unroll
+  for (int i = 1; i < 11; ++i) p = fma(p, f, kExp2P[i]);
+  const double q = fma(f, p, 1.0);
+  return __hiloint2double(__double2hiint(q) + k * (1 << 20), __double2loint(q));
+}
+
+// Table variant: esc64 = -64 log2(e)/(2 sigma^2); tab = this lane's column of the
+// replicated 2^(j/64) table (stride 32 doubles).
+__device__ __forceinline__ double gauss_exp64(double r2, double esc64, const double *tab) {
+  const double t = fma(r2, esc64, kMagic);
+  const double kd = t - kMagic;
+  const int k = __double2loint(t);
+  const double f = fma(r2, esc64, -kd);
+  double p = fma(f, kExp64A[0], kExp64A[1]);
+  p = fma(f, p, kExp64A[2]);
+  p = fma(f, p, kExp64A[3]);
+  p = fma(f, p, kExp64A[4]);
+  p = f * p;
+  const double T = tab[(k & 63) * 32];
   const double e = fma(T, p, T);
-  return __hiloint2double(__double2hiint(e) + ((k >> 6) << 20), __double2loint(e));
+  return __hiloint2double(__double2hiint(e) + (k >> 6) * (1 << 20), __double2loint(e));
+}
+
+__device__ __forceinline__ double4 ld_rec(const double4 *p) {
+  double4 v;
+  asm volatile("ld.global.nc.L1::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ int target_cell(const Geom &g, double2 p, int &cx, int &cy) {
+  double tx = floor(__ddiv_rn(__dsub_rn(p.x, g.x0), g.cell));
+  double ty = floor(__ddiv_rn(__dsub_rn(p.y, g.y0), g.cell));
+  cx = (int)fmin(fmax(tx, 0.0), (double)(g.ncx - 1));
+  cy = (int)fmin(fmax(ty, 0.0), (double)(g.ncy - 1));
+  return cy * g.ncx + cx;
 }
 
 // ---------------------------------------------------------------------------
-// Neighbour-list build (setup).  Chunks: ceil(n_t / 32) per owned cell.
+// Neighbour-list build (setup).  Each lane owns G consecutive targets (sorted
+// order) and walks the UNION of their in-cutoff lists: one record load then serves
+// G pairs, dividing the L1 bytes per pair by ~G (at ~88% slot efficiency for G = 2
+// on lattices; the masked-off slots are computed and discarded).  Entry =
+// source index (ext-relative) | bit (31 - j) set iff the source is within rc of
+// target j.  The union is enumerated in stencil order over the bounding box of the
+// G stencils, so each target sees exactly its own list in its own stencil order:
+// sums are bitwise independent of G and of the strip decomposition (reading Q20).
+// One thread per lane; a warp = a chunk of 32 G targets.
+// MODE 0: union length per chunk (max over lanes, rounded up to 4).
+// MODE 1: write the entries (ELL, groups of 4 per lane) and the padding (mask 0).
 // ---------------------------------------------------------------------------
-__global__ void k_chunk_count(Geom g, Strip st, const int *__restrict__ cell_start, int ncl,
-                              int *__restrict__ nchunk) {
-  int cl = blockIdx.x * blockDim.x + threadIdx.x;
-  if (cl > ncl) return;
-  if (cl == ncl) {
-    nchunk[cl] = 0;
-    return;
-  }
-  const int key = (st.row_lo + cl / g.ncx) * g.ncx + cl % g.ncx;
-  nchunk[cl] = (cell_start[key + 1] - cell_start[key] + 31) / 32;
-}
+template <int G>
+struct MvIdx {
+  static constexpr unsigned kIdxMask = (1u << (32 - G)) - 1u;
+  static __device__ __forceinline__ unsigned bit(int j) { return 1u << (31 - j); }
+};
 
-__global__ void k_chunk_fill(const int *__restrict__ chunk_first, int ncl,
-                             int *__restrict__ chunk_cell) {
-  int cl = blockIdx.x * blockDim.x + threadIdx.x;
-  if (cl >= ncl) return;
-  for (int c = chunk_first[cl]; c < chunk_first[cl + 1]; ++c) chunk_cell[c] = cl;
-}
-
-// MODE 0: per-chunk list length (max over lanes); MODE 1: write the entries.
-template <int MODE>
-__global__ __launch_bounds__(kMvThreads) void k_nlist(
-    Geom g, Strip st, const double2 *__restrict__ xy, const int *__restrict__ cell_start,
-    const int *__restrict__ chunk_cell, const int *__restrict__ chunk_first, int nchunks,
-    int *__restrict__ chunk_len, const long long *__restrict__ chunk_off,
-    int *__restrict__ list) {
+template <int MODE, int G>
+__global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const double2 *__restrict__ xy,
+                                                      const int *__restrict__ cell_start, long long nloc,
+                                                      int *__restrict__ chunk_len,
+                                                      const long long *__restrict__ chunk_off,
+                                                      unsigned *__restrict__ list) {
+  const long long lt = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // lane-group
+  const long long t0 = lt * G;                                            // first local target
   const int lane = threadIdx.x & 31;
-  const int ch = blockIdx.x * kMvWarps + (threadIdx.x >> 5);
-  if (ch >= nchunks) return;
-  const int cl = chunk_cell[ch];
-  const int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
-  const int key = cy * g.ncx + cx;
-  const int t = cell_start[key] + 32 * (ch - chunk_first[cl]) + lane;
-  const bool active = t < cell_start[key + 1];
-  const int bx0 = max(cx - g.kh, 0), bx1 = min(cx + g.kh, g.ncx - 1);
-  const int by0 = max(cy - g.kh, 0), by1 = min(cy + g.kh, g.ncy - 1);
-  const double2 *xye = xy - st.ext_lo;
-  const double2 p = xye[active ? t : cell_start[key]];
+  const long long ch = lt >> 5;
+  const bool in_chunk = (ch << 5) * G < nloc;  // lanes past the end of a ragged last chunk
+  const long long own_off = st.own_lo - st.ext_lo;
   int cnt = 0;
   long long base = 0;
-  if (MODE == 1) base = chunk_off[ch];
+  if (MODE == 1 && in_chunk) base = chunk_off[ch];
+  double2 p[G];
+  bool act[G];
+  int bx0 = g.ncx, bx1 = -1, by0 = g.ncy, by1 = -1;
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    act[j] = t0 + j < nloc;
+    p[j] = xy[own_off + (act[j] ? t0 + j : 0)];
+    if (act[j]) {
+      int cx, cy;
+      target_cell(g, p[j], cx, cy);
+      bx0 = min(bx0, max(cx - g.kh, 0));
+      bx1 = max(bx1, min(cx + g.kh, g.ncx - 1));
+      by0 = min(by0, max(cy - g.kh, 0));
+      by1 = max(by1, min(cy + g.kh, g.ncy - 1));
+    }
+  }
   for (int by = by0; by <= by1; ++by) {
     const int s0 = cell_start[by * g.ncx + bx0], s1 = cell_start[by * g.ncx + bx1 + 1];
     for (int s = s0; s < s1; ++s) {
-      const double2 o = xye[s];
-      const double dx = p.x - o.x, dy = p.y - o.y;
-      if (active && fma(dx, dx, dy * dy) < g.rc2) {
-        if (MODE == 1) list[base + ((long long)(cnt >> 2) * 32 + lane) * 4 + (cnt & 3)] = s;
+      const double2 o = xy[s - st.ext_lo];
+      unsigned m = 0;
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const double dx = p[j].x - o.x, dy = p[j].y - o.y;
+        if (act[j] && fma(dx, dx, dy * dy) < g.rc2) m |= MvIdx<G>::bit(j);
+      }
+      if (m) {
+        if (MODE == 1)
+          list[base + ((long long)(cnt >> 2) * 32 + lane) * 4 + (cnt & 3)] = (unsigned)(s - st.ext_lo) | m;
         ++cnt;
       }
     }
   }
   const int kmax = (__reduce_max_sync(0xffffffffu, cnt) + 3) & ~3;  // groups of 4
   if (MODE == 0) {
-    if (lane == 0) chunk_len[ch] = kmax;
-  } else {
-    for (int k = cnt; k < kmax; ++k) list[base + ((long long)(k >> 2) * 32 + lane) * 4 + (k & 3)] = kPad;
+    if (lane == 0 && in_chunk) chunk_len[ch] = kmax;
+  } else if (in_chunk) {  // padding: the lane's first target, no mask bit (also idle lanes)
+    const unsigned self = (unsigned)(own_off + (act[0] ? t0 : 0));
+    for (int k = cnt; k < kmax; ++k) list[base + ((long long)(k >> 2) * 32 + lane) * 4 + (k & 3)] = self;
   }
 }
 
-__global__ void k_len_to_entries(const int *__restrict__ len, int n, long long *__restrict__ out) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void k_len_to_entries(const int *__restrict__ len, long long n, long long *__restrict__ out) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) out[i] = 32LL * len[i];
 }
 
+__global__ void k_init_rec(const double2 *__restrict__ xy, long long n, double4 *__restrict__ rec) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) rec[i] = make_double4(xy[i].x, xy[i].y, 0.0, 0.0);
+}
+
+// w slot of the records (ext range); one streaming pass, 8 B in / 8 B out per point.
+__global__ void k_pack_w(const double *__restrict__ w, long long n, double4 *__restrict__ rec) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) reinterpret_cast<double *>(rec + i)[2] = w[i];
+}
+
 // ---------------------------------------------------------------------------
-// The matvec: one warp per target chunk, lanes walk their lists in lock step.
+// The matvec: one warp per chunk of 32 G consecutive targets, G per lane.
 // ---------------------------------------------------------------------------
-__global__ __launch_bounds__(kMvThreads) void k_matvec_ell(
-    Geom g, Strip st, const double2 *__restrict__ xy, const double *__restrict__ w,
-    const int *__restrict__ cell_start, const int *__restrict__ chunk_cell,
-    const int *__restrict__ chunk_first, int nchunks, const int *__restrict__ chunk_len,
-    const long long *__restrict__ chunk_off, const int *__restrict__ list,
-    double *__restrict__ y) {
-  __shared__ double s_tab[64];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x < 64) s_tab[threadIdx.x] = kExp2Tab64[threadIdx.x];
-  __syncthreads();
-  const int ch = blockIdx.x * kMvWarps + warp;
-  if (ch >= nchunks) return;
-  const int cl = chunk_cell[ch];
-  const int key = (st.row_lo + cl / g.ncx) * g.ncx + cl % g.ncx;
-  const int t = cell_start[key] + 32 * (ch - chunk_first[cl]) + lane;
-  const bool active = t < cell_start[key + 1];
-  const double2 *xye = xy - st.ext_lo;
-  const double *we = w - st.ext_lo;
-  const int self = active ? t : cell_start[key];
-  const double2 p = xye[self];
+template <int G, int EXPV>
+__global__ __launch_bounds__(kMvThreads) void k_matvec(
+    Geom g, long long nloc, long long own_off, const double4 *__restrict__ rec,
+    const int *__restrict__ chunk_len, const long long *__restrict__ chunk_off,
+    const unsigned *__restrict__ list, double *__restrict__ y) {
+  __shared__ double s_tab[EXPV == 0 ? 64 * 32 : 1];
+  const int lane = threadIdx.x & 31;
+  if (EXPV == 0) {
+    for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) s_tab[i] = kExp2Tab64[i >> 5];
+    __syncthreads();
+  }
+  const long long lt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long t0 = lt * G;
+  const long long ch = lt >> 5;
+  if ((ch << 5) * G >= nloc) return;  // whole warp beyond the last chunk
+  double2 me[G];
+  double acc[G];
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    const double4 r = rec[own_off + (t0 + j < nloc ? t0 + j : 0)];
+    me[j] = make_double2(r.x, r.y);
+    acc[j] = 0.0;
+  }
   const int K = chunk_len[ch];  // multiple of 4
-  const int4 *lp = reinterpret_cast<const int4 *>(list + chunk_off[ch]) + lane;
-  const double nscale = g.neg_inv_2s2;
-  double acc = 0.0;
-  // 4 entries per 16-byte load, the next group prefetched; padding entries point at
-  // the target itself with weight 0, so the loop is branch-free with 4 pairs in flight.
-  int4 nxt = (K > 0) ? __ldcs(lp) : make_int4(kPad, kPad, kPad, kPad);
+  const uint4 *lp = reinterpret_cast<const uint4 *>(list + chunk_off[ch]) + lane;
+  const double esc = EXPV == 0 ? g.esc64 : g.esc;
+  const double *tab = s_tab + lane;
+  uint4 nxt = (K > 0) ? __ldcs(lp) : make_uint4(0, 0, 0, 0);
   for (int k = 0; k < K; k += 4) {
-    const int4 ev = nxt;
+    const uint4 ev = nxt;
     if (k + 4 < K) nxt = __ldcs(lp + ((k >> 2) + 1) * 32);
-    const int es[4] = {ev.x, ev.y, ev.z, ev.w};
-    double2 o[4];
-    double wq[4];
+    const unsigned es[4] = {ev.x, ev.y, ev.z, ev.w};
+    double4 o[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) o[u] = ld_rec(rec + (es[u] & MvIdx<G>::kIdxMask));
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int src = es[u] < 0 ? self : es[u];
-      o[u] = xye[src];
-      wq[u] = es[u] < 0 ? 0.0 : we[src];
-    }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const double dx = p.x - o[u].x, dy = p.y - o[u].y;
-      const double r2 = fma(dx, dx, dy * dy);
-      acc = fma(wq[u], exp_neg_smem(r2 * nscale, s_tab), acc);
+      for (int j = 0; j < G; ++j) {
+        const double dx = me[j].x - o[u].x, dy = me[j].y - o[u].y;
+        const double r2 = fma(dx, dx, dy * dy);
+        const double e = EXPV == 0 ? gauss_exp64(r2, esc, tab) : gauss_exp2(r2, esc);
+        if (es[u] & MvIdx<G>::bit(j)) acc[j] = fma(o[u].z, e, acc[j]);
+      }
     }
   }
-  if (active) y[t - st.own_lo] = acc * g.norm;
+#pragma unroll
+  for (int j = 0; j < G; ++j)
+    if (t0 + j < nloc) y[t0 + j] = acc[j] * g.norm;
+}
+
+static int env_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
 }
 
 int build_nlist(rbf_ctx *c, cudaStream_t s) {
-  const int ncl = owned_cells(c);
-  if (ncl <= 0) return RBF_OK;
-  int *first = nullptr;
-  RBF_TRY(dalloc(c, (void **)&first, sizeof(int) * (ncl + 1), s));
-  k_chunk_count<<<(ncl + 1 + 255) / 256, 256, 0, s>>>(c->g, c->s, c->cell_start, ncl, first);
-  count_launch(1);
-  size_t tb = 0;
-  RBF_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, first, first, ncl + 1, s));
-  void *tmp = nullptr;
-  RBF_TRY(dalloc(c, &tmp, tb, s));
-  RBF_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, first, first, ncl + 1, s));
-  count_launch(2);
-  int nch = 0;
-  RBF_CUDA_TRY(cudaMemcpyAsync(&nch, first + ncl, sizeof(int), cudaMemcpyDeviceToHost, s));
-  RBF_CUDA_TRY(cudaStreamSynchronize(s));
-  dfree(tmp, s);
-  c->nchunks = nch;
-  c->chunk_first = first;
-  RBF_TRY(dalloc(c, (void **)&c->chunk_cell, sizeof(int) * (nch > 0 ? nch : 1), s));
-  RBF_TRY(dalloc(c, (void **)&c->chunk_len, sizeof(int) * (nch > 0 ? nch : 1), s));
+  const long long nl = n_loc(c), ne = n_ext(c);
+  c->mv_exp = env_int("RBF_MV_EXP", 1) ? 1 : 0;
+  c->mv_g = env_int("RBF_MV_G", 2);
+  if (c->mv_g < 1 || c->mv_g > 3) c->mv_g = 2;
+  if (ne >= (1LL << (32 - c->mv_g))) c->mv_g = 1;  // source index must fit beside the mask bits
+  if (ne >= (1LL << 31)) {
+    set_error("rbf_setup: %lld points in one strip exceed the 31-bit neighbour-list index", ne);
+    return RBF_EINVAL;
+  }
+  const int G = c->mv_g;
+  const long long lanes = (nl + G - 1) / G;
+  c->nchunks = (int)((lanes + 31) / 32);
+  RBF_TRY(dalloc(c, (void **)&c->rec, sizeof(double4) * (size_t)(ne > 0 ? ne : 1), s));
+  if (ne > 0) {
+    k_init_rec<<<(int)((ne + 255) / 256), 256, 0, s>>>(c->xy_ext, ne, c->rec);
+    count_launch(1);
+  }
+  if (nl <= 0) return RBF_OK;
+  const int nch = c->nchunks;
+  RBF_TRY(dalloc(c, (void **)&c->chunk_len, sizeof(int) * nch, s));
   RBF_TRY(dalloc(c, (void **)&c->chunk_off, sizeof(long long) * (nch + 1), s));
-  if (nch == 0) return RBF_OK;
-  k_chunk_fill<<<(ncl + 255) / 256, 256, 0, s>>>(first, ncl, c->chunk_cell);
-  count_launch(1);
-  const int blocks = (nch + kMvWarps - 1) / kMvWarps;
-  k_nlist<0><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->chunk_cell,
-                                           first, nch, c->chunk_len, nullptr, nullptr);
+  const int blocks = (int)((lanes + kMvThreads - 1) / kMvThreads);
+#define RBF_NLIST(MODE, off, lst)                                                                   \
+  switch (G) {                                                                                      \
+    case 1: k_nlist<MODE, 1><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, \
+                                                            c->chunk_len, off, lst); break;         \
+    case 2: k_nlist<MODE, 2><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, \
+                                                            c->chunk_len, off, lst); break;         \
+    default: k_nlist<MODE, 3><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, \
+                                                             c->chunk_len, off, lst); break;        \
+  }
+  RBF_NLIST(0, nullptr, nullptr);
   count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
   // offsets (in entries) = exclusive scan of 32 * len
@@ -208,8 +295,9 @@ int build_nlist(rbf_ctx *c, cudaStream_t s) {
   RBF_CUDA_TRY(cudaMemsetAsync(w64 + nch, 0, sizeof(long long), s));
   k_len_to_entries<<<(nch + 255) / 256, 256, 0, s>>>(c->chunk_len, nch, w64);
   count_launch(1);
-  tb = 0;
+  size_t tb = 0;
   RBF_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, w64, c->chunk_off, nch + 1, s));
+  void *tmp = nullptr;
   RBF_TRY(dalloc(c, &tmp, tb, s));
   RBF_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, w64, c->chunk_off, nch + 1, s));
   count_launch(2);
@@ -219,20 +307,32 @@ int build_nlist(rbf_ctx *c, cudaStream_t s) {
   dfree(tmp, s);
   dfree(w64, s);
   c->nlist_entries = total;
-  RBF_TRY(dalloc(c, (void **)&c->nlist, sizeof(int) * (size_t)(total > 0 ? total : 1), s));
-  k_nlist<1><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->chunk_cell,
-                                           first, nch, c->chunk_len, c->chunk_off, c->nlist);
+  RBF_TRY(dalloc(c, (void **)&c->nlist, sizeof(unsigned) * (size_t)(total > 0 ? total : 1), s));
+  RBF_NLIST(1, c->chunk_off, c->nlist);
+#undef RBF_NLIST
   count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
   return RBF_OK;
 }
 
 int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStream_t s) {
-  if (c->nchunks <= 0) return RBF_OK;
-  k_matvec_ell<<<(c->nchunks + kMvWarps - 1) / kMvWarps, kMvThreads, 0, s>>>(
-      c->g, c->s, c->xy_ext, w_ext, c->cell_start, c->chunk_cell, c->chunk_first, c->nchunks,
-      c->chunk_len, c->chunk_off, c->nlist, y_loc);
-  count_launch(1);
+  const long long ne = n_ext(c), nl = n_loc(c);
+  if (nl <= 0) return RBF_OK;
+  k_pack_w<<<(int)((ne + 255) / 256), 256, 0, s>>>(w_ext, ne, c->rec);
+  const int G = c->mv_g;
+  const long long lanes = (nl + G - 1) / G;
+  const int blocks = (int)((lanes + kMvThreads - 1) / kMvThreads);
+  const long long own_off = c->s.own_lo - c->s.ext_lo;
+#define RBF_MV(GG, E)                                                                          \
+  k_matvec<GG, E><<<blocks, kMvThreads, 0, s>>>(c->g, nl, own_off, c->rec, c->chunk_len,        \
+                                                c->chunk_off, c->nlist, y_loc)
+  if (c->mv_exp == 0) {
+    if (G == 1) RBF_MV(1, 0); else if (G == 2) RBF_MV(2, 0); else RBF_MV(3, 0);
+  } else {
+    if (G == 1) RBF_MV(1, 1); else if (G == 2) RBF_MV(2, 1); else RBF_MV(3, 1);
+  }
+#undef RBF_MV
+  count_launch(2);
   RBF_CUDA_TRY(cudaGetLastError());
   return RBF_OK;
 }
