@@ -300,6 +300,7 @@ def run_ours(args, rank, world):
             "matvec_ms": mv_ms, "rasm_apply_ms": pc_ms,
             "matvec_fp64_frac_useful": gpairs * 1e9 * FLOP_PER_PAIR / (FP64_PEAK_TFLOPS * 1e12),
             "rasm_apply_gbs": pc_alg_bytes / (pc_ms * 1e-3) / 1e9,
+            "step_ms": [round(x, 3) for x in ms],
             "roofline": roof, "clocks": clk, "gpu_launches": int(launches),
             "e2e": e2e, "cpu_baseline": cpu,
         }

@@ -184,6 +184,7 @@ __device__ __forceinline__ int smid() {
 
 struct AccSet {
   double a0, a1, b0, b1;  // two independent DMMA chains (even / odd kt)
+  double v0, v1;          // the tile's A_c entries at this lane's accumulator positions
   __device__ __forceinline__ void zero() { a0 = a1 = b0 = b1 = 0.0; }
 };
 
@@ -205,13 +206,19 @@ __device__ __forceinline__ void acc_range(AccSet &A, const double *sm, int it, i
   }
 }
 
-// C(it, jt) = A(it, jt) - acc, stored in place (accumulator layout)
-__device__ __forceinline__ void acc_finish(const AccSet &A, double *sm, int it, int jt, int lane) {
+// tile(it, jt) -= acc, in place (accumulator layout)
+__device__ __forceinline__ void acc_finish_rmw(const AccSet &A, double *sm, int it, int jt, int lane) {
   double2 *cp = reinterpret_cast<double2 *>(sm + toff(it, jt) + frag_acc(lane));
   double2 cv = *cp;
   cv.x -= A.a0 + A.b0;
   cv.y -= A.a1 + A.b1;
   *cp = cv;
+}
+
+// C(it, jt) = A(it, jt) - acc, stored (accumulator layout)
+__device__ __forceinline__ void acc_finish(const AccSet &A, double *sm, int it, int jt, int lane) {
+  double2 *cp = reinterpret_cast<double2 *>(sm + toff(it, jt) + frag_acc(lane));
+  *cp = make_double2(A.v0 - (A.a0 + A.b0), A.v1 - (A.a1 + A.b1));
 }
 
 // 8x8 Cholesky of the diagonal tile j in place (lanes 0..7 = rows) plus its inverse:
@@ -254,6 +261,35 @@ __device__ __forceinline__ bool diag_factor(double *sm, double *rdiag, int j, in
   return bad;
 }
 
+// A_c = R_c A_rc R_c^T (reading Q10) entries of tile (it, jt) at this lane's
+// accumulator positions (row lane>>2, columns 2(lane&3), +1), in factor order;
+// padding unknowns are decoupled identity rows/columns.  Evaluated just in time
+// (when the tile is finished), so the FP64 work of the assembly overlaps the
+// latency-bound factorization instead of running as a separate phase.
+__device__ __forceinline__ void a_entries(const double2 *pos, const TileShape &S, const Geom &g,
+                                          int it, int jt, int lane, double &v0, double &v1) {
+  const int r = lane >> 2, c0 = 2 * (lane & 3);
+  const int pi = it * 8 + r;
+  const bool padi = (pi >= S.n0 && pi < S.n0p) || pi >= S.n0p + S.n1;
+  const double2 xi = pos[pi];
+  double v[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int pj = jt * 8 + c0 + u;
+    const bool padj = (pj >= S.n0 && pj < S.n0p) || pj >= S.n0p + S.n1;
+    if (padi || padj) {
+      v[u] = (pi == pj) ? 1.0 : 0.0;
+    } else {
+      const double2 xj = pos[pj];
+      const double dx = xi.x - xj.x, dy = xi.y - xj.y;
+      const double r2 = fma(dx, dx, dy * dy);
+      v[u] = (r2 < g.rc2) ? exp_neg(r2 * g.neg_inv_2s2) * g.norm : 0.0;
+    }
+  }
+  v0 = v[0];
+  v1 = v[1];
+}
+
 __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
     Geom g, Strip st, const double2 *__restrict__ xy, const int *__restrict__ cell_start,
     const long long *__restrict__ x_off, double *__restrict__ X, int *__restrict__ counts,
@@ -284,32 +320,6 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
     pos[p] = (gi >= 0) ? xy[gi - st.ext_lo] : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  const int ntiles = T * (T + 1) / 2;
-  for (int t = warp; t < ntiles; t += kTcWarps) {
-    int it = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
-    while (it * (it + 1) / 2 > t) --it;
-    while ((it + 1) * (it + 2) / 2 <= t) ++it;
-    const int jt = t - it * (it + 1) / 2;
-    const int r = lane >> 2, c0 = 2 * (lane & 3);
-    const int pi = it * 8 + r;
-    const bool padi = (pi >= S.n0 && pi < S.n0p) || pi >= S.n0p + S.n1;
-    const double2 xi = pos[pi];
-    double v[2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int pj = jt * 8 + c0 + u;
-      const bool padj = (pj >= S.n0 && pj < S.n0p) || pj >= S.n0p + S.n1;
-      if (padi || padj) {
-        v[u] = (pi == pj) ? 1.0 : 0.0;
-      } else {
-        const double2 xj = pos[pj];
-        const double dx = xi.x - xj.x, dy = xi.y - xj.y;
-        const double r2 = fma(dx, dx, dy * dy);
-        v[u] = (r2 < g.rc2) ? exp_neg(r2 * g.neg_inv_2s2) * g.norm : 0.0;
-      }
-    }
-    *reinterpret_cast<double2 *>(&sm[toff(it, jt) + swz(r, c0)]) = make_double2(v[0], v[1]);
-  }
   __syncthreads();
 
   PROBE(1)
@@ -317,6 +327,16 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
   AccSet acc[2];
   acc[0].zero();
   acc[1].zero();
+  // A entries of the tiles finished in the first step (column 0)
+  if (warp < kAccWarps) {
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int it = 1 + warp + kAccWarps * m;
+      if (it < T) a_entries(pos, S, g, it, 0, lane, acc[m].v0, acc[m].v1);
+    }
+  } else if (warp == kAccWarps) {
+    a_entries(pos, S, g, 0, 0, lane, acc[0].v0, acc[0].v1);
+  }
   for (int j = 0; j < T; ++j) {
     const int dw = kAccWarps + (j & 1);  // diagonal warp of column j
     if (warp < kAccWarps) {
@@ -334,7 +354,10 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
       for (int m = 0; m < 2; ++m) {
         const int it = j + 2 + warp + kAccWarps * m;
         acc[m].zero();
-        if (it < T && j + 1 < T) acc_range(acc[m], sm, it, j + 1, 0, j, lane);
+        if (it < T && j + 1 < T) {
+          a_entries(pos, S, g, it, j + 1, lane, acc[m].v0, acc[m].v1);
+          acc_range(acc[m], sm, it, j + 1, 0, j, lane);
+        }
       }
     } else if (warp == dw) {
       // finish the diagonal tile (its sum over kt < j-1 was accumulated last step)
@@ -345,6 +368,7 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
     } else if (j + 1 < T) {
       // the other diagonal warp accumulates the next diagonal tile over kt < j
       acc[0].zero();
+      a_entries(pos, S, g, j + 1, j + 1, lane, acc[0].v0, acc[0].v1);
       acc_range(acc[0], sm, j + 1, j + 1, 0, j, lane);
     }
     __syncthreads();
@@ -406,7 +430,7 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
       A.a1 += B.a1;
       A.b0 += B.b0;
       A.b1 += B.b1;
-      acc_finish(A, sm, it, jt, lane);
+      acc_finish_rmw(A, sm, it, jt, lane);
       __syncwarp();
       // W(it, jt) = C L_d^-1   (B[k][n] = Linv[k][n])
       const double *D = sm + toff(jt, jt);

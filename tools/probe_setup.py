@@ -21,10 +21,10 @@ for _ in range(2):
     torch.cuda.synchronize()
     print(c.setup_times())
     c.close()
-buf = np.zeros(64 * 8 + 65536 * 3, dtype=np.int64)
+buf = np.zeros(64 * 8 + 65536 * 3 + 512, dtype=np.int64)
 assert L.rbf_debug_probe(buf.ctypes.data_as(C.c_void_p)) == 0
 out = buf[:512].reshape(64, 8)
-tr = buf[512:].reshape(65536, 3)[:42025]
+tr = buf[512:512 + 65536 * 3].reshape(65536, 3)[:42025]
 dur = (tr[:, 2] - tr[:, 1]) / 1e3
 print(f"CTA duration us: mean {dur.mean():.1f} min {dur.min():.1f} max {dur.max():.1f}")
 t0 = tr[:, 1].min()
@@ -35,8 +35,17 @@ for sm in (0, 1, 77):
     en = np.sort(tr[sel, 2])
     gaps = (st[1:] - en[:-1]) / 1e3
     print(f"sm {sm}: ctas {len(sel)}, mean gap between CTAs {gaps.mean():.2f} us, busy {(en - st).sum() / 1e3:.0f} us")
+out = out[out[:, 4] > 0]
 d = np.diff(out[:, :5], axis=1)
 names = ["assembly", "cholesky", "W+Sinv", "X write"]
 for i, nm in enumerate(names):
     print(f"{nm:10s} mean {d[:, i].mean():10.0f} cyc  min {d[:, i].min():8d} max {d[:, i].max():8d}")
 print("total", (out[:, 4] - out[:, 0]).mean())
+col = buf[512 + 65536 * 3:].reshape(2, 64, 4)
+c0 = col[0]
+base = c0[0, 0]
+print("per column (cycles since start of Cholesky), thread 0: [start, (i)+(ii) done, before sync, after sync]; diag warp 14: [start, factor start, factor done]")
+for j in range(30):
+    if c0[j, 0] == 0: break
+    w = col[1][j]
+    print(j, c0[j, 0] - base, c0[j, 3] - base, c0[j, 1] - base, c0[j, 2] - base, "| w14", *(w[[0, 1, 3]] - base if w[3] else []))
