@@ -263,3 +263,130 @@ def test_cfg2_solve_true_residual(cfg2):
     assert 40 <= rep.iterations <= 150  # [D4]: 73 on a 256^2 jittered model
     s = O.matvec_cells(wl.xy, lam, wl.sigma, wl.rc, wl.box, wl.cell)
     assert rel(s, wl.f) <= 1e-10
+
+
+# ------------------------------------------------------------------ full size, other configs
+# BASELINE.json configs[2] (cfg3, 16.8M lattice points), configs[3] (cfg4, 50M) and
+# configs[4] (cfg5, 4.2M clustered points): sampled outputs the oracle computes one
+# by one (rows of A_rc from the points of their cell stencil; cells' local solves),
+# plus properties that hold at any size (exact lattice pair counts, residuals).
+
+def lattice_pairs(n_side, rc_over_h):
+    """Exact in-cutoff ordered pair count (self pairs included) of an n x n lattice:
+    sum over offsets m with |m| < rc/h of (n - |mx|)(n - |my|) (SURVEY.md [D7])."""
+    R = int(np.floor(rc_over_h))
+    tot = 0
+    for mx in range(-R, R + 1):
+        for my in range(-R, R + 1):
+            if mx * mx + my * my < rc_over_h ** 2:
+                tot += (n_side - abs(mx)) * (n_side - abs(my))
+    return tot
+
+
+def test_lattice_pairs_closed_form_matches_cfg1_golden():
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "lattice_constants.json")))
+    assert lattice_pairs(100, 7.5) == g["cfg1_pairs"]
+
+
+def oracle_rows(wl, w, rows, cl):
+    """Rows of y = A_rc w by the oracle's brute-force definition restricted to the
+    (2k+1)^2 cell stencil of each row's cell (k = ceil(rc / cell): every j within rc
+    is in it)."""
+    key, perm, start = cl
+    ncx, ncy = O.grid_dims(wl.box, wl.cell)
+    kh = int(np.ceil(wl.rc / wl.cell))
+    out = np.empty(len(rows))
+    for q, i in enumerate(rows):
+        cx, cy = key[i] % ncx, key[i] // ncx
+        win = []
+        for by in range(max(cy - kh, 0), min(cy + kh, ncy - 1) + 1):
+            for bx in range(max(cx - kh, 0), min(cx + kh, ncx - 1) + 1):
+                b = by * ncx + bx
+                win.append(perm[start[b]:start[b + 1]])
+        win = np.concatenate(win)
+        pos = int(np.nonzero(win == i)[0][0])
+        out[q] = O.matvec_brute(wl.xy[win], w[win], wl.sigma, wl.rc, rows=[pos])[0]
+    return out
+
+
+def oracle_cell_solve(wl, r, cc, cl):
+    key, perm, start = cl
+    ncx, ncy = O.grid_dims(wl.box, wl.cell)
+    cx, cy = cc % ncx, cc // ncx
+    ov = np.concatenate([perm[start[by * ncx + bx]:start[by * ncx + bx + 1]]
+                         for by in range(max(cy - 1, 0), min(cy + 1, ncy - 1) + 1)
+                         for bx in range(max(cx - 1, 0), min(cx + 1, ncx - 1) + 1)])
+    own = perm[start[cc]:start[cc + 1]]
+    sol, _ = O.dense_factor_solve(O.assemble_dense(wl.xy[ov], wl.sigma, wl.rc), r[ov])
+    pos = {j: q for q, j in enumerate(ov)}
+    return own, np.array([sol[pos[j]] for j in own])
+
+
+BIG = {3: 40e9, 4: 140e9}  # device bytes the config needs (DESIGN.md §6)
+
+
+@pytest.fixture(scope="module", params=[3, 4], ids=["cfg3", "cfg4"])
+def big(request):
+    cfg = request.param
+    if torch.cuda.mem_get_info()[0] < BIG[cfg]:
+        pytest.skip(f"cfg{cfg} needs {BIG[cfg] / 1e9:.0f} GB of free device memory")
+    wl = W.config(cfg)
+    cl = O.cell_list(wl.xy, wl.box, wl.cell)
+    c = ctx_for(wl)
+    yield wl, c, cl
+    c.close()
+    torch.cuda.empty_cache()
+
+
+def test_big_matvec_sampled_rows(big):
+    wl, c, cl = big
+    rng = np.random.default_rng(17)
+    w = rng.standard_normal(wl.n)
+    n_side = wl.meta["n_side"]
+    rows = np.concatenate([[0, wl.n - 1, n_side - 1, wl.n - n_side], rng.choice(wl.n, 300, replace=False)])
+    got = to_caller(c, c.matvec(c.to_local(torch.from_numpy(w).cuda())))
+    assert rel(got[rows], oracle_rows(wl, w, rows, cl)) <= 1e-12
+    assert c.count_pairs() == lattice_pairs(n_side, wl.rc / wl.meta["h"] * (1 - 1e-12))
+
+
+def test_big_rasm_sampled_cells(big):
+    wl, c, cl = big
+    rng = np.random.default_rng(18)
+    r = rng.standard_normal(wl.n)
+    z = to_caller(c, c.rasm_apply(c.to_local(torch.from_numpy(r).cuda())))
+    ncx, ncy = O.grid_dims(wl.box, wl.cell)
+    for cc in [0, ncx - 1, ncx * ncy - 1, ncx * (ncy // 2) + ncx // 2] + list(rng.choice(ncx * ncy, 8)):
+        own, ref = oracle_cell_solve(wl, r, int(cc), cl)
+        assert rel(z[own], ref) <= 1e-10
+
+
+def test_big_solve_residual(big):
+    wl, c, cl = big
+    lam, rep = c.solve(c.to_local(torch.from_numpy(wl.f).cuda()), rtol=wl.tol)
+    lam = to_caller(c, lam)
+    assert rep.converged and rep.iterations <= 300
+    assert rep.resid_true <= 1e-10
+    rng = np.random.default_rng(19)
+    rows = rng.choice(wl.n, 200, replace=False)
+    res = wl.f[rows] - oracle_rows(wl, lam, rows, cl)
+    assert np.max(np.abs(res)) <= 1e-9 * np.max(np.abs(wl.f))
+
+
+def test_cfg5_matvec_sampled_rows():
+    """Clustered points: heavy cells, non-uniform pair counts (block-Jacobi context, so
+    only the matvec path is exercised here)."""
+    wl = W.config(5)
+    cl = O.cell_list(wl.xy, wl.box, wl.cell)
+    rng = np.random.default_rng(20)
+    w = rng.standard_normal(wl.n)
+    # rows in the densest cell and random rows
+    key, perm, start = cl
+    dense = int(np.argmax(np.diff(start)))
+    rows = np.concatenate([perm[start[dense]:start[dense] + 40], rng.choice(wl.n, 200, replace=False)])
+    with ctx_for(wl, rings=0) as c:
+        got = to_caller(c, c.matvec(c.to_local(torch.from_numpy(w).cuda())))
+        npairs = c.count_pairs()
+    assert rel(got[rows], oracle_rows(wl, w, rows, cl)) <= 1e-12
+    assert npairs == O.count_pairs(wl.xy, wl.rc, wl.box, wl.cell)
