@@ -175,8 +175,8 @@ __device__ __forceinline__ int smid() {
 }
 #define TRACE(i) \
   if (threadIdx.x == 0 && blockIdx.x < 65536) { g_trace[blockIdx.x][0] = smid(); g_trace[blockIdx.x][i] = gtimer(); }
-#define PROBE(i) \
-  if (threadIdx.x == 0 && blockIdx.x < 64) g_probe[blockIdx.x][i] = clock64();
+#define PROBE(i) /* 64 sampled CTAs spread over the grid (mostly interior cells) */ \
+  if (threadIdx.x == 0 && blockIdx.x % 509 == 300 && blockIdx.x / 509 < 64) g_probe[blockIdx.x / 509][i] = clock64();
 #else
 #define PROBE(i)
 #define TRACE(i)

@@ -96,6 +96,80 @@ __device__ __forceinline__ bool diag_factor_fast(double *sm, double *rdiag, int 
 }
 
 
+__device__ __forceinline__ double rsqrt_fast(double a) {
+  // fp32 hardware estimate, then two Newton steps in fp64: y <- y (3 - a y^2) / 2
+  double y = (double)rsqrtf((float)a);
+  double h = a * y;
+  double r = fma(-h, y, 1.0);
+  y = fma(0.5 * y, r, y);
+  h = a * y;
+  r = fma(-h, y, 1.0);
+  return fma(0.5 * y, r, y);
+}
+
+// Restructured: the next pivot row updates its diagonal lane-locally (the pivot
+// chain is shfl + rsqrt + mul + fma per step), off-diagonal updates in parallel.
+__device__ long long g_stamp[4];
+__device__ __forceinline__ bool diag_factor2(double *sm, double *rdiag, int j, int lane) {
+  long long t0 = clock64();
+  double *D = sm + toff(j, j);
+  double a[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) a[c] = (lane < 8) ? D[swz(lane, c)] : (c == 0 ? 1.0 : 0.0);
+  bool bad = false;
+  double rinv = 1.0;
+  double dcur = a[0];  // this lane's running diagonal candidate (meaningful for lane = next pivot)
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double akk = __shfl_sync(0xffffffffu, (lane == k) ? dcur : a[k], k);
+    bad |= !(akk > 0.0);
+    const double il = rsqrt(akk);
+    const double lik = (lane == k) ? akk * il : a[k] * il;  // row `lane`, column k of L
+    if (lane == k) rinv = il;
+    a[k] = (lane >= k) ? lik : 0.0;
+    if (k + 1 < 8) dcur = fma(-lik, lik, a[k + 1]);  // next pivot (lane k+1), lane-local
+#pragma unroll
+    for (int jj = k + 1; jj < 8; ++jj) {
+      const double ljk = __shfl_sync(0xffffffffu, lik, jj);
+      if (lane >= jj) a[jj] = fma(-lik, ljk, a[jj]);
+    }
+    if (k + 1 < 8 && lane == k + 1) dcur = a[k + 1];  // identical value, keeps a[] consistent
+  }
+  long long t1 = clock64() + (long long)(a[7] * 0.0);
+  double x[8];
+  double Lrow[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int m = 0; m < i; ++m) Lrow[i][m] = __shfl_sync(0xffffffffu, a[m], i);
+  double rd[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) rd[i] = __shfl_sync(0xffffffffu, rinv, i);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    double sacc = (lane == i) ? 1.0 : 0.0;
+#pragma unroll
+    for (int m = 0; m < i; ++m) sacc = fma(-Lrow[i][m], x[m], sacc);
+    x[i] = sacc * rd[i];
+  }
+  long long t2 = clock64() + (long long)(x[7] * 0.0);
+  if (lane < 8) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) D[swz(lane, c)] = (c <= lane) ? a[c] : x[c];
+    rdiag[j * 8 + lane] = rinv;
+  }
+  if (lane == 0) { g_stamp[0] += t1 - t0; g_stamp[1] += t2 - t1; g_stamp[2] += clock64() - t2; }
+  return bad;
+}
+
+template <int V>
+__global__ void lat(double *out, long long *cyc, int reps) {
+  double x = 2.0 + threadIdx.x * 1e-9;
+  long long t0 = clock64();
+  for (int i = 0; i < reps; ++i) x = 1.0 + (V == 0 ? rsqrt(x) : rsqrt_fast(x));
+  long long t1 = clock64();
+  if (threadIdx.x == 0) { cyc[2 + V] = (t1 - t0) / reps; out[2 + V] = x; }
+}
 template <int V>
 __global__ void k(double *out, long long *cyc, int reps) {
   __shared__ double sm[64 * 2];
@@ -108,17 +182,23 @@ __global__ void k(double *out, long long *cyc, int reps) {
     for (int e = lane; e < 64; e += 32) { int i = e / 8, c = e % 8; sm[swz(i, c)] = (i == c) ? 10.0 + r : 1.0 / (1 + i + c); }
     __syncwarp();
     long long t0 = clock64();
-    bad |= V == 0 ? diag_factor(sm, rdiag, 0, lane) : diag_factor_fast(sm, rdiag, 0, lane);
+    bad |= V == 0 ? diag_factor(sm, rdiag, 0, lane) : (V == 1 ? diag_factor_fast(sm, rdiag, 0, lane) : diag_factor2(sm, rdiag, 0, lane));
     __syncwarp();
     long long t1 = clock64();
     tot += t1 - t0;
   }
-  if (lane == 0) { cyc[V] = tot / reps; out[V] = sm[swz(7, 7)] + sm[swz(1, 6)] + rdiag[3] + bad; }
+  if (lane == 0) { cyc[V] = tot / reps; double cs = 0; for (int e = 0; e < 64; ++e) cs += sm[e] * (e + 1); out[V] = cs + rdiag[3] + bad; }
 }
 int main() {
-  double *o; long long *c; cudaMalloc(&o, 16); cudaMalloc(&c, 16);
-  k<0><<<1, 32>>>(o, c, 100); k<1><<<1, 32>>>(o, c, 100);
-  long long h[2]; double ho[2];
-  cudaMemcpy(h, c, 16, cudaMemcpyDeviceToHost); cudaMemcpy(ho, o, 16, cudaMemcpyDeviceToHost);
-  printf("diag_factor %lld cyc (check %.15g), diag_factor_fast %lld cyc (check %.15g)\n", h[0], ho[0], h[1], ho[1]);
+  double *o; long long *c; cudaMalloc(&o, 64); cudaMalloc(&c, 64);
+  lat<0><<<1, 32>>>(o, c, 1000); lat<1><<<1, 32>>>(o, c, 1000);
+  long long hl[4]; double hol[4];
+  cudaMemcpy(hl, c, 32, cudaMemcpyDeviceToHost); cudaMemcpy(hol, o, 32, cudaMemcpyDeviceToHost);
+  printf("rsqrt(double) chain latency %lld cyc (x=%.17g), rsqrt_fast %lld cyc (x=%.17g)\n", hl[2], hol[2], hl[3], hol[3]);
+  k<0><<<1, 32>>>(o, c, 100); k<1><<<1, 32>>>(o, c, 100); k<2><<<1, 32>>>(o, c, 100);
+  long long h[3]; double ho[3];
+  cudaMemcpy(h, c, 24, cudaMemcpyDeviceToHost); cudaMemcpy(ho, o, 24, cudaMemcpyDeviceToHost);
+  long long st[4]; cudaMemcpyFromSymbol(st, g_stamp, 32);
+  printf("diag_factor2 phases (per call): factor %lld inverse %lld store %lld\n", st[0] / 100, st[1] / 100, st[2] / 100);
+  printf("diag_factor %lld cyc (check %.17g)\ndiag_factor_fast %lld cyc (check %.17g)\ndiag_factor2 %lld cyc (check %.17g)\n", h[0], ho[0], h[1], ho[1], h[2], ho[2]);
 }
