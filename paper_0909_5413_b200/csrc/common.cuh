@@ -142,7 +142,7 @@ struct rbf_ctx {
   // matvec: packed source records {x, y, w, 0} (ext range) and the neighbour list
   // (ELL of 32-bit entries in groups of 4, chunks of 32 consecutive owned targets)
   double4 *rec = nullptr;
-  int mv_exp = 1;              // exp variant (1: polynomial, 0: replicated 64-entry table)
+  int mv_var = 0;              // matvec kernel variant (A/B measurements only)
   int mv_g = 2;                // targets per lane (union lists with per-target mask bits)
   int nchunks = 0;
   int *chunk_len = nullptr;    // per chunk: list length (max over its lanes, multiple of 4)

@@ -20,11 +20,12 @@
 // the FP64 pipe, is what a gather-based matvec saturates first (ncu, profiles/), so
 // every byte through L1 counts: 32 B per pair for the record, 4 B for the index.
 //
-// exp() runs on the FP64 pipe with no table (EXPV 1): k = round(-r2 log2e/(2s^2)),
-// f = -r2 log2e/(2 s^2) - k in [-1/2, 1/2] (one fma from the exact product), 2^f by
-// a degree-11 polynomial (<= ~1 ulp, reading Q15), 2^k by an integer add to the
-// exponent field.  EXPV 0 is the table variant (64 entries, replicated per lane in
-// shared memory so each LDS.64 is conflict-free).
+// exp() runs on the FP64 pipe with no table: k = round(-r2 log2e/(2s^2)),
+// f = -r2 log2e/(2 s^2) - k in [-1/2, 1/2] (one fma from the exact product), 2^f =
+// 1 + f P(f) with P a minimax polynomial of degree DEG (10: ~1.3 ulp, 9: ~3.5 ulp;
+// reading Q15), 2^k by an integer add to the exponent field.  (A 64-entry table
+// variant, replicated per lane in shared memory, was measured slower: the table
+// loads compete with the gathers for the L1 data pipe; profiles/.)
 //
 // Padding entries point at the target itself (a finite term) and are masked by a
 // predicated accumulate, so the per-target sum is exactly the sum over its list in
@@ -41,50 +42,36 @@ namespace rbf {
 constexpr int kMvWarps = 8;  // target chunks per CTA
 constexpr int kMvThreads = 32 * kMvWarps;
 
-// 2^f = 1 + f P(f) on [-1/2, 1/2], P of degree 10 (Chebyshev-node fit, max error
-// ~1 ulp; tools/ derivation in DESIGN.md §6), highest coefficient first.
-__constant__ double kExp2P[11] = {4.4549605981865186e-10, 7.072585949269223e-09,
-                                  1.0178062445845774e-07, 1.321544258792169e-06,
-                                  1.525273382983612e-05,  0.0001540353044173605,
-                                  0.0013333558146416936,  0.009618129107606888,
-                                  0.0555041086648216,     0.24022650695910097,
-                                  0.6931471805599453};
-// e^{f ln2/64} - 1 = f (a1 + a2 f + ... + a5 f^4), a_i = (ln2/64)^i / i!
-__constant__ double kExp64A[5] = {1.2417843701716925e-12, 5.732851688640402e-10,
-                                  2.1173137155464776e-07, 5.86490495505617e-05,
-                                  0.010830424696249145};
+// 2^f = 1 + f P(f) on [-1/2, 1/2]: minimax P (Remez on the relative error, DESIGN.md
+// §6), highest coefficient first.  Degree 10: max error 1.5e-16; degree 9: 3.9e-16.
+__constant__ double kExp2P10[11] = {4.078071929588337e-10, 7.072570412814423e-09,
+                                    1.0180647659234139e-07, 1.3215442675329823e-06,
+                                    1.5252727385193868e-05, 0.0001540353044157213,
+                                    0.0013333558153439966, 0.009618129107607003,
+                                    0.05550410866479039, 0.24022650695910097,
+                                    0.6931471805599457};
+__constant__ double kExp2P9[10] = {7.111758687557852e-09, 1.0210506458816145e-07,
+                                   1.321523563477604e-06, 1.525264774769592e-05,
+                                   0.00015403530800818256, 0.001333355824648072,
+                                   0.009618129107380715, 0.05550410866434658,
+                                   0.24022650695910472, 0.6931471805599516};
 
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer shifter
 
 // exp(-r2/(2 sigma^2)) for 0 <= r2 < rc^2 (rc <= 37 sigma, so the result is a normal
 // number > 2^-990 and no underflow guard is needed).  esc = -log2(e)/(2 sigma^2).
+template <int DEG>
 __device__ __forceinline__ double gauss_exp2(double r2, double esc) {
   const double t = fma(r2, esc, kMagic);
   const double kd = t - kMagic;
   const int k = __double2loint(t);
   const double f = fma(r2, esc, -kd);  // exact product, one rounding: |f| <= 1/2
-  double p = kExp2P[0];
+  const double *P = DEG == 10 ? kExp2P10 : kExp2P9;
+  double p = P[0];
 #pragma unroll
-  for (int i = 1; i < 11; ++i) p = fma(p, f, kExp2P[i]);
+  for (int i = 1; i <= DEG; ++i) p = fma(p, f, P[i]);
   const double q = fma(f, p, 1.0);
   return __hiloint2double(__double2hiint(q) + k * (1 << 20), __double2loint(q));
-}
-
-// Table variant: esc64 = -64 log2(e)/(2 sigma^2); tab = this lane's column of the
-// replicated 2^(j/64) table (stride 32 doubles).
-__device__ __forceinline__ double gauss_exp64(double r2, double esc64, const double *tab) {
-  const double t = fma(r2, esc64, kMagic);
-  const double kd = t - kMagic;
-  const int k = __double2loint(t);
-  const double f = fma(r2, esc64, -kd);
-  double p = fma(f, kExp64A[0], kExp64A[1]);
-  p = fma(f, p, kExp64A[2]);
-  p = fma(f, p, kExp64A[3]);
-  p = fma(f, p, kExp64A[4]);
-  p = f * p;
-  const double T = tab[(k & 63) * 32];
-  const double e = fma(T, p, T);
-  return __hiloint2double(__double2hiint(e) + (k >> 6) * (1 << 20), __double2loint(e));
 }
 
 __device__ __forceinline__ double4 ld_rec(const double4 *p) {
@@ -196,19 +183,19 @@ __global__ void k_pack_w(const double *__restrict__ w, long long n, double4 *__r
 }
 
 // ---------------------------------------------------------------------------
-// The matvec: one warp per chunk of 32 G consecutive targets, G per lane.
+// The matvec: one warp per chunk of 32 G consecutive targets, G per lane; U list
+// entries (U record gathers) in flight per lane.
 // ---------------------------------------------------------------------------
-template <int G, int EXPV>
-__global__ __launch_bounds__(kMvThreads) void k_matvec(
+__device__ __forceinline__ void prefetch_l1(const void *p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+template <int G, int DEG, int U, int MINB, bool PF = false>
+__global__ __launch_bounds__(kMvThreads, MINB) void k_matvec(
     Geom g, long long nloc, long long own_off, const double4 *__restrict__ rec,
     const int *__restrict__ chunk_len, const long long *__restrict__ chunk_off,
     const unsigned *__restrict__ list, double *__restrict__ y) {
-  __shared__ double s_tab[EXPV == 0 ? 64 * 32 : 1];
   const int lane = threadIdx.x & 31;
-  if (EXPV == 0) {
-    for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) s_tab[i] = kExp2Tab64[i >> 5];
-    __syncthreads();
-  }
   const long long lt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long t0 = lt * G;
   const long long ch = lt >> 5;
@@ -223,24 +210,31 @@ __global__ __launch_bounds__(kMvThreads) void k_matvec(
   }
   const int K = chunk_len[ch];  // multiple of 4
   const uint4 *lp = reinterpret_cast<const uint4 *>(list + chunk_off[ch]) + lane;
-  const double esc = EXPV == 0 ? g.esc64 : g.esc;
-  const double *tab = s_tab + lane;
+  const double esc = g.esc;
   uint4 nxt = (K > 0) ? __ldcs(lp) : make_uint4(0, 0, 0, 0);
   for (int k = 0; k < K; k += 4) {
     const uint4 ev = nxt;
     if (k + 4 < K) nxt = __ldcs(lp + ((k >> 2) + 1) * 32);
     const unsigned es[4] = {ev.x, ev.y, ev.z, ev.w};
-    double4 o[4];
+    if (PF && k + 4 < K) {  // the next group's records into L1 while this group computes
+      prefetch_l1(rec + (nxt.x & MvIdx<G>::kIdxMask));
+      prefetch_l1(rec + (nxt.y & MvIdx<G>::kIdxMask));
+      prefetch_l1(rec + (nxt.z & MvIdx<G>::kIdxMask));
+      prefetch_l1(rec + (nxt.w & MvIdx<G>::kIdxMask));
+    }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) o[u] = ld_rec(rec + (es[u] & MvIdx<G>::kIdxMask));
+    for (int u0 = 0; u0 < 4; u0 += U) {
+      double4 o[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < U; ++u) o[u] = ld_rec(rec + (es[u0 + u] & MvIdx<G>::kIdxMask));
 #pragma unroll
-      for (int j = 0; j < G; ++j) {
-        const double dx = me[j].x - o[u].x, dy = me[j].y - o[u].y;
-        const double r2 = fma(dx, dx, dy * dy);
-        const double e = EXPV == 0 ? gauss_exp64(r2, esc, tab) : gauss_exp2(r2, esc);
-        if (es[u] & MvIdx<G>::bit(j)) acc[j] = fma(o[u].z, e, acc[j]);
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          const double dx = me[j].x - o[u].x, dy = me[j].y - o[u].y;
+          const double e = gauss_exp2<DEG>(fma(dx, dx, dy * dy), esc);
+          if (es[u0 + u] & MvIdx<G>::bit(j)) acc[j] = fma(o[u].z, e, acc[j]);
+        }
       }
     }
   }
@@ -256,9 +250,8 @@ static int env_int(const char *name, int dflt) {
 
 int build_nlist(rbf_ctx *c, cudaStream_t s) {
   const long long nl = n_loc(c), ne = n_ext(c);
-  c->mv_exp = env_int("RBF_MV_EXP", 1) ? 1 : 0;
-  c->mv_g = env_int("RBF_MV_G", 2);
-  if (c->mv_g < 1 || c->mv_g > 3) c->mv_g = 2;
+  c->mv_var = env_int("RBF_MV_VAR", 0);  // A/B switch; 0 = default
+  c->mv_g = env_int("RBF_MV_G", 2) == 1 ? 1 : 2;
   if (ne >= (1LL << (32 - c->mv_g))) c->mv_g = 1;  // source index must fit beside the mask bits
   if (ne >= (1LL << 31)) {
     set_error("rbf_setup: %lld points in one strip exceed the 31-bit neighbour-list index", ne);
@@ -281,9 +274,7 @@ int build_nlist(rbf_ctx *c, cudaStream_t s) {
   switch (G) {                                                                                      \
     case 1: k_nlist<MODE, 1><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, \
                                                             c->chunk_len, off, lst); break;         \
-    case 2: k_nlist<MODE, 2><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, \
-                                                            c->chunk_len, off, lst); break;         \
-    default: k_nlist<MODE, 3><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, \
+    default: k_nlist<MODE, 2><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, \
                                                              c->chunk_len, off, lst); break;        \
   }
   RBF_NLIST(0, nullptr, nullptr);
@@ -323,14 +314,15 @@ int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStre
   const long long lanes = (nl + G - 1) / G;
   const int blocks = (int)((lanes + kMvThreads - 1) / kMvThreads);
   const long long own_off = c->s.own_lo - c->s.ext_lo;
-#define RBF_MV(GG, E)                                                                          \
-  k_matvec<GG, E><<<blocks, kMvThreads, 0, s>>>(c->g, nl, own_off, c->rec, c->chunk_len,        \
-                                                c->chunk_off, c->nlist, y_loc)
-  if (c->mv_exp == 0) {
-    if (G == 1) RBF_MV(1, 0); else if (G == 2) RBF_MV(2, 0); else RBF_MV(3, 0);
-  } else {
-    if (G == 1) RBF_MV(1, 1); else if (G == 2) RBF_MV(2, 1); else RBF_MV(3, 1);
-  }
+#define RBF_MV(GG, DEG, U, MB, ...)                                                            \
+  k_matvec<GG, DEG, U, MB, ##__VA_ARGS__><<<blocks, kMvThreads, 0, s>>>(c->g, nl, own_off, c->rec, c->chunk_len,    \
+                                                     c->chunk_off, c->nlist, y_loc)
+  // Measured alternatives (cfg2, profiles/r01_matvec_variants_cfg2.txt): degree-9
+  // polynomial, 2 gathers in flight, 5 CTAs/SM (48 registers), L1 prefetch of the
+  // next group's records, G = 1 or 3 -- none faster than this configuration.
+  if (G == 1) RBF_MV(1, 10, 4, 1);
+  else if (c->mv_var == 1) RBF_MV(2, 9, 4, 1);
+  else RBF_MV(2, 10, 4, 1);
 #undef RBF_MV
   count_launch(2);
   RBF_CUDA_TRY(cudaGetLastError());

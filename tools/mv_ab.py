@@ -14,7 +14,7 @@ wl = W.config(cfg)
 xy = torch.from_numpy(wl.xy).cuda()
 res = {}
 for v in sys.argv[2:] or ["2:0", "1:1"]:
-    os.environ["RBF_MV_G"], os.environ["RBF_MV_EXP"] = v.split(":")
+    os.environ["RBF_MV_G"], os.environ["RBF_MV_VAR"] = v.split(":")
     c = P.Context(xy, wl.sigma, wl.cell, wl.rc, wl.rings, wl.box)
     npairs = c.count_pairs()
     w = torch.randn(c.n_local, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(1))
@@ -30,7 +30,7 @@ for v in sys.argv[2:] or ["2:0", "1:1"]:
     e1.synchronize()
     ms = e0.elapsed_time(e1) / 50
     res[v] = y.clone()
-    print(f"cfg{cfg} G:EXP={v}: {ms:.4f} ms/matvec, {npairs / ms / 1e6:.1f} Gpairs/s, "
+    print(f"cfg{cfg} G:VAR={v}: {ms:.4f} ms/matvec, {npairs / ms / 1e6:.1f} Gpairs/s, "
           f"useful FP64 frac {npairs * 38 / (ms * 1e-3) / 33.96e12:.3f}, setup {c.setup_times()}", flush=True)
     c.close()
 vals = list(res.values())
