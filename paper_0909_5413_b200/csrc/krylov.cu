@@ -10,6 +10,8 @@
 // rank order (reading Q14).  The Hessenberg column, Givens rotations and the
 // residual estimate live on the device; the host reads back one scalar per
 // iteration to decide convergence.
+#include <cooperative_groups.h>
+
 #include <cmath>
 #include <cstdlib>
 
@@ -188,9 +190,16 @@ __global__ void k_givens(double *S, Scal L, const double *hall, int k, Mailbox *
 constexpr int kArThreads = 1024;
 constexpr int kArE = 8;  // elements per thread held in registers
 
-__device__ __forceinline__ void grid_sync(unsigned *bar, unsigned nb) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Warp 0 only: arrive at the grid barrier (count, generation) after this CTA's
+// partial is globally visible, and wait for the last CTA.
+__device__ __forceinline__ void grid_arrive_wait(unsigned *bar, unsigned nb, int lane) {
+  if (lane == 0) {
     volatile unsigned *vgen = bar + 1;
     const unsigned gen = *vgen;
     __threadfence();
@@ -203,67 +212,83 @@ __device__ __forceinline__ void grid_sync(unsigned *bar, unsigned nb) {
     }
     __threadfence();
   }
-  __syncthreads();
+  __syncwarp();
 }
 
-__device__ __forceinline__ double block_sum_ar(double v, double *sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __syncthreads();
-  if (lane == 0) sh[warp] = v;
-  __syncthreads();
-  double t = (threadIdx.x < kArThreads / 32) ? sh[threadIdx.x] : 0.0;
-  if (warp == 0) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (lane == 0) sh[32] = t;
-  }
-  __syncthreads();
-  return sh[32];
-}
-
+// Each step j: the dot <w, v_j> (or ||w||^2 for j = k+1) is reduced in a fixed
+// order (lanes, warps, then the CTAs' partials in CTA order by warp 0 of every CTA),
+// with two __syncthreads and one grid barrier per step; v_j stays in registers for
+// the update and v_{j+1} is loaded before the barrier, so the HBM latency of the
+// next projection overlaps the reduction.
 __global__ __launch_bounds__(kArThreads, 1) void k_arnoldi_fused(double *V, long long ldv, long long n,
                                                               int k, double *S, Scal L,
                                                               double *part, unsigned *bar,
                                                               Mailbox *mb, long long seq) {
-  __shared__ double sh[33];
+  __shared__ double sh_w[kArThreads / 32];
+  __shared__ double sh_h;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned G = gridDim.x;
   const long long chunk = (n + G - 1) / G;
   const long long base = (long long)blockIdx.x * chunk;
   const long long end = base + chunk < n ? base + chunk : n;
   double *wv = V + (long long)(k + 1) * ldv;
-  double w[kArE];
+  double w[kArE], vc[kArE], vn[kArE];
 #pragma unroll
   for (int e = 0; e < kArE; ++e) {
     const long long i = base + threadIdx.x + (long long)e * kArThreads;
     w[e] = i < end ? wv[i] : 0.0;
+    vc[e] = i < end ? V[i] : 0.0;  // v_0
   }
   for (int j = 0; j <= k + 1; ++j) {
     double acc = 0.0;
-    const double *vj = V + (long long)j * ldv;
     if (j <= k) {
 #pragma unroll
-      for (int e = 0; e < kArE; ++e) {
-        const long long i = base + threadIdx.x + (long long)e * kArThreads;
-        if (i < end) acc = fma(w[e], vj[i], acc);
+      for (int e = 0; e < kArE; ++e) acc = fma(w[e], vc[e], acc);
+      if (j + 1 <= k && threadIdx.x != 0) {  // prefetch v_{j+1} (not by thread 0: its fence
+        const double *vj1 = V + (long long)(j + 1) * ldv;  // in the grid barrier would wait for them)
+#pragma unroll
+        for (int e = 0; e < kArE; ++e) {
+          const long long i = base + threadIdx.x + (long long)e * kArThreads;
+          vn[e] = i < end ? vj1[i] : 0.0;
+        }
       }
     } else {
 #pragma unroll
       for (int e = 0; e < kArE; ++e) acc = fma(w[e], w[e], acc);
     }
-    const double bs = block_sum_ar(acc, sh);
-    if (threadIdx.x == 0) part[(long long)j * G + blockIdx.x] = bs;
-    grid_sync(bar, G);
-    double t = 0.0;
-    for (unsigned b = threadIdx.x; b < G; b += kArThreads) t += ((volatile double *)part)[(long long)j * G + b];
-    const double h = block_sum_ar(t, sh);
-    if (blockIdx.x == 0 && threadIdx.x == 0) S[L.hloc() + j] = h;
-    if (j <= k) {  // v_j re-read: this CTA's slice was just streamed, so it hits L1/L2
+    acc = warp_sum(acc);
+    if (lane == 0) sh_w[warp] = acc;
+    __syncthreads();
+    if (warp == 0) {
+      double t = (lane < kArThreads / 32) ? sh_w[lane] : 0.0;
+      t = warp_sum(t);
+      if (lane == 0) part[(long long)j * G + blockIdx.x] = t;
+    }
+    cooperative_groups::this_grid().sync();
+    if (threadIdx.x == 0 && j + 1 <= k) {
+      const double *vj1 = V + (long long)(j + 1) * ldv;
 #pragma unroll
       for (int e = 0; e < kArE; ++e) {
-        const long long i = base + threadIdx.x + (long long)e * kArThreads;
-        if (i < end) w[e] = fma(-h, vj[i], w[e]);
+        const long long i = base + (long long)e * kArThreads;
+        vn[e] = i < end ? vj1[i] : 0.0;
+      }
+    }
+    if (warp == 0) {
+      double hs = 0.0;
+      for (unsigned b = lane; b < G; b += 32) hs += ((volatile double *)part)[(long long)j * G + b];
+      hs = warp_sum(hs);
+      if (lane == 0) {
+        sh_h = hs;
+        if (blockIdx.x == 0) S[L.hloc() + j] = hs;
+      }
+    }
+    __syncthreads();
+    const double h = sh_h;
+    if (j <= k) {
+#pragma unroll
+      for (int e = 0; e < kArE; ++e) {
+        w[e] = fma(-h, vc[e], w[e]);
+        vc[e] = vn[e];
       }
     } else {
       const double hn = sqrt(h);
@@ -358,7 +383,8 @@ static int ensure_workspace(rbf_ctx *c, int m, cudaStream_t s) {
     RBF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_arnoldi_fused, kArThreads, 0));
     int coop = 0;
     RBF_CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-    c->ar_grid = (coop && per_sm > 0) ? sms * (per_sm < 2 ? per_sm : 2) : 0;
+    const int ar_per_sm = getenv("RBF_AR_PER_SM") ? atoi(getenv("RBF_AR_PER_SM")) : 2;
+    c->ar_grid = (coop && per_sm > 0) ? sms * (per_sm < ar_per_sm ? per_sm : ar_per_sm) : 0;
     if (getenv("RBF_NO_FUSED_ARNOLDI")) c->ar_grid = 0;
     if (c->ar_grid > 0 && (long long)c->ar_grid * kArThreads * kArE < n) c->ar_grid = 0;
     if (c->ar_grid > 0) {

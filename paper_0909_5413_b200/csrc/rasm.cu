@@ -92,7 +92,9 @@ struct TileShape {
   }
   __host__ __device__ bool fits_tc() const { return T <= kTcMaxTiles && n1p <= 32; }
   __host__ __device__ size_t smem_bytes() const {
-    return ((size_t)T * (T + 1) / 2 * 64 + (size_t)T * 8) * 8 + (size_t)N * sizeof(double2);
+    // tiles + rdiag + max(positions, the S^-1 phase's 10 M tiles + 1 scratch tile)
+    const size_t pos_or_m = (size_t)N * sizeof(double2) > 11 * 64 * 8 ? (size_t)N * sizeof(double2) : 11 * 64 * 8;
+    return ((size_t)T * (T + 1) / 2 * 64 + (size_t)T * 8) * 8 + pos_or_m;
   }
 };
 
@@ -403,7 +405,6 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
   PROBE(2)
   // ---- W = L21 L11^-1 (warps 0..T1-1, one own tile row each, right to left) and
   //      S^-1 = L22^-T L22^-1 (the other warps; lane = row, one column at a time)
-  double sinv[4];
   if (warp < T1) {
     const int it = T0 + warp;
     double *Wrow = sm + toff(it, 0);
@@ -446,52 +447,68 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
       *reinterpret_cast<double2 *>(Ct + frag_acc(lane)) = make_double2(d0, d1);
       __syncwarp();
     }
-  } else {
-    auto L22 = [&](int i, int j) -> double {
-      return sm[toff(T0 + (i >> 3), T0 + (j >> 3)) + swz(i & 7, j & 7)];
+  } else if (warp == T1) {
+    // S^-1 = L22^-T L22^-1 on tiles with the tensor cores (one warp, a few dozen DMMA):
+    //   M = L22^-1:  M(a,a) = L_a^-1 (already formed by the diagonal factorization),
+    //                M(a,b) = -L_a^-1 sum_{k=b}^{a-1} L22(a,k) M(k,b),   a > b;
+    //   S^-1(a,b) = sum_{k>=a} M(k,a)^T M(k,b),   a >= b  (row a last touches L_a^-1,
+    //   so each row's diagonal tile is written last, over the L_a / L_a^-1 storage).
+    // M lives in the positions buffer (dead after the factorization) + one scratch tile.
+    double *Mt = reinterpret_cast<double *>(pos);
+    double *scr = Mt + 10 * 64;
+    auto mt = [&](int a, int b) { return Mt + ((a * (a + 1)) / 2 + b) * 64; };
+    const int m_ = lane >> 2, q_ = lane & 3;
+    // Linv_a fragments: as A (A[m][k] = Linv[m][k]) or B (B[k][n] = Linv[k][n]); Linv[r][c]
+    // (r > c) is stored at (c, r) of the diagonal tile, 1 / L_rr in rdiag.
+    auto linvA = [&](int a, int h) -> double {
+      const double *D = sm + toff(T0 + a, T0 + a);
+      const int kk = 4 * h + q_;
+      return (m_ > kk) ? D[swz(kk, m_)] : (m_ == kk ? rdiag[(T0 + a) * 8 + m_] : 0.0);
     };
-    const int n1p = S.n1p;
-    const int nsw = kTcWarps - T1;  // warps solving for columns of S^-1
-    const double rd = (lane < n1p) ? rdiag[T0 * 8 + lane] : 1.0;  // 1 / L22[lane][lane]
-    // this warp's columns c = warp - T1 + sl * nsw, all advanced together (ILP)
-    double acc1[4], yv[4];
+    auto linvB = [&](int a, int h) -> double {
+      const double *D = sm + toff(T0 + a, T0 + a);
+      const int kk = 4 * h + q_;
+      return (kk > m_) ? D[swz(m_, kk)] : (kk == m_ ? rdiag[(T0 + a) * 8 + kk] : 0.0);
+    };
+    auto linvT = [&](int a, int h) -> double {  // A[m][k] = Linv[k][m] (transposed)
+      const double *D = sm + toff(T0 + a, T0 + a);
+      const int kk = 4 * h + q_;
+      return (kk > m_) ? D[swz(m_, kk)] : (kk == m_ ? rdiag[(T0 + a) * 8 + m_] : 0.0);
+    };
+    for (int a = 1; a < T1; ++a) {
+      for (int b = a - 1; b >= 0; --b) {
+        double d0 = 0.0, d1 = 0.0;
+        for (int k = b; k < a; ++k) {
+          const double *La = sm + toff(T0 + a, T0 + k);
 #pragma unroll
-    for (int sl = 0; sl < 4; ++sl) {
-      const int c = warp - T1 + sl * nsw;
-      acc1[sl] = (lane == c) ? 1.0 : 0.0;
-      yv[sl] = 0.0;
-    }
-    for (int i = 0; i < n1p; ++i) {  // L22 y = e_c
-      const double lli = (lane > i && lane < n1p) ? L22(lane, i) : 0.0;
+          for (int h = 0; h < 2; ++h)
+            dmma(d0, d1, La[frag_rowk(lane, h)], k == b ? linvB(b, h) : mt(k, b)[frag_colk(lane, h)]);
+        }
+        *reinterpret_cast<double2 *>(scr + frag_acc(lane)) = make_double2(d0, d1);
+        __syncwarp();
+        double e0 = 0.0, e1 = 0.0;
 #pragma unroll
-      for (int sl = 0; sl < 4; ++sl) {
-        if (lane == i) yv[sl] = acc1[sl] * rd;
-        const double yi = __shfl_sync(0xffffffffu, yv[sl], i);
-        acc1[sl] = fma(-lli, yi, acc1[sl]);
+        for (int h = 0; h < 2; ++h) dmma(e0, e1, linvA(a, h), scr[frag_colk(lane, h)]);
+        __syncwarp();
+        *reinterpret_cast<double2 *>(mt(a, b) + frag_acc(lane)) = make_double2(-e0, -e1);
+        __syncwarp();
       }
     }
+    for (int a = 0; a < T1; ++a) {
+      for (int bb = 0; bb <= a; ++bb) {  // the row's diagonal tile last
+        double d0 = 0.0, d1 = 0.0;
+        for (int k = a; k < T1; ++k) {
 #pragma unroll
-    for (int sl = 0; sl < 4; ++sl) {
-      acc1[sl] = yv[sl];
-      sinv[sl] = 0.0;
-    }
-    for (int i = n1p - 1; i >= 0; --i) {  // L22^T x = y
-      const double lil = (lane < i) ? L22(i, lane) : 0.0;
-#pragma unroll
-      for (int sl = 0; sl < 4; ++sl) {
-        if (lane == i) sinv[sl] = acc1[sl] * rd;
-        const double xi = __shfl_sync(0xffffffffu, sinv[sl], i);
-        acc1[sl] = fma(-lil, xi, acc1[sl]);
+          for (int h = 0; h < 2; ++h) {
+            const double av = (k == a) ? linvT(a, h) : mt(k, a)[frag_colk(lane, h)];
+            const double bv = (k == bb) ? linvB(bb, h) : mt(k, bb)[frag_colk(lane, h)];
+            dmma(d0, d1, av, bv);
+          }
+        }
+        __syncwarp();
+        *reinterpret_cast<double2 *>(sm + toff(T0 + a, T0 + bb) + frag_acc(lane)) = make_double2(d0, d1);
+        __syncwarp();
       }
-    }
-  }
-  __syncthreads();
-  if (warp >= T1) {  // S^-1 (symmetric) -> lower half of the L22 tiles
-#pragma unroll
-    for (int sl = 0; sl < 4; ++sl) {
-      const int c = warp - T1 + sl * (kTcWarps - T1);
-      if (c < S.n1p && lane >= c && lane < S.n1p)
-        sm[toff(T0 + (lane >> 3), T0 + (c >> 3)) + swz(lane & 7, c & 7)] = sinv[sl];
     }
   }
   __syncthreads();
@@ -763,8 +780,7 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
   RBF_TRY(dalloc(c, (void **)&c->X, sizeof(double) * (size_t)(total > 0 ? total : 2), s));
   if (ncl > 0 && c->nsub > hc[3]) {
     const int Tmax = hc[4];
-    const size_t smem = ((size_t)Tmax * (Tmax + 1) / 2 * 64 + (size_t)Tmax * 8) * 8 +
-                        (size_t)Tmax * 8 * sizeof(double2);
+    const size_t smem = TileShape(Tmax * 8, 0).smem_bytes();  // N = 8 Tmax
     RBF_CUDA_TRY(cudaFuncSetAttribute(k_rasm_setup_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
     k_rasm_setup_tc<<<ncl, kTcThreads, smem, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off,
