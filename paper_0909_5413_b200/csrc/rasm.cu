@@ -557,10 +557,43 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
 
 // Global-memory local solve for subdomains whose factor does not fit in shared
 // memory, and for cells whose Cholesky broke down (reading Q11): LU with partial
-// pivoting (largest |a|, lowest row on ties) of the full A_c in factor order, then
-// A_c Z = E_own by forward/back substitution; X_c = Z^T.  One CTA per cell, the
-// matrix lives in a per-CTA slice of a global workspace (L2-resident).
+// pivoting (largest |a|, lowest row on ties) of the augmented matrix [A_c | E_own]
+// in factor order, then back substitution U Z = L^-1 P E_own; X_c = Z^T.
+//
+// Right-looking and blocked by kLuNb columns so that the trailing matrix is read
+// and written once per panel instead of once per column: (1) the panel is factored
+// in a transposed copy PT (kLuNb x n, coalesced column access), whole rows are
+// swapped eagerly in A; (2) one pass over the remaining columns does the unit-lower
+// solve U12 = L11^-1 A12 and the rank-kLuNb update A22 -= L21 U12 with the U12
+// column in registers and L21 rows broadcast from shared memory.  The back
+// substitution is blocked the same way.  One CTA per cell; A (n x lda, lda = n +
+// n_own) and PT live in a per-CTA slice of a global workspace (L2).
 constexpr int kLuThreads = 512;
+constexpr int kLuNb = 32;     // panel width
+constexpr int kLuRows = 64;   // L21 rows staged in shared memory per pass
+
+__device__ __forceinline__ void lu_argmax(double v, int i, double *red_v, int *red_i, int *out) {
+  // CTA reduction: largest value, lowest index on ties; result in *out (shared)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, i, o);
+    if (v2 > v || (v2 == v && i2 < i)) { v = v2; i = i2; }
+  }
+  if (lane == 0) { red_v[warp] = v; red_i[warp] = i; }
+  __syncthreads();
+  if (warp == 0) {
+    v = (lane < (int)(blockDim.x >> 5)) ? red_v[lane] : -1.0;
+    i = (lane < (int)(blockDim.x >> 5)) ? red_i[lane] : 0x7fffffff;
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, i, o);
+      if (v2 > v || (v2 == v && i2 < i)) { v = v2; i = i2; }
+    }
+    if (lane == 0) *out = (v > 0.0) ? i : -1;
+  }
+  __syncthreads();
+}
 
 __global__ __launch_bounds__(kLuThreads) void k_rasm_setup_lu(
     Geom g, Strip st, const double2 *__restrict__ xy, const int *__restrict__ cell_start,
@@ -570,95 +603,187 @@ __global__ __launch_bounds__(kLuThreads) void k_rasm_setup_lu(
   __shared__ double red_v[kLuThreads / 32];
   __shared__ int red_i[kLuThreads / 32];
   __shared__ int s_piv;
-  const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ double Ls[kLuRows][kLuNb + 1];  // staged L21 / U rows (+1: no bank conflicts)
+  __shared__ double L11[kLuNb][kLuNb + 1];
+  __shared__ double prow[kLuNb];
+  const int tid = threadIdx.x, T = blockDim.x;
   if ((int)blockIdx.x >= count) return;
   const int cl = glist[first + blockIdx.x];
   const int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
   if (tid == 0) block_runs(g, cell_start, cx, cy, R);
   __syncthreads();
   const int n = R.n_ov, n_own = R.n_own, n0 = n - n_own, own_nat = R.own_nat_lo;
-  double *A = ws + (long long)blockIdx.x * ws_stride;  // n x n row-major
-  double *Z = A + (long long)n * n;                    // n x n_own row-major
-  double2 *pos = reinterpret_cast<double2 *>(A + (((long long)n * n + (long long)n * n_own + 1) & ~1LL));
+  const long long lda = n + n_own;
+  double *A = ws + (long long)blockIdx.x * ws_stride;  // n x lda row-major: [A_c | E_own]
+  double *PT = A + (long long)n * lda;                 // kLuNb x n: transposed panel
+  double2 *pos = reinterpret_cast<double2 *>(A + (((long long)n * lda + (long long)kLuNb * n + 1) & ~1LL));
   for (int p = tid; p < n; p += T) {
-    int q = (p < n0) ? (p < own_nat ? p : p + n_own) : own_nat + (p - n0);
+    const int q = (p < n0) ? (p < own_nat ? p : p + n_own) : own_nat + (p - n0);
     pos[p] = xy[nat_to_global(R, q) - st.ext_lo];
   }
   __syncthreads();
-  for (long long t = tid; t < (long long)n * n; t += T) {
-    const int i = (int)(t / n), j = (int)(t - (long long)i * n);
-    const double dx = pos[i].x - pos[j].x, dy = pos[i].y - pos[j].y;
-    const double r2 = fma(dx, dx, dy * dy);
-    A[t] = (r2 < g.rc2) ? exp(r2 * g.neg_inv_2s2) * g.norm : 0.0;
-  }
-  for (long long t = tid; t < (long long)n * n_own; t += T) {
-    const int i = (int)(t / n_own), r = (int)(t - (long long)i * n_own);
-    Z[t] = (i == n0 + r) ? 1.0 : 0.0;  // E_own in factor order
+  for (long long t = tid; t < (long long)n * lda; t += T) {
+    const int i = (int)(t / lda), j = (int)(t - (long long)i * lda);
+    double v;
+    if (j < n) {
+      const double dx = pos[i].x - pos[j].x, dy = pos[i].y - pos[j].y;
+      const double r2 = fma(dx, dx, dy * dy);
+      v = (r2 < g.rc2) ? exp(r2 * g.neg_inv_2s2) * g.norm : 0.0;
+    } else {
+      v = (i == n0 + (j - n)) ? 1.0 : 0.0;  // E_own in factor order
+    }
+    A[t] = v;
   }
   __syncthreads();
   bool singular = false;
-  for (int k = 0; k < n; ++k) {
-    // pivot: largest |A[i][k]|, i >= k, lowest index on ties
-    double best = -1.0;
-    int bi = n;
-    for (int i = k + tid; i < n; i += T) {
-      const double v = fabs(A[(long long)i * n + k]);
-      if (v > best) { best = v; bi = i; }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      const double v2 = __shfl_xor_sync(0xffffffffu, best, o);
-      const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (v2 > best || (v2 == best && i2 < bi)) { best = v2; bi = i2; }
-    }
-    if (lane == 0) { red_v[warp] = best; red_i[warp] = bi; }
-    __syncthreads();
-    if (tid == 0) {
-      double b = red_v[0];
-      int ii = red_i[0];
-      for (int w = 1; w < T / 32; ++w)
-        if (red_v[w] > b || (red_v[w] == b && red_i[w] < ii)) { b = red_v[w]; ii = red_i[w]; }
-      s_piv = (b > 0.0) ? ii : -1;
+  for (int k0 = 0; k0 < n && !singular; k0 += kLuNb) {
+    const int kb = n - k0 < kLuNb ? n - k0 : kLuNb;
+    // ---- panel: PT[c][i] = A[i][k0 + c], rows i >= k0
+    for (long long t = tid; t < (long long)kb * (n - k0); t += T) {
+      const int c = (int)(t / (n - k0)), i = k0 + (int)(t - (long long)c * (n - k0));
+      PT[(long long)c * n + i] = A[(long long)i * lda + k0 + c];
     }
     __syncthreads();
-    const int p = s_piv;
-    if (p < 0) { singular = true; break; }
-    if (p != k) {  // swap rows k and p of A and of the right-hand sides
-      for (int j = tid; j < n; j += T) {
-        const double t = A[(long long)k * n + j];
-        A[(long long)k * n + j] = A[(long long)p * n + j];
-        A[(long long)p * n + j] = t;
+    for (int c = 0; c < kb; ++c) {
+      const int kk = k0 + c;
+      double best = -1.0;
+      int bi = 0x7fffffff;
+      for (int i = kk + tid; i < n; i += T) {
+        const double v = fabs(PT[(long long)c * n + i]);
+        if (v > best) { best = v; bi = i; }
       }
-      for (int r = tid; r < n_own; r += T) {
-        const double t = Z[(long long)k * n_own + r];
-        Z[(long long)k * n_own + r] = Z[(long long)p * n_own + r];
-        Z[(long long)p * n_own + r] = t;
+      lu_argmax(best, bi, red_v, red_i, &s_piv);
+      const int p = s_piv;
+      if (p < 0) { singular = true; break; }
+      if (p != kk) {  // swap rows kk and p: the panel copy and the rest of the augmented row
+        for (int cc = tid; cc < kb; cc += T) {
+          const double t0 = PT[(long long)cc * n + kk];
+          PT[(long long)cc * n + kk] = PT[(long long)cc * n + p];
+          PT[(long long)cc * n + p] = t0;
+        }
+        for (long long j = tid; j < lda; j += T) {
+          if (j >= k0 && j < k0 + kb) continue;
+          const double t0 = A[(long long)kk * lda + j];
+          A[(long long)kk * lda + j] = A[(long long)p * lda + j];
+          A[(long long)p * lda + j] = t0;
+        }
       }
+      __syncthreads();
+      if (tid < kb) prow[tid] = PT[(long long)tid * n + kk];  // pivot row, panel part
+      __syncthreads();
+      const double inv = 1.0 / prow[c];
+      for (int i = kk + 1 + tid; i < n; i += T) {
+        const double l = PT[(long long)c * n + i] * inv;
+        PT[(long long)c * n + i] = l;
+        for (int cc = c + 1; cc < kb; ++cc) PT[(long long)cc * n + i] = fma(-l, prow[cc], PT[(long long)cc * n + i]);
+      }
+      __syncthreads();
+    }
+    if (singular) break;
+    // write the factored panel back (L below the diagonal, U on and above it)
+    for (long long t = tid; t < (long long)kb * (n - k0); t += T) {
+      const int c = (int)(t / (n - k0)), i = k0 + (int)(t - (long long)c * (n - k0));
+      A[(long long)i * lda + k0 + c] = PT[(long long)c * n + i];
+    }
+    for (int t = tid; t < kb * kb; t += T) {  // L11 (unit lower) to shared memory
+      const int r = t / kb, c = t - r * kb;
+      L11[r][c] = (c < r) ? PT[(long long)c * n + k0 + r] : 0.0;
     }
     __syncthreads();
-    const double inv = 1.0 / A[(long long)k * n + k];
-    const int m = n - 1 - k;
-    for (long long t = tid; t < (long long)m * (m + n_own); t += T) {
-      const int i = k + 1 + (int)(t / (m + n_own));
-      const int jj = (int)(t % (m + n_own));
-      const double l = A[(long long)i * n + k] * inv;
-      if (jj < m) A[(long long)i * n + k + 1 + jj] -= l * A[(long long)k * n + k + 1 + jj];
-      else Z[(long long)i * n_own + (jj - m)] -= l * Z[(long long)k * n_own + (jj - m)];
+    // ---- U12 = L11^-1 A12 and A22 -= L21 U12, one column per thread (U12 column in
+    //      registers), L21 rows staged in shared memory, kLuRows at a time
+    const int j0 = k0 + kb;
+    for (long long jb = j0; jb < lda; jb += T) {
+      const long long j = jb + tid;
+      const bool act = j < lda;
+      double u[kLuNb];
+#pragma unroll
+      for (int t = 0; t < kLuNb; ++t) u[t] = (act && t < kb) ? A[(long long)(k0 + t) * lda + j] : 0.0;
+#pragma unroll
+      for (int r = 1; r < kLuNb; ++r)
+#pragma unroll
+        for (int t = 0; t < r; ++t) u[r] = fma(-L11[r][t], u[t], u[r]);
+      if (act)
+#pragma unroll
+        for (int t = 0; t < kLuNb; ++t)
+          if (t < kb) A[(long long)(k0 + t) * lda + j] = u[t];
+      for (int i0 = j0; i0 < n; i0 += kLuRows) {
+        const int nr = n - i0 < kLuRows ? n - i0 : kLuRows;
+        __syncthreads();
+        for (int t = tid; t < nr * kLuNb; t += T) {
+          const int r = t / kLuNb, c = t - r * kLuNb;
+          Ls[r][c] = (c < kb) ? PT[(long long)c * n + i0 + r] : 0.0;
+        }
+        __syncthreads();
+        if (act) {
+          for (int r = 0; r < nr; ++r) {
+            double a = A[(long long)(i0 + r) * lda + j];
+#pragma unroll
+            for (int t = 0; t < kLuNb; ++t) a = fma(-Ls[r][t], u[t], a);
+            A[(long long)(i0 + r) * lda + j] = a;
+          }
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
   if (singular) {
     if (tid == 0) atomicMin(fail_key, cy * g.ncx + cx);
     return;
   }
-  // back substitution U Z = (L^-1 P E_own), column-oriented
-  for (int k = n - 1; k >= 0; --k) {
-    const double inv = 1.0 / A[(long long)k * n + k];
+  __syncthreads();
+  // ---- back substitution U Z = Y on the n_own right-hand-side columns (A[:, n:]),
+  //      blocks of kLuNb rows from the bottom; threads = (column, row group)
+  const int ngrp = T / (n_own > 0 ? n_own : 1) > 0 ? T / n_own : 1;
+  for (int r0 = ((n - 1) / kLuNb) * kLuNb; r0 >= 0; r0 -= kLuNb) {
+    const int kb = n - r0 < kLuNb ? n - r0 : kLuNb;
     __syncthreads();
-    for (int r = tid; r < n_own; r += T) Z[(long long)k * n_own + r] *= inv;
+    for (int t = tid; t < kb * kb; t += T) {  // U block (upper incl. diagonal)
+      const int r = t / kb, c = t - r * kb;
+      L11[r][c] = (c >= r) ? A[(long long)(r0 + r) * lda + r0 + c] : 0.0;
+    }
     __syncthreads();
-    for (long long t = tid; t < (long long)k * n_own; t += T) {
-      const int i = (int)(t / n_own), r = (int)(t - (long long)i * n_own);
-      Z[(long long)i * n_own + r] -= A[(long long)i * n + k] * Z[(long long)k * n_own + r];
+    if (tid < n_own) {  // solve the diagonal block for this column
+      const long long j = n + tid;
+      double z[kLuNb];
+#pragma unroll
+      for (int t = 0; t < kLuNb; ++t) z[t] = t < kb ? A[(long long)(r0 + t) * lda + j] : 0.0;
+#pragma unroll
+      for (int r = kLuNb - 1; r >= 0; --r) {
+        if (r < kb) {
+          double a = z[r];
+#pragma unroll
+          for (int t = r + 1; t < kLuNb; ++t) a = fma(-L11[r][t], z[t], a);
+          z[r] = a / L11[r][r];
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < kLuNb; ++t)
+        if (t < kb) A[(long long)(r0 + t) * lda + j] = z[t];
+    }
+    __syncthreads();
+    // rows above: Y[i] -= U[i, r0:r0+kb] z, columns x row groups
+    const int jc = tid % (n_own > 0 ? n_own : 1), grp = tid / (n_own > 0 ? n_own : 1);
+    const bool act = n_own > 0 && grp < ngrp;
+    double z[kLuNb];
+#pragma unroll
+    for (int t = 0; t < kLuNb; ++t) z[t] = (act && t < kb) ? A[(long long)(r0 + t) * lda + n + jc] : 0.0;
+    for (int i0 = 0; i0 < r0; i0 += kLuRows) {
+      const int nr = r0 - i0 < kLuRows ? r0 - i0 : kLuRows;
+      __syncthreads();
+      for (int t = tid; t < nr * kLuNb; t += T) {
+        const int r = t / kLuNb, c = t - r * kLuNb;
+        Ls[r][c] = (c < kb) ? A[(long long)(i0 + r) * lda + r0 + c] : 0.0;
+      }
+      __syncthreads();
+      if (act) {
+        for (int r = grp; r < nr; r += ngrp) {
+          double a = A[(long long)(i0 + r) * lda + n + jc];
+#pragma unroll
+          for (int t = 0; t < kLuNb; ++t) a = fma(-Ls[r][t], z[t], a);
+          A[(long long)(i0 + r) * lda + n + jc] = a;
+        }
+      }
     }
   }
   __syncthreads();
@@ -672,7 +797,7 @@ __global__ __launch_bounds__(kLuThreads) void k_rasm_setup_lu(
       if (q < own_nat) pp = q;
       else if (q < own_nat + n_own) pp = n0 + (q - own_nat);
       else pp = q - n_own;
-      v = Z[(long long)pp * n_own + o];
+      v = A[(long long)pp * lda + n + o];
     }
     Xc[t] = v;
   }
@@ -796,8 +921,8 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
     int *fail = cnt + 4;
     RBF_CUDA_TRY(cudaMemcpyAsync(fail, &hfail, sizeof(int), cudaMemcpyHostToDevice, s));
     const long long n = c->max_ov, no = c->max_own;
-    const long long stride = (((n * n + n * no + 1) & ~1LL) + 2 * n + 1) & ~1LL;
-    const long long budget = 4LL << 30;  // bytes of workspace per batch
+    const long long stride = (((n * (n + no) + (long long)kLuNb * n + 1) & ~1LL) + 2 * n + 1) & ~1LL;
+    const long long budget = 8LL << 30;  // bytes of workspace per batch
     long long batch = budget / (stride * 8);
     if (batch < 1) batch = 1;
     if (batch > nglobal) batch = nglobal;

@@ -83,6 +83,22 @@ def test_rasm_apply_parity(wl):
     assert rel(z, ref) <= 1e-10
 
 
+@pytest.mark.parametrize("rings,jit", [(2, 0.1), (3, 0.0)])
+def test_rasm_apply_parity_lu_path(rings, jit):
+    """Two and three rings of overlap: 625- and 1225-point subdomains exceed the
+    shared-memory tensor-core kernel and take the blocked global-memory LU path
+    (reading Q11; partial pivoting, largest |a|, lowest row on ties)."""
+    wl = W.make_lattice(48, jitter_frac=jit, seed=5)
+    r = np.random.default_rng(21).standard_normal(wl.n)
+    Pc = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, rings)
+    ref = Pc.apply(r)
+    Pc.close()
+    with ctx_for(wl, rings=rings) as c:
+        assert c.info()["n_lu"] > 0
+        z = to_caller(c, c.rasm_apply(c.to_local(torch.from_numpy(r).cuda())))
+    assert rel(z, ref) <= 1e-10
+
+
 def test_rasm_block_jacobi_parity():
     wl = W.make_lattice(30, jitter_frac=0.1, seed=2)
     r = np.random.default_rng(3).standard_normal(wl.n)
