@@ -31,7 +31,7 @@ sys.path.insert(0, ROOT)
 import rbf_workloads as W  # noqa: E402
 
 METRIC = "fp64 GMRES+RASM solve time and matvec Gpairs/s at 1/2/4/8 B200, % FP64 peak"
-FP64_PEAK_TFLOPS = 33.96  # measured DFMA peak on this pool's B200 (profiles/r01_fp64_peak.json)
+FP64_PEAK_TFLOPS = 36.86  # measured DFMA peak on this pool's B200 (profiles/r01_fp64_peak.json, tools/clock_under_load.cu)
 FLOP_PER_PAIR = 38        # algorithmic flops per in-cutoff pair
 SAMPLE_SIDE = 256         # oracle sample: 256^2 points of the same recipe
 
