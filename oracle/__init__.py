@@ -55,6 +55,8 @@ def lib():
         L.orc_assemble_dense.argtypes = [i64, ptr, dbl, dbl, ptr]
         L.orc_matvec_brute.argtypes = [i64, ptr, ptr, dbl, dbl, C.c_int, i64, ptr, ptr]
         L.orc_neglected_row_mass.argtypes = [i64, ptr, dbl, dbl, i64, ptr, ptr]
+        L.orc_evaluate.argtypes = [i64, ptr, i64, ptr, ptr, dbl, dbl, C.c_int, ptr]
+        L.orc_evaluate.restype = None
         L.orc_grid_dims.argtypes = [dbl, dbl, dbl, dbl, dbl, ptr, ptr]
         L.orc_cell_list.argtypes = [i64, ptr, dbl, dbl, dbl, dbl, dbl, ptr, ptr, ptr]
         L.orc_matvec_cells.restype = C.c_int
@@ -139,6 +141,19 @@ def matvec_brute(xy, w, sigma: float, rc: float | None, rows=None) -> np.ndarray
         lib().orc_matvec_brute(n, _p(xy), _p(w), float(sigma), 0.0 if exact else float(rc),
                                int(exact), rows.shape[0], _p(rows), _p(y))
     return y
+
+
+def evaluate(q, xy, lam, sigma: float, rc: float | None) -> np.ndarray:
+    """Interpolant s(q) = sum_j [|q - x_j| < rc] lambda_j phi(|q - x_j|^2) at query
+    points q (Eq.(1), Eq.(12)), brute force.  rc=None: the
+    untruncated sum.  Pinned by tests/test_oracle_kernel_matvec.py (queries at the
+    data points reproduce matvec_brute rows; Poisson summation for constant weights)."""
+    q, xy, lam = _f64(q), _f64(xy), _f64(lam)
+    s = np.empty(q.shape[0], dtype=np.float64)
+    exact = rc is None
+    lib().orc_evaluate(q.shape[0], _p(q), xy.shape[0], _p(xy), _p(lam), float(sigma),
+                       0.0 if exact else float(rc), int(exact), _p(s))
+    return s
 
 
 def neglected_row_mass(xy, sigma: float, rc: float, rows) -> np.ndarray:

@@ -101,6 +101,26 @@ void orc_matvec_brute(int64_t n, const double *xy, const double *w, double sigma
   }
 }
 
+/* Interpolant evaluation s(q_k) = sum_{j=0..n-1} [r2 < rc^2] lambda_j phi(r2), r2 =
+ * |q_k - x_j|^2 (Eq.(1) P:76-79 with the Gaussian of Eq.(12) and the truncation of
+ * reading Q1), brute force over all j in ascending order.  exact != 0
+ * drops the indicator.  At q_k = x_k this is row k of orc_matvec_brute. */
+void orc_evaluate(int64_t m, const double *q, int64_t n, const double *xy, const double *lam,
+                  double sigma, double rc, int exact, double *s) {
+  double rc2 = rc * rc;
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t k = 0; k < m; ++k) {
+    double acc = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+      double dx = q[2 * k] - xy[2 * j];
+      double dy = q[2 * k + 1] - xy[2 * j + 1];
+      double r2 = fma(dx, dx, dy * dy);
+      if (exact || r2 < rc2) acc += lam[j] * orc_phi(sigma, r2);
+    }
+    s[k] = acc;
+  }
+}
+
 /* Neglected row mass sum_{j: r2_ij >= rc^2} phi(r2_ij), brute force. */
 void orc_neglected_row_mass(int64_t n, const double *xy, double sigma, double rc,
                             int64_t nrows, const int64_t *rows, double *out) {

@@ -174,3 +174,40 @@ def test_dense_assembly_symmetric_spd():
     Ae = O.assemble_dense(wl.xy, wl.sigma, None)
     assert np.array_equal(Ae, Ae.T)
     assert np.all(Ae >= A)
+
+
+# ------------------------------------------------------------------ interpolant evaluation (§8.f1)
+
+def _theta_shift(h, s, d):
+    """h sum_m G_s,1D(mh - d) = 1 + 2 sum_k exp(-2 pi^2 s^2 k^2 / h^2) cos(2 pi k d / h)
+    (Poisson summation of a 1-D normalised Gaussian sampled on a shifted lattice)."""
+    return 1.0 + 2.0 * sum(math.exp(-2.0 * math.pi ** 2 * s * s * k * k / (h * h)) *
+                           math.cos(2.0 * math.pi * k * d / h) for k in range(1, 8))
+
+
+def test_evaluate_at_data_points_is_matvec_row():
+    wl = W.make_lattice(30, jitter_frac=0.2, seed=4)
+    lam = np.random.default_rng(5).standard_normal(wl.n)
+    rows = np.array([0, 17, 450, wl.n - 1])
+    s = O.evaluate(wl.xy[rows], wl.xy, lam, wl.sigma, wl.rc)
+    assert np.array_equal(s, O.matvec_brute(wl.xy, lam, wl.sigma, wl.rc, rows=rows))
+    s_ex = O.evaluate(wl.xy[rows], wl.xy, lam, wl.sigma, None)
+    assert np.array_equal(s_ex, O.matvec_brute(wl.xy, lam, wl.sigma, None, rows=rows))
+
+
+def test_evaluate_constant_weights_poisson_off_lattice():
+    """lambda_j = h^2 on the cfg1 lattice: s(q) = theta(dx) theta(dy) (exact sum) at
+    interior queries off the lattice, the truncated sum below it by at most the tail."""
+    wl = W.config(1)
+    h = wl.meta["h"]
+    lam = np.full(wl.n, h * h)
+    rng = np.random.default_rng(6)
+    q = rng.uniform(-0.3, 0.3, size=(40, 2))
+    s_ex = O.evaluate(q, wl.xy, lam, wl.sigma, None)
+    s_ct = O.evaluate(q, wl.xy, lam, wl.sigma, wl.rc)
+    # lattice x_i = -1 + (i + 1/2) h: offset of q from the lattice
+    d = np.mod(q + 1.0 - 0.5 * h, h)
+    expect = np.array([_theta_shift(h, wl.sigma, dx) * _theta_shift(h, wl.sigma, dy) for dx, dy in d])
+    assert np.max(np.abs(s_ex - expect)) <= 1e-14  # 10^4-term sum of O(1) values
+    gap = s_ex - s_ct
+    assert np.all(gap >= 0.0) and np.all(gap <= 3e-8)  # tail e^-18-scale mass (S:333)
