@@ -180,6 +180,17 @@ int rbf_interpolate_host(const double *xy_host, const double *f_host, int64_t n,
                          const rbf_params *p, const rbf_gmres_params *g,
                          double *lambda_host, rbf_report *rep, void *stream);
 
+/* Interpolant evaluation (the paper's application):
+ *   s(q_k) = sum_{j : |q_k - x_j| < rc} lambda_j exp(-|q_k - x_j|^2/(2 sigma^2)) / (2 pi sigma^2)
+ * (Eq.(1) P:76-79 with Eq.(12) and the truncation of reading Q1).
+ *  q_xy_dev        m x 2 interleaved query points (any order), inside the box.
+ *  lambda_loc_dev  weights, rank-local library order (e.g. rbf_solve's output).
+ *  s_dev           m values, in the order of the queries.
+ * Single-rank contexts only (RBF_EUNSUPPORTED otherwise); EINVAL for a query that is
+ * non-finite or outside the box (message names the first one).  Synchronises. */
+int rbf_evaluate(rbf_ctx *ctx, const double *q_xy_dev, int64_t m, const double *lambda_loc_dev,
+                 double *s_dev, void *stream);
+
 /* In-cutoff pair count of this rank's rows (for Gpairs/s; synchronises). */
 int rbf_count_pairs(rbf_ctx *ctx, int64_t *n_pairs, void *stream);
 

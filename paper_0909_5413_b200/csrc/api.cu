@@ -412,6 +412,12 @@ int rbf_solve(rbf_ctx *c, const double *f, const rbf_gmres_params *g, double *la
   return st;
 }
 
+int rbf_evaluate(rbf_ctx *c, const double *q, int64_t m, const double *lam, double *s, void *stream) {
+  if (!c || (m > 0 && (!q || !lam || !s))) { set_error("rbf_evaluate: NULL argument"); return RBF_EINVAL; }
+  if (m < 0) { set_error("rbf_evaluate: m < 0"); return RBF_EINVAL; }
+  return evaluate(c, q, m, lam, s, (cudaStream_t)stream);
+}
+
 int rbf_count_pairs(rbf_ctx *c, int64_t *np, void *stream) {
   if (!c || !np) { set_error("NULL argument"); return RBF_EINVAL; }
   long long v = 0;

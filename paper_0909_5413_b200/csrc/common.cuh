@@ -117,6 +117,49 @@ __device__ __forceinline__ double exp_neg(double x) {
   return __hiloint2double(__double2hiint(e) + ((k >> 6) << 20), __double2loint(e));
 }
 
+// ---------------------------------------------------------------------------
+// Table-free exp for the cutoff Gaussian (matvec, evaluation); reading Q15.
+// ---------------------------------------------------------------------------
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer shifter
+
+// 2^f = 1 + f P(f) on [-1/2, 1/2]: minimax P (Remez on the relative error, DESIGN.md
+// §6), highest coefficient first.  Degree 10: max error 1.5e-16; degree 9: 3.9e-16.
+static __constant__ double kExp2P10[11] = {4.078071929588337e-10, 7.072570412814423e-09,
+                                    1.0180647659234139e-07, 1.3215442675329823e-06,
+                                    1.5252727385193868e-05, 0.0001540353044157213,
+                                    0.0013333558153439966, 0.009618129107607003,
+                                    0.05550410866479039, 0.24022650695910097,
+                                    0.6931471805599457};
+static __constant__ double kExp2P9[10] = {7.111758687557852e-09, 1.0210506458816145e-07,
+                                   1.321523563477604e-06, 1.525264774769592e-05,
+                                   0.00015403530800818256, 0.001333355824648072,
+                                   0.009618129107380715, 0.05550410866434658,
+                                   0.24022650695910472, 0.6931471805599516};
+
+// exp(-r2/(2 sigma^2)) for 0 <= r2 < rc^2 (rc <= 37 sigma, so the result is a normal
+// number > 2^-990 and no underflow guard is needed).  esc = -log2(e)/(2 sigma^2).
+template <int DEG>
+__device__ __forceinline__ double gauss_exp2(double r2, double esc) {
+  const double t = fma(r2, esc, kMagic);
+  const double kd = t - kMagic;
+  const int k = __double2loint(t);
+  const double f = fma(r2, esc, -kd);  // exact product, one rounding: |f| <= 1/2
+  const double *P = DEG == 10 ? kExp2P10 : kExp2P9;
+  double p = P[0];
+#pragma unroll
+  for (int i = 1; i <= DEG; ++i) p = fma(p, f, P[i]);
+  const double q = fma(f, p, 1.0);
+  return __hiloint2double(__double2hiint(q) + k * (1 << 20), __double2loint(q));
+}
+
+__device__ __forceinline__ double4 ld_rec(const double4 *p) {  // one 256-bit gather
+  double4 v;
+  asm volatile("ld.global.nc.L1::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+               : "l"(p));
+  return v;
+}
+
 }  // namespace rbf
 
 struct rbf_ctx {
@@ -187,6 +230,10 @@ int launch_local_index(const rbf_ctx *c, int64_t *idx, cudaStream_t s);
 // matvec.cu
 int build_nlist(rbf_ctx *c, cudaStream_t s);
 int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStream_t s);
+int launch_pack_w(const rbf_ctx *c, const double *w_ext, cudaStream_t s);
+
+// evaluate.cu
+int evaluate(rbf_ctx *c, const double *q, long long m, const double *lam, double *out, cudaStream_t s);
 
 // rasm.cu
 int rasm_setup(rbf_ctx *c, cudaStream_t s);

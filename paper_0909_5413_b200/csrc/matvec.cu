@@ -42,45 +42,6 @@ namespace rbf {
 constexpr int kMvWarps = 8;  // target chunks per CTA
 constexpr int kMvThreads = 32 * kMvWarps;
 
-// 2^f = 1 + f P(f) on [-1/2, 1/2]: minimax P (Remez on the relative error, DESIGN.md
-// §6), highest coefficient first.  Degree 10: max error 1.5e-16; degree 9: 3.9e-16.
-__constant__ double kExp2P10[11] = {4.078071929588337e-10, 7.072570412814423e-09,
-                                    1.0180647659234139e-07, 1.3215442675329823e-06,
-                                    1.5252727385193868e-05, 0.0001540353044157213,
-                                    0.0013333558153439966, 0.009618129107607003,
-                                    0.05550410866479039, 0.24022650695910097,
-                                    0.6931471805599457};
-__constant__ double kExp2P9[10] = {7.111758687557852e-09, 1.0210506458816145e-07,
-                                   1.321523563477604e-06, 1.525264774769592e-05,
-                                   0.00015403530800818256, 0.001333355824648072,
-                                   0.009618129107380715, 0.05550410866434658,
-                                   0.24022650695910472, 0.6931471805599516};
-
-constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer shifter
-
-// exp(-r2/(2 sigma^2)) for 0 <= r2 < rc^2 (rc <= 37 sigma, so the result is a normal
-// number > 2^-990 and no underflow guard is needed).  esc = -log2(e)/(2 sigma^2).
-template <int DEG>
-__device__ __forceinline__ double gauss_exp2(double r2, double esc) {
-  const double t = fma(r2, esc, kMagic);
-  const double kd = t - kMagic;
-  const int k = __double2loint(t);
-  const double f = fma(r2, esc, -kd);  // exact product, one rounding: |f| <= 1/2
-  const double *P = DEG == 10 ? kExp2P10 : kExp2P9;
-  double p = P[0];
-#pragma unroll
-  for (int i = 1; i <= DEG; ++i) p = fma(p, f, P[i]);
-  const double q = fma(f, p, 1.0);
-  return __hiloint2double(__double2hiint(q) + k * (1 << 20), __double2loint(q));
-}
-
-__device__ __forceinline__ double4 ld_rec(const double4 *p) {
-  double4 v;
-  asm volatile("ld.global.nc.L1::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];"
-               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
-               : "l"(p));
-  return v;
-}
 
 __device__ __forceinline__ int target_cell(const Geom &g, double2 p, int &cx, int &cy) {
   double tx = floor(__ddiv_rn(__dsub_rn(p.x, g.x0), g.cell));
@@ -306,10 +267,20 @@ int build_nlist(rbf_ctx *c, cudaStream_t s) {
   return RBF_OK;
 }
 
+int launch_pack_w(const rbf_ctx *c, const double *w_ext, cudaStream_t s) {
+  const long long ne = n_ext(c);
+  if (ne > 0) {
+    k_pack_w<<<(int)((ne + 255) / 256), 256, 0, s>>>(w_ext, ne, c->rec);
+    count_launch(1);
+  }
+  RBF_CUDA_TRY(cudaGetLastError());
+  return RBF_OK;
+}
+
 int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStream_t s) {
-  const long long ne = n_ext(c), nl = n_loc(c);
+  const long long nl = n_loc(c);
   if (nl <= 0) return RBF_OK;
-  k_pack_w<<<(int)((ne + 255) / 256), 256, 0, s>>>(w_ext, ne, c->rec);
+  RBF_TRY(launch_pack_w(c, w_ext, s));
   const int G = c->mv_g;
   const long long lanes = (nl + G - 1) / G;
   const int blocks = (int)((lanes + kMvThreads - 1) / kMvThreads);
@@ -324,7 +295,7 @@ int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStre
   else if (c->mv_var == 1) RBF_MV(2, 9, 4, 1);
   else RBF_MV(2, 10, 4, 1);
 #undef RBF_MV
-  count_launch(2);
+  count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
   return RBF_OK;
 }

@@ -56,7 +56,7 @@ EXPORTS = ["rbf_get_nccl_id", "rbf_setup", "rbf_local_count", "rbf_ext_count", "
            "rbf_rasm_apply", "rbf_matvec_ext", "rbf_rasm_apply_ext", "rbf_solve",
            "rbf_interpolate_host", "rbf_count_pairs", "rbf_dot", "rbf_plan_strips",
            "rbf_last_error", "rbf_destroy", "rbf_info", "rbf_launch_count", "rbf_setup_times",
-           "rbf_plan_halo"]
+           "rbf_plan_halo", "rbf_evaluate"]
 
 _lib = None
 
@@ -87,6 +87,7 @@ def lib() -> C.CDLL:
             "rbf_interpolate_host": (C.c_int, [p, p, i64, C.POINTER(Params), C.POINTER(GmresParams),
                                                p, C.POINTER(Report), p]),
             "rbf_count_pairs": (C.c_int, [p, p, p]),
+            "rbf_evaluate": (C.c_int, [p, p, i64, p, p, p]),
             "rbf_dot": (C.c_int, [p, p, p, p, p]),
             "rbf_plan_strips": (C.c_int, [p, i64, i32, i64, p]),
             "rbf_last_error": (C.c_char_p, []),
@@ -254,6 +255,15 @@ class Context:
         y = self._new(self.n_local) if y is None else y
         _check(lib().rbf_matvec(self._h, _ptr(w), _ptr(y), _stream(self._stream)))
         return y
+
+    def evaluate(self, q_xy, lam, s=None):
+        """Interpolant s(q) at query points q_xy (m x 2, device, fp64) from the
+        local weights lam (rbf_evaluate, Eq.(1)); returns s in query order."""
+        m = int(q_xy.shape[0])
+        s = self._new(m) if s is None else s
+        _check(lib().rbf_evaluate(self._h, _ptr(q_xy.contiguous()), m, _ptr(lam), _ptr(s),
+                                  _stream(self._stream)))
+        return s
 
     def rasm_apply(self, r, z=None):
         z = self._new(self.n_local) if z is None else z

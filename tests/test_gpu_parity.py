@@ -406,3 +406,50 @@ def test_cfg5_matvec_sampled_rows():
         npairs = c.count_pairs()
     assert rel(got[rows], oracle_rows(wl, w, rows, cl)) <= 1e-12
     assert npairs == O.count_pairs(wl.xy, wl.rc, wl.box, wl.cell)
+
+
+# ------------------------------------------------------------------ interpolant evaluation (§8.f1)
+
+@pytest.mark.parametrize("wl", SMALL[:3] + [SMALL[4]], ids=IDS[:3] + [IDS[4]])
+def test_evaluate_parity(wl):
+    rng = np.random.default_rng(31)
+    lam = rng.standard_normal(wl.n)
+    x0, y0, x1, y1 = wl.box
+    q = np.column_stack([rng.uniform(x0, x1, 700), rng.uniform(y0, y1, 700)])
+    q = np.vstack([q, [[x0, y0], [x1, y1], [x0, y1]]])  # box corners
+    ref = O.evaluate(q, wl.xy, lam, wl.sigma, wl.rc)
+    with ctx_for(wl, rings=0) as c:
+        s = c.evaluate(torch.from_numpy(q).cuda(), c.to_local(torch.from_numpy(lam).cuda())).cpu().numpy()
+    assert rel(s, ref) <= 1e-12
+
+
+def test_evaluate_at_data_points_is_the_matvec():
+    wl = SMALL[2]
+    lam = np.random.default_rng(32).standard_normal(wl.n)
+    with ctx_for(wl, rings=0) as c:
+        ll = c.to_local(torch.from_numpy(lam).cuda())
+        y = to_caller(c, c.matvec(ll))
+        s = c.evaluate(torch.from_numpy(wl.xy).cuda(), ll).cpu().numpy()
+        with pytest.raises(P.RbfError):
+            c.evaluate(torch.tensor([[0.0, 0.0], [2.5, 0.0]], dtype=torch.float64, device="cuda"), ll)
+        assert c.evaluate(torch.zeros((0, 2), dtype=torch.float64, device="cuda"), ll).numel() == 0
+    assert np.array_equal(s, y)  # same sources, order, arithmetic
+
+
+def test_cfg2_interpolate_onto_lattice(cfg2):
+    """The paper's application: solve on the jittered cfg2 points, evaluate the
+    interpolant on a regular 512 x 512 lattice; sampled queries vs the oracle, and the
+    interpolation conditions s(x_i) = f_i at sampled data points."""
+    wl = cfg2
+    g = np.linspace(-0.999, 0.999, 512)
+    Q = np.stack(np.meshgrid(g, g), axis=-1).reshape(-1, 2)
+    with ctx_for(wl) as c:
+        lam_l, rep = c.solve(c.to_local(torch.from_numpy(wl.f).cuda()), rtol=wl.tol)
+        s = c.evaluate(torch.from_numpy(Q).cuda(), lam_l).cpu().numpy()
+        rows = np.random.default_rng(33).choice(wl.n, 64, replace=False)
+        s_data = c.evaluate(torch.from_numpy(wl.xy[rows]).cuda(), lam_l).cpu().numpy()
+        lam = to_caller(c, lam_l)
+    assert rep.converged
+    pick = np.random.default_rng(34).choice(Q.shape[0], 64, replace=False)
+    assert rel(s[pick], O.evaluate(Q[pick], wl.xy, lam, wl.sigma, wl.rc)) <= 1e-12
+    assert np.max(np.abs(s_data - wl.f[rows])) <= 1e-9 * np.max(np.abs(wl.f))
