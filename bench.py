@@ -36,6 +36,20 @@ FLOP_PER_PAIR = 38        # algorithmic flops per in-cutoff pair (DESIGN.md "Roo
 SAMPLE_SIDE = 256         # oracle sample: 256^2 points of the same recipe
 
 
+def ncu_traffic(kernel_prefix: str):
+    """DRAM bytes per launch of a kernel from the committed ncu --set full capture
+    (profiles/r01_ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+            d = json.load(f)["bytes_per_launch"]
+        for k, v in d.items():
+            if k == kernel_prefix or k.startswith(kernel_prefix + "<"):
+                return float(v)
+    except Exception:
+        pass
+    return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -233,14 +247,19 @@ def run_ours(args, rank, world):
     shares = {"matvec": mv_live, "rasm_apply": pc_live, "orth": orth_live}
     dom = max(("matvec", "rasm_apply"), key=lambda k: shares[k])
     if dom == "rasm_apply":
+        tr = ncu_traffic("k_rasm_apply") if args.config == 2 else None
         roof = {"kernel": "k_rasm_apply", "bound": "hbm", "achieved": pc_gbs, "peak": hbm_peak,
-                "unit": "GB/s", "frac": pc_gbs / hbm_peak, "traffic": None,
+                "unit": "GB/s", "frac": pc_gbs / hbm_peak, "traffic": tr,
+                "traffic_source": "profiles/r01_ncu_traffic.json (cfg2 capture)" if tr else None,
                 "peak_source": hbm_src, "alg_bytes_per_launch": pc_alg_bytes,
                 "ms_per_launch": pc_per_launch_ms}
     else:
+        tr = ncu_traffic("k_matvec") if args.config == 2 else None
         roof = {"kernel": "k_matvec", "bound": "alu", "achieved": mv_tflops,
                 "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": mv_tflops / FP64_PEAK_TFLOPS,
-                "traffic": None, "peak_source": "measured DFMA microbenchmark",
+                "traffic": tr, "traffic_unit": "bytes per launch (DRAM read + write)",
+                "traffic_source": "profiles/r01_ncu_traffic.json (cfg2 capture)" if tr else None,
+                "peak_source": "measured DFMA, tools/clock_under_load.cu",
                 "alg_flops_per_launch": mv_alg_flops, "ms_per_launch": mv_per_launch_ms}
     gpairs = n_pairs_local / (mv_ms * 1e-3) / 1e9
     if world > 1:

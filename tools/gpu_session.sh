@@ -15,6 +15,6 @@ if [ "${NCU:-1}" = "1" ]; then
   echo "launch rc=$?" >> $O/ncu_launch.log
   P="python tools/prof_cfg2.py 2"
   timeout 300 $P > $O/plain2.log 2>&1 && \
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_matvec_ell|k_rasm_apply|k_rasm_setup_tc|k_arnoldi_fused|k_nlist' -c 8 -o $O/prof $P > $O/ncu_full.log 2>&1
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_matvec|k_rasm_apply|k_rasm_setup_tc|k_arnoldi_fused|k_nlist|k_pack_w' -c 12 -o $O/prof $P > $O/ncu_full.log 2>&1
   echo "full rc=$?" >> $O/ncu_full.log
 fi

@@ -10,7 +10,7 @@ import torch  # noqa: E402
 import paper_0909_5413_b200.rbf as R  # noqa: E402
 import rbf_workloads as W  # noqa: E402
 
-R.LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "probe", "librbf.so")
+R.LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "probe", os.environ.get("PROBE_LIB", "librbf.so"))
 L = R.lib()
 L.rbf_debug_probe.argtypes = [C.c_void_p]
 L.rbf_debug_probe.restype = C.c_int
