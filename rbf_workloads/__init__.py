@@ -131,6 +131,41 @@ def make_clustered(n: int, seed: int, *, s2: float = 0.02, tol: float = 1e-13,
                     4.0 * sigma, 1, tol, meta=dict(seed=seed, s2=s2))
 
 
+def franke(xy: np.ndarray) -> np.ndarray:
+    """Franke's test function as printed in PAPER.md Eq.(13) at the points.
+    (The paper prints (9y+1)^2/10 in the second term where Franke's 1982 function has
+    (9y+1)/10; this follows the paper -- reading Q22 of DESIGN.md.  It is input data
+    only, no part of the method.)"""
+    x, y = xy[:, 0], xy[:, 1]
+    return (0.75 * np.exp(-0.25 * ((9 * x - 2) ** 2 + (9 * y - 2) ** 2))
+            + 0.75 * np.exp(-((9 * x + 1) ** 2) / 49.0 - ((9 * y + 1) ** 2) / 10.0)
+            + 0.5 * np.exp(-0.25 * ((9 * x - 7) ** 2 + (9 * y - 3) ** 2))
+            - 0.2 * np.exp(-((9 * x - 4) ** 2) - (9 * y - 7) ** 2))
+
+
+def make_paper_lattice(n_side: int, h_over_sigma: float, *, scatter_seed: int | None = None,
+                       tol: float = 1e-13, name: str | None = None) -> Workload:
+    """The paper's test problem: Franke data on an n x n lattice of
+    [0,1]^2 that includes the boundary (x_i = i h, h = 1/(n-1); N = (1/h + 1)^2 as in
+    the paper, reading Q4), sigma = h / (h/sigma); quasi-scattered variant: every
+    coordinate shifted by U[0, h/2), PCG64(scatter_seed).  The subdomain
+    geometry is this build's (rc = 6 sigma, cell = 4 sigma, one ring; readings Q1, Q9),
+    not the paper's B/D/T boxes."""
+    h = 1.0 / (n_side - 1)
+    sigma = h / h_over_sigma
+    c = np.arange(n_side, dtype=np.float64) * h
+    X, Y = np.meshgrid(c, c, indexing="xy")
+    xy = np.stack([X.ravel(), Y.ravel()], axis=1).copy()
+    box = (0.0, 0.0, 1.0, 1.0)
+    if scatter_seed is not None:
+        rng = np.random.Generator(np.random.PCG64(scatter_seed))
+        xy = xy + rng.uniform(0.0, 0.5 * h, size=xy.shape)
+        box = (0.0, 0.0, 1.0 + 0.5 * h, 1.0 + 0.5 * h)
+    return Workload(name or f"franke{n_side}_{h_over_sigma}", xy, franke(xy), sigma, 6.0 * sigma,
+                    4.0 * sigma, 1, tol, box=box,
+                    meta=dict(h=h, n_side=n_side, h_over_sigma=h_over_sigma, scatter=scatter_seed))
+
+
 def config(k: int) -> Workload:
     """BASELINE.json configs[k-1] (BJ:7-11) as seeded synthetic input."""
     if k == 1:

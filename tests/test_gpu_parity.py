@@ -453,3 +453,47 @@ def test_cfg2_interpolate_onto_lattice(cfg2):
     pick = np.random.default_rng(34).choice(Q.shape[0], 64, replace=False)
     assert rel(s[pick], O.evaluate(Q[pick], wl.xy, lam, wl.sigma, wl.rc)) <= 1e-12
     assert np.max(np.abs(s_data - wl.f[rows])) <= 1e-9 * np.max(np.abs(wl.f))
+
+
+# ------------------------------------------------------------------ the paper's test problem
+
+RATIOS = (1.0, 0.9, 0.8)
+
+
+@pytest.fixture(scope="module")
+def paper_sweep():
+    """Franke data on [0,1]^2 lattices (Eq.(13)) at the paper's three
+    h/sigma ratios, two mesh sizes at fixed ratio, plus the
+    quasi-scattered variant (U[0, h/2) shifts)."""
+    out = {}
+    for r in RATIOS:
+        for n in (101, 201):
+            wl = W.make_paper_lattice(n, r)
+            with ctx_for(wl) as c:
+                lam, rep = c.solve(c.to_local(torch.from_numpy(wl.f).cuda()), rtol=wl.tol)
+                out[(r, n, False)] = (wl, to_caller(c, lam), rep)
+        wl = W.make_paper_lattice(101, r, scatter_seed=9)
+        with ctx_for(wl) as c:
+            lam, rep = c.solve(c.to_local(torch.from_numpy(wl.f).cuda()), rtol=wl.tol)
+            out[(r, 101, True)] = (wl, to_caller(c, lam), rep)
+    return out
+
+
+def test_paper_ratios_iterations(paper_sweep):
+    """Mesh-independent iteration counts at fixed h/sigma that grow as
+    h/sigma decreases.  Counts are recorded in DESIGN.md."""
+    it = {k: v[2].iterations for k, v in paper_sweep.items()}
+    for k, v in paper_sweep.items():
+        assert v[2].converged, k
+        assert v[2].resid_true <= 1e-9, (k, v[2].resid_true)
+    for r in RATIOS:
+        assert abs(it[(r, 101, False)] - it[(r, 201, False)]) <= 3, it
+    assert it[(1.0, 201, False)] <= it[(0.9, 201, False)] <= it[(0.8, 201, False)], it
+
+
+@pytest.mark.parametrize("ratio", RATIOS)
+def test_paper_ratio_oracle_parity(paper_sweep, ratio):
+    wl, lam, rep = paper_sweep[(ratio, 101, False)]
+    ref = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, rtol=wl.tol)
+    assert ref.converged and abs(rep.iterations - ref.iterations) <= 2
+    assert rel(lam, ref.x) <= 1e-8

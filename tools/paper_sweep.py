@@ -1,0 +1,32 @@
+"""Iteration counts of the paper's test problem (Franke data) at
+h/sigma in {1.0, 0.9, 0.8} and several mesh sizes, lattice and quasi-scattered;
+prints a markdown table.  Not part of the product."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_0909_5413_b200 as P  # noqa: E402
+import rbf_workloads as W  # noqa: E402
+
+print("| h/sigma | points | N | iterations | true residual | setup ms | solve ms |")
+print("|---|---|---|---|---|---|---|")
+for r in (1.0, 0.9, 0.8):
+    for n, sc in ((101, None), (201, None), (401, None), (1001, None), (101, 9), (401, 9)):
+        wl = W.make_paper_lattice(n, r, scatter_seed=sc)
+        xy = torch.from_numpy(wl.xy).cuda()
+        f = torch.from_numpy(wl.f).cuda()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        c = P.Context(xy, wl.sigma, wl.cell, wl.rc, wl.rings, wl.box)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        lam, rep = c.solve(c.to_local(f), rtol=wl.tol)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        kind = "lattice" if sc is None else "scattered"
+        print(f"| {r} | {kind} {n}x{n} | {wl.n} | {rep.iterations} | {rep.resid_true:.1e} | "
+              f"{1e3 * (t1 - t0):.1f} | {1e3 * (t2 - t1):.1f} |", flush=True)
+        c.close()
