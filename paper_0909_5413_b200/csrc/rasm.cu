@@ -564,13 +564,14 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
 // and written once per panel instead of once per column: (1) the panel is factored
 // in a transposed copy PT (kLuNb x n, coalesced column access), whole rows are
 // swapped eagerly in A; (2) one pass over the remaining columns does the unit-lower
-// solve U12 = L11^-1 A12 and the rank-kLuNb update A22 -= L21 U12 with the U12
-// column in registers and L21 rows broadcast from shared memory.  The back
+// solve U12 = L11^-1 A12 and the rank-kLuNb update A22 -= L21 U12 on the fp64 tensor
+// cores (DMMA.8x8x4, U12 blocks in shared memory, L21 fragments in registers).  The back
 // substitution is blocked the same way.  One CTA per cell; A (n x lda, lda = n +
 // n_own) and PT live in a per-CTA slice of a global workspace (L2).
 constexpr int kLuThreads = 512;
 constexpr int kLuNb = 32;     // panel width
-constexpr int kLuRows = 64;   // L21 rows staged in shared memory per pass
+constexpr int kLuRows = 64;   // rows staged in shared memory per back-substitution pass
+constexpr int kLuCb = 64;     // trailing-update column block (U12 block in shared memory)
 
 __device__ __forceinline__ void lu_argmax(double v, int i, double *red_v, int *red_i, int *out) {
   // CTA reduction: largest value, lowest index on ties; result in *out (shared)
@@ -595,7 +596,7 @@ __device__ __forceinline__ void lu_argmax(double v, int i, double *red_v, int *r
   __syncthreads();
 }
 
-__global__ __launch_bounds__(kLuThreads) void k_rasm_setup_lu(
+__global__ __launch_bounds__(kLuThreads, 1) void k_rasm_setup_lu(
     Geom g, Strip st, const double2 *__restrict__ xy, const int *__restrict__ cell_start,
     const long long *__restrict__ x_off, double *__restrict__ X, const int *__restrict__ glist,
     int first, int count, double *__restrict__ ws, long long ws_stride, int *__restrict__ fail_key) {
@@ -606,6 +607,7 @@ __global__ __launch_bounds__(kLuThreads) void k_rasm_setup_lu(
   __shared__ double Ls[kLuRows][kLuNb + 1];  // staged L21 / U rows (+1: no bank conflicts)
   __shared__ double L11[kLuNb][kLuNb + 1];
   __shared__ double prow[kLuNb];
+  __shared__ double Ub[kLuNb][kLuCb + 1];  // U12 column block (B operand of the DMMA update)
   const int tid = threadIdx.x, T = blockDim.x;
   if ((int)blockIdx.x >= count) return;
   const int cl = glist[first + blockIdx.x];
@@ -690,38 +692,49 @@ __global__ __launch_bounds__(kLuThreads) void k_rasm_setup_lu(
       L11[r][c] = (c < r) ? PT[(long long)c * n + k0 + r] : 0.0;
     }
     __syncthreads();
-    // ---- U12 = L11^-1 A12 and A22 -= L21 U12, one column per thread (U12 column in
-    //      registers), L21 rows staged in shared memory, kLuRows at a time
+    // ---- U12 = L11^-1 A12 (one column per thread, L11 in shared memory), then
+    //      A22 -= L21 U12 on the fp64 tensor cores: column blocks of kLuCb columns with
+    //      the U12 block staged in shared memory; each warp walks 8-row tiles holding
+    //      its L21 fragments (8 x 32) in registers, 8 DMMA.8x8x4 per 8x8 output tile.
     const int j0 = k0 + kb;
-    for (long long jb = j0; jb < lda; jb += T) {
-      const long long j = jb + tid;
-      const bool act = j < lda;
-      double u[kLuNb];
+    for (long long jb = j0; jb < lda; jb += kLuCb) {
+      const int nc = (int)(lda - jb < kLuCb ? lda - jb : kLuCb);
+      if (tid < kLuCb) {
+        double u[kLuNb];
+        const long long j = jb + tid;
+        const bool act = tid < nc;
 #pragma unroll
-      for (int t = 0; t < kLuNb; ++t) u[t] = (act && t < kb) ? A[(long long)(k0 + t) * lda + j] : 0.0;
+        for (int t = 0; t < kLuNb; ++t) u[t] = (act && t < kb) ? A[(long long)(k0 + t) * lda + j] : 0.0;
 #pragma unroll
-      for (int r = 1; r < kLuNb; ++r)
+        for (int r = 1; r < kLuNb; ++r)
 #pragma unroll
-        for (int t = 0; t < r; ++t) u[r] = fma(-L11[r][t], u[t], u[r]);
-      if (act)
+          for (int t = 0; t < r; ++t) u[r] = fma(-L11[r][t], u[t], u[r]);
 #pragma unroll
-        for (int t = 0; t < kLuNb; ++t)
-          if (t < kb) A[(long long)(k0 + t) * lda + j] = u[t];
-      for (int i0 = j0; i0 < n; i0 += kLuRows) {
-        const int nr = n - i0 < kLuRows ? n - i0 : kLuRows;
-        __syncthreads();
-        for (int t = tid; t < nr * kLuNb; t += T) {
-          const int r = t / kLuNb, c = t - r * kLuNb;
-          Ls[r][c] = (c < kb) ? PT[(long long)c * n + i0 + r] : 0.0;
+        for (int t = 0; t < kLuNb; ++t) {
+          Ub[t][tid] = u[t];
+          if (act && t < kb) A[(long long)(k0 + t) * lda + j] = u[t];
         }
-        __syncthreads();
-        if (act) {
-          for (int r = 0; r < nr; ++r) {
-            double a = A[(long long)(i0 + r) * lda + j];
+      }
+      __syncthreads();
+      const int lane = tid & 31, nwarps = T >> 5, q = lane & 3, r8 = lane >> 2;
+      for (int i0 = j0 + 8 * (tid >> 5); i0 < n; i0 += 8 * nwarps) {
+        double af[kLuNb / 4];
+        const int ia = i0 + r8;
 #pragma unroll
-            for (int t = 0; t < kLuNb; ++t) a = fma(-Ls[r][t], u[t], a);
-            A[(long long)(i0 + r) * lda + j] = a;
-          }
+        for (int s4 = 0; s4 < kLuNb / 4; ++s4) {
+          const int k = 4 * s4 + q;
+          af[s4] = (k < kb && ia < n) ? PT[(long long)k * n + ia] : 0.0;
+        }
+        for (int cj = 0; cj < nc; cj += 8) {
+          const long long jc = jb + cj + 2 * q;
+          double *crow = A + (long long)ia * lda + jc;
+          const bool ok0 = ia < n && jc < lda, ok1 = ia < n && jc + 1 < lda;
+          const double c0 = ok0 ? crow[0] : 0.0, c1 = ok1 ? crow[1] : 0.0;
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int s4 = 0; s4 < kLuNb / 4; ++s4) dmma(d0, d1, af[s4], Ub[4 * s4 + q][cj + r8]);
+          if (ok0) crow[0] = c0 - d0;
+          if (ok1) crow[1] = c1 - d1;
         }
       }
       __syncthreads();
