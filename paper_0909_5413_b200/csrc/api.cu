@@ -235,6 +235,12 @@ void rbf_destroy(rbf_ctx *c) {
   dfree(c->dscal, s);
   dfree(c->ar_part, s);
   dfree(c->ar_bar, s);
+  if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
+  if (c->g_graph) cudaGraphDestroy(c->g_graph);
+  dfree(c->g_state, s);
+  dfree(c->g_hist, s);
+  dfree(c->g_f, s);
+  dfree(c->g_x, s);
   if (c->hpin) cudaFreeHost(c->hpin);
   comm_destroy(c);
   delete c;

@@ -205,6 +205,16 @@ struct rbf_ctx {
   int ar_grid = 0;             // CTAs of the fused single-rank Arnoldi kernel (0 = unused)
   double *ar_part = nullptr;   // its per-CTA partial sums
   unsigned *ar_bar = nullptr;  // its grid barrier (count, generation)
+  int ar_m = 0;                // restart length ar_part is sized for
+  // graph-driven solve (single rank): the whole restarted GMRES as one CUDA graph with
+  // device-side while loops (conditional nodes), built per restart length
+  cudaGraph_t g_graph = nullptr;
+  cudaGraphExec_t g_exec = nullptr;
+  int g_m = 0, g_hist_cap = 0;
+  const double *g_V = nullptr;  // V the graph was built for
+  void *g_state = nullptr;      // GState (krylov.cu)
+  double *g_hist = nullptr;     // per-iteration residual estimates
+  double *g_f = nullptr, *g_x = nullptr;  // the graph's right-hand side and iterate
   long long bytes = 0;
   double setup_ms[4] = {0, 0, 0, 0};
   cudaStream_t last_stream = nullptr;
@@ -229,7 +239,8 @@ int launch_local_index(const rbf_ctx *c, int64_t *idx, cudaStream_t s);
 
 // matvec.cu
 int build_nlist(rbf_ctx *c, cudaStream_t s);
-int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStream_t s);
+int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStream_t s,
+                  bool prepacked = false);  // prepacked: w already in the records' w slot
 int launch_pack_w(const rbf_ctx *c, const double *w_ext, cudaStream_t s);
 
 // evaluate.cu
@@ -250,5 +261,6 @@ int allgather_scalars(rbf_ctx *c, const double *send, double *recv, int count, c
 int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *g, double *x,
                 rbf_report *rep, cudaStream_t s);
 int dot_host(rbf_ctx *c, const double *a, const double *b, double *out, cudaStream_t s);
+int prebuild_solve(rbf_ctx *c, cudaStream_t s);  // GMRES workspace + solve graph (rbf_setup)
 
 }  // namespace rbf

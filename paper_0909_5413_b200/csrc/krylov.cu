@@ -106,12 +106,14 @@ __global__ __launch_bounds__(kRedThreads) void k_axpy_dot(const double *__restri
 }
 
 __global__ void k_scale_by_norm(double *__restrict__ w, long long n, const double *__restrict__ nrm2,
-                                int P) {
+                                int P, double4 *__restrict__ rec) {
   double h = sqrt(sum_ranks(nrm2, 0, P));
-  if (h == 0.0) return;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
-    w[i] = w[i] / h;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double v = (h == 0.0) ? w[i] : w[i] / h;
+    w[i] = v;
+    if (rec) reinterpret_cast<double *>(rec + i)[2] = v;  // single rank: pre-pack the matvec input
+  }
 }
 
 __global__ void k_sub(const double *__restrict__ f, double *__restrict__ t, long long n) {
@@ -220,10 +222,39 @@ __device__ __forceinline__ void grid_arrive_wait(unsigned *bar, unsigned nb, int
 // with two __syncthreads and one grid barrier per step; v_j stays in registers for
 // the update and v_{j+1} is loaded before the barrier, so the HBM latency of the
 // next projection overlaps the reduction.
+// Device-side loop state of the graph-driven solve (single rank).
+struct GState {
+  int k, it, conv, nan, kend, restarts, max_iters, pad;
+  double rtol, atol, tol_abs, beta0, beta_last;
+  double fsq, rsq;  // ||f||^2 and ||f - A x||^2 of the final iterate (report)
+};
+
+// After Arnoldi step k (block 0, thread 0): Givens, history, loop control.
+__device__ __forceinline__ void graph_step_end(double *S, const Scal &L, int k, GState *st,
+                                               double *hist, cudaGraphConditionalHandle inner) {
+  givens_step(S, L, S + L.hloc(), k);
+  const double gabs = S[L.out() + 0], hn = S[L.out() + 1];
+  const int it = st->it;
+  hist[it] = gabs / st->beta0;
+  st->it = it + 1;
+  st->k = k + 1;
+  st->kend = k + 1;
+  const bool bad = !isfinite(gabs) || !isfinite(hn);
+  const bool conv = !bad && (gabs <= st->tol_abs || hn == 0.0);
+  st->conv = conv;
+  st->nan |= bad;
+  const bool stop = conv || bad || k + 1 >= L.m || it + 1 >= st->max_iters;
+  cudaGraphSetConditional(inner, stop ? 0u : 1u);
+}
+
 __global__ __launch_bounds__(kArThreads, 1) void k_arnoldi_fused(double *V, long long ldv, long long n,
                                                               int k, double *S, Scal L,
                                                               double *part, unsigned *bar,
-                                                              Mailbox *mb, long long seq) {
+                                                              Mailbox *mb, long long seq,
+                                                              double4 *rec, const double *w_in,
+                                                              GState *st, double *hist,
+                                                              cudaGraphConditionalHandle inner) {
+  if (st) k = st->k;  // graph mode: the step index lives on the device
   __shared__ double sh_w[kArThreads / 32];
   __shared__ double sh_h;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -232,11 +263,12 @@ __global__ __launch_bounds__(kArThreads, 1) void k_arnoldi_fused(double *V, long
   const long long base = (long long)blockIdx.x * chunk;
   const long long end = base + chunk < n ? base + chunk : n;
   double *wv = V + (long long)(k + 1) * ldv;
+  const double *win = w_in ? w_in : wv;
   double w[kArE], vc[kArE], vn[kArE];
 #pragma unroll
   for (int e = 0; e < kArE; ++e) {
     const long long i = base + threadIdx.x + (long long)e * kArThreads;
-    w[e] = i < end ? wv[i] : 0.0;
+    w[e] = i < end ? win[i] : 0.0;
     vc[e] = i < end ? V[i] : 0.0;  // v_0
   }
   for (int j = 0; j <= k + 1; ++j) {
@@ -295,13 +327,85 @@ __global__ __launch_bounds__(kArThreads, 1) void k_arnoldi_fused(double *V, long
 #pragma unroll
       for (int e = 0; e < kArE; ++e) {
         const long long i = base + threadIdx.x + (long long)e * kArThreads;
-        if (i < end) wv[i] = (hn != 0.0) ? w[e] / hn : w[e];
+        if (i < end) {
+          const double v = (hn != 0.0) ? w[e] / hn : w[e];
+          wv[i] = v;
+          reinterpret_cast<double *>(rec + i)[2] = v;  // the next matvec's input, pre-packed
+        }
       }
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    givens_step(S, L, S + L.hloc(), k);
-    post_mailbox(mb, S, L, seq);
+    if (st) {
+      graph_step_end(S, L, k, st, hist, inner);
+    } else {
+      givens_step(S, L, S + L.hloc(), k);
+      post_mailbox(mb, S, L, seq);
+    }
+  }
+}
+
+// ---- graph-mode control kernels (one thread)
+__global__ void k_g_begin(const double *nrm2, GState *st, cudaGraphConditionalHandle outer) {
+  const double beta0 = sqrt(*nrm2);
+  st->beta0 = beta0;
+  st->tol_abs = fmax(st->rtol * beta0, st->atol);
+  st->it = 0;
+  st->k = 0;
+  st->kend = 0;
+  st->restarts = 0;
+  st->nan = !isfinite(beta0);
+  st->conv = beta0 == 0.0;
+  st->beta_last = beta0;
+  cudaGraphSetConditional(outer, (!st->conv && !st->nan && st->max_iters > 0) ? 1u : 0u);
+}
+
+__global__ void k_g_cycle(double *S, Scal L, const double *nrm2, GState *st,
+                          cudaGraphConditionalHandle inner) {
+  const double beta = sqrt(*nrm2);
+  for (int i = 0; i <= L.m; ++i) S[L.g() + i] = 0.0;
+  S[L.g()] = beta;
+  S[L.out() + 2] = beta;
+  st->k = 0;
+  st->kend = 0;
+  cudaGraphSetConditional(inner, (!st->conv && !st->nan && st->it < st->max_iters) ? 1u : 0u);
+}
+
+// End of a cycle: explicit preconditioned residual norm^2 in nrm2 (reading Q12).
+__global__ void k_g_end_cycle(const double *nrm2, GState *st, cudaGraphConditionalHandle outer) {
+  const double beta = sqrt(*nrm2);
+  st->beta_last = beta;
+  bool more = !st->conv && !st->nan && st->it < st->max_iters;
+  if (more) {
+    st->restarts += 1;
+    if (beta <= st->tol_abs) {
+      st->conv = 1;
+      more = false;
+    }
+  }
+  cudaGraphSetConditional(outer, more ? 1u : 0u);
+}
+
+__global__ void k_backsolve_g(double *S, Scal L, const GState *st) {
+  const int kend = st->kend, m = L.m;
+  const double *H = S + L.H(), *g = S + L.g();
+  double *y = S + L.y();
+  for (int i = kend - 1; i >= 0; --i) {
+    double sacc = g[i];
+    for (int j = i + 1; j < kend; ++j) sacc -= H[(long long)i * m + j] * y[j];
+    y[i] = sacc / H[(long long)i * m + i];
+  }
+}
+
+__global__ void k_update_x_g(double *__restrict__ x, const double *__restrict__ V, long long ldv,
+                             const double *__restrict__ S, Scal L, const GState *st, long long n) {
+  const int kend = st->kend;
+  const double *y = S + L.y();
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    double xi = x[i];
+    for (int j = 0; j < kend; ++j) xi += y[j] * V[j * ldv + i];
+    x[i] = xi;
   }
 }
 
@@ -335,13 +439,13 @@ struct Op {
   rbf_ctx *c;
   cudaStream_t s;
   // y = A w (halo of w first)
-  int matvec(const double *w, double *y) {
+  int matvec(const double *w, double *y, bool prepacked = false) {
     const double *src = w;
     if (c->nranks > 1) {
       RBF_TRY(halo_exchange(c, w, c->w_ext, true, s));
       src = c->w_ext;
     }
-    return launch_matvec(c, src, y, s);
+    return launch_matvec(c, src, y, s, prepacked);
   }
   int pc(const double *r, double *z) {
     const double *src = r;
@@ -376,7 +480,13 @@ static int ensure_workspace(rbf_ctx *c, int m, cudaStream_t s) {
     RBF_CUDA_TRY(cudaHostAlloc((void **)&c->hpin, sizeof(double) * (kHpinScal + 8 + c->nranks), cudaHostAllocMapped));
     RBF_CUDA_TRY(cudaHostGetDevicePointer((void **)&c->hpin_dev, c->hpin, 0));
   }
-  if (c->nranks == 1 && !c->ar_part) {
+  if (c->nranks == 1 && c->ar_part && c->ar_m < m) {  // per-step partials sized by m
+    dfree(c->ar_part, s);
+    c->ar_part = nullptr;
+    RBF_TRY(dalloc(c, (void **)&c->ar_part, sizeof(double) * (size_t)(m + 2) * c->ar_grid, s));
+    c->ar_m = m;
+  }
+  if (c->nranks == 1 && !c->ar_part && c->ar_m == 0) {
     int dev = 0, sms = 0, per_sm = 0;
     RBF_CUDA_TRY(cudaGetDevice(&dev));
     RBF_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -387,6 +497,7 @@ static int ensure_workspace(rbf_ctx *c, int m, cudaStream_t s) {
     c->ar_grid = (coop && per_sm > 0) ? sms * (per_sm < ar_per_sm ? per_sm : ar_per_sm) : 0;
     if (getenv("RBF_NO_FUSED_ARNOLDI")) c->ar_grid = 0;
     if (c->ar_grid > 0 && (long long)c->ar_grid * kArThreads * kArE < n) c->ar_grid = 0;
+    c->ar_m = m;
     if (c->ar_grid > 0) {
       RBF_TRY(dalloc(c, (void **)&c->ar_part, sizeof(double) * (size_t)(m + 2) * c->ar_grid, s));
       RBF_TRY(dalloc(c, (void **)&c->ar_bar, sizeof(unsigned) * 2, s));
@@ -504,11 +615,223 @@ static int wait_mailbox(rbf_ctx *c, long long seq, cudaStream_t s, double *gabs,
   return RBF_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Graph-driven solve (single rank with the fused Arnoldi kernel): the whole
+// restarted GMRES is ONE CUDA graph -- an outer while node over restart cycles and
+// an inner while node over Arnoldi steps, both driven by cudaGraphSetConditional
+// from the kernels that compute the residual estimates -- so no host round trip or
+// launch latency sits between iterations and host jitter cannot stall the GPU.
+// ---------------------------------------------------------------------------
+static int capture_leaf(cudaStream_t s, cudaGraphNode_t *leaf) {
+  cudaStreamCaptureStatus st;
+  const cudaGraphNode_t *deps = nullptr;
+  size_t nd = 0;
+  RBF_CUDA_TRY(cudaStreamGetCaptureInfo(s, &st, nullptr, nullptr, &deps, &nd));
+  if (nd != 1) {
+    set_error("graph capture: expected one leaf node, got %zu", nd);
+    return RBF_ECUDA;
+  }
+  *leaf = deps[0];
+  return RBF_OK;
+}
+
+static int build_solve_graph_on(rbf_ctx *c, int m, cudaStream_t s);
+
+static int build_solve_graph(rbf_ctx *c, int m, cudaStream_t user) {
+  // capture on a private stream (the legacy default stream cannot be captured);
+  // nothing is executed, so the user stream may still be busy (rbf_setup builds the
+  // graph while the RASM setup kernel runs)
+  (void)user;
+  cudaStream_t cs;
+  RBF_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  const int st = build_solve_graph_on(c, m, cs);
+  cudaStreamDestroy(cs);
+  return st;
+}
+
+static int build_solve_graph_on(rbf_ctx *c, int m, cudaStream_t s) {
+  const long long n = n_loc(c);
+  Scal L{m, 1};
+  double *V = c->V, *S = c->dscal, *slot0 = c->dscal + L.hloc();
+  GState *st = reinterpret_cast<GState *>(c->g_state);
+  const int blocks = grid_for(n);
+  if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
+  if (c->g_graph) cudaGraphDestroy(c->g_graph);
+  c->g_exec = nullptr;
+  c->g_graph = nullptr;
+  cudaGraph_t G;
+  RBF_CUDA_TRY(cudaGraphCreate(&G, 0));
+  c->g_graph = G;
+  cudaGraphConditionalHandle h_outer, h_inner;
+  RBF_CUDA_TRY(cudaGraphConditionalHandleCreate(&h_outer, G, 0, cudaGraphCondAssignDefault));
+  const cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  // -- prologue: x = 0, z0 = M^-1 f, ||z0||^2, tolerance, outer condition
+  cudaGraphNode_t leaf;
+  RBF_CUDA_TRY(cudaStreamBeginCaptureToGraph(s, G, nullptr, nullptr, 0, mode));
+  RBF_CUDA_TRY(cudaMemsetAsync(c->g_x, 0, sizeof(double) * (size_t)n, s));
+  RBF_TRY(axpy_dot(c, nullptr, c->g_f, nullptr, c->g_f, &st->fsq, s));
+  RBF_TRY(launch_rasm_apply(c, c->g_f, V, s));
+  RBF_TRY(axpy_dot(c, nullptr, V, nullptr, V, slot0, s));
+  k_g_begin<<<1, 1, 0, s>>>(slot0, st, h_outer);
+  count_launch(1);
+  RBF_TRY(capture_leaf(s, &leaf));
+  RBF_CUDA_TRY(cudaStreamEndCapture(s, &G));
+  // -- outer while: one restart cycle per iteration
+  cudaGraphNodeParams op = {};
+  op.type = cudaGraphNodeTypeConditional;
+  op.conditional.handle = h_outer;
+  op.conditional.type = cudaGraphCondTypeWhile;
+  op.conditional.size = 1;
+  cudaGraphNode_t outer_node;
+  RBF_CUDA_TRY(cudaGraphAddNode(&outer_node, G, &leaf, 1, &op));
+  cudaGraph_t B = op.conditional.phGraph_out[0];
+  RBF_CUDA_TRY(cudaGraphConditionalHandleCreate(&h_inner, B, 0, cudaGraphCondAssignDefault));
+  RBF_CUDA_TRY(cudaStreamBeginCaptureToGraph(s, B, nullptr, nullptr, 0, mode));
+  k_g_cycle<<<1, 1, 0, s>>>(S, L, slot0, st, h_inner);
+  k_scale_by_norm<<<blocks, kRedThreads, 0, s>>>(V, n, slot0, 1, c->rec);  // v0, pre-packed
+  count_launch(2);
+  RBF_TRY(capture_leaf(s, &leaf));
+  RBF_CUDA_TRY(cudaStreamEndCapture(s, &B));
+  // -- inner while: one Arnoldi step per iteration (matvec, RASM apply, fused MGS+Givens)
+  cudaGraphNodeParams ip = {};
+  ip.type = cudaGraphNodeTypeConditional;
+  ip.conditional.handle = h_inner;
+  ip.conditional.type = cudaGraphCondTypeWhile;
+  ip.conditional.size = 1;
+  cudaGraphNode_t inner_node;
+  RBF_CUDA_TRY(cudaGraphAddNode(&inner_node, B, &leaf, 1, &ip));
+  cudaGraph_t I = ip.conditional.phGraph_out[0];
+  RBF_CUDA_TRY(cudaStreamBeginCaptureToGraph(s, I, nullptr, nullptr, 0, mode));
+  RBF_TRY(launch_matvec(c, V, c->t1, s, true));
+  RBF_TRY(launch_rasm_apply(c, c->t1, c->t2, s));
+  {
+    double *Sp = S, *part = c->ar_part, *w_in = c->t2, *hist = c->g_hist;
+    unsigned *bar = c->ar_bar;
+    Mailbox *mb = nullptr;
+    double4 *rec = c->rec;
+    long long ldv_ = n, n_ = n, seq_ = 0;
+    int k_ = 0;
+    GState *st_ = st;
+    cudaGraphConditionalHandle h = h_inner;
+    void *args[] = {&V, &ldv_, &n_, &k_, &Sp, &L, &part, &bar, &mb, &seq_, &rec, &w_in, &st_, &hist, &h};
+    RBF_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_arnoldi_fused, c->ar_grid, kArThreads, args, 0, s));
+    count_launch(1);
+  }
+  RBF_CUDA_TRY(cudaStreamEndCapture(s, &I));
+  // -- end of cycle: x += V y, explicit residual f - A x, z = M^-1 (f - A x), ||z||^2
+  RBF_CUDA_TRY(cudaStreamBeginCaptureToGraph(s, B, &inner_node, nullptr, 1, mode));
+  k_backsolve_g<<<1, 1, 0, s>>>(S, L, st);
+  k_update_x_g<<<blocks, kRedThreads, 0, s>>>(c->g_x, V, n, S, L, st, n);
+  count_launch(2);
+  RBF_TRY(launch_matvec(c, c->g_x, c->t1, s, false));
+  k_sub<<<blocks, kRedThreads, 0, s>>>(c->g_f, c->t1, n);
+  count_launch(1);
+  RBF_TRY(axpy_dot(c, nullptr, c->t1, nullptr, c->t1, &st->rsq, s));
+  RBF_TRY(launch_rasm_apply(c, c->t1, V, s));
+  RBF_TRY(axpy_dot(c, nullptr, V, nullptr, V, slot0, s));
+  k_g_end_cycle<<<1, 1, 0, s>>>(slot0, st, h_outer);
+  count_launch(1);
+  RBF_CUDA_TRY(cudaStreamEndCapture(s, &B));
+  RBF_CUDA_TRY(cudaGraphInstantiate(&c->g_exec, G, 0));
+  c->g_m = m;
+  c->g_V = V;
+  return RBF_OK;
+}
+
+static int prepare_solve_graph(rbf_ctx *c, int m, int max_iters, cudaStream_t s) {
+  const long long n = n_loc(c);
+  if (!c->g_state) RBF_TRY(dalloc(c, &c->g_state, sizeof(GState), s));
+  if (!c->g_f) RBF_TRY(dalloc(c, (void **)&c->g_f, sizeof(double) * (size_t)(n > 0 ? n : 1), s));
+  if (!c->g_x) RBF_TRY(dalloc(c, (void **)&c->g_x, sizeof(double) * (size_t)(n > 0 ? n : 1), s));
+  bool rebuild = c->g_exec == nullptr || c->g_m != m || c->g_V != c->V;
+  if (c->g_hist_cap < max_iters) {
+    dfree(c->g_hist, s);
+    c->g_hist_cap = max_iters > 1024 ? max_iters : 1024;
+    RBF_TRY(dalloc(c, (void **)&c->g_hist, sizeof(double) * (size_t)c->g_hist_cap, s));
+    rebuild = true;
+  }
+  if (rebuild) RBF_TRY(build_solve_graph(c, m, s));
+  return RBF_OK;
+}
+
+static bool graph_path(const rbf_ctx *c, const rbf_gmres_params *gp) {
+  return c->nranks == 1 && c->ar_grid > 0 && !gp->timing && c->rec && !getenv("RBF_NO_GRAPH");
+}
+
+// rbf_setup hook: allocate the default GMRES workspace and build the solve graph while
+// the RASM setup kernel occupies the GPU (the capture and instantiation are host work).
+int prebuild_solve(rbf_ctx *c, cudaStream_t s) {
+  rbf_gmres_params gp{};
+  gp.restart = 30;
+  gp.max_iters = 1000;
+  RBF_TRY(ensure_workspace(c, gp.restart, s));
+  if (!graph_path(c, &gp)) return RBF_OK;
+  return prepare_solve_graph(c, gp.restart, gp.max_iters, s);
+}
+
+static int solve_gmres_graph(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double *x,
+                             rbf_report *rep, cudaStream_t s) {
+  const int m = gp->restart;
+  const long long n = n_loc(c);
+  RBF_TRY(prepare_solve_graph(c, m, gp->max_iters, s));
+  GState hs{};
+  hs.max_iters = gp->max_iters;
+  hs.rtol = gp->rtol;
+  hs.atol = gp->atol;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  RBF_CUDA_TRY(cudaEventCreate(&t0));
+  RBF_CUDA_TRY(cudaEventCreate(&t1));
+  RBF_CUDA_TRY(cudaMemcpyAsync(c->g_state, &hs, sizeof(GState), cudaMemcpyHostToDevice, s));
+  RBF_CUDA_TRY(cudaMemcpyAsync(c->g_f, f, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, s));
+  RBF_CUDA_TRY(cudaEventRecord(t0, s));
+  RBF_CUDA_TRY(cudaGraphLaunch(c->g_exec, s));
+  RBF_CUDA_TRY(cudaEventRecord(t1, s));
+  RBF_CUDA_TRY(cudaMemcpyAsync(x, c->g_x, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, s));
+  RBF_CUDA_TRY(cudaMemcpyAsync(&hs, c->g_state, sizeof(GState), cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  float ms = 0.0f;
+  cudaEventElapsedTime(&ms, t0, t1);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  // launches executed by the graph: prologue 3 (+ matvec/apply), per cycle 12, per step 4
+  const int cycles = hs.it > 0 ? hs.restarts + 1 : 0;
+  count_launch(4 + 12 * cycles + 4 * hs.it);
+  const bool converged = hs.conv != 0;
+  int status = RBF_OK;
+  if (hs.nan) status = RBF_ENUMERIC;
+  else if (!converged) status = RBF_NOT_CONVERGED;
+  if (rep) {
+    int hl = 0;
+    if (rep->history && rep->history_cap > 0 && hs.it > 0) {
+      hl = hs.it < rep->history_cap ? hs.it : rep->history_cap;
+      RBF_CUDA_TRY(cudaMemcpy(rep->history, c->g_hist, sizeof(double) * hl, cudaMemcpyDeviceToHost));
+    }
+    // the graph's last cycle left ||f - A x||^2 and ||M^-1 (f - A x)|| in the state
+    const double fsq = hs.fsq, rsq = hs.it > 0 ? hs.rsq : 0.0;
+    const double psq = hs.it > 0 ? hs.beta_last * hs.beta_last : 0.0;
+    double last = 0.0;
+    if (hs.it > 0) RBF_CUDA_TRY(cudaMemcpy(&last, c->g_hist + hs.it - 1, sizeof(double), cudaMemcpyDeviceToHost));
+    rep->iterations = hs.it;
+    rep->converged = converged;
+    rep->restarts = hs.restarts;
+    rep->beta0 = hs.beta0;
+    rep->resid_est = hs.it > 0 ? last : 0.0;
+    rep->resid_true = fsq > 0 ? std::sqrt(rsq / fsq) : 0.0;
+    rep->resid_precond = hs.beta0 > 0 ? std::sqrt(psq) / hs.beta0 : 0.0;
+    rep->history_len = hl;
+    rep->ms_matmult = rep->ms_pcapply = rep->ms_orth = 0.0;
+    rep->ms_total = ms;
+    rep->status = status;
+  }
+  return status;
+}
+
 int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double *x,
                 rbf_report *rep, cudaStream_t s) {
   const int m = gp->restart;
   const long long n = n_loc(c);
   RBF_TRY(ensure_workspace(c, m, s));
+  if (graph_path(c, gp)) return solve_gmres_graph(c, f, gp, x, rep, s);
   Scal L{m, c->nranks};
   Op op{c, s};
   double *V = c->V;
@@ -522,6 +845,7 @@ int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double 
     RBF_CUDA_TRY(cudaEventRecord(t_begin, s));
   }
   const int blocks = grid_for(n);
+  const bool prepack = c->nranks == 1 && c->ar_grid > 0 && c->rec != nullptr;
 
   RBF_CUDA_TRY(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)n, s));
   // beta0 = ||M^-1 f||  (x0 = 0)
@@ -540,7 +864,8 @@ int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double 
     for (;;) {
       // V0 holds the unscaled preconditioned residual; its ||.||^2 is in slot 0
       k_cycle_init<<<1, 1, 0, s>>>(c->dscal, L, hall_slot(c, L, 0)); count_launch(1);
-      k_scale_by_norm<<<blocks, kRedThreads, 0, s>>>(V, n, hall_slot(c, L, 0), L.P); count_launch(1);
+      k_scale_by_norm<<<blocks, kRedThreads, 0, s>>>(V, n, hall_slot(c, L, 0), L.P, prepack ? c->rec : nullptr);
+      count_launch(1);
       RBF_CUDA_TRY(cudaGetLastError());
       int kend = 0;
       bool done = false;
@@ -550,7 +875,9 @@ int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double 
         double *w = V + (long long)(k + 1) * ldv;
         const long long seq = ++seq_enq;
         pt.rec(seq, 0, s);
-        RBF_TRY(op.matvec(vk, c->t1));
+        // single rank: the basis vector v_k was written into the matvec records by the
+        // kernel that produced it (cycle start or the previous Arnoldi step)
+        RBF_TRY(op.matvec(vk, c->t1, prepack));
         pt.rec(seq, 1, s);
         RBF_TRY(op.pc(c->t1, w));
         pt.rec(seq, 2, s);
@@ -562,7 +889,12 @@ int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double 
           unsigned *bar = c->ar_bar;
           long long ldv_ = ldv, n_ = n, seq_ = seq;
           int k_ = k;
-          void *args[] = {&V, &ldv_, &n_, &k_, &Sp, &L, &part, &bar, &mb, &seq_};
+          double4 *rec = c->rec;
+          const double *w_in = nullptr;
+          GState *st = nullptr;
+          double *hist = nullptr;
+          cudaGraphConditionalHandle inner = 0;
+          void *args[] = {&V, &ldv_, &n_, &k_, &Sp, &L, &part, &bar, &mb, &seq_, &rec, &w_in, &st, &hist, &inner};
           RBF_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_arnoldi_fused, c->ar_grid,
                                                    kArThreads, args, 0, s));
           count_launch(1);
@@ -577,7 +909,7 @@ int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double 
           RBF_TRY(reduce_slot(c, L, k + 1, s));
           k_givens<<<1, 1, 0, s>>>(c->dscal, L, hall_slot(c, L, 0), k, mb, seq);
           count_launch(1);
-          k_scale_by_norm<<<blocks, kRedThreads, 0, s>>>(w, n, hall_slot(c, L, k + 1), L.P);
+          k_scale_by_norm<<<blocks, kRedThreads, 0, s>>>(w, n, hall_slot(c, L, k + 1), L.P, nullptr);
           count_launch(1);
         }
         RBF_CUDA_TRY(cudaGetLastError());

@@ -277,10 +277,10 @@ int launch_pack_w(const rbf_ctx *c, const double *w_ext, cudaStream_t s) {
   return RBF_OK;
 }
 
-int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStream_t s) {
+int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStream_t s, bool prepacked) {
   const long long nl = n_loc(c);
   if (nl <= 0) return RBF_OK;
-  RBF_TRY(launch_pack_w(c, w_ext, s));
+  if (!prepacked) RBF_TRY(launch_pack_w(c, w_ext, s));
   const int G = c->mv_g;
   const long long lanes = (nl + G - 1) / G;
   const int blocks = (int)((lanes + kMvThreads - 1) / kMvThreads);

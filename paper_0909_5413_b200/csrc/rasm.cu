@@ -925,6 +925,8 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
                                                   c->X, cnt, glist);
     count_launch(1);
     RBF_CUDA_TRY(cudaGetLastError());
+    // host work while the kernel runs: GMRES workspace and the solve graph (krylov.cu)
+    RBF_TRY(prebuild_solve(c, s));
     RBF_CUDA_TRY(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
     RBF_CUDA_TRY(cudaStreamSynchronize(s));
   }
