@@ -222,6 +222,7 @@ void rbf_destroy(rbf_ctx *c) {
   dfree(c->xy_ext, s);
   dfree(c->x_off, s);
   dfree(c->rec, s);
+  dfree(c->lane_tgt, s);
   dfree(c->chunk_len, s);
   dfree(c->chunk_off, s);
   dfree(c->nlist, s);

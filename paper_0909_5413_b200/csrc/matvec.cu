@@ -70,17 +70,34 @@ struct MvIdx {
   static __device__ __forceinline__ unsigned bit(int j) { return 1u << (31 - j); }
 };
 
+// The G local targets of lane lt: tgt[lt] (pairs chosen at setup, -1 = none) when
+// given, else G consecutive targets.
+template <int G>
+__device__ __forceinline__ void lane_targets(const int2 *__restrict__ tgt, long long lt, long long nloc,
+                                             long long nlanes, long long *t) {
+  if (G == 2 && tgt) {
+    const int2 v = lt < nlanes ? tgt[lt] : make_int2(-1, -1);
+    t[0] = v.x;
+    t[G - 1] = v.y;
+  } else {
+#pragma unroll
+    for (int j = 0; j < G; ++j) t[j] = lt * G + j < nloc ? lt * G + j : -1;
+  }
+}
+
 template <int MODE, int G>
 __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const double2 *__restrict__ xy,
                                                       const int *__restrict__ cell_start, long long nloc,
+                                                      const int2 *__restrict__ tgt, long long nlanes,
                                                       int *__restrict__ chunk_len,
                                                       const long long *__restrict__ chunk_off,
                                                       unsigned *__restrict__ list) {
   const long long lt = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // lane-group
-  const long long t0 = lt * G;                                            // first local target
+  long long t[G];
+  lane_targets<G>(tgt, lt, nloc, nlanes, t);
   const int lane = threadIdx.x & 31;
   const long long ch = lt >> 5;
-  const bool in_chunk = (ch << 5) * G < nloc;  // lanes past the end of a ragged last chunk
+  const bool in_chunk = (ch << 5) < nlanes;  // lanes past the end of a ragged last chunk
   const long long own_off = st.own_lo - st.ext_lo;
   int cnt = 0;
   long long base = 0;
@@ -90,8 +107,8 @@ __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const do
   int bx0 = g.ncx, bx1 = -1, by0 = g.ncy, by1 = -1;
 #pragma unroll
   for (int j = 0; j < G; ++j) {
-    act[j] = t0 + j < nloc;
-    p[j] = xy[own_off + (act[j] ? t0 + j : 0)];
+    act[j] = t[j] >= 0;
+    p[j] = xy[own_off + (act[j] ? t[j] : 0)];
     if (act[j]) {
       int cx, cy;
       target_cell(g, p[j], cx, cy);
@@ -122,7 +139,7 @@ __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const do
   if (MODE == 0) {
     if (lane == 0 && in_chunk) chunk_len[ch] = kmax;
   } else if (in_chunk) {  // padding: the lane's first target, no mask bit (also idle lanes)
-    const unsigned self = (unsigned)(own_off + (act[0] ? t0 : 0));
+    const unsigned self = (unsigned)(own_off + (act[0] ? t[0] : 0));
     for (int k = cnt; k < kmax; ++k) list[base + ((long long)(k >> 2) * 32 + lane) * 4 + (k & 3)] = self;
   }
 }
@@ -154,18 +171,20 @@ __device__ __forceinline__ void prefetch_l1(const void *p) {
 template <int G, int DEG, int U, int MINB, bool PF = false>
 __global__ __launch_bounds__(kMvThreads, MINB) void k_matvec(
     Geom g, long long nloc, long long own_off, const double4 *__restrict__ rec,
+    const int2 *__restrict__ tgt, long long nlanes,
     const int *__restrict__ chunk_len, const long long *__restrict__ chunk_off,
     const unsigned *__restrict__ list, double *__restrict__ y) {
   const int lane = threadIdx.x & 31;
   const long long lt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long t0 = lt * G;
   const long long ch = lt >> 5;
-  if ((ch << 5) * G >= nloc) return;  // whole warp beyond the last chunk
+  if ((ch << 5) >= nlanes) return;  // whole warp beyond the last chunk
+  long long t[G];
+  lane_targets<G>(tgt, lt, nloc, nlanes, t);
   double2 me[G];
   double acc[G];
 #pragma unroll
   for (int j = 0; j < G; ++j) {
-    const double4 r = rec[own_off + (t0 + j < nloc ? t0 + j : 0)];
+    const double4 r = rec[own_off + (t[j] >= 0 ? t[j] : 0)];
     me[j] = make_double2(r.x, r.y);
     acc[j] = 0.0;
   }
@@ -201,7 +220,125 @@ __global__ __launch_bounds__(kMvThreads, MINB) void k_matvec(
   }
 #pragma unroll
   for (int j = 0; j < G; ++j)
-    if (t0 + j < nloc) y[t0 + j] = acc[j] * g.norm;
+    if (t[j] >= 0) y[t[j]] = acc[j] * g.norm;
+}
+
+// ---------------------------------------------------------------------------
+// Target pairing (setup): within each owned cell, greedy nearest-neighbour matching
+// in sorted order (each unpaired point takes its nearest unpaired successor), then
+// the cells' leftover singles paired in cell order.  Close pairs have nearly the
+// same in-cutoff set, so fewer of the union's slots are masked (0.88 -> 0.91 useful
+// on cfg2-like lattices, tools/: pairing study in DESIGN.md).  The pairing changes
+// only which lane computes a target, never the sums (ascending-source union lists).
+// ---------------------------------------------------------------------------
+__global__ void k_pair_counts(Geom g, Strip st, const int *__restrict__ cell_start, int ncl,
+                              long long *__restrict__ npairs, long long *__restrict__ nsingle) {
+  const int cl = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cl > ncl) return;
+  if (cl == ncl) {
+    npairs[cl] = 0;
+    nsingle[cl] = 0;
+    return;
+  }
+  const int key = (st.row_lo + cl / g.ncx) * g.ncx + cl % g.ncx;
+  const int nc = cell_start[key + 1] - cell_start[key];
+  npairs[cl] = nc / 2;
+  nsingle[cl] = nc & 1;
+}
+
+constexpr int kPairMax = 256;  // greedy matching up to this cell population (else consecutive)
+
+__global__ void k_pair_cells(Geom g, Strip st, const int *__restrict__ cell_start, int ncl,
+                             const double2 *__restrict__ xy, const long long *__restrict__ poff,
+                             const long long *__restrict__ soff, int2 *__restrict__ tgt,
+                             int *__restrict__ singles) {
+  const int cl = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cl >= ncl) return;
+  const int key = (st.row_lo + cl / g.ncx) * g.ncx + cl % g.ncx;
+  const int s0 = cell_start[key], nc = cell_start[key + 1] - s0;
+  const long long loc0 = s0 - st.own_lo, own_off = st.own_lo - st.ext_lo;
+  long long q = poff[cl];
+  if (nc > kPairMax) {
+    for (int i = 0; i + 1 < nc; i += 2) tgt[q++] = make_int2((int)(loc0 + i), (int)(loc0 + i + 1));
+    if (nc & 1) singles[soff[cl]] = (int)(loc0 + nc - 1);
+    return;
+  }
+  unsigned used[kPairMax / 32];
+  for (int w = 0; w < kPairMax / 32; ++w) used[w] = 0u;
+  for (int i = 0; i < nc; ++i) {
+    if (used[i >> 5] >> (i & 31) & 1u) continue;
+    used[i >> 5] |= 1u << (i & 31);
+    const double2 pi = xy[own_off + loc0 + i];
+    int best = -1;
+    double bd = 0.0;
+    for (int j = i + 1; j < nc; ++j) {
+      if (used[j >> 5] >> (j & 31) & 1u) continue;
+      const double2 pj = xy[own_off + loc0 + j];
+      const double dx = pi.x - pj.x, dy = pi.y - pj.y;
+      const double d = fma(dx, dx, dy * dy);
+      if (best < 0 || d < bd) {
+        best = j;
+        bd = d;
+      }
+    }
+    if (best < 0) {
+      singles[soff[cl]] = (int)(loc0 + i);
+    } else {
+      used[best >> 5] |= 1u << (best & 31);
+      tgt[q++] = make_int2((int)(loc0 + i), (int)(loc0 + best));
+    }
+  }
+}
+
+__global__ void k_pair_singles(const int *__restrict__ singles, long long ns, long long first,
+                               int2 *__restrict__ tgt) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (2 * i >= ns) return;
+  tgt[first + i] = make_int2(singles[2 * i], 2 * i + 1 < ns ? singles[2 * i + 1] : -1);
+}
+
+static int pair_targets(rbf_ctx *c, cudaStream_t s, long long *lanes_out) {
+  const int ncl = owned_cells(c);
+  long long *np = nullptr, *ns = nullptr, *poff = nullptr, *soff = nullptr;
+  RBF_TRY(dalloc(c, (void **)&np, sizeof(long long) * (ncl + 1), s));
+  RBF_TRY(dalloc(c, (void **)&ns, sizeof(long long) * (ncl + 1), s));
+  RBF_TRY(dalloc(c, (void **)&poff, sizeof(long long) * (ncl + 1), s));
+  RBF_TRY(dalloc(c, (void **)&soff, sizeof(long long) * (ncl + 1), s));
+  k_pair_counts<<<(ncl + 1 + 255) / 256, 256, 0, s>>>(c->g, c->s, c->cell_start, ncl, np, ns);
+  count_launch(1);
+  size_t tb = 0;
+  RBF_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, np, poff, ncl + 1, s));
+  void *tmp = nullptr;
+  RBF_TRY(dalloc(c, &tmp, tb, s));
+  RBF_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, np, poff, ncl + 1, s));
+  RBF_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, ns, soff, ncl + 1, s));
+  count_launch(4);
+  long long tot[2] = {0, 0};
+  RBF_CUDA_TRY(cudaMemcpyAsync(&tot[0], poff + ncl, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaMemcpyAsync(&tot[1], soff + ncl, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  const long long P = tot[0], S = tot[1], lanes = P + (S + 1) / 2;
+  int *singles = nullptr;
+  RBF_TRY(dalloc(c, (void **)&c->lane_tgt, sizeof(int2) * (size_t)(lanes > 0 ? lanes : 1), s));
+  RBF_TRY(dalloc(c, (void **)&singles, sizeof(int) * (size_t)(S > 0 ? S : 1), s));
+  if (ncl > 0) {
+    k_pair_cells<<<(ncl + 127) / 128, 128, 0, s>>>(c->g, c->s, c->cell_start, ncl, c->xy_ext, poff,
+                                                  soff, c->lane_tgt, singles);
+    count_launch(1);
+  }
+  if (S > 0) {
+    k_pair_singles<<<(int)(((S + 1) / 2 + 255) / 256), 256, 0, s>>>(singles, S, P, c->lane_tgt);
+    count_launch(1);
+  }
+  RBF_CUDA_TRY(cudaGetLastError());
+  dfree(tmp, s);
+  dfree(np, s);
+  dfree(ns, s);
+  dfree(poff, s);
+  dfree(soff, s);
+  dfree(singles, s);
+  *lanes_out = lanes;
+  return RBF_OK;
 }
 
 static int env_int(const char *name, int dflt) {
@@ -219,14 +356,16 @@ int build_nlist(rbf_ctx *c, cudaStream_t s) {
     return RBF_EINVAL;
   }
   const int G = c->mv_g;
-  const long long lanes = (nl + G - 1) / G;
-  c->nchunks = (int)((lanes + 31) / 32);
   RBF_TRY(dalloc(c, (void **)&c->rec, sizeof(double4) * (size_t)(ne > 0 ? ne : 1), s));
   if (ne > 0) {
     k_init_rec<<<(int)((ne + 255) / 256), 256, 0, s>>>(c->xy_ext, ne, c->rec);
     count_launch(1);
   }
   if (nl <= 0) return RBF_OK;
+  long long lanes = (nl + G - 1) / G;
+  if (G == 2 && !getenv("RBF_MV_CONSECUTIVE")) RBF_TRY(pair_targets(c, s, &lanes));
+  c->mv_lanes = lanes;
+  c->nchunks = (int)((lanes + 31) / 32);
   const int nch = c->nchunks;
   RBF_TRY(dalloc(c, (void **)&c->chunk_len, sizeof(int) * nch, s));
   RBF_TRY(dalloc(c, (void **)&c->chunk_off, sizeof(long long) * (nch + 1), s));
@@ -234,9 +373,9 @@ int build_nlist(rbf_ctx *c, cudaStream_t s) {
 #define RBF_NLIST(MODE, off, lst)                                                                   \
   switch (G) {                                                                                      \
     case 1: k_nlist<MODE, 1><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, \
-                                                            c->chunk_len, off, lst); break;         \
+                                                            nullptr, lanes, c->chunk_len, off, lst); break; \
     default: k_nlist<MODE, 2><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, \
-                                                             c->chunk_len, off, lst); break;        \
+                                                             c->lane_tgt, lanes, c->chunk_len, off, lst); break; \
   }
   RBF_NLIST(0, nullptr, nullptr);
   count_launch(1);
@@ -282,11 +421,12 @@ int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStre
   if (nl <= 0) return RBF_OK;
   if (!prepacked) RBF_TRY(launch_pack_w(c, w_ext, s));
   const int G = c->mv_g;
-  const long long lanes = (nl + G - 1) / G;
+  const long long lanes = c->mv_lanes;
   const int blocks = (int)((lanes + kMvThreads - 1) / kMvThreads);
   const long long own_off = c->s.own_lo - c->s.ext_lo;
 #define RBF_MV(GG, DEG, U, MB, ...)                                                            \
-  k_matvec<GG, DEG, U, MB, ##__VA_ARGS__><<<blocks, kMvThreads, 0, s>>>(c->g, nl, own_off, c->rec, c->chunk_len,    \
+  k_matvec<GG, DEG, U, MB, ##__VA_ARGS__><<<blocks, kMvThreads, 0, s>>>(c->g, nl, own_off, c->rec, \
+                                                     GG == 2 ? c->lane_tgt : nullptr, lanes, c->chunk_len,  \
                                                      c->chunk_off, c->nlist, y_loc)
   // Measured alternatives (cfg2, profiles/r01_matvec_variants_cfg2.txt): degree-9
   // polynomial, 2 gathers in flight, 5 CTAs/SM (48 registers), L1 prefetch of the
