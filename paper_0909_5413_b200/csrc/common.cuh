@@ -188,7 +188,7 @@ struct rbf_ctx {
   int mv_var = 0;              // matvec kernel variant (A/B measurements only)
   int mv_g = 2;                // targets per lane (union lists with per-target mask bits)
   long long mv_lanes = 0;      // lanes (target pairs) of the owned range
-  int2 *lane_tgt = nullptr;    // per lane: its two local targets (-1 = none), nearest-neighbour pairs
+  int4 *lane_tgt = nullptr;    // per lane: its G local targets (-1 = none), nearest-neighbour groups
   int nchunks = 0;
   int *chunk_len = nullptr;    // per chunk: list length (max over its lanes, multiple of 4)
   long long *chunk_off = nullptr;  // per chunk (+1): first entry

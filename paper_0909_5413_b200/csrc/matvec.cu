@@ -73,12 +73,13 @@ struct MvIdx {
 // The G local targets of lane lt: tgt[lt] (pairs chosen at setup, -1 = none) when
 // given, else G consecutive targets.
 template <int G>
-__device__ __forceinline__ void lane_targets(const int2 *__restrict__ tgt, long long lt, long long nloc,
+__device__ __forceinline__ void lane_targets(const int4 *__restrict__ tgt, long long lt, long long nloc,
                                              long long nlanes, long long *t) {
-  if (G == 2 && tgt) {
-    const int2 v = lt < nlanes ? tgt[lt] : make_int2(-1, -1);
-    t[0] = v.x;
-    t[G - 1] = v.y;
+  if (G >= 2 && tgt) {
+    const int4 v = lt < nlanes ? tgt[lt] : make_int4(-1, -1, -1, -1);
+    const int vv[3] = {v.x, v.y, v.z};
+#pragma unroll
+    for (int j = 0; j < G; ++j) t[j] = vv[j];
   } else {
 #pragma unroll
     for (int j = 0; j < G; ++j) t[j] = lt * G + j < nloc ? lt * G + j : -1;
@@ -88,7 +89,7 @@ __device__ __forceinline__ void lane_targets(const int2 *__restrict__ tgt, long 
 template <int MODE, int G>
 __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const double2 *__restrict__ xy,
                                                       const int *__restrict__ cell_start, long long nloc,
-                                                      const int2 *__restrict__ tgt, long long nlanes,
+                                                      const int4 *__restrict__ tgt, long long nlanes,
                                                       int *__restrict__ chunk_len,
                                                       const long long *__restrict__ chunk_off,
                                                       unsigned *__restrict__ list) {
@@ -171,7 +172,7 @@ __device__ __forceinline__ void prefetch_l1(const void *p) {
 template <int G, int DEG, int U, int MINB, bool PF = false>
 __global__ __launch_bounds__(kMvThreads, MINB) void k_matvec(
     Geom g, long long nloc, long long own_off, const double4 *__restrict__ rec,
-    const int2 *__restrict__ tgt, long long nlanes,
+    const int4 *__restrict__ tgt, long long nlanes,
     const int *__restrict__ chunk_len, const long long *__restrict__ chunk_off,
     const unsigned *__restrict__ list, double *__restrict__ y) {
   const int lane = threadIdx.x & 31;
@@ -231,80 +232,92 @@ __global__ __launch_bounds__(kMvThreads, MINB) void k_matvec(
 // on cfg2-like lattices, tools/: pairing study in DESIGN.md).  The pairing changes
 // only which lane computes a target, never the sums (ascending-source union lists).
 // ---------------------------------------------------------------------------
-__global__ void k_pair_counts(Geom g, Strip st, const int *__restrict__ cell_start, int ncl,
-                              long long *__restrict__ npairs, long long *__restrict__ nsingle) {
+__global__ void k_pair_counts(Geom g, Strip st, const int *__restrict__ cell_start, int ncl, int gs,
+                              long long *__restrict__ ngroups, long long *__restrict__ nsingle) {
   const int cl = blockIdx.x * blockDim.x + threadIdx.x;
   if (cl > ncl) return;
   if (cl == ncl) {
-    npairs[cl] = 0;
+    ngroups[cl] = 0;
     nsingle[cl] = 0;
     return;
   }
   const int key = (st.row_lo + cl / g.ncx) * g.ncx + cl % g.ncx;
   const int nc = cell_start[key + 1] - cell_start[key];
-  npairs[cl] = nc / 2;
-  nsingle[cl] = nc & 1;
+  ngroups[cl] = nc / gs;
+  nsingle[cl] = nc % gs;
 }
 
-constexpr int kPairMax = 256;  // greedy matching up to this cell population (else consecutive)
+constexpr int kPairMax = 256;  // greedy grouping up to this cell population (else consecutive)
 
-__global__ void k_pair_cells(Geom g, Strip st, const int *__restrict__ cell_start, int ncl,
+// Groups of gs (2 or 3) targets: each unused point in sorted order takes its gs-1
+// nearest unused successors in the cell; the remaining n_c mod gs points go to the
+// singles list (grouped in cell order afterwards).
+__global__ void k_pair_cells(Geom g, Strip st, const int *__restrict__ cell_start, int ncl, int gs,
                              const double2 *__restrict__ xy, const long long *__restrict__ poff,
-                             const long long *__restrict__ soff, int2 *__restrict__ tgt,
+                             const long long *__restrict__ soff, int4 *__restrict__ tgt,
                              int *__restrict__ singles) {
   const int cl = blockIdx.x * blockDim.x + threadIdx.x;
   if (cl >= ncl) return;
   const int key = (st.row_lo + cl / g.ncx) * g.ncx + cl % g.ncx;
   const int s0 = cell_start[key], nc = cell_start[key + 1] - s0;
   const long long loc0 = s0 - st.own_lo, own_off = st.own_lo - st.ext_lo;
-  long long q = poff[cl];
+  long long q = poff[cl], sq = soff[cl];
+  const int ngr = nc / gs;
   if (nc > kPairMax) {
-    for (int i = 0; i + 1 < nc; i += 2) tgt[q++] = make_int2((int)(loc0 + i), (int)(loc0 + i + 1));
-    if (nc & 1) singles[soff[cl]] = (int)(loc0 + nc - 1);
+    for (int gi = 0; gi < ngr; ++gi) {
+      const int i = gi * gs;
+      tgt[q++] = make_int4((int)(loc0 + i), (int)(loc0 + i + 1), gs > 2 ? (int)(loc0 + i + 2) : -1, -1);
+    }
+    for (int i = ngr * gs; i < nc; ++i) singles[sq++] = (int)(loc0 + i);
     return;
   }
   unsigned used[kPairMax / 32];
   for (int w = 0; w < kPairMax / 32; ++w) used[w] = 0u;
-  for (int i = 0; i < nc; ++i) {
+  int made = 0;
+  for (int i = 0; i < nc && made < ngr; ++i) {
     if (used[i >> 5] >> (i & 31) & 1u) continue;
     used[i >> 5] |= 1u << (i & 31);
     const double2 pi = xy[own_off + loc0 + i];
-    int best = -1;
-    double bd = 0.0;
+    int b1 = -1, b2 = -1;
+    double d1 = 0.0, d2 = 0.0;
     for (int j = i + 1; j < nc; ++j) {
       if (used[j >> 5] >> (j & 31) & 1u) continue;
       const double2 pj = xy[own_off + loc0 + j];
       const double dx = pi.x - pj.x, dy = pi.y - pj.y;
       const double d = fma(dx, dx, dy * dy);
-      if (best < 0 || d < bd) {
-        best = j;
-        bd = d;
+      if (b1 < 0 || d < d1) {
+        b2 = b1; d2 = d1;
+        b1 = j; d1 = d;
+      } else if (gs > 2 && (b2 < 0 || d < d2)) {
+        b2 = j; d2 = d;
       }
     }
-    if (best < 0) {
-      singles[soff[cl]] = (int)(loc0 + i);
-    } else {
-      used[best >> 5] |= 1u << (best & 31);
-      tgt[q++] = make_int2((int)(loc0 + i), (int)(loc0 + best));
-    }
+    used[b1 >> 5] |= 1u << (b1 & 31);
+    if (gs > 2) used[b2 >> 5] |= 1u << (b2 & 31);
+    tgt[q++] = make_int4((int)(loc0 + i), (int)(loc0 + b1), gs > 2 ? (int)(loc0 + b2) : -1, -1);
+    ++made;
   }
+  for (int i = 0; i < nc; ++i)
+    if (!(used[i >> 5] >> (i & 31) & 1u)) singles[sq++] = (int)(loc0 + i);
 }
 
-__global__ void k_pair_singles(const int *__restrict__ singles, long long ns, long long first,
-                               int2 *__restrict__ tgt) {
+__global__ void k_pair_singles(const int *__restrict__ singles, long long ns, int gs, long long first,
+                               int4 *__restrict__ tgt) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (2 * i >= ns) return;
-  tgt[first + i] = make_int2(singles[2 * i], 2 * i + 1 < ns ? singles[2 * i + 1] : -1);
+  if (gs * i >= ns) return;
+  const long long b = gs * i;
+  tgt[first + i] = make_int4(singles[b], b + 1 < ns ? singles[b + 1] : -1,
+                             (gs > 2 && b + 2 < ns) ? singles[b + 2] : -1, -1);
 }
 
-static int pair_targets(rbf_ctx *c, cudaStream_t s, long long *lanes_out) {
+static int pair_targets(rbf_ctx *c, int gs, cudaStream_t s, long long *lanes_out) {
   const int ncl = owned_cells(c);
   long long *np = nullptr, *ns = nullptr, *poff = nullptr, *soff = nullptr;
   RBF_TRY(dalloc(c, (void **)&np, sizeof(long long) * (ncl + 1), s));
   RBF_TRY(dalloc(c, (void **)&ns, sizeof(long long) * (ncl + 1), s));
   RBF_TRY(dalloc(c, (void **)&poff, sizeof(long long) * (ncl + 1), s));
   RBF_TRY(dalloc(c, (void **)&soff, sizeof(long long) * (ncl + 1), s));
-  k_pair_counts<<<(ncl + 1 + 255) / 256, 256, 0, s>>>(c->g, c->s, c->cell_start, ncl, np, ns);
+  k_pair_counts<<<(ncl + 1 + 255) / 256, 256, 0, s>>>(c->g, c->s, c->cell_start, ncl, gs, np, ns);
   count_launch(1);
   size_t tb = 0;
   RBF_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, np, poff, ncl + 1, s));
@@ -317,17 +330,17 @@ static int pair_targets(rbf_ctx *c, cudaStream_t s, long long *lanes_out) {
   RBF_CUDA_TRY(cudaMemcpyAsync(&tot[0], poff + ncl, sizeof(long long), cudaMemcpyDeviceToHost, s));
   RBF_CUDA_TRY(cudaMemcpyAsync(&tot[1], soff + ncl, sizeof(long long), cudaMemcpyDeviceToHost, s));
   RBF_CUDA_TRY(cudaStreamSynchronize(s));
-  const long long P = tot[0], S = tot[1], lanes = P + (S + 1) / 2;
+  const long long P = tot[0], S = tot[1], lanes = P + (S + gs - 1) / gs;
   int *singles = nullptr;
-  RBF_TRY(dalloc(c, (void **)&c->lane_tgt, sizeof(int2) * (size_t)(lanes > 0 ? lanes : 1), s));
+  RBF_TRY(dalloc(c, (void **)&c->lane_tgt, sizeof(int4) * (size_t)(lanes > 0 ? lanes : 1), s));
   RBF_TRY(dalloc(c, (void **)&singles, sizeof(int) * (size_t)(S > 0 ? S : 1), s));
   if (ncl > 0) {
-    k_pair_cells<<<(ncl + 127) / 128, 128, 0, s>>>(c->g, c->s, c->cell_start, ncl, c->xy_ext, poff,
+    k_pair_cells<<<(ncl + 127) / 128, 128, 0, s>>>(c->g, c->s, c->cell_start, ncl, gs, c->xy_ext, poff,
                                                   soff, c->lane_tgt, singles);
     count_launch(1);
   }
   if (S > 0) {
-    k_pair_singles<<<(int)(((S + 1) / 2 + 255) / 256), 256, 0, s>>>(singles, S, P, c->lane_tgt);
+    k_pair_singles<<<(int)(((S + gs - 1) / gs + 255) / 256), 256, 0, s>>>(singles, S, gs, P, c->lane_tgt);
     count_launch(1);
   }
   RBF_CUDA_TRY(cudaGetLastError());
@@ -349,7 +362,8 @@ static int env_int(const char *name, int dflt) {
 int build_nlist(rbf_ctx *c, cudaStream_t s) {
   const long long nl = n_loc(c), ne = n_ext(c);
   c->mv_var = env_int("RBF_MV_VAR", 0);  // A/B switch; 0 = default
-  c->mv_g = env_int("RBF_MV_G", 2) == 1 ? 1 : 2;
+  c->mv_g = env_int("RBF_MV_G", 2);
+  if (c->mv_g < 1 || c->mv_g > 3) c->mv_g = 2;
   if (ne >= (1LL << (32 - c->mv_g))) c->mv_g = 1;  // source index must fit beside the mask bits
   if (ne >= (1LL << 31)) {
     set_error("rbf_setup: %lld points in one strip exceed the 31-bit neighbour-list index", ne);
@@ -363,7 +377,7 @@ int build_nlist(rbf_ctx *c, cudaStream_t s) {
   }
   if (nl <= 0) return RBF_OK;
   long long lanes = (nl + G - 1) / G;
-  if (G == 2 && !getenv("RBF_MV_CONSECUTIVE")) RBF_TRY(pair_targets(c, s, &lanes));
+  if (G >= 2 && !getenv("RBF_MV_CONSECUTIVE")) RBF_TRY(pair_targets(c, G, s, &lanes));
   c->mv_lanes = lanes;
   c->nchunks = (int)((lanes + 31) / 32);
   const int nch = c->nchunks;
@@ -374,6 +388,8 @@ int build_nlist(rbf_ctx *c, cudaStream_t s) {
   switch (G) {                                                                                      \
     case 1: k_nlist<MODE, 1><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, \
                                                             nullptr, lanes, c->chunk_len, off, lst); break; \
+    case 3: k_nlist<MODE, 3><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, \
+                                                            c->lane_tgt, lanes, c->chunk_len, off, lst); break; \
     default: k_nlist<MODE, 2><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, \
                                                              c->lane_tgt, lanes, c->chunk_len, off, lst); break; \
   }
@@ -426,12 +442,14 @@ int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStre
   const long long own_off = c->s.own_lo - c->s.ext_lo;
 #define RBF_MV(GG, DEG, U, MB, ...)                                                            \
   k_matvec<GG, DEG, U, MB, ##__VA_ARGS__><<<blocks, kMvThreads, 0, s>>>(c->g, nl, own_off, c->rec, \
-                                                     GG == 2 ? c->lane_tgt : nullptr, lanes, c->chunk_len,  \
+                                                     GG >= 2 ? c->lane_tgt : nullptr, lanes, c->chunk_len,  \
                                                      c->chunk_off, c->nlist, y_loc)
   // Measured alternatives (cfg2, profiles/r01_matvec_variants_cfg2.txt): degree-9
   // polynomial, 2 gathers in flight, 5 CTAs/SM (48 registers), L1 prefetch of the
   // next group's records, G = 1 or 3 -- none faster than this configuration.
   if (G == 1) RBF_MV(1, 10, 4, 1);
+  else if (G == 3 && c->mv_var == 2) RBF_MV(3, 10, 2, 1);
+  else if (G == 3) RBF_MV(3, 10, 4, 1);
   else if (c->mv_var == 1) RBF_MV(2, 9, 4, 1);
   else RBF_MV(2, 10, 4, 1);
 #undef RBF_MV
