@@ -497,3 +497,24 @@ def test_paper_ratio_oracle_parity(paper_sweep, ratio):
     ref = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, rtol=wl.tol)
     assert ref.converged and abs(rep.iterations - ref.iterations) <= 2
     assert rel(lam, ref.x) <= 1e-8
+
+
+# ------------------------------------------------------------------ matvec variants
+
+@pytest.mark.parametrize("env", [{"RBF_MV_G": "1"}, {"RBF_MV_G": "3"}, {"RBF_MV_CONSECUTIVE": "1"},
+                                 {"RBF_MV_VAR": "1"}], ids=["G1", "G3", "consecutive", "deg9"])
+def test_matvec_variants_parity(env, monkeypatch):
+    """Every neighbour-list layout (targets per lane, pairing) and the degree-9 exp
+    give the oracle's matvec; the layouts (same exp) agree bitwise with the default."""
+    wl = SMALL[3]
+    w = np.random.default_rng(41).standard_normal(wl.n)
+    ref = O.matvec_brute(wl.xy, w, wl.sigma, wl.rc)
+    with ctx_for(wl, rings=0) as c:
+        y0 = to_caller(c, c.matvec(c.to_local(torch.from_numpy(w).cuda())))
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    with ctx_for(wl, rings=0) as c:
+        y = to_caller(c, c.matvec(c.to_local(torch.from_numpy(w).cuda())))
+    assert rel(y, ref) <= 1e-12
+    if "RBF_MV_VAR" not in env:
+        assert np.array_equal(y, y0)
