@@ -92,9 +92,9 @@ struct TileShape {
   }
   __host__ __device__ bool fits_tc() const { return T <= kTcMaxTiles && n1p <= 32; }
   __host__ __device__ size_t smem_bytes() const {
-    // tiles + rdiag + max(positions, the S^-1 phase's 10 M tiles + 1 scratch tile)
-    const size_t pos_or_m = (size_t)N * sizeof(double2) > 11 * 64 * 8 ? (size_t)N * sizeof(double2) : 11 * 64 * 8;
-    return ((size_t)T * (T + 1) / 2 * 64 + (size_t)T * 8) * 8 + pos_or_m;
+    // tiles + rdiag + W partials + max(positions, the S^-1 phase's 6 M tiles + 1 scratch)
+    const size_t pos_or_m = (size_t)N * sizeof(double2) > 7 * 64 * 8 ? (size_t)N * sizeof(double2) : 7 * 64 * 8;
+    return ((size_t)T * (T + 1) / 2 * 64 + (size_t)T * 8 + 4 * 64) * 8 + pos_or_m;
   }
 };
 
@@ -314,7 +314,7 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
   const int T = S.T, T0 = S.T0, T1 = S.T1, N = S.N;
   PROBE(0)
   double *rdiag = sm + T * (T + 1) / 2 * 64;
-  double2 *pos = reinterpret_cast<double2 *>(rdiag + T * 8);
+  double2 *pos = reinterpret_cast<double2 *>(rdiag + T * 8 + 4 * 64);  // after rdiag and wpart
 
   // ---- positions in factor order, then A_c = R_c A_rc R_c^T (reading Q10)
   for (int p = tid; p < N; p += kTcThreads) {
@@ -403,24 +403,30 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
   }
 
   PROBE(2)
-  // ---- W = L21 L11^-1 (warps 0..T1-1, one own tile row each, right to left) and
-  //      S^-1 = L22^-T L22^-1 (the other warps; lane = row, one column at a time)
-  if (warp < T1) {
-    const int it = T0 + warp;
+  // ---- W = L21 L11^-1, own tile row r by the warp pair (r, r + 4), right to left: the
+  //      sum over kt > jt of W(it, kt) L(kt, jt) is split by kt parity between the two
+  //      warps (one per sub-partition pair, so twice the DMMA issue rate per row); the
+  //      partner's partial goes through shared memory and a 64-thread named barrier.
+  //      S^-1 = L22^-T L22^-1 concurrently on warp 15.
+  double *wpart = rdiag + T * 8;  // 4 rows x 64 doubles (after rdiag, before the M area)
+  if (warp < 8 && (warp & 3) < T1) {
+    const int r = warp & 3, half = warp >> 2;  // half 0 finishes the tiles
+    const int it = T0 + r;
     double *Wrow = sm + toff(it, 0);
+    const int f0 = frag_rowk(lane, 0), f1 = frag_rowk(lane, 1);
+    const int g0 = frag_colk(lane, 0), g1 = frag_colk(lane, 1);
+    const unsigned bar_id = 1 + r;
     for (int jt = T0 - 1; jt >= 0; --jt) {
       AccSet A, B;  // four independent DMMA chains
       A.zero();
       B.zero();
-      int kt = jt + 1;
-      const int f0 = frag_rowk(lane, 0), f1 = frag_rowk(lane, 1);
-      const int g0 = frag_colk(lane, 0), g1 = frag_colk(lane, 1);
-      for (; kt + 1 < T0; kt += 2) {
-        const double *Lk = sm + toff(kt, jt), *Lk1 = sm + toff(kt + 1, jt);
+      int kt = jt + 1 + half;
+      for (; kt + 2 < T0; kt += 4) {
+        const double *Lk = sm + toff(kt, jt), *Lk2 = sm + toff(kt + 2, jt);
         dmma(A.a0, A.a1, Wrow[kt * 64 + f0], Lk[g0]);
-        dmma(A.b0, A.b1, Wrow[(kt + 1) * 64 + f0], Lk1[g0]);
+        dmma(A.b0, A.b1, Wrow[(kt + 2) * 64 + f0], Lk2[g0]);
         dmma(B.a0, B.a1, Wrow[kt * 64 + f1], Lk[g1]);
-        dmma(B.b0, B.b1, Wrow[(kt + 1) * 64 + f1], Lk1[g1]);
+        dmma(B.b0, B.b1, Wrow[(kt + 2) * 64 + f1], Lk2[g1]);
       }
       if (kt < T0) {
         const double *Lk = sm + toff(kt, jt);
@@ -431,32 +437,41 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
       A.a1 += B.a1;
       A.b0 += B.b0;
       A.b1 += B.b1;
-      acc_finish_rmw(A, sm, it, jt, lane);
-      __syncwarp();
-      // W(it, jt) = C L_d^-1   (B[k][n] = Linv[k][n])
-      const double *D = sm + toff(jt, jt);
-      double *Ct = Wrow + jt * 64;
-      double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int k = 4 * h + (lane & 3), n = lane >> 2;
-        const double bv = (k > n) ? D[swz(n, k)] : (k == n ? rdiag[jt * 8 + k] : 0.0);
-        dmma(d0, d1, Ct[frag_rowk(lane, h)], bv);
+      if (half == 1) {
+        *reinterpret_cast<double2 *>(wpart + r * 64 + 2 * lane) = make_double2(A.a0 + A.b0, A.a1 + A.b1);
       }
-      __syncwarp();
-      *reinterpret_cast<double2 *>(Ct + frag_acc(lane)) = make_double2(d0, d1);
-      __syncwarp();
+      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+      if (half == 0) {
+        const double2 pp = *reinterpret_cast<const double2 *>(wpart + r * 64 + 2 * lane);
+        A.a0 += pp.x;
+        A.a1 += pp.y;
+        acc_finish_rmw(A, sm, it, jt, lane);
+        __syncwarp();
+        // W(it, jt) = C L_d^-1   (B[k][n] = Linv[k][n])
+        const double *D = sm + toff(jt, jt);
+        double *Ct = Wrow + jt * 64;
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k = 4 * h + (lane & 3), n = lane >> 2;
+          const double bv = (k > n) ? D[swz(n, k)] : (k == n ? rdiag[jt * 8 + k] : 0.0);
+          dmma(d0, d1, Ct[frag_rowk(lane, h)], bv);
+        }
+        __syncwarp();
+        *reinterpret_cast<double2 *>(Ct + frag_acc(lane)) = make_double2(d0, d1);
+      }
+      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
     }
-  } else if (warp == T1) {
+  } else if (warp == 15) {
     // S^-1 = L22^-T L22^-1 on tiles with the tensor cores (one warp, a few dozen DMMA):
     //   M = L22^-1:  M(a,a) = L_a^-1 (already formed by the diagonal factorization),
     //                M(a,b) = -L_a^-1 sum_{k=b}^{a-1} L22(a,k) M(k,b),   a > b;
     //   S^-1(a,b) = sum_{k>=a} M(k,a)^T M(k,b),   a >= b  (row a last touches L_a^-1,
     //   so each row's diagonal tile is written last, over the L_a / L_a^-1 storage).
-    // M lives in the positions buffer (dead after the factorization) + one scratch tile.
+    // M (strictly lower tiles) lives in the positions buffer (dead after the factorisation).
     double *Mt = reinterpret_cast<double *>(pos);
-    double *scr = Mt + 10 * 64;
-    auto mt = [&](int a, int b) { return Mt + ((a * (a + 1)) / 2 + b) * 64; };
+    double *scr = Mt + 6 * 64;
+    auto mt = [&](int a, int b) { return Mt + ((a * (a - 1)) / 2 + b) * 64; };  // a > b only
     const int m_ = lane >> 2, q_ = lane & 3;
     // Linv_a fragments: as A (A[m][k] = Linv[m][k]) or B (B[k][n] = Linv[k][n]); Linv[r][c]
     // (r > c) is stored at (c, r) of the diagonal tile, 1 / L_rr in rdiag.
