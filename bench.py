@@ -328,7 +328,8 @@ def run_ours(args, rank, world):
             "matvec_fp64_frac_useful": gpairs * 1e9 * FLOP_PER_PAIR / (FP64_PEAK_TFLOPS * 1e12),
             "rasm_apply_gbs": pc_alg_bytes / (pc_ms * 1e-3) / 1e9,
             "step_ms": [round(x, 3) for x in ms],
-            "step_setup_solve_ms": [[round(sd["total"], 2), round(r.ms_total, 2)] for sd, r in zip(setups, reps)],
+            "step_setup_solve_ms": [[round(sd["cell_list"], 2), round(sd["nlist"], 2), round(sd["rasm"], 2),
+                                     round(r.ms_total, 2)] for sd, r in zip(setups, reps)],
             "roofline": roof, "clocks": clk, "gpu_launches": int(launches),
             "e2e": e2e, "cpu_baseline": cpu,
         }

@@ -838,12 +838,10 @@ int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double 
   const long long ldv = n;
   PhaseTimer pt;
   RBF_TRY(pt.init(gp->timing != 0));
-  cudaEvent_t t_begin = nullptr, t_end = nullptr;
-  if (gp->timing) {
-    RBF_CUDA_TRY(cudaEventCreate(&t_begin));
-    RBF_CUDA_TRY(cudaEventCreate(&t_end));
-    RBF_CUDA_TRY(cudaEventRecord(t_begin, s));
-  }
+  cudaEvent_t t_begin = nullptr, t_end = nullptr;  // ms_total (always recorded)
+  RBF_CUDA_TRY(cudaEventCreate(&t_begin));
+  RBF_CUDA_TRY(cudaEventCreate(&t_end));
+  RBF_CUDA_TRY(cudaEventRecord(t_begin, s));
   const int blocks = grid_for(n);
   const bool prepack = c->nranks == 1 && c->ar_grid > 0 && c->rec != nullptr;
 
@@ -966,7 +964,7 @@ int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double 
     }
   }
   double ms_total = 0.0;
-  if (gp->timing) {
+  {
     RBF_CUDA_TRY(cudaEventRecord(t_end, s));
     RBF_CUDA_TRY(cudaEventSynchronize(t_end));
     float ms = 0;
