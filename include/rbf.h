@@ -210,6 +210,11 @@ int rbf_plan_strips(const int64_t *row_counts, int64_t ncy, int32_t nranks, int6
  * global-memory LU path, out[5..6] = ncx, ncy, out[7] = device bytes held. */
 int rbf_info(const rbf_ctx *ctx, int64_t out[8]);
 
+/* Matvec layout facts: out[0] = lanes (target groups), out[1] = chunks of 32 lanes,
+ * out[2] = neighbour-list entries stored (ELL, with padding; 4 bytes each),
+ * out[3] = sum over lanes of the union-list lengths (entries without padding). */
+int rbf_matvec_stats(const rbf_ctx *ctx, int64_t out[4]);
+
 /* Device time (ms, CUDA events) of rbf_setup's phases for this context:
  * out[0] = cell list, out[1] = positions + matvec neighbour list,
  * out[2] = RASM setup (assemble + factor + X), out[3] = whole rbf_setup. */

@@ -181,6 +181,15 @@ int rbf_info(const rbf_ctx *c, int64_t out[8]) {
   return RBF_OK;
 }
 
+int rbf_matvec_stats(const rbf_ctx *c, int64_t out[4]) {
+  if (!c || !out) { set_error("NULL argument"); return RBF_EINVAL; }
+  out[0] = c->mv_lanes;
+  out[1] = c->nchunks;
+  out[2] = c->nlist_entries;
+  out[3] = c->nlist_union;
+  return RBF_OK;
+}
+
 int rbf_get_nccl_id(unsigned char out[128]) {
   if (!out) { set_error("out is NULL"); return RBF_EINVAL; }
   ncclUniqueId id;

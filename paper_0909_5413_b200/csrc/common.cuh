@@ -193,7 +193,8 @@ struct rbf_ctx {
   int *chunk_len = nullptr;    // per chunk: list length (max over its lanes, multiple of 4)
   long long *chunk_off = nullptr;  // per chunk (+1): first entry
   unsigned *nlist = nullptr;      // source index (ext-relative sorted order) | target mask bits
-  long long nlist_entries = 0;
+  long long nlist_entries = 0;  // ELL entries including padding
+  long long nlist_union = 0;    // sum over lanes of the union-list lengths
   // workspaces
   double *w_ext = nullptr;     // n_ext (multi-rank only)
   double *V = nullptr;         // (restart+1) x n_loc Krylov basis

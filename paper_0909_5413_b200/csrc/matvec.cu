@@ -92,7 +92,9 @@ __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const do
                                                       const int4 *__restrict__ tgt, long long nlanes,
                                                       int *__restrict__ chunk_len,
                                                       const long long *__restrict__ chunk_off,
-                                                      unsigned *__restrict__ list) {
+                                                      unsigned *__restrict__ list,
+                                                      unsigned long long *__restrict__ n_union,
+                                                      int *__restrict__ lane_len) {
   const long long lt = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // lane-group
   long long t[G];
   lane_targets<G>(tgt, lt, nloc, nlanes, t);
@@ -139,6 +141,9 @@ __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const do
   const int kmax = (__reduce_max_sync(0xffffffffu, cnt) + 3) & ~3;  // groups of 4
   if (MODE == 0) {
     if (lane == 0 && in_chunk) chunk_len[ch] = kmax;
+    if (lane_len && lt < nlanes) lane_len[lt] = cnt;
+    const int csum = __reduce_add_sync(0xffffffffu, cnt);  // union entries (statistics)
+    if (lane == 0 && csum) atomicAdd(n_union, (unsigned long long)csum);
   } else if (in_chunk) {  // padding: the lane's first target, no mask bit (also idle lanes)
     const unsigned self = (unsigned)(own_off + (act[0] ? t[0] : 0));
     for (int k = cnt; k < kmax; ++k) list[base + ((long long)(k >> 2) * 32 + lane) * 4 + (k & 3)] = self;
@@ -354,6 +359,44 @@ static int pair_targets(rbf_ctx *c, int gs, cudaStream_t s, long long *lanes_out
   return RBF_OK;
 }
 
+// Lanes sorted by union-list length (descending) inside windows of kSortWin lanes, so
+// the 32 lanes of a chunk have similar lengths and the ELL padding (chunk length =
+// its longest lane) shrinks; windows keep the chunks spatially compact.  Ties keep
+// the original order (deterministic).  Also writes the chunk lengths.
+constexpr int kSortWin = 256;
+__global__ __launch_bounds__(kSortWin) void k_sort_lanes(const int *__restrict__ len,
+                                                         const int4 *__restrict__ tgt_in,
+                                                         long long nlanes, int4 *__restrict__ tgt_out,
+                                                         int *__restrict__ chunk_len) {
+  __shared__ int key[kSortWin];
+  __shared__ int idx[kSortWin];
+  const int t = threadIdx.x;
+  const long long base = (long long)blockIdx.x * kSortWin, l = base + t;
+  key[t] = l < nlanes ? len[l] : -1;
+  idx[t] = t;
+  __syncthreads();
+  for (int size = 2; size <= kSortWin; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const int p = t ^ stride;
+      if (p > t) {
+        // descending by key, ascending by idx on ties, within bitonic sequences
+        const bool up = (t & size) == 0;
+        const bool before = key[t] > key[p] || (key[t] == key[p] && idx[t] < idx[p]);
+        if (before != up) {
+          const int k0 = key[t], i0 = idx[t];
+          key[t] = key[p];
+          idx[t] = idx[p];
+          key[p] = k0;
+          idx[p] = i0;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (l < nlanes) tgt_out[l] = tgt_in[base + idx[t]];
+  if ((t & 31) == 0 && l < nlanes) chunk_len[l >> 5] = (key[t] + 3) & ~3;
+}
+
 static int env_int(const char *name, int dflt) {
   const char *v = getenv(name);
   return (v && *v) ? atoi(v) : dflt;
@@ -387,15 +430,33 @@ int build_nlist(rbf_ctx *c, cudaStream_t s) {
 #define RBF_NLIST(MODE, off, lst)                                                                   \
   switch (G) {                                                                                      \
     case 1: k_nlist<MODE, 1><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, \
-                                                            nullptr, lanes, c->chunk_len, off, lst); break; \
+                                                            nullptr, lanes, c->chunk_len, off, lst, nu, ll); break; \
     case 3: k_nlist<MODE, 3><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, \
-                                                            c->lane_tgt, lanes, c->chunk_len, off, lst); break; \
+                                                            c->lane_tgt, lanes, c->chunk_len, off, lst, nu, ll); break; \
     default: k_nlist<MODE, 2><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, \
-                                                             c->lane_tgt, lanes, c->chunk_len, off, lst); break; \
+                                                             c->lane_tgt, lanes, c->chunk_len, off, lst, nu, ll); break; \
   }
+  unsigned long long *nu = nullptr;
+  RBF_TRY(dalloc(c, (void **)&nu, sizeof(unsigned long long), s));
+  RBF_CUDA_TRY(cudaMemsetAsync(nu, 0, sizeof(unsigned long long), s));
+  int *ll = nullptr;
+  const bool sort_lanes = G >= 2 && c->lane_tgt && !getenv("RBF_MV_NOSORT");
+  if (sort_lanes) RBF_TRY(dalloc(c, (void **)&ll, sizeof(int) * (size_t)lanes, s));
   RBF_NLIST(0, nullptr, nullptr);
   count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
+  if (sort_lanes) {
+    int4 *sorted = nullptr;
+    RBF_TRY(dalloc(c, (void **)&sorted, sizeof(int4) * (size_t)lanes, s));
+    k_sort_lanes<<<(int)((lanes + kSortWin - 1) / kSortWin), kSortWin, 0, s>>>(ll, c->lane_tgt, lanes,
+                                                                             sorted, c->chunk_len);
+    count_launch(1);
+    RBF_CUDA_TRY(cudaGetLastError());
+    dfree(c->lane_tgt, s);
+    c->lane_tgt = sorted;
+    dfree(ll, s);
+    ll = nullptr;
+  }
   // offsets (in entries) = exclusive scan of 32 * len
   long long *w64 = nullptr;
   RBF_TRY(dalloc(c, (void **)&w64, sizeof(long long) * (nch + 1), s));
@@ -409,11 +470,15 @@ int build_nlist(rbf_ctx *c, cudaStream_t s) {
   RBF_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, w64, c->chunk_off, nch + 1, s));
   count_launch(2);
   long long total = 0;
+  unsigned long long hnu = 0;
   RBF_CUDA_TRY(cudaMemcpyAsync(&total, c->chunk_off + nch, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaMemcpyAsync(&hnu, nu, sizeof(hnu), cudaMemcpyDeviceToHost, s));
   RBF_CUDA_TRY(cudaStreamSynchronize(s));
   dfree(tmp, s);
   dfree(w64, s);
   c->nlist_entries = total;
+  c->nlist_union = (long long)hnu;
+  dfree(nu, s);
   RBF_TRY(dalloc(c, (void **)&c->nlist, sizeof(unsigned) * (size_t)(total > 0 ? total : 1), s));
   RBF_NLIST(1, c->chunk_off, c->nlist);
 #undef RBF_NLIST

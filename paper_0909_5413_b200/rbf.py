@@ -56,7 +56,7 @@ EXPORTS = ["rbf_get_nccl_id", "rbf_setup", "rbf_local_count", "rbf_ext_count", "
            "rbf_rasm_apply", "rbf_matvec_ext", "rbf_rasm_apply_ext", "rbf_solve",
            "rbf_interpolate_host", "rbf_count_pairs", "rbf_dot", "rbf_plan_strips",
            "rbf_last_error", "rbf_destroy", "rbf_info", "rbf_launch_count", "rbf_setup_times",
-           "rbf_plan_halo", "rbf_evaluate"]
+           "rbf_plan_halo", "rbf_evaluate", "rbf_matvec_stats"]
 
 _lib = None
 
@@ -88,6 +88,7 @@ def lib() -> C.CDLL:
                                                p, C.POINTER(Report), p]),
             "rbf_count_pairs": (C.c_int, [p, p, p]),
             "rbf_evaluate": (C.c_int, [p, p, i64, p, p, p]),
+            "rbf_matvec_stats": (C.c_int, [p, p]),
             "rbf_dot": (C.c_int, [p, p, p, p, p]),
             "rbf_plan_strips": (C.c_int, [p, i64, i32, i64, p]),
             "rbf_last_error": (C.c_char_p, []),
@@ -304,6 +305,11 @@ class Context:
         o = np.zeros(4, dtype=np.float64)
         _check(lib().rbf_setup_times(self._h, o.ctypes.data_as(C.c_void_p)))
         return dict(zip(["cell_list", "nlist", "rasm", "total"], map(float, o)))
+
+    def matvec_stats(self) -> dict:
+        o = (C.c_int64 * 4)()
+        _check(lib().rbf_matvec_stats(self._h, o))
+        return dict(zip(["lanes", "chunks", "ell_entries", "union_entries"], map(int, o)))
 
     def count_pairs(self) -> int:
         v = C.c_int64()

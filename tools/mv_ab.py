@@ -31,7 +31,7 @@ for v in sys.argv[2:] or ["2:0", "1:1"]:
     ms = e0.elapsed_time(e1) / 50
     res[v] = y.clone()
     print(f"cfg{cfg} G:VAR={v}: {ms:.4f} ms/matvec, {npairs / ms / 1e6:.1f} Gpairs/s, "
-          f"useful FP64 frac {npairs * 38 / (ms * 1e-3) / 33.96e12:.3f}, setup {c.setup_times()}", flush=True)
+          f"useful FP64 frac {npairs * 38 / (ms * 1e-3) / 36.86e12:.3f}, stats {c.matvec_stats()} pairs {npairs}", flush=True)
     c.close()
 vals = list(res.values())
 for k, b in zip(list(res)[1:], vals[1:]):
