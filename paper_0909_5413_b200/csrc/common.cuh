@@ -62,8 +62,8 @@ struct Strip {
   long long ext_lo, own_lo, own_hi, ext_hi;  // global sorted positions
 };
 
-constexpr int kRedBlocks = 296;   // 2 x 148 SMs: fixed grid for deterministic reductions
-constexpr int kRedThreads = 256;
+constexpr int kRedBlocks = 592;   // 4 x 148 SMs: fixed grid for deterministic reductions
+constexpr int kRedThreads = 512;
 
 struct Halo {  // one direction of a halo exchange, in element offsets
   long long send_off, send_cnt;  // relative to the owned (local) vector

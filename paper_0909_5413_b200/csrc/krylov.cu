@@ -92,16 +92,30 @@ __global__ __launch_bounds__(kRedThreads) void k_axpy_dot(const double *__restri
     for (int r = 0; r < P; ++r) a += coef[r];
   }
   const long long stride = (long long)gridDim.x * blockDim.x;
-  double acc = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
-    double wi = w[i];
-    if (coef) {
-      wi = fma(-a, x[i], wi);
-      w[i] = wi;
+  // 4 elements in flight per thread (strided, coalesced), 4 partial sums combined in
+  // a fixed order: deterministic for a fixed grid
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const bool alias = v == w;
+  for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
+    double wv[4], vv[4], xv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long i = i0 + u * stride;
+      wv[u] = i < n ? w[i] : 0.0;
+      vv[u] = i < n ? v[i] : 0.0;
+      xv[u] = (coef && i < n) ? x[i] : 0.0;
     }
-    acc = fma(wi, v[i], acc);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long i = i0 + u * stride;
+      if (coef) {
+        wv[u] = fma(-a, xv[u], wv[u]);
+        if (i < n) w[i] = wv[u];
+      }
+      acc[u] = fma(wv[u], alias ? wv[u] : vv[u], acc[u]);  // v may alias w (norm of the update)
+    }
   }
-  double bs = block_sum(acc, sh);
+  double bs = block_sum((acc[0] + acc[1]) + (acc[2] + acc[3]), sh);
   grid_finish(bs, blk, count, out);
 }
 
