@@ -74,15 +74,15 @@ struct MvIdx {
 // given, else G consecutive targets.
 template <int G>
 __device__ __forceinline__ void lane_targets(const int4 *__restrict__ tgt, long long lt, long long nloc,
-                                             long long nlanes, long long *t) {
+                                             long long nlanes, int *t) {
   if (G >= 2 && tgt) {
     const int4 v = lt < nlanes ? tgt[lt] : make_int4(-1, -1, -1, -1);
-    const int vv[3] = {v.x, v.y, v.z};
-#pragma unroll
-    for (int j = 0; j < G; ++j) t[j] = vv[j];
+    t[0] = v.x;
+    if (G > 1) t[1] = v.y;
+    if (G > 2) t[G - 1] = v.z;
   } else {
 #pragma unroll
-    for (int j = 0; j < G; ++j) t[j] = lt * G + j < nloc ? lt * G + j : -1;
+    for (int j = 0; j < G; ++j) t[j] = lt * G + j < nloc ? (int)(lt * G + j) : -1;
   }
 }
 
@@ -96,7 +96,7 @@ __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const do
                                                       unsigned long long *__restrict__ n_union,
                                                       int *__restrict__ lane_len) {
   const long long lt = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // lane-group
-  long long t[G];
+  int t[G];
   lane_targets<G>(tgt, lt, nloc, nlanes, t);
   const int lane = threadIdx.x & 31;
   const long long ch = lt >> 5;
@@ -184,7 +184,7 @@ __global__ __launch_bounds__(kMvThreads, MINB) void k_matvec(
   const long long lt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long ch = lt >> 5;
   if ((ch << 5) >= nlanes) return;  // whole warp beyond the last chunk
-  long long t[G];
+  int t[G];
   lane_targets<G>(tgt, lt, nloc, nlanes, t);
   double2 me[G];
   double acc[G];
@@ -516,7 +516,9 @@ int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStre
   else if (G == 3 && c->mv_var == 2) RBF_MV(3, 10, 2, 1);
   else if (G == 3) RBF_MV(3, 10, 4, 1);
   else if (c->mv_var == 1) RBF_MV(2, 9, 4, 1);
-  else RBF_MV(2, 10, 4, 1);
+  else if (c->mv_var == 3) RBF_MV(2, 10, 4, 4);  // 62 registers, 4 CTAs/SM
+  else if (c->mv_var == 4) RBF_MV(2, 10, 4, 1);  // 84 registers, 2 CTAs/SM
+  else RBF_MV(2, 10, 4, 3);                      // 80 registers, 3 CTAs/SM (fastest)
 #undef RBF_MV
   count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
