@@ -121,6 +121,7 @@ __device__ __forceinline__ double exp_neg(double x) {
 // Table-free exp for the cutoff Gaussian (matvec, evaluation); reading Q15.
 // ---------------------------------------------------------------------------
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer shifter
+constexpr int kExpDeg = 9;  // polynomial degree of the default matvec / evaluation exp
 
 // 2^f = 1 + f P(f) on [-1/2, 1/2]: minimax P (Remez on the relative error, DESIGN.md
 // §6), highest coefficient first.  Degree 10: max error 1.5e-16; degree 9: 3.9e-16.

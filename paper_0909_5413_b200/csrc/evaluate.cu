@@ -54,7 +54,7 @@ __global__ __launch_bounds__(256) void k_evaluate(Geom g, const double *__restri
       const double4 o = ld_rec(rec + j);
       const double dx = qx - o.x, dy = qy - o.y;
       const double r2 = fma(dx, dx, dy * dy);
-      if (r2 < g.rc2) acc = fma(o.z, gauss_exp2<10>(r2, g.esc), acc);
+      if (r2 < g.rc2) acc = fma(o.z, gauss_exp2<kExpDeg>(r2, g.esc), acc);
     }
   }
   s[k] = acc * g.norm;

@@ -22,8 +22,9 @@
 //
 // exp() runs on the FP64 pipe with no table: k = round(-r2 log2e/(2s^2)),
 // f = -r2 log2e/(2 s^2) - k in [-1/2, 1/2] (one fma from the exact product), 2^f =
-// 1 + f P(f) with P a minimax polynomial of degree DEG (10: ~1.3 ulp, 9: ~3.5 ulp;
-// reading Q15), 2^k by an integer add to the exponent field.  (A 64-entry table
+// 1 + f P(f) with P a minimax polynomial of degree DEG (default 9: max relative
+// error 3.9e-16 ~ 3.5 ulp; 10: 1.5e-16; reading Q15), 2^k by an integer add to the
+// exponent field.  (A 64-entry table
 // variant, replicated per lane in shared memory, was measured slower: the table
 // loads compete with the gathers for the L1 data pipe; profiles/.)
 //
@@ -509,16 +510,16 @@ int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStre
   k_matvec<GG, DEG, U, MB, ##__VA_ARGS__><<<blocks, kMvThreads, 0, s>>>(c->g, nl, own_off, c->rec, \
                                                      GG >= 2 ? c->lane_tgt : nullptr, lanes, c->chunk_len,  \
                                                      c->chunk_off, c->nlist, y_loc)
-  // Measured alternatives (cfg2, profiles/r01_matvec_variants_cfg2.txt): degree-9
-  // polynomial, 2 gathers in flight, 5 CTAs/SM (48 registers), L1 prefetch of the
-  // next group's records, G = 1 or 3 -- none faster than this configuration.
-  if (G == 1) RBF_MV(1, 10, 4, 1);
-  else if (G == 3 && c->mv_var == 2) RBF_MV(3, 10, 2, 1);
-  else if (G == 3) RBF_MV(3, 10, 4, 1);
+  // Measured alternatives: profiles/r01_matvec_variants_cfg2.txt (2 gathers in flight,
+  // 2/4/5 CTAs per SM, L1 prefetch of the next group's records, G = 1 or 3, the
+  // degree-10 exp: none faster than the default).
+  if (G == 1) RBF_MV(1, kExpDeg, 4, 1);
+  else if (G == 3) RBF_MV(3, kExpDeg, 4, 1);
   else if (c->mv_var == 1) RBF_MV(2, 9, 4, 1);
+  else if (c->mv_var == 2) RBF_MV(2, 10, 4, 3);  // degree-10 exp (1.5e-16), 3 CTAs/SM
   else if (c->mv_var == 3) RBF_MV(2, 10, 4, 4);  // 62 registers, 4 CTAs/SM
   else if (c->mv_var == 4) RBF_MV(2, 10, 4, 1);  // 84 registers, 2 CTAs/SM
-  else RBF_MV(2, 10, 4, 3);                      // 80 registers, 3 CTAs/SM (fastest)
+  else RBF_MV(2, kExpDeg, 4, 3);  // default: degree-9 exp (3.9e-16 = 3.5 ulp), 3 CTAs/SM (fastest)
 #undef RBF_MV
   count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
