@@ -979,160 +979,18 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
   return RBF_OK;
 }
 
-// ---------------------------------------------------------------------------
-// RASM apply, TMA version: a persistent CTA walks its cells; each cell's X block
-// (contiguous, n_own x ld doubles, 16-byte aligned) is fetched by one
-// cp.async.bulk (TMA, SASS UBLKCP) into a shared-memory stage signalled by an
-// mbarrier, double-buffered so the next cell's block streams in from HBM while
-// the current one is multiplied out of shared memory.  Blocks larger than a stage
-// (very dense cells) are streamed with plain 16-byte loads instead.
-// ---------------------------------------------------------------------------
-constexpr int kTmaThreads = 256;
-constexpr int kTmaStageBytes = 48 * 1024;
-
-__device__ __forceinline__ unsigned smem_u32(const void *p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned bytes,
-                                            unsigned long long *bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phase) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-
-__global__ __launch_bounds__(kTmaThreads) void k_rasm_apply_tma(
-    Geom g, Strip st, const int *__restrict__ cell_start, const long long *__restrict__ x_off,
-    const double *__restrict__ X, int ncl, int max_ov, const double *__restrict__ u,
-    double *__restrict__ z) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) unsigned long long bar[2];
-  double *stage[2] = {reinterpret_cast<double *>(smem),
-                      reinterpret_cast<double *>(smem + kTmaStageBytes)};
-  double *su = reinterpret_cast<double *>(smem + 2 * kTmaStageBytes);  // max_ov + 2 doubles
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  unsigned phase[2] = {0u, 0u};
-  auto block_bytes = [&](int cl) -> long long { return 8 * (x_off[cl + 1] - x_off[cl]); };
-  auto issue = [&](int cl, int sidx) {
-    const long long nb = block_bytes(cl);
-    if (nb > 0 && nb <= kTmaStageBytes) {
-      mbar_expect_tx(&bar[sidx], (unsigned)nb);
-      tma_load_1d(stage[sidx], X + x_off[cl], (unsigned)nb, &bar[sidx]);
-    }
-  };
-  int cl = blockIdx.x;
-  if (tid == 0 && cl < ncl) issue(cl, 0);
-  for (int it = 0; cl < ncl; ++it, cl += gridDim.x) {
-    const int sidx = it & 1;
-    const int nxt = cl + gridDim.x;
-    if (tid == 0 && nxt < ncl) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(nxt, sidx ^ 1);
-    }
-    const int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
-    Runs R;
-    block_runs(g, cell_start, cx, cy, R);
-    const long long nb = block_bytes(cl);
-    if (R.n_own > 0) {
-      const int n = R.n_ov;
-      const int ld = (n + 1) & ~1;
-      for (int q = tid; q < ld; q += kTmaThreads)
-        su[q] = (q < n) ? u[nat_to_global(R, q) - st.ext_lo] : 0.0;
-      const double2 *Xc;
-      if (nb <= kTmaStageBytes) {
-        mbar_wait(&bar[sidx], phase[sidx]);
-        phase[sidx] ^= 1u;
-        Xc = reinterpret_cast<const double2 *>(stage[sidx]);
-      } else {
-        Xc = reinterpret_cast<const double2 *>(X + x_off[cl]);
-      }
-      __syncthreads();
-      const double2 *u2 = reinterpret_cast<const double2 *>(su);
-      const int h = ld >> 1;
-      const int o0 = cell_start[cy * g.ncx + cx];
-      for (int o = warp; o < R.n_own; o += kTmaThreads / 32) {
-        const double2 *row = Xc + (long long)o * h;
-        double acc = 0.0, acc2 = 0.0;
-#pragma unroll 4
-        for (int j = lane; j < h; j += 32) {
-          const double2 xv = row[j];
-          const double2 uv = u2[j];
-          acc = fma(xv.x, uv.x, acc);
-          acc2 = fma(xv.y, uv.y, acc2);
-        }
-        acc += acc2;
-#pragma unroll
-        for (int sh = 16; sh > 0; sh >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, sh);
-        if (lane == 0) z[o0 + o - st.own_lo] = acc;
-      }
-    }
-    __syncthreads();  // stage sidx and su free for reuse
-  }
-  (void)max_ov;
-}
-
 int launch_rasm_apply(const rbf_ctx *c, const double *r_ext, double *z_loc, cudaStream_t s) {
   const int ncl = owned_cells(c);
   if (ncl <= 0 || c->nsub == 0) return RBF_OK;
-  static int use_tma = -1;
-  if (use_tma < 0) {
-    const char *e = getenv("RBF_APPLY_TMA");
-    use_tma = (e && e[0] == '1') ? 1 : 0;
-  }
-  if (!use_tma) {
-    const size_t smem = sizeof(double) * (size_t)(c->max_ov + 2);
-    static size_t attr_d = 48 * 1024;
-    if (smem > attr_d) {
-      RBF_CUDA_TRY(cudaFuncSetAttribute(k_rasm_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem));
-      attr_d = smem;
-    }
-    k_rasm_apply<<<ncl, kRaThreads, smem, s>>>(c->g, c->s, c->cell_start, c->x_off, c->X, r_ext,
-                                               z_loc);
-    count_launch(1);
-    RBF_CUDA_TRY(cudaGetLastError());
-    return RBF_OK;
-  }
-  const size_t smem = 2 * (size_t)kTmaStageBytes + sizeof(double) * (size_t)(c->max_ov + 2);
-  static size_t attr_bytes = 0;  // opt-in dynamic shared memory set so far
-  if (smem > attr_bytes) {
-    RBF_CUDA_TRY(cudaFuncSetAttribute(k_rasm_apply_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem = sizeof(double) * (size_t)(c->max_ov + 2);
+  static size_t attr_d = 48 * 1024;
+  if (smem > attr_d) {
+    RBF_CUDA_TRY(cudaFuncSetAttribute(k_rasm_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
-    attr_bytes = smem;
+    attr_d = smem;
   }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int per_sm = smem <= 113 * 1024 ? 2 : 1;
-  const int grid = ncl < sms * per_sm ? ncl : sms * per_sm;
-  k_rasm_apply_tma<<<grid, kTmaThreads, smem, s>>>(c->g, c->s, c->cell_start, c->x_off, c->X, ncl,
-                                                   c->max_ov, r_ext, z_loc);
+  k_rasm_apply<<<ncl, kRaThreads, smem, s>>>(c->g, c->s, c->cell_start, c->x_off, c->X, r_ext,
+                                             z_loc);
   count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
   return RBF_OK;
