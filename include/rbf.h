@@ -80,8 +80,17 @@ typedef struct {
  *                 device first).  RBF_COMM_NONE: "virtual strip" -- the context owns
  *                 strip `rank` of `nranks` but never communicates; only the *_ext
  *                 entry points (caller-supplied halos) are usable.
- *  nccl_id        from rbf_get_nccl_id() on rank 0, broadcast by the caller. */
-enum { RBF_COMM_NONE = 0, RBF_COMM_NCCL = 1 };
+ *                 RBF_COMM_THREADS: all nranks contexts live in ONE process on ONE
+ *                 device, each driven by its own host thread (own stream); halos and
+ *                 the reductions' all-gathers are device copies out of the peer
+ *                 context, ordered by stream synchronisation and a host barrier.  Same
+ *                 semantics and reduction order as NCCL; a transport for running and
+ *                 checking the multi-strip path on one GPU, not a performance path.
+ *                 Every collective call (rbf_matvec, rbf_rasm_apply, rbf_solve) must
+ *                 be made by all nranks threads, or the callers block.
+ *  nccl_id        NCCL: from rbf_get_nccl_id() on rank 0, broadcast by the caller.
+ *                 THREADS: any 128-byte key shared by the group's contexts. */
+enum { RBF_COMM_NONE = 0, RBF_COMM_NCCL = 1, RBF_COMM_THREADS = 2 };
 typedef struct {
   int32_t rank;
   int32_t nranks;

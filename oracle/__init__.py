@@ -75,6 +75,9 @@ def lib():
         L.orc_rasm_free.argtypes = [ptr]
         L.orc_gmres.restype = C.c_int
         L.orc_gmres.argtypes = [ptr, ptr, ptr, i64, i64, dbl, dbl, ptr, ptr, i64, ptr, ptr, ptr]
+        L.orc_gmres_orth.restype = C.c_int
+        L.orc_gmres_orth.argtypes = [ptr, ptr, ptr, i64, i64, dbl, dbl, C.c_int, ptr, ptr, i64, ptr,
+                                     ptr, ptr]
         L.orc_op_identity.argtypes = [ptr, i64]
         L.orc_op_dense.argtypes = [ptr, i64, ptr]
         L.orc_op_rbf.argtypes = [ptr, i64, ptr, dbl, dbl, dbl, dbl, dbl, dbl, dbl, C.c_int]
@@ -314,8 +317,10 @@ def op_rasm(P: Rasm, variant: str = "rasm"):
 
 
 def gmres(opA, opM, b, restart=30, max_iters=1000, rtol=1e-13, atol=0.0,
-          keep_basis=False) -> GmresResult:
-    """Left-preconditioned restarted GMRES(m), MGS, Givens, x0 = 0 (Q12)."""
+          keep_basis=False, orth="mgs") -> GmresResult:
+    """Left-preconditioned restarted GMRES(m), Givens, x0 = 0 (Q12); Arnoldi by
+    modified Gram-Schmidt (orth="mgs", Q12) or classical Gram-Schmidt twice
+    (orth="cgs2", reading Q23)."""
     b = _f64(b)
     n = b.shape[0]
     x = np.empty(n, dtype=np.float64)
@@ -323,8 +328,9 @@ def gmres(opA, opM, b, restart=30, max_iters=1000, rtol=1e-13, atol=0.0,
     rep = _Report()
     V = np.empty((restart + 1, n), dtype=np.float64) if keep_basis else None
     nv = C.c_int64(0)
-    st = lib().orc_gmres(_addr(opA[0]), _addr(opM[0]), _p(b), int(restart), int(max_iters), float(rtol),
-                         float(atol), _p(x), _p(hist), int(max_iters), C.byref(rep),
+    st = lib().orc_gmres_orth(_addr(opA[0]), _addr(opM[0]), _p(b), int(restart), int(max_iters),
+                         float(rtol), float(atol), {"mgs": 0, "cgs2": 1}[orth], _p(x), _p(hist),
+                         int(max_iters), C.byref(rep),
                          _p(V) if V is not None else None, C.byref(nv))
     if st == ORC_EINVAL:
         raise ValueError("invalid GMRES parameters")
@@ -336,7 +342,7 @@ def gmres(opA, opM, b, restart=30, max_iters=1000, rtol=1e-13, atol=0.0,
 
 
 def solve(xy, f, sigma, rc, box, cell, rings=1, restart=30, max_iters=1000, rtol=1e-13,
-          atol=0.0, brute=False) -> GmresResult:
+          atol=0.0, brute=False, orth="mgs") -> GmresResult:
     """Solve A_rc lambda = f by GMRES(restart) left-preconditioned with RASM
     (the paper's KSPSolve)."""
     P = Rasm(xy, sigma, rc, box, cell, rings)
@@ -344,7 +350,7 @@ def solve(xy, f, sigma, rc, box, cell, rings=1, restart=30, max_iters=1000, rtol
         raise ArithmeticError(f"RASM setup failed in cell {P.bad_cell}")
     try:
         return gmres(op_rbf(xy, sigma, rc, box, cell, brute), op_rasm(P), f, restart,
-                     max_iters, rtol, atol)
+                     max_iters, rtol, atol, orth=orth)
     finally:
         P.close()
 

@@ -600,17 +600,22 @@ typedef struct {
   double beta0;          /* ||M^-1 b||                                      */
 } orc_report;
 
-/* Left-preconditioned restarted GMRES(m) with modified Gram-Schmidt and Givens
- * rotations ("we use the GMRES"; reading Q12).  x0 = 0.
+/* Left-preconditioned restarted GMRES(m) with Givens rotations ("we use the
+ * GMRES"; reading Q12).  x0 = 0.  orth selects the Arnoldi
+ * orthogonalisation: 0 = modified Gram-Schmidt (Q12, BJ:5), 1 = classical
+ * Gram-Schmidt applied twice (CGS2: h = V^T w, w -= V h, twice, H column = the sum
+ * of both passes; SURVEY §8.f3 -- the communication-avoiding variant, reading Q23).
  * history[k] = |g_{k+1}| / beta0 after iteration k (up to hist_cap entries).
  * V_out (optional, (m+1) x n) receives the Krylov basis of the last cycle and
  * *v_count the number of basis vectors in it (for the orthogonality pin). */
-int orc_gmres(const orc_op *A, const orc_op *M, const double *b, int64_t restart,
-              int64_t max_iters, double rtol, double atol, double *x, double *history,
-              int64_t hist_cap, orc_report *rep, double *V_out, int64_t *v_count) {
+int orc_gmres_orth(const orc_op *A, const orc_op *M, const double *b, int64_t restart,
+                   int64_t max_iters, double rtol, double atol, int orth, double *x,
+                   double *history, int64_t hist_cap, orc_report *rep, double *V_out,
+                   int64_t *v_count) {
   int64_t n = A->n, m = restart;
   memset(rep, 0, sizeof(*rep));
-  if (m < 1 || rtol < 0.0 || atol < 0.0) return ORC_EINVAL;
+  if (m < 1 || rtol < 0.0 || atol < 0.0 || orth < 0 || orth > 1) return ORC_EINVAL;
+  double *hp = (double *)malloc(sizeof(double) * (size_t)(m + 1)); /* one CGS pass */
   double *V = (double *)malloc(sizeof(double) * (size_t)((m + 1) * n));
   double *H = (double *)calloc((size_t)((m + 1) * m), sizeof(double)); /* H[i*m + k] */
   double *cs = (double *)malloc(sizeof(double) * (size_t)m);
@@ -645,10 +650,21 @@ int orc_gmres(const orc_op *A, const orc_op *M, const double *b, int64_t restart
         double *w = &V[(k + 1) * n];
         op_apply(A, &V[k * n], t); /* w = M^-1 A v_k */
         op_apply(M, t, w);
-        for (int64_t j = 0; j <= k; ++j) { /* modified Gram-Schmidt */
-          double h = dot(n, w, &V[j * n]);
-          H[j * m + k] = h;
-          for (int64_t i = 0; i < n; ++i) w[i] -= h * V[j * n + i];
+        if (orth == 0) {
+          for (int64_t j = 0; j <= k; ++j) { /* modified Gram-Schmidt */
+            double h = dot(n, w, &V[j * n]);
+            H[j * m + k] = h;
+            for (int64_t i = 0; i < n; ++i) w[i] -= h * V[j * n + i];
+          }
+        } else {
+          for (int64_t j = 0; j <= k; ++j) H[j * m + k] = 0.0;
+          for (int pass = 0; pass < 2; ++pass) { /* classical Gram-Schmidt, twice */
+            for (int64_t j = 0; j <= k; ++j) hp[j] = dot(n, w, &V[j * n]);
+            for (int64_t j = 0; j <= k; ++j) {
+              H[j * m + k] += hp[j];
+              for (int64_t i = 0; i < n; ++i) w[i] -= hp[j] * V[j * n + i];
+            }
+          }
         }
         double hn = sqrt(dot(n, w, w));
         H[(k + 1) * m + k] = hn;
@@ -708,8 +724,15 @@ int orc_gmres(const orc_op *A, const orc_op *M, const double *b, int64_t restart
   rep->converged = converged;
   if (status == ORC_OK && !converged) status = ORC_NOT_CONVERGED;
   rep->status = status;
-  free(V); free(H); free(cs); free(sn); free(g); free(yk); free(t); free(r);
+  free(V); free(H); free(cs); free(sn); free(g); free(yk); free(t); free(r); free(hp);
   return status;
+}
+
+int orc_gmres(const orc_op *A, const orc_op *M, const double *b, int64_t restart,
+              int64_t max_iters, double rtol, double atol, double *x, double *history,
+              int64_t hist_cap, orc_report *rep, double *V_out, int64_t *v_count) {
+  return orc_gmres_orth(A, M, b, restart, max_iters, rtol, atol, 0, x, history, hist_cap, rep,
+                        V_out, v_count);
 }
 
 /* Convenience constructors used by the ctypes binding. */

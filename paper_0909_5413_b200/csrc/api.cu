@@ -10,6 +10,8 @@
 
 #include "common.cuh"
 
+#include <mutex>
+
 namespace rbf {
 
 static thread_local std::string g_err;
@@ -34,16 +36,15 @@ int owned_cells(const rbf_ctx *c) { return (c->s.row_hi - c->s.row_lo) * c->g.nc
 // freed memory (release threshold = max), so repeated setup/solve cycles do not
 // return memory to the driver between steps.
 int dalloc(rbf_ctx *c, void **p, size_t bytes, cudaStream_t s) {
-  static bool pool_configured = false;
-  if (!pool_configured) {
+  static std::once_flag pool_configured;
+  std::call_once(pool_configured, [] {
     int dev = 0;
     cudaMemPool_t pool;
     if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
       uint64_t thr = UINT64_MAX;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    pool_configured = true;
-  }
+  });
   if (bytes == 0) bytes = 16;
   cudaError_t e = cudaMallocAsync(p, bytes, s);
   if (e != cudaSuccess) {
@@ -274,7 +275,7 @@ int rbf_setup(rbf_ctx **out, const double *xy, int64_t n, const rbf_params *p, c
   c->n = n;
   if (d) {
     if (d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks ||
-        (d->comm != RBF_COMM_NONE && d->comm != RBF_COMM_NCCL)) {
+        (d->comm != RBF_COMM_NONE && d->comm != RBF_COMM_NCCL && d->comm != RBF_COMM_THREADS)) {
       set_error("rbf_setup: bad rbf_dist (rank %d of %d, comm %d)", d->rank, d->nranks, d->comm);
       delete c;
       return RBF_EINVAL;
@@ -415,7 +416,7 @@ int rbf_solve(rbf_ctx *c, const double *f, const rbf_gmres_params *g, double *la
     set_error("rbf_solve: restart >= 1, max_iters >= 1, rtol >= 0, atol >= 0 required");
     return RBF_EINVAL;
   }
-  if (c->nranks > 1 && c->comm_mode != RBF_COMM_NCCL) {
+  if (c->nranks > 1 && c->comm_mode == RBF_COMM_NONE) {
     set_error("rbf_solve: virtual strip contexts cannot solve (no communicator)");
     return RBF_EUNSUPPORTED;
   }

@@ -6,12 +6,73 @@
 // vicinity") and overlap_rings rows for RASM.  GMRES inner products are
 // reduced by an all-gather of the per-rank partials summed in rank order, so every
 // rank holds bit-identical scalars and runs are deterministic (reading Q14).
+//
+// RBF_COMM_THREADS is a second transport with the same semantics for contexts that
+// live in ONE process on ONE device, one host thread per strip: every exchange is a
+// device-to-device copy out of the peer context's buffers, ordered by stream
+// synchronisations and a host barrier (no kernel ever waits on another context).
+// It exists so the multi-strip solve (halo plans, reduction order, control flow) can
+// be run and checked on a single GPU; it is not a performance path.
 #include "common.cuh"
+
+#include <condition_variable>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
 
 namespace rbf {
 
+struct ThreadGroup {
+  int n = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long gen = 0;
+  std::vector<const double *> ptr[2];  // published per rank
+  std::vector<long long> cnt[2];
+
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const long long g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
+static std::mutex g_groups_mu;
+static std::map<std::string, ThreadGroup *> g_groups;  // process lifetime (test transport)
+
+static int thread_group_join(rbf_ctx *c, const rbf_dist *d) {
+  const std::string key(reinterpret_cast<const char *>(d->nccl_id), 128);
+  std::lock_guard<std::mutex> lk(g_groups_mu);
+  ThreadGroup *&g = g_groups[key];
+  if (!g) {
+    g = new ThreadGroup();
+    g->n = c->nranks;
+    for (int k = 0; k < 2; ++k) {
+      g->ptr[k].assign(c->nranks, nullptr);
+      g->cnt[k].assign(c->nranks, 0);
+    }
+  }
+  if (g->n != c->nranks) {
+    set_error("RBF_COMM_THREADS: group key already used with %d ranks (this context: %d)", g->n,
+              c->nranks);
+    return RBF_EINVAL;
+  }
+  c->tgroup = g;
+  return RBF_OK;
+}
+
 int comm_init(rbf_ctx *c, const rbf_dist *d) {
-  if (c->nranks <= 1 || c->comm_mode != RBF_COMM_NCCL) return RBF_OK;
+  if (c->nranks <= 1) return RBF_OK;
+  if (c->comm_mode == RBF_COMM_THREADS) return thread_group_join(c, d);
+  if (c->comm_mode != RBF_COMM_NCCL) return RBF_OK;
   ncclUniqueId id;
   static_assert(sizeof(id.internal) == 128, "nccl id size");
   memcpy(id.internal, d->nccl_id, 128);
@@ -26,9 +87,48 @@ void comm_destroy(rbf_ctx *c) {
   }
 }
 
+// RBF_COMM_THREADS exchange: publish this rank's send regions, copy the peers'.
+static int halo_exchange_threads(rbf_ctx *c, const double *v_loc, double *v_ext, const Halo *h,
+                                 cudaStream_t s) {
+  ThreadGroup *G = c->tgroup;
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));  // v_loc complete
+  for (int dir = 0; dir < 2; ++dir) {
+    G->ptr[dir][c->rank] = v_loc + h[dir].send_off;
+    G->cnt[dir][c->rank] = h[dir].send_cnt;
+  }
+  G->barrier();
+  int st = RBF_OK;
+  for (int dir = 0; dir < 2 && st == RBF_OK; ++dir) {
+    const int peer = dir == 0 ? c->rank - 1 : c->rank + 1;
+    if (peer < 0 || peer >= c->nranks || h[dir].recv_cnt == 0) continue;
+    // the peer's send towards this rank is its opposite direction
+    if (G->cnt[1 - dir][peer] != h[dir].recv_cnt) {
+      set_error("halo plan mismatch: rank %d expects %lld from rank %d, which sends %lld", c->rank,
+                (long long)h[dir].recv_cnt, peer, G->cnt[1 - dir][peer]);
+      st = RBF_EINVAL;
+      break;
+    }
+    if (cudaMemcpyAsync(v_ext + h[dir].recv_off, G->ptr[1 - dir][peer],
+                        sizeof(double) * (size_t)h[dir].recv_cnt, cudaMemcpyDeviceToDevice,
+                        s) != cudaSuccess) {
+      set_error("RBF_COMM_THREADS halo copy failed");
+      st = RBF_ECUDA;
+    }
+  }
+  if (cudaStreamSynchronize(s) != cudaSuccess && st == RBF_OK) st = RBF_ECUDA;
+  G->barrier();  // peers may overwrite their v_loc from here on
+  return st;
+}
+
 int halo_exchange(rbf_ctx *c, const double *v_loc, double *v_ext, bool matvec_depth,
                   cudaStream_t s) {
   if (c->nranks <= 1) return RBF_OK;
+  if (c->comm_mode == RBF_COMM_THREADS) {
+    const long long own_off = c->s.own_lo - c->s.ext_lo;
+    RBF_CUDA_TRY(cudaMemcpyAsync(v_ext + own_off, v_loc, sizeof(double) * n_loc(c),
+                                 cudaMemcpyDeviceToDevice, s));
+    return halo_exchange_threads(c, v_loc, v_ext, matvec_depth ? c->halo_mv : c->halo_pc, s);
+  }
   if (c->comm_mode != RBF_COMM_NCCL) {
     set_error("virtual strip context (RBF_COMM_NONE) has no communicator: use the *_ext calls");
     return RBF_EUNSUPPORTED;
@@ -54,6 +154,22 @@ int halo_exchange(rbf_ctx *c, const double *v_loc, double *v_ext, bool matvec_de
 
 int allgather_scalars(rbf_ctx *c, const double *send, double *recv, int count, cudaStream_t s) {
   if (c->nranks <= 1) return RBF_OK;  // single rank: recv aliases send
+  if (c->comm_mode == RBF_COMM_THREADS) {
+    ThreadGroup *G = c->tgroup;
+    RBF_CUDA_TRY(cudaStreamSynchronize(s));
+    G->ptr[0][c->rank] = send;
+    G->barrier();
+    int st = RBF_OK;
+    for (int r = 0; r < c->nranks && st == RBF_OK; ++r)
+      if (cudaMemcpyAsync(recv + (long long)r * count, G->ptr[0][r], sizeof(double) * count,
+                          cudaMemcpyDeviceToDevice, s) != cudaSuccess) {
+        set_error("RBF_COMM_THREADS all-gather copy failed");
+        st = RBF_ECUDA;
+      }
+    if (cudaStreamSynchronize(s) != cudaSuccess && st == RBF_OK) st = RBF_ECUDA;
+    G->barrier();
+    return st;
+  }
   if (c->comm_mode != RBF_COMM_NCCL) {
     set_error("virtual strip context (RBF_COMM_NONE) cannot reduce across strips");
     return RBF_EUNSUPPORTED;

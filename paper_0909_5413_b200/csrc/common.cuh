@@ -65,6 +65,8 @@ struct Strip {
 constexpr int kRedBlocks = 592;   // 4 x 148 SMs: fixed grid for deterministic reductions
 constexpr int kRedThreads = 512;
 
+struct ThreadGroup;  // RBF_COMM_THREADS rendezvous (comm.cu)
+
 struct Halo {  // one direction of a halo exchange, in element offsets
   long long send_off, send_cnt;  // relative to the owned (local) vector
   long long recv_off, recv_cnt;  // relative to the ext vector
@@ -170,6 +172,7 @@ struct rbf_ctx {
   long long n = 0;
   int rank = 0, nranks = 1, comm_mode = RBF_COMM_NONE;
   ncclComm_t nccl = nullptr;
+  rbf::ThreadGroup *tgroup = nullptr;  // RBF_COMM_THREADS (comm.cu)
   std::vector<long long> row_start;  // host: global sorted position of the first point of each cell row
   rbf::Halo halo_mv[2]{}, halo_pc[2]{};  // [0] = with rank-1 (below), [1] = with rank+1 (above)
 

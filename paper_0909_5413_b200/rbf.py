@@ -14,7 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librbf.so")
 
 RBF_OK, RBF_NOT_CONVERGED = 0, 2
-RBF_COMM_NONE, RBF_COMM_NCCL = 0, 1
+RBF_COMM_NONE, RBF_COMM_NCCL, RBF_COMM_THREADS = 0, 1, 2
 _ERRORS = {-1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENCCL", -5: "EFACTOR", -6: "ENUMERIC",
            -7: "EUNSUPPORTED"}
 
@@ -201,7 +201,8 @@ class Context:
         self.params = make_params(sigma, cell, rc, rings, box)
         dist = None
         if nranks > 1 or comm == "nccl":
-            dist = Dist(int(rank), int(nranks), RBF_COMM_NCCL if comm == "nccl" else RBF_COMM_NONE, 0)
+            mode = {"nccl": RBF_COMM_NCCL, "threads": RBF_COMM_THREADS, "none": RBF_COMM_NONE}[comm]
+            dist = Dist(int(rank), int(nranks), mode, 0)
             if nccl_id is not None:
                 C.memmove(dist.nccl_id, nccl_id, 128)
         self._h = C.c_void_p()

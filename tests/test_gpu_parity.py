@@ -224,11 +224,141 @@ def test_virtual_strips_bitwise(nranks):
     assert np.array_equal(np.concatenate(zs), z1)
 
 
+# ------------------------------------------------------------------ in-process strips
+# RBF_COMM_THREADS: nranks contexts on this one GPU, one host thread each, exchanging
+# halos and reduction partials by device copies (include/rbf.h).  Exercises the whole
+# multi-strip path (halo plans, exchange, rank-ordered reductions, host-driven GMRES)
+# that the NCCL transport carries between GPUs.
+
+def _run_threads(nranks, body, timeout=300):
+    import os
+    import threading
+
+    key = os.urandom(128)
+    out, err = [None] * nranks, [None] * nranks
+
+    def run(r):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                out[r] = body(r, key, st)
+            st.synchronize()
+        except BaseException as e:  # noqa: BLE001 - reported below
+            err[r] = e
+
+    ths = [threading.Thread(target=run, args=(r,), daemon=True) for r in range(nranks)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(timeout)
+    assert not any(t.is_alive() for t in ths), "a strip thread hung (collective mismatch)"
+    for e in err:
+        if e is not None:
+            raise e
+    return out
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_threads_strips_operators_bitwise(nranks):
+    """rbf_matvec / rbf_rasm_apply with in-library halo exchange: bitwise equal to one strip."""
+    wl = W.make_lattice(60, jitter_frac=0.1, seed=5)
+    rng = np.random.default_rng(2)
+    w = torch.from_numpy(rng.standard_normal(wl.n)).cuda()
+    xy = torch.from_numpy(wl.xy).cuda()
+    with ctx_for(wl) as c1:
+        y1 = c1.from_local(c1.matvec(c1.to_local(w))).cpu().numpy()
+        z1 = c1.from_local(c1.rasm_apply(c1.to_local(w))).cpu().numpy()
+
+    def body(r, key, st):
+        with P.Context(xy, wl.sigma, wl.cell, wl.rc, 1, wl.box, rank=r, nranks=nranks,
+                       comm="threads", nccl_id=key, stream=st) as c:
+            wl_ = c.to_local(w)
+            y = c.from_local(c.matvec(wl_)).cpu().numpy()
+            z = c.from_local(c.rasm_apply(wl_)).cpu().numpy()
+            return y, z, c.n_local
+
+    res = _run_threads(nranks, body)
+    assert sum(r[2] for r in res) == wl.n
+    assert np.array_equal(sum(r[0] for r in res), y1)
+    assert np.array_equal(sum(r[1] for r in res), z1)
+
+
+@pytest.mark.parametrize("nranks,wl", [(2, W.make_lattice(60, jitter_frac=0.1, seed=5)),
+                                       (4, W.make_lattice(100, jitter_frac=0.1, seed=9))],
+                         ids=["2x60", "4x100"])
+def test_threads_strips_solve(nranks, wl):
+    """Multi-strip GMRES (host-driven loop, all-gathered partials summed in rank order,
+    reading Q14) against the single-strip solve and the oracle's stopping rule."""
+    xy = torch.from_numpy(wl.xy).cuda()
+    f = torch.from_numpy(wl.f).cuda()
+    with ctx_for(wl) as c1:
+        lam1, rep1 = c1.solve(c1.to_local(f), rtol=1e-13)
+        lam1 = c1.from_local(lam1).cpu().numpy()
+
+    def body(r, key, st):
+        with P.Context(xy, wl.sigma, wl.cell, wl.rc, 1, wl.box, rank=r, nranks=nranks,
+                       comm="threads", nccl_id=key, stream=st) as c:
+            lam, rep = c.solve(c.to_local(f), rtol=1e-13)
+            return c.from_local(lam).cpu().numpy(), rep
+
+    res = _run_threads(nranks, body)
+    reps = [r[1] for r in res]
+    lam = sum(r[0] for r in res)
+    assert all(rp.converged for rp in reps)
+    # every strip ran the same iterations and holds the same (all-gathered) scalars
+    assert len({rp.iterations for rp in reps}) == 1 and len({rp.beta0 for rp in reps}) == 1
+    assert len({rp.resid_true for rp in reps}) == 1
+    assert abs(reps[0].iterations - rep1.iterations) <= 1
+    assert reps[0].resid_true <= 1e-10
+    assert rel(lam, lam1) <= 1e-8
+    # the caller-order weights satisfy the interpolation conditions (oracle matvec)
+    r_true = O.matvec_brute(wl.xy, lam, wl.sigma, wl.rc) - wl.f
+    assert np.linalg.norm(r_true) / np.linalg.norm(wl.f) <= 1e-10
+
+
+def test_threads_group_key_mismatch():
+    wl = W.make_lattice(60)
+    xy = torch.from_numpy(wl.xy).cuda()
+    import os
+
+    key = os.urandom(128)
+    with P.Context(xy, wl.sigma, wl.cell, wl.rc, 1, wl.box, rank=0, nranks=2, comm="threads",
+                   nccl_id=key):
+        with pytest.raises(P.RbfError):
+            P.Context(xy, wl.sigma, wl.cell, wl.rc, 1, wl.box, rank=0, nranks=3, comm="threads",
+                      nccl_id=key)
+
+
 # ------------------------------------------------------------------ full size (bench config)
 
 @pytest.fixture(scope="module")
 def cfg2():
     return W.config(2)
+
+
+def test_cfg2_threads_strips_solve(cfg2):
+    """The bench configuration on 2 in-process strips: same iterations and residual as
+    the single-strip solve (the multi-GPU path's algorithm at full size)."""
+    wl = cfg2
+    xy = torch.from_numpy(wl.xy).cuda()
+    f = torch.from_numpy(wl.f).cuda()
+    with ctx_for(wl) as c1:
+        lam1, rep1 = c1.solve(c1.to_local(f), rtol=wl.tol)
+        lam1 = c1.from_local(lam1).cpu().numpy()
+
+    def body(r, key, st):
+        with P.Context(xy, wl.sigma, wl.cell, wl.rc, wl.rings, wl.box, rank=r, nranks=2,
+                       comm="threads", nccl_id=key, stream=st) as c:
+            lam, rep = c.solve(c.to_local(f), rtol=wl.tol)
+            return c.from_local(lam).cpu().numpy(), rep
+
+    res = _run_threads(2, body, timeout=600)
+    reps = [r[1] for r in res]
+    assert all(rp.converged for rp in reps)
+    assert reps[0].iterations == reps[1].iterations
+    assert abs(reps[0].iterations - rep1.iterations) <= 2
+    assert reps[0].resid_true <= 10 * max(rep1.resid_true, 1e-12)
+    assert rel(sum(r[0] for r in res), lam1) <= 1e-8
 
 
 def test_cfg2_matvec_sampled_rows(cfg2):

@@ -190,6 +190,75 @@ def test_gmres_not_converged_status():
     assert not res.converged and res.status == O.ORC_NOT_CONVERGED and res.iterations == 7
 
 
+# ----------------------------------------------------------------- CGS2 (reading Q23)
+
+def _krylov_qr(A, b, k):
+    """Orthonormal basis of span{b, Ab, ..., A^k b} by Householder QR (LAPACK), signs
+    fixed so R has a positive diagonal -- the Arnoldi basis (h_{j+1,j} > 0)."""
+    K = np.empty((len(b), k + 1))
+    K[:, 0] = b / np.linalg.norm(b)
+    for j in range(k):
+        K[:, j + 1] = A @ K[:, j]
+        K[:, j + 1] /= np.linalg.norm(K[:, j + 1])
+    Q, R = np.linalg.qr(K)
+    return (Q * np.sign(np.diag(R))).T
+
+
+@pytest.mark.parametrize("orth", ["mgs", "cgs2"])
+def test_gmres_basis_is_the_krylov_qr(orth):
+    # implicit-Q theorem: any exact Arnoldi process yields the QR factor of the Krylov
+    # matrix; a dropped pass, wrong sign or wrong coefficient breaks the match
+    rng = np.random.default_rng(5)
+    G = rng.standard_normal((60, 60))
+    A = G @ G.T / 60 + np.eye(60)
+    b = rng.standard_normal(60)
+    res = O.gmres(O.op_dense(A), O.op_identity(60), b, restart=6, max_iters=6, rtol=0.0,
+                  keep_basis=True, orth=orth)
+    assert res.basis.shape == (7, 60)
+    assert np.max(np.abs(res.basis - _krylov_qr(A, b, 6))) < 1e-9
+
+
+def test_gmres_cgs2_same_solution_and_history_as_mgs():
+    rng = np.random.default_rng(6)
+    G = rng.standard_normal((80, 80))
+    A = G @ G.T + 2 * np.eye(80)
+    b = rng.standard_normal(80)
+    r1 = O.gmres(O.op_dense(A), O.op_identity(80), b, restart=15, rtol=1e-13)
+    r2 = O.gmres(O.op_dense(A), O.op_identity(80), b, restart=15, rtol=1e-13, orth="cgs2")
+    assert r1.converged and r2.converged
+    assert abs(r1.iterations - r2.iterations) <= 1
+    ref = np.linalg.solve(A, b)
+    assert np.linalg.norm(r2.x - ref) / np.linalg.norm(ref) < 1e-10
+    k = min(r1.iterations, r2.iterations)
+    big = r1.history[:k] > 1e-9
+    assert np.allclose(r1.history[:k][big], r2.history[:k][big], rtol=1e-6)
+
+
+def test_gmres_cgs2_orthogonal_where_one_pass_is_not():
+    # "twice is enough": on an ill-conditioned Krylov sequence CGS2 keeps
+    # ||I - V V^T|| at rounding level; MGS loses orthogonality in proportion to the
+    # condition of the Krylov basis
+    n = 120
+    A = np.diag(np.logspace(0, 10, n))
+    b = np.ones(n)
+    res = O.gmres(O.op_dense(A), O.op_identity(n), b, restart=40, max_iters=40, rtol=0.0,
+                  keep_basis=True, orth="cgs2")
+    V = res.basis
+    loss2 = np.max(np.abs(V @ V.T - np.eye(V.shape[0])))
+    assert loss2 < 1e-13
+    res = O.gmres(O.op_dense(A), O.op_identity(n), b, restart=40, max_iters=40, rtol=0.0,
+                  keep_basis=True, orth="mgs")
+    V = res.basis
+    assert np.max(np.abs(V @ V.T - np.eye(V.shape[0]))) > 100 * loss2  # the contrast (eps kappa)
+
+
+def test_cfg1_solve_cgs2_matches_mgs(cfg1_solution):
+    wl, res, lam = cfg1_solution
+    r2 = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, rtol=wl.tol, orth="cgs2")
+    assert r2.converged and abs(r2.iterations - res.iterations) <= 1
+    assert np.linalg.norm(r2.x - lam) / np.linalg.norm(lam) < 1e-8
+
+
 # ----------------------------------------------------------------- full solve
 
 @pytest.fixture(scope="module")
