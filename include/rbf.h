@@ -102,14 +102,19 @@ typedef struct {
 /* GMRES parameters (reading Q12).
  *  restart    m >= 1 (30).      max_iters  >= 1 (1000).
  *  rtol, atol >= 0: stop when the recurrence residual |g_{k+1}| <= max(rtol*||M^-1 f||, atol).
- *  timing     nonzero: record per-phase CUDA-event times into the report (adds events). */
+ *  timing     nonzero: record per-phase CUDA-event times into the report (adds events).
+ *  orth       Arnoldi orthogonalisation: RBF_ORTH_MGS (0, default; Q12, BJ:5) or
+ *             RBF_ORTH_CGS2 (classical Gram-Schmidt twice, reading Q23: 3 reductions per
+ *             step instead of k+2; requires restart <= RBF_CGS2_MAX_RESTART, else EINVAL). */
+enum { RBF_ORTH_MGS = 0, RBF_ORTH_CGS2 = 1 };
+#define RBF_CGS2_MAX_RESTART 32
 typedef struct {
   int32_t restart;
   int32_t max_iters;
   double rtol;
   double atol;
   int32_t timing;
-  int32_t reserved0;
+  int32_t orth;
 } rbf_gmres_params;
 
 /* Solve report.  Residuals are relative: resid_est = |g|/||M^-1 f|| (recurrence),

@@ -213,6 +213,10 @@ struct rbf_ctx {
   double *ar_part = nullptr;   // its per-CTA partial sums
   unsigned *ar_bar = nullptr;  // its grid barrier (count, generation)
   int ar_m = 0;                // restart length ar_part is sized for
+  int cg_grid = 0;             // CTAs of the fused CGS2 Arnoldi kernel (0 = unused)
+  double *cg_blk = nullptr;    // multi-kernel CGS2 per-block partials (kRedBlocks x 32)
+  unsigned *cg_count = nullptr;
+  int g_orth = -1;             // orthogonalisation the solve graph was built for
   // graph-driven solve (single rank): the whole restarted GMRES as one CUDA graph with
   // device-side while loops (conditional nodes), built per restart length
   cudaGraph_t g_graph = nullptr;

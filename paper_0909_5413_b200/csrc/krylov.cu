@@ -30,8 +30,21 @@ struct Scal {
   __host__ __device__ long long g() const { return sn() + m; }              // [m+1]
   __host__ __device__ long long y() const { return g() + m + 1; }           // [m]
   __host__ __device__ long long out() const { return y() + m; }             // [4]: |g|, hn, beta
-  __host__ __device__ long long total() const { return out() + 4; }
+  // CGS2 (reading Q23): this rank's pass-1 / pass-2 coefficients [m+2] and their
+  // all-gathers [P (m+2)], rank-major with stride = the step's count k+1
+  __host__ __device__ long long c1loc() const { return out() + 4; }
+  __host__ __device__ long long c1all() const { return c1loc() + m + 2; }
+  __host__ __device__ long long c2loc() const { return c1all() + (long long)(m + 2) * P; }
+  __host__ __device__ long long c2all() const { return c2loc() + m + 2; }
+  __host__ __device__ long long total() const { return c2all() + (long long)(m + 2) * P; }
 };
+
+// sum over ranks of entry j of a rank-major all-gather with `cnt` entries per rank
+__device__ __forceinline__ double sum_ranks_rm(const double *all, int j, int cnt, int P) {
+  double s = 0.0;
+  for (int r = 0; r < P; ++r) s += all[(long long)r * cnt + j];
+  return s;
+}
 
 __device__ __forceinline__ double sum_ranks(const double *hall, int slot, int P) {
   double s = 0.0;
@@ -146,11 +159,16 @@ __global__ void k_cycle_init(double *S, Scal L, const double *nrm2) {  // nrm2 =
 
 // Column k of H from the all-gathered MGS results, previous rotations, new rotation,
 // g update (Saad's GMRES with Givens; oracle orc_gmres follows the same steps).
-__device__ void givens_step(double *S, const Scal &L, const double *hall, int k) {
+// CGS2 (c1 != null): H(j,k) = pass-1 + pass-2 coefficients (rank-major all-gathers
+// with k+1 entries per rank); ||w||^2 still comes from hall slot k+1.
+__device__ void givens_step(double *S, const Scal &L, const double *hall, int k,
+                            const double *c1 = nullptr, const double *c2 = nullptr) {
   const int m = L.m;
   double *H = S + L.H();
   double *cs = S + L.cs(), *sn = S + L.sn(), *g = S + L.g();
-  for (int j = 0; j <= k; ++j) H[(long long)j * m + k] = sum_ranks(hall, j, L.P);
+  for (int j = 0; j <= k; ++j)
+    H[(long long)j * m + k] = c1 ? sum_ranks_rm(c1, j, k + 1, L.P) + sum_ranks_rm(c2, j, k + 1, L.P)
+                                 : sum_ranks(hall, j, L.P);
   const double hn = sqrt(sum_ranks(hall, k + 1, L.P));
   H[(long long)(k + 1) * m + k] = hn;
   for (int j = 0; j < k; ++j) {
@@ -190,8 +208,9 @@ __device__ __forceinline__ void post_mailbox(Mailbox *ring, const double *S, con
   v->seq = seq;
 }
 
-__global__ void k_givens(double *S, Scal L, const double *hall, int k, Mailbox *mb, long long seq) {
-  givens_step(S, L, hall, k);
+__global__ void k_givens(double *S, Scal L, const double *hall, int k, Mailbox *mb, long long seq,
+                         const double *c1, const double *c2) {
+  givens_step(S, L, hall, k, c1, c2);
   post_mailbox(mb, S, L, seq);
 }
 
@@ -359,6 +378,224 @@ __global__ __launch_bounds__(kArThreads, 1) void k_arnoldi_fused(double *V, long
   }
 }
 
+// ---------------------------------------------------------------------------
+// CGS2 Arnoldi step (reading Q23), single rank, ONE cooperative launch with three
+// grid barriers instead of k+2: pass 1 h1 = V^T w; pass 2 w -= V h1, then
+// h2 = V^T w; pass 3 w -= V h2 and ||w||^2.  Same layout as k_arnoldi_fused (w in
+// registers, kArE elements per thread); every pass loops over the basis vectors
+// with kArE independent loads per thread per vector, one warp reduction per vector
+// into shared memory, and one CTA-level reduction + grid barrier per pass.
+// Fixed-order reductions: deterministic.
+// ---------------------------------------------------------------------------
+constexpr int kCgMaxM = RBF_CGS2_MAX_RESTART;
+constexpr int kArWarps = kArThreads / 32;
+static_assert(kCgMaxM <= kArWarps, "one warp per coefficient in the CTA reductions");
+
+// CTA partials sh_red[j][warp] (j < cnt) -> part[j*G + cta]; grid barrier; CTA-order
+// sums of the partials -> sh_out[j].
+__device__ __forceinline__ void cg_reduce(double (*sh_red)[kArWarps], int cnt, double *part,
+                                          double *sh_out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned G = gridDim.x;
+  __syncthreads();
+  if (warp < cnt) {
+    const double t = warp_sum(sh_red[warp][lane]);
+    if (lane == 0) part[(long long)warp * G + blockIdx.x] = t;
+  }
+  cooperative_groups::this_grid().sync();
+  if (warp < cnt) {
+    double hs = 0.0;
+    for (unsigned b = lane; b < G; b += 32) hs += ((volatile double *)part)[(long long)warp * G + b];
+    hs = warp_sum(hs);
+    if (lane == 0) sh_out[warp] = hs;
+  }
+  __syncthreads();
+}
+
+__global__ __launch_bounds__(kArThreads, 1) void k_arnoldi_cgs2(double *V, long long ldv, long long n,
+                                                             int k, double *S, Scal L,
+                                                             double *part, unsigned *bar,
+                                                             Mailbox *mb, long long seq,
+                                                             double4 *rec, const double *w_in,
+                                                             GState *st, double *hist,
+                                                             cudaGraphConditionalHandle inner) {
+  (void)bar;
+  if (st) k = st->k;
+  __shared__ double sh_red[kCgMaxM][kArWarps];
+  __shared__ double sh_h1[kCgMaxM + 1], sh_h2[kCgMaxM + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned G = gridDim.x;
+  const long long chunk = (n + G - 1) / G;
+  const long long base = (long long)blockIdx.x * chunk;
+  const long long end = base + chunk < n ? base + chunk : n;
+  const int cnt = k + 1;
+  double *wv = V + (long long)(k + 1) * ldv;
+  const double *win = w_in ? w_in : wv;
+  double *part1 = part, *part2 = part + (long long)(kCgMaxM + 1) * G,
+         *part3 = part + 2LL * (kCgMaxM + 1) * G;
+  long long idx[kArE];
+  bool ok[kArE];
+  double w[kArE];
+#pragma unroll
+  for (int e = 0; e < kArE; ++e) {
+    idx[e] = base + threadIdx.x + (long long)e * kArThreads;
+    ok[e] = idx[e] < end;
+    w[e] = ok[e] ? win[idx[e]] : 0.0;
+  }
+  // <w, v_j> for all j < cnt -> sh_red[j][warp]
+  auto dots = [&]() {
+    for (int j = 0; j < cnt; ++j) {
+      const double *vj = V + (long long)j * ldv;
+      double vv[kArE];
+#pragma unroll
+      for (int e = 0; e < kArE; ++e) vv[e] = ok[e] ? __ldcg(vj + idx[e]) : 0.0;
+      double acc = 0.0;
+#pragma unroll
+      for (int e = 0; e < kArE; ++e) acc = fma(w[e], vv[e], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) sh_red[j][warp] = acc;
+    }
+  };
+  // w -= sum_j h[j] v_j
+  auto update = [&](const double *h) {
+    for (int j = 0; j < cnt; ++j) {
+      const double *vj = V + (long long)j * ldv;
+      const double hj = h[j];
+      double vv[kArE];
+#pragma unroll
+      for (int e = 0; e < kArE; ++e) vv[e] = ok[e] ? __ldcg(vj + idx[e]) : 0.0;
+#pragma unroll
+      for (int e = 0; e < kArE; ++e) w[e] = fma(-hj, vv[e], w[e]);
+    }
+  };
+  dots();  // pass 1
+  cg_reduce(sh_red, cnt, part1, sh_h1);
+  update(sh_h1);  // pass 2
+  dots();
+  cg_reduce(sh_red, cnt, part2, sh_h2);
+  if (blockIdx.x == 0 && threadIdx.x < cnt) S[L.hloc() + threadIdx.x] = sh_h1[threadIdx.x] + sh_h2[threadIdx.x];
+  update(sh_h2);  // pass 3
+  double nrm = 0.0;
+#pragma unroll
+  for (int e = 0; e < kArE; ++e) nrm = fma(w[e], w[e], nrm);
+  nrm = warp_sum(nrm);
+  if (lane == 0) sh_red[0][warp] = nrm;
+  cg_reduce(sh_red, 1, part3, sh_h1);
+  const double nsq = sh_h1[0];
+  if (blockIdx.x == 0 && threadIdx.x == 0) S[L.hloc() + cnt] = nsq;
+  // v_{k+1} = w / ||w||, also into the next matvec's records
+  const double hn = sqrt(nsq);
+#pragma unroll
+  for (int e = 0; e < kArE; ++e) {
+    if (ok[e]) {
+      const double v = (hn != 0.0) ? w[e] / hn : w[e];
+      wv[idx[e]] = v;
+      reinterpret_cast<double *>(rec + idx[e])[2] = v;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (st) {
+      graph_step_end(S, L, k, st, hist, inner);
+    } else {
+      givens_step(S, L, S + L.hloc(), k);
+      post_mailbox(mb, S, L, seq);
+    }
+  }
+}
+
+// CGS2 pass for the multi-kernel path (several ranks, or n beyond the cooperative
+// kernel's reach).  MODE 0: out[j] = <w, v_j>;  MODE 1: w -= V c, out[j] = <w, v_j>;
+// MODE 2: w -= V c, out[0] = ||w||^2;  c_j = sum over ranks of the previous pass's
+// all-gather (rank-major, cnt per rank).  Each thread holds kCpE elements of w in
+// registers per chunk and loops over the basis vectors (kCpE independent loads per
+// vector); per-warp partials accumulate in shared memory in chunk order, blocks'
+// partials blk[j * gridDim + b] are summed in block order by the last block:
+// deterministic for a fixed grid.
+constexpr int kCpE = 4;
+template <int MODE>
+__global__ __launch_bounds__(kRedThreads) void k_cgs_pass(double *w, const double *__restrict__ V,
+                                                          long long ldv, int cnt, long long n,
+                                                          const double *__restrict__ call, int P,
+                                                          double *__restrict__ blk,
+                                                          unsigned *__restrict__ count,
+                                                          double *__restrict__ out) {
+  constexpr int W_ = kRedThreads / 32;
+  __shared__ double sh_c[kCgMaxM];
+  __shared__ double sh_acc[kCgMaxM][W_];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nout = MODE == 2 ? 1 : cnt;
+  if (MODE > 0 && threadIdx.x < cnt) sh_c[threadIdx.x] = sum_ranks_rm(call, threadIdx.x, cnt, P);
+  for (int t = threadIdx.x; t < kCgMaxM * W_; t += blockDim.x) (&sh_acc[0][0])[t] = 0.0;
+  __syncthreads();
+  const long long cstride = (long long)gridDim.x * blockDim.x * kCpE;
+  for (long long c0 = (long long)blockIdx.x * blockDim.x * kCpE; c0 < n; c0 += cstride) {
+    long long idx[kCpE];
+    bool ok[kCpE];
+    double wv[kCpE];
+#pragma unroll
+    for (int e = 0; e < kCpE; ++e) {
+      idx[e] = c0 + threadIdx.x + (long long)e * blockDim.x;
+      ok[e] = idx[e] < n;
+      wv[e] = ok[e] ? w[idx[e]] : 0.0;
+    }
+    if (MODE > 0) {
+      for (int j = 0; j < cnt; ++j) {
+        const double *vj = V + (long long)j * ldv;
+        const double cj = sh_c[j];
+        double vv[kCpE];
+#pragma unroll
+        for (int e = 0; e < kCpE; ++e) vv[e] = ok[e] ? vj[idx[e]] : 0.0;
+#pragma unroll
+        for (int e = 0; e < kCpE; ++e) wv[e] = fma(-cj, vv[e], wv[e]);
+      }
+#pragma unroll
+      for (int e = 0; e < kCpE; ++e)
+        if (ok[e]) w[idx[e]] = wv[e];
+    }
+    if (MODE == 2) {
+      double acc = 0.0;
+#pragma unroll
+      for (int e = 0; e < kCpE; ++e) acc = fma(wv[e], wv[e], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) sh_acc[0][warp] += acc;
+    } else {
+      for (int j = 0; j < cnt; ++j) {
+        const double *vj = V + (long long)j * ldv;
+        double vv[kCpE];
+#pragma unroll
+        for (int e = 0; e < kCpE; ++e) vv[e] = ok[e] ? vj[idx[e]] : 0.0;
+        double acc = 0.0;
+#pragma unroll
+        for (int e = 0; e < kCpE; ++e) acc = fma(wv[e], vv[e], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) sh_acc[j][warp] += acc;
+      }
+    }
+  }
+  __syncthreads();
+  for (int j = warp; j < nout; j += W_) {
+    double t = lane < W_ ? sh_acc[j][lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) blk[(long long)j * gridDim.x + blockIdx.x] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(count, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int j = warp; j < nout; j += W_) {
+    double t = 0.0;
+    for (unsigned b = lane; b < gridDim.x; b += 32) t += ((volatile double *)blk)[(long long)j * gridDim.x + b];
+    t = warp_sum(t);
+    if (lane == 0) out[j] = t;
+  }
+  if (threadIdx.x == 0) *count = 0u;
+}
+
 // ---- graph-mode control kernels (one thread)
 __global__ void k_g_begin(const double *nrm2, GState *st, cudaGraphConditionalHandle outer) {
   const double beta0 = sqrt(*nrm2);
@@ -471,6 +708,13 @@ struct Op {
   }
 };
 
+// per-CTA partial sums of the fused Arnoldi kernels: MGS (m+2) slots, CGS2 3 passes
+static size_t part_doubles(const rbf_ctx *c, int m) {
+  const size_t a = (size_t)(m + 2) * (size_t)c->ar_grid;
+  const size_t b = (size_t)3 * (kCgMaxM + 1) * (size_t)c->cg_grid;
+  return (a > b ? a : b) + 1;
+}
+
 static int ensure_workspace(rbf_ctx *c, int m, cudaStream_t s) {
   const long long n = n_loc(c);
   if (c->V && c->V_m >= m) return RBF_OK;
@@ -494,10 +738,15 @@ static int ensure_workspace(rbf_ctx *c, int m, cudaStream_t s) {
     RBF_CUDA_TRY(cudaHostAlloc((void **)&c->hpin, sizeof(double) * (kHpinScal + 8 + c->nranks), cudaHostAllocMapped));
     RBF_CUDA_TRY(cudaHostGetDevicePointer((void **)&c->hpin_dev, c->hpin, 0));
   }
+  if (!c->cg_blk) {
+    RBF_TRY(dalloc(c, (void **)&c->cg_blk, sizeof(double) * (size_t)kRedBlocks * kCgMaxM, s));
+    RBF_TRY(dalloc(c, (void **)&c->cg_count, sizeof(unsigned), s));
+    RBF_CUDA_TRY(cudaMemsetAsync(c->cg_count, 0, sizeof(unsigned), s));
+  }
   if (c->nranks == 1 && c->ar_part && c->ar_m < m) {  // per-step partials sized by m
     dfree(c->ar_part, s);
     c->ar_part = nullptr;
-    RBF_TRY(dalloc(c, (void **)&c->ar_part, sizeof(double) * (size_t)(m + 2) * c->ar_grid, s));
+    RBF_TRY(dalloc(c, (void **)&c->ar_part, sizeof(double) * part_doubles(c, m), s));
     c->ar_m = m;
   }
   if (c->nranks == 1 && !c->ar_part && c->ar_m == 0) {
@@ -511,9 +760,15 @@ static int ensure_workspace(rbf_ctx *c, int m, cudaStream_t s) {
     c->ar_grid = (coop && per_sm > 0) ? sms * (per_sm < ar_per_sm ? per_sm : ar_per_sm) : 0;
     if (getenv("RBF_NO_FUSED_ARNOLDI")) c->ar_grid = 0;
     if (c->ar_grid > 0 && (long long)c->ar_grid * kArThreads * kArE < n) c->ar_grid = 0;
+    // fused CGS2: same layout as the MGS kernel (w in registers, kArE per thread)
+    int cg_per_sm = 0;
+    RBF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cg_per_sm, k_arnoldi_cgs2, kArThreads, 0));
+    c->cg_grid = (coop && cg_per_sm > 0) ? sms * (cg_per_sm < ar_per_sm ? cg_per_sm : ar_per_sm) : 0;
+    if (getenv("RBF_NO_FUSED_ARNOLDI")) c->cg_grid = 0;
+    if (c->cg_grid > 0 && (long long)c->cg_grid * kArThreads * kArE < n) c->cg_grid = 0;
     c->ar_m = m;
-    if (c->ar_grid > 0) {
-      RBF_TRY(dalloc(c, (void **)&c->ar_part, sizeof(double) * (size_t)(m + 2) * c->ar_grid, s));
+    if (c->ar_grid > 0 || c->cg_grid > 0) {
+      RBF_TRY(dalloc(c, (void **)&c->ar_part, sizeof(double) * part_doubles(c, m), s));
       RBF_TRY(dalloc(c, (void **)&c->ar_bar, sizeof(unsigned) * 2, s));
       RBF_CUDA_TRY(cudaMemsetAsync(c->ar_bar, 0, sizeof(unsigned) * 2, s));
     }
@@ -636,6 +891,35 @@ static int wait_mailbox(rbf_ctx *c, long long seq, cudaStream_t s, double *gabs,
 // from the kernels that compute the residual estimates -- so no host round trip or
 // launch latency sits between iterations and host jitter cannot stall the GPU.
 // ---------------------------------------------------------------------------
+// the single-rank cooperative Arnoldi kernel for this orthogonalisation is usable
+static bool fused_ok(const rbf_ctx *c, int orth) {
+  return c->nranks == 1 && c->rec && (orth == RBF_ORTH_CGS2 ? c->cg_grid : c->ar_grid) > 0;
+}
+
+static bool graph_path(const rbf_ctx *c, const rbf_gmres_params *gp) {
+  return fused_ok(c, gp->orth) && !gp->timing && !getenv("RBF_NO_GRAPH");
+}
+
+// one fused Arnoldi step (cooperative launch); graph mode passes st/hist/inner
+static int launch_fused_step(rbf_ctx *c, int orth, double *V, long long n, int k, Scal L,
+                             Mailbox *mb, long long seq, const double *w_in, GState *st,
+                             double *hist, cudaGraphConditionalHandle inner, cudaStream_t s) {
+  double *Sp = c->dscal, *part = c->ar_part;
+  unsigned *bar = c->ar_bar;
+  long long ldv_ = n, n_ = n, seq_ = seq;
+  int k_ = k;
+  double4 *rec = c->rec;
+  void *args[] = {&V, &ldv_, &n_, &k_, &Sp, &L, &part, &bar, &mb, &seq_, &rec, &w_in, &st, &hist, &inner};
+  if (orth == RBF_ORTH_CGS2)
+    RBF_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_arnoldi_cgs2, c->cg_grid, kArThreads, args,
+                                             0, s));
+  else
+    RBF_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_arnoldi_fused, c->ar_grid, kArThreads, args,
+                                             0, s));
+  count_launch(1);
+  return RBF_OK;
+}
+
 static int capture_leaf(cudaStream_t s, cudaGraphNode_t *leaf) {
   cudaStreamCaptureStatus st;
   const cudaGraphNode_t *deps = nullptr;
@@ -649,21 +933,21 @@ static int capture_leaf(cudaStream_t s, cudaGraphNode_t *leaf) {
   return RBF_OK;
 }
 
-static int build_solve_graph_on(rbf_ctx *c, int m, cudaStream_t s);
+static int build_solve_graph_on(rbf_ctx *c, int m, int orth, cudaStream_t s);
 
-static int build_solve_graph(rbf_ctx *c, int m, cudaStream_t user) {
+static int build_solve_graph(rbf_ctx *c, int m, int orth, cudaStream_t user) {
   // capture on a private stream (the legacy default stream cannot be captured);
   // nothing is executed, so the user stream may still be busy (rbf_setup builds the
   // graph while the RASM setup kernel runs)
   (void)user;
   cudaStream_t cs;
   RBF_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-  const int st = build_solve_graph_on(c, m, cs);
+  const int st = build_solve_graph_on(c, m, orth, cs);
   cudaStreamDestroy(cs);
   return st;
 }
 
-static int build_solve_graph_on(rbf_ctx *c, int m, cudaStream_t s) {
+static int build_solve_graph_on(rbf_ctx *c, int m, int orth, cudaStream_t s) {
   const long long n = n_loc(c);
   Scal L{m, 1};
   double *V = c->V, *S = c->dscal, *slot0 = c->dscal + L.hloc();
@@ -718,19 +1002,7 @@ static int build_solve_graph_on(rbf_ctx *c, int m, cudaStream_t s) {
   RBF_CUDA_TRY(cudaStreamBeginCaptureToGraph(s, I, nullptr, nullptr, 0, mode));
   RBF_TRY(launch_matvec(c, V, c->t1, s, true));
   RBF_TRY(launch_rasm_apply(c, c->t1, c->t2, s));
-  {
-    double *Sp = S, *part = c->ar_part, *w_in = c->t2, *hist = c->g_hist;
-    unsigned *bar = c->ar_bar;
-    Mailbox *mb = nullptr;
-    double4 *rec = c->rec;
-    long long ldv_ = n, n_ = n, seq_ = 0;
-    int k_ = 0;
-    GState *st_ = st;
-    cudaGraphConditionalHandle h = h_inner;
-    void *args[] = {&V, &ldv_, &n_, &k_, &Sp, &L, &part, &bar, &mb, &seq_, &rec, &w_in, &st_, &hist, &h};
-    RBF_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_arnoldi_fused, c->ar_grid, kArThreads, args, 0, s));
-    count_launch(1);
-  }
+  RBF_TRY(launch_fused_step(c, orth, V, n, 0, L, nullptr, 0, c->t2, st, c->g_hist, h_inner, s));
   RBF_CUDA_TRY(cudaStreamEndCapture(s, &I));
   // -- end of cycle: x += V y, explicit residual f - A x, z = M^-1 (f - A x), ||z||^2
   RBF_CUDA_TRY(cudaStreamBeginCaptureToGraph(s, B, &inner_node, nullptr, 1, mode));
@@ -749,28 +1021,26 @@ static int build_solve_graph_on(rbf_ctx *c, int m, cudaStream_t s) {
   RBF_CUDA_TRY(cudaGraphInstantiate(&c->g_exec, G, 0));
   c->g_m = m;
   c->g_V = V;
+  c->g_orth = orth;
   return RBF_OK;
 }
 
-static int prepare_solve_graph(rbf_ctx *c, int m, int max_iters, cudaStream_t s) {
+static int prepare_solve_graph(rbf_ctx *c, int m, int max_iters, int orth, cudaStream_t s) {
   const long long n = n_loc(c);
   if (!c->g_state) RBF_TRY(dalloc(c, &c->g_state, sizeof(GState), s));
   if (!c->g_f) RBF_TRY(dalloc(c, (void **)&c->g_f, sizeof(double) * (size_t)(n > 0 ? n : 1), s));
   if (!c->g_x) RBF_TRY(dalloc(c, (void **)&c->g_x, sizeof(double) * (size_t)(n > 0 ? n : 1), s));
-  bool rebuild = c->g_exec == nullptr || c->g_m != m || c->g_V != c->V;
+  bool rebuild = c->g_exec == nullptr || c->g_m != m || c->g_V != c->V || c->g_orth != orth;
   if (c->g_hist_cap < max_iters) {
     dfree(c->g_hist, s);
     c->g_hist_cap = max_iters > 1024 ? max_iters : 1024;
     RBF_TRY(dalloc(c, (void **)&c->g_hist, sizeof(double) * (size_t)c->g_hist_cap, s));
     rebuild = true;
   }
-  if (rebuild) RBF_TRY(build_solve_graph(c, m, s));
+  if (rebuild) RBF_TRY(build_solve_graph(c, m, orth, s));
   return RBF_OK;
 }
 
-static bool graph_path(const rbf_ctx *c, const rbf_gmres_params *gp) {
-  return c->nranks == 1 && c->ar_grid > 0 && !gp->timing && c->rec && !getenv("RBF_NO_GRAPH");
-}
 
 // rbf_setup hook: allocate the default GMRES workspace and build the solve graph while
 // the RASM setup kernel occupies the GPU (the capture and instantiation are host work).
@@ -780,14 +1050,14 @@ int prebuild_solve(rbf_ctx *c, cudaStream_t s) {
   gp.max_iters = 1000;
   RBF_TRY(ensure_workspace(c, gp.restart, s));
   if (!graph_path(c, &gp)) return RBF_OK;
-  return prepare_solve_graph(c, gp.restart, gp.max_iters, s);
+  return prepare_solve_graph(c, gp.restart, gp.max_iters, gp.orth, s);
 }
 
 static int solve_gmres_graph(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double *x,
                              rbf_report *rep, cudaStream_t s) {
   const int m = gp->restart;
   const long long n = n_loc(c);
-  RBF_TRY(prepare_solve_graph(c, m, gp->max_iters, s));
+  RBF_TRY(prepare_solve_graph(c, m, gp->max_iters, gp->orth, s));
   GState hs{};
   hs.max_iters = gp->max_iters;
   hs.rtol = gp->rtol;
@@ -857,7 +1127,9 @@ int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double 
   RBF_CUDA_TRY(cudaEventCreate(&t_end));
   RBF_CUDA_TRY(cudaEventRecord(t_begin, s));
   const int blocks = grid_for(n);
-  const bool prepack = c->nranks == 1 && c->ar_grid > 0 && c->rec != nullptr;
+  const int orth = gp->orth;
+  const bool fused = fused_ok(c, orth);
+  const bool prepack = fused;  // the fused kernels write v_{k+1} into the matvec records
 
   RBF_CUDA_TRY(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)n, s));
   // beta0 = ||M^-1 f||  (x0 = 0)
@@ -894,21 +1166,30 @@ int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double 
         RBF_TRY(op.pc(c->t1, w));
         pt.rec(seq, 2, s);
         Mailbox *mb = reinterpret_cast<Mailbox *>(c->hpin_dev);
-        if (c->ar_grid > 0) {
-          // single rank: MGS + norm + scale + Givens in one cooperative launch
-          double *Sp = c->dscal;
-          double *part = c->ar_part;
-          unsigned *bar = c->ar_bar;
-          long long ldv_ = ldv, n_ = n, seq_ = seq;
-          int k_ = k;
-          double4 *rec = c->rec;
-          const double *w_in = nullptr;
-          GState *st = nullptr;
-          double *hist = nullptr;
-          cudaGraphConditionalHandle inner = 0;
-          void *args[] = {&V, &ldv_, &n_, &k_, &Sp, &L, &part, &bar, &mb, &seq_, &rec, &w_in, &st, &hist, &inner};
-          RBF_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_arnoldi_fused, c->ar_grid,
-                                                   kArThreads, args, 0, s));
+        if (fused) {
+          // single rank: orthogonalisation + norm + scale + Givens in one cooperative launch
+          RBF_TRY(launch_fused_step(c, orth, V, n, k, L, mb, seq, nullptr, nullptr, nullptr, 0, s));
+        } else if (orth == RBF_ORTH_CGS2) {
+          // classical Gram-Schmidt twice: three passes, one all-gather each (reading Q23)
+          const int cnt = k + 1, P = c->nranks, gb = grid_for(n);
+          double *S = c->dscal;
+          double *c1l = S + L.c1loc(), *c2l = S + L.c2loc();
+          double *c1a = P > 1 ? S + L.c1all() : c1l, *c2a = P > 1 ? S + L.c2all() : c2l;
+          k_cgs_pass<0><<<gb, kRedThreads, 0, s>>>(w, V, ldv, cnt, n, nullptr, P, c->cg_blk,
+                                                   c->cg_count, c1l);
+          count_launch(1);
+          if (P > 1) RBF_TRY(allgather_scalars(c, c1l, c1a, cnt, s));
+          k_cgs_pass<1><<<gb, kRedThreads, 0, s>>>(w, V, ldv, cnt, n, c1a, P, c->cg_blk, c->cg_count,
+                                                   c2l);
+          count_launch(1);
+          if (P > 1) RBF_TRY(allgather_scalars(c, c2l, c2a, cnt, s));
+          k_cgs_pass<2><<<gb, kRedThreads, 0, s>>>(w, V, ldv, cnt, n, c2a, P, c->cg_blk, c->cg_count,
+                                                   S + L.hloc() + k + 1);
+          count_launch(1);
+          RBF_TRY(reduce_slot(c, L, k + 1, s));
+          k_givens<<<1, 1, 0, s>>>(S, L, hall_slot(c, L, 0), k, mb, seq, c1a, c2a);
+          count_launch(1);
+          k_scale_by_norm<<<blocks, kRedThreads, 0, s>>>(w, n, hall_slot(c, L, k + 1), L.P, nullptr);
           count_launch(1);
         } else {
           for (int j = 0; j <= k; ++j) {  // modified Gram-Schmidt, fused axpy + dot
@@ -919,7 +1200,7 @@ int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double 
           }
           RBF_TRY(axpy_dot(c, hall_slot(c, L, k), w, vk, w, c->dscal + L.hloc() + k + 1, s));
           RBF_TRY(reduce_slot(c, L, k + 1, s));
-          k_givens<<<1, 1, 0, s>>>(c->dscal, L, hall_slot(c, L, 0), k, mb, seq);
+          k_givens<<<1, 1, 0, s>>>(c->dscal, L, hall_slot(c, L, 0), k, mb, seq, nullptr, nullptr);
           count_launch(1);
           k_scale_by_norm<<<blocks, kRedThreads, 0, s>>>(w, n, hall_slot(c, L, k + 1), L.P, nullptr);
           count_launch(1);

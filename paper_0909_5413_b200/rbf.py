@@ -38,7 +38,7 @@ class Dist(C.Structure):
 
 class GmresParams(C.Structure):
     _fields_ = [("restart", C.c_int32), ("max_iters", C.c_int32), ("rtol", C.c_double),
-                ("atol", C.c_double), ("timing", C.c_int32), ("reserved0", C.c_int32)]
+                ("atol", C.c_double), ("timing", C.c_int32), ("orth", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -283,9 +283,10 @@ class Context:
         return z
 
     def solve(self, f_loc, restart=30, max_iters=1000, rtol=1e-13, atol=0.0, timing=False,
-              lam=None):
+              lam=None, orth="mgs"):
         lam = self._new(self.n_local) if lam is None else lam
-        gp = GmresParams(int(restart), int(max_iters), float(rtol), float(atol), int(timing), 0)
+        gp = GmresParams(int(restart), int(max_iters), float(rtol), float(atol), int(timing),
+                         {"mgs": 0, "cgs2": 1}[orth])
         hist = np.zeros(max_iters, dtype=np.float64)
         rep = Report()
         rep.history = hist.ctypes.data_as(C.POINTER(C.c_double))

@@ -152,6 +152,47 @@ def test_solve_parity_jittered_restarts():
     assert rel(lam, ref.x) <= 1e-8
 
 
+# ------------------------------------------------------------------ CGS2 (reading Q23)
+
+CGS2_CASES = [W.config(1), W.make_lattice(64, jitter_frac=0.1, seed=2, rhs="gauss", s2=0.02)]
+
+
+@pytest.mark.parametrize("path", ["graph", "hostloop", "multikernel"])
+@pytest.mark.parametrize("wl", CGS2_CASES, ids=["cfg1", "jitter64"])
+def test_solve_parity_cgs2(wl, path, monkeypatch):
+    """orth=CGS2 on all three single-rank paths (graph, host loop with the fused kernel,
+    three-pass kernels) against the oracle's CGS2 GMRES."""
+    if path == "multikernel":
+        monkeypatch.setenv("RBF_NO_FUSED_ARNOLDI", "1")
+    ref = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, rtol=wl.tol, orth="cgs2")
+    with ctx_for(wl) as c:
+        lam, rep = c.solve(c.to_local(torch.from_numpy(wl.f).cuda()), rtol=wl.tol, orth="cgs2",
+                           timing=(path == "hostloop"))
+        lam = to_caller(c, lam)
+        if path == "hostloop":
+            assert rep.ms_orth > 0  # the per-phase events ran: host-driven loop
+    assert rep.converged and ref.converged
+    assert abs(rep.iterations - ref.iterations) <= 2
+    assert rep.resid_true <= 1e-10
+    assert rel(lam, ref.x) <= 1e-8
+    n = min(len(rep.history), len(ref.history))
+    big = ref.history[:n] > 1e-9
+    # recurrence residuals (relative to beta0) agree to rounding: 1e-6 relative or 1e-12
+    # absolute (the orders of the CGS2 sums differ between the GPU passes and the oracle)
+    d = np.abs(rep.history[:n][big] - ref.history[:n][big])
+    assert np.all(d <= 1e-6 * ref.history[:n][big] + 1e-12)
+
+
+def test_cgs2_restart_limit():
+    wl = W.make_lattice(30)
+    with ctx_for(wl) as c:
+        f = c.to_local(torch.from_numpy(wl.f).cuda())
+        with pytest.raises(P.RbfError):
+            c.solve(f, restart=33, orth="cgs2")
+        lam, rep = c.solve(f, restart=32, orth="cgs2")
+        assert rep.converged
+
+
 # ------------------------------------------------------------------ edge cases
 
 def test_zero_rhs_and_not_converged():
@@ -283,22 +324,23 @@ def test_threads_strips_operators_bitwise(nranks):
     assert np.array_equal(sum(r[1] for r in res), z1)
 
 
+@pytest.mark.parametrize("orth", ["mgs", "cgs2"])
 @pytest.mark.parametrize("nranks,wl", [(2, W.make_lattice(60, jitter_frac=0.1, seed=5)),
                                        (4, W.make_lattice(100, jitter_frac=0.1, seed=9))],
                          ids=["2x60", "4x100"])
-def test_threads_strips_solve(nranks, wl):
+def test_threads_strips_solve(nranks, wl, orth):
     """Multi-strip GMRES (host-driven loop, all-gathered partials summed in rank order,
     reading Q14) against the single-strip solve and the oracle's stopping rule."""
     xy = torch.from_numpy(wl.xy).cuda()
     f = torch.from_numpy(wl.f).cuda()
     with ctx_for(wl) as c1:
-        lam1, rep1 = c1.solve(c1.to_local(f), rtol=1e-13)
+        lam1, rep1 = c1.solve(c1.to_local(f), rtol=1e-13, orth=orth)
         lam1 = c1.from_local(lam1).cpu().numpy()
 
     def body(r, key, st):
         with P.Context(xy, wl.sigma, wl.cell, wl.rc, 1, wl.box, rank=r, nranks=nranks,
                        comm="threads", nccl_id=key, stream=st) as c:
-            lam, rep = c.solve(c.to_local(f), rtol=1e-13)
+            lam, rep = c.solve(c.to_local(f), rtol=1e-13, orth=orth)
             return c.from_local(lam).cpu().numpy(), rep
 
     res = _run_threads(nranks, body)
