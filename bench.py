@@ -164,10 +164,14 @@ def run_ours(args, rank, world):
     kw = dict(rank=rank, nranks=world, comm="nccl", nccl_id=nccl_id) if world > 1 else {}
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
 
+    # Arnoldi orthogonalisation: MGS on one GPU (BJ:5, Q12); across GPUs CGS2 (reading
+    # Q23): 3 all-gathers per iteration instead of k+2
+    orth = args.orth or ("mgs" if world == 1 else "cgs2")
+
     def step(timing=False):
         c = P.Context(xy, wl.sigma, wl.cell, wl.rc, wl.rings, wl.box, **kw)
         fl = c.to_local(f)
-        lam, rep = c.solve(fl, rtol=wl.tol, timing=timing)
+        lam, rep = c.solve(fl, rtol=wl.tol, timing=timing, orth=orth)
         return c, lam, rep
 
     def barrier():
@@ -273,8 +277,35 @@ def run_ours(args, rank, world):
         dist.all_reduce(mvt, op=dist.ReduceOp.MAX)
         gpairs = float(tot.item()) / (float(mvt.item()) * 1e-3) / 1e9
 
-    # ---- e2e: host buffers through the public C ABI (rbf_interpolate_host), N=1
+    # ---- e2e: host buffers through the public API.  N=1: rbf_interpolate_host (one
+    # C call); N>1: per rank pinned xy, f -> device, Context (strip setup) + to_local +
+    # solve, this rank's weights -> host; max over ranks of the wall time.
     e2e = None
+    if world > 1:
+        xy_pin = xy_h.pin_memory()
+        f_pin = f_h.pin_memory()
+        e2e_ms, d2h = [], 0
+        for k in range(max(1, min(args.steps, 3)) + 1):
+            flush.fill_(float(k))
+            barrier()
+            t0 = time.perf_counter()
+            xy_d = xy_pin.cuda(non_blocking=True)
+            f_d = f_pin.cuda(non_blocking=True)
+            c = P.Context(xy_d, wl.sigma, wl.cell, wl.rc, wl.rings, wl.box, **kw)
+            lam, rep_h = c.solve(c.to_local(f_d), rtol=wl.tol, orth=orth)
+            lam_h = lam.cpu()
+            torch.cuda.synchronize()
+            dt = torch.tensor([(time.perf_counter() - t0) * 1e3], dtype=torch.float64, device="cuda")
+            c.close()
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            if k > 0:
+                e2e_ms.append(float(dt.item()))
+            d2h = int(lam_h.numel() * 8)
+        e2e = {"value": statistics.mean(e2e_ms) / 1e3, "unit": "s",
+               "h2d_bytes_per_step": int(xy_pin.numel() * 8 + f_pin.numel() * 8),
+               "d2h_bytes_per_step": d2h,
+               "api": "per rank: Context + to_local + solve (pinned host xy, f -> this rank's "
+                      "lambda on the host); bytes per rank; max over ranks"}
     if world == 1:
         xy_pin = xy_h.pin_memory().numpy()
         f_pin = f_h.pin_memory().numpy()
@@ -311,6 +342,7 @@ def run_ours(args, rank, world):
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": wl.name, "N": wl.n, "desc": W.CONFIG_DESCRIPTIONS[args.config],
+                       "orth": orth,
                        "parallelism": f"strips{world}", "l2": "flushed (256 MiB write) between steps",
                        "step": "rbf_setup (cell list + RASM setup) + rbf_solve, inputs in HBM"},
             "iterations": iters, "restarts": r0.restarts, "resid_est": r0.resid_est,
@@ -320,7 +352,9 @@ def run_ours(args, rank, world):
                          "solve_host_loop": rep_t.ms_total,
                          "source": "one extra step with per-phase events (host-driven loop)"},
             "solve_ms": statistics.mean(r.ms_total for r in reps),
-            "solve_path": "one CUDA graph per solve (device-side while loops)",
+            "solve_path": ("one CUDA graph per solve (device-side while loops)" if world == 1 else
+                           "host-driven loop, NCCL halos + all-gathers"),
+            "orth": orth,
             "other_ms": ms_per_step - statistics.mean(r.ms_total for r in reps)
                         - statistics.mean(sd["total"] for sd in setups),
             "matvec_gpairs_s": gpairs,
@@ -344,6 +378,8 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--orth", choices=["mgs", "cgs2"], default=None,
+                    help="GMRES orthogonalisation (default: mgs on 1 GPU, cgs2 across GPUs)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
