@@ -67,6 +67,8 @@ def lib():
         L.orc_dense_factor_solve.argtypes = [i64, ptr, ptr, ptr, ptr]
         L.orc_rasm_setup.restype = ptr
         L.orc_rasm_setup.argtypes = [i64, ptr, dbl, dbl, dbl, dbl, dbl, dbl, dbl, i64]
+        L.orc_rasm_setup_box.restype = ptr
+        L.orc_rasm_setup_box.argtypes = [i64, ptr, dbl, dbl, dbl, dbl, dbl, dbl, dbl, i64, dbl]
         L.orc_rasm_status.restype = C.c_int
         L.orc_rasm_status.argtypes = [ptr, ptr, ptr, ptr]
         L.orc_rasm_sub_info.argtypes = [ptr, i64, ptr, ptr]
@@ -222,14 +224,18 @@ def dense_factor_solve(A, b) -> tuple[np.ndarray, bool]:
 
 class Rasm:
     """M^-1 = sum_c R~_c^T A_c^-1 R_c (Eq.(11)); one subdomain per
-    non-empty cell, overlap `rings` cell rings (Q9), A_c the principal submatrix
-    of A_rc (Q10), Cholesky with LU fallback (Q11)."""
+    non-empty cell, overlap `rings` cell rings (Q9) -- or, with overlap_width > 0,
+    the points of that block inside the cell's box grown by overlap_width (the
+    paper's D box, reading Q24) -- A_c the principal submatrix of A_rc (Q10),
+    Cholesky with LU fallback (Q11)."""
 
-    def __init__(self, xy, sigma: float, rc: float, box, cell: float, rings: int = 1):
+    def __init__(self, xy, sigma: float, rc: float, box, cell: float, rings: int = 1,
+                 overlap_width: float = 0.0):
         self.xy = _f64(xy)
         self.n = self.xy.shape[0]
-        self._h = lib().orc_rasm_setup(self.n, _p(self.xy), float(sigma), float(rc),
-                                       *map(float, box), float(cell), int(rings))
+        self._h = lib().orc_rasm_setup_box(self.n, _p(self.xy), float(sigma), float(rc),
+                                           *map(float, box), float(cell), int(rings),
+                                           float(overlap_width))
         bad, nsub, nlu = C.c_int64(), C.c_int64(), C.c_int64()
         self.status = lib().orc_rasm_status(self._h, C.byref(bad), C.byref(nsub), C.byref(nlu))
         self.bad_cell, self.nsub, self.n_lu = bad.value, nsub.value, nlu.value
@@ -342,10 +348,10 @@ def gmres(opA, opM, b, restart=30, max_iters=1000, rtol=1e-13, atol=0.0,
 
 
 def solve(xy, f, sigma, rc, box, cell, rings=1, restart=30, max_iters=1000, rtol=1e-13,
-          atol=0.0, brute=False, orth="mgs") -> GmresResult:
+          atol=0.0, brute=False, orth="mgs", overlap_width=0.0) -> GmresResult:
     """Solve A_rc lambda = f by GMRES(restart) left-preconditioned with RASM
     (the paper's KSPSolve)."""
-    P = Rasm(xy, sigma, rc, box, cell, rings)
+    P = Rasm(xy, sigma, rc, box, cell, rings, overlap_width)
     if P.status != ORC_OK:
         raise ArithmeticError(f"RASM setup failed in cell {P.bad_cell}")
     try:

@@ -398,9 +398,30 @@ typedef struct {
  * per non-empty cell (Q9), A_c the principal submatrix of A_rc (Q10), factored
  * by Cholesky with LU fallback (Q11).  variant_asm != 0 keeps the ASM form
  * (Eq.(8)): every point of Omega_c receives the local solution. */
+orc_rasm *orc_rasm_setup_box(int64_t n, const double *xy, double sigma, double rc,
+                             double x0, double y0, double x1, double y1, double cell,
+                             int64_t rings, double delta);
+
 orc_rasm *orc_rasm_setup(int64_t n, const double *xy, double sigma, double rc,
                          double x0, double y0, double x1, double y1, double cell,
                          int64_t rings) {
+  return orc_rasm_setup_box(n, xy, sigma, rc, x0, y0, x1, y1, cell, rings, 0.0);
+}
+
+/* Box overlap (reading Q24, the paper's "overlapping subdomains of size D"):
+ * with delta > 0, Omega_c keeps, of the block's points, own(c) and every point inside
+ * cell c's box grown by delta on each side, [x0 + cx c - delta, x0 + (cx+1) c + delta]
+ * x [same in y] (closed; D = c + 2 delta).  The order stays the block order. */
+static int in_grown_box(const double *p, int64_t cx, int64_t cy, double x0, double y0,
+                        double cell, double delta) {
+  const double lx = x0 + (double)cx * cell, hx = x0 + (double)(cx + 1) * cell;
+  const double ly = y0 + (double)cy * cell, hy = y0 + (double)(cy + 1) * cell;
+  return p[0] >= lx - delta && p[0] <= hx + delta && p[1] >= ly - delta && p[1] <= hy + delta;
+}
+
+orc_rasm *orc_rasm_setup_box(int64_t n, const double *xy, double sigma, double rc,
+                             double x0, double y0, double x1, double y1, double cell,
+                             int64_t rings, double delta) {
   orc_rasm *P = (orc_rasm *)calloc(1, sizeof(orc_rasm));
   orc_grid g = make_grid(x0, y0, x1, y1, cell);
   int64_t ncells = g.ncx * g.ncy;
@@ -429,8 +450,12 @@ orc_rasm *orc_rasm_setup(int64_t n, const double *xy, double sigma, double rc,
     int64_t cnt = 0;
     for (int64_t by = cy - rings; by <= cy + rings; ++by)
       for (int64_t bx = cx - rings; bx <= cx + rings; ++bx)
-        if (by >= 0 && by < g.ncy && bx >= 0 && bx < g.ncx)
-          cnt += start[by * g.ncx + bx + 1] - start[by * g.ncx + bx];
+        if (by >= 0 && by < g.ncy && bx >= 0 && bx < g.ncx) {
+          int64_t b = by * g.ncx + bx;
+          for (int64_t t = start[b]; t < start[b + 1]; ++t)
+            if (delta <= 0.0 || b == c || in_grown_box(&xy[2 * perm[t]], cx, cy, x0, y0, cell, delta))
+              ++cnt;
+        }
     S->n_ov = cnt;
     S->n_own = start[c + 1] - start[c];
     S->ov = (int64_t *)malloc(sizeof(int64_t) * (size_t)cnt);
@@ -441,6 +466,8 @@ orc_rasm *orc_rasm_setup(int64_t n, const double *xy, double sigma, double rc,
         if (by < 0 || by >= g.ncy || bx < 0 || bx >= g.ncx) continue;
         int64_t b = by * g.ncx + bx;
         for (int64_t t = start[b]; t < start[b + 1]; ++t) {
+          if (!(delta <= 0.0 || b == c || in_grown_box(&xy[2 * perm[t]], cx, cy, x0, y0, cell, delta)))
+            continue;
           if (b == c) S->own_pos[o++] = q;
           S->ov[q++] = perm[t];
         }

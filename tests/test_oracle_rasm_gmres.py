@@ -26,8 +26,9 @@ def _cells(xy, box, cell):
     return cx, cy, ncx, ncy
 
 
-def _explicit_minv(xy, sigma, rc, box, cell, rings, variant="rasm"):
-    """Eq.(5),(9),(11) with explicit 0/1 matrices (N small)."""
+def _explicit_minv(xy, sigma, rc, box, cell, rings, variant="rasm", overlap_width=0.0):
+    """Eq.(5),(9),(11) with explicit 0/1 matrices (N small); overlap_width > 0: the
+    block's points inside the cell box grown by overlap_width (reading Q24)."""
     n = xy.shape[0]
     d = xy[:, None, :] - xy[None, :, :]
     r2 = d[..., 0] ** 2 + d[..., 1] ** 2
@@ -39,7 +40,15 @@ def _explicit_minv(xy, sigma, rc, box, cell, rings, variant="rasm"):
         own = np.nonzero((cx == ccx) & (cy == ccy))[0]
         if own.size == 0:
             continue
-        ov = np.nonzero((np.abs(cx - ccx) <= rings) & (np.abs(cy - ccy) <= rings))[0]
+        inblock = (np.abs(cx - ccx) <= rings) & (np.abs(cy - ccy) <= rings)
+        if overlap_width > 0:
+            lx, hx = box[0] + float(ccx) * cell, box[0] + float(ccx + 1) * cell
+            ly, hy = box[1] + float(ccy) * cell, box[1] + float(ccy + 1) * cell
+            d = overlap_width
+            inbox = ((xy[:, 0] >= lx - d) & (xy[:, 0] <= hx + d) & (xy[:, 1] >= ly - d)
+                     & (xy[:, 1] <= hy + d))
+            inblock &= inbox | ((cx == ccx) & (cy == ccy))
+        ov = np.nonzero(inblock)[0]
         R = np.zeros((ov.size, n)); R[np.arange(ov.size), ov] = 1.0
         Ai = R @ A @ R.T
         if variant == "rasm":
@@ -117,6 +126,58 @@ def test_rasm_partition_property_and_index_sets():
         z2 = P.apply(r2)
         assert np.array_equal(z[own], z2[own])
     P.close()
+
+
+# ----------------------------------------------------------------- box overlap (Q24)
+
+@pytest.mark.parametrize("wl,frac", [(W.make_lattice(14, jitter_frac=0.1, seed=3), 0.45),
+                                     (W.make_lattice(16, jitter_frac=0.3, seed=4), 0.25),
+                                     (W.make_lattice(13), 0.45)])
+def test_rasm_box_overlap_equals_explicit_eq11(wl, frac):
+    """The paper's D = (1 + 2 frac) B overlap box (D = 1.9 B at frac 0.45)."""
+    d = frac * wl.cell
+    Minv, _ = _explicit_minv(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, 1, overlap_width=d)
+    P = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, 1, overlap_width=d)
+    r = np.random.default_rng(9).standard_normal(wl.n)
+    ref = Minv @ r
+    assert np.linalg.norm(P.apply(r) - ref) / np.linalg.norm(ref) < 1e-10
+    P.close()
+
+
+def test_rasm_box_overlap_index_sets_and_limits():
+    wl = W.make_lattice(30, jitter_frac=0.2, seed=6)
+    cx, cy, ncx, ncy = _cells(wl.xy, wl.box, wl.cell)
+    d = 0.45 * wl.cell
+    P = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, 1, overlap_width=d)
+    Pr = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, 1)
+    nonempty = [c for c in range(ncx * ncy) if np.any((cx == c % ncx) & (cy == c // ncx))]
+    for s in (0, 5, 17, P.nsub - 1):
+        c = nonempty[s]
+        ov, own_pos = P.subdomain(s)
+        ovr, _ = Pr.subdomain(s)
+        # brute force over ALL points: inside the grown box (closed) or in the cell
+        lx, ly = wl.box[0] + float(c % ncx) * wl.cell, wl.box[1] + float(c // ncx) * wl.cell
+        hx, hy = wl.box[0] + float(c % ncx + 1) * wl.cell, wl.box[1] + float(c // ncx + 1) * wl.cell
+        x, y = wl.xy[:, 0], wl.xy[:, 1]
+        mine = (cx == c % ncx) & (cy == c // ncx)
+        inside = mine | ((x >= lx - d) & (x <= hx + d) & (y >= ly - d) & (y <= hy + d))
+        assert set(ov.tolist()) == set(np.nonzero(inside)[0].tolist())
+        # block order preserved: the box set is the one-ring set filtered
+        assert list(ov) == [j for j in ovr if inside[j]]
+        assert set(ov[own_pos].tolist()) == set(np.nonzero(mine)[0].tolist())
+    # a box wider than the block keeps the whole block: the one-ring preconditioner
+    Pw = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, 1, overlap_width=10 * wl.cell)
+    r = np.random.default_rng(1).standard_normal(wl.n)
+    assert np.array_equal(Pw.apply(r), Pr.apply(r))
+    P.close(), Pr.close(), Pw.close()
+
+
+def test_solve_box_overlap_vs_dense(cfg1_solution):
+    wl, res, lam = cfg1_solution
+    r = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, rtol=wl.tol,
+                overlap_width=0.45 * wl.cell)
+    assert r.converged and np.linalg.norm(r.x - lam) / np.linalg.norm(lam) < 1e-8
+    assert r.iterations > res.iterations  # a smaller overlap converges more slowly
 
 
 def test_dense_factor_examples_and_lu_fallback():
