@@ -63,7 +63,14 @@ enum {
  *                 fma(dx,dx,dy*dy) < rc*rc (reading Q1).
  *  overlap_rings  >= 0: Omega_c = the (2r+1)^2 block of cells around cell c,
  *                 clipped to the grid (reading Q9); 0 = block Jacobi.
- *  x0,y0,x1,y1    domain box; every point must satisfy x0 <= x <= x1, y0 <= y <= y1. */
+ *  x0,y0,x1,y1    domain box; every point must satisfy x0 <= x <= x1, y0 <= y <= y1.
+ *  overlap_width  >= 0.  0: Omega_c is the whole block (above).  > 0: the paper's box
+ *                 overlap ("overlapping subdomains of size D"; reading Q24):
+ *                 Omega_c = own(c) and the block's points inside cell c's box grown
+ *                 by overlap_width on every side (closed), in block order; D = cell +
+ *                 2 overlap_width (D = 1.9 B: overlap_width = 0.45 cell).  Points
+ *                 outside the block are never included (choose overlap_rings >=
+ *                 overlap_width / cell). */
 typedef struct {
   double sigma;
   double cell;
@@ -71,6 +78,7 @@ typedef struct {
   int32_t overlap_rings;
   int32_t reserved0;
   double x0, y0, x1, y1;
+  double overlap_width;
 } rbf_params;
 
 /* Domain decomposition into strips of cell rows.

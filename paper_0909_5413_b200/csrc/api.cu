@@ -140,6 +140,10 @@ static int validate(const rbf_params *p, long long n) {
     set_error("overlap_rings must be in [0, 7]");
     return RBF_EINVAL;
   }
+  if (!(p->overlap_width >= 0.0) || !std::isfinite(p->overlap_width)) {
+    set_error("overlap_width must be >= 0 (finite)");
+    return RBF_EINVAL;
+  }
   if (!(p->x1 > p->x0) || !(p->y1 > p->y0) || !std::isfinite(p->x0) || !std::isfinite(p->x1) ||
       !std::isfinite(p->y0) || !std::isfinite(p->y1)) {
     set_error("box must satisfy x0 < x1, y0 < y1 (finite)");
@@ -231,6 +235,9 @@ void rbf_destroy(rbf_ctx *c) {
   dfree(c->perm, s);
   dfree(c->xy_ext, s);
   dfree(c->x_off, s);
+  dfree(c->ov_idx, s);
+  dfree(c->ov_off, s);
+  dfree(c->ov_own, s);
   dfree(c->rec, s);
   dfree(c->lane_tgt, s);
   dfree(c->chunk_len, s);
@@ -300,6 +307,7 @@ int rbf_setup(rbf_ctx **out, const double *xy, int64_t n, const rbf_params *p, c
   if (g.ncy < 1) g.ncy = 1;
   g.kh = (int)std::ceil(p->rc / p->cell * (1.0 + 1e-12));
   g.rings = p->overlap_rings;
+  g.ovw = p->overlap_width;
   cudaEvent_t ev[4];
   for (auto &e : ev) cudaEventCreate(&e);
   cudaEventRecord(ev[0], s);

@@ -53,6 +53,16 @@ struct Geom {
   int ncx, ncy;
   int kh;              // matvec search rings = ceil(rc/c), bumped on near-integral rc/c
   int rings;           // RASM overlap rings
+  double ovw;          // box overlap width delta (reading Q24); 0 = whole rings
+};
+
+// Per-cell overlap index lists of the box-overlap subdomains (ovw > 0): the global
+// sorted indices of Omega_c in block order (idx[off[cl] ..]), own(c)'s position
+// inside it (own[cl]).  idx == nullptr: Omega_c is the whole block.
+struct OvList {
+  const int *idx;
+  const long long *off;
+  const int *own;
 };
 
 // This rank's strip of cell rows and its position in the global sorted order.
@@ -182,6 +192,9 @@ struct rbf_ctx {
   double2 *xy_ext = nullptr;   // positions of the ext range, sorted
   // RASM
   long long *x_off = nullptr;  // per owned cell (ncx * owned rows + 1), in doubles
+  int *ov_idx = nullptr;       // box-overlap index lists (OvList), when g.ovw > 0
+  long long *ov_off = nullptr;
+  int *ov_own = nullptr;
   double *X = nullptr;         // rows of A_c^-1 for own(c), row-major, ld = n_ov rounded up to even
   long long x_count = 0;
   int max_ov = 0, max_own = 0, nsub = 0, n_lu = 0;

@@ -31,6 +31,7 @@ struct Runs {
   int lo[kMaxRuns];      // global sorted start of each run
   int len[kMaxRuns];
   int n_ov, n_own, own_nat_lo;
+  const int *list;       // box overlap: Omega_c's global indices (else null: the runs)
 };
 
 // The overlapping subdomain of cell (cx, cy): one contiguous run of the sorted
@@ -43,6 +44,7 @@ __device__ __forceinline__ void block_runs(const Geom &g, const int *__restrict_
   R.n = by1 - by0 + 1;
   R.n_ov = 0;
   R.own_nat_lo = 0;
+  R.list = nullptr;
   for (int r = 0; r < R.n; ++r) {
     const int by = by0 + r;
     R.lo[r] = cell_start[by * g.ncx + bx0];
@@ -53,7 +55,66 @@ __device__ __forceinline__ void block_runs(const Geom &g, const int *__restrict_
   R.n_own = cell_start[key + 1] - cell_start[key];
 }
 
+// Omega_c of owned cell cl: the block's runs, or with box overlap its index list
+__device__ __forceinline__ void sub_runs(const Geom &g, const int *__restrict__ cell_start,
+                                         const OvList &ov, int cl, int cx, int cy, Runs &R) {
+  block_runs(g, cell_start, cx, cy, R);
+  if (ov.idx) {
+    const long long o0 = ov.off[cl];
+    R.list = ov.idx + o0;
+    R.n_ov = (int)(ov.off[cl + 1] - o0);
+    R.own_nat_lo = ov.own[cl];
+  }
+}
+
+// Box-overlap membership (reading Q24): cell (cx, cy)'s box grown by g.ovw, closed;
+// the edges are x0 + cx*c rounded twice (no contraction), exactly as in the oracle.
+__device__ __forceinline__ bool in_grown_box(const Geom &g, double2 p, int cx, int cy) {
+  const double lx = __dadd_rn(g.x0, __dmul_rn((double)cx, g.cell));
+  const double hx = __dadd_rn(g.x0, __dmul_rn((double)(cx + 1), g.cell));
+  const double ly = __dadd_rn(g.y0, __dmul_rn((double)cy, g.cell));
+  const double hy = __dadd_rn(g.y0, __dmul_rn((double)(cy + 1), g.cell));
+  return p.x >= __dsub_rn(lx, g.ovw) && p.x <= __dadd_rn(hx, g.ovw) && p.y >= __dsub_rn(ly, g.ovw) &&
+         p.y <= __dadd_rn(hy, g.ovw);
+}
+
+// MODE 0: |Omega_c| per owned cell (sizes[ncl] = 0 for the scan);  MODE 1: the lists.
+template <int MODE>
+__global__ void k_ov_lists(Geom g, Strip st, const double2 *__restrict__ xy,
+                           const int *__restrict__ cell_start, int ncl, long long *__restrict__ sizes,
+                           const long long *__restrict__ off, int *__restrict__ idx,
+                           int *__restrict__ own) {
+  const int cl = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cl >= ncl) {
+    if (MODE == 0 && cl == ncl) sizes[cl] = 0;
+    return;
+  }
+  const int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
+  const int key = cy * g.ncx + cx;
+  const int o0 = cell_start[key], o1 = cell_start[key + 1];
+  if (o1 == o0) {  // no subdomain
+    if (MODE == 0) sizes[cl] = 0;
+    else own[cl] = 0;
+    return;
+  }
+  Runs R;
+  block_runs(g, cell_start, cx, cy, R);
+  long long q = MODE == 1 ? off[cl] : 0;
+  int cnt = 0, own_at = 0;
+  for (int r = 0; r < R.n; ++r)
+    for (int s = R.lo[r]; s < R.lo[r] + R.len[r]; ++s) {
+      const bool mine = s >= o0 && s < o1;
+      if (!mine && !in_grown_box(g, xy[s - st.ext_lo], cx, cy)) continue;
+      if (s == o0) own_at = cnt;
+      if (MODE == 1) idx[q + cnt] = s;
+      ++cnt;
+    }
+  if (MODE == 0) sizes[cl] = cnt;
+  else own[cl] = own_at;
+}
+
 __device__ __forceinline__ int nat_to_global(const Runs &R, int q) {
+  if (R.list) return R.list[q];
   int r = 0;
   while (q >= R.len[r]) { q -= R.len[r]; ++r; }
   return R.lo[r] + q;
@@ -131,7 +192,7 @@ __device__ __forceinline__ int nat_to_fac(const Runs &R, const TileShape &S, int
 // kernel cannot take (they go to the global-memory LU kernel).
 __global__ void k_rasm_sizes(Geom g, Strip st, const int *__restrict__ cell_start, int ncl,
                              long long *__restrict__ sizes, int *__restrict__ maxes,
-                             int *__restrict__ glist) {
+                             int *__restrict__ glist, OvList ov) {
   int cl = blockIdx.x * blockDim.x + threadIdx.x;
   if (cl >= ncl) {
     if (cl == ncl) sizes[cl] = 0;
@@ -139,7 +200,7 @@ __global__ void k_rasm_sizes(Geom g, Strip st, const int *__restrict__ cell_star
   }
   int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
   Runs R;
-  block_runs(g, cell_start, cx, cy, R);
+  sub_runs(g, cell_start, ov, cl, cx, cy, R);
   long long ld = (R.n_ov + 1) & ~1;
   sizes[cl] = R.n_own ? (long long)R.n_own * ld : 0;
   if (R.n_own) {
@@ -295,7 +356,7 @@ __device__ __forceinline__ void a_entries(const double2 *pos, const TileShape &S
 __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
     Geom g, Strip st, const double2 *__restrict__ xy, const int *__restrict__ cell_start,
     const long long *__restrict__ x_off, double *__restrict__ X, int *__restrict__ counts,
-    int *__restrict__ glist) {
+    int *__restrict__ glist, OvList ov) {
   TRACE(1)
   extern __shared__ __align__(16) double sm[];
   __shared__ Runs R;
@@ -304,7 +365,7 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
   const int cl = blockIdx.x;
   const int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
   if (tid == 0) {
-    block_runs(g, cell_start, cx, cy, R);
+    sub_runs(g, cell_start, ov, cl, cx, cy, R);
     s_fail = 0;
   }
   __syncthreads();
@@ -614,7 +675,8 @@ __device__ __forceinline__ void lu_argmax(double v, int i, double *red_v, int *r
 __global__ __launch_bounds__(kLuThreads, 1) void k_rasm_setup_lu(
     Geom g, Strip st, const double2 *__restrict__ xy, const int *__restrict__ cell_start,
     const long long *__restrict__ x_off, double *__restrict__ X, const int *__restrict__ glist,
-    int first, int count, double *__restrict__ ws, long long ws_stride, int *__restrict__ fail_key) {
+    int first, int count, double *__restrict__ ws, long long ws_stride, int *__restrict__ fail_key,
+    OvList ov) {
   __shared__ Runs R;
   __shared__ double red_v[kLuThreads / 32];
   __shared__ int red_i[kLuThreads / 32];
@@ -627,7 +689,7 @@ __global__ __launch_bounds__(kLuThreads, 1) void k_rasm_setup_lu(
   if ((int)blockIdx.x >= count) return;
   const int cl = glist[first + blockIdx.x];
   const int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
-  if (tid == 0) block_runs(g, cell_start, cx, cy, R);
+  if (tid == 0) sub_runs(g, cell_start, ov, cl, cx, cy, R);
   __syncthreads();
   const int n = R.n_ov, n_own = R.n_own, n0 = n - n_own, own_nat = R.own_nat_lo;
   const long long lda = n + n_own;
@@ -839,7 +901,7 @@ __global__ __launch_bounds__(kLuThreads, 1) void k_rasm_setup_lu(
 // current row's reduction, so the HBM stream never waits on the gather.
 __global__ __launch_bounds__(kRaThreads) void k_rasm_apply(
     Geom g, Strip st, const int *__restrict__ cell_start, const long long *__restrict__ x_off,
-    const double *__restrict__ X, const double *__restrict__ u, double *__restrict__ z) {
+    const double *__restrict__ X, const double *__restrict__ u, double *__restrict__ z, OvList ov) {
   extern __shared__ double su[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int cl = blockIdx.x;
@@ -861,7 +923,7 @@ __global__ __launch_bounds__(kRaThreads) void k_rasm_apply(
   double2 xv[4];
   load4(warp, 0, xv);  // in flight during the gather below
   Runs R;
-  block_runs(g, cell_start, cx, cy, R);
+  sub_runs(g, cell_start, ov, cl, cx, cy, R);
   const int n = R.n_ov;
   for (int q = tid; q < ld; q += kRaThreads) su[q] = (q < n) ? u[nat_to_global(R, q) - st.ext_lo] : 0.0;
   __syncthreads();
@@ -900,6 +962,40 @@ int probe_read(long long *out) {
 #endif
 }
 
+static OvList ov_of(const rbf_ctx *c) { return OvList{c->ov_idx, c->ov_off, c->ov_own}; }
+
+// Box-overlap index lists (reading Q24): count, scan, fill.
+static int build_ov_lists(rbf_ctx *c, int ncl, cudaStream_t s) {
+  dfree(c->ov_idx, s);
+  dfree(c->ov_off, s);
+  dfree(c->ov_own, s);
+  c->ov_idx = nullptr;
+  long long *sizes = nullptr;
+  RBF_TRY(dalloc(c, (void **)&sizes, sizeof(long long) * (ncl + 1), s));
+  RBF_TRY(dalloc(c, (void **)&c->ov_off, sizeof(long long) * (ncl + 1), s));
+  RBF_TRY(dalloc(c, (void **)&c->ov_own, sizeof(int) * (ncl > 0 ? ncl : 1), s));
+  const int blocks = (ncl + 1 + 255) / 256;
+  k_ov_lists<0><<<blocks, 256, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, ncl, sizes, nullptr,
+                                       nullptr, nullptr);
+  RBF_CUDA_TRY(cudaGetLastError());
+  size_t tmp_bytes = 0;
+  RBF_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, sizes, c->ov_off, ncl + 1, s));
+  void *tmp = nullptr;
+  RBF_TRY(dalloc(c, &tmp, tmp_bytes, s));
+  RBF_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, sizes, c->ov_off, ncl + 1, s));
+  long long total = 0;
+  RBF_CUDA_TRY(cudaMemcpyAsync(&total, c->ov_off + ncl, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  dfree(tmp, s);
+  dfree(sizes, s);
+  RBF_TRY(dalloc(c, (void **)&c->ov_idx, sizeof(int) * (size_t)(total > 0 ? total : 1), s));
+  k_ov_lists<1><<<blocks, 256, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, ncl, nullptr, c->ov_off,
+                                       c->ov_idx, c->ov_own);
+  count_launch(3);  // count, scan, fill
+  RBF_CUDA_TRY(cudaGetLastError());
+  return RBF_OK;
+}
+
 int rasm_setup(rbf_ctx *c, cudaStream_t s) {
   const int ncl = owned_cells(c);
   long long *sizes = nullptr;
@@ -909,8 +1005,10 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
   RBF_TRY(dalloc(c, (void **)&cnt, sizeof(int) * 8, s));
   RBF_TRY(dalloc(c, (void **)&glist, sizeof(int) * (ncl > 0 ? ncl : 1), s));
   RBF_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * 8, s));
+  if (c->g.ovw > 0.0) RBF_TRY(build_ov_lists(c, ncl, s));
+  const OvList ov = ov_of(c);
   k_rasm_sizes<<<(ncl + 1 + 255) / 256, 256, 0, s>>>(c->g, c->s, c->cell_start, ncl, sizes, cnt,
-                                                     glist);
+                                                     glist, ov);
   count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
   size_t tmp_bytes = 0;
@@ -937,7 +1035,7 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
     RBF_CUDA_TRY(cudaFuncSetAttribute(k_rasm_setup_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
     k_rasm_setup_tc<<<ncl, kTcThreads, smem, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off,
-                                                  c->X, cnt, glist);
+                                                  c->X, cnt, glist, ov);
     count_launch(1);
     RBF_CUDA_TRY(cudaGetLastError());
     // host work while the kernel runs: GMRES workspace and the solve graph (krylov.cu)
@@ -961,7 +1059,8 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
     for (int first = 0; first < nglobal; first += (int)batch) {
       int count = nglobal - first < batch ? nglobal - first : (int)batch;
       k_rasm_setup_lu<<<count, kLuThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off,
-                                                   c->X, glist, first, count, ws, stride, fail); count_launch(1);
+                                                   c->X, glist, first, count, ws, stride, fail, ov);
+      count_launch(1);
       RBF_CUDA_TRY(cudaGetLastError());
     }
     RBF_CUDA_TRY(cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -990,7 +1089,7 @@ int launch_rasm_apply(const rbf_ctx *c, const double *r_ext, double *z_loc, cuda
     attr_d = smem;
   }
   k_rasm_apply<<<ncl, kRaThreads, smem, s>>>(c->g, c->s, c->cell_start, c->x_off, c->X, r_ext,
-                                             z_loc);
+                                             z_loc, ov_of(c));
   count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
   return RBF_OK;

@@ -30,6 +30,7 @@ class Workload:
     tol: float = 1e-13
     box: tuple = BOX
     meta: dict = field(default_factory=dict)
+    overlap_width: float = 0.0  # box overlap delta (reading Q24); 0 = whole rings
 
     @property
     def n(self) -> int:
@@ -144,13 +145,15 @@ def franke(xy: np.ndarray) -> np.ndarray:
 
 
 def make_paper_lattice(n_side: int, h_over_sigma: float, *, scatter_seed: int | None = None,
-                       tol: float = 1e-13, name: str | None = None) -> Workload:
+                       tol: float = 1e-13, name: str | None = None,
+                       b_over_sigma: float | None = None, d_over_b: float | None = None) -> Workload:
     """The paper's test problem: Franke data on an n x n lattice of
     [0,1]^2 that includes the boundary (x_i = i h, h = 1/(n-1); N = (1/h + 1)^2 as in
     the paper, reading Q4), sigma = h / (h/sigma); quasi-scattered variant: every
-    coordinate shifted by U[0, h/2), PCG64(scatter_seed).  The subdomain
-    geometry is this build's (rc = 6 sigma, cell = 4 sigma, one ring; readings Q1, Q9),
-    not the paper's B/D/T boxes."""
+    coordinate shifted by U[0, h/2), PCG64(scatter_seed).  Subdomain geometry:
+    this build's by default (rc = 6 sigma, cell = 4 sigma, one ring; readings Q1, Q9);
+    with b_over_sigma / d_over_b the paper's boxes: cell B = b sigma,
+    overlap box D = d B (overlap_width (D - B)/2, reading Q24), rc = 6 sigma."""
     h = 1.0 / (n_side - 1)
     sigma = h / h_over_sigma
     c = np.arange(n_side, dtype=np.float64) * h
@@ -161,9 +164,16 @@ def make_paper_lattice(n_side: int, h_over_sigma: float, *, scatter_seed: int | 
         rng = np.random.Generator(np.random.PCG64(scatter_seed))
         xy = xy + rng.uniform(0.0, 0.5 * h, size=xy.shape)
         box = (0.0, 0.0, 1.0 + 0.5 * h, 1.0 + 0.5 * h)
+    cell, ow, rings = 4.0 * sigma, 0.0, 1
+    if b_over_sigma is not None:
+        cell = b_over_sigma * sigma
+        ow = 0.5 * (d_over_b - 1.0) * cell
+        rings = max(1, int(math.ceil(ow / cell - 1e-12)))
     return Workload(name or f"franke{n_side}_{h_over_sigma}", xy, franke(xy), sigma, 6.0 * sigma,
-                    4.0 * sigma, 1, tol, box=box,
-                    meta=dict(h=h, n_side=n_side, h_over_sigma=h_over_sigma, scatter=scatter_seed))
+                    cell, rings, tol, box=box,
+                    meta=dict(h=h, n_side=n_side, h_over_sigma=h_over_sigma, scatter=scatter_seed,
+                              b_over_sigma=b_over_sigma, d_over_b=d_over_b),
+                    overlap_width=ow)
 
 
 def config(k: int) -> Workload:

@@ -24,6 +24,7 @@ import paper_0909_5413_b200 as P  # noqa: E402
 
 def ctx_for(wl, rings=None, **kw):
     xy = torch.from_numpy(wl.xy).cuda()
+    kw.setdefault("overlap_width", wl.overlap_width)
     return P.Context(xy, wl.sigma, wl.cell, wl.rc, wl.rings if rings is None else rings, wl.box, **kw)
 
 
@@ -97,6 +98,61 @@ def test_rasm_apply_parity_lu_path(rings, jit):
         assert c.info()["n_lu"] > 0
         z = to_caller(c, c.rasm_apply(c.to_local(torch.from_numpy(r).cuda())))
     assert rel(z, ref) <= 1e-10
+
+
+# ------------------------------------------------------------------ box overlap (Q24)
+
+@pytest.mark.parametrize("wl,rings,frac", [(SMALL[2], 1, 0.45), (SMALL[1], 1, 0.25),
+                                           (SMALL[3], 1, 0.45),
+                                           (W.make_lattice(48, jitter_frac=0.1, seed=5), 2, 1.5)],
+                         ids=["jitter40", "ragged24", "jitter37", "lu-path"])
+def test_rasm_apply_parity_box_overlap(wl, rings, frac):
+    """The paper's D box: Omega_c = the block's points within overlap_width of
+    the cell box; the last case (640-point boxes) takes the LU path."""
+    d = frac * wl.cell
+    r = np.random.default_rng(23).standard_normal(wl.n)
+    Pc = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, rings, overlap_width=d)
+    ref = Pc.apply(r)
+    Pc.close()
+    with ctx_for(wl, rings=rings, overlap_width=d) as c:
+        if frac > 1:
+            assert c.info()["n_lu"] > 0
+        z = to_caller(c, c.rasm_apply(c.to_local(torch.from_numpy(r).cuda())))
+    assert rel(z, ref) <= 1e-10
+
+
+def test_box_overlap_wide_box_is_whole_block_and_strips():
+    wl = W.make_lattice(60, jitter_frac=0.1, seed=5)
+    r = torch.from_numpy(np.random.default_rng(4).standard_normal(wl.n)).cuda()
+    with ctx_for(wl) as c0, ctx_for(wl, overlap_width=5 * wl.cell) as c1:
+        assert np.array_equal(c0.rasm_apply(c0.to_local(r)).cpu().numpy(),
+                              c1.rasm_apply(c1.to_local(r)).cpu().numpy())
+    d = 0.45 * wl.cell
+    xy = torch.from_numpy(wl.xy).cuda()
+    with ctx_for(wl, overlap_width=d) as c:
+        z1 = c.rasm_apply(c.to_local(r)).cpu().numpy()
+        rs = c.to_local(r)
+    zs = []
+    for g in range(3):  # virtual strips: bitwise the same per-point results (Q20)
+        with P.Context(xy, wl.sigma, wl.cell, wl.rc, 1, wl.box, rank=g, nranks=3,
+                       overlap_width=d) as c:
+            zs.append(c.rasm_apply_ext(rs[c.ext_lo:c.ext_hi].contiguous()).cpu().numpy())
+    assert np.array_equal(np.concatenate(zs), z1)
+
+
+@pytest.mark.parametrize("hs", [1.0, 0.9])
+def test_solve_parity_paper_geometry(hs):
+    """Franke lattice with the paper's optimal boxes B = 5 sigma, D = 1.9 B."""
+    wl = W.make_paper_lattice(81, hs, b_over_sigma=5.0, d_over_b=1.9)
+    ref = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, wl.rings, rtol=wl.tol,
+                  overlap_width=wl.overlap_width)
+    with ctx_for(wl) as c:
+        lam, rep = c.solve(c.to_local(torch.from_numpy(wl.f).cuda()), rtol=wl.tol)
+        lam = to_caller(c, lam)
+    assert rep.converged and ref.converged
+    assert abs(rep.iterations - ref.iterations) <= 2
+    assert rep.resid_true <= 1e-10
+    assert rel(lam, ref.x) <= 1e-8
 
 
 def test_rasm_block_jacobi_parity():
