@@ -61,6 +61,12 @@ def lib():
         L.orc_cell_list.argtypes = [i64, ptr, dbl, dbl, dbl, dbl, dbl, ptr, ptr, ptr]
         L.orc_matvec_cells.restype = C.c_int
         L.orc_matvec_cells.argtypes = [i64, ptr, ptr, dbl, dbl, dbl, dbl, dbl, dbl, dbl, ptr]
+        L.orc_matvec_tbox.argtypes = [i64, ptr, ptr, dbl, dbl, dbl, dbl, dbl, dbl, dbl, i64, ptr,
+                                      ptr]
+        L.orc_matvec_tbox.restype = None
+        L.orc_matvec_tbox_cells.restype = C.c_int
+        L.orc_matvec_tbox_cells.argtypes = [i64, ptr, ptr, dbl, dbl, dbl, dbl, dbl, dbl, dbl, ptr]
+        L.orc_op_rbf_tbox.argtypes = [ptr, i64, ptr, dbl, dbl, dbl, dbl, dbl, dbl, dbl]
         L.orc_count_pairs.restype = i64
         L.orc_count_pairs.argtypes = [i64, ptr, dbl, dbl, dbl, dbl, dbl, dbl]
         L.orc_dense_factor_solve.restype = C.c_int
@@ -201,6 +207,32 @@ def matvec_cells(xy, w, sigma: float, rc: float, box, cell: float) -> np.ndarray
     return y
 
 
+def matvec_tbox(xy, w, sigma: float, box, cell: float, tau: float, rows=None,
+                cells: bool = False) -> np.ndarray:
+    """The paper's T-box truncation (reading Q25): y_i = sum_j
+    [x_j in T(cell(i))] w_j phi(r2_ij), T(c) = cell c's box grown by tau on every side
+    (closed), brute force over all j (cells=True: the cell-list form, all rows)."""
+    xy, w = _f64(xy), _f64(w)
+    n = xy.shape[0]
+    if cells:
+        y = np.empty(n, dtype=np.float64)
+        st = lib().orc_matvec_tbox_cells(n, _p(xy), _p(w), float(sigma), *map(float, box),
+                                         float(cell), float(tau), _p(y))
+        if st != ORC_OK:
+            raise MemoryError("orc_matvec_tbox_cells")
+        return y
+    if rows is None:
+        y = np.empty(n, dtype=np.float64)
+        lib().orc_matvec_tbox(n, _p(xy), _p(w), float(sigma), *map(float, box), float(cell),
+                              float(tau), 0, None, _p(y))
+    else:
+        rows = _i64(rows)
+        y = np.empty(rows.shape[0], dtype=np.float64)
+        lib().orc_matvec_tbox(n, _p(xy), _p(w), float(sigma), *map(float, box), float(cell),
+                              float(tau), rows.shape[0], _p(rows), _p(y))
+    return y
+
+
 def count_pairs(xy, rc: float, box, cell: float) -> int:
     """Number of ordered pairs (i, j), i == j included, with r2_ij < rc^2."""
     xy = _f64(xy)
@@ -318,6 +350,14 @@ def op_rbf(xy, sigma, rc, box, cell, brute=False):
     return (b, xy)
 
 
+def op_rbf_tbox(xy, sigma, box, cell, tau):
+    xy = _f64(xy)
+    b = _op_buf()
+    lib().orc_op_rbf_tbox(_addr(b), xy.shape[0], _p(xy), float(sigma), *map(float, box),
+                          float(cell), float(tau))
+    return (b, xy)
+
+
 def op_rasm(P: Rasm, variant: str = "rasm"):
     b = _op_buf(); lib().orc_op_rasm(_addr(b), P._h, int(variant == "asm")); return (b, P)
 
@@ -348,14 +388,18 @@ def gmres(opA, opM, b, restart=30, max_iters=1000, rtol=1e-13, atol=0.0,
 
 
 def solve(xy, f, sigma, rc, box, cell, rings=1, restart=30, max_iters=1000, rtol=1e-13,
-          atol=0.0, brute=False, orth="mgs", overlap_width=0.0) -> GmresResult:
+          atol=0.0, brute=False, orth="mgs", overlap_width=0.0,
+          trunc_width=0.0) -> GmresResult:
     """Solve A_rc lambda = f by GMRES(restart) left-preconditioned with RASM
-    (the paper's KSPSolve)."""
+    (the paper's KSPSolve).  trunc_width > 0 solves with the
+    paper's T-box matvec instead (reading Q25; the local matrices stay A_rc's)."""
     P = Rasm(xy, sigma, rc, box, cell, rings, overlap_width)
     if P.status != ORC_OK:
         raise ArithmeticError(f"RASM setup failed in cell {P.bad_cell}")
     try:
-        return gmres(op_rbf(xy, sigma, rc, box, cell, brute), op_rasm(P), f, restart,
+        opA = (op_rbf_tbox(xy, sigma, box, cell, trunc_width) if trunc_width > 0
+               else op_rbf(xy, sigma, rc, box, cell, brute))
+        return gmres(opA, op_rasm(P), f, restart,
                      max_iters, rtol, atol, orth=orth)
     finally:
         P.close()

@@ -28,6 +28,9 @@
  *       rotations, x0 = 0; stop when |g_{k+1}| <= max(rtol*||M^-1 f||, atol);
  *       explicit preconditioned residual at each restart; happy breakdown when
  *       h_{k+1,k} == 0.
+ *   Q25 (optional) the paper's T-box matvec truncation: row i
+ *       keeps the sources inside target i's cell box grown by tau (closed); the
+ *       local matrices of the preconditioner stay principal submatrices of A_rc.
  */
 #include <math.h>
 #include <stdint.h>
@@ -275,6 +278,86 @@ int64_t orc_count_pairs(int64_t n, const double *xy, double rc, double x0,
   free(perm);
   free(start);
   return total;
+}
+
+/* ------------------------------------------------------------------------ */
+/* T-box truncation (the paper's own matvec rule; reading Q25): */
+/* "an additional subdomain with size T, which defines the non-zero entries   */
+/* for the matrix-vector multiplication.  Everything outside of this region   */
+/* is neglected when calculating A x for Omega~_i", T = B + 4 sigma*/
+/* for h/sigma >= 0.9 and B + 6 sigma for 0.8.  Row i keeps      */
+/* source j iff x_j lies in the closed box of target i's cell (the B box)     */
+/* grown by tau = (T - B)/2 on every side:                                    */
+/*   [x0 + cx c - tau, x0 + (cx+1) c + tau] x [same in y],                    */
+/* edges formed as in reading Q24.  No radial test; the matrix is not         */
+/* symmetric (targets of one cell share one box).                             */
+/* ------------------------------------------------------------------------ */
+
+static int in_tbox(const double *p, int64_t cx, int64_t cy, double x0, double y0, double cell,
+                   double tau) {
+  const double lx = x0 + (double)cx * cell, hx = x0 + (double)(cx + 1) * cell;
+  const double ly = y0 + (double)cy * cell, hy = y0 + (double)(cy + 1) * cell;
+  return p[0] >= lx - tau && p[0] <= hx + tau && p[1] >= ly - tau && p[1] <= hy + tau;
+}
+
+/* Plain definition, O(N^2): y_i = sum_{j=0..n-1} [x_j in T(cell(i))] w_j phi(r2_ij),
+ * ascending j.  rows as in orc_matvec_brute. */
+void orc_matvec_tbox(int64_t n, const double *xy, const double *w, double sigma, double x0,
+                     double y0, double x1, double y1, double cell, double tau, int64_t nrows,
+                     const int64_t *rows, double *y) {
+  orc_grid g = make_grid(x0, y0, x1, y1, cell);
+  int64_t m = rows ? nrows : n;
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t k = 0; k < m; ++k) {
+    int64_t i = rows ? rows[k] : k;
+    int64_t cx = cell_coord(xy[2 * i], g.x0, g.cell, g.ncx);
+    int64_t cy = cell_coord(xy[2 * i + 1], g.y0, g.cell, g.ncy);
+    double acc = 0.0;
+    for (int64_t j = 0; j < n; ++j)
+      if (in_tbox(&xy[2 * j], cx, cy, x0, y0, cell, tau))
+        acc += w[j] * orc_phi(sigma, sqdist(xy, i, j));
+    y[k] = acc;
+  }
+}
+
+/* Cell-list version (an acceleration only, pinned to orc_matvec_tbox): the box
+ * reaches floor(tau/c) + 1 cells beyond the target's cell at most. */
+int orc_matvec_tbox_cells(int64_t n, const double *xy, const double *w, double sigma,
+                          double x0, double y0, double x1, double y1, double cell, double tau,
+                          double *y) {
+  orc_grid g = make_grid(x0, y0, x1, y1, cell);
+  int64_t ncells = g.ncx * g.ncy;
+  int64_t *key = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+  int64_t *perm = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+  int64_t *start = (int64_t *)malloc(sizeof(int64_t) * (size_t)(ncells + 1));
+  if (!key || !perm || !start) {
+    free(key); free(perm); free(start);
+    return ORC_ENOMEM;
+  }
+  orc_cell_list(n, xy, x0, y0, x1, y1, cell, key, perm, start);
+  int64_t kh = (int64_t)floor(tau / cell * (1.0 + 1e-12)) + 1;
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t cx = key[i] % g.ncx, cy = key[i] / g.ncx;
+    double acc = 0.0;
+    for (int64_t by = cy - kh; by <= cy + kh; ++by) {
+      if (by < 0 || by >= g.ncy) continue;
+      for (int64_t bx = cx - kh; bx <= cx + kh; ++bx) {
+        if (bx < 0 || bx >= g.ncx) continue;
+        int64_t c = by * g.ncx + bx;
+        for (int64_t s = start[c]; s < start[c + 1]; ++s) {
+          int64_t j = perm[s];
+          if (in_tbox(&xy[2 * j], cx, cy, x0, y0, cell, tau))
+            acc += w[j] * orc_phi(sigma, sqdist(xy, i, j));
+        }
+      }
+    }
+    y[i] = acc;
+  }
+  free(key);
+  free(perm);
+  free(start);
+  return ORC_OK;
 }
 
 /* ------------------------------------------------------------------------ */
@@ -572,13 +655,14 @@ void orc_rasm_free(orc_rasm *P) {
 typedef void (*orc_apply_fn)(void *ctx, const double *x, double *y);
 
 enum { ORC_OP_IDENTITY = 0, ORC_OP_DENSE = 1, ORC_OP_RBF = 2, ORC_OP_RASM = 3,
-       ORC_OP_RBF_BRUTE = 4 };
+       ORC_OP_RBF_BRUTE = 4, ORC_OP_RBF_TBOX = 5 };
 
 typedef struct {
   int kind;
   int64_t n;
   const double *A; /* dense */
   const double *xy; double sigma, rc, x0, y0, x1, y1, cell; /* rbf */
+  double tau;                                                /* rbf T-box (Q25) */
   const orc_rasm *P; int asm_variant;                        /* rasm */
 } orc_op;
 
@@ -602,6 +686,10 @@ static void op_apply(const orc_op *op, const double *x, double *y) {
     break;
   case ORC_OP_RBF_BRUTE:
     orc_matvec_brute(n, op->xy, x, op->sigma, op->rc, 0, 0, NULL, y);
+    break;
+  case ORC_OP_RBF_TBOX:
+    orc_matvec_tbox_cells(n, op->xy, x, op->sigma, op->x0, op->y0, op->x1, op->y1, op->cell,
+                          op->tau, y);
     break;
   case ORC_OP_RASM:
     orc_rasm_apply(op->P, x, y, op->asm_variant);
@@ -774,6 +862,14 @@ void orc_op_rbf(orc_op *op, int64_t n, const double *xy, double sigma, double rc
   memset(op, 0, sizeof(*op));
   op->kind = brute ? ORC_OP_RBF_BRUTE : ORC_OP_RBF;
   op->n = n; op->xy = xy; op->sigma = sigma; op->rc = rc;
+  op->x0 = x0; op->y0 = y0; op->x1 = x1; op->y1 = y1; op->cell = cell;
+}
+/* the T-box operator of reading Q25 (cell-list form) */
+void orc_op_rbf_tbox(orc_op *op, int64_t n, const double *xy, double sigma, double x0,
+                     double y0, double x1, double y1, double cell, double tau) {
+  memset(op, 0, sizeof(*op));
+  op->kind = ORC_OP_RBF_TBOX;
+  op->n = n; op->xy = xy; op->sigma = sigma; op->tau = tau;
   op->x0 = x0; op->y0 = y0; op->x1 = x1; op->y1 = y1; op->cell = cell;
 }
 void orc_op_rasm(orc_op *op, const orc_rasm *P, int asm_variant) {

@@ -211,3 +211,82 @@ def test_evaluate_constant_weights_poisson_off_lattice():
     assert np.max(np.abs(s_ex - expect)) <= 1e-14  # 10^4-term sum of O(1) values
     gap = s_ex - s_ct
     assert np.all(gap >= 0.0) and np.all(gap <= 3e-8)  # tail e^-18-scale mass
+
+
+# ------------------------------------------- T-box truncation (reading Q25, §8.f2)
+# The paper's matvec rule: row i keeps the sources inside the box T of
+# target i's cell, T = B + 2 tau (tau = 2 sigma for h/sigma >= 0.9, 3 sigma at 0.8,
+# P:307, 348).
+
+def _tbox_separable(n_side, tau_over_h, ax, by):
+    """Closed form on a cell-centred lattice with cell = 5h and separable weights
+    w_j = ax[jx] * by[jy]: the box is a product of index intervals, so row i is
+    norm * (sum_{jx in Jx} ax[jx] e^{-(ix-jx)^2 h^2/2s^2}) * (same in y), with Jx found
+    in exact rational arithmetic from x_j = -1 + (j + 1/2) h and the cell edges
+    -1 + 5 cx h (no floating-point membership test)."""
+    from fractions import Fraction as F
+    q = F(tau_over_h)
+    c2 = 0.8 * 0.8 / 2.0  # h^2 / (2 sigma^2) at h/sigma = 0.8
+    cells = (n_side + 4) // 5
+
+    def interval(c):
+        lo = [j for j in range(n_side) if F(2 * j + 1, 2) >= 5 * c - q]
+        hi = [j for j in range(n_side) if F(2 * j + 1, 2) <= 5 * c + 5 + q]
+        return range(lo[0], hi[-1] + 1)
+
+    J = [interval(c) for c in range(cells)]
+    sx = np.array([sum(ax[j] * math.exp(-c2 * (i - j) ** 2) for j in J[i // 5]) for i in range(n_side)])
+    sy = np.array([sum(by[j] * math.exp(-c2 * (i - j) ** 2) for j in J[i // 5]) for i in range(n_side)])
+    return np.outer(sy, sx).ravel()  # index iy * n + ix
+
+
+@pytest.mark.parametrize("n_side,tau_over_h", [(62, "15/4"), (62, "2"), (40, "6/5")])
+def test_tbox_separable_closed_form(n_side, tau_over_h):
+    from fractions import Fraction as F
+    wl = W.make_lattice(n_side)
+    h = wl.meta["h"]
+    rng = np.random.default_rng(25)
+    ax, by = rng.uniform(0.5, 1.5, n_side), rng.uniform(-1.0, 1.0, n_side)
+    w = np.outer(by, ax).ravel()
+    tau = float(F(tau_over_h)) * h
+    y = O.matvec_tbox(wl.xy, w, wl.sigma, wl.box, wl.cell, tau)
+    ref = _tbox_separable(n_side, tau_over_h, ax, by) / (2.0 * math.pi * wl.sigma ** 2)
+    assert np.abs(y - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_tbox_covering_everything_is_the_exact_operator():
+    wl = W.make_lattice(24, jitter_frac=0.1, seed=2)
+    w = np.random.default_rng(3).standard_normal(wl.n)
+    y = O.matvec_tbox(wl.xy, w, wl.sigma, wl.box, wl.cell, 2.5)
+    ref = O.matvec_brute(wl.xy, w, wl.sigma, None)
+    assert np.abs(y - ref).max() <= 1e-14 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("kind", ["jitter", "clustered"])
+def test_tbox_pattern_and_cells_form(kind):
+    wl = (W.make_lattice(21, jitter_frac=0.1, seed=4) if kind == "jitter"
+          else W.make_clustered(500, seed=5))
+    n, box, c = wl.n, wl.box, wl.cell
+    for tau in (2 * wl.sigma, 3 * wl.sigma, c, 2 * c):
+        # the dense matrix column by column vs a numpy membership scan
+        A = np.stack([O.matvec_tbox(wl.xy, np.eye(n)[j], wl.sigma, box, c, tau) for j in range(n)], 1)
+        key, _, _ = O.cell_list(wl.xy, box, c)
+        ncx, _ = O.grid_dims(box, c)
+        cx, cy = key % ncx, key // ncx
+        lx, ly = box[0] + cx * c, box[1] + cy * c
+        hx, hy = box[0] + (cx + 1) * c, box[1] + (cy + 1) * c
+        X, Y = wl.xy[:, 0][None, :], wl.xy[:, 1][None, :]
+        M = ((X >= (lx - tau)[:, None]) & (X <= (hx + tau)[:, None]) &
+             (Y >= (ly - tau)[:, None]) & (Y <= (hy + tau)[:, None]))
+        assert np.array_equal(A != 0.0, M)
+        d2 = ((wl.xy[:, None, :] - wl.xy[None, :, :]) ** 2).sum(-1)
+        ref = np.exp(-d2 / (2 * wl.sigma ** 2)) / (2 * math.pi * wl.sigma ** 2)
+        assert np.allclose(A[M], ref[M], rtol=1e-13, atol=0)
+        if tau < c:
+            assert not np.array_equal(M, M.T)  # one box per target cell: not symmetric
+        w = np.random.default_rng(6).standard_normal(n)
+        y1 = O.matvec_tbox(wl.xy, w, wl.sigma, box, c, tau)
+        y2 = O.matvec_tbox(wl.xy, w, wl.sigma, box, c, tau, cells=True)
+        assert np.abs(y1 - y2).max() <= 1e-14 * np.abs(y1).max()
+        rows = np.array([0, n // 3, n - 1])
+        assert np.array_equal(O.matvec_tbox(wl.xy, w, wl.sigma, box, c, tau, rows=rows), y1[rows])

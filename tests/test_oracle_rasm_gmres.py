@@ -363,3 +363,44 @@ def test_mesh_independent_iterations():
         assert res.converged
         its.append(res.iterations)
     assert abs(its[0] - its[1]) <= 3
+
+
+@pytest.mark.parametrize("case", ["lattice0.8_tau3", "paper1.0_tau2", "paper0.9_tau2_scattered"])
+def test_solve_tbox_vs_dense(case):
+    # The paper's T-box matvec (reading Q25; T = B + 6 sigma at h/sigma = 0.8,
+    # B + 4 sigma at h/sigma >= 0.9): GMRES + RASM on A_T lambda = f reaches
+    # the LAPACK solution of the dense (non-symmetric) A_T.
+    if case == "lattice0.8_tau3":
+        wl = W.make_lattice(26, jitter_frac=0.1, seed=2, s2=0.05)
+        tau = 3.0 * wl.sigma
+    elif case == "paper1.0_tau2":
+        wl = W.make_paper_lattice(27, 1.0, b_over_sigma=5.0, d_over_b=1.9)
+        tau = 2.0 * wl.sigma
+    else:
+        wl = W.make_paper_lattice(25, 0.9, scatter_seed=7, b_over_sigma=6.0, d_over_b=1.9)
+        tau = 3.0 * wl.sigma
+    n = wl.n
+    A = np.stack([O.matvec_tbox(wl.xy, np.eye(n)[j], wl.sigma, wl.box, wl.cell, tau)
+                  for j in range(n)], 1)
+    lam = np.linalg.solve(A, wl.f)
+    r = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, rings=wl.rings, rtol=1e-13,
+                overlap_width=wl.overlap_width, trunc_width=tau)
+    assert r.converged
+    assert np.linalg.norm(r.x - lam) / np.linalg.norm(lam) < 1e-8
+    assert np.linalg.norm(wl.f - A @ r.x) / np.linalg.norm(wl.f) < 1e-10
+    assert r.resid_true < 1e-10
+
+
+def test_tbox_too_small_at_h_sigma_08_stalls():
+    # The paper's reason for T = B + 6 sigma at h/sigma = 0.8: with
+    # T = B + 4 sigma the truncated matrix has an eigenvalue of negative real part
+    # on this lattice and preconditioned GMRES stalls.
+    wl = W.make_lattice(26, jitter_frac=0.1, seed=2, s2=0.05)
+    tau = 2.0 * wl.sigma
+    n = wl.n
+    A = np.stack([O.matvec_tbox(wl.xy, np.eye(n)[j], wl.sigma, wl.box, wl.cell, tau)
+                  for j in range(n)], 1)
+    assert np.linalg.eigvals(A).real.min() < 0.0
+    r = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, rtol=1e-13, max_iters=200,
+                trunc_width=tau)
+    assert not r.converged
