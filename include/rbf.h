@@ -70,7 +70,17 @@ enum {
  *                 by overlap_width on every side (closed), in block order; D = cell +
  *                 2 overlap_width (D = 1.9 B: overlap_width = 0.45 cell).  Points
  *                 outside the block are never included (choose overlap_rings >=
- *                 overlap_width / cell). */
+ *                 overlap_width / cell).
+ *  trunc_width    >= 0, <= 8 cell.  0: the matvec keeps the pairs with r < rc (Q1).  > 0:
+ *                 the paper's T-box truncation ("an additional subdomain with
+ *                 size T, which defines the non-zero entries for the matrix-vector
+ *                 multiplication"; T = B + 4 sigma for h/sigma >= 0.9, B + 6 sigma at 0.8,
+ *                 P:307, 348; reading Q25): row i of A keeps the sources inside target i's
+ *                 cell box grown by trunc_width on every side (closed, edges as in Q24),
+ *                 with no radial test; the matrix is then not symmetric.  It applies to
+ *                 rbf_matvec, rbf_solve (A_T lambda = f), rbf_evaluate (the query's cell
+ *                 box) and rbf_count_pairs; the preconditioner's local matrices stay the
+ *                 principal submatrices of A_rc (rc still required). */
 typedef struct {
   double sigma;
   double cell;
@@ -79,6 +89,7 @@ typedef struct {
   int32_t reserved0;
   double x0, y0, x1, y1;
   double overlap_width;
+  double trunc_width;
 } rbf_params;
 
 /* Domain decomposition into strips of cell rows.
@@ -179,7 +190,8 @@ int rbf_to_local(const rbf_ctx *ctx, const double *v_caller_dev, double *v_loc_d
 int rbf_from_local(const rbf_ctx *ctx, const double *v_loc_dev, double *v_caller_dev, void *stream);
 
 /* y = A_rc w on this rank's points (MatMult): halo exchange of w
- * (ceil(rc/c) cell rows from each strip neighbour) then the cutoff matvec. */
+ * (ceil(rc/c) cell rows from each strip neighbour; floor(trunc_width/c) + 1 rows
+ * with the T-box) then the cutoff matvec (y = A_T w with the T-box, reading Q25). */
 int rbf_matvec(rbf_ctx *ctx, const double *w_loc_dev, double *y_loc_dev, void *stream);
 /* z = M^-1 r (PCApply / MatSolve, Eq.(10)-(11)): halo exchange of r
  * (overlap_rings rows), then z[own(c)] = (A_c^-1 R_c r)[own(c)] for every cell. */

@@ -66,6 +66,9 @@ def lib():
         L.orc_matvec_tbox.restype = None
         L.orc_matvec_tbox_cells.restype = C.c_int
         L.orc_matvec_tbox_cells.argtypes = [i64, ptr, ptr, dbl, dbl, dbl, dbl, dbl, dbl, dbl, ptr]
+        L.orc_evaluate_tbox.argtypes = [i64, ptr, i64, ptr, ptr, dbl, dbl, dbl, dbl, dbl, dbl,
+                                        dbl, ptr]
+        L.orc_evaluate_tbox.restype = None
         L.orc_op_rbf_tbox.argtypes = [ptr, i64, ptr, dbl, dbl, dbl, dbl, dbl, dbl, dbl]
         L.orc_count_pairs.restype = i64
         L.orc_count_pairs.argtypes = [i64, ptr, dbl, dbl, dbl, dbl, dbl, dbl]
@@ -164,6 +167,17 @@ def evaluate(q, xy, lam, sigma: float, rc: float | None) -> np.ndarray:
     exact = rc is None
     lib().orc_evaluate(q.shape[0], _p(q), xy.shape[0], _p(xy), _p(lam), float(sigma),
                        0.0 if exact else float(rc), int(exact), _p(s))
+    return s
+
+
+def evaluate_tbox(q, xy, lam, sigma: float, box, cell: float, tau: float) -> np.ndarray:
+    """Interpolant with the T-box of reading Q25: s(q) = sum_j [x_j in T(cell(q))]
+    lambda_j phi(|q - x_j|^2), brute force.  Pinned: at the data points it is
+    matvec_tbox (tests/test_oracle_kernel_matvec.py)."""
+    q, xy, lam = _f64(q), _f64(xy), _f64(lam)
+    s = np.empty(q.shape[0], dtype=np.float64)
+    lib().orc_evaluate_tbox(q.shape[0], _p(q), xy.shape[0], _p(xy), _p(lam), float(sigma),
+                            *map(float, box), float(cell), float(tau), _p(s))
     return s
 
 

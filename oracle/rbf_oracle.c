@@ -320,6 +320,28 @@ void orc_matvec_tbox(int64_t n, const double *xy, const double *w, double sigma,
   }
 }
 
+/* Interpolant with the T-box (Eq.(1), reading Q25): s(q_k) = sum_j [x_j in
+ * T(cell(q_k))] lambda_j phi(|q_k - x_j|^2), ascending j.  At q_k = x_k: row k of
+ * orc_matvec_tbox. */
+void orc_evaluate_tbox(int64_t m, const double *q, int64_t n, const double *xy,
+                       const double *lam, double sigma, double x0, double y0, double x1,
+                       double y1, double cell, double tau, double *s) {
+  orc_grid g = make_grid(x0, y0, x1, y1, cell);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t k = 0; k < m; ++k) {
+    int64_t cx = cell_coord(q[2 * k], g.x0, g.cell, g.ncx);
+    int64_t cy = cell_coord(q[2 * k + 1], g.y0, g.cell, g.ncy);
+    double acc = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+      if (!in_tbox(&xy[2 * j], cx, cy, x0, y0, cell, tau)) continue;
+      double dx = q[2 * k] - xy[2 * j];
+      double dy = q[2 * k + 1] - xy[2 * j + 1];
+      acc += lam[j] * orc_phi(sigma, fma(dx, dx, dy * dy));
+    }
+    s[k] = acc;
+  }
+}
+
 /* Cell-list version (an acceleration only, pinned to orc_matvec_tbox): the box
  * reaches floor(tau/c) + 1 cells beyond the target's cell at most. */
 int orc_matvec_tbox_cells(int64_t n, const double *xy, const double *w, double sigma,

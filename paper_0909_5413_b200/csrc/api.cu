@@ -144,6 +144,10 @@ static int validate(const rbf_params *p, long long n) {
     set_error("overlap_width must be >= 0 (finite)");
     return RBF_EINVAL;
   }
+  if (!(p->trunc_width >= 0.0) || !(p->trunc_width <= 8.0 * p->cell)) {
+    set_error("trunc_width must be in [0, 8 cell] (finite)");
+    return RBF_EINVAL;
+  }
   if (!(p->x1 > p->x0) || !(p->y1 > p->y0) || !std::isfinite(p->x0) || !std::isfinite(p->x1) ||
       !std::isfinite(p->y0) || !std::isfinite(p->y1)) {
     set_error("box must satisfy x0 < x1, y0 < y1 (finite)");
@@ -306,6 +310,9 @@ int rbf_setup(rbf_ctx **out, const double *xy, int64_t n, const rbf_params *p, c
   if (g.ncx < 1) g.ncx = 1;
   if (g.ncy < 1) g.ncy = 1;
   g.kh = (int)std::ceil(p->rc / p->cell * (1.0 + 1e-12));
+  g.tw = p->trunc_width;
+  // T-box (reading Q25): the box reaches floor(tw/c) + 1 cells beyond the target's cell
+  if (g.tw > 0.0) g.kh = (int)std::floor(g.tw / p->cell * (1.0 + 1e-12)) + 1;
   g.rings = p->overlap_rings;
   g.ovw = p->overlap_width;
   cudaEvent_t ev[4];

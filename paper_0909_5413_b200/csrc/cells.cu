@@ -193,6 +193,7 @@ __global__ void k_count_pairs(Geom g, Strip st, const double2 *__restrict__ xy,
   int bx0 = max(cx - g.kh, 0), bx1 = min(cx + g.kh, g.ncx - 1);
   int by0 = max(cy - g.kh, 0), by1 = min(cy + g.kh, g.ncy - 1);
   unsigned long long cnt = 0;
+  const CellBox tb = cell_box(g, cx, cy, g.tw);  // T-box rows (reading Q25)
   for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
     double2 p = xy[t - st.ext_lo];
     for (int by = by0; by <= by1; ++by) {
@@ -200,7 +201,7 @@ __global__ void k_count_pairs(Geom g, Strip st, const double2 *__restrict__ xy,
       for (int q = s0; q < s1; ++q) {
         double2 o = xy[q - st.ext_lo];
         double dx = p.x - o.x, dy = p.y - o.y;
-        if (fma(dx, dx, dy * dy) < g.rc2) ++cnt;
+        if (g.tw > 0.0 ? in_box(tb, o.x, o.y) : fma(dx, dx, dy * dy) < g.rc2) ++cnt;
       }
     }
   }

@@ -54,7 +54,25 @@ struct Geom {
   int kh;              // matvec search rings = ceil(rc/c), bumped on near-integral rc/c
   int rings;           // RASM overlap rings
   double ovw;          // box overlap width delta (reading Q24); 0 = whole rings
+  double tw;           // T-box truncation width tau (reading Q25); 0 = radial cutoff rc
 };
+
+// Cell (cx, cy)'s box grown by w on every side, closed (readings Q24, Q25); the
+// edges are x0 + cx*c rounded twice (no contraction), exactly as in the oracle.
+struct CellBox {
+  double lx, hx, ly, hy;
+};
+__device__ __forceinline__ CellBox cell_box(const Geom &g, int cx, int cy, double w) {
+  CellBox b;
+  b.lx = __dsub_rn(__dadd_rn(g.x0, __dmul_rn((double)cx, g.cell)), w);
+  b.hx = __dadd_rn(__dadd_rn(g.x0, __dmul_rn((double)(cx + 1), g.cell)), w);
+  b.ly = __dsub_rn(__dadd_rn(g.y0, __dmul_rn((double)cy, g.cell)), w);
+  b.hy = __dadd_rn(__dadd_rn(g.y0, __dmul_rn((double)(cy + 1), g.cell)), w);
+  return b;
+}
+__device__ __forceinline__ bool in_box(const CellBox &b, double x, double y) {
+  return x >= b.lx && x <= b.hx && y >= b.ly && y <= b.hy;
+}
 
 // Per-cell overlap index lists of the box-overlap subdomains (ovw > 0): the global
 // sorted indices of Omega_c in block order (idx[off[cl] ..]), own(c)'s position

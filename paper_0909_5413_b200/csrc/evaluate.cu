@@ -2,6 +2,8 @@
 //
 //   s(q) = norm * sum_{j : |q - x_j| < rc} lambda_j exp(-|q - x_j|^2 / (2 sigma^2))
 //
+// (with the T-box of reading Q25: j in the query cell's box grown by trunc_width)
+//
 // the RBF interpolant of Eq.(1) with the Gaussian of Eq.(12) and the
 // truncation of reading Q1 -- the paper's application, interpolation from
 // scattered points onto a lattice.
@@ -47,6 +49,8 @@ __global__ __launch_bounds__(256) void k_evaluate(Geom g, const double *__restri
   const double qx = q[2LL * k], qy = q[2LL * k + 1];
   const int bx0 = max(cx - g.kh, 0), bx1 = min(cx + g.kh, g.ncx - 1);
   const int by0 = max(cy - g.kh, 0), by1 = min(cy + g.kh, g.ncy - 1);
+  const CellBox tb = cell_box(g, cx, cy, g.tw);  // the query cell's T-box (reading Q25)
+  const bool tbox = g.tw > 0.0;
   double acc = 0.0;
   for (int by = by0; by <= by1; ++by) {
     const int s0 = cell_start[by * g.ncx + bx0], s1 = cell_start[by * g.ncx + bx1 + 1];
@@ -54,7 +58,7 @@ __global__ __launch_bounds__(256) void k_evaluate(Geom g, const double *__restri
       const double4 o = ld_rec(rec + j);
       const double dx = qx - o.x, dy = qy - o.y;
       const double r2 = fma(dx, dx, dy * dy);
-      if (r2 < g.rc2) acc = fma(o.z, gauss_exp2<kExpDeg>(r2, g.esc), acc);
+      if (tbox ? in_box(tb, o.x, o.y) : r2 < g.rc2) acc = fma(o.z, gauss_exp2<kExpDeg>(r2, g.esc), acc);
     }
   }
   s[k] = acc * g.norm;

@@ -108,14 +108,17 @@ __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const do
   if (MODE == 1 && in_chunk) base = chunk_off[ch];
   double2 p[G];
   bool act[G];
+  CellBox tb[G];  // T-box of each target's cell (reading Q25; used when g.tw > 0)
+  const bool tbox = g.tw > 0.0;
   int bx0 = g.ncx, bx1 = -1, by0 = g.ncy, by1 = -1;
 #pragma unroll
   for (int j = 0; j < G; ++j) {
     act[j] = t[j] >= 0;
     p[j] = xy[own_off + (act[j] ? t[j] : 0)];
+    int cx = 0, cy = 0;
+    if (act[j]) target_cell(g, p[j], cx, cy);
+    tb[j] = cell_box(g, cx, cy, g.tw);
     if (act[j]) {
-      int cx, cy;
-      target_cell(g, p[j], cx, cy);
       bx0 = min(bx0, max(cx - g.kh, 0));
       bx1 = max(bx1, min(cx + g.kh, g.ncx - 1));
       by0 = min(by0, max(cy - g.kh, 0));
@@ -130,7 +133,8 @@ __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const do
 #pragma unroll
       for (int j = 0; j < G; ++j) {
         const double dx = p[j].x - o.x, dy = p[j].y - o.y;
-        if (act[j] && fma(dx, dx, dy * dy) < g.rc2) m |= MvIdx<G>::bit(j);
+        const bool in = tbox ? in_box(tb[j], o.x, o.y) : fma(dx, dx, dy * dy) < g.rc2;
+        if (act[j] && in) m |= MvIdx<G>::bit(j);
       }
       if (m) {
         if (MODE == 1)

@@ -70,12 +70,7 @@ __device__ __forceinline__ void sub_runs(const Geom &g, const int *__restrict__ 
 // Box-overlap membership (reading Q24): cell (cx, cy)'s box grown by g.ovw, closed;
 // the edges are x0 + cx*c rounded twice (no contraction), exactly as in the oracle.
 __device__ __forceinline__ bool in_grown_box(const Geom &g, double2 p, int cx, int cy) {
-  const double lx = __dadd_rn(g.x0, __dmul_rn((double)cx, g.cell));
-  const double hx = __dadd_rn(g.x0, __dmul_rn((double)(cx + 1), g.cell));
-  const double ly = __dadd_rn(g.y0, __dmul_rn((double)cy, g.cell));
-  const double hy = __dadd_rn(g.y0, __dmul_rn((double)(cy + 1), g.cell));
-  return p.x >= __dsub_rn(lx, g.ovw) && p.x <= __dadd_rn(hx, g.ovw) && p.y >= __dsub_rn(ly, g.ovw) &&
-         p.y <= __dadd_rn(hy, g.ovw);
+  return in_box(cell_box(g, cx, cy, g.ovw), p.x, p.y);
 }
 
 // MODE 0: |Omega_c| per owned cell (sizes[ncl] = 0 for the scan);  MODE 1: the lists.

@@ -29,7 +29,7 @@ class Params(C.Structure):
     _fields_ = [("sigma", C.c_double), ("cell", C.c_double), ("rc", C.c_double),
                 ("overlap_rings", C.c_int32), ("reserved0", C.c_int32),
                 ("x0", C.c_double), ("y0", C.c_double), ("x1", C.c_double), ("y1", C.c_double),
-                ("overlap_width", C.c_double)]
+                ("overlap_width", C.c_double), ("trunc_width", C.c_double)]
 
 
 class Dist(C.Structure):
@@ -124,9 +124,10 @@ def _stream(stream):
     return C.c_void_p(s.cuda_stream)
 
 
-def make_params(sigma, cell, rc, rings=1, box=(-1.0, -1.0, 1.0, 1.0), overlap_width=0.0) -> Params:
+def make_params(sigma, cell, rc, rings=1, box=(-1.0, -1.0, 1.0, 1.0), overlap_width=0.0,
+                trunc_width=0.0) -> Params:
     return Params(float(sigma), float(cell), float(rc), int(rings), 0, *map(float, box),
-                  float(overlap_width))
+                  float(overlap_width), float(trunc_width))
 
 
 def launch_count() -> int:
@@ -194,14 +195,14 @@ class Context:
 
     def __init__(self, xy, sigma, cell, rc, rings=1, box=(-1.0, -1.0, 1.0, 1.0), *, rank=0,
                  nranks=1, comm="none", nccl_id: bytes | None = None, stream=None,
-                 overlap_width=0.0):
+                 overlap_width=0.0, trunc_width=0.0):
         import torch
 
         if not (isinstance(xy, torch.Tensor) and xy.is_cuda and xy.dtype == torch.float64):
             raise TypeError("xy must be a CUDA float64 tensor of shape (N, 2)")
         xy = xy.contiguous()
         self.n = int(xy.shape[0])
-        self.params = make_params(sigma, cell, rc, rings, box, overlap_width)
+        self.params = make_params(sigma, cell, rc, rings, box, overlap_width, trunc_width)
         dist = None
         if nranks > 1 or comm == "nccl":
             mode = {"nccl": RBF_COMM_NCCL, "threads": RBF_COMM_THREADS, "none": RBF_COMM_NONE}[comm]
@@ -346,12 +347,12 @@ class Context:
 
 def interpolate_host(xy: np.ndarray, f: np.ndarray, sigma, cell, rc, rings=1,
                      box=(-1.0, -1.0, 1.0, 1.0), restart=30, max_iters=1000, rtol=1e-13,
-                     atol=0.0, stream=None, overlap_width=0.0, orth="mgs"):
+                     atol=0.0, stream=None, overlap_width=0.0, orth="mgs", trunc_width=0.0):
     """rbf_interpolate_host: host buffers in caller order -> weights lambda (host)."""
     xy = np.ascontiguousarray(xy, dtype=np.float64)
     f = np.ascontiguousarray(f, dtype=np.float64)
     lam = np.empty_like(f)
-    prm = make_params(sigma, cell, rc, rings, box, overlap_width)
+    prm = make_params(sigma, cell, rc, rings, box, overlap_width, trunc_width)
     gp = GmresParams(int(restart), int(max_iters), float(rtol), float(atol), 0,
                      {"mgs": 0, "cgs2": 1}[orth])
     hist = np.zeros(max_iters, dtype=np.float64)

@@ -746,3 +746,83 @@ def test_matvec_variants_parity(env, monkeypatch):
     assert rel(y, ref) <= 1e-12
     if "RBF_MV_VAR" not in env:
         assert np.array_equal(y, y0)
+
+
+# ------------------------------------------------ T-box truncation (reading Q25, §8.f2)
+TBOX_CASES = [(SMALL[0], 3.0), (SMALL[1], 2.0), (SMALL[2], 3.0), (SMALL[4], 3.0),
+              (SMALL[2], 4.0), (SMALL[3], 8.0)]
+
+
+@pytest.mark.parametrize("wl,ts", TBOX_CASES,
+                         ids=["cfg1-3s", "ragged24-2s", "jitter40-3s", "clustered-3s",
+                              "jitter40-1cell", "jitter37-2cells"])
+def test_tbox_matvec_parity(wl, ts):
+    """The paper's matvec rule: sources inside the target cell's box grown by
+    tau; tau = 4 sigma and 8 sigma are exact multiples of the cell (box edges on cell
+    edges, halo floor(tau/c) + 1 rows)."""
+    tau = ts * wl.sigma
+    w = np.random.default_rng(41).standard_normal(wl.n)
+    ref = O.matvec_tbox(wl.xy, w, wl.sigma, wl.box, wl.cell, tau)
+    with ctx_for(wl, rings=0, trunc_width=tau) as c:
+        got = to_caller(c, c.matvec(c.to_local(torch.from_numpy(w).cuda())))
+        npairs = c.count_pairs()
+    assert rel(got, ref) <= 1e-12
+    # pair count = the T-box pattern (dense columns of the oracle on the small cases)
+    if wl.n <= 1600:
+        A = np.stack([O.matvec_tbox(wl.xy, np.eye(wl.n)[j], wl.sigma, wl.box, wl.cell, tau)
+                      for j in range(wl.n)], 1)
+        assert npairs == int(np.count_nonzero(A))
+
+
+def test_tbox_strips_bitwise_and_evaluate():
+    wl = W.make_lattice(60, jitter_frac=0.1, seed=5)
+    tau = 3.0 * wl.sigma
+    w = torch.from_numpy(np.random.default_rng(42).standard_normal(wl.n)).cuda()
+    xy = torch.from_numpy(wl.xy).cuda()
+    with ctx_for(wl, trunc_width=tau) as c1:
+        ws = c1.to_local(w)
+        y1 = c1.matvec(ws).cpu().numpy()
+        s = c1.evaluate(xy, ws).cpu().numpy()  # at the data points: the matvec rows
+        assert np.array_equal(s, to_caller(c1, c1.matvec(ws)))
+        rng = np.random.default_rng(43)
+        q = np.column_stack([rng.uniform(-1, 1, 500), rng.uniform(-1, 1, 500)])
+        sq = c1.evaluate(torch.from_numpy(q).cuda(), ws).cpu().numpy()
+    assert rel(sq, O.evaluate_tbox(q, wl.xy, w.cpu().numpy(), wl.sigma, wl.box, wl.cell, tau)) <= 1e-12
+    for nranks in (2, 3):
+        ys = []
+        for g in range(nranks):
+            with P.Context(xy, wl.sigma, wl.cell, wl.rc, 1, wl.box, rank=g, nranks=nranks,
+                           trunc_width=tau) as c:
+                ys.append(c.matvec_ext(ws[c.ext_lo:c.ext_hi].contiguous()).cpu().numpy())
+        assert np.array_equal(np.concatenate(ys), y1)
+
+
+@pytest.mark.parametrize("case", ["lattice0.8_tau3", "paper1.0_tau2", "paper0.9_scattered_B6"])
+def test_tbox_solve_parity(case):
+    """GMRES + RASM on A_T lambda = f (the paper's configuration) vs the oracle."""
+    if case == "lattice0.8_tau3":
+        wl, ts = W.make_lattice(64, jitter_frac=0.1, seed=2, s2=0.05), 3.0
+    elif case == "paper1.0_tau2":
+        wl, ts = W.make_paper_lattice(81, 1.0, b_over_sigma=5.0, d_over_b=1.9), 2.0
+    else:
+        wl, ts = W.make_paper_lattice(61, 0.9, scatter_seed=7, b_over_sigma=6.0, d_over_b=1.9), 3.0
+    tau = ts * wl.sigma
+    ref = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, wl.rings, rtol=1e-13,
+                  overlap_width=wl.overlap_width, trunc_width=tau)
+    with ctx_for(wl, trunc_width=tau) as c:
+        lam, rep = c.solve(c.to_local(torch.from_numpy(wl.f).cuda()), rtol=1e-13)
+        lam = to_caller(c, lam)
+    assert rep.converged and ref.converged
+    assert abs(rep.iterations - ref.iterations) <= 2
+    assert rep.resid_true <= 1e-10
+    assert rel(lam, ref.x) <= 1e-8
+    y = O.matvec_tbox(wl.xy, lam, wl.sigma, wl.box, wl.cell, tau)
+    assert rel(y, wl.f) <= 1e-10  # interpolation conditions of A_T at the data
+
+
+def test_tbox_invalid():
+    wl = SMALL[1]
+    with pytest.raises(P.RbfError):
+        ctx_for(wl, trunc_width=-1.0)
+    with pytest.raises(P.RbfError):
+        ctx_for(wl, trunc_width=9 * wl.cell)

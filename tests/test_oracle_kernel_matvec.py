@@ -290,3 +290,18 @@ def test_tbox_pattern_and_cells_form(kind):
         assert np.abs(y1 - y2).max() <= 1e-14 * np.abs(y1).max()
         rows = np.array([0, n // 3, n - 1])
         assert np.array_equal(O.matvec_tbox(wl.xy, w, wl.sigma, box, c, tau, rows=rows), y1[rows])
+
+
+def test_tbox_evaluate_at_data_points_is_matvec_row():
+    wl = W.make_lattice(20, jitter_frac=0.1, seed=9)
+    lam = np.random.default_rng(10).standard_normal(wl.n)
+    tau = 3 * wl.sigma
+    s = O.evaluate_tbox(wl.xy, wl.xy, lam, wl.sigma, wl.box, wl.cell, tau)
+    y = O.matvec_tbox(wl.xy, lam, wl.sigma, wl.box, wl.cell, tau)
+    assert np.array_equal(s, y)
+    # a query keeps the sources of ITS cell's box: two queries in one cell see one set
+    q = np.array([[wl.box[0] + 0.2 * wl.cell, wl.box[1] + 0.3 * wl.cell],
+                  [wl.box[0] + 0.9 * wl.cell, wl.box[1] + 0.8 * wl.cell]])
+    one = np.ones(wl.n)
+    big = O.evaluate_tbox(q, wl.xy, one, 1e6, wl.box, wl.cell, tau)  # phi ~ constant
+    assert big[0] == pytest.approx(big[1], rel=1e-9)
