@@ -63,6 +63,14 @@ enum {
  *                 fma(dx,dx,dy*dy) < rc*rc (reading Q1).
  *  overlap_rings  >= 0: Omega_c = the (2r+1)^2 block of cells around cell c,
  *                 clipped to the grid (reading Q9); 0 = block Jacobi.
+ *  schwarz        RBF_SCHWARZ_RASM (0, default): restricted additive Schwarz, Eq.(11)
+ *                 (P:221-225), each subdomain writes its own points only.
+ *                 RBF_SCHWARZ_ASM (1): additive Schwarz, Eq.(8), M^-1 =
+ *                 sum_c R_c^T A_c^-1 R_c: every subdomain adds its whole local solution
+ *                 (sums in ascending cell order, reading Q26).  Stores the full A_c^-1
+ *                 (|Omega_c|^2 doubles per cell, ~9x the RASM blocks) and solves every
+ *                 subdomain with the LU path; single-rank contexts only (EUNSUPPORTED
+ *                 otherwise).
  *  x0,y0,x1,y1    domain box; every point must satisfy x0 <= x <= x1, y0 <= y <= y1.
  *  overlap_width  >= 0.  0: Omega_c is the whole block (above).  > 0: the paper's box
  *                 overlap ("overlapping subdomains of size D"; reading Q24):
@@ -81,12 +89,13 @@ enum {
  *                 rbf_matvec, rbf_solve (A_T lambda = f), rbf_evaluate (the query's cell
  *                 box) and rbf_count_pairs; the preconditioner's local matrices stay the
  *                 principal submatrices of A_rc (rc still required). */
+enum { RBF_SCHWARZ_RASM = 0, RBF_SCHWARZ_ASM = 1 };
 typedef struct {
   double sigma;
   double cell;
   double rc;
   int32_t overlap_rings;
-  int32_t reserved0;
+  int32_t schwarz;
   double x0, y0, x1, y1;
   double overlap_width;
   double trunc_width;
@@ -194,7 +203,9 @@ int rbf_from_local(const rbf_ctx *ctx, const double *v_loc_dev, double *v_caller
  * with the T-box) then the cutoff matvec (y = A_T w with the T-box, reading Q25). */
 int rbf_matvec(rbf_ctx *ctx, const double *w_loc_dev, double *y_loc_dev, void *stream);
 /* z = M^-1 r (PCApply / MatSolve, Eq.(10)-(11)): halo exchange of r
- * (overlap_rings rows), then z[own(c)] = (A_c^-1 R_c r)[own(c)] for every cell. */
+ * (overlap_rings rows), then z[own(c)] = (A_c^-1 R_c r)[own(c)] for every cell
+ * (with RBF_SCHWARZ_ASM: t_c = A_c^-1 R_c r per cell, then z_i = sum of the t_c entries
+ * of point i over the subdomains containing it, ascending cell order, Eq.(8)). */
 int rbf_rasm_apply(rbf_ctx *ctx, const double *r_loc_dev, double *z_loc_dev, void *stream);
 /* Same two operators with the halo supplied by the caller: w_ext_dev holds
  * rbf_ext_count() entries = global sorted entries [ext_lo, ext_hi). */
@@ -240,7 +251,7 @@ int rbf_plan_strips(const int64_t *row_counts, int64_t ncy, int32_t nranks, int6
 
 /* Context facts: out[0] = doubles stored in the X blocks (RASM apply streams
  * 8*out[0] bytes per application), out[1] = subdomains, out[2] = largest
- * |Omega_c|, out[3] = largest |own(c)|, out[4] = subdomains solved by the
+ * |Omega_c|, out[3] = largest |own(c)| (rows of X per cell; |Omega_c| with ASM), out[4] = subdomains solved by the
  * global-memory LU path, out[5..6] = ncx, ncy, out[7] = device bytes held. */
 int rbf_info(const rbf_ctx *ctx, int64_t out[8]);
 

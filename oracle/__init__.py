@@ -403,17 +403,18 @@ def gmres(opA, opM, b, restart=30, max_iters=1000, rtol=1e-13, atol=0.0,
 
 def solve(xy, f, sigma, rc, box, cell, rings=1, restart=30, max_iters=1000, rtol=1e-13,
           atol=0.0, brute=False, orth="mgs", overlap_width=0.0,
-          trunc_width=0.0) -> GmresResult:
+          trunc_width=0.0, schwarz="rasm") -> GmresResult:
     """Solve A_rc lambda = f by GMRES(restart) left-preconditioned with RASM
     (the paper's KSPSolve).  trunc_width > 0 solves with the
-    paper's T-box matvec instead (reading Q25; the local matrices stay A_rc's)."""
+    paper's T-box matvec instead (reading Q25; the local matrices stay A_rc's);
+    schwarz="asm" preconditions with Eq.(8) instead of Eq.(11) (reading Q26)."""
     P = Rasm(xy, sigma, rc, box, cell, rings, overlap_width)
     if P.status != ORC_OK:
         raise ArithmeticError(f"RASM setup failed in cell {P.bad_cell}")
     try:
         opA = (op_rbf_tbox(xy, sigma, box, cell, trunc_width) if trunc_width > 0
                else op_rbf(xy, sigma, rc, box, cell, brute))
-        return gmres(opA, op_rasm(P), f, restart,
+        return gmres(opA, op_rasm(P, schwarz), f, restart,
                      max_iters, rtol, atol, orth=orth)
     finally:
         P.close()

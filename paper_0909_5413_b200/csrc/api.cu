@@ -144,6 +144,10 @@ static int validate(const rbf_params *p, long long n) {
     set_error("overlap_width must be >= 0 (finite)");
     return RBF_EINVAL;
   }
+  if (p->schwarz != RBF_SCHWARZ_RASM && p->schwarz != RBF_SCHWARZ_ASM) {
+    set_error("schwarz must be RBF_SCHWARZ_RASM (0) or RBF_SCHWARZ_ASM (1)");
+    return RBF_EINVAL;
+  }
   if (!(p->trunc_width >= 0.0) || !(p->trunc_width <= 8.0 * p->cell)) {
     set_error("trunc_width must be in [0, 8 cell] (finite)");
     return RBF_EINVAL;
@@ -248,6 +252,10 @@ void rbf_destroy(rbf_ctx *c) {
   dfree(c->chunk_off, s);
   dfree(c->nlist, s);
   dfree(c->X, s);
+  dfree(c->asm_toff, s);
+  dfree(c->asm_t, s);
+  dfree(c->asm_map, s);
+  dfree(c->asm_poff, s);
   dfree(c->w_ext, s);
   dfree(c->V, s);
   dfree(c->t1, s);
@@ -311,6 +319,12 @@ int rbf_setup(rbf_ctx **out, const double *xy, int64_t n, const rbf_params *p, c
   if (g.ncy < 1) g.ncy = 1;
   g.kh = (int)std::ceil(p->rc / p->cell * (1.0 + 1e-12));
   g.tw = p->trunc_width;
+  g.asm_full = p->schwarz == RBF_SCHWARZ_ASM;
+  if (g.asm_full && c->nranks > 1) {
+    set_error("rbf_setup: RBF_SCHWARZ_ASM is single-rank only (the Eq.(8) sums cross strips)");
+    rbf_destroy(c);
+    return RBF_EUNSUPPORTED;
+  }
   // T-box (reading Q25): the box reaches floor(tw/c) + 1 cells beyond the target's cell
   if (g.tw > 0.0) g.kh = (int)std::floor(g.tw / p->cell * (1.0 + 1e-12)) + 1;
   g.rings = p->overlap_rings;

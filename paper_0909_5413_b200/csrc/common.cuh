@@ -55,6 +55,7 @@ struct Geom {
   int rings;           // RASM overlap rings
   double ovw;          // box overlap width delta (reading Q24); 0 = whole rings
   double tw;           // T-box truncation width tau (reading Q25); 0 = radial cutoff rc
+  int asm_full;        // 1: additive Schwarz, Eq.(8) (full A_c^-1 per cell, reading Q26)
 };
 
 // Cell (cx, cy)'s box grown by w on every side, closed (readings Q24, Q25); the
@@ -214,6 +215,11 @@ struct rbf_ctx {
   long long *ov_off = nullptr;
   int *ov_own = nullptr;
   double *X = nullptr;         // rows of A_c^-1 for own(c), row-major, ld = n_ov rounded up to even
+                               // (ASM: all n_ov rows of A_c^-1)
+  long long *asm_toff = nullptr;  // ASM: offset of cell cl's local solution t_c (sum of n_ov)
+  double *asm_t = nullptr;        // ASM: the local solutions t_c = A_c^-1 R_c u
+  int *asm_map = nullptr;         // ASM: per point, the t entries that sum to z_i (cell order)
+  long long *asm_poff = nullptr;  // ASM: CSR offsets of asm_map (n_loc + 1)
   long long x_count = 0;
   int max_ov = 0, max_own = 0, nsub = 0, n_lu = 0;
   int max_cell = 0;            // largest cell population (all cells of the ext range)

@@ -185,25 +185,32 @@ __device__ __forceinline__ int nat_to_fac(const Runs &R, const TileShape &S, int
 
 // Per owned cell: X block size, maxima, and the list of cells that the tensor-core
 // kernel cannot take (they go to the global-memory LU kernel).
+// ASM (reading Q26): X holds all n_ov rows, every cell takes the LU path, and tsizes
+// (non-null) receives n_ov per cell for the local-solution buffer.
 __global__ void k_rasm_sizes(Geom g, Strip st, const int *__restrict__ cell_start, int ncl,
                              long long *__restrict__ sizes, int *__restrict__ maxes,
-                             int *__restrict__ glist, OvList ov) {
+                             int *__restrict__ glist, OvList ov, long long *__restrict__ tsizes) {
   int cl = blockIdx.x * blockDim.x + threadIdx.x;
   if (cl >= ncl) {
-    if (cl == ncl) sizes[cl] = 0;
+    if (cl == ncl) {
+      sizes[cl] = 0;
+      if (tsizes) tsizes[cl] = 0;
+    }
     return;
   }
   int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
   Runs R;
   sub_runs(g, cell_start, ov, cl, cx, cy, R);
   long long ld = (R.n_ov + 1) & ~1;
-  sizes[cl] = R.n_own ? (long long)R.n_own * ld : 0;
+  const int rows = g.asm_full ? R.n_ov : R.n_own;
+  sizes[cl] = R.n_own ? (long long)rows * ld : 0;
+  if (tsizes) tsizes[cl] = R.n_own ? R.n_ov : 0;
   if (R.n_own) {
     atomicMax(&maxes[0], R.n_ov);
-    atomicMax(&maxes[1], R.n_own);
+    atomicMax(&maxes[1], rows);
     atomicAdd(&maxes[2], 1);
     TileShape S(R.n_ov, R.n_own);
-    if (!S.fits_tc()) glist[atomicAdd(&maxes[3], 1)] = cl;
+    if (g.asm_full || !S.fits_tc()) glist[atomicAdd(&maxes[3], 1)] = cl;
     else atomicMax(&maxes[4], S.T);
   }
 }
@@ -687,8 +694,10 @@ __global__ __launch_bounds__(kLuThreads, 1) void k_rasm_setup_lu(
   if (tid == 0) sub_runs(g, cell_start, ov, cl, cx, cy, R);
   __syncthreads();
   const int n = R.n_ov, n_own = R.n_own, n0 = n - n_own, own_nat = R.own_nat_lo;
-  const long long lda = n + n_own;
-  double *A = ws + (long long)blockIdx.x * ws_stride;  // n x lda row-major: [A_c | E_own]
+  // right-hand sides: E_own (RASM), or the identity in natural order (ASM, reading Q26)
+  const int nrhs = g.asm_full ? n : n_own;
+  const long long lda = n + nrhs;
+  double *A = ws + (long long)blockIdx.x * ws_stride;  // n x lda row-major: [A_c | E]
   double *PT = A + (long long)n * lda;                 // kLuNb x n: transposed panel
   double2 *pos = reinterpret_cast<double2 *>(A + (((long long)n * lda + (long long)kLuNb * n + 1) & ~1LL));
   for (int p = tid; p < n; p += T) {
@@ -703,8 +712,10 @@ __global__ __launch_bounds__(kLuThreads, 1) void k_rasm_setup_lu(
       const double dx = pos[i].x - pos[j].x, dy = pos[i].y - pos[j].y;
       const double r2 = fma(dx, dx, dy * dy);
       v = (r2 < g.rc2) ? exp(r2 * g.neg_inv_2s2) * g.norm : 0.0;
-    } else {
-      v = (i == n0 + (j - n)) ? 1.0 : 0.0;  // E_own in factor order
+    } else {  // column j - n = e_{natural index}, in factor order (own points last)
+      const int q = g.asm_full ? (int)(j - n) : own_nat + (int)(j - n);
+      const int fq = q < own_nat ? q : (q < own_nat + n_own ? n0 + (q - own_nat) : q - n_own);
+      v = (i == fq) ? 1.0 : 0.0;
     }
     A[t] = v;
   }
@@ -817,9 +828,12 @@ __global__ __launch_bounds__(kLuThreads, 1) void k_rasm_setup_lu(
     return;
   }
   __syncthreads();
-  // ---- back substitution U Z = Y on the n_own right-hand-side columns (A[:, n:]),
-  //      blocks of kLuNb rows from the bottom; threads = (column, row group)
-  const int ngrp = T / (n_own > 0 ? n_own : 1) > 0 ? T / n_own : 1;
+  // ---- back substitution U Z = Y on the nrhs right-hand-side columns (A[:, n:]),
+  //      blocks of kLuNb rows from the bottom; threads = (column, row group); column
+  //      chunks of at most T columns (ASM has n of them)
+  for (int cb = 0; cb < nrhs; cb += T) {
+  const int nc = nrhs - cb < T ? nrhs - cb : T;
+  const int ngrp = T / nc;
   for (int r0 = ((n - 1) / kLuNb) * kLuNb; r0 >= 0; r0 -= kLuNb) {
     const int kb = n - r0 < kLuNb ? n - r0 : kLuNb;
     __syncthreads();
@@ -828,8 +842,8 @@ __global__ __launch_bounds__(kLuThreads, 1) void k_rasm_setup_lu(
       L11[r][c] = (c >= r) ? A[(long long)(r0 + r) * lda + r0 + c] : 0.0;
     }
     __syncthreads();
-    if (tid < n_own) {  // solve the diagonal block for this column
-      const long long j = n + tid;
+    if (tid < nc) {  // solve the diagonal block for this column
+      const long long j = n + cb + tid;
       double z[kLuNb];
 #pragma unroll
       for (int t = 0; t < kLuNb; ++t) z[t] = t < kb ? A[(long long)(r0 + t) * lda + j] : 0.0;
@@ -848,11 +862,12 @@ __global__ __launch_bounds__(kLuThreads, 1) void k_rasm_setup_lu(
     }
     __syncthreads();
     // rows above: Y[i] -= U[i, r0:r0+kb] z, columns x row groups
-    const int jc = tid % (n_own > 0 ? n_own : 1), grp = tid / (n_own > 0 ? n_own : 1);
-    const bool act = n_own > 0 && grp < ngrp;
+    const int jc = tid % nc, grp = tid / nc;
+    const bool act = grp < ngrp;
+    const long long jcol = n + cb + jc;
     double z[kLuNb];
 #pragma unroll
-    for (int t = 0; t < kLuNb; ++t) z[t] = (act && t < kb) ? A[(long long)(r0 + t) * lda + n + jc] : 0.0;
+    for (int t = 0; t < kLuNb; ++t) z[t] = (act && t < kb) ? A[(long long)(r0 + t) * lda + jcol] : 0.0;
     for (int i0 = 0; i0 < r0; i0 += kLuRows) {
       const int nr = r0 - i0 < kLuRows ? r0 - i0 : kLuRows;
       __syncthreads();
@@ -863,18 +878,19 @@ __global__ __launch_bounds__(kLuThreads, 1) void k_rasm_setup_lu(
       __syncthreads();
       if (act) {
         for (int r = grp; r < nr; r += ngrp) {
-          double a = A[(long long)(i0 + r) * lda + n + jc];
+          double a = A[(long long)(i0 + r) * lda + jcol];
 #pragma unroll
           for (int t = 0; t < kLuNb; ++t) a = fma(-Ls[r][t], z[t], a);
-          A[(long long)(i0 + r) * lda + n + jc] = a;
+          A[(long long)(i0 + r) * lda + jcol] = a;
         }
       }
     }
   }
+  }
   __syncthreads();
   const long long ld = (n + 1) & ~1;
   double *Xc = X + x_off[cl];
-  for (long long t = tid; t < (long long)n_own * ld; t += T) {
+  for (long long t = tid; t < (long long)nrhs * ld; t += T) {  // row o: RHS column o
     const int o = (int)(t / ld), q = (int)(t - (long long)o * ld);
     double v = 0.0;
     if (q < n) {
@@ -945,6 +961,115 @@ __global__ __launch_bounds__(kRaThreads) void k_rasm_apply(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Additive Schwarz, Eq.(8) (reading Q26): z = sum_c R_c^T A_c^-1 R_c u.
+// (1) k_asm_local: t_c = A_c^-1 u[Omega_c] for every cell (all n_ov rows of the stored
+//     inverse, the RASM GEMV with every row kept), into t at asm_toff[cl];
+// (2) k_asm_gather: z_i = sum of the t entries of point i, in ascending cell order
+//     (a CSR map built once at setup by a stable sort of (point, t index) pairs), so
+//     the sums are deterministic and need no atomics.
+// ---------------------------------------------------------------------------
+__global__ __launch_bounds__(kRaThreads) void k_asm_local(
+    Geom g, Strip st, const int *__restrict__ cell_start, const long long *__restrict__ x_off,
+    const long long *__restrict__ t_off, const double *__restrict__ X, const double *__restrict__ u,
+    double *__restrict__ t, OvList ov) {
+  extern __shared__ double su[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cl = blockIdx.x;
+  const int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
+  Runs R;
+  sub_runs(g, cell_start, ov, cl, cx, cy, R);
+  if (R.n_own == 0) return;
+  const int n = R.n_ov, ld = (n + 1) & ~1, h = ld >> 1;
+  for (int q = tid; q < ld; q += kRaThreads) su[q] = (q < n) ? u[nat_to_global(R, q) - st.ext_lo] : 0.0;
+  __syncthreads();
+  const double2 *u2 = reinterpret_cast<const double2 *>(su);
+  const double2 *Xc = reinterpret_cast<const double2 *>(X + x_off[cl]);
+  double *tc = t + t_off[cl];
+  for (int o = warp; o < n; o += kRaThreads / 32) {
+    const double2 *row = Xc + (long long)o * h;
+    double acc = 0.0, acc2 = 0.0;
+    for (int j = lane; j < h; j += 32) {
+      const double2 xv = __ldcs(row + j), uv = u2[j];
+      acc = fma(xv.x, uv.x, acc);
+      acc2 = fma(xv.y, uv.y, acc2);
+    }
+    acc += acc2;
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, sh);
+    if (lane == 0) tc[o] = acc;
+  }
+}
+
+// (point, t index) pairs in (cell, position) order, for the stable sort by point
+__global__ void k_asm_entries(Geom g, Strip st, const int *__restrict__ cell_start,
+                              const long long *__restrict__ t_off, int *__restrict__ key,
+                              int *__restrict__ val, OvList ov) {
+  const int cl = blockIdx.x;
+  const int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
+  Runs R;
+  sub_runs(g, cell_start, ov, cl, cx, cy, R);
+  if (R.n_own == 0) return;
+  const long long o = t_off[cl];
+  for (int q = threadIdx.x; q < R.n_ov; q += blockDim.x) {
+    key[o + q] = nat_to_global(R, q) - (int)st.own_lo;
+    val[o + q] = (int)(o + q);
+  }
+}
+
+// CSR offsets from the sorted keys: every point has >= 1 entry (its own cell)
+__global__ void k_asm_offsets(const int *__restrict__ skey, long long total, long long npts,
+                              long long *__restrict__ poff) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k < total && (k == 0 || skey[k] != skey[k - 1])) poff[skey[k]] = k;
+  if (k == 0) poff[npts] = total;
+}
+
+__global__ void k_asm_gather(const long long *__restrict__ poff, const int *__restrict__ map,
+                             const double *__restrict__ t, long long npts, double *__restrict__ z) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= npts) return;
+  double acc = 0.0;
+  for (long long k = poff[i]; k < poff[i + 1]; ++k) acc += t[map[k]];
+  z[i] = acc;
+}
+
+static OvList ov_of(const rbf_ctx *c) { return OvList{c->ov_idx, c->ov_off, c->ov_own}; }
+
+static int build_asm_map(rbf_ctx *c, int ncl, long long total, cudaStream_t s) {
+  const long long np = n_loc(c);
+  if (total >= (1LL << 31)) {
+    set_error("rbf_setup: ASM needs %lld local-solution entries (limit 2^31)", total);
+    return RBF_EUNSUPPORTED;
+  }
+  int *key = nullptr, *val = nullptr, *skey = nullptr;
+  RBF_TRY(dalloc(c, (void **)&key, sizeof(int) * (size_t)total, s));
+  RBF_TRY(dalloc(c, (void **)&val, sizeof(int) * (size_t)total, s));
+  RBF_TRY(dalloc(c, (void **)&skey, sizeof(int) * (size_t)total, s));
+  RBF_TRY(dalloc(c, (void **)&c->asm_map, sizeof(int) * (size_t)total, s));
+  RBF_TRY(dalloc(c, (void **)&c->asm_poff, sizeof(long long) * (size_t)(np + 1), s));
+  RBF_TRY(dalloc(c, (void **)&c->asm_t, sizeof(double) * (size_t)total, s));
+  k_asm_entries<<<ncl, 128, 0, s>>>(c->g, c->s, c->cell_start, c->asm_toff, key, val, ov_of(c));
+  RBF_CUDA_TRY(cudaGetLastError());
+  int end_bit = 1;
+  while ((1LL << end_bit) < np) ++end_bit;
+  size_t tb = 0;
+  RBF_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, key, skey, val, c->asm_map, (int)total, 0,
+                                               end_bit, s));
+  void *tmp = nullptr;
+  RBF_TRY(dalloc(c, &tmp, tb, s));
+  RBF_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tb, key, skey, val, c->asm_map, (int)total, 0,
+                                               end_bit, s));  // stable: cell order kept per point
+  k_asm_offsets<<<(int)((total + 255) / 256), 256, 0, s>>>(skey, total, np, c->asm_poff);
+  count_launch(3 + (end_bit + 7) / 8);
+  RBF_CUDA_TRY(cudaGetLastError());
+  dfree(tmp, s);
+  dfree(key, s);
+  dfree(val, s);
+  dfree(skey, s);
+  return RBF_OK;
+}
+
 int probe_read(long long *out) {
 #ifdef RBF_PROBE
   RBF_CUDA_TRY(cudaMemcpyFromSymbol(out, g_probe, sizeof(long long) * 64 * 8));
@@ -957,7 +1082,6 @@ int probe_read(long long *out) {
 #endif
 }
 
-static OvList ov_of(const rbf_ctx *c) { return OvList{c->ov_idx, c->ov_off, c->ov_own}; }
 
 // Box-overlap index lists (reading Q24): count, scan, fill.
 static int build_ov_lists(rbf_ctx *c, int ncl, cudaStream_t s) {
@@ -1002,8 +1126,13 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
   RBF_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * 8, s));
   if (c->g.ovw > 0.0) RBF_TRY(build_ov_lists(c, ncl, s));
   const OvList ov = ov_of(c);
+  long long *tsizes = nullptr;
+  if (c->g.asm_full) {
+    RBF_TRY(dalloc(c, (void **)&tsizes, sizeof(long long) * (ncl + 1), s));
+    RBF_TRY(dalloc(c, (void **)&c->asm_toff, sizeof(long long) * (ncl + 1), s));
+  }
   k_rasm_sizes<<<(ncl + 1 + 255) / 256, 256, 0, s>>>(c->g, c->s, c->cell_start, ncl, sizes, cnt,
-                                                     glist, ov);
+                                                     glist, ov, tsizes);
   count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
   size_t tmp_bytes = 0;
@@ -1012,6 +1141,12 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
   RBF_TRY(dalloc(c, &tmp, tmp_bytes, s));
   RBF_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, sizes, c->x_off, ncl + 1, s));
   count_launch(2);  // init + scan
+  long long asm_total = 0;
+  if (c->g.asm_full) {
+    RBF_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, tsizes, c->asm_toff, ncl + 1, s));
+    count_launch(2);
+    RBF_CUDA_TRY(cudaMemcpyAsync(&asm_total, c->asm_toff + ncl, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  }
   int hc[8];
   long long total = 0;
   RBF_CUDA_TRY(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
@@ -1019,6 +1154,8 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
   RBF_CUDA_TRY(cudaStreamSynchronize(s));
   dfree(tmp, s);
   dfree(sizes, s);
+  dfree(tsizes, s);
+  if (c->g.asm_full && ncl > 0) RBF_TRY(build_asm_map(c, ncl, asm_total, s));
   c->max_ov = hc[0];
   c->max_own = hc[1];
   c->nsub = hc[2];
@@ -1038,7 +1175,8 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
     RBF_CUDA_TRY(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
     RBF_CUDA_TRY(cudaStreamSynchronize(s));
   }
-  const int nglobal = hc[3];  // big cells + Cholesky breakdowns
+  const int nglobal = hc[3];  // big cells + Cholesky breakdowns (ASM: every cell)
+  if (ncl > 0 && c->nsub == nglobal) RBF_TRY(prebuild_solve(c, s));  // no tensor-core pass
   int hfail = 0x7fffffff;
   if (nglobal > 0) {
     int *fail = cnt + 4;
@@ -1077,6 +1215,21 @@ int launch_rasm_apply(const rbf_ctx *c, const double *r_ext, double *z_loc, cuda
   const int ncl = owned_cells(c);
   if (ncl <= 0 || c->nsub == 0) return RBF_OK;
   const size_t smem = sizeof(double) * (size_t)(c->max_ov + 2);
+  if (c->g.asm_full) {  // Eq.(8): local solutions, then the per-point sums
+    static size_t attr_a = 48 * 1024;
+    if (smem > attr_a) {
+      RBF_CUDA_TRY(cudaFuncSetAttribute(k_asm_local, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+      attr_a = smem;
+    }
+    k_asm_local<<<ncl, kRaThreads, smem, s>>>(c->g, c->s, c->cell_start, c->x_off, c->asm_toff, c->X,
+                                              r_ext, c->asm_t, ov_of(c));
+    const long long np = n_loc(c);
+    k_asm_gather<<<(int)((np + 255) / 256), 256, 0, s>>>(c->asm_poff, c->asm_map, c->asm_t, np, z_loc);
+    count_launch(2);
+    RBF_CUDA_TRY(cudaGetLastError());
+    return RBF_OK;
+  }
   static size_t attr_d = 48 * 1024;
   if (smem > attr_d) {
     RBF_CUDA_TRY(cudaFuncSetAttribute(k_rasm_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,

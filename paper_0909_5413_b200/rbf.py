@@ -27,7 +27,7 @@ class RbfError(RuntimeError):
 
 class Params(C.Structure):
     _fields_ = [("sigma", C.c_double), ("cell", C.c_double), ("rc", C.c_double),
-                ("overlap_rings", C.c_int32), ("reserved0", C.c_int32),
+                ("overlap_rings", C.c_int32), ("schwarz", C.c_int32),
                 ("x0", C.c_double), ("y0", C.c_double), ("x1", C.c_double), ("y1", C.c_double),
                 ("overlap_width", C.c_double), ("trunc_width", C.c_double)]
 
@@ -124,10 +124,13 @@ def _stream(stream):
     return C.c_void_p(s.cuda_stream)
 
 
+SCHWARZ = {"rasm": 0, "asm": 1}
+
+
 def make_params(sigma, cell, rc, rings=1, box=(-1.0, -1.0, 1.0, 1.0), overlap_width=0.0,
-                trunc_width=0.0) -> Params:
-    return Params(float(sigma), float(cell), float(rc), int(rings), 0, *map(float, box),
-                  float(overlap_width), float(trunc_width))
+                trunc_width=0.0, schwarz="rasm") -> Params:
+    return Params(float(sigma), float(cell), float(rc), int(rings), SCHWARZ[schwarz],
+                  *map(float, box), float(overlap_width), float(trunc_width))
 
 
 def launch_count() -> int:
@@ -195,14 +198,14 @@ class Context:
 
     def __init__(self, xy, sigma, cell, rc, rings=1, box=(-1.0, -1.0, 1.0, 1.0), *, rank=0,
                  nranks=1, comm="none", nccl_id: bytes | None = None, stream=None,
-                 overlap_width=0.0, trunc_width=0.0):
+                 overlap_width=0.0, trunc_width=0.0, schwarz="rasm"):
         import torch
 
         if not (isinstance(xy, torch.Tensor) and xy.is_cuda and xy.dtype == torch.float64):
             raise TypeError("xy must be a CUDA float64 tensor of shape (N, 2)")
         xy = xy.contiguous()
         self.n = int(xy.shape[0])
-        self.params = make_params(sigma, cell, rc, rings, box, overlap_width, trunc_width)
+        self.params = make_params(sigma, cell, rc, rings, box, overlap_width, trunc_width, schwarz)
         dist = None
         if nranks > 1 or comm == "nccl":
             mode = {"nccl": RBF_COMM_NCCL, "threads": RBF_COMM_THREADS, "none": RBF_COMM_NONE}[comm]

@@ -826,3 +826,47 @@ def test_tbox_invalid():
         ctx_for(wl, trunc_width=-1.0)
     with pytest.raises(P.RbfError):
         ctx_for(wl, trunc_width=9 * wl.cell)
+
+
+# ------------------------------------------------ additive Schwarz, Eq.(8) (reading Q26)
+@pytest.mark.parametrize("wl,rings,ow", [(SMALL[0], 1, 0.0), (SMALL[1], 1, 0.0), (SMALL[2], 1, 0.0),
+                                         (SMALL[3], 2, 0.0), (SMALL[2], 1, 0.45),
+                                         (W.make_lattice(30, jitter_frac=0.1, seed=2), 0, 0.0)],
+                         ids=["cfg1", "ragged24", "jitter40", "jitter37-2rings", "jitter40-box",
+                              "rings0"])
+def test_asm_apply_parity(wl, rings, ow):
+    # (the clustered set is left out as for RASM: its local matrices are singular in fp64, Q8)
+    d = ow * wl.cell
+    r = np.random.default_rng(51).standard_normal(wl.n)
+    Pc = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, rings, overlap_width=d)
+    ref = Pc.apply(r, "asm")
+    ref_r = Pc.apply(r, "rasm")
+    Pc.close()
+    with ctx_for(wl, rings=rings, overlap_width=d, schwarz="asm") as c:
+        z = to_caller(c, c.rasm_apply(c.to_local(torch.from_numpy(r).cuda())))
+    assert rel(z, ref) <= 1e-10
+    if rings == 0:  # block Jacobi: ASM = RASM
+        assert rel(z, ref_r) <= 1e-10
+    else:
+        assert rel(z, ref_r) > 1e-3
+
+
+@pytest.mark.parametrize("wl", [SMALL[0], W.make_paper_lattice(61, 0.9, b_over_sigma=5.0, d_over_b=1.9)],
+                         ids=["cfg1", "paper0.9-B5"])
+def test_asm_solve_parity(wl):
+    ref = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, wl.rings, rtol=1e-13,
+                  overlap_width=wl.overlap_width, schwarz="asm")
+    with ctx_for(wl, schwarz="asm") as c:
+        lam, rep = c.solve(c.to_local(torch.from_numpy(wl.f).cuda()), rtol=1e-13)
+        lam = to_caller(c, lam)
+    assert rep.converged and ref.converged
+    assert abs(rep.iterations - ref.iterations) <= 2
+    assert rep.resid_true <= 1e-10
+    assert rel(lam, ref.x) <= 1e-8
+
+
+def test_asm_multirank_unsupported():
+    wl = W.make_lattice(60, jitter_frac=0.1, seed=5)
+    xy = torch.from_numpy(wl.xy).cuda()
+    with pytest.raises(P.RbfError):
+        P.Context(xy, wl.sigma, wl.cell, wl.rc, 1, wl.box, rank=0, nranks=2, schwarz="asm")

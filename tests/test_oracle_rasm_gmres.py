@@ -404,3 +404,11 @@ def test_tbox_too_small_at_h_sigma_08_stalls():
     r = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, rtol=1e-13, max_iters=200,
                 trunc_width=tau)
     assert not r.converged
+
+
+def test_solve_asm_same_weights_as_rasm(cfg1_solution):
+    # Eq.(8) ASM and Eq.(11) RASM precondition the same system A_rc lambda = f (reading Q26)
+    wl, res, lam = cfg1_solution
+    r = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, rtol=wl.tol, schwarz="asm")
+    assert r.converged and r.resid_true < 1e-10
+    assert np.linalg.norm(r.x - lam) / np.linalg.norm(lam) < 1e-8
