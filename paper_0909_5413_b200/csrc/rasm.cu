@@ -238,6 +238,10 @@ __device__ __forceinline__ int smid() {
   asm volatile("mov.u32 %0, %smid;" : "=r"(r));
   return r;
 }
+__device__ long long g_col[2][64][4];  // per tile column of one interior CTA (see PCOL)
+constexpr int kColCta = 20660;
+#define PCOL(a, j, k) \
+  if ((threadIdx.x & 31) == 0 && blockIdx.x == kColCta && (j) < 64) g_col[a][j][k] = clock64();
 #define TRACE(i) \
   if (threadIdx.x == 0 && blockIdx.x < 65536) { g_trace[blockIdx.x][0] = smid(); g_trace[blockIdx.x][i] = gtimer(); }
 #define PROBE(i) /* 64 sampled CTAs spread over the grid (mostly interior cells) */ \
@@ -245,6 +249,7 @@ __device__ __forceinline__ int smid() {
 #else
 #define PROBE(i)
 #define TRACE(i)
+#define PCOL(a, j, k)
 #endif
 
 struct AccSet {
@@ -404,6 +409,8 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
   }
   for (int j = 0; j < T; ++j) {
     const int dw = kAccWarps + (j & 1);  // diagonal warp of column j
+    if (warp == 0) PCOL(0, j, 0)
+    if (warp == dw) PCOL(1, j, 0)
     if (warp < kAccWarps) {
       // step 1: finish column j (tiles it > j) with the kt = j-1 term
 #pragma unroll
@@ -429,14 +436,18 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
       if (j >= 1) acc_range(acc[0], sm, j, j, j - 1, j, lane);
       acc_finish(acc[0], sm, j, j, lane);
       __syncwarp();
+      PCOL(1, j, 1)
       if (diag_factor(sm, rdiag, j, lane) && lane == 0) s_fail = 1;
+      PCOL(1, j, 2)
     } else if (j + 1 < T) {
       // the other diagonal warp accumulates the next diagonal tile over kt < j
       acc[0].zero();
       a_entries(pos, S, g, j + 1, j + 1, lane, acc[0].v0, acc[0].v1);
       acc_range(acc[0], sm, j + 1, j + 1, 0, j, lane);
     }
+    if (warp == 0) PCOL(0, j, 1)
     __syncthreads();
+    if (warp == 0) PCOL(0, j, 2)
     if (s_fail) break;  // uniform
     // step 4: panel L(it, j) = C(it, j) L_d^-T  (B[k][n] = Linv[n][k])
     if (warp < kAccWarps) {
@@ -459,6 +470,7 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
       }
     }
     __syncthreads();
+    if (warp == 0) PCOL(0, j, 3)
   }
   if (s_fail) {  // Cholesky broke down: redo this cell with LU (reading Q11)
     if (tid == 0) glist[atomicAdd(&counts[3], 1)] = cl;
@@ -1074,6 +1086,7 @@ int probe_read(long long *out) {
 #ifdef RBF_PROBE
   RBF_CUDA_TRY(cudaMemcpyFromSymbol(out, g_probe, sizeof(long long) * 64 * 8));
   RBF_CUDA_TRY(cudaMemcpyFromSymbol(out + 64 * 8, g_trace, sizeof(long long) * 65536 * 3));
+  RBF_CUDA_TRY(cudaMemcpyFromSymbol(out + 64 * 8 + 65536 * 3, g_col, sizeof(long long) * 512));
   return RBF_OK;
 #else
   (void)out;

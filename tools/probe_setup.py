@@ -42,10 +42,12 @@ for i, nm in enumerate(names):
     print(f"{nm:10s} mean {d[:, i].mean():10.0f} cyc  min {d[:, i].min():8d} max {d[:, i].max():8d}")
 print("total", (out[:, 4] - out[:, 0]).mean())
 col = buf[512 + 65536 * 3:].reshape(2, 64, 4)
-c0 = col[0]
+c0, cd = col[0], col[1]
 base = c0[0, 0]
-print("per column (cycles since start of Cholesky), thread 0: [start, (i)+(ii) done, before sync, after sync]; diag warp 14: [start, factor start, factor done]")
+print("per tile column j of one interior CTA (cycles): warp 0 [step1+2 time, wait at sync 1, panel+sync 2]; "
+      "diagonal warp [finish time, 8x8 factor time]; column total")
 for j in range(30):
-    if c0[j, 0] == 0: break
-    w = col[1][j]
-    print(j, c0[j, 0] - base, c0[j, 3] - base, c0[j, 1] - base, c0[j, 2] - base, "| w14", *(w[[0, 1, 3]] - base if w[3] else []))
+    if c0[j, 0] == 0:
+        break
+    print(f"{j:2d} w0: {c0[j, 1] - c0[j, 0]:6d} {c0[j, 2] - c0[j, 1]:6d} {c0[j, 3] - c0[j, 2]:6d} | "
+          f"dw: {cd[j, 1] - cd[j, 0]:6d} {cd[j, 2] - cd[j, 1]:6d} | col {c0[j, 3] - c0[j, 0]:6d}")
