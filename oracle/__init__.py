@@ -389,7 +389,7 @@ def gmres(opA, opM, b, restart=30, max_iters=1000, rtol=1e-13, atol=0.0,
     V = np.empty((restart + 1, n), dtype=np.float64) if keep_basis else None
     nv = C.c_int64(0)
     st = lib().orc_gmres_orth(_addr(opA[0]), _addr(opM[0]), _p(b), int(restart), int(max_iters),
-                         float(rtol), float(atol), {"mgs": 0, "cgs2": 1}[orth], _p(x), _p(hist),
+                         float(rtol), float(atol), {"mgs": 0, "cgs2": 1, "dcgs2": 2}[orth], _p(x), _p(hist),
                          int(max_iters), C.byref(rep),
                          _p(V) if V is not None else None, C.byref(nv))
     if st == ORC_EINVAL:

@@ -745,13 +745,20 @@ typedef struct {
  * history[k] = |g_{k+1}| / beta0 after iteration k (up to hist_cap entries).
  * V_out (optional, (m+1) x n) receives the Krylov basis of the last cycle and
  * *v_count the number of basis vectors in it (for the orthogonality pin). */
+static int gmres_dcgs2(const orc_op *A, const orc_op *M, const double *b, int64_t restart,
+                       int64_t max_iters, double rtol, double atol, double *x, double *history,
+                       int64_t hist_cap, orc_report *rep, double *V_out, int64_t *v_count);
+
 int orc_gmres_orth(const orc_op *A, const orc_op *M, const double *b, int64_t restart,
                    int64_t max_iters, double rtol, double atol, int orth, double *x,
                    double *history, int64_t hist_cap, orc_report *rep, double *V_out,
                    int64_t *v_count) {
   int64_t n = A->n, m = restart;
   memset(rep, 0, sizeof(*rep));
-  if (m < 1 || rtol < 0.0 || atol < 0.0 || orth < 0 || orth > 1) return ORC_EINVAL;
+  if (m < 1 || rtol < 0.0 || atol < 0.0 || orth < 0 || orth > 2) return ORC_EINVAL;
+  if (orth == 2)
+    return gmres_dcgs2(A, M, b, restart, max_iters, rtol, atol, x, history, hist_cap, rep, V_out,
+                       v_count);
   double *hp = (double *)malloc(sizeof(double) * (size_t)(m + 1)); /* one CGS pass */
   double *V = (double *)malloc(sizeof(double) * (size_t)((m + 1) * n));
   double *H = (double *)calloc((size_t)((m + 1) * m), sizeof(double)); /* H[i*m + k] */
@@ -862,6 +869,177 @@ int orc_gmres_orth(const orc_op *A, const orc_op *M, const double *b, int64_t re
   if (status == ORC_OK && !converged) status = ORC_NOT_CONVERGED;
   rep->status = status;
   free(V); free(H); free(cs); free(sn); free(g); free(yk); free(t); free(r); free(hp);
+  return status;
+}
+
+/* GMRES with delayed classical Gram-Schmidt reorthogonalisation, one reduction per
+ * Arnoldi step (orth = 2; SURVEY §8.f3 "one allreduce per iteration"; reading Q27).
+ * The low-synchronisation Arnoldi of Swirydowicz, Langou, Ananthan, Yang, Thomas
+ * (2020) and Bielich et al. (2022) ("DCGS2"), restated:
+ *   slot k of V holds u_k = the k-th direction after ONE classical Gram-Schmidt pass,
+ *   not yet reorthogonalised nor normalised (u_0 = the preconditioned residual).
+ *   Step k (k = 0..m):
+ *     w = B u_k (B = M^-1 A; skipped at k = m)
+ *     one block reduction:  a_j = <v_j, u_k>, alpha = <u_k, u_k>,
+ *                           b_j = <v_j, w>,   gamma = <u_k, w>        (j < k)
+ *     rho = sqrt(alpha - sum a_j^2)            (Pythagoras: ||u_k - V a||)
+ *     column k-1 of the Arnoldi relation:  H(j, k-1) = s_j + a_j,  H(k, k-1) = rho
+ *       (s = the first-pass coefficients of u_k), then the Givens update (Q12);
+ *       k = 0: beta = rho, g = beta e_1
+ *     v_k = (u_k - sum_j a_j v_j) / rho
+ *     c = V_{0..k}^T w / ... :  c_j = b_j (j < k),  c_k = (gamma - a^T b) / rho
+ *     next first pass of B v_k = (w - B V a)/rho with B V a = V H a (Arnoldi):
+ *       s_j = (c_j - sum_{i<k} H(j, i) a_i) / rho        (j = 0..k)
+ *       u_{k+1} = (w - V_{0..k} c) / rho = (w - sum_{j<k} (b_j - e a_j) v_j - e u_k) / rho,
+ *       e = c_k / rho
+ *   Column k-1's residual estimate is known at step k, one matvec after it was
+ *   started; the iteration count is the number of finished columns, as for MGS.
+ *   A rho that is zero (or alpha - |a|^2 <= 0 in rounding) is a happy breakdown. */
+static int gmres_dcgs2(const orc_op *A, const orc_op *M, const double *b, int64_t restart,
+                       int64_t max_iters, double rtol, double atol, double *x, double *history,
+                       int64_t hist_cap, orc_report *rep, double *V_out, int64_t *v_count) {
+  int64_t n = A->n, m = restart;
+  double *V = (double *)malloc(sizeof(double) * (size_t)((m + 1) * n));
+  double *Hr = (double *)calloc((size_t)((m + 1) * m), sizeof(double)); /* unrotated */
+  double *H = (double *)calloc((size_t)((m + 1) * m), sizeof(double));  /* rotated */
+  double *cs = (double *)malloc(sizeof(double) * (size_t)m);
+  double *sn = (double *)malloc(sizeof(double) * (size_t)m);
+  double *g = (double *)malloc(sizeof(double) * (size_t)(m + 1));
+  double *yk = (double *)malloc(sizeof(double) * (size_t)(m + 1));
+  double *aa = (double *)malloc(sizeof(double) * (size_t)(m + 1));
+  double *bb = (double *)malloc(sizeof(double) * (size_t)(m + 1));
+  double *cc = (double *)malloc(sizeof(double) * (size_t)(m + 1));
+  double *s = (double *)malloc(sizeof(double) * (size_t)(m + 1));
+  double *w = (double *)malloc(sizeof(double) * (size_t)n);
+  double *t = (double *)malloc(sizeof(double) * (size_t)n);
+  double *r = (double *)malloc(sizeof(double) * (size_t)n);
+  double *vk = (double *)malloc(sizeof(double) * (size_t)n);
+  for (int64_t i = 0; i < n; ++i) x[i] = 0.0;
+  op_apply(M, b, r);
+  double beta0 = sqrt(dot(n, r, r));
+  rep->beta0 = beta0;
+  double bnorm = sqrt(dot(n, b, b));
+  int64_t it = 0;
+  int converged = 0, status = ORC_OK;
+  if (v_count) *v_count = 0;
+  if (beta0 == 0.0) {
+    converged = 1;
+  } else {
+    double tol = fmax(rtol * beta0, atol);
+    for (;;) {
+      for (int64_t i = 0; i < n; ++i) V[i] = r[i]; /* u_0 */
+      int64_t k_end = 0;
+      int done = 0;
+      for (int64_t k = 0; k <= m; ++k) {
+        double *u = &V[k * n];
+        int more = k < m;
+        if (more) {
+          op_apply(A, u, t);
+          op_apply(M, t, w);
+        }
+        for (int64_t j = 0; j < k; ++j) aa[j] = dot(n, &V[j * n], u);
+        double alpha = dot(n, u, u), gamma = 0.0;
+        if (more) {
+          for (int64_t j = 0; j < k; ++j) bb[j] = dot(n, &V[j * n], w);
+          gamma = dot(n, u, w);
+        }
+        double asq = 0.0;
+        for (int64_t j = 0; j < k; ++j) asq += aa[j] * aa[j];
+        double rho2 = alpha - asq;
+        double rho = rho2 > 0.0 ? sqrt(rho2) : 0.0;
+        if (!isfinite(rho)) { status = ORC_ENUMERIC; done = 1; k_end = k > 0 ? k - 1 : 0; break; }
+        /* v_k = (u_k - sum_j a_j v_j) / rho */
+        for (int64_t i = 0; i < n; ++i) {
+          double v = u[i];
+          for (int64_t j = 0; j < k; ++j) v -= aa[j] * V[j * n + i];
+          vk[i] = rho > 0.0 ? v / rho : 0.0;
+        }
+        if (k == 0) {
+          for (int64_t i = 0; i <= m; ++i) g[i] = 0.0;
+          g[0] = rho;
+        } else {
+          int64_t kc = k - 1; /* finish column k-1 */
+          for (int64_t j = 0; j < k; ++j) Hr[j * m + kc] = s[j] + aa[j];
+          Hr[k * m + kc] = rho;
+          for (int64_t j = 0; j <= k; ++j) H[j * m + kc] = Hr[j * m + kc];
+          for (int64_t j = 0; j < kc; ++j) {
+            double p = H[j * m + kc], q = H[(j + 1) * m + kc];
+            H[j * m + kc] = cs[j] * p + sn[j] * q;
+            H[(j + 1) * m + kc] = -sn[j] * p + cs[j] * q;
+          }
+          double p = H[kc * m + kc], q = H[k * m + kc];
+          double den = hypot(p, q);
+          cs[kc] = p / den;
+          sn[kc] = q / den;
+          H[kc * m + kc] = den;
+          H[k * m + kc] = 0.0;
+          g[k] = -sn[kc] * g[kc];
+          g[kc] = cs[kc] * g[kc];
+          ++it;
+          if (it - 1 < hist_cap) history[it - 1] = fabs(g[k]) / beta0;
+          k_end = k;
+          int stop = 0;
+          if (fabs(g[k]) <= tol || rho == 0.0) { converged = 1; stop = 1; }
+          else if (it >= max_iters) stop = 1;
+          if (stop) { /* slot k = v_k: the basis of the last cycle is complete (V_out) */
+            memcpy(u, vk, sizeof(double) * (size_t)n);
+            done = 1;
+            break;
+          }
+        }
+        if (!more) { memcpy(u, vk, sizeof(double) * (size_t)n); break; }
+        /* the first pass of the next direction (u_k still unnormalised here) */
+        double ab = 0.0;
+        for (int64_t j = 0; j < k; ++j) ab += aa[j] * bb[j];
+        for (int64_t j = 0; j < k; ++j) cc[j] = bb[j];
+        cc[k] = (gamma - ab) / rho;
+        for (int64_t j = 0; j <= k; ++j) {
+          double ha = 0.0;
+          for (int64_t i = 0; i < k; ++i) ha += Hr[j * m + i] * aa[i];
+          s[j] = (cc[j] - ha) / rho;
+        }
+        double e = cc[k] / rho;
+        double *un = &V[(k + 1) * n];
+        for (int64_t i = 0; i < n; ++i) {
+          double nx = w[i] - e * u[i];
+          for (int64_t j = 0; j < k; ++j) nx -= (bb[j] - e * aa[j]) * V[j * n + i];
+          un[i] = nx / rho;
+        }
+        memcpy(u, vk, sizeof(double) * (size_t)n);
+      }
+      if (V_out) {
+        int64_t nv = k_end + 1;
+        memcpy(V_out, V, sizeof(double) * (size_t)(nv * n));
+        if (v_count) *v_count = nv;
+      }
+      for (int64_t i = k_end - 1; i >= 0; --i) {
+        double sum = g[i];
+        for (int64_t j = i + 1; j < k_end; ++j) sum -= H[i * m + j] * yk[j];
+        yk[i] = sum / H[i * m + i];
+      }
+      for (int64_t j = 0; j < k_end; ++j)
+        for (int64_t i = 0; i < n; ++i) x[i] += yk[j] * V[j * n + i];
+      rep->resid_est = fabs(g[k_end]) / beta0;
+      if (done) break;
+      op_apply(A, x, t);
+      for (int64_t i = 0; i < n; ++i) t[i] = b[i] - t[i];
+      op_apply(M, t, r);
+      double beta = sqrt(dot(n, r, r));
+      rep->restarts += 1;
+      if (beta <= tol) { converged = 1; rep->resid_est = beta / beta0; break; }
+    }
+  }
+  op_apply(A, x, t);
+  for (int64_t i = 0; i < n; ++i) t[i] = b[i] - t[i];
+  rep->resid_true = (bnorm > 0.0) ? sqrt(dot(n, t, t)) / bnorm : 0.0;
+  op_apply(M, t, r);
+  rep->resid_precond = (beta0 > 0.0) ? sqrt(dot(n, r, r)) / beta0 : 0.0;
+  rep->iterations = it;
+  rep->converged = converged;
+  if (status == ORC_OK && !converged) status = ORC_NOT_CONVERGED;
+  rep->status = status;
+  free(V); free(Hr); free(H); free(cs); free(sn); free(g); free(yk); free(aa); free(bb);
+  free(cc); free(s); free(w); free(t); free(r); free(vk);
   return status;
 }
 

@@ -265,7 +265,7 @@ def _krylov_qr(A, b, k):
     return (Q * np.sign(np.diag(R))).T
 
 
-@pytest.mark.parametrize("orth", ["mgs", "cgs2"])
+@pytest.mark.parametrize("orth", ["mgs", "cgs2", "dcgs2"])
 def test_gmres_basis_is_the_krylov_qr(orth):
     # implicit-Q theorem: any exact Arnoldi process yields the QR factor of the Krylov
     # matrix; a dropped pass, wrong sign or wrong coefficient breaks the match
@@ -279,13 +279,14 @@ def test_gmres_basis_is_the_krylov_qr(orth):
     assert np.max(np.abs(res.basis - _krylov_qr(A, b, 6))) < 1e-9
 
 
-def test_gmres_cgs2_same_solution_and_history_as_mgs():
+@pytest.mark.parametrize("orth", ["cgs2", "dcgs2"])
+def test_gmres_cgs2_same_solution_and_history_as_mgs(orth):
     rng = np.random.default_rng(6)
     G = rng.standard_normal((80, 80))
     A = G @ G.T + 2 * np.eye(80)
     b = rng.standard_normal(80)
     r1 = O.gmres(O.op_dense(A), O.op_identity(80), b, restart=15, rtol=1e-13)
-    r2 = O.gmres(O.op_dense(A), O.op_identity(80), b, restart=15, rtol=1e-13, orth="cgs2")
+    r2 = O.gmres(O.op_dense(A), O.op_identity(80), b, restart=15, rtol=1e-13, orth=orth)
     assert r1.converged and r2.converged
     assert abs(r1.iterations - r2.iterations) <= 1
     ref = np.linalg.solve(A, b)
@@ -295,15 +296,16 @@ def test_gmres_cgs2_same_solution_and_history_as_mgs():
     assert np.allclose(r1.history[:k][big], r2.history[:k][big], rtol=1e-6)
 
 
-def test_gmres_cgs2_orthogonal_where_one_pass_is_not():
-    # "twice is enough": on an ill-conditioned Krylov sequence CGS2 keeps
-    # ||I - V V^T|| at rounding level; MGS loses orthogonality in proportion to the
-    # condition of the Krylov basis
+@pytest.mark.parametrize("orth", ["cgs2", "dcgs2"])
+def test_gmres_cgs2_orthogonal_where_one_pass_is_not(orth):
+    # "twice is enough": on an ill-conditioned Krylov sequence CGS2 (and its delayed
+    # one-reduction form, reading Q27) keeps ||I - V V^T|| at rounding level; MGS loses
+    # orthogonality in proportion to the condition of the Krylov basis
     n = 120
     A = np.diag(np.logspace(0, 10, n))
     b = np.ones(n)
     res = O.gmres(O.op_dense(A), O.op_identity(n), b, restart=40, max_iters=40, rtol=0.0,
-                  keep_basis=True, orth="cgs2")
+                  keep_basis=True, orth=orth)
     V = res.basis
     loss2 = np.max(np.abs(V @ V.T - np.eye(V.shape[0])))
     assert loss2 < 1e-13
@@ -313,9 +315,10 @@ def test_gmres_cgs2_orthogonal_where_one_pass_is_not():
     assert np.max(np.abs(V @ V.T - np.eye(V.shape[0]))) > 100 * loss2  # the contrast (eps kappa)
 
 
-def test_cfg1_solve_cgs2_matches_mgs(cfg1_solution):
+@pytest.mark.parametrize("orth", ["cgs2", "dcgs2"])
+def test_cfg1_solve_cgs2_matches_mgs(cfg1_solution, orth):
     wl, res, lam = cfg1_solution
-    r2 = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, rtol=wl.tol, orth="cgs2")
+    r2 = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, rtol=wl.tol, orth=orth)
     assert r2.converged and abs(r2.iterations - res.iterations) <= 1
     assert np.linalg.norm(r2.x - lam) / np.linalg.norm(lam) < 1e-8
 
@@ -412,3 +415,23 @@ def test_solve_asm_same_weights_as_rasm(cfg1_solution):
     r = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, rtol=wl.tol, schwarz="asm")
     assert r.converged and r.resid_true < 1e-10
     assert np.linalg.norm(r.x - lam) / np.linalg.norm(lam) < 1e-8
+
+
+def test_gmres_dcgs2_restarts_breakdown_and_limits():
+    # restarts: the same iterates as MGS across cycles (jittered lattice, GMRES(10))
+    wl = W.make_lattice(40, jitter_frac=0.1, seed=5)
+    r1 = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, restart=10, rtol=1e-13)
+    r3 = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, restart=10, rtol=1e-13, orth="dcgs2")
+    assert r1.converged and r3.converged and r1.restarts >= 2
+    assert abs(r1.iterations - r3.iterations) <= 2 and r3.restarts == r1.restarts
+    assert np.linalg.norm(r3.x - r1.x) / np.linalg.norm(r1.x) < 1e-8
+    # happy breakdown: b in a 3-dimensional invariant subspace -> 3 iterations
+    A = np.diag([1.0, 2.0, 3.0] + [5.0] * 17)
+    b = np.zeros(20)
+    b[:3] = 1.0
+    r = O.gmres(O.op_dense(A), O.op_identity(20), b, restart=10, rtol=0.0, orth="dcgs2")
+    assert r.converged and r.iterations == 3
+    assert np.allclose(r.x[:3], [1.0, 0.5, 1.0 / 3.0], rtol=1e-12) and not r.x[3:].any()
+    # max_iters and the identity operator
+    r = O.gmres(O.op_identity(5), O.op_identity(5), np.arange(1.0, 6.0), orth="dcgs2")
+    assert r.converged and r.iterations == 1
