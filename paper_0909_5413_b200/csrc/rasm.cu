@@ -249,7 +249,7 @@ constexpr int kColCta = 20660;
 #else
 #define PROBE(i)
 #define TRACE(i)
-#define PCOL(a, j, k)
+#define PCOL(a, j, k) {}
 #endif
 
 struct AccSet {
