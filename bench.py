@@ -164,9 +164,9 @@ def run_ours(args, rank, world):
     kw = dict(rank=rank, nranks=world, comm="nccl", nccl_id=nccl_id) if world > 1 else {}
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
 
-    # Arnoldi orthogonalisation: MGS on one GPU (BJ:5, Q12); across GPUs CGS2 (reading
-    # Q23): 3 all-gathers per iteration instead of k+2
-    orth = args.orth or ("mgs" if world == 1 else "cgs2")
+    # Arnoldi orthogonalisation: MGS on one GPU (BJ:5, Q12); across GPUs delayed CGS2
+    # (reading Q27): ONE all-gather per iteration instead of k+2
+    orth = args.orth or ("mgs" if world == 1 else "dcgs2")
 
     def step(timing=False):
         c = P.Context(xy, wl.sigma, wl.cell, wl.rc, wl.rings, wl.box, **kw)
@@ -378,8 +378,8 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--orth", choices=["mgs", "cgs2"], default=None,
-                    help="GMRES orthogonalisation (default: mgs on 1 GPU, cgs2 across GPUs)")
+    ap.add_argument("--orth", choices=["mgs", "cgs2", "dcgs2"], default=None,
+                    help="GMRES orthogonalisation (default: mgs on 1 GPU, dcgs2 across GPUs)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

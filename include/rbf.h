@@ -131,10 +131,14 @@ typedef struct {
  *  restart    m >= 1 (30).      max_iters  >= 1 (1000).
  *  rtol, atol >= 0: stop when the recurrence residual |g_{k+1}| <= max(rtol*||M^-1 f||, atol).
  *  timing     nonzero: record per-phase CUDA-event times into the report (adds events).
- *  orth       Arnoldi orthogonalisation: RBF_ORTH_MGS (0, default; Q12, BJ:5) or
+ *  orth       Arnoldi orthogonalisation: RBF_ORTH_MGS (0, default; Q12, BJ:5),
  *             RBF_ORTH_CGS2 (classical Gram-Schmidt twice, reading Q23: 3 reductions per
- *             step instead of k+2; requires restart <= RBF_CGS2_MAX_RESTART, else EINVAL). */
-enum { RBF_ORTH_MGS = 0, RBF_ORTH_CGS2 = 1 };
+ *             step instead of k+2) or RBF_ORTH_DCGS2 (CGS2 with the second pass delayed
+ *             into the next step and Pythagorean normalisation, reading Q27: ONE reduction
+ *             per step -- one all-gather across GPUs; a column's residual is known one
+ *             operator application later).  CGS2/DCGS2 require restart <=
+ *             RBF_CGS2_MAX_RESTART, else EINVAL. */
+enum { RBF_ORTH_MGS = 0, RBF_ORTH_CGS2 = 1, RBF_ORTH_DCGS2 = 2 };
 #define RBF_CGS2_MAX_RESTART 32
 typedef struct {
   int32_t restart;

@@ -266,6 +266,7 @@ void rbf_destroy(rbf_ctx *c) {
   dfree(c->ar_part, s);
   dfree(c->ar_bar, s);
   dfree(c->cg_blk, s);
+  dfree(c->dc_blk, s);
   dfree(c->cg_count, s);
   if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
   if (c->g_graph) cudaGraphDestroy(c->g_graph);
@@ -447,12 +448,12 @@ int rbf_solve(rbf_ctx *c, const double *f, const rbf_gmres_params *g, double *la
     set_error("rbf_solve: restart >= 1, max_iters >= 1, rtol >= 0, atol >= 0 required");
     return RBF_EINVAL;
   }
-  if (g->orth != RBF_ORTH_MGS && g->orth != RBF_ORTH_CGS2) {
-    set_error("rbf_solve: orth must be RBF_ORTH_MGS or RBF_ORTH_CGS2 (got %d)", g->orth);
+  if (g->orth != RBF_ORTH_MGS && g->orth != RBF_ORTH_CGS2 && g->orth != RBF_ORTH_DCGS2) {
+    set_error("rbf_solve: orth must be RBF_ORTH_MGS, RBF_ORTH_CGS2 or RBF_ORTH_DCGS2 (got %d)", g->orth);
     return RBF_EINVAL;
   }
-  if (g->orth == RBF_ORTH_CGS2 && g->restart > RBF_CGS2_MAX_RESTART) {
-    set_error("rbf_solve: CGS2 supports restart <= %d (got %d)", RBF_CGS2_MAX_RESTART, g->restart);
+  if (g->orth != RBF_ORTH_MGS && g->restart > RBF_CGS2_MAX_RESTART) {
+    set_error("rbf_solve: CGS2/DCGS2 support restart <= %d (got %d)", RBF_CGS2_MAX_RESTART, g->restart);
     return RBF_EINVAL;
   }
   if (c->nranks > 1 && c->comm_mode == RBF_COMM_NONE) {

@@ -252,6 +252,7 @@ struct rbf_ctx {
   int ar_m = 0;                // restart length ar_part is sized for
   int cg_grid = 0;             // CTAs of the fused CGS2 Arnoldi kernel (0 = unused)
   double *cg_blk = nullptr;    // multi-kernel CGS2 per-block partials (kRedBlocks x 32)
+  double *dc_blk = nullptr;    // DCGS2 block-dot per-block partials (kRedBlocks x (2 m + 2))
   unsigned *cg_count = nullptr;
   int g_orth = -1;             // orthogonalisation the solve graph was built for
   // graph-driven solve (single rank): the whole restarted GMRES as one CUDA graph with

@@ -36,7 +36,15 @@ struct Scal {
   __host__ __device__ long long c1all() const { return c1loc() + m + 2; }
   __host__ __device__ long long c2loc() const { return c1all() + (long long)(m + 2) * P; }
   __host__ __device__ long long c2all() const { return c2loc() + m + 2; }
-  __host__ __device__ long long total() const { return c2all() + (long long)(m + 2) * P; }
+  // DCGS2 (reading Q27): this step's block dots [<x_r, u>, <x_r, w>] (r = 0..k: v_0..v_{k-1},
+  // u_k) and their all-gather (rank-major, stride 2(k+1)); unrotated Hessenberg; pending
+  // first-pass coefficients; sweep coefficients {a_0..a_m, d_0..d_m, rho, e}
+  __host__ __device__ long long dloc() const { return c2all() + (long long)(m + 2) * P; }
+  __host__ __device__ long long dall() const { return dloc() + 2 * (m + 2); }
+  __host__ __device__ long long Hraw() const { return dall() + (long long)2 * (m + 2) * P; }
+  __host__ __device__ long long sp() const { return Hraw() + (long long)(m + 1) * m; }
+  __host__ __device__ long long cf() const { return sp() + m + 2; }
+  __host__ __device__ long long total() const { return cf() + 2 * (m + 2) + 2; }
 };
 
 // sum over ranks of entry j of a rank-major all-gather with `cnt` entries per rank
@@ -199,6 +207,7 @@ struct Mailbox {
 constexpr int kMbSlots = 4;
 constexpr int kHpinScal = 16;  // hpin[kHpinScal...] : scalar read-backs (after the ring)
 static_assert(sizeof(Mailbox) * kMbSlots <= sizeof(double) * kHpinScal, "mailbox ring overlaps");
+constexpr int kDcMaxOut = 2 * (RBF_CGS2_MAX_RESTART + 1);  // DCGS2 block-dot outputs per step
 
 __device__ __forceinline__ void post_mailbox(Mailbox *ring, const double *S, const Scal &L, long long seq) {
   volatile Mailbox *v = ring + (seq % kMbSlots);
@@ -596,6 +605,196 @@ __global__ __launch_bounds__(kRedThreads) void k_cgs_pass(double *w, const doubl
   if (threadIdx.x == 0) *count = 0u;
 }
 
+// ---------------------------------------------------------------------------
+// DCGS2 (reading Q27; oracle gmres_dcgs2): per Arnoldi step k ONE block reduction,
+//   k_dcgs_dots:   x_r = <v_r, u_k>, y_r = <v_r, w> for r < k, and <u_k, u_k>, <u_k, w>
+//                  (w = B u_k; absent at the cycle's last step) -- one pass over
+//                  V_0..V_{k-1}, u_k, w with fixed-order sums;
+//   all-gather of the 2(k+1) partials (several ranks);
+//   k_dcgs_scalar: rho = sqrt(alpha - |a|^2), column k-1 of H (= pending first pass + a,
+//                  rho), its Givens rotation and residual estimate (mailbox), the next
+//                  first-pass coefficients s = (c - H a) / rho and the sweep coefficients;
+//   k_dcgs_update: v_k = (u_k - V a) / rho,  u_{k+1} = (w - V d - e u_k) / rho  (one pass).
+// ---------------------------------------------------------------------------
+__global__ __launch_bounds__(kRedThreads) void k_dcgs_dots(const double *__restrict__ V, long long ldv,
+                                                           int k, long long n,
+                                                           const double *__restrict__ w,
+                                                           double *__restrict__ blk,
+                                                           unsigned *__restrict__ count,
+                                                           double *__restrict__ out) {
+  constexpr int W_ = kRedThreads / 32;
+  __shared__ double sh_acc[kDcMaxOut][W_];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cnt = k + 1, nout = 2 * cnt;
+  const double *u = V + (long long)k * ldv;
+  for (int t = threadIdx.x; t < kDcMaxOut * W_; t += blockDim.x) (&sh_acc[0][0])[t] = 0.0;
+  __syncthreads();
+  const long long cstride = (long long)gridDim.x * blockDim.x * kCpE;
+  for (long long c0 = (long long)blockIdx.x * blockDim.x * kCpE; c0 < n; c0 += cstride) {
+    long long idx[kCpE];
+    bool ok[kCpE];
+    double uv[kCpE], wv[kCpE];
+#pragma unroll
+    for (int e = 0; e < kCpE; ++e) {
+      idx[e] = c0 + threadIdx.x + (long long)e * blockDim.x;
+      ok[e] = idx[e] < n;
+      uv[e] = ok[e] ? u[idx[e]] : 0.0;
+      wv[e] = (ok[e] && w) ? w[idx[e]] : 0.0;
+    }
+    for (int j = 0; j < cnt; ++j) {
+      double vv[kCpE];
+      if (j < k) {
+        const double *vj = V + (long long)j * ldv;
+#pragma unroll
+        for (int e = 0; e < kCpE; ++e) vv[e] = ok[e] ? vj[idx[e]] : 0.0;
+      } else {
+#pragma unroll
+        for (int e = 0; e < kCpE; ++e) vv[e] = uv[e];
+      }
+      double au = 0.0, aw = 0.0;
+#pragma unroll
+      for (int e = 0; e < kCpE; ++e) {
+        au = fma(vv[e], uv[e], au);
+        aw = fma(vv[e], wv[e], aw);
+      }
+      au = warp_sum(au);
+      aw = warp_sum(aw);
+      if (lane == 0) {
+        sh_acc[j][warp] += au;
+        sh_acc[cnt + j][warp] += aw;
+      }
+    }
+  }
+  __syncthreads();
+  for (int j = warp; j < nout; j += W_) {
+    double t = lane < W_ ? sh_acc[j][lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) blk[(long long)j * gridDim.x + blockIdx.x] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(count, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int j = warp; j < nout; j += W_) {
+    double t = 0.0;
+    for (unsigned b = lane; b < gridDim.x; b += 32) t += ((volatile double *)blk)[(long long)j * gridDim.x + b];
+    t = warp_sum(t);
+    if (lane == 0) out[j] = t;
+  }
+  if (threadIdx.x == 0) *count = 0u;
+}
+
+// One thread.  all = rank-major all-gather of the step's 2(k+1) partials.
+__global__ void k_dcgs_scalar(double *S, Scal L, const double *all, int k, Mailbox *mb, long long seq) {
+  const int m = L.m, P = L.P, cnt = k + 1, stride = 2 * cnt;
+  double *Hr = S + L.Hraw(), *H = S + L.H(), *sp = S + L.sp(), *cf = S + L.cf();
+  double *cs = S + L.cs(), *sn = S + L.sn(), *g = S + L.g();
+  double *a = cf, *d = cf + (m + 2);
+  double asq = 0.0;
+  for (int j = 0; j < k; ++j) {
+    a[j] = sum_ranks_rm(all, j, stride, P);
+    asq += a[j] * a[j];
+  }
+  const double alpha = sum_ranks_rm(all, k, stride, P);
+  const double rho2 = alpha - asq;
+  const double rho = rho2 > 0.0 ? sqrt(rho2) : (rho2 == rho2 ? 0.0 : rho2);  // NaN stays NaN
+  if (k == 0) {  // cycle start: beta = ||u_0||, g = beta e_1
+    for (int i = 0; i <= m; ++i) g[i] = 0.0;
+    g[0] = rho;
+    S[L.out() + 2] = rho;
+  } else {  // finish column k-1 of the Arnoldi relation, then Givens (as givens_step)
+    const int kc = k - 1;
+    for (int j = 0; j < k; ++j) Hr[(long long)j * m + kc] = sp[j] + a[j];
+    Hr[(long long)k * m + kc] = rho;
+    for (int j = 0; j <= k; ++j) H[(long long)j * m + kc] = Hr[(long long)j * m + kc];
+    for (int j = 0; j < kc; ++j) {
+      const double p = H[(long long)j * m + kc], q = H[(long long)(j + 1) * m + kc];
+      H[(long long)j * m + kc] = cs[j] * p + sn[j] * q;
+      H[(long long)(j + 1) * m + kc] = -sn[j] * p + cs[j] * q;
+    }
+    const double p = H[(long long)kc * m + kc], q = H[(long long)k * m + kc];
+    const double den = hypot(p, q);
+    cs[kc] = p / den;
+    sn[kc] = q / den;
+    H[(long long)kc * m + kc] = den;
+    H[(long long)k * m + kc] = 0.0;
+    g[k] = -sn[kc] * g[kc];
+    g[kc] = cs[kc] * g[kc];
+    S[L.out() + 0] = fabs(g[k]);
+    S[L.out() + 1] = rho;
+    post_mailbox(mb, S, L, seq);
+  }
+  if (k < m) {  // the next direction's first pass (w = B u_k present)
+    double ab = 0.0;
+    for (int j = 0; j < k; ++j) ab += a[j] * sum_ranks_rm(all, cnt + j, stride, P);
+    const double gamma = sum_ranks_rm(all, cnt + k, stride, P);
+    const double ck = (gamma - ab) / rho, e = ck / rho;
+    for (int j = 0; j <= k; ++j) {
+      const double cj = j < k ? sum_ranks_rm(all, cnt + j, stride, P) : ck;
+      double ha = 0.0;
+      for (int i = 0; i < k; ++i) ha += Hr[(long long)j * m + i] * a[i];
+      sp[j] = (cj - ha) / rho;
+      if (j < k) d[j] = cj - e * a[j];
+    }
+    cf[2 * (m + 2)] = rho;
+    cf[2 * (m + 2) + 1] = e;
+  }
+}
+
+// v_k = (u_k - sum_j a_j v_j) / rho  -> slot k;  u_{k+1} = (w - sum_j d_j v_j - e u_k) / rho
+// -> slot k+1 (w is read from there); rec (single rank): u_{k+1} packed for the next matvec.
+constexpr int kDuE = 4;
+__global__ __launch_bounds__(kRedThreads) void k_dcgs_update(double *V, long long ldv, int k, long long n,
+                                                             const double *__restrict__ S, Scal L,
+                                                             double4 *__restrict__ rec) {
+  __shared__ double sa[kCgMaxM + 2], sd[kCgMaxM + 2];
+  const double *cf = S + L.cf();
+  if (threadIdx.x < k) {
+    sa[threadIdx.x] = cf[threadIdx.x];
+    sd[threadIdx.x] = cf[(L.m + 2) + threadIdx.x];
+  }
+  __syncthreads();
+  const double rho = cf[2 * (L.m + 2)], e = cf[2 * (L.m + 2) + 1];
+  double *u = V + (long long)k * ldv, *w = V + (long long)(k + 1) * ldv;
+  const long long cstride = (long long)gridDim.x * blockDim.x * kDuE;
+  for (long long c0 = (long long)blockIdx.x * blockDim.x * kDuE; c0 < n; c0 += cstride) {
+    long long idx[kDuE];
+    bool ok[kDuE];
+    double uv[kDuE], vk[kDuE], nx[kDuE];
+#pragma unroll
+    for (int q = 0; q < kDuE; ++q) {
+      idx[q] = c0 + threadIdx.x + (long long)q * blockDim.x;
+      ok[q] = idx[q] < n;
+      uv[q] = ok[q] ? u[idx[q]] : 0.0;
+      vk[q] = uv[q];
+      nx[q] = ok[q] ? fma(-e, uv[q], w[idx[q]]) : 0.0;
+    }
+    for (int j = 0; j < k; ++j) {
+      const double *vj = V + (long long)j * ldv;
+      const double aj = sa[j], dj = sd[j];
+#pragma unroll
+      for (int q = 0; q < kDuE; ++q) {
+        const double v = ok[q] ? vj[idx[q]] : 0.0;
+        vk[q] = fma(-aj, v, vk[q]);
+        nx[q] = fma(-dj, v, nx[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kDuE; ++q)
+      if (ok[q]) {
+        u[idx[q]] = vk[q] / rho;
+        const double un = nx[q] / rho;
+        w[idx[q]] = un;
+        if (rec) reinterpret_cast<double *>(rec + idx[q])[2] = un;
+      }
+  }
+}
+
 // ---- graph-mode control kernels (one thread)
 __global__ void k_g_begin(const double *nrm2, GState *st, cudaGraphConditionalHandle outer) {
   const double beta0 = sqrt(*nrm2);
@@ -738,6 +937,7 @@ static int ensure_workspace(rbf_ctx *c, int m, cudaStream_t s) {
     RBF_CUDA_TRY(cudaHostAlloc((void **)&c->hpin, sizeof(double) * (kHpinScal + 8 + c->nranks), cudaHostAllocMapped));
     RBF_CUDA_TRY(cudaHostGetDevicePointer((void **)&c->hpin_dev, c->hpin, 0));
   }
+  if (!c->dc_blk) RBF_TRY(dalloc(c, (void **)&c->dc_blk, sizeof(double) * (size_t)kRedBlocks * kDcMaxOut, s));
   if (!c->cg_blk) {
     RBF_TRY(dalloc(c, (void **)&c->cg_blk, sizeof(double) * (size_t)kRedBlocks * kCgMaxM, s));
     RBF_TRY(dalloc(c, (void **)&c->cg_count, sizeof(unsigned), s));
@@ -893,6 +1093,7 @@ static int wait_mailbox(rbf_ctx *c, long long seq, cudaStream_t s, double *gabs,
 // ---------------------------------------------------------------------------
 // the single-rank cooperative Arnoldi kernel for this orthogonalisation is usable
 static bool fused_ok(const rbf_ctx *c, int orth) {
+  if (orth == RBF_ORTH_DCGS2) return false;  // multi-kernel path (one reduction per step)
   return c->nranks == 1 && c->rec && (orth == RBF_ORTH_CGS2 ? c->cg_grid : c->ar_grid) > 0;
 }
 
@@ -1146,13 +1347,75 @@ int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double 
     long long seq_enq = 0, seq_base = 0;  // Arnoldi steps enqueued; steps before this cycle
     for (int i = 0; i < kMbSlots; ++i) reinterpret_cast<volatile Mailbox *>(c->hpin)[i].seq = -1;
     for (;;) {
+      int kend = 0;
+      bool done = false;
+      if (orth == RBF_ORTH_DCGS2) {
+        // ---- delayed CGS2, one reduction per step (reading Q27): V0 holds u_0 (the
+        // unscaled preconditioned residual); step k (0..m) applies the operator to u_k,
+        // reduces [V_{<k}, u_k]^T [u_k, w] once, finishes column k-1 (mailbox) and
+        // forms v_k and u_{k+1}.  The host waits for column kc at step kc+1 while step
+        // kc+2 is already enqueued (one-step lookahead, as for MGS).
+        const int P = c->nranks;
+        const bool pk = P == 1 && c->rec != nullptr;  // u_{k+1} packed by the sweep
+        double *S = c->dscal;
+        double *dl = S + L.dloc(), *da = P > 1 ? S + L.dall() : dl;
+        Mailbox *mb = reinterpret_cast<Mailbox *>(c->hpin_dev);
+        auto enqueue_d = [&](int k) -> int {
+          const long long seq = ++seq_enq;
+          double *u = V + (long long)k * ldv;
+          double *w = V + (long long)(k + 1) * ldv;
+          pt.rec(seq, 0, s);
+          if (k < m) RBF_TRY(op.matvec(u, c->t1, pk && k > 0));
+          pt.rec(seq, 1, s);
+          if (k < m) RBF_TRY(op.pc(c->t1, w));
+          pt.rec(seq, 2, s);
+          k_dcgs_dots<<<grid_for(n), kRedThreads, 0, s>>>(V, ldv, k, n, k < m ? w : nullptr, c->dc_blk,
+                                                          c->cg_count, dl);
+          count_launch(1);
+          if (P > 1) RBF_TRY(allgather_scalars(c, dl, da, 2 * (k + 1), s));
+          k_dcgs_scalar<<<1, 1, 0, s>>>(S, L, da, k, mb, seq);
+          count_launch(1);
+          if (k < m) {
+            k_dcgs_update<<<blocks, kRedThreads, 0, s>>>(V, ldv, k, n, S, L, pk ? c->rec : nullptr);
+            count_launch(1);
+          }
+          RBF_CUDA_TRY(cudaGetLastError());
+          pt.rec(seq, 3, s);
+          return RBF_OK;
+        };
+        RBF_TRY(enqueue_d(0));
+        RBF_TRY(enqueue_d(1));
+        for (int kc = 0; kc < m; ++kc) {
+          if (kc + 2 <= m && it + 1 < gp->max_iters) RBF_TRY(enqueue_d(kc + 2));
+          double gabs = 0.0, hn = 0.0;
+          RBF_TRY(wait_mailbox(c, seq_base + kc + 2, s, &gabs, &hn));  // step kc+1
+          pt.accumulate(seq_base + kc + 1, false);                     // step kc: complete
+          ++it;
+          resid_est = gabs / beta0;
+          if (rep && rep->history && hist_len < rep->history_cap) rep->history[hist_len++] = resid_est;
+          kend = kc + 1;
+          if (!std::isfinite(gabs) || !std::isfinite(hn)) {
+            status = RBF_ENUMERIC;
+            done = true;
+            break;
+          }
+          if (gabs <= tol || hn == 0.0) {
+            converged = 1;
+            done = true;
+            break;
+          }
+          if (it >= gp->max_iters) {
+            done = true;
+            break;
+          }
+        }
+        if (kend >= 1) pt.accumulate(seq_base + kend + 1, true);
+      } else {
       // V0 holds the unscaled preconditioned residual; its ||.||^2 is in slot 0
       k_cycle_init<<<1, 1, 0, s>>>(c->dscal, L, hall_slot(c, L, 0)); count_launch(1);
       k_scale_by_norm<<<blocks, kRedThreads, 0, s>>>(V, n, hall_slot(c, L, 0), L.P, prepack ? c->rec : nullptr);
       count_launch(1);
       RBF_CUDA_TRY(cudaGetLastError());
-      int kend = 0;
-      bool done = false;
       // enqueue Arnoldi step k (matvec, preconditioner, orthogonalisation, Givens)
       auto enqueue = [&](int k) -> int {
         double *vk = V + (long long)k * ldv;
@@ -1238,6 +1501,7 @@ int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *gp, double 
         }
       }
       if (kend >= 1) pt.accumulate(seq_base + kend, true);  // last step of the cycle
+      }  // MGS / CGS2
       seq_base = seq_enq;
       k_backsolve<<<1, 1, 0, s>>>(c->dscal, L, kend); count_launch(1);
       k_update_x<<<blocks, kRedThreads, 0, s>>>(x, V, ldv, c->dscal, L, kend, n); count_launch(1);

@@ -293,7 +293,7 @@ class Context:
               lam=None, orth="mgs"):
         lam = self._new(self.n_local) if lam is None else lam
         gp = GmresParams(int(restart), int(max_iters), float(rtol), float(atol), int(timing),
-                         {"mgs": 0, "cgs2": 1}[orth])
+                         {"mgs": 0, "cgs2": 1, "dcgs2": 2}[orth])
         hist = np.zeros(max_iters, dtype=np.float64)
         rep = Report()
         rep.history = hist.ctypes.data_as(C.POINTER(C.c_double))
@@ -357,7 +357,7 @@ def interpolate_host(xy: np.ndarray, f: np.ndarray, sigma, cell, rc, rings=1,
     lam = np.empty_like(f)
     prm = make_params(sigma, cell, rc, rings, box, overlap_width, trunc_width)
     gp = GmresParams(int(restart), int(max_iters), float(rtol), float(atol), 0,
-                     {"mgs": 0, "cgs2": 1}[orth])
+                     {"mgs": 0, "cgs2": 1, "dcgs2": 2}[orth])
     hist = np.zeros(max_iters, dtype=np.float64)
     rep = Report()
     rep.history = hist.ctypes.data_as(C.POINTER(C.c_double))

@@ -239,6 +239,46 @@ def test_solve_parity_cgs2(wl, path, monkeypatch):
     assert np.all(d <= 1e-6 * ref.history[:n][big] + 1e-12)
 
 
+@pytest.mark.parametrize("timing", [False, True])
+@pytest.mark.parametrize("wl", CGS2_CASES + [W.make_paper_lattice(61, 0.9, b_over_sigma=5.0, d_over_b=1.9)],
+                         ids=["cfg1", "jitter64", "paper0.9-B5"])
+def test_solve_parity_dcgs2(wl, timing):
+    """orth=DCGS2 (one reduction per Arnoldi step, reading Q27) against the oracle's DCGS2."""
+    ref = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, wl.rings, rtol=wl.tol, orth="dcgs2",
+                  overlap_width=wl.overlap_width)
+    with ctx_for(wl) as c:
+        lam, rep = c.solve(c.to_local(torch.from_numpy(wl.f).cuda()), rtol=wl.tol, orth="dcgs2",
+                           timing=timing)
+        lam = to_caller(c, lam)
+        if timing:
+            assert rep.ms_orth > 0
+    assert rep.converged and ref.converged
+    assert abs(rep.iterations - ref.iterations) <= 2 and rep.restarts == ref.restarts
+    assert rep.resid_true <= 1e-10
+    assert rel(lam, ref.x) <= 1e-8
+    n = min(len(rep.history), len(ref.history))
+    big = ref.history[:n] > 1e-9
+    d = np.abs(rep.history[:n][big] - ref.history[:n][big])
+    assert np.all(d <= 1e-6 * ref.history[:n][big] + 1e-12)
+
+
+def test_dcgs2_restarts_and_max_iters():
+    wl = W.make_lattice(40, jitter_frac=0.1, seed=5)
+    ref = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, restart=10, rtol=1e-13, orth="dcgs2")
+    with ctx_for(wl) as c:
+        f = c.to_local(torch.from_numpy(wl.f).cuda())
+        lam, rep = c.solve(f, restart=10, rtol=1e-13, orth="dcgs2")
+        assert rep.converged and rep.restarts == ref.restarts >= 2
+        assert abs(rep.iterations - ref.iterations) <= 2
+        assert rel(to_caller(c, lam), ref.x) <= 1e-8
+        lam, rep = c.solve(f, restart=10, max_iters=7, rtol=1e-13, orth="dcgs2")
+        assert not rep.converged and rep.iterations == 7
+        with pytest.raises(P.RbfError):
+            c.solve(f, restart=33, orth="dcgs2")
+        z, rep = c.solve(torch.zeros_like(f), orth="dcgs2")
+        assert rep.iterations == 0 and not z.any()
+
+
 def test_cgs2_restart_limit():
     wl = W.make_lattice(30)
     with ctx_for(wl) as c:
@@ -380,7 +420,7 @@ def test_threads_strips_operators_bitwise(nranks):
     assert np.array_equal(sum(r[1] for r in res), z1)
 
 
-@pytest.mark.parametrize("orth", ["mgs", "cgs2"])
+@pytest.mark.parametrize("orth", ["mgs", "cgs2", "dcgs2"])
 @pytest.mark.parametrize("nranks,wl", [(2, W.make_lattice(60, jitter_frac=0.1, seed=5)),
                                        (4, W.make_lattice(100, jitter_frac=0.1, seed=9))],
                          ids=["2x60", "4x100"])
