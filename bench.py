@@ -151,7 +151,8 @@ def run_ours(args, rank, world):
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream()
-    wl = W.config(args.config)
+    weak = args.scaling == "weak"
+    wl = W.weak(world) if weak else W.config(args.config)
     xy_h = torch.from_numpy(wl.xy)
     f_h = torch.from_numpy(wl.f)
     xy = xy_h.cuda()
@@ -339,9 +340,11 @@ def run_ours(args, rank, world):
         line = {
             "metric": METRIC, "value": ms_per_step / 1e3, "unit": "s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": False, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": wl.name, "N": wl.n, "desc": W.CONFIG_DESCRIPTIONS[args.config],
+            "config": {"workload": wl.name, "N": wl.n,
+                       "desc": (W.CONFIG_DESCRIPTIONS[2] + f"; {world} copies stacked in y, one per GPU"
+                                if weak else W.CONFIG_DESCRIPTIONS[args.config]),
                        "orth": orth,
                        "parallelism": f"strips{world}", "l2": "flushed (256 MiB write) between steps",
                        "step": "rbf_setup (cell list + RASM setup) + rbf_solve, inputs in HBM"},
@@ -378,6 +381,9 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="strong: one BASELINE config on all GPUs (default); weak: one cfg2-sized "
+                         "block per GPU (rbf_workloads.weak)")
     ap.add_argument("--orth", choices=["mgs", "cgs2", "dcgs2"], default=None,
                     help="GMRES orthogonalisation (default: mgs on 1 GPU, dcgs2 across GPUs)")
     args = ap.parse_args()

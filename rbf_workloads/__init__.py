@@ -176,6 +176,25 @@ def make_paper_lattice(n_side: int, h_over_sigma: float, *, scatter_seed: int | 
                     overlap_width=ow)
 
 
+def weak(world: int) -> Workload:
+    """Weak-scaling version of cfg2: `world` copies of the cfg2 block stacked
+    in y -- a 1024 x (1024 world) lattice with the same h, jitter recipe (PCG64(2) in point
+    order, so the first 1024^2 points ARE cfg2's) and one unit-mass Gaussian (s^2 = 0.02)
+    at the centre of every [-1,1] x [2g-1, 2g+1] block; box [-1,1] x [-1, 2 world - 1].
+    Strips balanced by point count give every GPU one cfg2-sized block."""
+    n = 1024
+    h, sigma, rc, cell = lattice_params(n)
+    c = -1.0 + (np.arange(n, dtype=np.float64) + 0.5) * h
+    cy = -1.0 + (np.arange(n * world, dtype=np.float64) + 0.5) * h
+    X, Y = np.meshgrid(c, cy, indexing="xy")
+    xy = jitter(np.stack([X.ravel(), Y.ravel()], axis=1).copy(), h, 0.1, 2)
+    f = np.zeros(xy.shape[0])
+    for g in range(world):
+        f += gauss_rhs(xy - np.array([0.0, 2.0 * g]), 0.02)
+    return Workload(f"cfg2-weak{world}", xy, f, sigma, rc, cell, 1, 1e-13,
+                    box=(-1.0, -1.0, 1.0, 2.0 * world - 1.0), meta=dict(h=h, world=world))
+
+
 def config(k: int) -> Workload:
     """BASELINE.json configs[k-1] (BJ:7-11) as seeded synthetic input."""
     if k == 1:

@@ -118,3 +118,23 @@ def test_product_does_not_import_oracle():
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text
                 assert "rbf_oracle" not in text
+
+
+def test_weak_scaling_workload_and_strips():
+    """bench.py --scaling weak: world copies of cfg2 stacked in y; one copy per strip."""
+    import rbf_workloads as W
+    import oracle as O
+
+    P = _lib()
+    a, b = W.weak(1), W.config(2)
+    assert np.array_equal(a.xy, b.xy) and np.array_equal(a.f, b.f) and a.box == b.box
+    c = W.weak(4)
+    assert c.n == 4 * b.n and np.array_equal(c.xy[:b.n], b.xy)
+    assert np.max(np.abs(c.f[:b.n] - b.f)) < 1e-9 * np.max(np.abs(b.f))
+    # strips balanced by point count give each rank one block (+- one cell row)
+    key, _, start = O.cell_list(c.xy, c.box, c.cell)
+    ncx, ncy = O.grid_dims(c.box, c.cell)
+    rows = np.array([start[(r + 1) * ncx] - start[r * ncx] for r in range(ncy)])
+    bnd = P.plan_strips(rows, 4, 2)
+    own = [int(rows[bnd[g]:bnd[g + 1]].sum()) for g in range(4)]
+    assert sum(own) == c.n and max(abs(o - b.n) for o in own) <= 2 * rows.max()
