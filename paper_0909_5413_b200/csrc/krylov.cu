@@ -388,6 +388,130 @@ __global__ __launch_bounds__(kArThreads, 1) void k_arnoldi_fused(double *V, long
 }
 
 // ---------------------------------------------------------------------------
+// The same MGS step with TWO projections per grid barrier (reading Q28): for the pair
+// (v_j, v_{j+1}) one reduction gives D1 = <w, v_j>, D2 = <w, v_{j+1}>, D3 = <v_j, v_{j+1}>;
+// then h_j = D1 and h_{j+1} = <w - h_j v_j, v_{j+1}> = D2 - h_j D3 (MGS's coefficient,
+// the inner product of the updated vector, expanded), and w -= h_j v_j, then
+// w -= h_{j+1} v_{j+1} in MGS's order.  ceil((k+1)/2) + 1 barriers instead of k + 2.
+// The pair's vectors are loaded after the barrier (the next pair is prefetched into L2
+// during it); part slots: D1, D2 at j, j+1 and D3 at (m + 2) + j.
+// ---------------------------------------------------------------------------
+__global__ __launch_bounds__(kArThreads, 1) void k_arnoldi_mgs2(double *V, long long ldv, long long n,
+                                                             int k, double *S, Scal L,
+                                                             double *part, unsigned *bar,
+                                                             Mailbox *mb, long long seq,
+                                                             double4 *rec, const double *w_in,
+                                                             GState *st, double *hist,
+                                                             cudaGraphConditionalHandle inner) {
+  if (st) k = st->k;
+  __shared__ double sh_w[3][kArThreads / 32];
+  __shared__ double sh_h[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned G = gridDim.x;
+  const long long chunk = (n + G - 1) / G;
+  const long long base = (long long)blockIdx.x * chunk;
+  const long long end = base + chunk < n ? base + chunk : n;
+  const long long d3 = (long long)(L.m + 2) * G;
+  double *wv = V + (long long)(k + 1) * ldv;
+  const double *win = w_in ? w_in : wv;
+  double w[kArE], va[kArE], vb[kArE];
+#pragma unroll
+  for (int e = 0; e < kArE; ++e) {
+    const long long i = base + threadIdx.x + (long long)e * kArThreads;
+    w[e] = i < end ? win[i] : 0.0;
+  }
+  for (int j = 0; j <= k + 1; j += 2) {
+    const bool norm = j == k + 1;           // the last step: ||w||^2 only
+    const bool pair = !norm && j + 1 <= k;  // two projections in this step
+    double a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (norm) {
+#pragma unroll
+      for (int e = 0; e < kArE; ++e) a1 = fma(w[e], w[e], a1);
+    } else {
+      const double *vj = V + (long long)j * ldv, *vj1 = V + (long long)(j + 1) * ldv;
+#pragma unroll
+      for (int e = 0; e < kArE; ++e) {
+        const long long i = base + threadIdx.x + (long long)e * kArThreads;
+        va[e] = i < end ? vj[i] : 0.0;
+        vb[e] = (pair && i < end) ? vj1[i] : 0.0;
+      }
+#pragma unroll
+      for (int e = 0; e < kArE; ++e) {
+        a1 = fma(w[e], va[e], a1);
+        a2 = fma(w[e], vb[e], a2);
+        a3 = fma(va[e], vb[e], a3);
+      }
+    }
+    a1 = warp_sum(a1);
+    a2 = warp_sum(a2);
+    a3 = warp_sum(a3);
+    if (lane == 0) {
+      sh_w[0][warp] = a1;
+      sh_w[1][warp] = a2;
+      sh_w[2][warp] = a3;
+    }
+    __syncthreads();
+    if (warp < 3) {
+      double t = (lane < kArThreads / 32) ? sh_w[warp][lane] : 0.0;
+      t = warp_sum(t);
+      if (lane == 0) part[(warp == 2 ? d3 + (long long)j * G : (long long)(j + warp) * G) + blockIdx.x] = t;
+    }
+    if (!norm && j + 2 <= k) {  // the next pair into L2 while the barrier runs
+      const long long i = base + threadIdx.x;
+      if (i < end) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(V + (long long)(j + 2) * ldv + i));
+        if (j + 3 <= k) asm volatile("prefetch.global.L2 [%0];" ::"l"(V + (long long)(j + 3) * ldv + i));
+      }
+    }
+    cooperative_groups::this_grid().sync();
+    if (warp < 3) {
+      double hs = 0.0;
+      const long long off = warp == 2 ? d3 + (long long)j * G : (long long)(j + warp) * G;
+      if (warp == 0 || pair)
+        for (unsigned b = lane; b < G; b += 32) hs += ((volatile double *)part)[off + b];
+      hs = warp_sum(hs);
+      if (lane == 0) sh_w[warp][0] = hs;  // sh_w is free again after the barrier
+    }
+    __syncthreads();
+    if (norm) {
+      const double hn = sqrt(sh_w[0][0]);
+      if (blockIdx.x == 0 && threadIdx.x == 0) S[L.hloc() + j] = sh_w[0][0];
+#pragma unroll
+      for (int e = 0; e < kArE; ++e) {
+        const long long i = base + threadIdx.x + (long long)e * kArThreads;
+        if (i < end) {
+          const double v = (hn != 0.0) ? w[e] / hn : w[e];
+          wv[i] = v;
+          reinterpret_cast<double *>(rec + i)[2] = v;  // the next matvec's input, pre-packed
+        }
+      }
+    } else {
+      const double h1 = sh_w[0][0];
+      const double h2 = pair ? sh_w[1][0] - h1 * sh_w[2][0] : 0.0;
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        S[L.hloc() + j] = h1;
+        if (pair) S[L.hloc() + j + 1] = h2;
+      }
+#pragma unroll
+      for (int e = 0; e < kArE; ++e) {
+        w[e] = fma(-h1, va[e], w[e]);
+        if (pair) w[e] = fma(-h2, vb[e], w[e]);
+      }
+      if (!pair) j -= 1;  // odd count: the norm step follows directly (j + 2 - 1 = k + 1)
+    }
+    __syncthreads();  // sh_w reused by the next step's partials
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (st) {
+      graph_step_end(S, L, k, st, hist, inner);
+    } else {
+      givens_step(S, L, S + L.hloc(), k);
+      post_mailbox(mb, S, L, seq);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // CGS2 Arnoldi step (reading Q23), single rank, ONE cooperative launch with three
 // grid barriers instead of k+2: pass 1 h1 = V^T w; pass 2 w -= V h1, then
 // h2 = V^T w; pass 3 w -= V h2 and ||w||^2.  Same layout as k_arnoldi_fused (w in
@@ -909,7 +1033,7 @@ struct Op {
 
 // per-CTA partial sums of the fused Arnoldi kernels: MGS (m+2) slots, CGS2 3 passes
 static size_t part_doubles(const rbf_ctx *c, int m) {
-  const size_t a = (size_t)(m + 2) * (size_t)c->ar_grid;
+  const size_t a = (size_t)2 * (m + 2) * (size_t)c->ar_grid;  // MGS pairs: D3 after the m+2 slots
   const size_t b = (size_t)3 * (kCgMaxM + 1) * (size_t)c->cg_grid;
   return (a > b ? a : b) + 1;
 }
@@ -1111,12 +1235,15 @@ static int launch_fused_step(rbf_ctx *c, int orth, double *V, long long n, int k
   int k_ = k;
   double4 *rec = c->rec;
   void *args[] = {&V, &ldv_, &n_, &k_, &Sp, &L, &part, &bar, &mb, &seq_, &rec, &w_in, &st, &hist, &inner};
+  static int mgs_pair = -1;  // two MGS projections per grid barrier (reading Q28)
+  if (mgs_pair < 0) mgs_pair = getenv("RBF_MGS_PAIR") ? atoi(getenv("RBF_MGS_PAIR")) : 1;
   if (orth == RBF_ORTH_CGS2)
     RBF_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_arnoldi_cgs2, c->cg_grid, kArThreads, args,
                                              0, s));
   else
-    RBF_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_arnoldi_fused, c->ar_grid, kArThreads, args,
-                                             0, s));
+    RBF_CUDA_TRY(cudaLaunchCooperativeKernel(
+        mgs_pair ? (const void *)k_arnoldi_mgs2 : (const void *)k_arnoldi_fused, c->ar_grid, kArThreads,
+        args, 0, s));
   count_launch(1);
   return RBF_OK;
 }
