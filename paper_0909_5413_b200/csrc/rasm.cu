@@ -239,6 +239,9 @@ __device__ __forceinline__ int smid() {
   return r;
 }
 __device__ long long g_col[2][64][4];  // per tile column of one interior CTA (see PCOL)
+__device__ long long g_wcol[32][4];    // W phase of the same CTA: warp 0 per jt; [31] = warp 15
+#define PW(jt, k) \
+  if (lane == 0 && blockIdx.x == kColCta && (jt) < 32) g_wcol[jt][k] = clock64();
 constexpr int kColCta = 20660;
 #define PCOL(a, j, k) \
   if ((threadIdx.x & 31) == 0 && blockIdx.x == kColCta && (j) < 64) g_col[a][j][k] = clock64();
@@ -250,6 +253,7 @@ constexpr int kColCta = 20660;
 #define PROBE(i)
 #define TRACE(i)
 #define PCOL(a, j, k) {}
+#define PW(jt, k) {}
 #endif
 
 struct AccSet {
@@ -492,6 +496,7 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
     const int g0 = frag_colk(lane, 0), g1 = frag_colk(lane, 1);
     const unsigned bar_id = 1 + r;
     for (int jt = T0 - 1; jt >= 0; --jt) {
+      if (warp == 0) PW(jt, 0)
       AccSet A, B;  // four independent DMMA chains
       A.zero();
       B.zero();
@@ -515,7 +520,9 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
       if (half == 1) {
         *reinterpret_cast<double2 *>(wpart + r * 64 + 2 * lane) = make_double2(A.a0 + A.b0, A.a1 + A.b1);
       }
+      if (warp == 0) PW(jt, 1)
       asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+      if (warp == 0) PW(jt, 2)
       if (half == 0) {
         const double2 pp = *reinterpret_cast<const double2 *>(wpart + r * 64 + 2 * lane);
         A.a0 += pp.x;
@@ -535,9 +542,11 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
         __syncwarp();
         *reinterpret_cast<double2 *>(Ct + frag_acc(lane)) = make_double2(d0, d1);
       }
+      if (warp == 0) PW(jt, 3)
       asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
     }
   } else if (warp == 15) {
+    PW(31, 0)
     // S^-1 = L22^-T L22^-1 on tiles with the tensor cores (one warp, a few dozen DMMA):
     //   M = L22^-1:  M(a,a) = L_a^-1 (already formed by the diagonal factorization),
     //                M(a,b) = -L_a^-1 sum_{k=b}^{a-1} L22(a,k) M(k,b),   a > b;
@@ -600,6 +609,7 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
         __syncwarp();
       }
     }
+    PW(31, 1)
   }
   __syncthreads();
 
@@ -1087,6 +1097,7 @@ int probe_read(long long *out) {
   RBF_CUDA_TRY(cudaMemcpyFromSymbol(out, g_probe, sizeof(long long) * 64 * 8));
   RBF_CUDA_TRY(cudaMemcpyFromSymbol(out + 64 * 8, g_trace, sizeof(long long) * 65536 * 3));
   RBF_CUDA_TRY(cudaMemcpyFromSymbol(out + 64 * 8 + 65536 * 3, g_col, sizeof(long long) * 512));
+  RBF_CUDA_TRY(cudaMemcpyFromSymbol(out + 64 * 8 + 65536 * 3 + 512, g_wcol, sizeof(long long) * 128));
   return RBF_OK;
 #else
   (void)out;

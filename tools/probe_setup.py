@@ -21,7 +21,7 @@ for _ in range(2):
     torch.cuda.synchronize()
     print(c.setup_times())
     c.close()
-buf = np.zeros(64 * 8 + 65536 * 3 + 512, dtype=np.int64)
+buf = np.zeros(64 * 8 + 65536 * 3 + 512 + 128, dtype=np.int64)
 assert L.rbf_debug_probe(buf.ctypes.data_as(C.c_void_p)) == 0
 out = buf[:512].reshape(64, 8)
 tr = buf[512:512 + 65536 * 3].reshape(65536, 3)[:42025]
@@ -41,7 +41,7 @@ names = ["assembly", "cholesky", "W+Sinv", "X write"]
 for i, nm in enumerate(names):
     print(f"{nm:10s} mean {d[:, i].mean():10.0f} cyc  min {d[:, i].min():8d} max {d[:, i].max():8d}")
 print("total", (out[:, 4] - out[:, 0]).mean())
-col = buf[512 + 65536 * 3:].reshape(2, 64, 4)
+col = buf[512 + 65536 * 3:512 + 65536 * 3 + 512].reshape(2, 64, 4)
 c0, cd = col[0], col[1]
 base = c0[0, 0]
 print("per tile column j of one interior CTA (cycles): warp 0 [step1+2 time, wait at sync 1, panel+sync 2]; "
@@ -51,3 +51,10 @@ for j in range(30):
         break
     print(f"{j:2d} w0: {c0[j, 1] - c0[j, 0]:6d} {c0[j, 2] - c0[j, 1]:6d} {c0[j, 3] - c0[j, 2]:6d} | "
           f"dw: {cd[j, 1] - cd[j, 0]:6d} {cd[j, 2] - cd[j, 1]:6d} | col {c0[j, 3] - c0[j, 0]:6d}")
+wc = buf[512 + 65536 * 3 + 512:].reshape(32, 4)
+print("W phase, warp 0 (own row 0) per jt: [accumulate, wait bar 1, finish + L^-1 + store]; warp 15 S^-1 total")
+for jt in range(31):
+    if wc[jt, 0] == 0:
+        continue
+    print(f"jt {jt:2d}: {wc[jt, 1] - wc[jt, 0]:6d} {wc[jt, 2] - wc[jt, 1]:6d} {wc[jt, 3] - wc[jt, 2]:6d}")
+print("S^-1 (warp 15):", wc[31, 1] - wc[31, 0])
