@@ -910,3 +910,20 @@ def test_asm_multirank_unsupported():
     xy = torch.from_numpy(wl.xy).cuda()
     with pytest.raises(P.RbfError):
         P.Context(xy, wl.sigma, wl.cell, wl.rc, 1, wl.box, rank=0, nranks=2, schwarz="asm")
+
+
+@pytest.mark.parametrize("orth", ["mgs", "dcgs2"])
+@pytest.mark.parametrize("restart", [1, 2, 3, 5])
+def test_small_restarts_vs_oracle(restart, orth):
+    """GMRES(m) for small m on every orthogonalisation path: the pairwise-MGS fused kernel's
+    odd/even projection counts (reading Q28) and DCGS2's cycle end at k = m (reading Q27)."""
+    wl = W.make_lattice(24, jitter_frac=0.1, seed=3, s2=0.05)
+    ref = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, restart=restart, rtol=1e-12,
+                  max_iters=3000, orth=orth)
+    with ctx_for(wl) as c:
+        lam, rep = c.solve(c.to_local(torch.from_numpy(wl.f).cuda()), restart=restart, rtol=1e-12,
+                           max_iters=3000, orth=orth)
+        lam = to_caller(c, lam)
+    assert rep.converged and ref.converged
+    assert abs(rep.iterations - ref.iterations) <= max(2, ref.iterations // 50)
+    assert rep.resid_true <= 1e-10 and rel(lam, ref.x) <= 1e-8
