@@ -116,7 +116,10 @@ typedef struct {
  *                 checking the multi-strip path on one GPU, not a performance path.
  *                 Every collective call (rbf_matvec, rbf_rasm_apply, rbf_solve) must
  *                 be made by all nranks threads, or the callers block.
- *  nccl_id        NCCL: from rbf_get_nccl_id() on rank 0, broadcast by the caller.
+ *  nccl_id        NCCL: from rbf_get_nccl_id() on rank 0, broadcast by the caller.  The
+ *                 first context set up with an id creates the communicator; later
+ *                 contexts with the same id (same rank, rank count and device) reuse it --
+ *                 a unique id seeds one communicator -- and it lives until process exit.
  *                 THREADS: any 128-byte key shared by the group's contexts. */
 enum { RBF_COMM_NONE = 0, RBF_COMM_NCCL = 1, RBF_COMM_THREADS = 2 };
 typedef struct {

@@ -69,22 +69,48 @@ static int thread_group_join(rbf_ctx *c, const rbf_dist *d) {
   return RBF_OK;
 }
 
+// NCCL communicators, one per unique id per process.  An ncclUniqueId seeds exactly one
+// communicator (its bootstrap root serves one ncclCommInitRank round), so contexts set
+// up later with the same id -- e.g. one context per benchmark step -- reuse the
+// communicator instead of re-initialising from a spent id (which would hang), and the
+// communicator's creation cost is paid once.  They live until the process exits.
+struct NcclEntry {
+  ncclComm_t comm;
+  int rank, nranks, device;
+};
+static std::mutex g_nccl_mu;
+static std::map<std::string, NcclEntry> g_nccl;
+
 int comm_init(rbf_ctx *c, const rbf_dist *d) {
   if (c->nranks <= 1) return RBF_OK;
   if (c->comm_mode == RBF_COMM_THREADS) return thread_group_join(c, d);
   if (c->comm_mode != RBF_COMM_NCCL) return RBF_OK;
+  const std::string key(reinterpret_cast<const char *>(d->nccl_id), 128);
+  int dev = 0;
+  RBF_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  auto it = g_nccl.find(key);
+  if (it != g_nccl.end()) {
+    const NcclEntry &e = it->second;
+    if (e.rank != c->rank || e.nranks != c->nranks || e.device != dev) {
+      set_error("rbf_setup: nccl_id already seeded a communicator as rank %d of %d on device %d "
+                "(this context: rank %d of %d on device %d)", e.rank, e.nranks, e.device, c->rank,
+                c->nranks, dev);
+      return RBF_EINVAL;
+    }
+    c->nccl = e.comm;
+    return RBF_OK;
+  }
   ncclUniqueId id;
   static_assert(sizeof(id.internal) == 128, "nccl id size");
   memcpy(id.internal, d->nccl_id, 128);
   RBF_NCCL_TRY(ncclCommInitRank(&c->nccl, c->nranks, id, c->rank));
+  g_nccl[key] = NcclEntry{c->nccl, c->rank, c->nranks, dev};
   return RBF_OK;
 }
 
 void comm_destroy(rbf_ctx *c) {
-  if (c->nccl) {
-    ncclCommDestroy(c->nccl);
-    c->nccl = nullptr;
-  }
+  c->nccl = nullptr;  // the communicator stays with its id (process lifetime, above)
 }
 
 // RBF_COMM_THREADS exchange: publish this rank's send regions, copy the peers'.
