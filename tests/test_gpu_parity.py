@@ -927,3 +927,44 @@ def test_small_restarts_vs_oracle(restart, orth):
     assert rep.converged and ref.converged
     assert abs(rep.iterations - ref.iterations) <= max(2, ref.iterations // 50)
     assert rep.resid_true <= 1e-10 and rel(lam, ref.x) <= 1e-8
+
+
+def test_combined_options_solve_parity():
+    """The paper's full configuration with every option at once: box overlap (Q24), T-box
+    matvec (Q25), additive Schwarz (Q26) and one-reduction orthogonalisation (Q27)."""
+    wl = W.make_paper_lattice(61, 0.9, scatter_seed=7, b_over_sigma=6.0, d_over_b=1.9)
+    tau = 3.0 * wl.sigma
+    for schwarz, orth in (("rasm", "dcgs2"), ("asm", "mgs"), ("asm", "dcgs2")):
+        ref = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, wl.rings, rtol=1e-13,
+                      overlap_width=wl.overlap_width, trunc_width=tau, schwarz=schwarz, orth=orth)
+        with ctx_for(wl, trunc_width=tau, schwarz=schwarz) as c:
+            lam, rep = c.solve(c.to_local(torch.from_numpy(wl.f).cuda()), rtol=1e-13, orth=orth)
+            lam = to_caller(c, lam)
+        assert rep.converged and ref.converged, (schwarz, orth)
+        assert abs(rep.iterations - ref.iterations) <= 2, (schwarz, orth)
+        assert rel(lam, ref.x) <= 1e-8, (schwarz, orth)
+
+
+def test_threads_strips_box_overlap_tbox_dcgs2():
+    """Two in-process strips with box overlap and the T-box matvec, DCGS2: same solution as
+    one strip."""
+    wl = W.make_paper_lattice(81, 0.9, b_over_sigma=5.0, d_over_b=1.9)
+    tau = 2.0 * wl.sigma
+    xy = torch.from_numpy(wl.xy).cuda()
+    f = torch.from_numpy(wl.f).cuda()
+    with ctx_for(wl, trunc_width=tau) as c1:
+        lam1, rep1 = c1.solve(c1.to_local(f), rtol=1e-13, orth="dcgs2")
+        lam1 = c1.from_local(lam1).cpu().numpy()
+
+    def body(r, key, st):
+        with P.Context(xy, wl.sigma, wl.cell, wl.rc, wl.rings, wl.box, rank=r, nranks=2,
+                       comm="threads", nccl_id=key, stream=st, overlap_width=wl.overlap_width,
+                       trunc_width=tau) as c:
+            lam, rep = c.solve(c.to_local(f), rtol=1e-13, orth="dcgs2")
+            return c.from_local(lam).cpu().numpy(), rep
+
+    res = _run_threads(2, body)
+    reps = [r[1] for r in res]
+    assert all(rp.converged for rp in reps) and reps[0].iterations == reps[1].iterations
+    assert abs(reps[0].iterations - rep1.iterations) <= 1
+    assert rel(sum(r[0] for r in res), lam1) <= 1e-8
