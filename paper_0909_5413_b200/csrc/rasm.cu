@@ -129,6 +129,7 @@ __device__ __forceinline__ int nat_to_global(const Runs &R, int q) {
 constexpr int kTcThreads = 512;
 constexpr int kTcWarps = kTcThreads / 32;
 constexpr int kTcMaxTiles = 29;  // N <= 232: 435 tiles = 222,720 B of shared memory
+constexpr size_t kTcMaxSmem = 227 * 1024 - 1024;  // dynamic shared memory (static part ~0.6 KB)
 
 __device__ __forceinline__ int toff(int it, int jt) { return ((it * (it + 1)) / 2 + jt) * 64; }
 __device__ __forceinline__ int swz(int r, int c) { return r * 8 + (c ^ (((r >> 1) & 1) << 2)); }
@@ -146,10 +147,15 @@ struct TileShape {
     T0 = n0p / 8;
     T1 = n1p / 8;
   }
-  __host__ __device__ bool fits_tc() const { return T <= kTcMaxTiles && n1p <= 32; }
+  // own(c) up to 64 points (8 tile rows): one W warp per own tile row (pairs up to 4 rows)
+  __host__ __device__ bool fits_tc() const {
+    return T <= kTcMaxTiles && n1p <= 64 && smem_bytes() <= kTcMaxSmem;
+  }
   __host__ __device__ size_t smem_bytes() const {
-    // tiles + rdiag + W partials + max(positions, the S^-1 phase's 6 M tiles + 1 scratch)
-    const size_t pos_or_m = (size_t)N * sizeof(double2) > 7 * 64 * 8 ? (size_t)N * sizeof(double2) : 7 * 64 * 8;
+    // tiles + rdiag + W partials + max(positions, the S^-1 phase's T1(T1-1)/2 M tiles + 1 scratch)
+    const size_t mt = ((size_t)T1 * (T1 - 1) / 2 + 1) * 64 * 8;
+    const size_t m = mt > 7 * 64 * 8 ? mt : 7 * 64 * 8;
+    const size_t pos_or_m = (size_t)N * sizeof(double2) > m ? (size_t)N * sizeof(double2) : m;
     return ((size_t)T * (T + 1) / 2 * 64 + (size_t)T * 8 + 4 * 64) * 8 + pos_or_m;
   }
 };
@@ -211,7 +217,7 @@ __global__ void k_rasm_sizes(Geom g, Strip st, const int *__restrict__ cell_star
     atomicAdd(&maxes[2], 1);
     TileShape S(R.n_ov, R.n_own);
     if (g.asm_full || !S.fits_tc()) glist[atomicAdd(&maxes[3], 1)] = cl;
-    else atomicMax(&maxes[4], S.T);
+    else atomicMax(&maxes[4], (int)S.smem_bytes());
   }
 }
 
@@ -488,8 +494,10 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
   //      partner's partial goes through shared memory and a 64-thread named barrier.
   //      S^-1 = L22^-T L22^-1 concurrently on warp 15.
   double *wpart = rdiag + T * 8;  // 4 rows x 64 doubles (after rdiag, before the M area)
-  if (warp < 8 && (warp & 3) < T1) {
-    const int r = warp & 3, half = warp >> 2;  // half 0 finishes the tiles
+  // up to 4 own tile rows: a warp pair per row; 5..8 rows (own(c) up to 64): one warp per row
+  const bool wpairs = T1 <= 4;
+  if (wpairs ? (warp < 8 && (warp & 3) < T1) : warp < T1) {
+    const int r = wpairs ? warp & 3 : warp, half = wpairs ? warp >> 2 : 0;  // half 0 finishes
     const int it = T0 + r;
     double *Wrow = sm + toff(it, 0);
     const int f0 = frag_rowk(lane, 0), f1 = frag_rowk(lane, 1);
@@ -500,18 +508,20 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
       AccSet A, B;  // four independent DMMA chains
       A.zero();
       B.zero();
-      int kt = jt + 1 + half;
-      for (; kt + 2 < T0; kt += 4) {
-        const double *Lk = sm + toff(kt, jt), *Lk2 = sm + toff(kt + 2, jt);
-        dmma(A.a0, A.a1, Wrow[kt * 64 + f0], Lk[g0]);
-        dmma(A.b0, A.b1, Wrow[(kt + 2) * 64 + f0], Lk2[g0]);
-        dmma(B.a0, B.a1, Wrow[kt * 64 + f1], Lk[g1]);
-        dmma(B.b0, B.b1, Wrow[(kt + 2) * 64 + f1], Lk2[g1]);
-      }
-      if (kt < T0) {
-        const double *Lk = sm + toff(kt, jt);
-        dmma(A.a0, A.a1, Wrow[kt * 64 + f0], Lk[g0]);
-        dmma(B.a0, B.a1, Wrow[kt * 64 + f1], Lk[g1]);
+      for (int par = half; par < 2; par += wpairs ? 2 : 1) {  // kt parity (both for a lone warp)
+        int kt = jt + 1 + par;
+        for (; kt + 2 < T0; kt += 4) {
+          const double *Lk = sm + toff(kt, jt), *Lk2 = sm + toff(kt + 2, jt);
+          dmma(A.a0, A.a1, Wrow[kt * 64 + f0], Lk[g0]);
+          dmma(A.b0, A.b1, Wrow[(kt + 2) * 64 + f0], Lk2[g0]);
+          dmma(B.a0, B.a1, Wrow[kt * 64 + f1], Lk[g1]);
+          dmma(B.b0, B.b1, Wrow[(kt + 2) * 64 + f1], Lk2[g1]);
+        }
+        if (kt < T0) {
+          const double *Lk = sm + toff(kt, jt);
+          dmma(A.a0, A.a1, Wrow[kt * 64 + f0], Lk[g0]);
+          dmma(B.a0, B.a1, Wrow[kt * 64 + f1], Lk[g1]);
+        }
       }
       A.a0 += B.a0;
       A.a1 += B.a1;
@@ -521,12 +531,14 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
         *reinterpret_cast<double2 *>(wpart + r * 64 + 2 * lane) = make_double2(A.a0 + A.b0, A.a1 + A.b1);
       }
       if (warp == 0) PW(jt, 1)
-      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+      if (wpairs) asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
       if (warp == 0) PW(jt, 2)
       if (half == 0) {
-        const double2 pp = *reinterpret_cast<const double2 *>(wpart + r * 64 + 2 * lane);
-        A.a0 += pp.x;
-        A.a1 += pp.y;
+        if (wpairs) {
+          const double2 pp = *reinterpret_cast<const double2 *>(wpart + r * 64 + 2 * lane);
+          A.a0 += pp.x;
+          A.a1 += pp.y;
+        }
         acc_finish_rmw(A, sm, it, jt, lane);
         __syncwarp();
         // W(it, jt) = C L_d^-1   (B[k][n] = Linv[k][n])
@@ -543,7 +555,8 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
         *reinterpret_cast<double2 *>(Ct + frag_acc(lane)) = make_double2(d0, d1);
       }
       if (warp == 0) PW(jt, 3)
-      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+      if (wpairs) asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+      else __syncwarp();
     }
   } else if (warp == 15) {
     PW(31, 0)
@@ -554,7 +567,7 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
     //   so each row's diagonal tile is written last, over the L_a / L_a^-1 storage).
     // M (strictly lower tiles) lives in the positions buffer (dead after the factorisation).
     double *Mt = reinterpret_cast<double *>(pos);
-    double *scr = Mt + 6 * 64;
+    double *scr = Mt + (T1 * (T1 - 1) / 2) * 64;
     auto mt = [&](int a, int b) { return Mt + ((a * (a - 1)) / 2 + b) * 64; };  // a > b only
     const int m_ = lane >> 2, q_ = lane & 3;
     // Linv_a fragments: as A (A[m][k] = Linv[m][k]) or B (B[k][n] = Linv[k][n]); Linv[r][c]
@@ -1186,8 +1199,7 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
   c->x_count = total;
   RBF_TRY(dalloc(c, (void **)&c->X, sizeof(double) * (size_t)(total > 0 ? total : 2), s));
   if (ncl > 0 && c->nsub > hc[3]) {
-    const int Tmax = hc[4];
-    const size_t smem = TileShape(Tmax * 8, 0).smem_bytes();  // N = 8 Tmax
+    const size_t smem = (size_t)hc[4];  // the largest per-cell layout of the tensor-core cells
     RBF_CUDA_TRY(cudaFuncSetAttribute(k_rasm_setup_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
     k_rasm_setup_tc<<<ncl, kTcThreads, smem, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off,

@@ -968,3 +968,19 @@ def test_threads_strips_box_overlap_tbox_dcgs2():
     assert all(rp.converged for rp in reps) and reps[0].iterations == reps[1].iterations
     assert abs(reps[0].iterations - rep1.iterations) <= 1
     assert rel(sum(r[0] for r in res), lam1) <= 1e-8
+
+
+@pytest.mark.parametrize("b_over_sigma", [5.0, 7.0])
+def test_rasm_apply_parity_large_own(b_over_sigma):
+    """Cells of 33..64 own points (the paper's B = 5 sigma at h/sigma = 0.9, and larger)
+    take the tensor-core setup with one W warp per own tile row."""
+    wl = W.make_paper_lattice(61, 0.9, b_over_sigma=b_over_sigma, d_over_b=1.5)
+    r = np.random.default_rng(61).standard_normal(wl.n)
+    Pc = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, wl.rings, overlap_width=wl.overlap_width)
+    ref = Pc.apply(r)
+    Pc.close()
+    with ctx_for(wl) as c:
+        info = c.info()
+        z = to_caller(c, c.rasm_apply(c.to_local(torch.from_numpy(r).cuda())))
+    assert info["max_own"] > 32 and info["n_lu"] < info["nsub"] // 2
+    assert rel(z, ref) <= 1e-10
