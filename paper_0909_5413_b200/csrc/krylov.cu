@@ -405,7 +405,6 @@ __global__ __launch_bounds__(kArThreads, 1) void k_arnoldi_mgs2(double *V, long 
                                                              cudaGraphConditionalHandle inner) {
   if (st) k = st->k;
   __shared__ double sh_w[3][kArThreads / 32];
-  __shared__ double sh_h[2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned G = gridDim.x;
   const long long chunk = (n + G - 1) / G;

@@ -18,6 +18,7 @@
 // is written by exactly one cell (partition property): no atomics.
 #include <cub/cub.cuh>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -496,7 +497,9 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
   double *wpart = rdiag + T * 8;  // 4 rows x 64 doubles (after rdiag, before the M area)
   // up to 4 own tile rows: a warp pair per row; 5..8 rows (own(c) up to 64): one warp per row
   const bool wpairs = T1 <= 4;
-  if (wpairs ? (warp < 8 && (warp & 3) < T1) : warp < T1) {
+  // the row loop, specialised for warp pairs (PAIRS) or one warp per row
+  auto wloop = [&](auto pairs_tag) {
+    constexpr bool wpairs = decltype(pairs_tag)::value;
     const int r = wpairs ? warp & 3 : warp, half = wpairs ? warp >> 2 : 0;  // half 0 finishes
     const int it = T0 + r;
     double *Wrow = sm + toff(it, 0);
@@ -558,6 +561,10 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
       if (wpairs) asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
       else __syncwarp();
     }
+  };
+  if (wpairs ? (warp < 8 && (warp & 3) < T1) : warp < T1) {
+    if (wpairs) wloop(std::true_type{});
+    else wloop(std::false_type{});
   } else if (warp == 15) {
     PW(31, 0)
     // S^-1 = L22^-T L22^-1 on tiles with the tensor cores (one warp, a few dozen DMMA):
