@@ -182,7 +182,8 @@ int rbf_get_nccl_id(unsigned char out[128]);
  *  xy_dev  N x 2 interleaved fp64 (x0,y0,x1,y1,...) in caller order; every rank
  *          passes the full, identical point set.  Copied; may be freed afterwards.
  *  dist    NULL = single GPU.
- * Errors: EINVAL (n < 1, non-finite or out-of-box points, bad params, strips
+ * Errors: EINVAL (n < 1, non-finite or out-of-box points, two points with equal
+ * coordinates -- A is singular for repeated nodes, reading Q30 --, bad params, strips
  * thinner than the halo), ENOMEM, EFACTOR, ECUDA, ENCCL, EUNSUPPORTED (a
  * subdomain larger than this build's local-solve limit). */
 int rbf_setup(rbf_ctx **ctx, const double *xy_dev, int64_t n, const rbf_params *p,

@@ -85,6 +85,28 @@ __global__ void k_local_index(const int *__restrict__ perm, long long own_lo, lo
 
 static int blocks_for(long long n, int t) { return (int)((n + t - 1) / t); }
 
+// Coincident points (reading Q30): equal coordinates fall into the same cell, so each
+// cell compares its points pairwise; out[0] = the smallest caller index that repeats an
+// earlier point, out[1] = the caller index it repeats (lowest such pair).
+__global__ void k_dup_check(const double *__restrict__ xy, const int *__restrict__ perm,
+                            const int *__restrict__ cell_start, int ncells,
+                            unsigned long long *__restrict__ out) {
+  for (int cl = blockIdx.x; cl < ncells; cl += gridDim.x) {
+    const int s0 = cell_start[cl], s1 = cell_start[cl + 1];
+    for (int a = s0 + (int)threadIdx.x; a < s1; a += blockDim.x) {
+      const int ia = perm[a];
+      const double xa = xy[2LL * ia], ya = xy[2LL * ia + 1];
+      for (int b = a + 1; b < s1; ++b) {
+        const int ib = perm[b];
+        if (xy[2LL * ib] == xa && xy[2LL * ib + 1] == ya) {
+          const unsigned lo = ia < ib ? ia : ib, hi = ia < ib ? ib : ia;
+          atomicMin(out, ((unsigned long long)hi << 32) | lo);
+        }
+      }
+    }
+  }
+}
+
 int build_cell_list(rbf_ctx *c, const double *xy, cudaStream_t s) {
   const int n = (int)c->n;
   const int ncells = c->g.ncx * c->g.ncy;
@@ -118,6 +140,13 @@ int build_cell_list(rbf_ctx *c, const double *xy, cudaStream_t s) {
   k_row_start<<<blocks_for(c->g.ncy + 1, 256), 256, 0, s>>>(c->cell_start, c->g.ncx, c->g.ncy, rs); count_launch(1);
   k_max_cell<<<blocks_for(ncells, 256), 256, 0, s>>>(c->cell_start, ncells, bad + 1);
   count_launch(1);
+  unsigned long long *dup = nullptr, hdup = ~0ULL;
+  RBF_TRY(dalloc(c, (void **)&dup, sizeof(unsigned long long), s));
+  RBF_CUDA_TRY(cudaMemsetAsync(dup, 0xff, sizeof(unsigned long long), s));
+  k_dup_check<<<ncells < 4096 ? ncells : 4096, 128, 0, s>>>(xy, c->perm, c->cell_start, ncells, dup);
+  count_launch(1);
+  RBF_CUDA_TRY(cudaGetLastError());
+  RBF_CUDA_TRY(cudaMemcpyAsync(&hdup, dup, sizeof(hdup), cudaMemcpyDeviceToHost, s));
   int hmax = 0;
   c->row_start.assign(c->g.ncy + 1, 0);
   int hbad = 0;
@@ -133,9 +162,15 @@ int build_cell_list(rbf_ctx *c, const double *xy, cudaStream_t s) {
   dfree(skeys, s);
   dfree(bad, s);
   dfree(rs, s);
+  dfree(dup, s);
   if (hbad != 0x7fffffff) {
     set_error("rbf_setup: point %d is non-finite or outside the box [%g,%g]x[%g,%g]", hbad,
               c->g.x0, c->g.x1, c->g.y0, c->g.y1);
+    return RBF_EINVAL;
+  }
+  if (hdup != ~0ULL) {
+    set_error("rbf_setup: points %u and %u coincide (the interpolation matrix is singular for "
+              "repeated nodes; SPEC S:53)", (unsigned)(hdup & 0xffffffffULL), (unsigned)(hdup >> 32));
     return RBF_EINVAL;
   }
   return RBF_OK;

@@ -984,3 +984,22 @@ def test_rasm_apply_parity_large_own(b_over_sigma):
         z = to_caller(c, c.rasm_apply(c.to_local(torch.from_numpy(r).cuda())))
     assert info["max_own"] > 32 and info["n_lu"] < info["nsub"] // 2
     assert rel(z, ref) <= 1e-10
+
+
+def test_duplicate_point_rejected():
+    """Two identical points make A singular (SPD for distinct points); the
+    oracle's factorisation meets an exact zero pivot (EFACTOR), the library rejects the
+    input up front naming the pair (reading Q30) -- rounding in a blocked GPU LU need not
+    produce an exact zero."""
+    wl = W.make_lattice(20, jitter_frac=0.1, seed=1)
+    xy = np.vstack([wl.xy, wl.xy[[37]]])
+    Pc = O.Rasm(xy, wl.sigma, wl.rc, wl.box, wl.cell, 1)
+    assert Pc.status == -5
+    Pc.close()
+    with pytest.raises(P.RbfError) as e:
+        P.Context(torch.from_numpy(xy).cuda(), wl.sigma, wl.cell, wl.rc, 1, wl.box)
+    assert e.value.code == -1 and f"points 37 and {wl.n} coincide" in str(e.value)
+    # a point very close to another is valid input
+    xy2 = np.vstack([wl.xy, wl.xy[[37]] + [1e-9, 0.0]])
+    with P.Context(torch.from_numpy(xy2).cuda(), wl.sigma, wl.cell, wl.rc, 1, wl.box) as c:
+        assert c.n_local == wl.n + 1
