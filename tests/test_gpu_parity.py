@@ -1003,3 +1003,77 @@ def test_duplicate_point_rejected():
     xy2 = np.vstack([wl.xy, wl.xy[[37]] + [1e-9, 0.0]])
     with P.Context(torch.from_numpy(xy2).cuda(), wl.sigma, wl.cell, wl.rc, 1, wl.box) as c:
         assert c.n_local == wl.n + 1
+
+
+def test_points_on_cell_edges_and_box_corners():
+    """Points exactly on cell edges and on the box boundary: the cell of a point is
+    floor((x - x0) / c) in IEEE division on both sides (reading Q5), so perm and
+    cell_start stay bit-identical, and the operators match."""
+    c = 0.1
+    k = np.arange(0, 21)
+    X, Y = np.meshgrid(-1.0 + k * c, -1.0 + k * c, indexing="xy")  # includes x = 1 (clamped)
+    rng = np.random.default_rng(71)
+    xy = np.vstack([np.stack([X.ravel(), Y.ravel()], 1), rng.uniform(-1, 1, (300, 2))])
+    sigma = c / 4.0
+    wl = W.Workload("edges", xy, np.exp(-(xy ** 2).sum(1) / 0.1), sigma, 6 * sigma, c)
+    key, perm, start = O.cell_list(xy, wl.box, c)
+    with ctx_for(wl, rings=1) as ctx:
+        gperm, gstart, _ = ctx.cell_list()
+        assert np.array_equal(gperm.cpu().numpy(), perm) and np.array_equal(gstart.cpu().numpy(), start)
+        w = rng.standard_normal(wl.n)
+        got = to_caller(ctx, ctx.matvec(ctx.to_local(torch.from_numpy(w).cuda())))
+        r = rng.standard_normal(wl.n)
+        z = to_caller(ctx, ctx.rasm_apply(ctx.to_local(torch.from_numpy(r).cuda())))
+    assert rel(got, O.matvec_brute(xy, w, sigma, wl.rc)) <= 1e-12
+    Pc = O.Rasm(xy, sigma, wl.rc, wl.box, c, 1)
+    assert rel(z, Pc.apply(r)) <= 1e-10
+    Pc.close()
+
+
+def test_empty_band_and_strips():
+    """Two clusters separated by an empty band of cell rows: empty cells have no
+    subdomain, a strip may hold nothing but halo -- same solution on one and two strips."""
+    rng = np.random.default_rng(72)
+    a = W.lattice(40)
+    a = a[np.abs(a[:, 1]) > 0.45]  # drop the middle band
+    xy = W.jitter(a, 2.0 / 40, 0.1, 3)
+    h = 2.0 / 40
+    sigma = h / 0.8
+    wl = W.Workload("band", xy, W.gauss_rhs(xy - [0.0, 0.7], 0.05) + W.gauss_rhs(xy + [0.0, 0.7], 0.05),
+                    sigma, 6 * sigma, 4 * sigma)
+    ref = O.solve(wl.xy, wl.f, sigma, wl.rc, wl.box, wl.cell, rtol=1e-13)
+    with ctx_for(wl) as c1:
+        lam, rep = c1.solve(c1.to_local(torch.from_numpy(wl.f).cuda()), rtol=1e-13)
+        lam1 = to_caller(c1, lam)
+    assert rep.converged and abs(rep.iterations - ref.iterations) <= 2 and rel(lam1, ref.x) <= 1e-8
+    xy_d, f_d = torch.from_numpy(wl.xy).cuda(), torch.from_numpy(wl.f).cuda()
+
+    def body(r, key, st):
+        with P.Context(xy_d, sigma, wl.cell, wl.rc, 1, wl.box, rank=r, nranks=2, comm="threads",
+                       nccl_id=key, stream=st) as c:
+            lam, rep = c.solve(c.to_local(f_d), rtol=1e-13)
+            return c.from_local(lam).cpu().numpy(), rep
+
+    res = _run_threads(2, body)
+    assert all(r[1].converged for r in res)
+    assert rel(sum(r[0] for r in res), lam1) <= 1e-8
+
+
+def test_wide_cutoff_three_cell_rings():
+    """rc = 3 cells (cell = 2 sigma): the matvec searches 3 cell rings, the RASM overlap
+    stays one ring."""
+    h = 2.0 / 48
+    sigma = h / 0.8
+    xy = W.jitter(W.lattice(48), h, 0.1, 5)
+    wl = W.Workload("wide", xy, W.gauss_rhs(xy, 0.05), sigma, 6 * sigma, 2 * sigma)
+    w = np.random.default_rng(73).standard_normal(wl.n)
+    with ctx_for(wl) as c:
+        got = to_caller(c, c.matvec(c.to_local(torch.from_numpy(w).cuda())))
+        lam, rep = c.solve(c.to_local(torch.from_numpy(wl.f).cuda()), rtol=1e-12, max_iters=2000)
+        lam = to_caller(c, lam)
+    assert rel(got, O.matvec_brute(xy, w, sigma, wl.rc)) <= 1e-12
+    ref = O.solve(wl.xy, wl.f, sigma, wl.rc, wl.box, wl.cell, rtol=1e-12, max_iters=2000)
+    assert rep.converged == ref.converged
+    if ref.converged:
+        assert abs(rep.iterations - ref.iterations) <= max(2, ref.iterations // 50)
+        assert rel(lam, ref.x) <= 1e-8
