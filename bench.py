@@ -51,6 +51,21 @@ def ncu_traffic(kernel_prefix: str):
     return None
 
 
+def ncu_fp64(kernel_prefix: str):
+    """Executed FP64 fractions of a kernel from the committed ncu capture: ALU flops
+    (dadd + dmul + 2 dfma thread instructions) over the DFMA peak, and the fp64 tensor
+    pipe's % of peak (profiles/r01_ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+            d = json.load(f)["fp64_executed"]
+        for k, v in d.items():
+            if k == kernel_prefix or k.startswith(kernel_prefix + "<"):
+                return v
+    except Exception:
+        pass
+    return None
+
+
 def setup_flops(wl) -> float:
     """Algorithmic flops of the RASM setup: per subdomain with n = |Omega_c|,
     n1 = |own(c)|, n0 = n - n1: Cholesky n^3/3, W = L21 L11^-1 n1 n0^2, S^-1 n1^3,
@@ -292,9 +307,11 @@ def run_ours(args, rank, world):
     # every hot kernel against its own roof (the contract's `roofline` is the dominant one)
     rasm_ms = statistics.mean(sd["rasm"] for sd in setups)
     sflops = setup_flops(wl) / world if wl.overlap_width == 0.0 else None
+    ex_mv, ex_su = ncu_fp64("k_matvec"), ncu_fp64("k_rasm_setup_tc")
     roof_all = [
         {"kernel": "k_matvec", "bound": "alu", "achieved": mv_tflops, "peak": FP64_PEAK_TFLOPS,
          "unit": "TFLOP/s", "frac": mv_tflops / FP64_PEAK_TFLOPS, "ms_per_launch": mv_per_launch_ms,
+         "executed_frac_ncu": ex_mv["fp64_alu_frac_of_peak"] if ex_mv and args.config == 2 else None,
          "traffic_note": "DRAM traffic is the neighbour list (4 B per union entry, streamed once per "
                          "launch); the kernel is bound by the FP64 pipe and the L1 gathers"},
         {"kernel": "k_rasm_apply", "bound": "hbm", "achieved": pc_gbs, "peak": hbm_peak, "unit": "GB/s",
@@ -303,6 +320,7 @@ def run_ours(args, rank, world):
          if sflops else None, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
          "frac": sflops / (rasm_ms * 1e-3) / 1e12 / DMMA_PEAK_TFLOPS if sflops else None,
          "ms_per_launch": rasm_ms, "alg_flops_per_launch": sflops,
+         "executed_frac_ncu": ex_su["fp64_tensor_pct_of_peak"] / 100 if ex_su and args.config == 2 else None,
          "flops_model": "per subdomain n^3/3 + n1 n0^2 + n1^3 + 2 n1^2 n0 (Cholesky, W, S^-1, X)"},
     ]
     gpairs = n_pairs_local / (mv_ms * 1e-3) / 1e9
