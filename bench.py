@@ -253,6 +253,7 @@ def run_ours(args, rank, world):
     c = P.Context(xy, wl.sigma, wl.cell, wl.rc, wl.rings, wl.box, **kw)
     info = c.info()
     n_pairs_local = c.count_pairs()
+    mstats = c.matvec_stats()  # executed (target, entry) slots vs in-cutoff pairs
     w = torch.randn(c.n_local, dtype=torch.float64, device="cuda")
     y = torch.empty_like(w)
 
@@ -415,6 +416,7 @@ def run_ours(args, rank, world):
                         - statistics.mean(sd["total"] for sd in setups),
             "matvec_gpairs_s": gpairs,
             "matvec_ms": mv_ms, "rasm_apply_ms": pc_ms,
+            "matvec_slots_per_pair": 2.0 * mstats["ell_entries"] / max(n_pairs_local, 1),
             "matvec_fp64_frac_useful": gpairs * 1e9 * FLOP_PER_PAIR / (FP64_PEAK_TFLOPS * 1e12),
             "rasm_apply_gbs": pc_alg_bytes / (pc_ms * 1e-3) / 1e9,
             "step_ms": [round(x, 3) for x in ms],
