@@ -688,7 +688,9 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
 // cores (DMMA.8x8x4, U12 blocks in shared memory, L21 fragments in registers).  The back
 // substitution is blocked the same way.  One CTA per cell; A (n x lda, lda = n +
 // n_own) and PT live in a per-CTA slice of a global workspace (L2).
-constexpr int kLuThreads = 512;
+// threads per LU CTA: 512 (one cell per SM) for subdomains beyond kLuBigN points, else
+// 256 (two cells in flight per SM: the panel's barrier and L2 latency hide better)
+constexpr int kLuBigN = 600;
 constexpr int kLuNb = 32;     // panel width
 constexpr int kLuRows = 64;   // rows staged in shared memory per back-substitution pass
 constexpr int kLuCb = 64;     // trailing-update column block (U12 block in shared memory)
@@ -716,11 +718,14 @@ __device__ __forceinline__ void lu_argmax(double v, int i, double *red_v, int *r
   __syncthreads();
 }
 
-__global__ __launch_bounds__(kLuThreads, 1) void k_rasm_setup_lu(
-    Geom g, Strip st, const double2 *__restrict__ xy, const int *__restrict__ cell_start,
-    const long long *__restrict__ x_off, double *__restrict__ X, const int *__restrict__ glist,
-    int first, int count, double *__restrict__ ws, long long ws_stride, int *__restrict__ fail_key,
-    OvList ov) {
+// One cell of the LU path (the body of the persistent kernel below); A and PT live in
+// this CTA's workspace slice ws.
+template <int kLuThreads>
+__device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restrict__ xy,
+                                        const int *__restrict__ cell_start,
+                                        const long long *__restrict__ x_off, double *__restrict__ X,
+                                        const int cl, double *__restrict__ ws,
+                                        int *__restrict__ fail_key, OvList ov) {
   __shared__ Runs R;
   __shared__ double red_v[kLuThreads / 32];
   __shared__ int red_i[kLuThreads / 32];
@@ -730,8 +735,6 @@ __global__ __launch_bounds__(kLuThreads, 1) void k_rasm_setup_lu(
   __shared__ double prow[kLuNb];
   __shared__ double Ub[kLuNb][kLuCb + 1];  // U12 column block (B operand of the DMMA update)
   const int tid = threadIdx.x, T = blockDim.x;
-  if ((int)blockIdx.x >= count) return;
-  const int cl = glist[first + blockIdx.x];
   const int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
   if (tid == 0) sub_runs(g, cell_start, ov, cl, cx, cy, R);
   __syncthreads();
@@ -739,7 +742,7 @@ __global__ __launch_bounds__(kLuThreads, 1) void k_rasm_setup_lu(
   // right-hand sides: E_own (RASM), or the identity in natural order (ASM, reading Q26)
   const int nrhs = g.asm_full ? n : n_own;
   const long long lda = n + nrhs;
-  double *A = ws + (long long)blockIdx.x * ws_stride;  // n x lda row-major: [A_c | E]
+  double *A = ws;  // n x lda row-major: [A_c | E]
   double *PT = A + (long long)n * lda;                 // kLuNb x n: transposed panel
   double2 *pos = reinterpret_cast<double2 *>(A + (((long long)n * lda + (long long)kLuNb * n + 1) & ~1LL));
   for (int p = tid; p < n; p += T) {
@@ -944,6 +947,39 @@ __global__ __launch_bounds__(kLuThreads, 1) void k_rasm_setup_lu(
     }
     Xc[t] = v;
   }
+}
+
+// Persistent LU kernel: one CTA per SM takes the cells of glist (sorted largest first)
+// from an atomic counter, so the cell sizes (tens to thousands of points on clustered
+// data) balance over the SMs in ONE launch, and the workspace is one slice per CTA.
+template <int kLuThreads>
+__global__ __launch_bounds__(kLuThreads, 512 / kLuThreads) void k_rasm_setup_lu(
+    Geom g, Strip st, const double2 *__restrict__ xy, const int *__restrict__ cell_start,
+    const long long *__restrict__ x_off, double *__restrict__ X, const int *__restrict__ glist,
+    int count, double *__restrict__ ws, long long ws_stride, int *__restrict__ fail_key,
+    OvList ov, int *__restrict__ next) {
+  __shared__ int s_item;
+  double *slice = ws + (long long)blockIdx.x * ws_stride;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(next, 1);
+    __syncthreads();
+    const int item = s_item;
+    __syncthreads();
+    if (item >= count) break;
+    lu_cell<kLuThreads>(g, st, xy, cell_start, x_off, X, glist[item], slice, fail_key, ov);
+    __syncthreads();
+  }
+}
+
+// |Omega_c| of the LU cells (sort keys, largest first)
+__global__ void k_lu_sizes(Geom g, Strip st, const int *__restrict__ cell_start, const int *__restrict__ glist,
+                           int count, int *__restrict__ key, OvList ov) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const int cl = glist[i];
+  Runs R;
+  sub_runs(g, cell_start, ov, cl, cl % g.ncx, st.row_lo + cl / g.ncx, R);
+  key[i] = R.n_ov;
 }
 
 // z[own(c)] = X_c u[Omega_c]: one CTA per cell; u[Omega_c] gathered into shared
@@ -1226,19 +1262,40 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
     RBF_CUDA_TRY(cudaMemcpyAsync(fail, &hfail, sizeof(int), cudaMemcpyHostToDevice, s));
     const long long n = c->max_ov, no = c->max_own;
     const long long stride = (((n * (n + no) + (long long)kLuNb * n + 1) & ~1LL) + 2 * n + 1) & ~1LL;
-    const long long budget = 8LL << 30;  // bytes of workspace per batch
-    long long batch = budget / (stride * 8);
-    if (batch < 1) batch = 1;
-    if (batch > nglobal) batch = nglobal;
+    // largest subdomains first (longest-processing-time order for the work queue)
+    int *keys = nullptr, *skeys = nullptr, *sorted = nullptr, *next = cnt + 5;
+    RBF_TRY(dalloc(c, (void **)&keys, sizeof(int) * nglobal, s));
+    RBF_TRY(dalloc(c, (void **)&skeys, sizeof(int) * nglobal, s));
+    RBF_TRY(dalloc(c, (void **)&sorted, sizeof(int) * nglobal, s));
+    k_lu_sizes<<<(nglobal + 255) / 256, 256, 0, s>>>(c->g, c->s, c->cell_start, glist, nglobal, keys, ov);
+    size_t tb = 0;
+    RBF_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, keys, skeys, glist, sorted, nglobal, 0,
+                                                           32, s));
+    void *tmp = nullptr;
+    RBF_TRY(dalloc(c, &tmp, tb, s));
+    RBF_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(tmp, tb, keys, skeys, glist, sorted, nglobal, 0,
+                                                           32, s));
+    RBF_CUDA_TRY(cudaMemsetAsync(next, 0, sizeof(int), s));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const bool big = c->max_ov > kLuBigN;
+    const int per_sm = big ? 1 : 2;
+    const int grid = nglobal < sms * per_sm ? nglobal : sms * per_sm;
     double *ws = nullptr;
-    RBF_TRY(dalloc(c, (void **)&ws, sizeof(double) * (size_t)(stride * batch), s));
-    for (int first = 0; first < nglobal; first += (int)batch) {
-      int count = nglobal - first < batch ? nglobal - first : (int)batch;
-      k_rasm_setup_lu<<<count, kLuThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off,
-                                                   c->X, glist, first, count, ws, stride, fail, ov);
-      count_launch(1);
-      RBF_CUDA_TRY(cudaGetLastError());
-    }
+    RBF_TRY(dalloc(c, (void **)&ws, sizeof(double) * (size_t)(stride * grid), s));
+    if (big)
+      k_rasm_setup_lu<512><<<grid, 512, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off, c->X,
+                                                sorted, nglobal, ws, stride, fail, ov, next);
+    else
+      k_rasm_setup_lu<256><<<grid, 256, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off, c->X,
+                                                sorted, nglobal, ws, stride, fail, ov, next);
+    count_launch(2 + 4);  // sizes, sort, LU
+    RBF_CUDA_TRY(cudaGetLastError());
+    dfree(tmp, s);
+    dfree(keys, s);
+    dfree(skeys, s);
+    dfree(sorted, s);
     RBF_CUDA_TRY(cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
     RBF_CUDA_TRY(cudaStreamSynchronize(s));
     dfree(ws, s);
