@@ -268,6 +268,13 @@ int rbf_info(const rbf_ctx *ctx, int64_t out[8]);
  * out[3] = sum over lanes of the union-list lengths (entries without padding). */
 int rbf_matvec_stats(const rbf_ctx *ctx, int64_t out[4]);
 
+/* RASM setup facts (reading Q11): out[0] = subdomains solved by the global-memory LU
+ * path, out[1] = of those, the ones factored with partial pivoting (Cholesky breakdowns
+ * of the tensor-core pass, cells whose no-pivot factorisation met a non-positive pivot,
+ * and every remaining cell when the probe wave of largest cells needed pivoting in more
+ * than a quarter of cases).  EINVAL on NULL. */
+int rbf_lu_stats(const rbf_ctx *ctx, int64_t out[2]);
+
 /* Device time (ms, CUDA events) of rbf_setup's phases for this context:
  * out[0] = cell list, out[1] = positions + matvec neighbour list,
  * out[2] = RASM setup (assemble + factor + X), out[3] = whole rbf_setup. */

@@ -194,6 +194,13 @@ int rbf_info(const rbf_ctx *c, int64_t out[8]) {
   return RBF_OK;
 }
 
+int rbf_lu_stats(const rbf_ctx *c, int64_t out[2]) {
+  if (!c || !out) { set_error("NULL argument"); return RBF_EINVAL; }
+  out[0] = c->n_lu;
+  out[1] = c->n_lu_pivot;
+  return RBF_OK;
+}
+
 int rbf_matvec_stats(const rbf_ctx *c, int64_t out[4]) {
   if (!c || !out) { set_error("NULL argument"); return RBF_EINVAL; }
   out[0] = c->mv_lanes;

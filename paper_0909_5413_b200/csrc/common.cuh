@@ -222,6 +222,7 @@ struct rbf_ctx {
   long long *asm_poff = nullptr;  // ASM: CSR offsets of asm_map (n_loc + 1)
   long long x_count = 0;
   int max_ov = 0, max_own = 0, nsub = 0, n_lu = 0;
+  int n_lu_pivot = 0;          // LU-path subdomains that needed row exchanges
   int max_cell = 0;            // largest cell population (all cells of the ext range)
   // matvec: packed source records {x, y, w, 0} (ext range) and the neighbour list
   // (ELL of 32-bit entries in groups of 4, chunks of 32 consecutive owned targets)

@@ -19,6 +19,8 @@
 #include <cub/cub.cuh>
 #include <cstdlib>
 #include <type_traits>
+#include <vector>
+#include <algorithm>
 
 #include "common.cuh"
 
@@ -720,12 +722,16 @@ __device__ __forceinline__ void lu_argmax(double v, int i, double *red_v, int *r
 
 // One cell of the LU path (the body of the persistent kernel below); A and PT live in
 // this CTA's workspace slice ws.
-template <int kLuThreads>
+// PIV = false: no row exchanges -- LU of an SPD matrix needs none (it is Cholesky with
+// the diagonal kept in U); a pivot that is not positive sends the cell to the retry list
+// for the pivoting pass (reading Q11's fallback, unchanged).
+template <int kLuThreads, bool PIV>
 __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restrict__ xy,
                                         const int *__restrict__ cell_start,
                                         const long long *__restrict__ x_off, double *__restrict__ X,
                                         const int cl, double *__restrict__ ws,
-                                        int *__restrict__ fail_key, OvList ov) {
+                                        int *__restrict__ fail_key, OvList ov,
+                                        int *__restrict__ retry, int *__restrict__ nretry) {
   __shared__ Runs R;
   __shared__ double red_v[kLuThreads / 32];
   __shared__ int red_i[kLuThreads / 32];
@@ -776,6 +782,8 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
     __syncthreads();
     for (int c = 0; c < kb; ++c) {
       const int kk = k0 + c;
+      int p = kk;
+      if (PIV) {
       double best = -1.0;
       int bi = 0x7fffffff;
       for (int i = kk + tid; i < n; i += T) {
@@ -783,9 +791,10 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
         if (v > best) { best = v; bi = i; }
       }
       lu_argmax(best, bi, red_v, red_i, &s_piv);
-      const int p = s_piv;
+      p = s_piv;
       if (p < 0) { singular = true; break; }
-      if (p != kk) {  // swap rows kk and p: the panel copy and the rest of the augmented row
+      }
+      if (PIV && p != kk) {  // swap rows kk and p: the panel copy and the rest of the augmented row
         for (int cc = tid; cc < kb; cc += T) {
           const double t0 = PT[(long long)cc * n + kk];
           PT[(long long)cc * n + kk] = PT[(long long)cc * n + p];
@@ -801,6 +810,7 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
       __syncthreads();
       if (tid < kb) prow[tid] = PT[(long long)tid * n + kk];  // pivot row, panel part
       __syncthreads();
+      if (!PIV && !(prow[c] > 0.0)) { singular = true; break; }  // uniform: not SPD here
       const double inv = 1.0 / prow[c];
       for (int i = kk + 1 + tid; i < n; i += T) {
         const double l = PT[(long long)c * n + i] * inv;
@@ -815,9 +825,11 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
       const int c = (int)(t / (n - k0)), i = k0 + (int)(t - (long long)c * (n - k0));
       A[(long long)i * lda + k0 + c] = PT[(long long)c * n + i];
     }
-    for (int t = tid; t < kb * kb; t += T) {  // L11 (unit lower) to shared memory
-      const int r = t / kb, c = t - r * kb;
-      L11[r][c] = (c < r) ? PT[(long long)c * n + k0 + r] : 0.0;
+    // L11 (unit lower) to shared memory, zero beyond kb: the unrolled solves below run
+    // over all kLuNb rows and columns, and 0 * (stale shared memory) can be NaN
+    for (int t = tid; t < kLuNb * kLuNb; t += T) {
+      const int r = t / kLuNb, c = t - r * kLuNb;
+      L11[r][c] = (c < r && r < kb) ? PT[(long long)c * n + k0 + r] : 0.0;
     }
     __syncthreads();
     // ---- U12 = L11^-1 A12 (one column per thread, L11 in shared memory), then
@@ -869,7 +881,10 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
     }
   }
   if (singular) {
-    if (tid == 0) atomicMin(fail_key, cy * g.ncx + cx);
+    if (tid == 0) {
+      if (PIV) atomicMin(fail_key, cy * g.ncx + cx);
+      else retry[atomicAdd(nretry, 1)] = cl;  // to the pivoting pass
+    }
     return;
   }
   __syncthreads();
@@ -882,9 +897,9 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
   for (int r0 = ((n - 1) / kLuNb) * kLuNb; r0 >= 0; r0 -= kLuNb) {
     const int kb = n - r0 < kLuNb ? n - r0 : kLuNb;
     __syncthreads();
-    for (int t = tid; t < kb * kb; t += T) {  // U block (upper incl. diagonal)
-      const int r = t / kb, c = t - r * kb;
-      L11[r][c] = (c >= r) ? A[(long long)(r0 + r) * lda + r0 + c] : 0.0;
+    for (int t = tid; t < kLuNb * kLuNb; t += T) {  // U block (upper incl. diagonal), zero beyond kb
+      const int r = t / kLuNb, c = t - r * kLuNb;
+      L11[r][c] = (c >= r && c < kb) ? A[(long long)(r0 + r) * lda + r0 + c] : 0.0;
     }
     __syncthreads();
     if (tid < nc) {  // solve the diagonal block for this column
@@ -952,12 +967,12 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
 // Persistent LU kernel: one CTA per SM takes the cells of glist (sorted largest first)
 // from an atomic counter, so the cell sizes (tens to thousands of points on clustered
 // data) balance over the SMs in ONE launch, and the workspace is one slice per CTA.
-template <int kLuThreads>
+template <int kLuThreads, bool PIV>
 __global__ __launch_bounds__(kLuThreads, 512 / kLuThreads) void k_rasm_setup_lu(
     Geom g, Strip st, const double2 *__restrict__ xy, const int *__restrict__ cell_start,
     const long long *__restrict__ x_off, double *__restrict__ X, const int *__restrict__ glist,
     int count, double *__restrict__ ws, long long ws_stride, int *__restrict__ fail_key,
-    OvList ov, int *__restrict__ next) {
+    OvList ov, int *__restrict__ next, int *__restrict__ retry, int *__restrict__ nretry) {
   __shared__ int s_item;
   double *slice = ws + (long long)blockIdx.x * ws_stride;
   for (;;) {
@@ -966,20 +981,22 @@ __global__ __launch_bounds__(kLuThreads, 512 / kLuThreads) void k_rasm_setup_lu(
     const int item = s_item;
     __syncthreads();
     if (item >= count) break;
-    lu_cell<kLuThreads>(g, st, xy, cell_start, x_off, X, glist[item], slice, fail_key, ov);
+    lu_cell<kLuThreads, PIV>(g, st, xy, cell_start, x_off, X, glist[item], slice, fail_key, ov, retry, nretry);
     __syncthreads();
   }
 }
 
-// |Omega_c| of the LU cells (sort keys, largest first)
+// sort keys of the LU cells: |Omega_c|, plus kLuBreakdown for the cells whose Cholesky
+// broke down in the tensor-core pass (glist[n_nonfit:]), so those sort first
+constexpr int kLuBreakdown = 1 << 24;
 __global__ void k_lu_sizes(Geom g, Strip st, const int *__restrict__ cell_start, const int *__restrict__ glist,
-                           int count, int *__restrict__ key, OvList ov) {
+                           int count, int n_nonfit, int *__restrict__ key, OvList ov) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
   const int cl = glist[i];
   Runs R;
   sub_runs(g, cell_start, ov, cl, cl % g.ncx, st.row_lo + cl / g.ncx, R);
-  key[i] = R.n_ov;
+  key[i] = R.n_ov + (i >= n_nonfit ? kLuBreakdown : 0);
 }
 
 // z[own(c)] = X_c u[Omega_c]: one CTA per cell; u[Omega_c] gathered into shared
@@ -1240,6 +1257,7 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
   c->max_own = hc[1];
   c->nsub = hc[2];
   c->x_count = total;
+  const int n_nonfit = hc[3];  // cells routed to LU by size (before the Cholesky breakdowns)
   RBF_TRY(dalloc(c, (void **)&c->X, sizeof(double) * (size_t)(total > 0 ? total : 2), s));
   if (ncl > 0 && c->nsub > hc[3]) {
     const size_t smem = (size_t)hc[4];  // the largest per-cell layout of the tensor-core cells
@@ -1262,40 +1280,113 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
     RBF_CUDA_TRY(cudaMemcpyAsync(fail, &hfail, sizeof(int), cudaMemcpyHostToDevice, s));
     const long long n = c->max_ov, no = c->max_own;
     const long long stride = (((n * (n + no) + (long long)kLuNb * n + 1) & ~1LL) + 2 * n + 1) & ~1LL;
-    // largest subdomains first (longest-processing-time order for the work queue)
-    int *keys = nullptr, *skeys = nullptr, *sorted = nullptr, *next = cnt + 5;
+    // largest subdomains first (longest-processing-time order for the work queue), ties
+    // by cell index: glist's order comes from atomics, so it is sorted by cell first (the
+    // radix sort is stable) and the probe wave below is the same cells on every run
+    int *keys = nullptr, *skeys = nullptr, *sorted = nullptr, *keys2 = nullptr, *cells2 = nullptr;
+    int *next = cnt + 5;
     RBF_TRY(dalloc(c, (void **)&keys, sizeof(int) * nglobal, s));
     RBF_TRY(dalloc(c, (void **)&skeys, sizeof(int) * nglobal, s));
     RBF_TRY(dalloc(c, (void **)&sorted, sizeof(int) * nglobal, s));
-    k_lu_sizes<<<(nglobal + 255) / 256, 256, 0, s>>>(c->g, c->s, c->cell_start, glist, nglobal, keys, ov);
-    size_t tb = 0;
-    RBF_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, keys, skeys, glist, sorted, nglobal, 0,
+    RBF_TRY(dalloc(c, (void **)&keys2, sizeof(int) * nglobal, s));
+    RBF_TRY(dalloc(c, (void **)&cells2, sizeof(int) * nglobal, s));
+    k_lu_sizes<<<(nglobal + 255) / 256, 256, 0, s>>>(c->g, c->s, c->cell_start, glist, nglobal, n_nonfit,
+                                                      keys, ov);
+    size_t tb = 0, tb2 = 0;
+    RBF_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, glist, cells2, keys, keys2, nglobal, 0, 32, s));
+    RBF_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb2, keys2, skeys, cells2, sorted, nglobal, 0,
                                                            32, s));
+    tb = std::max(tb, tb2);
     void *tmp = nullptr;
     RBF_TRY(dalloc(c, &tmp, tb, s));
-    RBF_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(tmp, tb, keys, skeys, glist, sorted, nglobal, 0,
+    RBF_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tb, glist, cells2, keys, keys2, nglobal, 0, 32, s));
+    RBF_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(tmp, tb, keys2, skeys, cells2, sorted, nglobal, 0,
                                                            32, s));
-    RBF_CUDA_TRY(cudaMemsetAsync(next, 0, sizeof(int), s));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const bool big = c->max_ov > kLuBigN;
-    const int per_sm = big ? 1 : 2;
-    const int grid = nglobal < sms * per_sm ? nglobal : sms * per_sm;
+    // Cholesky breakdowns (numerically indefinite A_c, sorted first): partial pivoting
+    // right away.  The cells routed here by size: a pass without row exchanges (SPD
+    // subdomains), then the pivoting pass for those whose pivots were not all positive.
+    // Each pass: 512 threads one CTA per SM if its largest cell exceeds kLuBigN points,
+    // else 256 threads two per SM.
+    std::vector<int> hk(nglobal);
+    RBF_CUDA_TRY(cudaMemcpyAsync(hk.data(), skeys, sizeof(int) * nglobal, cudaMemcpyDeviceToHost, s));
+    RBF_CUDA_TRY(cudaStreamSynchronize(s));
+    int nbd = 0;
+    while (nbd < nglobal && hk[nbd] >= kLuBreakdown) ++nbd;
+    const int nsz = nglobal - nbd;
+    const long long n_bd = nbd > 0 ? hk[0] - kLuBreakdown : 0, n_sz = nsz > 0 ? hk[nbd] : 0;
+    auto stride_of = [&](long long nn) {
+      const long long oo = no < nn ? no : nn;  // rows of X_c <= |Omega_c|
+      return (((nn * (nn + oo) + (long long)kLuNb * nn + 1) & ~1LL) + 2 * nn + 1) & ~1LL;
+    };
+    auto grid_of = [&](long long nn, int cnt_) {
+      const int per_sm = nn > kLuBigN ? 1 : 2;
+      return cnt_ < per_sm * sms ? cnt_ : per_sm * sms;
+    };
+    const int probe = grid_of(n_sz, nsz), rest = nsz - probe;  // see the no-pivot probe below
+    const long long n_rest = rest > 0 ? hk[nbd + probe] : 0;
+    const long long wsz = std::max({stride_of(n_bd) * grid_of(n_bd, nbd), stride_of(n_sz) * grid_of(n_sz, nsz),
+                                    stride_of(n_rest) * grid_of(n_rest, rest)});
     double *ws = nullptr;
-    RBF_TRY(dalloc(c, (void **)&ws, sizeof(double) * (size_t)(stride * grid), s));
-    if (big)
-      k_rasm_setup_lu<512><<<grid, 512, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off, c->X,
-                                                sorted, nglobal, ws, stride, fail, ov, next);
-    else
-      k_rasm_setup_lu<256><<<grid, 256, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off, c->X,
-                                                sorted, nglobal, ws, stride, fail, ov, next);
-    count_launch(2 + 4);  // sizes, sort, LU
+    RBF_TRY(dalloc(c, (void **)&ws, sizeof(double) * (size_t)(wsz > 0 ? wsz : 1), s));
+    int *retry = keys, *nretry = cnt + 6;  // keys are free after the sort
+    auto pass = [&](bool piv, const int *list, int count, long long nn) -> int {
+      const int grid = grid_of(nn, count);
+      const long long st = stride_of(nn);
+      RBF_CUDA_TRY(cudaMemsetAsync(next, 0, sizeof(int), s));
+      if (nn > kLuBigN) {
+        if (piv) k_rasm_setup_lu<512, true><<<grid, 512, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off,
+                                                                c->X, list, count, ws, st, fail, ov, next,
+                                                                nullptr, nullptr);
+        else k_rasm_setup_lu<512, false><<<grid, 512, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off,
+                                                              c->X, list, count, ws, st, fail, ov, next, retry,
+                                                              nretry);
+      } else {
+        if (piv) k_rasm_setup_lu<256, true><<<grid, 256, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off,
+                                                                c->X, list, count, ws, st, fail, ov, next,
+                                                                nullptr, nullptr);
+        else k_rasm_setup_lu<256, false><<<grid, 256, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off,
+                                                              c->X, list, count, ws, st, fail, ov, next, retry,
+                                                              nretry);
+      }
+      count_launch(1);
+      RBF_CUDA_TRY(cudaGetLastError());
+      return RBF_OK;
+    };
+    if (nbd > 0) RBF_TRY(pass(true, sorted, nbd, n_bd));
+    const char *nopiv_env = getenv("RBF_LU_NOPIV");  // "0": pivot every LU cell (A/B knob)
+    const bool nopiv = !(nopiv_env && nopiv_env[0] == '0');
+    int hretry = 0;
+    bool rest_piv = false;
+    if (nsz > 0 && !nopiv) RBF_TRY(pass(true, sorted + nbd, nsz, n_sz));
+    if (nsz > 0 && nopiv) {
+      // probe: the largest cells, one wave, without pivoting.  If more than a quarter of
+      // them need pivoting the data is numerically indefinite at this size and the rest
+      // take the pivoting pass directly.  The decision depends only on the data, so the
+      // factors (and every result) are reproducible run to run.
+      RBF_CUDA_TRY(cudaMemsetAsync(nretry, 0, sizeof(int), s));
+      RBF_TRY(pass(false, sorted + nbd, probe, n_sz));
+      RBF_CUDA_TRY(cudaMemcpyAsync(&hretry, nretry, sizeof(int), cudaMemcpyDeviceToHost, s));
+      RBF_CUDA_TRY(cudaStreamSynchronize(s));
+      rest_piv = 4 * hretry > probe;
+      if (rest > 0) RBF_TRY(pass(rest_piv, sorted + nbd + probe, rest, n_rest));
+      if (rest > 0 && !rest_piv) {
+        RBF_CUDA_TRY(cudaMemcpyAsync(&hretry, nretry, sizeof(int), cudaMemcpyDeviceToHost, s));
+        RBF_CUDA_TRY(cudaStreamSynchronize(s));
+      }
+      if (hretry > 0) RBF_TRY(pass(true, retry, hretry, n_sz));
+    }
+    c->n_lu_pivot = nbd + (nopiv ? hretry + (rest_piv ? rest : 0) : nsz);  // cells factored with partial pivoting
+    count_launch(9);  // sizes, two sorts
     RBF_CUDA_TRY(cudaGetLastError());
     dfree(tmp, s);
     dfree(keys, s);
     dfree(skeys, s);
     dfree(sorted, s);
+    dfree(keys2, s);
+    dfree(cells2, s);
     RBF_CUDA_TRY(cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
     RBF_CUDA_TRY(cudaStreamSynchronize(s));
     dfree(ws, s);

@@ -57,7 +57,7 @@ EXPORTS = ["rbf_get_nccl_id", "rbf_setup", "rbf_local_count", "rbf_ext_count", "
            "rbf_rasm_apply", "rbf_matvec_ext", "rbf_rasm_apply_ext", "rbf_solve",
            "rbf_interpolate_host", "rbf_count_pairs", "rbf_dot", "rbf_plan_strips",
            "rbf_last_error", "rbf_destroy", "rbf_info", "rbf_launch_count", "rbf_setup_times",
-           "rbf_plan_halo", "rbf_evaluate", "rbf_matvec_stats"]
+           "rbf_plan_halo", "rbf_evaluate", "rbf_matvec_stats", "rbf_lu_stats"]
 
 _lib = None
 
@@ -90,6 +90,7 @@ def lib() -> C.CDLL:
             "rbf_count_pairs": (C.c_int, [p, p, p]),
             "rbf_evaluate": (C.c_int, [p, p, i64, p, p, p]),
             "rbf_matvec_stats": (C.c_int, [p, p]),
+            "rbf_lu_stats": (C.c_int, [p, p]),
             "rbf_dot": (C.c_int, [p, p, p, p, p]),
             "rbf_plan_strips": (C.c_int, [p, i64, i32, i64, p]),
             "rbf_last_error": (C.c_char_p, []),
@@ -319,6 +320,11 @@ class Context:
         o = (C.c_int64 * 4)()
         _check(lib().rbf_matvec_stats(self._h, o))
         return dict(zip(["lanes", "chunks", "ell_entries", "union_entries"], map(int, o)))
+
+    def lu_stats(self) -> dict:
+        o = (C.c_int64 * 2)()
+        _check(lib().rbf_lu_stats(self._h, o))
+        return {"n_lu": int(o[0]), "n_lu_pivot": int(o[1])}
 
     def count_pairs(self) -> int:
         v = C.c_int64()

@@ -84,20 +84,50 @@ def test_rasm_apply_parity(wl):
     assert rel(z, ref) <= 1e-10
 
 
+@pytest.mark.parametrize("pivot_all", [False, True], ids=["nopiv-pass", "pivot-all"])
 @pytest.mark.parametrize("rings,jit", [(2, 0.1), (3, 0.0)])
-def test_rasm_apply_parity_lu_path(rings, jit):
+def test_rasm_apply_parity_lu_path(rings, jit, pivot_all, monkeypatch):
     """Two and three rings of overlap: 625- and 1225-point subdomains exceed the
     shared-memory tensor-core kernel and take the blocked global-memory LU path
-    (reading Q11; partial pivoting, largest |a|, lowest row on ties)."""
+    (reading Q11).  The lattice subdomains are SPD: the no-pivot pass factors all of
+    them; RBF_LU_NOPIV=0 forces partial pivoting (largest |a|, lowest row on ties) on
+    every cell, so both factorisations are held to the oracle."""
+    if pivot_all:
+        monkeypatch.setenv("RBF_LU_NOPIV", "0")
     wl = W.make_lattice(48, jitter_frac=jit, seed=5)
     r = np.random.default_rng(21).standard_normal(wl.n)
     Pc = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, rings)
     ref = Pc.apply(r)
     Pc.close()
     with ctx_for(wl, rings=rings) as c:
-        assert c.info()["n_lu"] > 0
+        st = c.lu_stats()
+        assert st["n_lu"] == c.info()["n_lu"] > 0
+        assert st["n_lu_pivot"] == (st["n_lu"] if pivot_all else 0)
         z = to_caller(c, c.rasm_apply(c.to_local(torch.from_numpy(r).cuda())))
     assert rel(z, ref) <= 1e-10
+
+
+def test_lu_pivot_routing_clustered_reproducible(monkeypatch):
+    """Clustered data (reading Q8): most large subdomain matrices are numerically
+    indefinite, so the no-pivot probe wave fails in more than a quarter of cases and
+    the LU cells are factored with pivoting; the routing depends only on the data, so
+    two setups give bitwise-identical preconditioners.  With every cell pivoted the
+    preconditioner agrees to rounding (the cells the no-pivot pass did factor are SPD)."""
+    wl = W.make_clustered(20000, seed=5)
+    r = torch.from_numpy(np.random.default_rng(3).standard_normal(wl.n)).cuda()
+    outs = []
+    for _ in range(2):
+        with ctx_for(wl, rings=2) as c:
+            st = c.lu_stats()
+            assert 0 < st["n_lu_pivot"] < st["n_lu"]
+            outs.append(to_caller(c, c.rasm_apply(c.to_local(r))))
+    assert np.array_equal(outs[0], outs[1])
+    monkeypatch.setenv("RBF_LU_NOPIV", "0")
+    with ctx_for(wl, rings=2) as c:
+        st = c.lu_stats()
+        assert st["n_lu_pivot"] == st["n_lu"]
+        z = to_caller(c, c.rasm_apply(c.to_local(r)))
+    assert rel(outs[0], z) <= 1e-10  # measured 9e-14
 
 
 # ------------------------------------------------------------------ box overlap (Q24)
