@@ -275,6 +275,13 @@ int rbf_matvec_stats(const rbf_ctx *ctx, int64_t out[4]);
  * than a quarter of cases).  EINVAL on NULL. */
 int rbf_lu_stats(const rbf_ctx *ctx, int64_t out[2]);
 
+/* Test hook: fill the shared memory of every SM with 0xFF bytes (NaN in every double)
+ * on the current device and synchronise, so that a following kernel that reads shared
+ * memory it did not write produces NaN in the parity tests.  The environment variable
+ * RBF_POISON=1 does the same for every device buffer the library allocates.  Changes
+ * no library state.  ECUDA on a CUDA error. */
+int rbf_debug_poison_shared(void);
+
 /* Device time (ms, CUDA events) of rbf_setup's phases for this context:
  * out[0] = cell list, out[1] = positions + matvec neighbour list,
  * out[2] = RASM setup (assemble + factor + X), out[3] = whole rbf_setup. */

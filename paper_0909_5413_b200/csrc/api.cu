@@ -52,6 +52,10 @@ int dalloc(rbf_ctx *c, void **p, size_t bytes, cudaStream_t s) {
     set_error("device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
     return e == cudaErrorMemoryAllocation ? RBF_ENOMEM : RBF_ECUDA;
   }
+  // test hook: every new buffer filled with 0xFF bytes (a NaN in every double), so a
+  // kernel reading scratch it never wrote shows up in the parity tests
+  const char *poison = getenv("RBF_POISON");
+  if (poison && poison[0] == '1') cudaMemsetAsync(*p, 0xFF, bytes, s);
   if (c) c->bytes += (long long)bytes;
   return RBF_OK;
 }
@@ -174,6 +178,29 @@ int64_t rbf_launch_count(void) { return g_launches.load(); }
 
 /* debug: per-CTA clock64 phase stamps of the RASM setup kernel (RBF_PROBE builds) */
 int rbf_debug_probe(int64_t *out) { return rbf::probe_read((long long *)out); }
+
+namespace {
+__global__ void k_poison_shared(int words) {
+  extern __shared__ unsigned int sm_words[];
+  for (int i = threadIdx.x; i < words; i += blockDim.x) sm_words[i] = 0xFFFFFFFFu;
+  __syncthreads();
+  if (threadIdx.x == 0 && sm_words[words - 1] != 0xFFFFFFFFu) __trap();  // keep the stores
+}
+}  // namespace
+
+int rbf_debug_poison_shared(void) {
+  int dev = 0, sms = 0, optin = 0;
+  RBF_CUDA_TRY(cudaGetDevice(&dev));
+  RBF_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  RBF_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  RBF_CUDA_TRY(cudaFuncSetAttribute(k_poison_shared, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  // one CTA with all the shared memory a block can hold per SM, several waves
+  k_poison_shared<<<4 * sms, 1024, optin>>>(optin / 4);
+  count_launch(1);
+  RBF_CUDA_TRY(cudaGetLastError());
+  RBF_CUDA_TRY(cudaDeviceSynchronize());
+  return RBF_OK;
+}
 
 int rbf_setup_times(const rbf_ctx *c, double out[4]) {
   if (!c || !out) { set_error("NULL argument"); return RBF_EINVAL; }

@@ -57,7 +57,8 @@ EXPORTS = ["rbf_get_nccl_id", "rbf_setup", "rbf_local_count", "rbf_ext_count", "
            "rbf_rasm_apply", "rbf_matvec_ext", "rbf_rasm_apply_ext", "rbf_solve",
            "rbf_interpolate_host", "rbf_count_pairs", "rbf_dot", "rbf_plan_strips",
            "rbf_last_error", "rbf_destroy", "rbf_info", "rbf_launch_count", "rbf_setup_times",
-           "rbf_plan_halo", "rbf_evaluate", "rbf_matvec_stats", "rbf_lu_stats"]
+           "rbf_plan_halo", "rbf_evaluate", "rbf_matvec_stats", "rbf_lu_stats",
+           "rbf_debug_poison_shared"]
 
 _lib = None
 
@@ -91,6 +92,7 @@ def lib() -> C.CDLL:
             "rbf_evaluate": (C.c_int, [p, p, i64, p, p, p]),
             "rbf_matvec_stats": (C.c_int, [p, p]),
             "rbf_lu_stats": (C.c_int, [p, p]),
+            "rbf_debug_poison_shared": (C.c_int, []),
             "rbf_dot": (C.c_int, [p, p, p, p, p]),
             "rbf_plan_strips": (C.c_int, [p, i64, i32, i64, p]),
             "rbf_last_error": (C.c_char_p, []),
@@ -132,6 +134,11 @@ def make_params(sigma, cell, rc, rings=1, box=(-1.0, -1.0, 1.0, 1.0), overlap_wi
                 trunc_width=0.0, schwarz="rasm") -> Params:
     return Params(float(sigma), float(cell), float(rc), int(rings), SCHWARZ[schwarz],
                   *map(float, box), float(overlap_width), float(trunc_width))
+
+
+def poison_shared() -> None:
+    """Test hook: NaN-fill every SM's shared memory (rbf_debug_poison_shared)."""
+    _check(lib().rbf_debug_poison_shared())
 
 
 def launch_count() -> int:
