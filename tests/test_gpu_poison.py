@@ -94,3 +94,75 @@ def test_solve_poisoned(orth):
     assert abs(rep.iterations - ref.iterations) <= 2
     assert rep.resid_true <= 1e-10
     assert rel(lam, ref.x) <= 1e-8
+
+
+@pytest.mark.parametrize("tbox", [False, True], ids=["rc", "tbox"])
+def test_matvec_and_evaluate_poisoned(tbox):
+    wl = W.make_lattice(37, jitter_frac=0.3, seed=3)
+    tau = 5.0 * wl.sigma
+    rng = np.random.default_rng(44)
+    w = rng.standard_normal(wl.n)
+    q = np.column_stack([rng.uniform(-1, 1, 600), rng.uniform(-1, 1, 600)])
+    if tbox:
+        ref_y = O.matvec_tbox(wl.xy, w, wl.sigma, wl.box, wl.cell, tau)
+        ref_s = O.evaluate_tbox(q, wl.xy, w, wl.sigma, wl.box, wl.cell, tau)
+    else:
+        ref_y = O.matvec_brute(wl.xy, w, wl.sigma, wl.rc)
+        ref_s = O.evaluate(q, wl.xy, w, wl.sigma, wl.rc)
+    with ctx_for(wl, rings=0, trunc_width=tau if tbox else 0.0) as c:
+        wl_ = c.to_local(torch.from_numpy(w).cuda())
+        P.poison_shared()
+        y = to_caller(c, c.matvec(wl_))
+        P.poison_shared()
+        s = c.evaluate(torch.from_numpy(q).cuda(), wl_).cpu().numpy()
+    assert rel(y, ref_y) <= 1e-12
+    assert rel(s, ref_s) <= 1e-12
+
+
+@pytest.mark.parametrize("orth", ["mgs", "dcgs2"])
+def test_threads_strips_solve_poisoned(orth):
+    """The multi-strip path (halo plans and exchange, rank-ordered reductions) on the
+    in-process transport, every buffer NaN-filled, against the single-strip solve."""
+    import os
+    import threading
+
+    wl = W.make_lattice(60, jitter_frac=0.1, seed=5)
+    xy = torch.from_numpy(wl.xy).cuda()
+    f = torch.from_numpy(wl.f).cuda()
+    with ctx_for(wl) as c1:
+        lam1, rep1 = c1.solve(c1.to_local(f), rtol=1e-13, orth=orth)
+        lam1 = c1.from_local(lam1).cpu().numpy()
+    nranks, key = 2, os.urandom(128)
+    out, err = [None] * nranks, [None] * nranks
+
+    def run(r):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                with P.Context(xy, wl.sigma, wl.cell, wl.rc, 1, wl.box, rank=r, nranks=nranks,
+                               comm="threads", nccl_id=key, stream=st) as c:
+                    lam, rep = c.solve(c.to_local(f), rtol=1e-13, orth=orth)
+                    out[r] = (c.from_local(lam).cpu().numpy(), rep)
+            st.synchronize()
+        except BaseException as e:  # noqa: BLE001 - reported below
+            err[r] = e
+
+    P.poison_shared()
+    ths = [threading.Thread(target=run, args=(r,), daemon=True) for r in range(nranks)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(300)
+    assert not any(t.is_alive() for t in ths)
+    for e in err:
+        if e is not None:
+            raise e
+    assert rep1.converged
+    assert len({o[1].iterations for o in out}) == 1
+    for lam, rep in out:
+        assert rep.converged and abs(rep.iterations - rep1.iterations) <= 1
+        assert rep.resid_true <= 1e-10
+        assert np.all(np.isfinite(lam))
+    # the strips' owned entries, summed over ranks, are the single-strip solution
+    got = sum(o[0] for o in out)
+    assert rel(got, lam1) <= 1e-8
