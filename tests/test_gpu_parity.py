@@ -706,6 +706,44 @@ def test_cfg5_matvec_sampled_rows():
     assert npairs == O.count_pairs(wl.xy, wl.rc, wl.box, wl.cell)
 
 
+def test_cfg5_bench_config_sampled_cells_and_solve():
+    """cfg5 in the bench's configuration (one ring of overlap, MGS): RASM local solves
+    of sampled cells in the uniform outer region against the oracle's dense solves;
+    the solve (which does not converge, reading Q8 -- parity unpinned) checked through
+    properties that hold at any size: finite history, residual estimates non-increasing
+    within each GMRES(30) cycle (|g_k+1| = |s_k| |g_k|), and the residual f - A lambda of
+    the GPU's weights on sampled rows equal to the oracle's rows of A_rc lambda."""
+    wl = W.config(5)
+    cl = O.cell_list(wl.xy, wl.box, wl.cell)
+    key, perm, start = cl
+    ncx, ncy = O.grid_dims(wl.box, wl.cell)
+    rng = np.random.default_rng(21)
+    r = rng.standard_normal(wl.n)
+    x0, y0 = wl.box[0], wl.box[1]
+    cxs, cys = np.meshgrid(np.arange(ncx), np.arange(ncy))
+    ctr = np.hypot(x0 + (cxs.ravel() + 0.5) * wl.cell, y0 + (cys.ravel() + 0.5) * wl.cell)
+    outer = np.nonzero((ctr > 0.7) & (np.diff(start) > 0))[0]
+    cells = [0, ncx - 1, ncx * ncy - 1] + list(rng.choice(outer, 9, replace=False))
+    with ctx_for(wl) as c:
+        z = to_caller(c, c.rasm_apply(c.to_local(torch.from_numpy(r).cuda())))
+        for cc in cells:
+            own, ref = oracle_cell_solve(wl, r, int(cc), cl)
+            assert rel(z[own], ref) <= 1e-10, cc
+        f = torch.from_numpy(wl.f).cuda()
+        lam_loc, rep = c.solve(c.to_local(f), rtol=wl.tol)
+        y = to_caller(c, c.matvec(lam_loc))
+        lam = to_caller(c, lam_loc)
+    h = rep.history
+    assert len(h) == rep.iterations > 0 and np.all(np.isfinite(h)) and np.isfinite(rep.resid_true)
+    for s0 in range(0, len(h), 30):
+        seg = h[s0:s0 + 30]
+        assert np.all(seg[1:] <= seg[:-1] * (1 + 1e-12))
+    rows = np.concatenate([perm[start[int(np.argmax(np.diff(start)))]:][:20], rng.choice(wl.n, 150, replace=False)])
+    ref_rows = oracle_rows(wl, lam, rows, cl)
+    assert rel(y[rows], ref_rows) <= 1e-12
+    assert abs(rep.resid_true - np.linalg.norm(wl.f - y) / np.linalg.norm(wl.f)) <= 1e-6 * rep.resid_true
+
+
 # ------------------------------------------------------------------ interpolant evaluation (§8.f1)
 
 @pytest.mark.parametrize("wl", SMALL[:3] + [SMALL[4]], ids=IDS[:3] + [IDS[4]])
