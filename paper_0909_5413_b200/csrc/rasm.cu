@@ -731,7 +731,8 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
                                         const long long *__restrict__ x_off, double *__restrict__ X,
                                         const int cl, double *__restrict__ ws,
                                         int *__restrict__ fail_key, OvList ov,
-                                        int *__restrict__ retry, int *__restrict__ nretry) {
+                                        int *__restrict__ retry, int *__restrict__ nretry,
+                                        double *pt_sm) {
   __shared__ Runs R;
   __shared__ double red_v[kLuThreads / 32];
   __shared__ int red_i[kLuThreads / 32];
@@ -749,7 +750,8 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
   const int nrhs = g.asm_full ? n : n_own;
   const long long lda = n + nrhs;
   double *A = ws;  // n x lda row-major: [A_c | E]
-  double *PT = A + (long long)n * lda;                 // kLuNb x n: transposed panel
+  // kLuNb x n: transposed panel, in dynamic shared memory when the launch gave it room
+  double *PT = pt_sm ? pt_sm : A + (long long)n * lda;
   double2 *pos = reinterpret_cast<double2 *>(A + (((long long)n * lda + (long long)kLuNb * n + 1) & ~1LL));
   for (int p = tid; p < n; p += T) {
     const int q = (p < n0) ? (p < own_nat ? p : p + n_own) : own_nat + (p - n0);
@@ -972,7 +974,8 @@ __global__ __launch_bounds__(kLuThreads, 512 / kLuThreads) void k_rasm_setup_lu(
     Geom g, Strip st, const double2 *__restrict__ xy, const int *__restrict__ cell_start,
     const long long *__restrict__ x_off, double *__restrict__ X, const int *__restrict__ glist,
     int count, double *__restrict__ ws, long long ws_stride, int *__restrict__ fail_key,
-    OvList ov, int *__restrict__ next, int *__restrict__ retry, int *__restrict__ nretry) {
+    OvList ov, int *__restrict__ next, int *__restrict__ retry, int *__restrict__ nretry, int pt_smem) {
+  extern __shared__ double lu_dyn[];
   __shared__ int s_item;
   double *slice = ws + (long long)blockIdx.x * ws_stride;
   for (;;) {
@@ -981,7 +984,8 @@ __global__ __launch_bounds__(kLuThreads, 512 / kLuThreads) void k_rasm_setup_lu(
     const int item = s_item;
     __syncthreads();
     if (item >= count) break;
-    lu_cell<kLuThreads, PIV>(g, st, xy, cell_start, x_off, X, glist[item], slice, fail_key, ov, retry, nretry);
+    lu_cell<kLuThreads, PIV>(g, st, xy, cell_start, x_off, X, glist[item], slice, fail_key, ov, retry, nretry,
+                             pt_smem ? lu_dyn : nullptr);
     __syncthreads();
   }
 }
@@ -1332,28 +1336,41 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
     double *ws = nullptr;
     RBF_TRY(dalloc(c, (void **)&ws, sizeof(double) * (size_t)(wsz > 0 ? wsz : 1), s));
     int *retry = keys, *nretry = cnt + 6;  // keys are free after the sort
-    auto pass = [&](bool piv, const int *list, int count, long long nn) -> int {
-      const int grid = grid_of(nn, count);
-      const long long st = stride_of(nn);
-      RBF_CUDA_TRY(cudaMemsetAsync(next, 0, sizeof(int), s));
-      if (nn > kLuBigN) {
-        if (piv) k_rasm_setup_lu<512, true><<<grid, 512, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off,
-                                                                c->X, list, count, ws, st, fail, ov, next,
-                                                                nullptr, nullptr);
-        else k_rasm_setup_lu<512, false><<<grid, 512, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off,
-                                                              c->X, list, count, ws, st, fail, ov, next, retry,
-                                                              nretry);
-      } else {
-        if (piv) k_rasm_setup_lu<256, true><<<grid, 256, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off,
-                                                                c->X, list, count, ws, st, fail, ov, next,
-                                                                nullptr, nullptr);
-        else k_rasm_setup_lu<256, false><<<grid, 256, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off,
-                                                              c->X, list, count, ws, st, fail, ov, next, retry,
-                                                              nretry);
+    // the transposed panel (kLuNb x n, re-read and re-written once per panel column) in
+    // dynamic shared memory whenever that keeps the CTAs per SM of the global-memory
+    // layout; RBF_LU_SMEM=0 keeps it in the workspace (A/B knob)
+    const char *sm_env = getenv("RBF_LU_SMEM");
+    const bool sm_panel = !(sm_env && sm_env[0] == '0');
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    auto launch = [&](auto kern, int threads, bool with_retry, const int *list, int count, long long nn) -> int {
+      int grid = grid_of(nn, count);
+      size_t dyn = 0;
+      if (sm_panel) {
+        const size_t need = sizeof(double) * kLuNb * (size_t)nn;
+        cudaFuncAttributes fa;
+        RBF_CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
+        if (need + fa.sharedSizeBytes <= (size_t)optin) {
+          RBF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+          int occ = 0;
+          RBF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, need));
+          if (occ >= (nn > kLuBigN ? 1 : 2)) dyn = need;
+        }
       }
+      RBF_CUDA_TRY(cudaMemsetAsync(next, 0, sizeof(int), s));
+      kern<<<grid, threads, dyn, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off, c->X, list, count, ws,
+                                      stride_of(nn), fail, ov, next, with_retry ? retry : nullptr,
+                                      with_retry ? nretry : nullptr, dyn > 0);
       count_launch(1);
       RBF_CUDA_TRY(cudaGetLastError());
       return RBF_OK;
+    };
+    auto pass = [&](bool piv, const int *list, int count, long long nn) -> int {
+      if (nn > kLuBigN)
+        return piv ? launch(k_rasm_setup_lu<512, true>, 512, false, list, count, nn)
+                   : launch(k_rasm_setup_lu<512, false>, 512, true, list, count, nn);
+      return piv ? launch(k_rasm_setup_lu<256, true>, 256, false, list, count, nn)
+                 : launch(k_rasm_setup_lu<256, false>, 256, true, list, count, nn);
     };
     if (nbd > 0) RBF_TRY(pass(true, sorted, nbd, n_bd));
     const char *nopiv_env = getenv("RBF_LU_NOPIV");  // "0": pivot every LU cell (A/B knob)
