@@ -737,10 +737,15 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
   __shared__ double red_v[kLuThreads / 32];
   __shared__ int red_i[kLuThreads / 32];
   __shared__ int s_piv;
-  __shared__ double Ls[kLuRows][kLuNb + 1];  // staged L21 / U rows (+1: no bank conflicts)
+  // Ls (back substitution) and Ub (trailing update) are never live together: one buffer,
+  // so that the shared-memory panel leaves room for two CTAs per SM on larger cells
+  constexpr int kLsUb = (kLuRows * (kLuNb + 1) > kLuNb * (kLuCb + 1)) ? kLuRows * (kLuNb + 1)
+                                                                        : kLuNb * (kLuCb + 1);
+  __shared__ double LsUb[kLsUb];
+  double (*Ls)[kLuNb + 1] = reinterpret_cast<double (*)[kLuNb + 1]>(LsUb);  // staged U rows
+  double (*Ub)[kLuCb + 1] = reinterpret_cast<double (*)[kLuCb + 1]>(LsUb);  // U12 column block
   __shared__ double L11[kLuNb][kLuNb + 1];
   __shared__ double prow[kLuNb];
-  __shared__ double Ub[kLuNb][kLuCb + 1];  // U12 column block (B operand of the DMMA update)
   const int tid = threadIdx.x, T = blockDim.x;
   const int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
   if (tid == 0) sub_runs(g, cell_start, ov, cl, cx, cy, R);
