@@ -692,7 +692,7 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
 // n_own) and PT live in a per-CTA slice of a global workspace (L2).
 // threads per LU CTA: 512 (one cell per SM) for subdomains beyond kLuBigN points, else
 // 256 (two cells in flight per SM: the panel's barrier and L2 latency hide better)
-constexpr int kLuBigN = 600;
+constexpr int kLuBigN = 330;
 constexpr int kLuNb = 32;     // panel width
 constexpr int kLuRows = 64;   // rows staged in shared memory per back-substitution pass
 constexpr int kLuCb = 64;     // trailing-update column block (U12 block in shared memory)
