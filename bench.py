@@ -1,17 +1,21 @@
 #!/usr/bin/env python
 """Benchmark of the PetRBF hot path on B200 (contract: README/DESIGN.md "Bench").
 
-One step = one full interpolation solve of BASELINE.json configs[1] (cfg2: 1,048,576
-jittered lattice points, h/sigma = 0.8, rc = 6 sigma, cell = 4 sigma, GMRES(30) +
-RASM, tol 1e-13): rbf_setup (cell list + RASM setup) + rbf_solve, inputs resident in
-HBM.  metric/unit follow BASELINE.json: solve time (s, lower is better) plus the
-matvec Gpairs/s and the FP64-peak fractions.
+One step = one full interpolation solve of the largest single-GPU configuration in
+BASELINE.json: configs[3], cfg4 (the paper-scale case north_star's strong scaling is
+quoted on: 7072^2 = 50,013,184 lattice points, h/sigma = 0.8, rc = 6 sigma, cell =
+4 sigma, GMRES(30) + RASM, tol 1e-15): rbf_setup (cell list + RASM setup) +
+rbf_solve, inputs resident in HBM.  metric/unit follow BASELINE.json: solve time (s,
+lower is better) plus the matvec Gpairs/s and the FP64-peak fractions.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl reference]
 
-Multi-GPU: launched by torchrun, one rank per GPU; strips of cell rows with NCCL
-halos/all-gathers (strong scaling: total work fixed).  --impl reference times the
-oracle (plain C, host cores) on a bounded sample of the same workload.
+Multi-GPU: one rank per GPU (torchrun; `--gpus N` without a torchrun environment
+re-launches itself under torch.distributed.run with N ranks), strips of cell rows with
+NCCL halos/all-gathers (strong scaling: total work fixed).  --impl reference times the
+oracle (plain C, host cores): its matvec on the full workload, its RASM setup and
+per-iteration preconditioner + orthogonalisation cost on a bounded sample of the same
+recipe scaled per point.
 """
 from __future__ import annotations
 
@@ -34,36 +38,35 @@ METRIC = "fp64 GMRES+RASM solve time and matvec Gpairs/s at 1/2/4/8 B200, % FP64
 FP64_PEAK_TFLOPS = 36.86  # measured DFMA peak on this pool's B200 (profiles/r01_fp64_peak.json, tools/clock_under_load.cu)
 FLOP_PER_PAIR = 38        # algorithmic flops per in-cutoff pair
 DMMA_PEAK_TFLOPS = 37.13  # measured fp64 tensor-core (DMMA) peak, profiles/r01_fp64_peak.json
-SAMPLE_SIDE = 256         # oracle sample: 256^2 points of the same recipe
+SAMPLE_SIDE = 512         # oracle sample: 512^2 points of the same recipe
 
 
-def ncu_traffic(kernel_prefix: str):
-    """DRAM bytes per launch of a kernel from the committed ncu --set full capture
-    (profiles/r01_ncu_traffic.json), or None."""
+def _ncu_entry(kernel_prefix: str, workload: str):
+    """The committed ncu --set full summary of one kernel on one workload
+    (profiles/ncu_traffic.json: {workload: {kernel: {...}}}), or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
-            d = json.load(f)["bytes_per_launch"]
-        for k, v in d.items():
-            if k == kernel_prefix or k.startswith(kernel_prefix + "<"):
-                return float(v)
-    except Exception:
-        pass
-    return None
-
-
-def ncu_fp64(kernel_prefix: str):
-    """Executed FP64 fractions of a kernel from the committed ncu capture: ALU flops
-    (dadd + dmul + 2 dfma thread instructions) over the DFMA peak, and the fp64 tensor
-    pipe's % of peak (profiles/r01_ncu_traffic.json), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
-            d = json.load(f)["fp64_executed"]
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)[workload]
         for k, v in d.items():
             if k == kernel_prefix or k.startswith(kernel_prefix + "<"):
                 return v
     except Exception:
         pass
     return None
+
+
+def ncu_traffic(kernel_prefix: str, workload: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch, or None."""
+    e = _ncu_entry(kernel_prefix, workload)
+    return float(e["dram_bytes_per_launch"]) if e and "dram_bytes_per_launch" in e else None
+
+
+def ncu_fp64(kernel_prefix: str, workload: str, key: str, scale: float = 1.0):
+    """Executed FP64 fraction from the same capture: ALU flops (dadd + dmul + 2 dfma)
+    over the DFMA peak ('fp64_alu_frac_of_peak') or the fp64 tensor pipe's % of peak
+    ('fp64_tensor_pct_of_peak'), or None."""
+    e = _ncu_entry(kernel_prefix, workload)
+    return float(e[key]) * scale if e and key in e else None
 
 
 def setup_flops(wl) -> float:
@@ -130,47 +133,87 @@ class Clocks:
 
 
 # --------------------------------------------------------------------------- reference arm
-def oracle_sample(cfg: int):
-    """The oracle on a bounded sample of the workload: the same recipe on a
-    SAMPLE_SIDE^2 lattice (same h/sigma, cell/sigma, rc/sigma, jitter, rhs)."""
+def sample_workload(cfg: int, full):
+    """A bounded sample of the same recipe: SAMPLE_SIDE^2 points with the same h/sigma,
+    cell/sigma, rc/sigma, jitter/rhs kind and tolerance (cfg5: the clustered recipe at
+    SAMPLE_SIDE^2 points)."""
+    n = SAMPLE_SIDE
+    if cfg == 1:
+        return full
+    if cfg == 2:
+        return W.make_lattice(n, jitter_frac=0.1, seed=2, rhs="gauss", s2=0.02, tol=full.tol)
+    if cfg == 3:
+        return W.make_lattice(n, seed=3, rhs="blobs", tol=full.tol)
+    if cfg == 5:
+        return W.make_clustered(n * n, seed=5, tol=full.tol)
+    return W.make_lattice(n, rhs="gauss", s2=0.02, tol=full.tol)
+
+
+def oracle_estimate(cfg: int, full=None):
+    """The oracle (plain C + OpenMP on the host cores, as it stands) timed on this
+    workload.  cfg1: the whole solve.  Larger configs (the oracle's RASM blocks for cfg4
+    need 90 GB of host RAM): the oracle's matvec is timed on the FULL
+    workload; the RASM setup and the per-iteration preconditioner apply +
+    orthogonalisation are timed in a full oracle solve of a SAMPLE_SIDE^2 sample of the
+    same recipe and scaled by the point count (both are O(N): per-cell work is the same,
+    P:322, 465); the iteration count is the sample's (mesh-independent at fixed h/sigma,
+    P:346).  Returns (seconds, description)."""
     import oracle as O
 
-    full = W.config(cfg)
-    if cfg == 2:
-        wl = W.make_lattice(SAMPLE_SIDE, jitter_frac=0.1, seed=2, rhs="gauss", s2=0.02)
-    elif cfg == 1:
-        wl = full
-    else:
-        wl = W.make_lattice(SAMPLE_SIDE, rhs="gauss", s2=0.02)
+    full = full or W.config(cfg)
+    wl = sample_workload(cfg, full)
     t0 = time.perf_counter()
-    res = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, rtol=full.tol)
-    dt = time.perf_counter() - t0
-    scale = full.n / wl.n  # O(N) time per solve (P:322, 465)
-    return dt, scale, res, wl, full
+    P = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, wl.rings, wl.overlap_width)
+    t_su = time.perf_counter() - t0
+    opA = O.op_rbf(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell)
+    t0 = time.perf_counter()
+    res = O.gmres(opA, O.op_rasm(P), wl.f, rtol=full.tol)
+    t_sol = time.perf_counter() - t0
+    w_s = np.random.default_rng(0).standard_normal(wl.n)
+    t0 = time.perf_counter()
+    O.matvec_cells(wl.xy, w_s, wl.sigma, wl.rc, wl.box, wl.cell)
+    t_mv_s = time.perf_counter() - t0
+    P.close()
+    n_mv = res.iterations + res.restarts + 1   # one per iteration, per restart residual, final check
+    if wl is full:
+        return t_su + t_sol, (f"oracle setup + solve of {full.name} itself ({full.n} points, "
+                              f"{res.iterations} it): setup {t_su:.2f} s, solve {t_sol:.2f} s")
+    w = np.random.default_rng(0).standard_normal(full.n)
+    t0 = time.perf_counter()
+    O.matvec_cells(full.xy, w, full.sigma, full.rc, full.box, full.cell)
+    t_mv = time.perf_counter() - t0
+    scale = full.n / wl.n
+    rest = max(t_sol - n_mv * t_mv_s, 0.0) / max(res.iterations, 1)  # PC apply + orth per iteration
+    est = t_su * scale + n_mv * t_mv + res.iterations * rest * scale
+    desc = (f"matvec timed on {full.name} itself ({full.n} points): {t_mv:.2f} s; RASM setup "
+            f"{t_su:.2f} s and PC apply + orthogonalisation {rest * 1e3:.1f} ms/iteration timed in "
+            f"a full oracle solve of a {wl.n}-point sample of the same recipe ({wl.name}, "
+            f"{res.iterations} it, {res.restarts} restarts), x{scale:.1f} per point; "
+            f"estimate = setup + {n_mv} matvecs + {res.iterations} iterations x (PC + orth)")
+    return est, desc
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    # all host cores (torchrun exports OMP_NUM_THREADS=1 to every rank: override it
+    # before the oracle's OpenMP runtime is loaded)
+    cores = os.cpu_count() or 1
+    os.environ["OMP_NUM_THREADS"] = str(cores)
+    full = W.config(args.config)
     times = []
-    res = wl = full = None
-    scale = 1.0
+    desc = ""
     for i in range(args.warmup + args.steps):
-        dt, scale, res, wl, full = oracle_sample(args.config)
+        v, desc = oracle_estimate(args.config, full)
         if i >= args.warmup:
-            times.append(dt * scale)
+            times.append(v)
     v = statistics.mean(times)
-    sample = (f"oracle solve of a {wl.n}-point sample ({wl.name}, same recipe) in "
-              f"{v / scale:.2f} s, {res.iterations} iterations; x{scale:.1f} linear-in-N "
-              f"extrapolation to {full.name} (N={full.n})")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": full.name, "N": full.n},
             "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "oracle",
-                             "sample": sample},
+                             "sample": desc},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -199,9 +242,10 @@ def run_ours(args, rank, world):
     kw = dict(rank=rank, nranks=world, comm="nccl", nccl_id=nccl_id) if world > 1 else {}
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
 
-    # Arnoldi orthogonalisation: MGS on one GPU (BJ:5, Q12); across GPUs delayed CGS2
-    # (reading Q27): ONE all-gather per iteration instead of k+2
-    orth = args.orth or ("mgs" if world == 1 else "dcgs2")
+    # Arnoldi orthogonalisation: MGS (BJ:5 "modified Gram-Schmidt", reading Q12) for every
+    # GPU count, so a strong-scaling series runs one algorithm; --orth dcgs2 selects the
+    # one-reduction variant (reading Q27)
+    orth = args.orth or "mgs"
 
     def step(timing=False):
         c = P.Context(xy, wl.sigma, wl.cell, wl.rc, wl.rings, wl.box, **kw)
@@ -277,53 +321,67 @@ def run_ours(args, rank, world):
     mv_live = rep_t.ms_matmult
     pc_live = rep_t.ms_pcapply
     orth_live = rep_t.ms_orth
-    # matvec launches per solve: one per iteration + one per restart + 0 (beta0 uses PC only)
-    mv_launches = statistics.mean(r.iterations + r.restarts for r in reps)
-    pc_launches = statistics.mean(r.iterations + r.restarts + 1 for r in reps)
+    # launches inside the timing step's phases: the matvec once per iteration, once per
+    # restart residual and once for the final true residual; the PC once more (beta0)
+    mv_launches = rep_t.iterations + rep_t.restarts + 1
+    pc_launches = rep_t.iterations + rep_t.restarts + 2
     x_bytes = 8 * info["x_doubles"]
     pc_alg_bytes = x_bytes + 16 * n_loc          # X streamed once + u read + z written
     mv_alg_flops = FLOP_PER_PAIR * n_pairs_local
     hbm_peak, hbm_src = peaks()
-    pc_per_launch_ms = pc_live / max(rep_t.iterations, 1)   # live: phase time / launches in the phase
-    mv_per_launch_ms = mv_live / max(rep_t.iterations, 1)
+    pc_per_launch_ms = pc_live / max(pc_launches, 1)   # live: phase time / launches in the phase
+    mv_per_launch_ms = mv_live / max(mv_launches, 1)
     pc_gbs = pc_alg_bytes / (pc_per_launch_ms * 1e-3) / 1e9
     mv_tflops = mv_alg_flops / (mv_per_launch_ms * 1e-3) / 1e12
-    shares = {"matvec": mv_live, "rasm_apply": pc_live, "orth": orth_live}
-    dom = max(("matvec", "rasm_apply"), key=lambda k: shares[k])
-    if dom == "rasm_apply":
-        tr = ncu_traffic("k_rasm_apply") if args.config == 2 else None
-        roof = {"kernel": "k_rasm_apply", "bound": "hbm", "achieved": pc_gbs, "peak": hbm_peak,
-                "unit": "GB/s", "frac": pc_gbs / hbm_peak, "traffic": tr,
-                "traffic_source": "profiles/r01_ncu_traffic.json (cfg2 capture)" if tr else None,
-                "peak_source": hbm_src, "alg_bytes_per_launch": pc_alg_bytes,
-                "ms_per_launch": pc_per_launch_ms}
-    else:
-        tr = ncu_traffic("k_matvec") if args.config == 2 else None
-        roof = {"kernel": "k_matvec", "bound": "alu", "achieved": mv_tflops,
-                "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": mv_tflops / FP64_PEAK_TFLOPS,
-                "traffic": tr, "traffic_unit": "bytes per launch (DRAM read + write)",
-                "traffic_source": "profiles/r01_ncu_traffic.json (cfg2 capture)" if tr else None,
-                "peak_source": "measured DFMA, tools/clock_under_load.cu",
-                "alg_flops_per_launch": mv_alg_flops, "ms_per_launch": mv_per_launch_ms}
-    # every hot kernel against its own roof (the contract's `roofline` is the dominant one)
+    # Arnoldi (MGS) vector traffic: step k of a cycle reads w and v_0..v_k and writes the
+    # new basis vector: (k + 3) x 8 B per point (algorithmic)
+    orth_bytes = 8.0 * n_loc * sum((i % 30) + 3 for i in range(rep_t.iterations))
+    orth_gbs = orth_bytes / (orth_live * 1e-3) / 1e9 if orth_live > 0 else None
     rasm_ms = statistics.mean(sd["rasm"] for sd in setups)
     sflops = setup_flops(wl) / world if wl.overlap_width == 0.0 else None
-    ex_mv, ex_su = ncu_fp64("k_matvec"), ncu_fp64("k_rasm_setup_tc")
-    roof_all = [
-        {"kernel": "k_matvec", "bound": "alu", "achieved": mv_tflops, "peak": FP64_PEAK_TFLOPS,
-         "unit": "TFLOP/s", "frac": mv_tflops / FP64_PEAK_TFLOPS, "ms_per_launch": mv_per_launch_ms,
-         "executed_frac_ncu": ex_mv["fp64_alu_frac_of_peak"] if ex_mv and args.config == 2 else None,
-         "traffic_note": "DRAM traffic is the neighbour list (4 B per union entry, streamed once per "
-                         "launch); the kernel is bound by the FP64 pipe and the L1 gathers"},
-        {"kernel": "k_rasm_apply", "bound": "hbm", "achieved": pc_gbs, "peak": hbm_peak, "unit": "GB/s",
-         "frac": pc_gbs / hbm_peak, "ms_per_launch": pc_per_launch_ms},
-        {"kernel": "k_rasm_setup_tc", "bound": "tensor", "achieved": sflops / (rasm_ms * 1e-3) / 1e12
-         if sflops else None, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-         "frac": sflops / (rasm_ms * 1e-3) / 1e12 / DMMA_PEAK_TFLOPS if sflops else None,
-         "ms_per_launch": rasm_ms, "alg_flops_per_launch": sflops,
-         "executed_frac_ncu": ex_su["fp64_tensor_pct_of_peak"] / 100 if ex_su and args.config == 2 else None,
-         "flops_model": "per subdomain n^3/3 + n1 n0^2 + n1^3 + 2 n1^2 n0 (Cholesky, W, S^-1, X)"},
-    ]
+    su_tflops = sflops / (rasm_ms * 1e-3) / 1e12 if sflops else None
+    tr_src = f"profiles/ncu_traffic.json ({wl.name} capture)"
+    roof_all = {
+        "k_matvec": {"kernel": "k_matvec", "bound": "alu", "achieved": mv_tflops,
+                     "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": mv_tflops / FP64_PEAK_TFLOPS,
+                     "traffic": ncu_traffic("k_matvec", wl.name),
+                     "peak_source": "measured DFMA, tools/clock_under_load.cu (profiles/r01_fp64_peak.json)",
+                     "alg_flops_per_launch": mv_alg_flops, "ms_per_launch": mv_per_launch_ms,
+                     "ms_per_step": mv_live,
+                     "executed_frac_ncu": ncu_fp64("k_matvec", wl.name, "fp64_alu_frac_of_peak")},
+        "k_rasm_apply": {"kernel": "k_rasm_apply", "bound": "hbm", "achieved": pc_gbs, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": pc_gbs / hbm_peak, "peak_source": hbm_src,
+                         "traffic": ncu_traffic("k_rasm_apply", wl.name),
+                         "alg_bytes_per_launch": pc_alg_bytes, "ms_per_launch": pc_per_launch_ms,
+                         "ms_per_step": pc_live},
+        "k_rasm_setup_tc": {"kernel": "k_rasm_setup_tc", "bound": "tensor", "achieved": su_tflops,
+                            "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                            "frac": su_tflops / DMMA_PEAK_TFLOPS if su_tflops else None,
+                            "peak_source": "measured fp64 DMMA (profiles/r01_fp64_peak.json); nominal "
+                                           "148 SM x 128 flop/clk x 1.965 GHz = 37.2",
+                            "traffic": ncu_traffic("k_rasm_setup_tc", wl.name),
+                            "ms_per_launch": rasm_ms, "ms_per_step": rasm_ms,
+                            "alg_flops_per_launch": sflops,
+                            "executed_frac_ncu": ncu_fp64("k_rasm_setup_tc", wl.name,
+                                                          "fp64_tensor_pct_of_peak", 0.01),
+                            "flops_model": "per subdomain n^3/3 + n1 n0^2 + n1^3 + 2 n1^2 n0 "
+                                           "(Cholesky, W, S^-1, X)"},
+        "arnoldi": {"kernel": "MGS vector kernels (k_arnoldi_* / k_axpy_dot)", "bound": "hbm",
+                    "achieved": orth_gbs, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": orth_gbs / hbm_peak if orth_gbs else None, "peak_source": hbm_src,
+                    "alg_bytes_per_step": orth_bytes, "ms_per_step": orth_live,
+                    "bytes_model": "(k + 3) x 8 B per point for Arnoldi step k of a cycle"},
+    }
+    for r_ in roof_all.values():
+        if r_.get("traffic") is not None:
+            r_["traffic_source"] = tr_src
+            r_["traffic_unit"] = "DRAM bytes read + written per launch"
+    # the contract's `roofline`: the kernel with the largest share of the step
+    dom = max(("k_matvec", "k_rasm_apply", "k_rasm_setup_tc", "arnoldi"),
+              key=lambda k: roof_all[k]["ms_per_step"] or 0.0)
+    roof = dict(roof_all[dom])
+    roof["share_of_step"] = roof["ms_per_step"] / ms_per_step
+    roof_all = list(roof_all.values())
     gpairs = n_pairs_local / (mv_ms * 1e-3) / 1e9
     if world > 1:
         tot = torch.tensor([float(n_pairs_local)], dtype=torch.float64, device="cuda")
@@ -383,11 +441,8 @@ def run_ours(args, rank, world):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
         os.environ["OMP_NUM_THREADS"] = str(cores)
-        dt, scale, res, swl, full = oracle_sample(args.config)
-        cpu = {"value": dt * scale, "unit": "s", "cores": cores, "kind": "oracle",
-               "sample": f"oracle solve of {swl.n} points ({swl.name}, same recipe) took "
-                         f"{dt:.2f} s ({res.iterations} it); x{scale:.1f} linear-in-N "
-                         f"extrapolation to {full.name}"}
+        v, desc = oracle_estimate(args.config, None if weak else wl)
+        cpu = {"value": v, "unit": "s", "cores": cores, "kind": "oracle", "sample": desc}
 
     if rank == 0:
         r0 = reps[0]
@@ -402,7 +457,9 @@ def run_ours(args, rank, world):
                        "orth": orth,
                        "parallelism": f"strips{world}", "l2": "flushed (256 MiB write) between steps",
                        "step": "rbf_setup (cell list + RASM setup) + rbf_solve, inputs in HBM"},
-            "iterations": iters, "restarts": r0.restarts, "resid_est": r0.resid_est,
+            "iterations": iters, "restarts": r0.restarts,
+            "converged": all(r.converged for r in reps),
+            "status": sorted({int(r.status) for r in reps}), "resid_est": r0.resid_est,
             "resid_true": r0.resid_true, "resid_precond": r0.resid_precond,
             "setup_ms": {k: statistics.mean(sd[k] for sd in setups) for k in setups[0]},
             "phase_ms": {"matvec": mv_live, "rasm_apply": pc_live, "orth": orth_live,
@@ -433,7 +490,10 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4,
+                    help="BASELINE.json config (default 4: the largest single-GPU case, 50M points)")
+    ap.add_argument("--dry-run-ranks", action="store_true",
+                    help="print this rank's launch environment as JSON and exit (launcher test)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
@@ -442,8 +502,27 @@ def main():
     ap.add_argument("--orth", choices=["mgs", "cgs2", "dcgs2"], default=None,
                     help="GMRES orthogonalisation (default: mgs on 1 GPU, dcgs2 across GPUs)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this script under torch.distributed.run
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+               os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}; using WORLD_SIZE",
+              file=sys.stderr)
+    if args.dry_run_ranks:
+        print(json.dumps({k: os.environ.get(k) for k in
+                          ("RANK", "LOCAL_RANK", "WORLD_SIZE", "MASTER_ADDR", "MASTER_PORT")}),
+              flush=True)
+        return
     if args.impl == "reference":
         return run_reference(args, rank, world)
     if world > 1:

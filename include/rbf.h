@@ -275,6 +275,14 @@ int rbf_matvec_stats(const rbf_ctx *ctx, int64_t out[4]);
  * than a quarter of cases).  EINVAL on NULL. */
 int rbf_lu_stats(const rbf_ctx *ctx, int64_t out[2]);
 
+/* Test hook (Krylov orthogonality, reading Q28): copy the first nvec vectors of the
+ * context's GMRES basis workspace -- after rbf_solve, the basis v_0, v_1, ... of its last
+ * restart cycle (MGS/CGS2: orthonormal vectors; DCGS2: slot k holds the unnormalised
+ * first-pass vector of step k) -- into V_dev (nvec x rbf_local_count doubles, row-major,
+ * device).  EINVAL when no solve has allocated the basis or nvec exceeds restart + 1.
+ * Synchronises. */
+int rbf_debug_krylov_basis(const rbf_ctx *ctx, double *V_dev, int32_t nvec, void *stream);
+
 /* Test hook: fill the shared memory of every SM with 0xFF bytes (NaN in every double)
  * on the current device and synchronise, so that a following kernel that reads shared
  * memory it did not write produces NaN in the parity tests.  The environment variable

@@ -10,11 +10,15 @@
 
 #include "common.cuh"
 
+#include <map>
 #include <mutex>
+#include <unordered_map>
 
 namespace rbf {
 
 static thread_local std::string g_err;
+static std::mutex g_alloc_mu;  // live device bytes per context (dalloc / dfree)
+static std::unordered_map<void *, std::pair<rbf_ctx *, long long>> g_allocs;
 static std::atomic<long long> g_launches{0};
 
 void count_launch(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
@@ -56,12 +60,40 @@ int dalloc(rbf_ctx *c, void **p, size_t bytes, cudaStream_t s) {
   // kernel reading scratch it never wrote shows up in the parity tests
   const char *poison = getenv("RBF_POISON");
   if (poison && poison[0] == '1') cudaMemsetAsync(*p, 0xFF, bytes, s);
-  if (c) c->bytes += (long long)bytes;
+  if (c) {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    c->bytes += (long long)bytes;
+    g_allocs[*p] = {c, (long long)bytes};
+  }
   return RBF_OK;
 }
 
+// c->bytes counts the bytes a context holds NOW: dfree subtracts what dalloc added
 void dfree(void *p, cudaStream_t s) {
-  if (p) cudaFreeAsync(p, s);
+  if (!p) return;
+  {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    auto it = g_allocs.find(p);
+    if (it != g_allocs.end()) {
+      it->second.first->bytes -= it->second.second;
+      g_allocs.erase(it);
+    }
+  }
+  cudaFreeAsync(p, s);
+}
+
+int ensure_dyn_smem(const void *fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void *>, size_t> high;
+  int dev = 0;
+  RBF_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t &h = high[{dev, fn}];
+  if (bytes > h) {
+    RBF_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    h = bytes;
+  }
+  return RBF_OK;
 }
 
 int gather_positions(rbf_ctx *c, const double *xy, cudaStream_t s);  // cells.cu
@@ -225,6 +257,19 @@ int rbf_lu_stats(const rbf_ctx *c, int64_t out[2]) {
   if (!c || !out) { set_error("NULL argument"); return RBF_EINVAL; }
   out[0] = c->n_lu;
   out[1] = c->n_lu_pivot;
+  return RBF_OK;
+}
+
+int rbf_debug_krylov_basis(const rbf_ctx *c, double *V_dev, int32_t nvec, void *stream) {
+  if (!c || !V_dev) { set_error("NULL argument"); return RBF_EINVAL; }
+  if (!c->V || nvec < 1 || nvec > c->V_m + 1) {
+    set_error("rbf_debug_krylov_basis: %d vectors requested, %d held (solve first)", nvec,
+              c->V ? c->V_m + 1 : 0);
+    return RBF_EINVAL;
+  }
+  const size_t bytes = sizeof(double) * (size_t)nvec * (size_t)n_loc(c);
+  RBF_CUDA_TRY(cudaMemcpyAsync(V_dev, c->V, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  RBF_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
   return RBF_OK;
 }
 
@@ -528,10 +573,11 @@ int rbf_interpolate_host(const double *xy_h, const double *f_h, int64_t n, const
   RBF_TRY(validate(p, n));
   cudaStream_t s = (cudaStream_t)stream;
   double *xy = nullptr, *fc = nullptr, *fl = nullptr, *ll = nullptr;
-  RBF_TRY(dalloc(nullptr, (void **)&xy, sizeof(double) * 2 * (size_t)n, s));
-  RBF_TRY(dalloc(nullptr, (void **)&fc, sizeof(double) * (size_t)n, s));
-  RBF_TRY(dalloc(nullptr, (void **)&fl, sizeof(double) * (size_t)n, s));
-  RBF_TRY(dalloc(nullptr, (void **)&ll, sizeof(double) * (size_t)n, s));
+  ScratchGuard sg(s);
+  RBF_TRY(sg.alloc(nullptr, &xy, sizeof(double) * 2 * (size_t)n));
+  RBF_TRY(sg.alloc(nullptr, &fc, sizeof(double) * (size_t)n));
+  RBF_TRY(sg.alloc(nullptr, &fl, sizeof(double) * (size_t)n));
+  RBF_TRY(sg.alloc(nullptr, &ll, sizeof(double) * (size_t)n));
   int st = RBF_OK;
   rbf_ctx *c = nullptr;
   do {
@@ -557,10 +603,6 @@ int rbf_interpolate_host(const double *xy_h, const double *f_h, int64_t n, const
     }
   } while (0);
   if (c) rbf_destroy(c);
-  dfree(xy, s);
-  dfree(fc, s);
-  dfree(fl, s);
-  dfree(ll, s);
   return st;
 }
 

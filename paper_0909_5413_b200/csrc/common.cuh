@@ -36,6 +36,12 @@ void count_launch(int k);  // kernel launches issued by this library (rbf_launch
     }                                                                                    \
   } while (0)
 
+// Raise kernel `fn`'s dynamic shared-memory limit on the current device to at least
+// `bytes` (thread-safe, never lowers it): a per-device high-water mark under a mutex, so
+// a launch that needs `bytes` cannot see another host thread lower the attribute
+// between this call and the launch (concurrent contexts, RBF_COMM_THREADS).
+int ensure_dyn_smem(const void *fn, size_t bytes);
+
 #define RBF_TRY(call)          \
   do {                         \
     int s_ = (call);           \
@@ -279,6 +285,22 @@ int owned_cells(const rbf_ctx *c);
 // device allocation helpers (stream-ordered pool allocator)
 int dalloc(rbf_ctx *c, void **p, size_t bytes, cudaStream_t s);
 void dfree(void *p, cudaStream_t s);
+
+// Scratch buffers freed (stream-ordered) when the guard goes out of scope, so early
+// error returns (RBF_TRY) do not leak them.
+struct ScratchGuard {
+  cudaStream_t s;
+  std::vector<void *> ptrs;
+  explicit ScratchGuard(cudaStream_t s_) : s(s_) {}
+  template <class T> int alloc(rbf_ctx *c, T **p, size_t bytes) {
+    int st = dalloc(c, (void **)p, bytes, s);
+    if (st == RBF_OK) ptrs.push_back((void *)*p);
+    return st;
+  }
+  ~ScratchGuard() {
+    for (void *p : ptrs) dfree(p, s);
+  }
+};
 
 // cells.cu
 int build_cell_list(rbf_ctx *c, const double *xy_caller, cudaStream_t s);

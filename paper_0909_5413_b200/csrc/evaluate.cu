@@ -79,11 +79,12 @@ int evaluate(rbf_ctx *c, const double *q, long long m, const double *lam, double
   }
   int *keys = nullptr, *vals = nullptr, *skeys = nullptr, *order = nullptr;
   long long *bad = nullptr;
-  RBF_TRY(dalloc(nullptr, (void **)&keys, sizeof(int) * m, s));
-  RBF_TRY(dalloc(nullptr, (void **)&vals, sizeof(int) * m, s));
-  RBF_TRY(dalloc(nullptr, (void **)&skeys, sizeof(int) * m, s));
-  RBF_TRY(dalloc(nullptr, (void **)&order, sizeof(int) * m, s));
-  RBF_TRY(dalloc(nullptr, (void **)&bad, sizeof(long long), s));
+  ScratchGuard sg(s);
+  RBF_TRY(sg.alloc(nullptr, &keys, sizeof(int) * m));
+  RBF_TRY(sg.alloc(nullptr, &vals, sizeof(int) * m));
+  RBF_TRY(sg.alloc(nullptr, &skeys, sizeof(int) * m));
+  RBF_TRY(sg.alloc(nullptr, &order, sizeof(int) * m));
+  RBF_TRY(sg.alloc(nullptr, &bad, sizeof(long long)));
   RBF_CUDA_TRY(cudaMemsetAsync(bad, 0xff, sizeof(long long), s));
   const int blocks = (int)((m + 255) / 256);
   k_query_keys<<<blocks, 256, 0, s>>>(q, m, c->g, keys, vals, bad);
@@ -95,7 +96,7 @@ int evaluate(rbf_ctx *c, const double *q, long long m, const double *lam, double
   size_t tb = 0;
   RBF_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, skeys, vals, order, (int)m, 0, end_bit, s));
   void *tmp = nullptr;
-  RBF_TRY(dalloc(nullptr, &tmp, tb, s));
+  RBF_TRY(sg.alloc(nullptr, &tmp, tb));
   RBF_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, skeys, vals, order, (int)m, 0, end_bit, s));
   count_launch(1 + (end_bit + 7) / 8);
   RBF_TRY(launch_pack_w(c, lam, s));
@@ -105,12 +106,6 @@ int evaluate(rbf_ctx *c, const double *q, long long m, const double *lam, double
   long long hbad = -1;
   RBF_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof(long long), cudaMemcpyDeviceToHost, s));
   RBF_CUDA_TRY(cudaStreamSynchronize(s));
-  dfree(tmp, s);
-  dfree(keys, s);
-  dfree(vals, s);
-  dfree(skeys, s);
-  dfree(order, s);
-  dfree(bad, s);
   if (hbad != -1) {
     set_error("rbf_evaluate: query %lld is non-finite or outside the box [%g,%g]x[%g,%g]", hbad,
               c->g.x0, c->g.x1, c->g.y0, c->g.y1);

@@ -1076,7 +1076,11 @@ static int ensure_workspace(rbf_ctx *c, int m, cudaStream_t s) {
     int dev = 0, sms = 0, per_sm = 0;
     RBF_CUDA_TRY(cudaGetDevice(&dev));
     RBF_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    // the grid must fit both MGS kernels (launch_fused_step picks one of them)
+    int per_sm2 = 0;
     RBF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_arnoldi_fused, kArThreads, 0));
+    RBF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_arnoldi_mgs2, kArThreads, 0));
+    per_sm = per_sm < per_sm2 ? per_sm : per_sm2;
     int coop = 0;
     RBF_CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
     const int ar_per_sm = getenv("RBF_AR_PER_SM") ? atoi(getenv("RBF_AR_PER_SM")) : 2;

@@ -1270,8 +1270,7 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
   RBF_TRY(dalloc(c, (void **)&c->X, sizeof(double) * (size_t)(total > 0 ? total : 2), s));
   if (ncl > 0 && c->nsub > hc[3]) {
     const size_t smem = (size_t)hc[4];  // the largest per-cell layout of the tensor-core cells
-    RBF_CUDA_TRY(cudaFuncSetAttribute(k_rasm_setup_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
+    RBF_TRY(ensure_dyn_smem((const void *)k_rasm_setup_tc, smem));
     k_rasm_setup_tc<<<ncl, kTcThreads, smem, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off,
                                                   c->X, cnt, glist, ov);
     count_launch(1);
@@ -1356,7 +1355,7 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
         cudaFuncAttributes fa;
         RBF_CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
         if (need + fa.sharedSizeBytes <= (size_t)optin) {
-          RBF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+          RBF_TRY(ensure_dyn_smem((const void *)kern, need));
           int occ = 0;
           RBF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, need));
           if (occ >= (nn > kLuBigN ? 1 : 2)) dyn = need;
@@ -1429,12 +1428,7 @@ int launch_rasm_apply(const rbf_ctx *c, const double *r_ext, double *z_loc, cuda
   if (ncl <= 0 || c->nsub == 0) return RBF_OK;
   const size_t smem = sizeof(double) * (size_t)(c->max_ov + 2);
   if (c->g.asm_full) {  // Eq.(8): local solutions, then the per-point sums
-    static size_t attr_a = 48 * 1024;
-    if (smem > attr_a) {
-      RBF_CUDA_TRY(cudaFuncSetAttribute(k_asm_local, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem));
-      attr_a = smem;
-    }
+    RBF_TRY(ensure_dyn_smem((const void *)k_asm_local, smem));
     k_asm_local<<<ncl, kRaThreads, smem, s>>>(c->g, c->s, c->cell_start, c->x_off, c->asm_toff, c->X,
                                               r_ext, c->asm_t, ov_of(c));
     const long long np = n_loc(c);
@@ -1443,12 +1437,7 @@ int launch_rasm_apply(const rbf_ctx *c, const double *r_ext, double *z_loc, cuda
     RBF_CUDA_TRY(cudaGetLastError());
     return RBF_OK;
   }
-  static size_t attr_d = 48 * 1024;
-  if (smem > attr_d) {
-    RBF_CUDA_TRY(cudaFuncSetAttribute(k_rasm_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-    attr_d = smem;
-  }
+  RBF_TRY(ensure_dyn_smem((const void *)k_rasm_apply, smem));
   k_rasm_apply<<<ncl, kRaThreads, smem, s>>>(c->g, c->s, c->cell_start, c->x_off, c->X, r_ext,
                                              z_loc, ov_of(c));
   count_launch(1);

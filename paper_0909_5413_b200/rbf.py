@@ -58,7 +58,7 @@ EXPORTS = ["rbf_get_nccl_id", "rbf_setup", "rbf_local_count", "rbf_ext_count", "
            "rbf_interpolate_host", "rbf_count_pairs", "rbf_dot", "rbf_plan_strips",
            "rbf_last_error", "rbf_destroy", "rbf_info", "rbf_launch_count", "rbf_setup_times",
            "rbf_plan_halo", "rbf_evaluate", "rbf_matvec_stats", "rbf_lu_stats",
-           "rbf_debug_poison_shared"]
+           "rbf_debug_poison_shared", "rbf_debug_krylov_basis"]
 
 _lib = None
 
@@ -93,6 +93,7 @@ def lib() -> C.CDLL:
             "rbf_matvec_stats": (C.c_int, [p, p]),
             "rbf_lu_stats": (C.c_int, [p, p]),
             "rbf_debug_poison_shared": (C.c_int, []),
+            "rbf_debug_krylov_basis": (C.c_int, [p, p, i32, p]),
             "rbf_dot": (C.c_int, [p, p, p, p, p]),
             "rbf_plan_strips": (C.c_int, [p, i64, i32, i64, p]),
             "rbf_last_error": (C.c_char_p, []),
@@ -332,6 +333,15 @@ class Context:
         o = (C.c_int64 * 2)()
         _check(lib().rbf_lu_stats(self._h, o))
         return {"n_lu": int(o[0]), "n_lu_pivot": int(o[1])}
+
+    def krylov_basis(self, nvec: int):
+        """Test hook: the first nvec GMRES basis vectors of the last solve's last cycle
+        (rbf_debug_krylov_basis), an (nvec, n_local) device tensor."""
+        import torch
+
+        V = torch.empty((int(nvec), self.n_local), dtype=torch.float64, device="cuda")
+        _check(lib().rbf_debug_krylov_basis(self._h, _ptr(V), int(nvec), _stream(self._stream)))
+        return V
 
     def count_pairs(self) -> int:
         v = C.c_int64()

@@ -686,6 +686,17 @@ def test_big_solve_residual(big):
     rows = rng.choice(wl.n, 200, replace=False)
     res = wl.f[rows] - oracle_rows(wl, lam, rows, cl)
     assert np.max(np.abs(res)) <= 1e-9 * np.max(np.abs(wl.f))
+    # the deconvolution closed form ([D4]; oracle pin in
+    # test_oracle_pins_r2.py): cfg4 over the whole domain, cfg3 per blob in |x|_inf <= 0.4
+    from closed_forms import CF_TOL, closed_form_blobs, closed_form_gauss
+
+    if wl.name == "cfg4":
+        lc = closed_form_gauss(wl, wl.meta["s2"])
+        assert np.max(np.abs(lam - lc)) <= CF_TOL * np.max(np.abs(lc))
+    else:
+        lc = closed_form_blobs(wl, wl.meta["seed"])
+        inner = np.max(np.abs(wl.xy), axis=1) <= 0.4
+        assert np.max(np.abs(lam - lc)[inner]) <= CF_TOL * np.max(np.abs(lc))
 
 
 def test_cfg5_matvec_sampled_rows():

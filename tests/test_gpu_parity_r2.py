@@ -1,0 +1,115 @@
+"""Round-2 GPU parity cases (-m gpu, through the C ABI):
+
+  * pivoted LU on genuinely indefinite subdomain matrices against the oracle's LU
+    (reading Q11): a short cutoff rc = 2.5 sigma makes every A_c of a jittered lattice
+    indefinite with kappa(A_c) <= ~3e6 (computed here), so the tensor-core Cholesky
+    breaks down on every cell (one ring) and the no-pivot probe fails (two rings); the
+    bar is 20 kappa_max eps (backward-stable LU with partial pivoting);
+  * the LU path's transposed panel in shared memory vs in the workspace (RBF_LU_SMEM)
+    on 361-400-point subdomains, with and without pivoting: bitwise equal, and <= 1e-10
+    against the oracle;
+  * the Krylov basis of the one-GPU pairwise MGS (reading Q28) against the oracle's
+    MGS on an ill-conditioned cycle (SURVEY §8.c.3 "Krylov orthogonality").
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import rbf_workloads as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_0909_5413_b200 as P  # noqa: E402
+
+EPS = np.finfo(np.float64).eps
+
+
+def to_caller(ctx, v_loc):
+    idx = ctx.local_index().cpu().numpy()
+    out = np.zeros(ctx.n)
+    out[idx] = v_loc.cpu().numpy()
+    return out
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("rings", [1, 2])
+def test_lu_pivoting_indefinite_subdomains_vs_oracle(rings):
+    wl = W.make_lattice(40, jitter_frac=0.3, seed=7)
+    rc = 2.5 * wl.sigma
+    Pc = O.Rasm(wl.xy, wl.sigma, rc, wl.box, wl.cell, rings)
+    assert Pc.status == 0 and Pc.n_lu == Pc.nsub  # the oracle's Cholesky fails everywhere
+    kap = 0.0
+    for s in range(Pc.nsub):
+        ov, _ = Pc.subdomain(s)
+        ev = np.linalg.eigvalsh(O.assemble_dense(wl.xy[ov], wl.sigma, rc))
+        assert ev[0] < 0  # genuinely indefinite
+        kap = max(kap, np.max(np.abs(ev)) / np.min(np.abs(ev)))
+    assert kap < 1e8
+    r = np.random.default_rng(31).standard_normal(wl.n)
+    ref = Pc.apply(r)
+    Pc.close()
+    xy = torch.from_numpy(wl.xy).cuda()
+    with P.Context(xy, wl.sigma, wl.cell, rc, rings, wl.box) as c:
+        st = c.lu_stats()
+        assert st["n_lu"] == st["n_lu_pivot"] == c.info()["nsub"]
+        z = to_caller(c, c.rasm_apply(c.to_local(torch.from_numpy(r).cuda())))
+    assert rel(z, ref) <= 20 * kap * EPS
+
+
+@pytest.mark.parametrize("pivot", ["0", "1"], ids=["pivot-all", "nopiv-pass"])
+def test_lu_shared_panel_matches_workspace_panel(pivot, monkeypatch):
+    wl = W.make_lattice(64, jitter_frac=0.1, seed=9)
+    cell = 6.4 * wl.meta["h"]  # 3x3 blocks of ~6.4 h cells: 361-400-point subdomains
+    r = np.random.default_rng(32).standard_normal(wl.n)
+    Pc = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, cell, 1)
+    ref = Pc.apply(r)
+    Pc.close()
+    monkeypatch.setenv("RBF_LU_NOPIV", pivot)
+    xy = torch.from_numpy(wl.xy).cuda()
+    out = {}
+    for smem in ("0", "1"):
+        monkeypatch.setenv("RBF_LU_SMEM", smem)
+        with P.Context(xy, wl.sigma, cell, wl.rc, 1, wl.box) as c:
+            info = c.info()
+            assert 300 < info["max_ov"] <= 420 and info["n_lu"] > 0
+            st = c.lu_stats()
+            assert st["n_lu_pivot"] == (st["n_lu"] if pivot == "0" else 0)
+            out[smem] = to_caller(c, c.rasm_apply(c.to_local(torch.from_numpy(r).cuda())))
+    assert np.array_equal(out["0"], out["1"])
+    assert rel(out["1"], ref) <= 1e-10
+
+
+def test_pairwise_mgs_orthogonality_vs_oracle_mgs():
+    """cfg1, RASM, one GMRES(30) cycle at rtol 0: after 20 steps the recurrence residual
+    is ~1e-11 and kappa(K) ~1e11, where MGS has lost orthogonality to O(eps kappa)
+    (oracle pin in test_oracle_pins_r2.py).  The GPU's pairwise projections (reading Q28)
+    must stay within 10x of the oracle's MGS loss, and both bases must span the same
+    space to the same accuracy (same leading vectors)."""
+    wl = W.config(1)
+    Pc = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, 1)
+    opA = O.op_rbf(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell)
+    r = O.gmres(opA, O.op_rasm(Pc), wl.f, restart=30, max_iters=30, rtol=0.0, keep_basis=True)
+    Pc.close()
+    Vo = r.basis[:20]
+    loss_o = np.max(np.abs(Vo @ Vo.T - np.eye(20)))
+    xy = torch.from_numpy(wl.xy).cuda()
+    with P.Context(xy, wl.sigma, wl.cell, wl.rc, 1, wl.box) as c:
+        f = c.to_local(torch.from_numpy(wl.f).cuda())
+        _, rep = c.solve(f, restart=30, max_iters=30, rtol=0.0)
+        assert rep.iterations == 30
+        Vg_loc = c.krylov_basis(20)
+        idx = c.local_index().cpu().numpy()
+    Vg = np.zeros((20, wl.n))
+    Vg[:, idx] = Vg_loc.cpu().numpy()
+    loss_g = np.max(np.abs(Vg @ Vg.T - np.eye(20)))
+    assert loss_g <= 10 * loss_o
+    # the first basis vectors (before rounding drives the two recurrences apart) agree
+    for j in range(6):
+        assert rel(Vg[j], Vo[j]) <= 1e-8
