@@ -100,7 +100,7 @@ def peaks():
 class Clocks:
     def __init__(self, gpu_index: int):
         self.path = f"/tmp/rbf_clocks_{os.getpid()}.csv"
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+        q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
         try:
@@ -110,16 +110,29 @@ class Clocks:
         except Exception:
             self.p = None
 
+    def mark(self):
+        """Start of the timed window (the sampler is started earlier, so its start-up
+        does not fall into the timed steps)."""
+        self.t0 = time.time()
+
     def stop(self):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t1 = time.time()
         self.p.terminate()
         self.p.wait()
         rows = []
+        import datetime
+
         for line in open(self.path):
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 7:
-                rows.append(parts)
+            if len(parts) >= 8:
+                try:
+                    ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                except ValueError:
+                    ts = None
+                if ts is None or getattr(self, "t0", None) is None or self.t0 - 0.5 <= ts <= t1 + 0.5:
+                    rows.append(parts[1:])
         os.unlink(self.path)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
@@ -258,6 +271,9 @@ def run_ours(args, rank, world):
             dist.barrier()
         torch.cuda.synchronize()
 
+    # the clock sampler starts before the warm-up (nvidia-smi's start-up stays out of the
+    # timed steps); only its samples inside the timed window are kept
+    clocks = Clocks(dev) if not os.environ.get("RBF_BENCH_NO_CLOCKS") else None
     # warm-up (also: facts for the roofline)
     for _ in range(args.warmup):
         c, lam, rep = step()
@@ -265,7 +281,8 @@ def run_ours(args, rank, world):
         c.close()
     barrier()
     # timed region: K steps, each bracketed by CUDA events; L2 flushed between steps
-    clocks = Clocks(dev) if not os.environ.get("RBF_BENCH_NO_CLOCKS") else None
+    if clocks:
+        clocks.mark()
     launches0 = P.launch_count()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
@@ -321,10 +338,11 @@ def run_ours(args, rank, world):
     mv_live = rep_t.ms_matmult
     pc_live = rep_t.ms_pcapply
     orth_live = rep_t.ms_orth
-    # launches inside the timing step's phases: the matvec once per iteration, once per
-    # restart residual and once for the final true residual; the PC once more (beta0)
-    mv_launches = rep_t.iterations + rep_t.restarts + 1
-    pc_launches = rep_t.iterations + rep_t.restarts + 2
+    # launches inside the timing step's phases: the matvec once per iteration and once per
+    # restart residual; the PC once more (beta0).  The report's final residuals are
+    # computed outside the timed phases.
+    mv_launches = rep_t.iterations + rep_t.restarts
+    pc_launches = rep_t.iterations + rep_t.restarts + 1
     x_bytes = 8 * info["x_doubles"]
     pc_alg_bytes = x_bytes + 16 * n_loc          # X streamed once + u read + z written
     mv_alg_flops = FLOP_PER_PAIR * n_pairs_local

@@ -102,7 +102,9 @@ def test_pairwise_mgs_orthogonality_vs_oracle_mgs():
     xy = torch.from_numpy(wl.xy).cuda()
     with P.Context(xy, wl.sigma, wl.cell, wl.rc, 1, wl.box) as c:
         f = c.to_local(torch.from_numpy(wl.f).cuda())
-        _, rep = c.solve(f, restart=30, max_iters=30, rtol=0.0)
+        # the host-driven loop (timing=True) runs the same pairwise-MGS kernel and stops
+        # before the restart residual would overwrite v_0 (the graph path computes it)
+        _, rep = c.solve(f, restart=30, max_iters=30, rtol=0.0, timing=True)
         assert rep.iterations == 30
         Vg_loc = c.krylov_basis(20)
         idx = c.local_index().cpu().numpy()
