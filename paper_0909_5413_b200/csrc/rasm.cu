@@ -233,6 +233,7 @@ __global__ void k_rasm_sizes(Geom g, Strip st, const int *__restrict__ cell_star
 //   X_c = S^-1 [-W, I]  (the rows of A_c^-1 for own(c), Eq.(9)-(11)),
 // written to HBM in natural column order.
 constexpr int kAccWarps = kTcWarps - 2;  // warps 14, 15 alternate as diagonal warps
+constexpr int kWWarps = 12;              // W phase warps (the other four form S^-1)
 
 #ifdef RBF_PROBE
 __device__ long long g_probe[64][8];
@@ -491,92 +492,80 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
   }
 
   PROBE(2)
-  // ---- W = L21 L11^-1, own tile row r by the warp pair (r, r + 4), right to left: the
-  //      sum over kt > jt of W(it, kt) L(kt, jt) is split by kt parity between the two
-  //      warps (one per sub-partition pair, so twice the DMMA issue rate per row); the
-  //      partner's partial goes through shared memory and a 64-thread named barrier.
-  //      S^-1 = L22^-T L22^-1 concurrently on warp 15.
-  double *wpart = rdiag + T * 8;  // 4 rows x 64 doubles (after rdiag, before the M area)
-  // up to 4 own tile rows: a warp pair per row; 5..8 rows (own(c) up to 64): one warp per row
-  const bool wpairs = T1 <= 4;
-  // the row loop, specialised for warp pairs (PAIRS) or one warp per row
-  auto wloop = [&](auto pairs_tag) {
-    constexpr bool wpairs = decltype(pairs_tag)::value;
-    const int r = wpairs ? warp & 3 : warp, half = wpairs ? warp >> 2 : 0;  // half 0 finishes
-    const int it = T0 + r;
-    double *Wrow = sm + toff(it, 0);
+  // ---- W = L21 L11^-1 (warps 0..11) and S^-1 = L22^-T L22^-1 (warps 12..15), concurrently.
+  //
+  // W solves W L11 = L21 backwards over the tile columns of L11.  Right-looking: once
+  // column kt of W is final, every own tile row r subtracts W(r,kt) L(kt,jt) from its
+  // columns jt < kt (in place in the L21 tiles), so the work of a step is spread over
+  // twelve warps and the chain from one column to the next is only the jt = kt-1 update
+  // and that column's finish W(r,kt-1) = C(r,kt-1) L_d(kt-1)^-1, done first by the
+  // owners of (r, kt-1), then one named barrier.  Tile (r, jt) belongs to warp
+  // (r + T1 jt) mod 12: the T1 <= 8 rows of a column are on distinct warps.
+  if (warp < kWWarps) {
     const int f0 = frag_rowk(lane, 0), f1 = frag_rowk(lane, 1);
     const int g0 = frag_colk(lane, 0), g1 = frag_colk(lane, 1);
-    const unsigned bar_id = 1 + r;
-    for (int jt = T0 - 1; jt >= 0; --jt) {
-      if (warp == 0) PW(jt, 0)
-      AccSet A, B;  // four independent DMMA chains
-      A.zero();
-      B.zero();
-      for (int par = half; par < 2; par += wpairs ? 2 : 1) {  // kt parity (both for a lone warp)
-        int kt = jt + 1 + par;
-        for (; kt + 2 < T0; kt += 4) {
-          const double *Lk = sm + toff(kt, jt), *Lk2 = sm + toff(kt + 2, jt);
-          dmma(A.a0, A.a1, Wrow[kt * 64 + f0], Lk[g0]);
-          dmma(A.b0, A.b1, Wrow[(kt + 2) * 64 + f0], Lk2[g0]);
-          dmma(B.a0, B.a1, Wrow[kt * 64 + f1], Lk[g1]);
-          dmma(B.b0, B.b1, Wrow[(kt + 2) * 64 + f1], Lk2[g1]);
-        }
-        if (kt < T0) {
-          const double *Lk = sm + toff(kt, jt);
-          dmma(A.a0, A.a1, Wrow[kt * 64 + f0], Lk[g0]);
-          dmma(B.a0, B.a1, Wrow[kt * 64 + f1], Lk[g1]);
-        }
-      }
-      A.a0 += B.a0;
-      A.a1 += B.a1;
-      A.b0 += B.b0;
-      A.b1 += B.b1;
-      if (half == 1) {
-        *reinterpret_cast<double2 *>(wpart + r * 64 + 2 * lane) = make_double2(A.a0 + A.b0, A.a1 + A.b1);
-      }
-      if (warp == 0) PW(jt, 1)
-      if (wpairs) asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-      if (warp == 0) PW(jt, 2)
-      if (half == 0) {
-        if (wpairs) {
-          const double2 pp = *reinterpret_cast<const double2 *>(wpart + r * 64 + 2 * lane);
-          A.a0 += pp.x;
-          A.a1 += pp.y;
-        }
-        acc_finish_rmw(A, sm, it, jt, lane);
-        __syncwarp();
-        // W(it, jt) = C L_d^-1   (B[k][n] = Linv[k][n])
-        const double *D = sm + toff(jt, jt);
-        double *Ct = Wrow + jt * 64;
-        double d0 = 0.0, d1 = 0.0;
+    // W(r, jt) = C(r, jt) L_d(jt)^-1   (B[k][n] = Linv[k][n])
+    auto finish = [&](int r, int jt) {
+      double *Ct = sm + toff(T0 + r, jt);
+      const double *D = sm + toff(jt, jt);
+      double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int k = 4 * h + (lane & 3), n = lane >> 2;
-          const double bv = (k > n) ? D[swz(n, k)] : (k == n ? rdiag[jt * 8 + k] : 0.0);
-          dmma(d0, d1, Ct[frag_rowk(lane, h)], bv);
-        }
-        __syncwarp();
-        *reinterpret_cast<double2 *>(Ct + frag_acc(lane)) = make_double2(d0, d1);
+      for (int h = 0; h < 2; ++h) {
+        const int k = 4 * h + (lane & 3), n = lane >> 2;
+        const double bv = (k > n) ? D[swz(n, k)] : (k == n ? rdiag[jt * 8 + k] : 0.0);
+        dmma(d0, d1, Ct[frag_rowk(lane, h)], bv);
       }
-      if (warp == 0) PW(jt, 3)
-      if (wpairs) asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-      else __syncwarp();
+      __syncwarp();
+      *reinterpret_cast<double2 *>(Ct + frag_acc(lane)) = make_double2(d0, d1);
+    };
+    // C(r, jt) -= W(r, kt) L(kt, jt)
+    auto update = [&](int r, int kt, int jt) {
+      const double *Wt = sm + toff(T0 + r, kt), *Lk = sm + toff(kt, jt);
+      double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+      dmma(d0, d1, Wt[f0], Lk[g0]);
+      dmma(e0, e1, Wt[f1], Lk[g1]);
+      double2 *cp = reinterpret_cast<double2 *>(sm + toff(T0 + r, jt) + frag_acc(lane));
+      double2 cv = *cp;
+      cv.x -= d0 + e0;
+      cv.y -= d1 + e1;
+      *cp = cv;
+    };
+    // the first column has no pending updates
+    if (T0 > 0)
+      for (int r = 0; r < T1; ++r)
+        if ((r + T1 * (T0 - 1)) % kWWarps == warp) finish(r, T0 - 1);
+    for (int kt = T0 - 1; kt >= 1; --kt) {
+      if (warp == 0) PW(kt, 0)
+      asm volatile("bar.sync 1, %0;" ::"n"(kWWarps * 32) : "memory");  // W(:, kt) final
+      if (warp == 0) PW(kt, 1)
+      // the chain: column kt-1's update from kt and its finish
+      for (int r = 0; r < T1; ++r)
+        if ((r + T1 * (kt - 1)) % kWWarps == warp) {
+          update(r, kt, kt - 1);
+          __syncwarp();
+          finish(r, kt - 1);
+        }
+      if (warp == 0) PW(kt, 2)
+      // the rest of this step's updates (off the chain)
+      for (int jt = kt - 2; jt >= 0; --jt)
+        for (int r = 0; r < T1; ++r)
+          if ((r + T1 * jt) % kWWarps == warp) update(r, kt, jt);
+      if (warp == 0) PW(kt, 3)
     }
-  };
-  if (wpairs ? (warp < 8 && (warp & 3) < T1) : warp < T1) {
-    if (wpairs) wloop(std::true_type{});
-    else wloop(std::false_type{});
-  } else if (warp == 15) {
-    PW(31, 0)
-    // S^-1 = L22^-T L22^-1 on tiles with the tensor cores (one warp, a few dozen DMMA):
+  } else {
+    if (warp == kWWarps) PW(31, 0)
+    // S^-1 = L22^-T L22^-1 on tiles with the tensor cores, warps 12..15:
     //   M = L22^-1:  M(a,a) = L_a^-1 (already formed by the diagonal factorization),
-    //                M(a,b) = -L_a^-1 sum_{k=b}^{a-1} L22(a,k) M(k,b),   a > b;
-    //   S^-1(a,b) = sum_{k>=a} M(k,a)^T M(k,b),   a >= b  (row a last touches L_a^-1,
-    //   so each row's diagonal tile is written last, over the L_a / L_a^-1 storage).
-    // M (strictly lower tiles) lives in the positions buffer (dead after the factorisation).
+    //                M(a,b) = -L_a^-1 sum_{k=b}^{a-1} L22(a,k) M(k,b),   a > b:
+    //                the columns b of M are independent -- one warp per column;
+    //   S^-1(a,b) = sum_{k>=a} M(k,a)^T M(k,b),   a >= b: tiles spread over the four
+    //                warps, held in registers and written over L22 after a barrier (they
+    //                read the L_a^-1 scratch of the diagonal tiles they overwrite).
+    // M (strictly lower tiles) lives in the positions buffer (dead after the factorisation),
+    // each warp's product scratch tile in the (former) W partials area.
+    const int sw = warp - kWWarps;
     double *Mt = reinterpret_cast<double *>(pos);
-    double *scr = Mt + (T1 * (T1 - 1) / 2) * 64;
+    double *scr = rdiag + T * 8 + sw * 64;
     auto mt = [&](int a, int b) { return Mt + ((a * (a - 1)) / 2 + b) * 64; };  // a > b only
     const int m_ = lane >> 2, q_ = lane & 3;
     // Linv_a fragments: as A (A[m][k] = Linv[m][k]) or B (B[k][n] = Linv[k][n]); Linv[r][c]
@@ -596,8 +585,8 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
       const int kk = 4 * h + q_;
       return (kk > m_) ? D[swz(m_, kk)] : (kk == m_ ? rdiag[(T0 + a) * 8 + m_] : 0.0);
     };
-    for (int a = 1; a < T1; ++a) {
-      for (int b = a - 1; b >= 0; --b) {
+    for (int b = sw; b < T1 - 1; b += kTcWarps - kWWarps) {
+      for (int a = b + 1; a < T1; ++a) {
         double d0 = 0.0, d1 = 0.0;
         for (int k = b; k < a; ++k) {
           const double *La = sm + toff(T0 + a, T0 + k);
@@ -615,64 +604,103 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
         __syncwarp();
       }
     }
-    for (int a = 0; a < T1; ++a) {
-      for (int bb = 0; bb <= a; ++bb) {  // the row's diagonal tile last
-        double d0 = 0.0, d1 = 0.0;
+    asm volatile("bar.sync 2, %0;" ::"n"((kTcWarps - kWWarps) * 32) : "memory");  // M complete
+    constexpr int kSlots = (8 * 9 / 2 + kTcWarps - kWWarps - 1) / (kTcWarps - kWWarps);
+    double res[kSlots][2];
+    const int ntl = T1 * (T1 + 1) / 2;
+#pragma unroll
+    for (int sl = 0; sl < kSlots; ++sl) {
+      const int t = sw + sl * (kTcWarps - kWWarps);
+      res[sl][0] = res[sl][1] = 0.0;
+      if (t < ntl) {
+        int a = 0;
+        while ((a + 1) * (a + 2) / 2 <= t) ++a;
+        const int bb = t - a * (a + 1) / 2;
         for (int k = a; k < T1; ++k) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const double av = (k == a) ? linvT(a, h) : mt(k, a)[frag_colk(lane, h)];
             const double bv = (k == bb) ? linvB(bb, h) : mt(k, bb)[frag_colk(lane, h)];
-            dmma(d0, d1, av, bv);
+            dmma(res[sl][0], res[sl][1], av, bv);
           }
         }
-        __syncwarp();
-        *reinterpret_cast<double2 *>(sm + toff(T0 + a, T0 + bb) + frag_acc(lane)) = make_double2(d0, d1);
-        __syncwarp();
       }
     }
-    PW(31, 1)
+    asm volatile("bar.sync 2, %0;" ::"n"((kTcWarps - kWWarps) * 32) : "memory");  // L^-1 scratch read
+#pragma unroll
+    for (int sl = 0; sl < kSlots; ++sl) {
+      const int t = sw + sl * (kTcWarps - kWWarps);
+      if (t < ntl) {
+        int a = 0;
+        while ((a + 1) * (a + 2) / 2 <= t) ++a;
+        const int bb = t - a * (a + 1) / 2;
+        *reinterpret_cast<double2 *>(sm + toff(T0 + a, T0 + bb) + frag_acc(lane)) =
+            make_double2(res[sl][0], res[sl][1]);
+      }
+    }
+    if (warp == kWWarps) PW(31, 1)
   }
   __syncthreads();
 
   PROBE(3)
-  // ---- X_c = S^-1 [-W, I] in natural column order, ld = n rounded up to even.
-  // X_other = -S^-1 W straight from the DMMA accumulators; X_own = S^-1.
+  // ---- X_c = S^-1 [-W, I] in natural column order, ld = n rounded up to even, staged
+  // in shared memory (the L11 tiles are dead) as the contiguous n_own x ld block and
+  // written to HBM by one bulk copy (TMA), which drains while the next CTA starts.
+  // X_other = -S^-1 W straight from the DMMA accumulators; X_own = S^-1 (full tiles).
   const int n = S.n;
   const int ld = (n + 1) & ~1;
-  double *Xc = X + x_off[cl];
+  // the staging block must lie inside the dead L11 tiles (the X loop still reads the W
+  // and S^-1 tiles beyond them); else (small T0) the rows go straight to HBM
+  const bool stage = (long long)S.n1 * ld <= (long long)toff(T0, 0);
+  double *Xs = stage ? sm : X + x_off[cl];
   for (int task = warp; task < T1 * T0; task += kTcWarps) {
     const int ot = task / T0, jt = task - ot * T0;
     double d0 = 0.0, d1 = 0.0;
     for (int kt = 0; kt < T1; ++kt) {
-      // A = S^-1 tile (ot, kt): only the lower triangle of S^-1 is stored (the upper
-      // half of diagonal tiles still holds the L^-1 scratch), so read (k, m) above it.
+      // A = S^-1 tile (ot, kt): the lower tiles are stored, (ot, kt) above the diagonal
+      // is the transpose of (kt, ot); diagonal tiles are full (symmetric)
       const bool lower = kt <= ot;
       const double *At = lower ? sm + toff(T0 + ot, T0 + kt) : sm + toff(T0 + kt, T0 + ot);
       const double *Bt = sm + toff(T0 + kt, jt);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int m = lane >> 2, k = 4 * h + (lane & 3);
-        const bool below = (kt < ot) || (kt == ot && k <= m);
-        const double av = below ? At[swz(m, k)] : At[swz(k, m)];
+        const double av = lower ? At[swz(m, k)] : At[swz(k, m)];
         dmma(d0, d1, av, Bt[frag_colk(lane, h)]);
       }
     }
     const int o = ot * 8 + (lane >> 2);
     const int p0 = jt * 8 + 2 * (lane & 3);
+    // the X rows overlap tiles of L11 only (rows of factor order < T0): other warps
+    // may still read W / S^-1 tiles, which lie beyond toff(T0, 0)
     if (o < S.n1) {
-      if (p0 < S.n0) Xc[o * ld + (p0 < R.own_nat_lo ? p0 : p0 + S.n1)] = -d0;
-      if (p0 + 1 < S.n0) Xc[o * ld + (p0 + 1 < R.own_nat_lo ? p0 + 1 : p0 + 1 + S.n1)] = -d1;
+      if (p0 < S.n0) Xs[o * ld + (p0 < R.own_nat_lo ? p0 : p0 + S.n1)] = -d0;
+      if (p0 + 1 < S.n0) Xs[o * ld + (p0 + 1 < R.own_nat_lo ? p0 + 1 : p0 + 1 + S.n1)] = -d1;
     }
   }
   for (int t = tid; t < S.n1 * S.n1; t += kTcThreads) {
     const int o = t / S.n1, j = t - o * S.n1;
     const int i1 = o >= j ? o : j, j1 = o >= j ? j : o;
-    Xc[o * ld + R.own_nat_lo + j] = sm[toff(T0 + (i1 >> 3), T0 + (j1 >> 3)) + swz(i1 & 7, j1 & 7)];
+    Xs[o * ld + R.own_nat_lo + j] = sm[toff(T0 + (i1 >> 3), T0 + (j1 >> 3)) + swz(i1 & 7, j1 & 7)];
   }
   if (ld != n)
-    for (int o = tid; o < S.n1; o += kTcThreads) Xc[o * ld + n] = 0.0;
+    for (int o = tid; o < S.n1; o += kTcThreads) Xs[o * ld + n] = 0.0;
+  if (!stage) {  // written straight to HBM
+    PROBE(4)
+    TRACE(2)
+    return;
+  }
+  // generic-proxy shared-memory writes -> visible to the async (bulk copy) proxy
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
+  if (tid == 0) {
+    const unsigned bytes = (unsigned)(S.n1 * ld * sizeof(double));
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(X + x_off[cl]),
+                 "r"((unsigned)__cvta_generic_to_shared(Xs)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem read out: may exit
+  }
   PROBE(4)
   TRACE(2)
 }

@@ -52,9 +52,9 @@ for j in range(30):
     print(f"{j:2d} w0: {c0[j, 1] - c0[j, 0]:6d} {c0[j, 2] - c0[j, 1]:6d} {c0[j, 3] - c0[j, 2]:6d} | "
           f"dw: {cd[j, 1] - cd[j, 0]:6d} {cd[j, 2] - cd[j, 1]:6d} | col {c0[j, 3] - c0[j, 0]:6d}")
 wc = buf[512 + 65536 * 3 + 512:].reshape(32, 4)
-print("W phase, warp 0 (own row 0) per jt: [accumulate, wait bar 1, finish + L^-1 + store]; warp 15 S^-1 total")
+print("W phase (right-looking), warp 0 per column kt: [wait at the step barrier, chain update + finish, other updates]; S^-1 warps total")
 for jt in range(31):
     if wc[jt, 0] == 0:
         continue
-    print(f"jt {jt:2d}: {wc[jt, 1] - wc[jt, 0]:6d} {wc[jt, 2] - wc[jt, 1]:6d} {wc[jt, 3] - wc[jt, 2]:6d}")
+    print(f"kt {jt:2d}: {wc[jt, 1] - wc[jt, 0]:6d} {wc[jt, 2] - wc[jt, 1]:6d} {wc[jt, 3] - wc[jt, 2]:6d}")
 print("S^-1 (warp 15):", wc[31, 1] - wc[31, 0])
