@@ -234,6 +234,7 @@ __global__ void k_rasm_sizes(Geom g, Strip st, const int *__restrict__ cell_star
 // written to HBM in natural column order.
 constexpr int kAccWarps = kTcWarps - 2;  // warps 14, 15 alternate as diagonal warps
 constexpr int kWWarps = 12;              // W phase warps (the other four form S^-1)
+constexpr int kWSlots = 9;               // W tiles per warp and row group: ceil(T0 / Q) <= 25 / 3
 
 #ifdef RBF_PROBE
 __device__ long long g_probe[64][8];
@@ -518,39 +519,63 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
       __syncwarp();
       *reinterpret_cast<double2 *>(Ct + frag_acc(lane)) = make_double2(d0, d1);
     };
-    // C(r, jt) -= W(r, kt) L(kt, jt)
-    auto update = [&](int r, int kt, int jt) {
-      const double *Wt = sm + toff(T0 + r, kt), *Lk = sm + toff(kt, jt);
-      double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
-      dmma(d0, d1, Wt[f0], Lk[g0]);
-      dmma(e0, e1, Wt[f1], Lk[g1]);
-      double2 *cp = reinterpret_cast<double2 *>(sm + toff(T0 + r, jt) + frag_acc(lane));
-      double2 cv = *cp;
-      cv.x -= d0 + e0;
-      cv.y -= d1 + e1;
-      *cp = cv;
-    };
-    // the first column has no pending updates
-    if (T0 > 0)
-      for (int r = 0; r < T1; ++r)
-        if ((r + T1 * (T0 - 1)) % kWWarps == warp) finish(r, T0 - 1);
-    for (int kt = T0 - 1; kt >= 1; --kt) {
-      if (warp == 0) PW(kt, 0)
-      asm volatile("bar.sync 1, %0;" ::"n"(kWWarps * 32) : "memory");  // W(:, kt) final
-      if (warp == 0) PW(kt, 1)
-      // the chain: column kt-1's update from kt and its finish
-      for (int r = 0; r < T1; ++r)
-        if ((r + T1 * (kt - 1)) % kWWarps == warp) {
-          update(r, kt, kt - 1);
-          __syncwarp();
-          finish(r, kt - 1);
+    // Own tile rows in groups of up to four (rows are independent).  In a group of Tg
+    // rows, Q = 12 / Tg column classes: warp w < Q Tg owns row rg + w % Tg and the
+    // columns jt = q + Q s (q = w / Tg, slot s).  The contributions sum_{kt > jt}
+    // W(r,kt) L(kt,jt) of its tiles accumulate in registers, one column kt per step
+    // (the W(r,kt) fragments are loaded once per step for all slots), and a tile is
+    // finished in the step after its last contribution: (C(r,jt) - acc) L_d(jt)^-1.
+    for (int rg = 0; rg < T1; rg += 4) {
+      const int Tg = T1 - rg < 4 ? T1 - rg : 4, Q = kWWarps / Tg;
+      const bool active = warp < Q * Tg;
+      const int r = rg + warp % Tg, q = warp / Tg;
+      double acc0[kWSlots], acc1[kWSlots];
+#pragma unroll
+      for (int s = 0; s < kWSlots; ++s) acc0[s] = acc1[s] = 0.0;
+      // the last column has no contributions
+      if (active && T0 - 1 - q >= 0 && (T0 - 1 - q) % Q == 0) finish(r, T0 - 1);
+      // d = kt - 1 - q (column kt-1 is slot d / Q when d % Q == 0), dm = d mod Q, s_lim =
+      // slots with jt < kt - 1 = ceil(d / Q): kept incrementally (no division per step)
+      int d = T0 - 2 - q, dm = d >= 0 ? d % Q : 0, s_lim = d > 0 ? (d + Q - 1) / Q : 0;
+      for (int kt = T0 - 1; kt >= 1; --kt, --d) {
+        if (warp == 0) PW(kt, 0)
+        asm volatile("bar.sync 1, %0;" ::"n"(kWWarps * 32) : "memory");  // W(:, kt) final
+        if (warp == 0) PW(kt, 1)
+        if (active && d >= 0) {
+          const double *Wt = sm + toff(T0 + r, kt), *Lrow = sm + toff(kt, 0);
+          const double wa = Wt[f0], wb = Wt[f1];
+          // the chain first: column kt-1's last contribution and its finish
+          if (dm == 0) {
+#pragma unroll
+            for (int s = 0; s < kWSlots; ++s)
+              if (s == s_lim) {
+                const double *Lk = Lrow + (kt - 1) * 64;
+                dmma(acc0[s], acc1[s], wa, Lk[g0]);
+                dmma(acc0[s], acc1[s], wb, Lk[g1]);
+                double2 *cp = reinterpret_cast<double2 *>(sm + toff(T0 + r, kt - 1) + frag_acc(lane));
+                double2 cv = *cp;
+                cv.x -= acc0[s];
+                cv.y -= acc1[s];
+                *cp = cv;
+              }
+            __syncwarp();
+            finish(r, kt - 1);
+          }
+          if (warp == 0) PW(kt, 2)
+          // the other tiles' contributions from column kt (jt < kt - 1)
+#pragma unroll
+          for (int s = 0; s < kWSlots; ++s)
+            if (s < s_lim) {
+              const double *Lk = Lrow + (q + Q * s) * 64;
+              dmma(acc0[s], acc1[s], wa, Lk[g0]);
+              dmma(acc0[s], acc1[s], wb, Lk[g1]);
+            }
+          if (warp == 0) PW(kt, 3)
+          if (dm == 1 || (Q == 1 && d > 0)) --s_lim;  // ceil((d-1)/Q)
+          dm = dm == 0 ? Q - 1 : dm - 1;
         }
-      if (warp == 0) PW(kt, 2)
-      // the rest of this step's updates (off the chain)
-      for (int jt = kt - 2; jt >= 0; --jt)
-        for (int r = 0; r < T1; ++r)
-          if ((r + T1 * jt) % kWWarps == warp) update(r, kt, jt);
-      if (warp == 0) PW(kt, 3)
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kWWarps * 32) : "memory");  // the group's W final
     }
   } else {
     if (warp == kWWarps) PW(31, 0)
