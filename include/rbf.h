@@ -122,11 +122,18 @@ typedef struct {
  *                 a unique id seeds one communicator -- and it lives until process exit.
  *                 THREADS: any 128-byte key shared by the group's contexts. */
 enum { RBF_COMM_NONE = 0, RBF_COMM_NCCL = 1, RBF_COMM_THREADS = 2 };
+/* flags: RBF_DIST_NO_OVERLAP -- exchange the halo first, then apply the whole operator.
+ * Default (0): rbf_matvec / rbf_rasm_apply / rbf_solve overlap the halo exchange with the
+ * interior work -- the targets (matvec) and cells (RASM) whose stencils stay inside the
+ * strip are computed while the halo is in flight (NCCL on a high-priority stream), the
+ * ones next to a strip edge after it has arrived.  Results are bitwise
+ * identical either way. */
+enum { RBF_DIST_NO_OVERLAP = 1 };
 typedef struct {
   int32_t rank;
   int32_t nranks;
   int32_t comm;
-  int32_t reserved0;
+  int32_t flags;
   unsigned char nccl_id[128];
 } rbf_dist;
 

@@ -384,6 +384,7 @@ int rbf_setup(rbf_ctx **out, const double *xy, int64_t n, const rbf_params *p, c
     c->rank = d->rank;
     c->nranks = d->nranks;
     c->comm_mode = d->comm;
+    c->overlap = !(d->flags & RBF_DIST_NO_OVERLAP) && d->comm != RBF_COMM_NONE;
   }
   Geom &g = c->g;
   g.x0 = p->x0; g.y0 = p->y0; g.x1 = p->x1; g.y1 = p->y1;
@@ -491,23 +492,15 @@ int rbf_from_local(const rbf_ctx *c, const double *vl, double *vc, void *stream)
 int rbf_matvec(rbf_ctx *c, const double *w, double *y, void *stream) {
   if (!c || !w || !y) { set_error("NULL argument"); return RBF_EINVAL; }
   cudaStream_t s = (cudaStream_t)stream;
-  const double *src = w;
-  if (c->nranks > 1) {
-    RBF_TRY(halo_exchange(c, w, c->w_ext, true, s));
-    src = c->w_ext;
-  }
-  return launch_matvec(c, src, y, s);
+  if (c->nranks > 1) return dist_matvec(c, w, y, s);
+  return launch_matvec(c, w, y, s);
 }
 
 int rbf_rasm_apply(rbf_ctx *c, const double *r, double *z, void *stream) {
   if (!c || !r || !z) { set_error("NULL argument"); return RBF_EINVAL; }
   cudaStream_t s = (cudaStream_t)stream;
-  const double *src = r;
-  if (c->nranks > 1) {
-    RBF_TRY(halo_exchange(c, r, c->w_ext, false, s));
-    src = c->w_ext;
-  }
-  return launch_rasm_apply(c, src, z, s);
+  if (c->nranks > 1) return dist_rasm_apply(c, r, z, s);
+  return launch_rasm_apply(c, r, z, s);
 }
 
 int rbf_matvec_ext(rbf_ctx *c, const double *w_ext, double *y, void *stream) {

@@ -85,6 +85,13 @@ int comm_init(rbf_ctx *c, const rbf_dist *d) {
   if (c->nranks <= 1) return RBF_OK;
   if (c->comm_mode == RBF_COMM_THREADS) return thread_group_join(c, d);
   if (c->comm_mode != RBF_COMM_NCCL) return RBF_OK;
+  // the halo exchange runs on its own stream, at the highest priority, so the NCCL kernel
+  // gets SMs while the interior work fills the GPU
+  int lo = 0, hi = 0;
+  RBF_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  RBF_CUDA_TRY(cudaStreamCreateWithPriority(&c->s_comm, cudaStreamNonBlocking, hi));
+  RBF_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+  RBF_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
   const std::string key(reinterpret_cast<const char *>(d->nccl_id), 128);
   int dev = 0;
   RBF_CUDA_TRY(cudaGetDevice(&dev));
@@ -111,6 +118,12 @@ int comm_init(rbf_ctx *c, const rbf_dist *d) {
 
 void comm_destroy(rbf_ctx *c) {
   c->nccl = nullptr;  // the communicator stays with its id (process lifetime, above)
+  if (c->s_comm) cudaStreamSynchronize(c->s_comm);
+  if (c->ev_in) cudaEventDestroy(c->ev_in);
+  if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+  if (c->s_comm) cudaStreamDestroy(c->s_comm);
+  c->ev_in = c->ev_halo = nullptr;
+  c->s_comm = nullptr;
 }
 
 // RBF_COMM_THREADS exchange: publish this rank's send regions, copy the peers'.
@@ -146,6 +159,22 @@ static int halo_exchange_threads(rbf_ctx *c, const double *v_loc, double *v_ext,
   return st;
 }
 
+// NCCL send/recv of one halo (both neighbours) on stream `cs`: sends from the owned
+// vector, receives into the ext vector's halo slots
+static int nccl_halo(rbf_ctx *c, const double *v_loc, double *v_ext, const Halo *h, cudaStream_t cs) {
+  RBF_NCCL_TRY(ncclGroupStart());
+  for (int dir = 0; dir < 2; ++dir) {
+    const int peer = dir == 0 ? c->rank - 1 : c->rank + 1;
+    if (peer < 0 || peer >= c->nranks) continue;
+    if (h[dir].send_cnt > 0)
+      RBF_NCCL_TRY(ncclSend(v_loc + h[dir].send_off, (size_t)h[dir].send_cnt, ncclDouble, peer, c->nccl, cs));
+    if (h[dir].recv_cnt > 0)
+      RBF_NCCL_TRY(ncclRecv(v_ext + h[dir].recv_off, (size_t)h[dir].recv_cnt, ncclDouble, peer, c->nccl, cs));
+  }
+  RBF_NCCL_TRY(ncclGroupEnd());
+  return RBF_OK;
+}
+
 int halo_exchange(rbf_ctx *c, const double *v_loc, double *v_ext, bool matvec_depth,
                   cudaStream_t s) {
   if (c->nranks <= 1) return RBF_OK;
@@ -162,20 +191,69 @@ int halo_exchange(rbf_ctx *c, const double *v_loc, double *v_ext, bool matvec_de
   const long long own_off = c->s.own_lo - c->s.ext_lo;
   RBF_CUDA_TRY(cudaMemcpyAsync(v_ext + own_off, v_loc, sizeof(double) * n_loc(c),
                                cudaMemcpyDeviceToDevice, s));
-  const Halo *h = matvec_depth ? c->halo_mv : c->halo_pc;
-  RBF_NCCL_TRY(ncclGroupStart());
-  for (int dir = 0; dir < 2; ++dir) {
-    const int peer = dir == 0 ? c->rank - 1 : c->rank + 1;
-    if (peer < 0 || peer >= c->nranks) continue;
-    if (h[dir].send_cnt > 0)
-      RBF_NCCL_TRY(ncclSend(v_loc + h[dir].send_off, (size_t)h[dir].send_cnt, ncclDouble, peer,
-                            c->nccl, s));
-    if (h[dir].recv_cnt > 0)
-      RBF_NCCL_TRY(ncclRecv(v_ext + h[dir].recv_off, (size_t)h[dir].recv_cnt, ncclDouble, peer,
-                            c->nccl, s));
+  return nccl_halo(c, v_loc, v_ext, matvec_depth ? c->halo_mv : c->halo_pc, s);
+}
+
+// Start the halo exchange of v_loc into c->w_ext.  NCCL: on the context's comm stream
+// after the work already queued on s (the producer of v_loc); finish_halo makes s wait
+// for it.  THREADS: synchronous (host barrier + device copies on s).
+static int start_halo(rbf_ctx *c, const double *v_loc, const Halo *h, cudaStream_t s) {
+  if (c->comm_mode == RBF_COMM_THREADS) return halo_exchange_threads(c, v_loc, c->w_ext, h, s);
+  if (c->comm_mode != RBF_COMM_NCCL) {
+    set_error("virtual strip context (RBF_COMM_NONE) has no communicator: use the *_ext calls");
+    return RBF_EUNSUPPORTED;
   }
-  RBF_NCCL_TRY(ncclGroupEnd());
+  RBF_CUDA_TRY(cudaEventRecord(c->ev_in, s));
+  RBF_CUDA_TRY(cudaStreamWaitEvent(c->s_comm, c->ev_in, 0));
+  RBF_TRY(nccl_halo(c, v_loc, c->w_ext, h, c->s_comm));
+  RBF_CUDA_TRY(cudaEventRecord(c->ev_halo, c->s_comm));
   return RBF_OK;
+}
+
+static int finish_halo(rbf_ctx *c, cudaStream_t s) {
+  if (c->comm_mode == RBF_COMM_NCCL) RBF_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_halo, 0));
+  return RBF_OK;
+}
+
+// y = A_rc w across strips.  Overlapped: the owned records are packed from w_loc and
+// the interior lanes run while the halo is exchanged (NCCL: concurrently; THREADS: the
+// exchange follows them in stream order), then the halo records and the boundary lanes.
+int dist_matvec(rbf_ctx *c, const double *w_loc, double *y_loc, cudaStream_t s) {
+  const long long own_off = c->s.own_lo - c->s.ext_lo;
+  if (!c->overlap) {
+    RBF_TRY(halo_exchange(c, w_loc, c->w_ext, true, s));
+    return launch_matvec(c, c->w_ext, y_loc, s);
+  }
+  const bool nccl = c->comm_mode == RBF_COMM_NCCL;
+  if (nccl) RBF_TRY(start_halo(c, w_loc, c->halo_mv, s));
+  RBF_TRY(launch_pack_range(c, w_loc, n_loc(c), own_off, s));
+  RBF_TRY(launch_matvec(c, nullptr, y_loc, s, true, 1));
+  if (!nccl) RBF_TRY(start_halo(c, w_loc, c->halo_mv, s));
+  RBF_TRY(finish_halo(c, s));
+  for (int dir = 0; dir < 2; ++dir) {
+    const Halo &h = c->halo_mv[dir];
+    if (h.recv_cnt > 0) RBF_TRY(launch_pack_range(c, c->w_ext + h.recv_off, h.recv_cnt, h.recv_off, s));
+  }
+  return launch_matvec(c, nullptr, y_loc, s, true, 2);
+}
+
+// z = M^-1 r across strips, the same way: the owned part of r into the ext vector and
+// the interior cells while the halo (overlap_rings rows) is exchanged, then the cells
+// next to the strip edges.
+int dist_rasm_apply(rbf_ctx *c, const double *r_loc, double *z_loc, cudaStream_t s) {
+  if (!c->overlap) {
+    RBF_TRY(halo_exchange(c, r_loc, c->w_ext, false, s));
+    return launch_rasm_apply(c, c->w_ext, z_loc, s);
+  }
+  const bool nccl = c->comm_mode == RBF_COMM_NCCL;
+  if (nccl) RBF_TRY(start_halo(c, r_loc, c->halo_pc, s));
+  const long long own_off = c->s.own_lo - c->s.ext_lo;
+  RBF_CUDA_TRY(cudaMemcpyAsync(c->w_ext + own_off, r_loc, sizeof(double) * n_loc(c),
+                               cudaMemcpyDeviceToDevice, s));
+  RBF_TRY(launch_rasm_apply(c, c->w_ext, z_loc, s, 1));
+  if (!nccl) RBF_TRY(start_halo(c, r_loc, c->halo_pc, s));
+  RBF_TRY(finish_halo(c, s));
+  return launch_rasm_apply(c, c->w_ext, z_loc, s, 2);
 }
 
 int allgather_scalars(rbf_ctx *c, const double *send, double *recv, int count, cudaStream_t s) {

@@ -245,6 +245,11 @@ struct rbf_ctx {
   long long nlist_union = 0;    // sum over lanes of the union-list lengths
   // workspaces
   double *w_ext = nullptr;     // n_ext (multi-rank only)
+  // multi-rank overlap of the halo exchange with the interior work
+  int overlap = 0;             // 1 unless rbf_dist.flags has RBF_DIST_NO_OVERLAP
+  long long mv_int_chunks = 0; // matvec: chunks [0, mv_int_chunks) need no halo
+  cudaStream_t s_comm = nullptr;  // NCCL: high-priority stream of the halo exchange
+  cudaEvent_t ev_in = nullptr, ev_halo = nullptr;
   double *V = nullptr;         // (restart+1) x n_loc Krylov basis
   int V_m = 0;
   double *t1 = nullptr, *t2 = nullptr;
@@ -311,8 +316,11 @@ int launch_local_index(const rbf_ctx *c, int64_t *idx, cudaStream_t s);
 
 // matvec.cu
 int build_nlist(rbf_ctx *c, cudaStream_t s);
+int launch_pack_range(const rbf_ctx *c, const double *src, long long cnt, long long off, cudaStream_t s);
+// prepacked: w already in the records' w slot; part 0 = all targets, 1 = interior lanes,
+// 2 = boundary lanes (multi-rank overlap: only the boundary lanes read the halo)
 int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStream_t s,
-                  bool prepacked = false);  // prepacked: w already in the records' w slot
+                  bool prepacked = false, int part = 0);
 int launch_pack_w(const rbf_ctx *c, const double *w_ext, cudaStream_t s);
 
 // evaluate.cu
@@ -321,13 +329,20 @@ int evaluate(rbf_ctx *c, const double *q, long long m, const double *lam, double
 // rasm.cu
 int rasm_setup(rbf_ctx *c, cudaStream_t s);
 int probe_read(long long *out);  // RBF_PROBE builds only
-int launch_rasm_apply(const rbf_ctx *c, const double *r_ext, double *z_loc, cudaStream_t s);
+// part 0 = every cell, 1 = the interior cells, 2 = the cells within overlap_rings rows of
+// a strip edge with a neighbour rank (only these read the halo)
+int launch_rasm_apply(const rbf_ctx *c, const double *r_ext, double *z_loc, cudaStream_t s, int part = 0);
 
 // comm.cu
 int comm_init(rbf_ctx *c, const rbf_dist *d);
 void comm_destroy(rbf_ctx *c);
 int halo_exchange(rbf_ctx *c, const double *v_loc, double *v_ext, bool matvec_depth, cudaStream_t s);
 int allgather_scalars(rbf_ctx *c, const double *send, double *recv, int count, cudaStream_t s);
+// The two operators across strips: halo exchange overlapped with the interior work
+// (interior lanes / cells while the halo is in flight, then the boundary ones); without
+// overlap (RBF_DIST_NO_OVERLAP) exchange first, then the whole operator.
+int dist_matvec(rbf_ctx *c, const double *w_loc, double *y_loc, cudaStream_t s);
+int dist_rasm_apply(rbf_ctx *c, const double *r_loc, double *z_loc, cudaStream_t s);
 
 // krylov.cu
 int solve_gmres(rbf_ctx *c, const double *f, const rbf_gmres_params *g, double *x,

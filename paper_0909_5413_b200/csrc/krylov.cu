@@ -1013,20 +1013,12 @@ struct Op {
   cudaStream_t s;
   // y = A w (halo of w first)
   int matvec(const double *w, double *y, bool prepacked = false) {
-    const double *src = w;
-    if (c->nranks > 1) {
-      RBF_TRY(halo_exchange(c, w, c->w_ext, true, s));
-      src = c->w_ext;
-    }
-    return launch_matvec(c, src, y, s, prepacked);
+    if (c->nranks > 1) return dist_matvec(c, w, y, s);
+    return launch_matvec(c, w, y, s, prepacked);
   }
   int pc(const double *r, double *z) {
-    const double *src = r;
-    if (c->nranks > 1) {
-      RBF_TRY(halo_exchange(c, r, c->w_ext, false, s));
-      src = c->w_ext;
-    }
-    return launch_rasm_apply(c, src, z, s);
+    if (c->nranks > 1) return dist_rasm_apply(c, r, z, s);
+    return launch_rasm_apply(c, r, z, s);
   }
 };
 

@@ -184,9 +184,9 @@ __global__ __launch_bounds__(kMvThreads, MINB) void k_matvec(
     Geom g, long long nloc, long long own_off, const double4 *__restrict__ rec,
     const int4 *__restrict__ tgt, long long nlanes,
     const int *__restrict__ chunk_len, const long long *__restrict__ chunk_off,
-    const unsigned *__restrict__ list, double *__restrict__ y) {
+    const unsigned *__restrict__ list, double *__restrict__ y, long long lane0) {
   const int lane = threadIdx.x & 31;
-  const long long lt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long lt = lane0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long ch = lt >> 5;
   if ((ch << 5) >= nlanes) return;  // whole warp beyond the last chunk
   int t[G];
@@ -402,6 +402,77 @@ __global__ __launch_bounds__(kSortWin) void k_sort_lanes(const int *__restrict__
   if ((t & 31) == 0 && l < nlanes) chunk_len[l >> 5] = (key[t] + 3) & ~3;
 }
 
+// Interior / boundary split of the lanes (multi-rank overlap): a lane is a
+// boundary lane if one of its targets lies in the kh cell rows next to a strip edge that
+// has a neighbour rank (its stencil reaches the halo).  Interior lanes first (stable),
+// padded with empty lanes to a multiple of the sort window, then the boundary lanes:
+// chunks never mix the two, so the interior chunks can run while the halo is in flight.
+// Which lane computes a target never changes its sum (union lists in stencil order).
+__global__ void k_lane_class(Geom g, Strip st, int nranks, int rank, const double2 *__restrict__ xy,
+                             const int4 *__restrict__ tgt, long long nlanes, int *__restrict__ inner,
+                             int *__restrict__ outer) {
+  const long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (l >= nlanes) return;
+  const int4 v = tgt[l];
+  const int t[3] = {v.x, v.y, v.z};
+  const long long own_off = st.own_lo - st.ext_lo;
+  bool bnd = false;
+  for (int j = 0; j < 3; ++j) {
+    if (t[j] < 0) continue;
+    int cx = 0, cy = 0;
+    target_cell(g, xy[own_off + t[j]], cx, cy);
+    bnd |= (rank > 0 && cy < st.row_lo + g.kh) || (rank < nranks - 1 && cy >= st.row_hi - g.kh);
+  }
+  inner[l] = !bnd;
+  outer[l] = bnd;
+}
+
+__global__ void k_fill_int4(int4 *__restrict__ p, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) p[i] = make_int4(-1, -1, -1, -1);
+}
+
+static int split_lanes(rbf_ctx *c, cudaStream_t s, long long *lanes_io) {
+  const long long L = *lanes_io;
+  if (c->nranks <= 1 || L <= 0) return RBF_OK;
+  ScratchGuard sg(s);
+  int *fi = nullptr, *fo = nullptr, *cnt = nullptr;
+  RBF_TRY(sg.alloc(c, &fi, sizeof(int) * L));
+  RBF_TRY(sg.alloc(c, &fo, sizeof(int) * L));
+  RBF_TRY(sg.alloc(c, &cnt, sizeof(int) * 2));
+  k_lane_class<<<(int)((L + 255) / 256), 256, 0, s>>>(c->g, c->s, c->nranks, c->rank, c->xy_ext, c->lane_tgt,
+                                                      L, fi, fo);
+  count_launch(1);
+  size_t tb = 0;
+  RBF_CUDA_TRY(cub::DeviceSelect::Flagged(nullptr, tb, c->lane_tgt, fi, c->lane_tgt, cnt, (int)L, s));
+  void *tmp = nullptr;
+  RBF_TRY(sg.alloc(c, &tmp, tb));
+  // count the interior lanes first (to place the boundary block after the padding)
+  int4 *scratch = nullptr;
+  RBF_TRY(sg.alloc(c, &scratch, sizeof(int4) * (size_t)L));
+  RBF_CUDA_TRY(cub::DeviceSelect::Flagged(tmp, tb, c->lane_tgt, fi, scratch, cnt, (int)L, s));
+  int h_in = 0;
+  RBF_CUDA_TRY(cudaMemcpyAsync(&h_in, cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  const long long pad = (h_in + kSortWin - 1) / kSortWin * kSortWin;
+  const long long L2 = pad + (L - h_in);
+  int4 *out = nullptr;
+  RBF_TRY(dalloc(c, (void **)&out, sizeof(int4) * (size_t)L2, s));
+  RBF_CUDA_TRY(cudaMemcpyAsync(out, scratch, sizeof(int4) * (size_t)h_in, cudaMemcpyDeviceToDevice, s));
+  if (pad > h_in) {
+    k_fill_int4<<<(int)((pad - h_in + 255) / 256), 256, 0, s>>>(out + h_in, pad - h_in);
+    count_launch(1);
+  }
+  RBF_CUDA_TRY(cub::DeviceSelect::Flagged(tmp, tb, c->lane_tgt, fo, out + pad, cnt + 1, (int)L, s));
+  count_launch(4);
+  RBF_CUDA_TRY(cudaGetLastError());
+  dfree(c->lane_tgt, s);
+  c->lane_tgt = out;
+  c->mv_int_chunks = pad / 32;
+  *lanes_io = L2;
+  return RBF_OK;
+}
+
 static int env_int(const char *name, int dflt) {
   const char *v = getenv(name);
   return (v && *v) ? atoi(v) : dflt;
@@ -426,6 +497,8 @@ int build_nlist(rbf_ctx *c, cudaStream_t s) {
   if (nl <= 0) return RBF_OK;
   long long lanes = (nl + G - 1) / G;
   if (G >= 2 && !getenv("RBF_MV_CONSECUTIVE")) RBF_TRY(pair_targets(c, G, s, &lanes));
+  c->mv_int_chunks = 0;
+  if (c->overlap && c->lane_tgt) RBF_TRY(split_lanes(c, s, &lanes));
   c->mv_lanes = lanes;
   c->nchunks = (int)((lanes + 31) / 32);
   const int nch = c->nchunks;
@@ -493,30 +566,41 @@ int build_nlist(rbf_ctx *c, cudaStream_t s) {
 }
 
 int launch_pack_w(const rbf_ctx *c, const double *w_ext, cudaStream_t s) {
-  const long long ne = n_ext(c);
-  if (ne > 0) {
-    k_pack_w<<<(int)((ne + 255) / 256), 256, 0, s>>>(w_ext, ne, c->rec);
+  return launch_pack_range(c, w_ext, n_ext(c), 0, s);
+}
+
+// w slot of records [off, off + cnt) of the ext range from src[0 .. cnt)
+int launch_pack_range(const rbf_ctx *c, const double *src, long long cnt, long long off, cudaStream_t s) {
+  if (cnt > 0) {
+    k_pack_w<<<(int)((cnt + 255) / 256), 256, 0, s>>>(src, cnt, c->rec + off);
     count_launch(1);
   }
   RBF_CUDA_TRY(cudaGetLastError());
   return RBF_OK;
 }
 
-int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStream_t s, bool prepacked) {
+int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStream_t s, bool prepacked,
+                  int part) {
   const long long nl = n_loc(c);
   if (nl <= 0) return RBF_OK;
   if (!prepacked) RBF_TRY(launch_pack_w(c, w_ext, s));
   const int G = c->mv_g;
+  // part 0: every lane; 1: the interior chunks; 2: the boundary chunks (split_lanes)
+  const long long split = 32LL * c->mv_int_chunks < c->mv_lanes ? 32LL * c->mv_int_chunks : c->mv_lanes;
+  const long long lane0 = part == 2 ? split : 0;
+  const long long lane1 = part == 1 ? split : c->mv_lanes;
   const long long lanes = c->mv_lanes;
-  const int blocks = (int)((lanes + kMvThreads - 1) / kMvThreads);
+  if (lane1 <= lane0) return RBF_OK;
+  const int blocks = (int)((lane1 - lane0 + kMvThreads - 1) / kMvThreads);
   const long long own_off = c->s.own_lo - c->s.ext_lo;
 #define RBF_MV(GG, DEG, U, MB, ...)                                                            \
   k_matvec<GG, DEG, U, MB, ##__VA_ARGS__><<<blocks, kMvThreads, 0, s>>>(c->g, nl, own_off, c->rec, \
-                                                     GG >= 2 ? c->lane_tgt : nullptr, lanes, c->chunk_len,  \
-                                                     c->chunk_off, c->nlist, y_loc)
+                                                     GG >= 2 ? c->lane_tgt : nullptr, lane1, c->chunk_len,  \
+                                                     c->chunk_off, c->nlist, y_loc, lane0)
   // Measured alternatives: profiles/r01_matvec_variants_cfg2.txt (2 gathers in flight,
   // 2/4/5 CTAs per SM, L1 prefetch of the next group's records, G = 1 or 3, the
   // degree-10 exp: none faster than the default).
+  (void)lanes;
   if (G == 1) RBF_MV(1, kExpDeg, 4, 1);
   else if (G == 3) RBF_MV(3, kExpDeg, 4, 1);
   else if (c->mv_var == 1) RBF_MV(2, 9, 4, 1);

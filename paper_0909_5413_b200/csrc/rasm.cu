@@ -1069,10 +1069,11 @@ __global__ void k_lu_sizes(Geom g, Strip st, const int *__restrict__ cell_start,
 // current row's reduction, so the HBM stream never waits on the gather.
 __global__ __launch_bounds__(kRaThreads) void k_rasm_apply(
     Geom g, Strip st, const int *__restrict__ cell_start, const long long *__restrict__ x_off,
-    const double *__restrict__ X, const double *__restrict__ u, double *__restrict__ z, OvList ov) {
+    const double *__restrict__ X, const double *__restrict__ u, double *__restrict__ z, OvList ov,
+    int cl_split, int cl_skip) {
   extern __shared__ double su[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int cl = blockIdx.x;
+  const int cl = (int)blockIdx.x < cl_split ? (int)blockIdx.x : (int)blockIdx.x + cl_skip;
   const int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
   const int key = cy * g.ncx + cx;
   const int o0 = cell_start[key], n_own = cell_start[key + 1] - o0;
@@ -1476,11 +1477,12 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
   return RBF_OK;
 }
 
-int launch_rasm_apply(const rbf_ctx *c, const double *r_ext, double *z_loc, cudaStream_t s) {
+int launch_rasm_apply(const rbf_ctx *c, const double *r_ext, double *z_loc, cudaStream_t s, int part) {
   const int ncl = owned_cells(c);
   if (ncl <= 0 || c->nsub == 0) return RBF_OK;
   const size_t smem = sizeof(double) * (size_t)(c->max_ov + 2);
-  if (c->g.asm_full) {  // Eq.(8): local solutions, then the per-point sums
+  if (c->g.asm_full) {  // Eq.(8): local solutions, then the per-point sums (single rank)
+    if (part == 2) return RBF_OK;
     RBF_TRY(ensure_dyn_smem((const void *)k_asm_local, smem));
     k_asm_local<<<ncl, kRaThreads, smem, s>>>(c->g, c->s, c->cell_start, c->x_off, c->asm_toff, c->X,
                                               r_ext, c->asm_t, ov_of(c));
@@ -1490,9 +1492,26 @@ int launch_rasm_apply(const rbf_ctx *c, const double *r_ext, double *z_loc, cuda
     RBF_CUDA_TRY(cudaGetLastError());
     return RBF_OK;
   }
+  // cell rows next to a strip edge with a neighbour rank read the halo (rings rows)
+  const int nrows = c->s.row_hi - c->s.row_lo, ncx = c->g.ncx;
+  int rb = (c->nranks > 1 && c->rank > 0) ? c->g.rings : 0;
+  int ra = (c->nranks > 1 && c->rank < c->nranks - 1) ? c->g.rings : 0;
+  rb = rb < nrows ? rb : nrows;
+  ra = ra < nrows - rb ? ra : nrows - rb;
+  int grid = ncl, split = ncl, skip = 0;
+  if (part == 1) {
+    grid = (nrows - ra - rb) * ncx;
+    split = 0;
+    skip = rb * ncx;
+  } else if (part == 2) {
+    grid = (rb + ra) * ncx;
+    split = rb * ncx;
+    skip = (nrows - ra - rb) * ncx;
+  }
+  if (grid <= 0) return RBF_OK;
   RBF_TRY(ensure_dyn_smem((const void *)k_rasm_apply, smem));
-  k_rasm_apply<<<ncl, kRaThreads, smem, s>>>(c->g, c->s, c->cell_start, c->x_off, c->X, r_ext,
-                                             z_loc, ov_of(c));
+  k_rasm_apply<<<grid, kRaThreads, smem, s>>>(c->g, c->s, c->cell_start, c->x_off, c->X, r_ext, z_loc,
+                                              ov_of(c), split, skip);
   count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
   return RBF_OK;

@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(_HERE, "librbf.so")
 
 RBF_OK, RBF_NOT_CONVERGED = 0, 2
 RBF_COMM_NONE, RBF_COMM_NCCL, RBF_COMM_THREADS = 0, 1, 2
+RBF_DIST_NO_OVERLAP = 1
 _ERRORS = {-1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENCCL", -5: "EFACTOR", -6: "ENUMERIC",
            -7: "EUNSUPPORTED"}
 
@@ -34,7 +35,7 @@ class Params(C.Structure):
 
 class Dist(C.Structure):
     _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("comm", C.c_int32),
-                ("reserved0", C.c_int32), ("nccl_id", C.c_ubyte * 128)]
+                ("flags", C.c_int32), ("nccl_id", C.c_ubyte * 128)]
 
 
 class GmresParams(C.Structure):
@@ -207,7 +208,7 @@ class Context:
 
     def __init__(self, xy, sigma, cell, rc, rings=1, box=(-1.0, -1.0, 1.0, 1.0), *, rank=0,
                  nranks=1, comm="none", nccl_id: bytes | None = None, stream=None,
-                 overlap_width=0.0, trunc_width=0.0, schwarz="rasm"):
+                 overlap_width=0.0, trunc_width=0.0, schwarz="rasm", overlap=True):
         import torch
 
         if not (isinstance(xy, torch.Tensor) and xy.is_cuda and xy.dtype == torch.float64):
@@ -218,7 +219,7 @@ class Context:
         dist = None
         if nranks > 1 or comm == "nccl":
             mode = {"nccl": RBF_COMM_NCCL, "threads": RBF_COMM_THREADS, "none": RBF_COMM_NONE}[comm]
-            dist = Dist(int(rank), int(nranks), mode, 0)
+            dist = Dist(int(rank), int(nranks), mode, 0 if overlap else RBF_DIST_NO_OVERLAP)
             if nccl_id is not None:
                 C.memmove(dist.nccl_id, nccl_id, 128)
         self._h = C.c_void_p()

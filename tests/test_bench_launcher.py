@@ -3,6 +3,7 @@ script under torch.distributed.run with N ranks (one process per GPU), each seei
 rank environment the driver's own torchrun launch provides."""
 import json
 import os
+import re
 import subprocess
 import sys
 
@@ -16,7 +17,8 @@ def test_bench_gpus_flag_spawns_ranks():
                           "--dry-run-ranks"], capture_output=True, text=True, env=env,
                          timeout=300, cwd=ROOT)
     assert out.returncode == 0, out.stderr
-    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    # the two ranks print concurrently: their lines may interleave, so parse objects
+    lines = [json.loads(m) for m in re.findall(r"\{[^{}]*\}", out.stdout)]
     assert sorted(int(d["RANK"]) for d in lines) == [0, 1]
     assert sorted(int(d["LOCAL_RANK"]) for d in lines) == [0, 1]
     assert all(d["WORLD_SIZE"] == "2" and d["MASTER_ADDR"] == "127.0.0.1" for d in lines)

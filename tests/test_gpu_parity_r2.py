@@ -115,3 +115,52 @@ def test_pairwise_mgs_orthogonality_vs_oracle_mgs():
     # the first basis vectors (before rounding drives the two recurrences apart) agree
     for j in range(6):
         assert rel(Vg[j], Vo[j]) <= 1e-8
+
+
+# ------------------------------------------------------------------ halo / interior overlap
+# The multi-strip operators compute the interior lanes / cells while the halo is in
+# flight and the boundary ones after it (include/rbf.h RBF_DIST_NO_OVERLAP).  On the
+# in-process transport (RBF_COMM_THREADS) the same split runs in stream order; results
+# must be bitwise identical with and without the split, and to one strip (reading Q20).
+
+def _threads(nranks, body):
+    from test_gpu_parity import _run_threads
+
+    return _run_threads(nranks, body)
+
+
+OVERLAP_CASES = [
+    ("lattice60", dict(wl=W.make_lattice(60, jitter_frac=0.1, seed=5), rings=1, tw=0.0), 2),
+    ("lattice60-3", dict(wl=W.make_lattice(60, jitter_frac=0.1, seed=5), rings=1, tw=0.0), 3),
+    ("rings2", dict(wl=W.make_lattice(80, jitter_frac=0.1, seed=6), rings=2, tw=0.0), 2),
+    ("tbox", dict(wl=W.make_lattice(80, jitter_frac=0.1, seed=6), rings=1, tw=None), 4),
+]
+
+
+@pytest.mark.parametrize("name,case,nranks", OVERLAP_CASES, ids=[c[0] for c in OVERLAP_CASES])
+def test_threads_overlap_bitwise(name, case, nranks):
+    wl, rings = case["wl"], case["rings"]
+    tw = case["tw"] if case["tw"] is not None else 1.5 * wl.sigma
+    rng = np.random.default_rng(8)
+    w = torch.from_numpy(rng.standard_normal(wl.n)).cuda()
+    xy = torch.from_numpy(wl.xy).cuda()
+    with P.Context(xy, wl.sigma, wl.cell, wl.rc, rings, wl.box, trunc_width=tw) as c1:
+        y1 = c1.from_local(c1.matvec(c1.to_local(w))).cpu().numpy()
+        z1 = c1.from_local(c1.rasm_apply(c1.to_local(w))).cpu().numpy()
+    out = {}
+    for ov in (True, False):
+        def body(r, key, st, ov=ov):
+            with P.Context(xy, wl.sigma, wl.cell, wl.rc, rings, wl.box, rank=r, nranks=nranks,
+                           comm="threads", nccl_id=key, stream=st, trunc_width=tw, overlap=ov) as c:
+                wl_ = c.to_local(w)
+                y = c.from_local(c.matvec(wl_)).cpu().numpy()
+                z = c.from_local(c.rasm_apply(wl_)).cpu().numpy()
+                lam, rep = c.solve(c.to_local(torch.from_numpy(wl.f).cuda()), rtol=1e-11, max_iters=200)
+                return y, z, c.from_local(lam).cpu().numpy(), rep.history
+        out[ov] = _threads(nranks, body)
+    for ov in (True, False):
+        assert np.array_equal(sum(r[0] for r in out[ov]), y1)
+        assert np.array_equal(sum(r[1] for r in out[ov]), z1)
+    # the whole multi-strip solve is bitwise the same with and without the split
+    assert np.array_equal(sum(r[2] for r in out[True]), sum(r[2] for r in out[False]))
+    assert np.array_equal(out[True][0][3], out[False][0][3])
