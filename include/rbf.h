@@ -246,10 +246,18 @@ int rbf_interpolate_host(const double *xy_host, const double *f_host, int64_t n,
  *  q_xy_dev        m x 2 interleaved query points (any order), inside the box.
  *  lambda_loc_dev  weights, rank-local library order (e.g. rbf_solve's output).
  *  s_dev           m values, in the order of the queries.
- * Single-rank contexts only (RBF_EUNSUPPORTED otherwise); EINVAL for a query that is
- * non-finite or outside the box (message names the first one).  Synchronises. */
+ * Multi-rank: every rank passes all m queries; each evaluates the queries in its strip of
+ * cell rows (its weights plus the matvec halo, exchanged here) and the results are summed
+ * over the ranks (each query has one nonzero contribution, so the sum is exact), so every
+ * rank receives all m values.  Collective: all ranks call it.  EINVAL for a query that is
+ * non-finite or outside the box (message names the first one); EUNSUPPORTED on a virtual
+ * strip (RBF_COMM_NONE).  Synchronises. */
 int rbf_evaluate(rbf_ctx *ctx, const double *q_xy_dev, int64_t m, const double *lambda_loc_dev,
                  double *s_dev, void *stream);
+
+/* In-cutoff (query, source) pair count of an evaluation (all ranks; for Gpairs/s). */
+int rbf_evaluate_count_pairs(rbf_ctx *ctx, const double *q_xy_dev, int64_t m, int64_t *n_pairs,
+                             void *stream);
 
 /* In-cutoff pair count of this rank's rows (for Gpairs/s; synchronises). */
 int rbf_count_pairs(rbf_ctx *ctx, int64_t *n_pairs, void *stream);

@@ -547,6 +547,14 @@ int rbf_evaluate(rbf_ctx *c, const double *q, int64_t m, const double *lam, doub
   return evaluate(c, q, m, lam, s, (cudaStream_t)stream);
 }
 
+int rbf_evaluate_count_pairs(rbf_ctx *c, const double *q, int64_t m, int64_t *n_pairs, void *stream) {
+  if (!c || (!q && m > 0) || !n_pairs) { set_error("rbf_evaluate_count_pairs: NULL argument"); return RBF_EINVAL; }
+  unsigned long long n = 0;
+  RBF_TRY(evaluate(c, q, m, nullptr, nullptr, (cudaStream_t)stream, &n));
+  *n_pairs = (int64_t)n;
+  return RBF_OK;
+}
+
 int rbf_count_pairs(rbf_ctx *c, int64_t *np, void *stream) {
   if (!c || !np) { set_error("NULL argument"); return RBF_EINVAL; }
   long long v = 0;

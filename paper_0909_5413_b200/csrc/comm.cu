@@ -283,3 +283,41 @@ int allgather_scalars(rbf_ctx *c, const double *send, double *recv, int count, c
 }
 
 }  // namespace rbf
+
+namespace rbf {
+
+__global__ void k_add_vec(double *__restrict__ v, const double *__restrict__ a, long long n, int first) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) v[i] = first ? a[i] : v[i] + a[i];
+}
+
+int allreduce_vector(rbf_ctx *c, double *v, long long count, cudaStream_t s) {
+  if (c->nranks <= 1 || count == 0) return RBF_OK;
+  if (c->comm_mode == RBF_COMM_NCCL) {
+    RBF_NCCL_TRY(ncclAllReduce(v, v, (size_t)count, ncclDouble, ncclSum, c->nccl, s));
+    return RBF_OK;
+  }
+  if (c->comm_mode != RBF_COMM_THREADS) {
+    set_error("virtual strip context (RBF_COMM_NONE) cannot reduce across strips");
+    return RBF_EUNSUPPORTED;
+  }
+  ThreadGroup *G = c->tgroup;
+  ScratchGuard sg(s);
+  double *tmp = nullptr;
+  RBF_TRY(sg.alloc(nullptr, &tmp, sizeof(double) * (size_t)count));
+  RBF_CUDA_TRY(cudaMemcpyAsync(tmp, v, sizeof(double) * (size_t)count, cudaMemcpyDeviceToDevice, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  G->ptr[0][c->rank] = tmp;
+  G->barrier();
+  const int blocks = (int)((count + 255) / 256);
+  for (int r = 0; r < c->nranks; ++r) {  // rank order
+    k_add_vec<<<blocks, 256, 0, s>>>(v, G->ptr[0][r], count, r == 0);
+    count_launch(1);
+  }
+  int st = cudaStreamSynchronize(s) == cudaSuccess ? RBF_OK : RBF_ECUDA;
+  if (st != RBF_OK) set_error("RBF_COMM_THREADS vector all-reduce failed");
+  G->barrier();  // the peers' tmp buffers may be freed from here on
+  return st;
+}
+
+}  // namespace rbf

@@ -324,7 +324,9 @@ int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStre
 int launch_pack_w(const rbf_ctx *c, const double *w_ext, cudaStream_t s);
 
 // evaluate.cu
-int evaluate(rbf_ctx *c, const double *q, long long m, const double *lam, double *out, cudaStream_t s);
+// pairs_out: count the in-cutoff (query, source) pairs instead of evaluating
+int evaluate(rbf_ctx *c, const double *q, long long m, const double *lam, double *out, cudaStream_t s,
+             unsigned long long *pairs_out = nullptr);
 
 // rasm.cu
 int rasm_setup(rbf_ctx *c, cudaStream_t s);
@@ -338,6 +340,10 @@ int comm_init(rbf_ctx *c, const rbf_dist *d);
 void comm_destroy(rbf_ctx *c);
 int halo_exchange(rbf_ctx *c, const double *v_loc, double *v_ext, bool matvec_depth, cudaStream_t s);
 int allgather_scalars(rbf_ctx *c, const double *send, double *recv, int count, cudaStream_t s);
+// v (count doubles, device) <- the sum of every rank's v, summed in rank order (THREADS)
+// or by ncclAllReduce (callers use it only where at most one rank holds a nonzero per
+// entry, so the sum is exact in any order)
+int allreduce_vector(rbf_ctx *c, double *v, long long count, cudaStream_t s);
 // The two operators across strips: halo exchange overlapped with the interior work
 // (interior lanes / cells while the halo is in flight, then the boundary ones); without
 // overlap (RBF_DIST_NO_OVERLAP) exchange first, then the whole operator.

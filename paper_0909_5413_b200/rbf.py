@@ -59,7 +59,7 @@ EXPORTS = ["rbf_get_nccl_id", "rbf_setup", "rbf_local_count", "rbf_ext_count", "
            "rbf_interpolate_host", "rbf_count_pairs", "rbf_dot", "rbf_plan_strips",
            "rbf_last_error", "rbf_destroy", "rbf_info", "rbf_launch_count", "rbf_setup_times",
            "rbf_plan_halo", "rbf_evaluate", "rbf_matvec_stats", "rbf_lu_stats",
-           "rbf_debug_poison_shared", "rbf_debug_krylov_basis"]
+           "rbf_debug_poison_shared", "rbf_debug_krylov_basis", "rbf_evaluate_count_pairs"]
 
 _lib = None
 
@@ -91,6 +91,7 @@ def lib() -> C.CDLL:
                                                p, C.POINTER(Report), p]),
             "rbf_count_pairs": (C.c_int, [p, p, p]),
             "rbf_evaluate": (C.c_int, [p, p, i64, p, p, p]),
+            "rbf_evaluate_count_pairs": (C.c_int, [p, p, i64, C.POINTER(i64), p]),
             "rbf_matvec_stats": (C.c_int, [p, p]),
             "rbf_lu_stats": (C.c_int, [p, p]),
             "rbf_debug_poison_shared": (C.c_int, []),
@@ -283,6 +284,13 @@ class Context:
         _check(lib().rbf_evaluate(self._h, _ptr(q_xy.contiguous()), m, _ptr(lam), _ptr(s),
                                   _stream(self._stream)))
         return s
+
+    def evaluate_count_pairs(self, q_xy) -> int:
+        """In-cutoff (query, source) pairs of an evaluation at q_xy (rbf_evaluate_count_pairs)."""
+        v = C.c_int64()
+        _check(lib().rbf_evaluate_count_pairs(self._h, _ptr(q_xy.contiguous()), int(q_xy.shape[0]),
+                                              C.byref(v), _stream(self._stream)))
+        return v.value
 
     def rasm_apply(self, r, z=None):
         z = self._new(self.n_local) if z is None else z
