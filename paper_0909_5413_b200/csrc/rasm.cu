@@ -375,123 +375,14 @@ __device__ __forceinline__ void a_entries(const double2 *pos, const TileShape &S
   v1 = v[1];
 }
 
-__global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
-    Geom g, Strip st, const double2 *__restrict__ xy, const int *__restrict__ cell_start,
-    const long long *__restrict__ x_off, double *__restrict__ X, int *__restrict__ counts,
-    int *__restrict__ glist, OvList ov) {
-  TRACE(1)
-  extern __shared__ __align__(16) double sm[];
-  __shared__ Runs R;
-  __shared__ int s_fail;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int cl = blockIdx.x;
-  const int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
-  if (tid == 0) {
-    sub_runs(g, cell_start, ov, cl, cx, cy, R);
-    s_fail = 0;
-  }
-  __syncthreads();
-  if (R.n_own == 0) return;
-  const TileShape S(R.n_ov, R.n_own);
-  if (!S.fits_tc()) return;  // handled by k_rasm_setup_lu
-  const int T = S.T, T0 = S.T0, T1 = S.T1, N = S.N;
-  PROBE(0)
-  double *rdiag = sm + T * (T + 1) / 2 * 64;
-  double2 *pos = reinterpret_cast<double2 *>(rdiag + T * 8 + 4 * 64);  // after rdiag and wpart
-
-  // ---- positions in factor order, then A_c = R_c A_rc R_c^T (reading Q10)
-  for (int p = tid; p < N; p += kTcThreads) {
-    const int gi = fac_to_global(R, S, p);
-    pos[p] = (gi >= 0) ? xy[gi - st.ext_lo] : make_double2(0.0, 0.0);
-  }
-  __syncthreads();
-  __syncthreads();
-
-  PROBE(1)
-  // ---- software-pipelined left-looking Cholesky over tile columns
-  AccSet acc[2];
-  acc[0].zero();
-  acc[1].zero();
-  // A entries of the tiles finished in the first step (column 0)
-  if (warp < kAccWarps) {
-#pragma unroll
-    for (int m = 0; m < 2; ++m) {
-      const int it = 1 + warp + kAccWarps * m;
-      if (it < T) a_entries(pos, S, g, it, 0, lane, acc[m].v0, acc[m].v1);
-    }
-  } else if (warp == kAccWarps) {
-    a_entries(pos, S, g, 0, 0, lane, acc[0].v0, acc[0].v1);
-  }
-  for (int j = 0; j < T; ++j) {
-    const int dw = kAccWarps + (j & 1);  // diagonal warp of column j
-    if (warp == 0) PCOL(0, j, 0)
-    if (warp == dw) PCOL(1, j, 0)
-    if (warp < kAccWarps) {
-      // step 1: finish column j (tiles it > j) with the kt = j-1 term
-#pragma unroll
-      for (int m = 0; m < 2; ++m) {
-        const int it = j + 1 + warp + kAccWarps * m;
-        if (it < T) {
-          if (j >= 1) acc_range(acc[m], sm, it, j, j - 1, j, lane);
-          acc_finish(acc[m], sm, it, j, lane);
-        }
-      }
-      // step 2: accumulate column j+1 (tiles it > j+1) over kt < j
-#pragma unroll
-      for (int m = 0; m < 2; ++m) {
-        const int it = j + 2 + warp + kAccWarps * m;
-        acc[m].zero();
-        if (it < T && j + 1 < T) {
-          a_entries(pos, S, g, it, j + 1, lane, acc[m].v0, acc[m].v1);
-          acc_range(acc[m], sm, it, j + 1, 0, j, lane);
-        }
-      }
-    } else if (warp == dw) {
-      // finish the diagonal tile (its sum over kt < j-1 was accumulated last step)
-      if (j >= 1) acc_range(acc[0], sm, j, j, j - 1, j, lane);
-      acc_finish(acc[0], sm, j, j, lane);
-      __syncwarp();
-      PCOL(1, j, 1)
-      if (diag_factor(sm, rdiag, j, lane) && lane == 0) s_fail = 1;
-      PCOL(1, j, 2)
-    } else if (j + 1 < T) {
-      // the other diagonal warp accumulates the next diagonal tile over kt < j
-      acc[0].zero();
-      a_entries(pos, S, g, j + 1, j + 1, lane, acc[0].v0, acc[0].v1);
-      acc_range(acc[0], sm, j + 1, j + 1, 0, j, lane);
-    }
-    if (warp == 0) PCOL(0, j, 1)
-    __syncthreads();
-    if (warp == 0) PCOL(0, j, 2)
-    if (s_fail) break;  // uniform
-    // step 4: panel L(it, j) = C(it, j) L_d^-T  (B[k][n] = Linv[n][k])
-    if (warp < kAccWarps) {
-      const double *D = sm + toff(j, j);
-#pragma unroll
-      for (int m = 0; m < 2; ++m) {
-        const int it = j + 1 + warp + kAccWarps * m;
-        if (it < T) {
-          double *Ct = sm + toff(it, j);
-          double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int k = 4 * h + (lane & 3), n = lane >> 2;
-            const double bv = (n > k) ? D[swz(k, n)] : (n == k ? rdiag[j * 8 + k] : 0.0);
-            dmma(d0, d1, Ct[frag_rowk(lane, h)], bv);
-          }
-          __syncwarp();
-          *reinterpret_cast<double2 *>(Ct + frag_acc(lane)) = make_double2(d0, d1);
-        }
-      }
-    }
-    __syncthreads();
-    if (warp == 0) PCOL(0, j, 3)
-  }
-  if (s_fail) {  // Cholesky broke down: redo this cell with LU (reading Q11)
-    if (tid == 0) glist[atomicAdd(&counts[3], 1)] = cl;
-    return;
-  }
-
+// The phases after the factorisation: W = L21 L11^-1,
+// S^-1 = L22^-T L22^-1, and X_c = S^-1 [-W, I] written to HBM.
+__device__ __forceinline__ void setup_post(double *sm, double *rdiag, double2 *pos, const TileShape &S,
+                                           const Runs &R, const Geom &g, double *__restrict__ X,
+                                           const long long *__restrict__ x_off, int cl, int tid,
+                                           int lane, int warp) {
+  const int T = S.T, T0 = S.T0, T1 = S.T1;
+  (void)T;
   PROBE(2)
   // ---- W = L21 L11^-1 (warps 0..11) and S^-1 = L22^-T L22^-1 (warps 12..15), concurrently.
   //
@@ -728,6 +619,126 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
   }
   PROBE(4)
   TRACE(2)
+}
+
+__global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
+    Geom g, Strip st, const double2 *__restrict__ xy, const int *__restrict__ cell_start,
+    const long long *__restrict__ x_off, double *__restrict__ X, int *__restrict__ counts,
+    int *__restrict__ glist, OvList ov) {
+  TRACE(1)
+  extern __shared__ __align__(16) double sm[];
+  __shared__ Runs R;
+  __shared__ int s_fail;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cl = blockIdx.x;
+  const int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
+  if (tid == 0) {
+    sub_runs(g, cell_start, ov, cl, cx, cy, R);
+    s_fail = 0;
+  }
+  __syncthreads();
+  if (R.n_own == 0) return;
+  const TileShape S(R.n_ov, R.n_own);
+  if (!S.fits_tc()) return;  // handled by k_rasm_setup_lu
+  const int T = S.T, N = S.N;
+  PROBE(0)
+  double *rdiag = sm + T * (T + 1) / 2 * 64;
+  double2 *pos = reinterpret_cast<double2 *>(rdiag + T * 8 + 4 * 64);  // after rdiag and wpart
+
+  // ---- positions in factor order, then A_c = R_c A_rc R_c^T (reading Q10)
+  for (int p = tid; p < N; p += kTcThreads) {
+    const int gi = fac_to_global(R, S, p);
+    pos[p] = (gi >= 0) ? xy[gi - st.ext_lo] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  __syncthreads();
+
+  PROBE(1)
+  // ---- software-pipelined left-looking Cholesky over tile columns
+  AccSet acc[2];
+  acc[0].zero();
+  acc[1].zero();
+  // A entries of the tiles finished in the first step (column 0)
+  if (warp < kAccWarps) {
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int it = 1 + warp + kAccWarps * m;
+      if (it < T) a_entries(pos, S, g, it, 0, lane, acc[m].v0, acc[m].v1);
+    }
+  } else if (warp == kAccWarps) {
+    a_entries(pos, S, g, 0, 0, lane, acc[0].v0, acc[0].v1);
+  }
+  for (int j = 0; j < T; ++j) {
+    const int dw = kAccWarps + (j & 1);  // diagonal warp of column j
+    if (warp == 0) PCOL(0, j, 0)
+    if (warp == dw) PCOL(1, j, 0)
+    if (warp < kAccWarps) {
+      // step 1: finish column j (tiles it > j) with the kt = j-1 term
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int it = j + 1 + warp + kAccWarps * m;
+        if (it < T) {
+          if (j >= 1) acc_range(acc[m], sm, it, j, j - 1, j, lane);
+          acc_finish(acc[m], sm, it, j, lane);
+        }
+      }
+      // step 2: accumulate column j+1 (tiles it > j+1) over kt < j
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int it = j + 2 + warp + kAccWarps * m;
+        acc[m].zero();
+        if (it < T && j + 1 < T) {
+          a_entries(pos, S, g, it, j + 1, lane, acc[m].v0, acc[m].v1);
+          acc_range(acc[m], sm, it, j + 1, 0, j, lane);
+        }
+      }
+    } else if (warp == dw) {
+      // finish the diagonal tile (its sum over kt < j-1 was accumulated last step)
+      if (j >= 1) acc_range(acc[0], sm, j, j, j - 1, j, lane);
+      acc_finish(acc[0], sm, j, j, lane);
+      __syncwarp();
+      PCOL(1, j, 1)
+      if (diag_factor(sm, rdiag, j, lane) && lane == 0) s_fail = 1;
+      PCOL(1, j, 2)
+    } else if (j + 1 < T) {
+      // the other diagonal warp accumulates the next diagonal tile over kt < j
+      acc[0].zero();
+      a_entries(pos, S, g, j + 1, j + 1, lane, acc[0].v0, acc[0].v1);
+      acc_range(acc[0], sm, j + 1, j + 1, 0, j, lane);
+    }
+    if (warp == 0) PCOL(0, j, 1)
+    __syncthreads();
+    if (warp == 0) PCOL(0, j, 2)
+    if (s_fail) break;  // uniform
+    // step 4: panel L(it, j) = C(it, j) L_d^-T  (B[k][n] = Linv[n][k])
+    if (warp < kAccWarps) {
+      const double *D = sm + toff(j, j);
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int it = j + 1 + warp + kAccWarps * m;
+        if (it < T) {
+          double *Ct = sm + toff(it, j);
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int k = 4 * h + (lane & 3), n = lane >> 2;
+            const double bv = (n > k) ? D[swz(k, n)] : (n == k ? rdiag[j * 8 + k] : 0.0);
+            dmma(d0, d1, Ct[frag_rowk(lane, h)], bv);
+          }
+          __syncwarp();
+          *reinterpret_cast<double2 *>(Ct + frag_acc(lane)) = make_double2(d0, d1);
+        }
+      }
+    }
+    __syncthreads();
+    if (warp == 0) PCOL(0, j, 3)
+  }
+  if (s_fail) {  // Cholesky broke down: redo this cell with LU (reading Q11)
+    if (tid == 0) glist[atomicAdd(&counts[3], 1)] = cl;
+    return;
+  }
+
+  setup_post(sm, rdiag, pos, S, R, g, X, x_off, cl, tid, lane, warp);
 }
 
 // Global-memory local solve for subdomains whose factor does not fit in shared
@@ -1341,7 +1352,6 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
     int *fail = cnt + 4;
     RBF_CUDA_TRY(cudaMemcpyAsync(fail, &hfail, sizeof(int), cudaMemcpyHostToDevice, s));
     const long long n = c->max_ov, no = c->max_own;
-    const long long stride = (((n * (n + no) + (long long)kLuNb * n + 1) & ~1LL) + 2 * n + 1) & ~1LL;
     // largest subdomains first (longest-processing-time order for the work queue), ties
     // by cell index: glist's order comes from atomics, so it is sorted by cell first (the
     // radix sort is stable) and the probe wave below is the same cells on every run

@@ -44,8 +44,8 @@ print("total", (out[:, 4] - out[:, 0]).mean())
 col = buf[512 + 65536 * 3:512 + 65536 * 3 + 512].reshape(2, 64, 4)
 c0, cd = col[0], col[1]
 base = c0[0, 0]
-print("per tile column j of one interior CTA (cycles): warp 0 [step1+2 time, wait at sync 1, panel+sync 2]; "
-      "diagonal warp [finish time, 8x8 factor time]; column total")
+print("per tile column j of one interior CTA (cycles).  Column-loop kernel: warp 0 [step1+2, wait at sync 1, panel+sync 2], "
+      "diagonal warp [finish, 8x8 factor], column total.")
 for j in range(30):
     if c0[j, 0] == 0:
         break
