@@ -238,6 +238,8 @@ def run_ours(args, rank, world):
 
     import paper_0909_5413_b200 as P
 
+    if os.environ.get("RBF_BENCH_NO_GRAPH"):  # profiling only: host-driven GMRES loop
+        P.set_option("solve_graph", 0)
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream()

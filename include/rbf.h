@@ -300,9 +300,9 @@ int rbf_debug_krylov_basis(const rbf_ctx *ctx, double *V_dev, int32_t nvec, void
 
 /* Test hook: fill the shared memory of every SM with 0xFF bytes (NaN in every double)
  * on the current device and synchronise, so that a following kernel that reads shared
- * memory it did not write produces NaN in the parity tests.  The environment variable
- * RBF_POISON=1 does the same for every device buffer the library allocates.  Changes
- * no library state.  ECUDA on a CUDA error. */
+ * memory it did not write produces NaN in the parity tests.  The option "poison" (below)
+ * does the same for every device buffer the library allocates.  Changes no library
+ * state.  ECUDA on a CUDA error. */
 int rbf_debug_poison_shared(void);
 
 /* Device time (ms, CUDA events) of rbf_setup's phases for this context:
@@ -322,6 +322,26 @@ int64_t rbf_launch_count(void);
  * relative to the extended vector [ext_lo, ext_hi)). */
 int rbf_plan_halo(const int64_t *row_start, int64_t ncy, const int64_t *row_bounds, int32_t nranks,
                   int32_t rank, int32_t kh, int32_t rings, int64_t out[12]);
+
+/* Process-wide options: test and A/B switches of the hot path (the library reads no
+ * environment variables).  None changes a result beyond rounding; the defaults are the
+ * product path and are what every benchmark uses.  Read at rbf_setup / rbf_solve time;
+ * set them between contexts, not concurrently with library calls on other threads.
+ *   "poison"              0   1: NaN-fill every new device buffer (uninitialised reads)
+ *   "lu_nopiv"            1   LU path: no-pivot first pass for cells routed there by size
+ *                              (reading Q11); 0: partial pivoting for every LU cell
+ *   "lu_smem_panel"       1   LU path: transposed panel in shared memory when it fits
+ *   "mv_targets_per_lane" 2   matvec union lists of 1..3 targets per lane
+ *   "mv_pair_targets"     1   matvec: nearest-neighbour target groups; 0: consecutive targets
+ *   "mv_sort_lanes"       1   matvec: lanes sorted by list length within windows
+ *   "mv_variant"          0   matvec kernel variant 0..4 (A/B measurements)
+ *   "solve_graph"         1   single-rank solve as one CUDA graph; 0: host-driven loop
+ *   "fused_arnoldi"       1   single-rank fused cooperative Arnoldi kernel; 0: per-step kernels
+ *   "mgs_pairs"           1   fused MGS: two projections per grid barrier (reading Q28)
+ *   "arnoldi_ctas_per_sm" 2   fused Arnoldi CTAs per SM (1..4)
+ * EINVAL for an unknown name or a value out of range. */
+int rbf_set_option(const char *name, int64_t value);
+int rbf_get_option(const char *name, int64_t *value);
 
 const char *rbf_last_error(void);
 void rbf_destroy(rbf_ctx *ctx);

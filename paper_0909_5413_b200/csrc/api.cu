@@ -23,6 +23,30 @@ static std::atomic<long long> g_launches{0};
 
 void count_launch(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
+struct OptDef {
+  const char *name;
+  long long dflt, lo, hi;
+};
+static const OptDef kOptDefs[OPT_COUNT] = {
+    {"poison", 0, 0, 1},         {"lu_nopiv", 1, 0, 1},    {"lu_smem_panel", 1, 0, 1},
+    {"mv_targets_per_lane", 2, 1, 3}, {"mv_pair_targets", 1, 0, 1}, {"mv_sort_lanes", 1, 0, 1},
+    {"mv_variant", 0, 0, 4},     {"solve_graph", 1, 0, 1}, {"fused_arnoldi", 1, 0, 1},
+    {"mgs_pairs", 1, 0, 1},      {"arnoldi_ctas_per_sm", 2, 1, 4},
+};
+static std::atomic<long long> g_opt[OPT_COUNT] = {};
+static std::once_flag g_opt_init;
+
+static void opt_init() {
+  std::call_once(g_opt_init, [] {
+    for (int i = 0; i < OPT_COUNT; ++i) g_opt[i].store(kOptDefs[i].dflt);
+  });
+}
+
+long long opt(Opt o) {
+  opt_init();
+  return g_opt[o].load(std::memory_order_relaxed);
+}
+
 void set_error(const char *fmt, ...) {
   char buf[1024];
   va_list ap;
@@ -58,8 +82,7 @@ int dalloc(rbf_ctx *c, void **p, size_t bytes, cudaStream_t s) {
   }
   // test hook: every new buffer filled with 0xFF bytes (a NaN in every double), so a
   // kernel reading scratch it never wrote shows up in the parity tests
-  const char *poison = getenv("RBF_POISON");
-  if (poison && poison[0] == '1') cudaMemsetAsync(*p, 0xFF, bytes, s);
+  if (opt(OPT_POISON)) cudaMemsetAsync(*p, 0xFF, bytes, s);
   if (c) {
     std::lock_guard<std::mutex> lk(g_alloc_mu);
     c->bytes += (long long)bytes;
@@ -251,6 +274,34 @@ int rbf_info(const rbf_ctx *c, int64_t out[8]) {
   out[6] = c->g.ncy;
   out[7] = c->bytes;
   return RBF_OK;
+}
+
+int rbf_set_option(const char *name, int64_t value) {
+  opt_init();
+  if (!name) { set_error("rbf_set_option: NULL name"); return RBF_EINVAL; }
+  for (int i = 0; i < OPT_COUNT; ++i)
+    if (!strcmp(name, kOptDefs[i].name)) {
+      if (value < kOptDefs[i].lo || value > kOptDefs[i].hi) {
+        set_error("rbf_set_option: %s must be in [%lld, %lld]", name, kOptDefs[i].lo, kOptDefs[i].hi);
+        return RBF_EINVAL;
+      }
+      g_opt[i].store(value);
+      return RBF_OK;
+    }
+  set_error("rbf_set_option: unknown option '%s'", name);
+  return RBF_EINVAL;
+}
+
+int rbf_get_option(const char *name, int64_t *value) {
+  opt_init();
+  if (!name || !value) { set_error("rbf_get_option: NULL argument"); return RBF_EINVAL; }
+  for (int i = 0; i < OPT_COUNT; ++i)
+    if (!strcmp(name, kOptDefs[i].name)) {
+      *value = g_opt[i].load();
+      return RBF_OK;
+    }
+  set_error("rbf_get_option: unknown option '%s'", name);
+  return RBF_EINVAL;
 }
 
 int rbf_lu_stats(const rbf_ctx *c, int64_t out[2]) {

@@ -36,6 +36,24 @@ void count_launch(int k);  // kernel launches issued by this library (rbf_launch
     }                                                                                    \
   } while (0)
 
+// Process-wide library options (rbf_set_option, include/rbf.h): test and A/B switches
+// that never change results beyond rounding; the defaults are the product path.
+enum Opt {
+  OPT_POISON = 0,        // NaN-fill every new device buffer (uninitialised-read tests)
+  OPT_LU_NOPIV,          // LU path: no-pivot first pass for cells routed by size (1)
+  OPT_LU_SMEM_PANEL,     // LU path: transposed panel in shared memory when it fits (1)
+  OPT_MV_G,              // matvec targets per lane (union lists), 1..3 (2)
+  OPT_MV_PAIR,           // matvec: nearest-neighbour target groups (1) or consecutive (0)
+  OPT_MV_SORT,           // matvec: lanes sorted by list length in windows (1)
+  OPT_MV_VARIANT,        // matvec kernel variant for A/B measurements (0)
+  OPT_SOLVE_GRAPH,       // single-rank solve as one CUDA graph (1) or host-driven loop (0)
+  OPT_FUSED_ARNOLDI,     // single-rank fused cooperative Arnoldi kernel (1)
+  OPT_MGS_PAIRS,         // fused MGS: two projections per grid barrier (1, reading Q28)
+  OPT_ARNOLDI_PER_SM,    // fused Arnoldi: CTAs per SM (2)
+  OPT_COUNT
+};
+long long opt(Opt o);
+
 // Raise kernel `fn`'s dynamic shared-memory limit on the current device to at least
 // `bytes` (thread-safe, never lowers it): a per-device high-water mark under a mutex, so
 // a launch that needs `bytes` cannot see another host thread lower the attribute

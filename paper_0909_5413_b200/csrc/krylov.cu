@@ -1075,15 +1075,15 @@ static int ensure_workspace(rbf_ctx *c, int m, cudaStream_t s) {
     per_sm = per_sm < per_sm2 ? per_sm : per_sm2;
     int coop = 0;
     RBF_CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-    const int ar_per_sm = getenv("RBF_AR_PER_SM") ? atoi(getenv("RBF_AR_PER_SM")) : 2;
+    const int ar_per_sm = (int)opt(OPT_ARNOLDI_PER_SM);
     c->ar_grid = (coop && per_sm > 0) ? sms * (per_sm < ar_per_sm ? per_sm : ar_per_sm) : 0;
-    if (getenv("RBF_NO_FUSED_ARNOLDI")) c->ar_grid = 0;
+    if (!opt(OPT_FUSED_ARNOLDI)) c->ar_grid = 0;
     if (c->ar_grid > 0 && (long long)c->ar_grid * kArThreads * kArE < n) c->ar_grid = 0;
     // fused CGS2: same layout as the MGS kernel (w in registers, kArE per thread)
     int cg_per_sm = 0;
     RBF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cg_per_sm, k_arnoldi_cgs2, kArThreads, 0));
     c->cg_grid = (coop && cg_per_sm > 0) ? sms * (cg_per_sm < ar_per_sm ? cg_per_sm : ar_per_sm) : 0;
-    if (getenv("RBF_NO_FUSED_ARNOLDI")) c->cg_grid = 0;
+    if (!opt(OPT_FUSED_ARNOLDI)) c->cg_grid = 0;
     if (c->cg_grid > 0 && (long long)c->cg_grid * kArThreads * kArE < n) c->cg_grid = 0;
     c->ar_m = m;
     if (c->ar_grid > 0 || c->cg_grid > 0) {
@@ -1217,7 +1217,7 @@ static bool fused_ok(const rbf_ctx *c, int orth) {
 }
 
 static bool graph_path(const rbf_ctx *c, const rbf_gmres_params *gp) {
-  return fused_ok(c, gp->orth) && !gp->timing && !getenv("RBF_NO_GRAPH");
+  return fused_ok(c, gp->orth) && !gp->timing && opt(OPT_SOLVE_GRAPH);
 }
 
 // one fused Arnoldi step (cooperative launch); graph mode passes st/hist/inner
@@ -1230,8 +1230,7 @@ static int launch_fused_step(rbf_ctx *c, int orth, double *V, long long n, int k
   int k_ = k;
   double4 *rec = c->rec;
   void *args[] = {&V, &ldv_, &n_, &k_, &Sp, &L, &part, &bar, &mb, &seq_, &rec, &w_in, &st, &hist, &inner};
-  static int mgs_pair = -1;  // two MGS projections per grid barrier (reading Q28)
-  if (mgs_pair < 0) mgs_pair = getenv("RBF_MGS_PAIR") ? atoi(getenv("RBF_MGS_PAIR")) : 1;
+  const bool mgs_pair = opt(OPT_MGS_PAIRS) != 0;  // two MGS projections per grid barrier (reading Q28)
   if (orth == RBF_ORTH_CGS2)
     RBF_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_arnoldi_cgs2, c->cg_grid, kArThreads, args,
                                              0, s));

@@ -473,15 +473,10 @@ static int split_lanes(rbf_ctx *c, cudaStream_t s, long long *lanes_io) {
   return RBF_OK;
 }
 
-static int env_int(const char *name, int dflt) {
-  const char *v = getenv(name);
-  return (v && *v) ? atoi(v) : dflt;
-}
-
 int build_nlist(rbf_ctx *c, cudaStream_t s) {
   const long long nl = n_loc(c), ne = n_ext(c);
-  c->mv_var = env_int("RBF_MV_VAR", 0);  // A/B switch; 0 = default
-  c->mv_g = env_int("RBF_MV_G", 2);
+  c->mv_var = (int)opt(OPT_MV_VARIANT);  // A/B switch; 0 = default
+  c->mv_g = (int)opt(OPT_MV_G);
   if (c->mv_g < 1 || c->mv_g > 3) c->mv_g = 2;
   if (ne >= (1LL << (32 - c->mv_g))) c->mv_g = 1;  // source index must fit beside the mask bits
   if (ne >= (1LL << 31)) {
@@ -496,7 +491,7 @@ int build_nlist(rbf_ctx *c, cudaStream_t s) {
   }
   if (nl <= 0) return RBF_OK;
   long long lanes = (nl + G - 1) / G;
-  if (G >= 2 && !getenv("RBF_MV_CONSECUTIVE")) RBF_TRY(pair_targets(c, G, s, &lanes));
+  if (G >= 2 && opt(OPT_MV_PAIR)) RBF_TRY(pair_targets(c, G, s, &lanes));
   c->mv_int_chunks = 0;
   if (c->overlap && c->lane_tgt) RBF_TRY(split_lanes(c, s, &lanes));
   c->mv_lanes = lanes;
@@ -518,7 +513,7 @@ int build_nlist(rbf_ctx *c, cudaStream_t s) {
   RBF_TRY(dalloc(c, (void **)&nu, sizeof(unsigned long long), s));
   RBF_CUDA_TRY(cudaMemsetAsync(nu, 0, sizeof(unsigned long long), s));
   int *ll = nullptr;
-  const bool sort_lanes = G >= 2 && c->lane_tgt && !getenv("RBF_MV_NOSORT");
+  const bool sort_lanes = G >= 2 && c->lane_tgt && opt(OPT_MV_SORT);
   if (sort_lanes) RBF_TRY(dalloc(c, (void **)&ll, sizeof(int) * (size_t)lanes, s));
   RBF_NLIST(0, nullptr, nullptr);
   count_launch(1);

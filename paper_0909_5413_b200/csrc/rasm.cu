@@ -1351,7 +1351,7 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
   if (nglobal > 0) {
     int *fail = cnt + 4;
     RBF_CUDA_TRY(cudaMemcpyAsync(fail, &hfail, sizeof(int), cudaMemcpyHostToDevice, s));
-    const long long n = c->max_ov, no = c->max_own;
+    const long long no = c->max_own;
     // largest subdomains first (longest-processing-time order for the work queue), ties
     // by cell index: glist's order comes from atomics, so it is sorted by cell first (the
     // radix sort is stable) and the probe wave below is the same cells on every run
@@ -1406,9 +1406,8 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
     int *retry = keys, *nretry = cnt + 6;  // keys are free after the sort
     // the transposed panel (kLuNb x n, re-read and re-written once per panel column) in
     // dynamic shared memory whenever that keeps the CTAs per SM of the global-memory
-    // layout; RBF_LU_SMEM=0 keeps it in the workspace (A/B knob)
-    const char *sm_env = getenv("RBF_LU_SMEM");
-    const bool sm_panel = !(sm_env && sm_env[0] == '0');
+    // layout; option lu_smem_panel = 0 keeps it in the workspace (A/B knob)
+    const bool sm_panel = opt(OPT_LU_SMEM_PANEL) != 0;
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     auto launch = [&](auto kern, int threads, bool with_retry, const int *list, int count, long long nn) -> int {
@@ -1441,8 +1440,7 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
                  : launch(k_rasm_setup_lu<256, false>, 256, true, list, count, nn);
     };
     if (nbd > 0) RBF_TRY(pass(true, sorted, nbd, n_bd));
-    const char *nopiv_env = getenv("RBF_LU_NOPIV");  // "0": pivot every LU cell (A/B knob)
-    const bool nopiv = !(nopiv_env && nopiv_env[0] == '0');
+    const bool nopiv = opt(OPT_LU_NOPIV) != 0;  // 0: pivot every LU cell (A/B knob)
     int hretry = 0;
     bool rest_piv = false;
     if (nsz > 0 && !nopiv) RBF_TRY(pass(true, sorted + nbd, nsz, n_sz));

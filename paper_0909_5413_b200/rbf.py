@@ -59,7 +59,7 @@ EXPORTS = ["rbf_get_nccl_id", "rbf_setup", "rbf_local_count", "rbf_ext_count", "
            "rbf_interpolate_host", "rbf_count_pairs", "rbf_dot", "rbf_plan_strips",
            "rbf_last_error", "rbf_destroy", "rbf_info", "rbf_launch_count", "rbf_setup_times",
            "rbf_plan_halo", "rbf_evaluate", "rbf_matvec_stats", "rbf_lu_stats",
-           "rbf_debug_poison_shared", "rbf_debug_krylov_basis", "rbf_evaluate_count_pairs"]
+           "rbf_debug_poison_shared", "rbf_debug_krylov_basis", "rbf_evaluate_count_pairs", "rbf_set_option", "rbf_get_option"]
 
 _lib = None
 
@@ -95,6 +95,8 @@ def lib() -> C.CDLL:
             "rbf_matvec_stats": (C.c_int, [p, p]),
             "rbf_lu_stats": (C.c_int, [p, p]),
             "rbf_debug_poison_shared": (C.c_int, []),
+            "rbf_set_option": (C.c_int, [C.c_char_p, i64]),
+            "rbf_get_option": (C.c_int, [C.c_char_p, C.POINTER(i64)]),
             "rbf_debug_krylov_basis": (C.c_int, [p, p, i32, p]),
             "rbf_dot": (C.c_int, [p, p, p, p, p]),
             "rbf_plan_strips": (C.c_int, [p, i64, i32, i64, p]),
@@ -142,6 +144,35 @@ def make_params(sigma, cell, rc, rings=1, box=(-1.0, -1.0, 1.0, 1.0), overlap_wi
 def poison_shared() -> None:
     """Test hook: NaN-fill every SM's shared memory (rbf_debug_poison_shared)."""
     _check(lib().rbf_debug_poison_shared())
+
+
+def set_option(name: str, value: int) -> None:
+    """rbf_set_option: a process-wide test / A/B switch (include/rbf.h)."""
+    _check(lib().rbf_set_option(name.encode(), int(value)))
+
+
+def get_option(name: str) -> int:
+    v = C.c_int64()
+    _check(lib().rbf_get_option(name.encode(), C.byref(v)))
+    return v.value
+
+
+class options:
+    """Context manager: set library options, restore them on exit (tests, tools)."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+        self.old = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.old[k] = get_option(k)
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            set_option(k, v)
 
 
 def launch_count() -> int:

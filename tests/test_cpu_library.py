@@ -138,3 +138,25 @@ def test_weak_scaling_workload_and_strips():
     bnd = P.plan_strips(rows, 4, 2)
     own = [int(rows[bnd[g]:bnd[g + 1]].sum()) for g in range(4)]
     assert sum(own) == c.n and max(abs(o - b.n) for o in own) <= 2 * rows.max()
+
+
+def test_options_api_without_gpu():
+    """rbf_set_option / rbf_get_option (include/rbf.h): the library's only switches (it
+    reads no environment variables); range-checked, restorable, no GPU needed."""
+    import paper_0909_5413_b200 as P
+
+    assert P.get_option("lu_nopiv") == 1 and P.get_option("solve_graph") == 1
+    with P.options(lu_nopiv=0, mv_targets_per_lane=3):
+        assert P.get_option("lu_nopiv") == 0 and P.get_option("mv_targets_per_lane") == 3
+    assert P.get_option("lu_nopiv") == 1 and P.get_option("mv_targets_per_lane") == 2
+    with pytest.raises(P.RbfError):
+        P.set_option("mv_targets_per_lane", 4)
+    with pytest.raises(P.RbfError):
+        P.set_option("no_such_option", 1)
+
+
+def test_library_reads_no_environment():
+    import glob
+
+    for f in glob.glob(os.path.join(ROOT, "paper_0909_5413_b200", "csrc", "*.cu*")):
+        assert "getenv" not in open(f).read(), f

@@ -86,14 +86,14 @@ def test_rasm_apply_parity(wl):
 
 @pytest.mark.parametrize("pivot_all", [False, True], ids=["nopiv-pass", "pivot-all"])
 @pytest.mark.parametrize("rings,jit", [(2, 0.1), (3, 0.0)])
-def test_rasm_apply_parity_lu_path(rings, jit, pivot_all, monkeypatch):
+def test_rasm_apply_parity_lu_path(rings, jit, pivot_all, lib_options):
     """Two and three rings of overlap: 625- and 1225-point subdomains exceed the
     shared-memory tensor-core kernel and take the blocked global-memory LU path
     (reading Q11).  The lattice subdomains are SPD: the no-pivot pass factors all of
-    them; RBF_LU_NOPIV=0 forces partial pivoting (largest |a|, lowest row on ties) on
+    them; option lu_nopiv = 0 forces partial pivoting (largest |a|, lowest row on ties) on
     every cell, so both factorisations are held to the oracle."""
     if pivot_all:
-        monkeypatch.setenv("RBF_LU_NOPIV", "0")
+        lib_options(lu_nopiv=0)
     wl = W.make_lattice(48, jitter_frac=jit, seed=5)
     r = np.random.default_rng(21).standard_normal(wl.n)
     Pc = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, rings)
@@ -107,7 +107,7 @@ def test_rasm_apply_parity_lu_path(rings, jit, pivot_all, monkeypatch):
     assert rel(z, ref) <= 1e-10
 
 
-def test_lu_pivot_routing_clustered_reproducible(monkeypatch):
+def test_lu_pivot_routing_clustered_reproducible(lib_options):
     """Clustered data (reading Q8): most large subdomain matrices are numerically
     indefinite, so the no-pivot probe wave fails in more than a quarter of cases and
     the LU cells are factored with pivoting; the routing depends only on the data, so
@@ -122,7 +122,7 @@ def test_lu_pivot_routing_clustered_reproducible(monkeypatch):
             assert 0 < st["n_lu_pivot"] < st["n_lu"]
             outs.append(to_caller(c, c.rasm_apply(c.to_local(r))))
     assert np.array_equal(outs[0], outs[1])
-    monkeypatch.setenv("RBF_LU_NOPIV", "0")
+    lib_options(lu_nopiv=0)
     with ctx_for(wl, rings=2) as c:
         st = c.lu_stats()
         assert st["n_lu_pivot"] == st["n_lu"]
@@ -245,11 +245,11 @@ CGS2_CASES = [W.config(1), W.make_lattice(64, jitter_frac=0.1, seed=2, rhs="gaus
 
 @pytest.mark.parametrize("path", ["graph", "hostloop", "multikernel"])
 @pytest.mark.parametrize("wl", CGS2_CASES, ids=["cfg1", "jitter64"])
-def test_solve_parity_cgs2(wl, path, monkeypatch):
+def test_solve_parity_cgs2(wl, path, lib_options):
     """orth=CGS2 on all three single-rank paths (graph, host loop with the fused kernel,
     three-pass kernels) against the oracle's CGS2 GMRES."""
     if path == "multikernel":
-        monkeypatch.setenv("RBF_NO_FUSED_ARNOLDI", "1")
+        lib_options(fused_arnoldi=0)
     ref = O.solve(wl.xy, wl.f, wl.sigma, wl.rc, wl.box, wl.cell, rtol=wl.tol, orth="cgs2")
     with ctx_for(wl) as c:
         lam, rep = c.solve(c.to_local(torch.from_numpy(wl.f).cuda()), rtol=wl.tol, orth="cgs2",
@@ -848,9 +848,10 @@ def test_paper_ratio_oracle_parity(paper_sweep, ratio):
 
 # ------------------------------------------------------------------ matvec variants
 
-@pytest.mark.parametrize("env", [{"RBF_MV_G": "1"}, {"RBF_MV_G": "3"}, {"RBF_MV_CONSECUTIVE": "1"},
-                                 {"RBF_MV_VAR": "1"}], ids=["G1", "G3", "consecutive", "deg9"])
-def test_matvec_variants_parity(env, monkeypatch):
+@pytest.mark.parametrize("env", [{"mv_targets_per_lane": 1}, {"mv_targets_per_lane": 3},
+                                 {"mv_pair_targets": 0}, {"mv_variant": 1}],
+                         ids=["G1", "G3", "consecutive", "deg9"])
+def test_matvec_variants_parity(env, lib_options):
     """Every neighbour-list layout (targets per lane, pairing) and the degree-9 exp
     give the oracle's matvec; the layouts (same exp) agree bitwise with the default."""
     wl = SMALL[3]
@@ -858,12 +859,11 @@ def test_matvec_variants_parity(env, monkeypatch):
     ref = O.matvec_brute(wl.xy, w, wl.sigma, wl.rc)
     with ctx_for(wl, rings=0) as c:
         y0 = to_caller(c, c.matvec(c.to_local(torch.from_numpy(w).cuda())))
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
+    lib_options(**env)
     with ctx_for(wl, rings=0) as c:
         y = to_caller(c, c.matvec(c.to_local(torch.from_numpy(w).cuda())))
     assert rel(y, ref) <= 1e-12
-    if "RBF_MV_VAR" not in env:
+    if "mv_variant" not in env:
         assert np.array_equal(y, y0)
 
 

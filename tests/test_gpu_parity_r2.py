@@ -5,7 +5,7 @@
     indefinite with kappa(A_c) <= ~3e6 (computed here), so the tensor-core Cholesky
     breaks down on every cell (one ring) and the no-pivot probe fails (two rings); the
     bar is 20 kappa_max eps (backward-stable LU with partial pivoting);
-  * the LU path's transposed panel in shared memory vs in the workspace (RBF_LU_SMEM)
+  * the LU path's transposed panel in shared memory vs in the workspace (lu_smem_panel)
     on 361-400-point subdomains, with and without pivoting: bitwise equal, and <= 1e-10
     against the oracle;
   * the Krylov basis of the one-GPU pairwise MGS (reading Q28) against the oracle's
@@ -64,18 +64,18 @@ def test_lu_pivoting_indefinite_subdomains_vs_oracle(rings):
 
 
 @pytest.mark.parametrize("pivot", ["0", "1"], ids=["pivot-all", "nopiv-pass"])
-def test_lu_shared_panel_matches_workspace_panel(pivot, monkeypatch):
+def test_lu_shared_panel_matches_workspace_panel(pivot, lib_options):
     wl = W.make_lattice(64, jitter_frac=0.1, seed=9)
     cell = 6.4 * wl.meta["h"]  # 3x3 blocks of ~6.4 h cells: 361-400-point subdomains
     r = np.random.default_rng(32).standard_normal(wl.n)
     Pc = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, cell, 1)
     ref = Pc.apply(r)
     Pc.close()
-    monkeypatch.setenv("RBF_LU_NOPIV", pivot)
+    lib_options(lu_nopiv=int(pivot))
     xy = torch.from_numpy(wl.xy).cuda()
     out = {}
     for smem in ("0", "1"):
-        monkeypatch.setenv("RBF_LU_SMEM", smem)
+        lib_options(lu_smem_panel=int(smem))
         with P.Context(xy, wl.sigma, cell, wl.rc, 1, wl.box) as c:
             info = c.info()
             assert 300 < info["max_ov"] <= 420 and info["n_lu"] > 0

@@ -1,6 +1,6 @@
 """Uninitialised-memory checks: every SM's shared memory filled with NaN right before
 each setup (rbf_debug_poison_shared) and every library buffer allocated NaN-filled
-(RBF_POISON=1), then the same parity bars as tests/test_gpu_parity.py.  A kernel
+(option "poison"), then the same parity bars as tests/test_gpu_parity.py.  A kernel
 that reads shared memory or scratch it never wrote -- even multiplied by zero --
 turns the result into NaN here.  (Found: the LU path's 32x32 shared L11/U block was
 filled only up to the last panel's width; 0 * stale shared memory gave NaN.)"""
@@ -20,8 +20,8 @@ import paper_0909_5413_b200 as P  # noqa: E402
 
 
 @pytest.fixture(autouse=True)
-def poisoned_allocations(monkeypatch):
-    monkeypatch.setenv("RBF_POISON", "1")
+def poisoned_allocations(lib_options):
+    lib_options(poison=1)
 
 
 def ctx_for(wl, rings=None, **kw):

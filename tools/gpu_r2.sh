@@ -18,11 +18,11 @@ if [ "${NCU:-1}" = "1" ]; then
   CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline"
   timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_cfg4.csv $CMD > $O/ncu_launch.log 2>&1
   echo "launch rc=$?" >> $O/ncu_launch.log
-  P4="env RBF_NO_GRAPH=1 python tools/prof_cfg2.py 4"
+  P4="python tools/prof_cfg2.py 4 --no-graph"
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
      -k regex:'k_matvec|k_rasm_apply|k_rasm_setup_tc|k_axpy_dot|k_arnoldi' -c 12 --csv --log-file $O/dram_cfg4.csv $P4 > $O/ncu_dram4.log 2>&1
   echo "dram rc=$?" >> $O/ncu_dram4.log
-  P2="env RBF_NO_GRAPH=1 python tools/prof_cfg2.py 2"
+  P2="python tools/prof_cfg2.py 2 --no-graph"
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_matvec|k_rasm_apply|k_rasm_setup_tc|k_arnoldi_mgs2' -c 8 -o $O/prof2 $P2 > $O/ncu_full.log 2>&1
   echo "full rc=$?" >> $O/ncu_full.log
 fi

@@ -14,10 +14,10 @@ if [ "${NCU:-1}" = "1" ]; then
   timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $CMD > $O/ncu_launch.log 2>&1
   echo "launch rc=$?" >> $O/ncu_launch.log
   # the same with the host-driven GMRES loop (same kernels, listed one by one)
-  RBF_NO_GRAPH=1 timeout 600 $CMD > $O/plain_nog.log 2>&1 && \
-  RBF_NO_GRAPH=1 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_nograph.csv $CMD > $O/ncu_launch_nog.log 2>&1
+  RBF_BENCH_NO_GRAPH=1 timeout 600 $CMD > $O/plain_nog.log 2>&1 && \
+  RBF_BENCH_NO_GRAPH=1 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_nograph.csv $CMD > $O/ncu_launch_nog.log 2>&1
   echo "launch nograph rc=$?" >> $O/ncu_launch_nog.log
-  P="env RBF_NO_GRAPH=1 python tools/prof_cfg2.py 2"
+  P="python tools/prof_cfg2.py 2 --no-graph"
   timeout 300 $P > $O/plain2.log 2>&1 && \
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_matvec|k_rasm_apply|k_rasm_setup_tc|k_arnoldi_fused|k_arnoldi_mgs2|k_nlist|k_pack_w' -c 16 -o $O/prof $P > $O/ncu_full.log 2>&1
   echo "full rc=$?" >> $O/ncu_full.log

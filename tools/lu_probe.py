@@ -16,8 +16,8 @@ cases = [("clustered3000 r1", W.make_clustered(3000, seed=11), 1),
          ("lattice48 r2", W.make_lattice(48, jitter_frac=0.1, seed=5), 2)]
 for name, wl, rings in cases:
     for knob in ("1", "0"):
-        os.environ["RBF_LU_NOPIV"] = knob
+        P.set_option("lu_nopiv", int(knob))
         xy = torch.from_numpy(wl.xy).cuda()
         with P.Context(xy, wl.sigma, wl.cell, wl.rc, rings, wl.box) as c:
             print(name, "nopiv" if knob == "1" else "pivot-all", c.lu_stats(), c.info()["max_ov"], flush=True)
-os.environ.pop("RBF_LU_NOPIV")
+P.set_option("lu_nopiv", 1)

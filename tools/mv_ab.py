@@ -1,4 +1,5 @@
-"""A/B timing of matvec variants G:EXP (RBF_MV_G, RBF_MV_EXP) on a config; not part of the product.
+"""A/B timing of matvec variants G:VAR (options mv_targets_per_lane, mv_variant) on a config;
+not part of the product.
 Usage: mv_ab.py CFG 2:0 1:1 ..."""
 import os
 import sys
@@ -14,7 +15,9 @@ wl = W.config(cfg)
 xy = torch.from_numpy(wl.xy).cuda()
 res = {}
 for v in sys.argv[2:] or ["2:0", "1:1"]:
-    os.environ["RBF_MV_G"], os.environ["RBF_MV_VAR"] = v.split(":")
+    g_, var_ = v.split(":")
+    P.set_option("mv_targets_per_lane", int(g_))
+    P.set_option("mv_variant", int(var_))
     c = P.Context(xy, wl.sigma, wl.cell, wl.rc, wl.rings, wl.box)
     npairs = c.count_pairs()
     w = torch.randn(c.n_local, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(1))

@@ -10,6 +10,8 @@ import paper_0909_5413_b200 as P  # noqa: E402
 import rbf_workloads as W  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+if "--no-graph" in sys.argv:  # host-driven GMRES loop: every kernel launched on its own
+    P.set_option("solve_graph", 0)
 wl = W.config(cfg)
 xy = torch.from_numpy(wl.xy).cuda()
 c = P.Context(xy, wl.sigma, wl.cell, wl.rc, wl.rings, wl.box)
