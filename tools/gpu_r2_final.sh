@@ -1,0 +1,20 @@
+#!/bin/bash
+# Round-2 evidence session: bench lines for every config, the reference arm, launch
+# lists and ncu captures (profiles/r02_*).
+O=gpurun_out/${TAG:-f1}
+mkdir -p $O
+nproc > $O/nproc.txt; nvidia-smi > $O/nvsmi.txt 2>&1
+timeout 900 python bench.py --steps 5 --warmup 3 > $O/bench_cfg4.log 2>&1; echo "rc=$?" >> $O/bench_cfg4.log
+for cfg in 1 2 3 5; do
+  timeout 900 python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_cfg$cfg.log 2>&1; echo "rc=$?" >> $O/bench_cfg$cfg.log
+done
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref.log 2>&1; echo "rc=$?" >> $O/bench_ref.log
+CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline"
+RBF_BENCH_NO_GRAPH=1 timeout 900 $CMD > $O/plain_nog.log 2>&1 && \
+RBF_BENCH_NO_GRAPH=1 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_cfg4_hostloop.csv $CMD > $O/ncu_launch.log 2>&1
+echo "launch rc=$?" >> $O/ncu_launch.log
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active --clock-control none \
+   -k regex:'k_matvec|k_rasm_apply|k_rasm_setup_tc|k_axpy_dot|k_nlist' -c 14 --csv --log-file $O/dram_cfg4.csv python tools/prof_cfg2.py 4 --no-graph > $O/ncu_dram4.log 2>&1
+echo "dram rc=$?" >> $O/ncu_dram4.log
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_matvec|k_rasm_apply|k_rasm_setup_tc|k_arnoldi_mgs2|k_axpy_dot|k_evaluate' -c 10 -o $O/prof2 python tools/prof_cfg2.py 2 --no-graph > $O/ncu_full.log 2>&1
+echo "full rc=$?" >> $O/ncu_full.log

@@ -21,6 +21,8 @@ for _ in range(2):
     y = c.matvec(w)
     z = c.rasm_apply(w)
 lam, rep = c.solve(f, rtol=wl.tol, max_iters=5)
+q = xy[: min(c.n, 1 << 20)] * 0.999
+s_ = c.evaluate(q, lam)
 torch.cuda.synchronize()
 print("ok", rep.iterations, c.info())
 c.close()
