@@ -240,6 +240,8 @@ def run_ours(args, rank, world):
 
     if os.environ.get("RBF_BENCH_NO_GRAPH"):  # profiling only: host-driven GMRES loop
         P.set_option("solve_graph", 0)
+    if os.environ.get("RBF_BENCH_LOG_ALLOC"):  # diagnostics: slow device allocations
+        P.set_option("log_slow_alloc", int(os.environ["RBF_BENCH_LOG_ALLOC"]))
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream()

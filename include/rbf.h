@@ -323,6 +323,16 @@ int64_t rbf_launch_count(void);
 int rbf_plan_halo(const int64_t *row_start, int64_t ncy, const int64_t *row_bounds, int32_t nranks,
                   int32_t rank, int32_t kh, int32_t rings, int64_t out[12]);
 
+/* Device memory.  Buffers from 256 MB up that a context frees are kept by the library
+ * (with an event on the freeing stream) and handed to the next context that asks for
+ * the same size, so repeated setups of one configuration do not go back to the memory
+ * pool's fit rules (which stalled cudaMallocAsync for 0.1-1 s at random steps on cfg4).
+ * An allocation that fails returns them to the pool and retries.  rbf_trim_memory()
+ * releases the kept buffers and trims the device's default memory pool to zero
+ * (synchronises the device): call it before handing the memory to another allocator.
+ * ECUDA without a device. */
+int rbf_trim_memory(void);
+
 /* Process-wide options: test and A/B switches of the hot path (the library reads no
  * environment variables).  None changes a result beyond rounding; the defaults are the
  * product path and are what every benchmark uses.  Read at rbf_setup / rbf_solve time;
@@ -339,6 +349,7 @@ int rbf_plan_halo(const int64_t *row_start, int64_t ncy, const int64_t *row_boun
  *   "fused_arnoldi"       1   single-rank fused cooperative Arnoldi kernel; 0: per-step kernels
  *   "mgs_pairs"           1   fused MGS: two projections per grid barrier (reading Q28)
  *   "arnoldi_ctas_per_sm" 2   fused Arnoldi CTAs per SM (1..4)
+ *   "log_slow_alloc"      0   diagnostics: report device allocations slower than N ms (stderr)
  * EINVAL for an unknown name or a value out of range. */
 int rbf_set_option(const char *name, int64_t value);
 int rbf_get_option(const char *name, int64_t *value);

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstring>
@@ -32,6 +33,7 @@ static const OptDef kOptDefs[OPT_COUNT] = {
     {"mv_targets_per_lane", 2, 1, 3}, {"mv_pair_targets", 1, 0, 1}, {"mv_sort_lanes", 1, 0, 1},
     {"mv_variant", 0, 0, 4},     {"solve_graph", 1, 0, 1}, {"fused_arnoldi", 1, 0, 1},
     {"mgs_pairs", 1, 0, 1},      {"arnoldi_ctas_per_sm", 2, 1, 4},
+    {"log_slow_alloc", 0, 0, 1000000},
 };
 static std::atomic<long long> g_opt[OPT_COUNT] = {};
 static std::once_flag g_opt_init;
@@ -63,6 +65,33 @@ int owned_cells(const rbf_ctx *c) { return (c->s.row_hi - c->s.row_lo) * c->g.nc
 // Stream-ordered allocations from the device's default memory pool.  The pool keeps
 // freed memory (release threshold = max), so repeated setup/solve cycles do not
 // return memory to the driver between steps.
+//
+// Buffers from 256 MB up (the X blocks, the neighbour list, the Krylov basis, ...) are
+// recycled by the library itself: a freed big buffer is kept with an event recorded on
+// the freeing stream, and a later request of the same size (within 1/8) takes it back
+// after waiting on that event.  The pool alone picks blocks by its own fit rules, and a
+// setup whose 19 GB neighbour list landed inside the previous context's 90 GB X block
+// had to map fresh memory for the next X -- 0.1-1 s stalls in cudaMallocAsync on cfg4,
+// at random steps (measured).  A failed allocation returns the cached
+// buffers to the pool and retries once; rbf_trim_memory() releases everything.
+constexpr size_t kCacheMin = 256ull << 20;
+constexpr size_t kCacheCap = 140ull << 30;  // bytes kept for reuse at most
+struct CachedBuf {
+  void *p;
+  size_t bytes;
+  int dev;
+  cudaEvent_t ev;
+};
+static std::mutex g_cache_mu;
+static std::vector<CachedBuf> g_cache;               // oldest first
+static std::unordered_map<void *, std::pair<size_t, int>> g_big;  // live big buffers
+
+static void cache_release(CachedBuf &b, cudaStream_t s) {  // caller holds g_cache_mu
+  cudaStreamWaitEvent(s, b.ev, 0);
+  cudaEventDestroy(b.ev);
+  cudaFreeAsync(b.p, s);
+}
+
 int dalloc(rbf_ctx *c, void **p, size_t bytes, cudaStream_t s) {
   static std::once_flag pool_configured;
   std::call_once(pool_configured, [] {
@@ -74,11 +103,53 @@ int dalloc(rbf_ctx *c, void **p, size_t bytes, cudaStream_t s) {
     }
   });
   if (bytes == 0) bytes = 16;
-  cudaError_t e = cudaMallocAsync(p, bytes, s);
-  if (e != cudaSuccess) {
-    *p = nullptr;
-    set_error("device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
-    return e == cudaErrorMemoryAllocation ? RBF_ENOMEM : RBF_ECUDA;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  *p = nullptr;
+  if (bytes >= kCacheMin) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    int best = -1;
+    for (int i = 0; i < (int)g_cache.size(); ++i) {
+      const CachedBuf &b = g_cache[i];
+      if (b.dev == dev && b.bytes >= bytes && b.bytes <= bytes + bytes / 8 &&
+          (best < 0 || b.bytes < g_cache[best].bytes))
+        best = i;
+    }
+    if (best >= 0) {
+      CachedBuf b = g_cache[best];
+      g_cache.erase(g_cache.begin() + best);
+      cudaStreamWaitEvent(s, b.ev, 0);  // the previous owner's work on it is done
+      cudaEventDestroy(b.ev);
+      *p = b.p;
+      g_big[b.p] = {b.bytes, dev};
+    }
+  }
+  if (!*p) {
+    const long long slow = opt(OPT_LOG_SLOW_ALLOC);
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaError_t e = cudaMallocAsync(p, bytes, s);
+    if (e == cudaErrorMemoryAllocation) {  // hand the cached buffers back and retry
+      (void)cudaGetLastError();
+      {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        for (auto &b : g_cache) cache_release(b, s);
+        g_cache.clear();
+      }
+      e = cudaMallocAsync(p, bytes, s);
+    }
+    if (slow > 0) {
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      if (ms >= (double)slow) fprintf(stderr, "librbf: cudaMallocAsync(%zu B) took %.1f ms\n", bytes, ms);
+    }
+    if (e != cudaSuccess) {
+      *p = nullptr;
+      set_error("device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+      return e == cudaErrorMemoryAllocation ? RBF_ENOMEM : RBF_ECUDA;
+    }
+    if (bytes >= kCacheMin) {
+      std::lock_guard<std::mutex> lk(g_cache_mu);
+      g_big[*p] = {bytes, dev};
+    }
   }
   // test hook: every new buffer filled with 0xFF bytes (a NaN in every double), so a
   // kernel reading scratch it never wrote shows up in the parity tests
@@ -102,7 +173,43 @@ void dfree(void *p, cudaStream_t s) {
       g_allocs.erase(it);
     }
   }
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_big.find(p);
+    if (it != g_big.end()) {
+      CachedBuf b{p, it->second.first, it->second.second, nullptr};
+      g_big.erase(it);
+      if (cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming) == cudaSuccess &&
+          cudaEventRecord(b.ev, s) == cudaSuccess) {
+        g_cache.push_back(b);
+        size_t tot = 0;
+        for (auto &x : g_cache) tot += x.bytes;
+        while (tot > kCacheCap && !g_cache.empty()) {  // oldest first
+          tot -= g_cache.front().bytes;
+          cache_release(g_cache.front(), s);
+          g_cache.erase(g_cache.begin());
+        }
+        return;
+      }
+      if (b.ev) cudaEventDestroy(b.ev);
+    }
+  }
   cudaFreeAsync(p, s);
+}
+
+int trim_memory() {
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    for (auto &b : g_cache) cache_release(b, nullptr);
+    g_cache.clear();
+  }
+  RBF_CUDA_TRY(cudaDeviceSynchronize());
+  int dev = 0;
+  cudaMemPool_t pool;
+  RBF_CUDA_TRY(cudaGetDevice(&dev));
+  RBF_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+  RBF_CUDA_TRY(cudaMemPoolTrimTo(pool, 0));
+  return RBF_OK;
 }
 
 int ensure_dyn_smem(const void *fn, size_t bytes) {
@@ -302,6 +409,15 @@ int rbf_get_option(const char *name, int64_t *value) {
     }
   set_error("rbf_get_option: unknown option '%s'", name);
   return RBF_EINVAL;
+}
+
+int rbf_trim_memory(void) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+    set_error("rbf_trim_memory: no CUDA device (this library has no CPU fallback)");
+    return RBF_ECUDA;
+  }
+  return trim_memory();
 }
 
 int rbf_lu_stats(const rbf_ctx *c, int64_t out[2]) {

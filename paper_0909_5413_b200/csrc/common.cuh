@@ -50,6 +50,7 @@ enum Opt {
   OPT_FUSED_ARNOLDI,     // single-rank fused cooperative Arnoldi kernel (1)
   OPT_MGS_PAIRS,         // fused MGS: two projections per grid barrier (1, reading Q28)
   OPT_ARNOLDI_PER_SM,    // fused Arnoldi: CTAs per SM (2)
+  OPT_LOG_SLOW_ALLOC,    // diagnostics: log device allocations slower than this many ms (0 = off)
   OPT_COUNT
 };
 long long opt(Opt o);

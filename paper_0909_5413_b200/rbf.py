@@ -59,7 +59,7 @@ EXPORTS = ["rbf_get_nccl_id", "rbf_setup", "rbf_local_count", "rbf_ext_count", "
            "rbf_interpolate_host", "rbf_count_pairs", "rbf_dot", "rbf_plan_strips",
            "rbf_last_error", "rbf_destroy", "rbf_info", "rbf_launch_count", "rbf_setup_times",
            "rbf_plan_halo", "rbf_evaluate", "rbf_matvec_stats", "rbf_lu_stats",
-           "rbf_debug_poison_shared", "rbf_debug_krylov_basis", "rbf_evaluate_count_pairs", "rbf_set_option", "rbf_get_option"]
+           "rbf_debug_poison_shared", "rbf_debug_krylov_basis", "rbf_evaluate_count_pairs", "rbf_set_option", "rbf_get_option", "rbf_trim_memory"]
 
 _lib = None
 
@@ -96,6 +96,7 @@ def lib() -> C.CDLL:
             "rbf_lu_stats": (C.c_int, [p, p]),
             "rbf_debug_poison_shared": (C.c_int, []),
             "rbf_set_option": (C.c_int, [C.c_char_p, i64]),
+            "rbf_trim_memory": (C.c_int, []),
             "rbf_get_option": (C.c_int, [C.c_char_p, C.POINTER(i64)]),
             "rbf_debug_krylov_basis": (C.c_int, [p, p, i32, p]),
             "rbf_dot": (C.c_int, [p, p, p, p, p]),
@@ -149,6 +150,11 @@ def poison_shared() -> None:
 def set_option(name: str, value: int) -> None:
     """rbf_set_option: a process-wide test / A/B switch (include/rbf.h)."""
     _check(lib().rbf_set_option(name.encode(), int(value)))
+
+
+def trim_memory() -> None:
+    """rbf_trim_memory: release the library's kept buffers and trim the memory pool."""
+    _check(lib().rbf_trim_memory())
 
 
 def get_option(name: str) -> int:

@@ -644,6 +644,8 @@ BIG = {3: 40e9, 4: 140e9}  # device bytes the config needs
 @pytest.fixture(scope="module", params=[3, 4], ids=["cfg3", "cfg4"])
 def big(request):
     cfg = request.param
+    P.trim_memory()
+    torch.cuda.empty_cache()
     if torch.cuda.mem_get_info()[0] < BIG[cfg]:
         pytest.skip(f"cfg{cfg} needs {BIG[cfg] / 1e9:.0f} GB of free device memory")
     wl = W.config(cfg)
@@ -651,6 +653,7 @@ def big(request):
     c = ctx_for(wl)
     yield wl, c, cl
     c.close()
+    P.trim_memory()
     torch.cuda.empty_cache()
 
 
