@@ -386,7 +386,7 @@ def run_ours(args, rank, world):
                      "peak_source": "measured DFMA, tools/clock_under_load.cu (profiles/r01_fp64_peak.json)",
                      "alg_flops_per_launch": mv_alg_flops, "ms_per_launch": mv_per_launch_ms,
                      "ms_per_step": mv_live,
-                     "executed_frac_ncu": ncu_fp64("k_matvec", wl.name, "fp64_alu_frac_of_peak")},
+                     "fp64_pipe_active_ncu": ncu_fp64("k_matvec", wl.name, "fp64_pipe_pct_of_peak", 0.01)},
         "k_rasm_apply": {"kernel": "k_rasm_apply", "bound": "hbm", "achieved": pc_gbs, "peak": hbm_peak,
                          "unit": "GB/s", "frac": pc_gbs / hbm_peak, "peak_source": hbm_src,
                          "traffic": ncu_traffic("k_rasm_apply", wl.name),
