@@ -51,6 +51,7 @@ enum Opt {
   OPT_MGS_PAIRS,         // fused MGS: two projections per grid barrier (1, reading Q28)
   OPT_ARNOLDI_PER_SM,    // fused Arnoldi: CTAs per SM (2)
   OPT_LOG_SLOW_ALLOC,    // diagnostics: log device allocations slower than this many ms (0 = off)
+  OPT_MV_INDEX16,        // matvec: 16-bit neighbour-list entries when they fit (1)
   OPT_COUNT
 };
 long long opt(Opt o);
@@ -259,7 +260,9 @@ struct rbf_ctx {
   int nchunks = 0;
   int *chunk_len = nullptr;    // per chunk: list length (max over its lanes, multiple of 4)
   long long *chunk_off = nullptr;  // per chunk (+1): first entry
-  unsigned *nlist = nullptr;      // source index (ext-relative sorted order) | target mask bits
+  void *nlist = nullptr;       // 32-bit: source index (ext-relative sorted order) | target mask bits;
+                               // 16-bit (mv_w16): mask bits | row step | offset in the row's run
+  int mv_w16 = 0;
   long long nlist_entries = 0;  // ELL entries including padding
   long long nlist_union = 0;    // sum over lanes of the union-list lengths
   // workspaces

@@ -87,15 +87,22 @@ __device__ __forceinline__ void lane_targets(const int4 *__restrict__ tgt, long 
   }
 }
 
-template <int MODE, int G>
+// 16-bit entries (W16, G = 2 only): [15:14] the two targets' mask bits, [13:11] the rows
+// the lane's box walk advanced since its previous entry, [10:0] the offset from the start
+// of the current row's run (cell_start[(by0 + row) ncx + bx0]); the lane's box corner key
+// by0 ncx + bx0 is kept in its lane_tgt .w.  MODE 0 reports the largest offset and row
+// step (fmt[0], fmt[1]) so the host picks 16-bit entries only when they fit.
+template <int MODE, int G, bool W16 = false>
 __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const double2 *__restrict__ xy,
                                                       const int *__restrict__ cell_start, long long nloc,
-                                                      const int4 *__restrict__ tgt, long long nlanes,
+                                                      int4 *__restrict__ tgt, long long nlanes,
                                                       int *__restrict__ chunk_len,
                                                       const long long *__restrict__ chunk_off,
-                                                      unsigned *__restrict__ list,
+                                                      void *__restrict__ list_v,
                                                       unsigned long long *__restrict__ n_union,
-                                                      int *__restrict__ lane_len) {
+                                                      int *__restrict__ lane_len, int *__restrict__ fmt) {
+  unsigned *list = reinterpret_cast<unsigned *>(list_v);
+  unsigned short *list16 = reinterpret_cast<unsigned short *>(list_v);
   const long long lt = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // lane-group
   int t[G];
   lane_targets<G>(tgt, lt, nloc, nlanes, t);
@@ -125,6 +132,7 @@ __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const do
       by1 = max(by1, min(cy + g.kh, g.ncy - 1));
     }
   }
+  int prev_row = 0, max_off = 0, max_step = 0;
   for (int by = by0; by <= by1; ++by) {
     const int s0 = cell_start[by * g.ncx + bx0], s1 = cell_start[by * g.ncx + bx1 + 1];
     for (int s = s0; s < s1; ++s) {
@@ -137,11 +145,27 @@ __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const do
         if (act[j] && in) m |= MvIdx<G>::bit(j);
       }
       if (m) {
-        if (MODE == 1)
-          list[base + ((long long)(cnt >> 2) * 32 + lane) * 4 + (cnt & 3)] = (unsigned)(s - st.ext_lo) | m;
+        const int row = by - by0, step = row - prev_row, off = s - s0;
+        prev_row = row;
+        max_off = max(max_off, off);
+        max_step = max(max_step, step);
+        const long long at = base + ((long long)(cnt >> 2) * 32 + lane) * 4 + (cnt & 3);
+        if (MODE == 1 && W16)
+          list16[at] = (unsigned short)((m >> 16) | ((unsigned)step << 11) | (unsigned)off);
+        else if (MODE == 1)
+          list[at] = (unsigned)(s - st.ext_lo) | m;
         ++cnt;
       }
     }
+  }
+  if (MODE == 0) {
+    max_off = __reduce_max_sync(0xffffffffu, max_off);
+    max_step = __reduce_max_sync(0xffffffffu, max_step);
+    if (lane == 0 && fmt) {
+      atomicMax(&fmt[0], max_off);
+      atomicMax(&fmt[1], max_step);
+    }
+    if (tgt && lt < nlanes) tgt[lt].w = bx1 >= bx0 ? by0 * g.ncx + bx0 : -1;  // the lane's box corner
   }
   const int kmax = (__reduce_max_sync(0xffffffffu, cnt) + 3) & ~3;  // groups of 4
   if (MODE == 0) {
@@ -149,9 +173,14 @@ __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const do
     if (lane_len && lt < nlanes) lane_len[lt] = cnt;
     const int csum = __reduce_add_sync(0xffffffffu, cnt);  // union entries (statistics)
     if (lane == 0 && csum) atomicAdd(n_union, (unsigned long long)csum);
-  } else if (in_chunk) {  // padding: the lane's first target, no mask bit (also idle lanes)
+  } else if (in_chunk) {  // padding: no mask bit (32-bit: the lane's first target; 16-bit:
+                          // offset 0 of the current row, clamped into the ext range)
     const unsigned self = (unsigned)(own_off + (act[0] ? t[0] : 0));
-    for (int k = cnt; k < kmax; ++k) list[base + ((long long)(k >> 2) * 32 + lane) * 4 + (k & 3)] = self;
+    for (int k = cnt; k < kmax; ++k) {
+      const long long at = base + ((long long)(k >> 2) * 32 + lane) * 4 + (k & 3);
+      if (W16) list16[at] = 0;
+      else list[at] = self;
+    }
   }
 }
 
@@ -231,6 +260,67 @@ __global__ __launch_bounds__(kMvThreads, MINB) void k_matvec(
   }
 #pragma unroll
   for (int j = 0; j < G; ++j)
+    if (t[j] >= 0) y[t[j]] = acc[j] * g.norm;
+}
+
+// The same matvec over 16-bit entries (two targets per lane): the source index is
+// the current row's run start + the entry's offset; a lane moves to its next box row
+// (one cell_start load) when an entry says so.  Half the list bytes of k_matvec.
+template <int DEG, int MINB>
+__global__ __launch_bounds__(kMvThreads, MINB) void k_matvec16(
+    Geom g, long long own_off, long long ext_lo, long long n_ext, const int *__restrict__ cell_start,
+    const double4 *__restrict__ rec, const int4 *__restrict__ tgt, long long nlanes,
+    const int *__restrict__ chunk_len, const long long *__restrict__ chunk_off,
+    const unsigned short *__restrict__ list, double *__restrict__ y, long long lane0) {
+  const int lane = threadIdx.x & 31;
+  const long long lt = lane0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long ch = lt >> 5;
+  if ((ch << 5) >= nlanes) return;  // whole warp beyond the last chunk
+  const int4 tv = lt < nlanes ? tgt[lt] : make_int4(-1, -1, -1, -1);
+  const int t[2] = {tv.x, tv.y};
+  double2 me[2];
+  double acc[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const double4 r = rec[own_off + (t[j] >= 0 ? t[j] : 0)];
+    me[j] = make_double2(r.x, r.y);
+    acc[j] = 0.0;
+  }
+  int row_key = tv.w;
+  long long rbase = row_key >= 0 ? (long long)cell_start[row_key] - ext_lo : own_off;
+  const long long last = n_ext - 1;
+  const int K = chunk_len[ch];  // multiple of 4
+  const uint2 *lp = reinterpret_cast<const uint2 *>(list + chunk_off[ch]) + lane;
+  const double esc = g.esc;
+  uint2 nxt = (K > 0) ? __ldcs(lp) : make_uint2(0, 0);
+  for (int k = 0; k < K; k += 4) {
+    const uint2 ev = nxt;
+    if (k + 4 < K) nxt = __ldcs(lp + ((k >> 2) + 1) * 32);
+    const unsigned es[4] = {ev.x & 0xffffu, ev.x >> 16, ev.y & 0xffffu, ev.y >> 16};
+    double4 o[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const unsigned step = (es[u] >> 11) & 7u;
+      if (step) {
+        row_key += (int)step * g.ncx;
+        rbase = (long long)cell_start[row_key] - ext_lo;
+      }
+      long long idx = rbase + (long long)(es[u] & 0x7ffu);
+      idx = idx < last ? idx : last;
+      o[u] = ld_rec(rec + idx);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const double dx = me[j].x - o[u].x, dy = me[j].y - o[u].y;
+        const double e = gauss_exp2<DEG>(fma(dx, dx, dy * dy), esc);
+        if (es[u] & (0x8000u >> j)) acc[j] = fma(o[u].z, e, acc[j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
     if (t[j] >= 0) y[t[j]] = acc[j] * g.norm;
 }
 
@@ -500,22 +590,25 @@ int build_nlist(rbf_ctx *c, cudaStream_t s) {
   RBF_TRY(dalloc(c, (void **)&c->chunk_len, sizeof(int) * nch, s));
   RBF_TRY(dalloc(c, (void **)&c->chunk_off, sizeof(long long) * (nch + 1), s));
   const int blocks = (int)((lanes + kMvThreads - 1) / kMvThreads);
-#define RBF_NLIST(MODE, off, lst)                                                                   \
+#define RBF_NLIST(MODE, W16, off, lst)                                                              \
   switch (G) {                                                                                      \
     case 1: k_nlist<MODE, 1><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, \
-                                                            nullptr, lanes, c->chunk_len, off, lst, nu, ll); break; \
+                                                            nullptr, lanes, c->chunk_len, off, lst, nu, ll, fmt); break; \
     case 3: k_nlist<MODE, 3><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, \
-                                                            c->lane_tgt, lanes, c->chunk_len, off, lst, nu, ll); break; \
-    default: k_nlist<MODE, 2><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, \
-                                                             c->lane_tgt, lanes, c->chunk_len, off, lst, nu, ll); break; \
+                                                            c->lane_tgt, lanes, c->chunk_len, off, lst, nu, ll, fmt); break; \
+    default: k_nlist<MODE, 2, W16><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, \
+                                                             c->lane_tgt, lanes, c->chunk_len, off, lst, nu, ll, fmt); break; \
   }
+  int *fmt = nullptr;  // largest row offset and row step of any entry (16-bit format check)
+  RBF_TRY(dalloc(c, (void **)&fmt, sizeof(int) * 2, s));
+  RBF_CUDA_TRY(cudaMemsetAsync(fmt, 0, sizeof(int) * 2, s));
   unsigned long long *nu = nullptr;
   RBF_TRY(dalloc(c, (void **)&nu, sizeof(unsigned long long), s));
   RBF_CUDA_TRY(cudaMemsetAsync(nu, 0, sizeof(unsigned long long), s));
   int *ll = nullptr;
   const bool sort_lanes = G >= 2 && c->lane_tgt && opt(OPT_MV_SORT);
   if (sort_lanes) RBF_TRY(dalloc(c, (void **)&ll, sizeof(int) * (size_t)lanes, s));
-  RBF_NLIST(0, nullptr, nullptr);
+  RBF_NLIST(0, false, nullptr, nullptr);
   count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
   if (sort_lanes) {
@@ -544,16 +637,27 @@ int build_nlist(rbf_ctx *c, cudaStream_t s) {
   count_launch(2);
   long long total = 0;
   unsigned long long hnu = 0;
+  int hfmt[2] = {0, 0};
   RBF_CUDA_TRY(cudaMemcpyAsync(&total, c->chunk_off + nch, sizeof(long long), cudaMemcpyDeviceToHost, s));
   RBF_CUDA_TRY(cudaMemcpyAsync(&hnu, nu, sizeof(hnu), cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaMemcpyAsync(hfmt, fmt, sizeof(hfmt), cudaMemcpyDeviceToHost, s));
   RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  dfree(fmt, s);
+  fmt = nullptr;
+  // 16-bit entries when every row offset fits 11 bits and every row step 3 bits
+  c->mv_w16 = G == 2 && c->lane_tgt && opt(OPT_MV_INDEX16) && hfmt[0] < 2048 && hfmt[1] < 8 &&
+              c->mv_var == 0;
   dfree(tmp, s);
   dfree(w64, s);
   c->nlist_entries = total;
   c->nlist_union = (long long)hnu;
   dfree(nu, s);
-  RBF_TRY(dalloc(c, (void **)&c->nlist, sizeof(unsigned) * (size_t)(total > 0 ? total : 1), s));
-  RBF_NLIST(1, c->chunk_off, c->nlist);
+  RBF_TRY(dalloc(c, (void **)&c->nlist, (c->mv_w16 ? 2 : 4) * (size_t)(total > 0 ? total : 1), s));
+  if (c->mv_w16) {
+    RBF_NLIST(1, true, c->chunk_off, c->nlist);
+  } else {
+    RBF_NLIST(1, false, c->chunk_off, c->nlist);
+  }
 #undef RBF_NLIST
   count_launch(1);
   RBF_CUDA_TRY(cudaGetLastError());
@@ -591,12 +695,16 @@ int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStre
 #define RBF_MV(GG, DEG, U, MB, ...)                                                            \
   k_matvec<GG, DEG, U, MB, ##__VA_ARGS__><<<blocks, kMvThreads, 0, s>>>(c->g, nl, own_off, c->rec, \
                                                      GG >= 2 ? c->lane_tgt : nullptr, lane1, c->chunk_len,  \
-                                                     c->chunk_off, c->nlist, y_loc, lane0)
+                                                     c->chunk_off, reinterpret_cast<const unsigned *>(c->nlist), y_loc, lane0)
   // Measured alternatives: profiles/r01_matvec_variants_cfg2.txt (2 gathers in flight,
   // 2/4/5 CTAs per SM, L1 prefetch of the next group's records, G = 1 or 3, the
   // degree-10 exp: none faster than the default).
   (void)lanes;
-  if (G == 1) RBF_MV(1, kExpDeg, 4, 1);
+  if (c->mv_w16) {
+    k_matvec16<kExpDeg, 3><<<blocks, kMvThreads, 0, s>>>(
+        c->g, own_off, c->s.ext_lo, n_ext(c), c->cell_start, c->rec, c->lane_tgt, lane1, c->chunk_len,
+        c->chunk_off, reinterpret_cast<const unsigned short *>(c->nlist), y_loc, lane0);
+  } else if (G == 1) RBF_MV(1, kExpDeg, 4, 1);
   else if (G == 3) RBF_MV(3, kExpDeg, 4, 1);
   else if (c->mv_var == 1) RBF_MV(2, 9, 4, 1);
   else if (c->mv_var == 2) RBF_MV(2, 10, 4, 3);  // degree-10 exp (1.5e-16), 3 CTAs/SM
