@@ -350,7 +350,8 @@ int rbf_trim_memory(void);
  *   "mgs_pairs"           1   fused MGS: two projections per grid barrier (reading Q28)
  *   "arnoldi_ctas_per_sm" 2   fused Arnoldi CTAs per SM (1..4)
  *   "log_slow_alloc"      0   diagnostics: report device allocations slower than N ms (stderr)
- *   "mv_index16"          1   matvec: 16-bit neighbour-list entries when every row offset fits
+ *   "mv_index16"          0   1: 16-bit neighbour-list entries when every row offset fits (half
+ *                              the list bytes; measured 8-10% slower)
  * EINVAL for an unknown name or a value out of range. */
 int rbf_set_option(const char *name, int64_t value);
 int rbf_get_option(const char *name, int64_t *value);

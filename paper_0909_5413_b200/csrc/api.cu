@@ -33,7 +33,7 @@ static const OptDef kOptDefs[OPT_COUNT] = {
     {"mv_targets_per_lane", 2, 1, 3}, {"mv_pair_targets", 1, 0, 1}, {"mv_sort_lanes", 1, 0, 1},
     {"mv_variant", 0, 0, 4},     {"solve_graph", 1, 0, 1}, {"fused_arnoldi", 1, 0, 1},
     {"mgs_pairs", 1, 0, 1},      {"arnoldi_ctas_per_sm", 2, 1, 4},
-    {"log_slow_alloc", 0, 0, 1000000}, {"mv_index16", 1, 0, 1},
+    {"log_slow_alloc", 0, 0, 1000000}, {"mv_index16", 0, 0, 1},
 };
 static std::atomic<long long> g_opt[OPT_COUNT] = {};
 static std::once_flag g_opt_init;

@@ -51,7 +51,7 @@ enum Opt {
   OPT_MGS_PAIRS,         // fused MGS: two projections per grid barrier (1, reading Q28)
   OPT_ARNOLDI_PER_SM,    // fused Arnoldi: CTAs per SM (2)
   OPT_LOG_SLOW_ALLOC,    // diagnostics: log device allocations slower than this many ms (0 = off)
-  OPT_MV_INDEX16,        // matvec: 16-bit neighbour-list entries when they fit (1)
+  OPT_MV_INDEX16,        // matvec: 16-bit neighbour-list entries when they fit (0: measured slower)
   OPT_COUNT
 };
 long long opt(Opt o);

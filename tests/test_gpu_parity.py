@@ -852,8 +852,8 @@ def test_paper_ratio_oracle_parity(paper_sweep, ratio):
 # ------------------------------------------------------------------ matvec variants
 
 @pytest.mark.parametrize("env", [{"mv_targets_per_lane": 1}, {"mv_targets_per_lane": 3},
-                                 {"mv_pair_targets": 0}, {"mv_variant": 1}, {"mv_index16": 0}],
-                         ids=["G1", "G3", "consecutive", "deg9", "index32"])
+                                 {"mv_pair_targets": 0}, {"mv_variant": 1}, {"mv_index16": 1}],
+                         ids=["G1", "G3", "consecutive", "deg9", "index16"])
 def test_matvec_variants_parity(env, lib_options):
     """Every neighbour-list layout (targets per lane, pairing) and the degree-9 exp
     give the oracle's matvec; the layouts (same exp) agree bitwise with the default."""

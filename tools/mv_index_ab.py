@@ -32,6 +32,6 @@ for v in (1, 0, 1, 0):
     c.close()
     del c
     P.trim_memory()
-P.set_option("mv_index16", 1)
+P.set_option("mv_index16", 0)
 print(f"cfg{cfg}: 16-bit {res[1][0]:.3f} ms, 32-bit {res[0][0]:.3f} ms, bitwise equal "
       f"{bool(torch.equal(res[1][1], res[0][1]))}, stats {res[1][2]}")
