@@ -435,3 +435,24 @@ def test_gmres_dcgs2_restarts_breakdown_and_limits():
     # max_iters and the identity operator
     r = O.gmres(O.op_identity(5), O.op_identity(5), np.arange(1.0, 6.0), orth="dcgs2")
     assert r.converged and r.iterations == 1
+
+
+@pytest.mark.parametrize("orth", ["mgs", "cgs2", "dcgs2"])
+def test_gmres_history_is_the_minimal_residual(orth):
+    """GMRES's definition (Saad & Schultz): after k steps the iterate minimises ||b - A x||
+    over the Krylov space K_k(A, b) (identity preconditioner, x0 = 0).  The residual
+    estimates of every orthogonalisation -- including the delayed one-reduction form,
+    whose recurrences the GPU restates (reading Q27) -- must equal the least-squares
+    minimum computed independently by numpy over an explicit Krylov basis."""
+    rng = np.random.default_rng(9)
+    n, k = 50, 8
+    G = rng.standard_normal((n, n))
+    A = G @ G.T / n + np.eye(n)  # SPD, well conditioned: the Krylov basis stays accurate
+    b = rng.standard_normal(n)
+    res = O.gmres(O.op_dense(A), O.op_identity(n), b, restart=30, max_iters=k, rtol=0.0, orth=orth)
+    assert len(res.history) == k
+    Q = _krylov_qr(A, b, k).T  # n x (k + 1) orthonormal basis of K_{k+1}
+    for j in range(1, k + 1):
+        y, *_ = np.linalg.lstsq(A @ Q[:, :j], b, rcond=None)
+        rmin = np.linalg.norm(b - A @ Q[:, :j] @ y) / np.linalg.norm(b)
+        assert res.history[j - 1] == pytest.approx(rmin, rel=1e-8)
