@@ -134,7 +134,9 @@ constexpr int kTcWarps = kTcThreads / 32;
 constexpr int kTcMaxTiles = 29;  // N <= 232: 435 tiles = 222,720 B of shared memory
 constexpr size_t kTcMaxSmem = 227 * 1024 - 1024;  // dynamic shared memory (static part ~0.6 KB)
 
-__device__ __forceinline__ int toff(int it, int jt) { return ((it * (it + 1)) / 2 + jt) * 64; }
+__device__ __forceinline__ int toff(int it, int jt) {  // it >= 0: the shift is the division
+  return ((int)((unsigned)(it * (it + 1)) >> 1) + jt) * 64;
+}
 __device__ __forceinline__ int swz(int r, int c) { return r * 8 + (c ^ (((r >> 1) & 1) << 2)); }
 
 struct TileShape {
@@ -710,9 +712,16 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
     __syncthreads();
     if (warp == 0) PCOL(0, j, 2)
     if (s_fail) break;  // uniform
-    // step 4: panel L(it, j) = C(it, j) L_d^-T  (B[k][n] = Linv[n][k])
-    if (warp < kAccWarps) {
+    // step 4: panel L(it, j) = C(it, j) L_d^-T  (B[k][n] = Linv[n][k]; the B fragments
+    // are loaded once per column)
+    if (warp < kAccWarps && j + 1 + warp < T) {
       const double *D = sm + toff(j, j);
+      double bv[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int k = 4 * h + (lane & 3), n = lane >> 2;
+        bv[h] = (n > k) ? D[swz(k, n)] : (n == k ? rdiag[j * 8 + k] : 0.0);
+      }
 #pragma unroll
       for (int m = 0; m < 2; ++m) {
         const int it = j + 1 + warp + kAccWarps * m;
@@ -720,11 +729,7 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
           double *Ct = sm + toff(it, j);
           double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int k = 4 * h + (lane & 3), n = lane >> 2;
-            const double bv = (n > k) ? D[swz(k, n)] : (n == k ? rdiag[j * 8 + k] : 0.0);
-            dmma(d0, d1, Ct[frag_rowk(lane, h)], bv);
-          }
+          for (int h = 0; h < 2; ++h) dmma(d0, d1, Ct[frag_rowk(lane, h)], bv[h]);
           __syncwarp();
           *reinterpret_cast<double2 *>(Ct + frag_acc(lane)) = make_double2(d0, d1);
         }
