@@ -563,7 +563,8 @@ __device__ __forceinline__ void setup_post(double *sm, double *rdiag, double2 *p
   PROBE(3)
   // ---- X_c = S^-1 [-W, I] in natural column order, ld = n rounded up to even, staged
   // in shared memory (the L11 tiles are dead) as the contiguous n_own x ld block and
-  // written to HBM by one bulk copy (TMA), which drains while the next CTA starts.
+  // written to HBM by one bulk copy (TMA), which drains while the next CTA starts (one
+  // copy per row was measured no faster).
   // X_other = -S^-1 W straight from the DMMA accumulators; X_own = S^-1 (full tiles).
   const int n = S.n;
   const int ld = (n + 1) & ~1;
@@ -571,22 +572,8 @@ __device__ __forceinline__ void setup_post(double *sm, double *rdiag, double2 *p
   // and S^-1 tiles beyond them); else (small T0) the rows go straight to HBM
   const bool stage = (long long)S.n1 * ld <= (long long)toff(T0, 0);
   double *Xs = stage ? sm : X + x_off[cl];
-  for (int task = warp; task < T1 * T0; task += kTcWarps) {
-    const int ot = task / T0, jt = task - ot * T0;
-    double d0 = 0.0, d1 = 0.0;
-    for (int kt = 0; kt < T1; ++kt) {
-      // A = S^-1 tile (ot, kt): the lower tiles are stored, (ot, kt) above the diagonal
-      // is the transpose of (kt, ot); diagonal tiles are full (symmetric)
-      const bool lower = kt <= ot;
-      const double *At = lower ? sm + toff(T0 + ot, T0 + kt) : sm + toff(T0 + kt, T0 + ot);
-      const double *Bt = sm + toff(T0 + kt, jt);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int m = lane >> 2, k = 4 * h + (lane & 3);
-        const double av = lower ? At[swz(m, k)] : At[swz(k, m)];
-        dmma(d0, d1, av, Bt[frag_colk(lane, h)]);
-      }
-    }
+  // the X_other tile (ot, jt) = -sum_kt S^-1(ot, kt) W(kt, jt)
+  auto x_store = [&](int ot, int jt, double d0, double d1) {
     const int o = ot * 8 + (lane >> 2);
     const int p0 = jt * 8 + 2 * (lane & 3);
     // the X rows overlap tiles of L11 only (rows of factor order < T0): other warps
@@ -595,7 +582,52 @@ __device__ __forceinline__ void setup_post(double *sm, double *rdiag, double2 *p
       if (p0 < S.n0) Xs[o * ld + (p0 < R.own_nat_lo ? p0 : p0 + S.n1)] = -d0;
       if (p0 + 1 < S.n0) Xs[o * ld + (p0 + 1 < R.own_nat_lo ? p0 + 1 : p0 + 1 + S.n1)] = -d1;
     }
+  };
+  // A = S^-1 tile (ot, kt): the lower tiles are stored, (ot, kt) above the diagonal is
+  // the transpose of (kt, ot); diagonal tiles are full (symmetric)
+  auto sinv_frag = [&](int ot, int kt, int h) -> double {
+    const bool lower = kt <= ot;
+    const double *At = lower ? sm + toff(T0 + ot, T0 + kt) : sm + toff(T0 + kt, T0 + ot);
+    const int m = lane >> 2, k = 4 * h + (lane & 3);
+    return lower ? At[swz(m, k)] : At[swz(k, m)];
+  };
+  if (T1 == 4) {
+    // four warps per own tile row ot: the row's S^-1 fragments (4 tiles x 2 halves) are
+    // loaded once and reused for the warp's columns jt = q, q + 4, ...; two DMMA chains
+    const int ot = warp & 3, q = warp >> 2;
+    double a[4][2];
+#pragma unroll
+    for (int kt = 0; kt < 4; ++kt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) a[kt][h] = sinv_frag(ot, kt, h);
+    for (int jt = q; jt < T0; jt += 4) {
+      double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < 4; ++kt) {
+        const double *Bt = sm + toff(T0 + kt, jt);
+        if (kt & 1) {
+          dmma(e0, e1, a[kt][0], Bt[frag_colk(lane, 0)]);
+          dmma(e0, e1, a[kt][1], Bt[frag_colk(lane, 1)]);
+        } else {
+          dmma(d0, d1, a[kt][0], Bt[frag_colk(lane, 0)]);
+          dmma(d0, d1, a[kt][1], Bt[frag_colk(lane, 1)]);
+        }
+      }
+      x_store(ot, jt, d0 + e0, d1 + e1);
+    }
+  } else {
+    for (int task = warp; task < T1 * T0; task += kTcWarps) {
+      const int ot = task / T0, jt = task - ot * T0;
+      double d0 = 0.0, d1 = 0.0;
+      for (int kt = 0; kt < T1; ++kt) {
+        const double *Bt = sm + toff(T0 + kt, jt);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) dmma(d0, d1, sinv_frag(ot, kt, h), Bt[frag_colk(lane, h)]);
+      }
+      x_store(ot, jt, d0, d1);
+    }
   }
+  PROBE(5)
   for (int t = tid; t < S.n1 * S.n1; t += kTcThreads) {
     const int o = t / S.n1, j = t - o * S.n1;
     const int i1 = o >= j ? o : j, j1 = o >= j ? j : o;
@@ -611,6 +643,7 @@ __device__ __forceinline__ void setup_post(double *sm, double *rdiag, double2 *p
   // generic-proxy shared-memory writes -> visible to the async (bulk copy) proxy
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
+  PROBE(6)
   if (tid == 0) {
     const unsigned bytes = (unsigned)(S.n1 * ld * sizeof(double));
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(X + x_off[cl]),

@@ -41,6 +41,9 @@ names = ["assembly", "cholesky", "W+Sinv", "X write"]
 for i, nm in enumerate(names):
     print(f"{nm:10s} mean {d[:, i].mean():10.0f} cyc  min {d[:, i].min():8d} max {d[:, i].max():8d}")
 print("total", (out[:, 4] - out[:, 0]).mean())
+if (out[:, 5] > 0).all():
+    print(f"X phase: thread 0's tasks {(out[:, 5] - out[:, 3]).mean():.0f}, own part + barrier "
+          f"{(out[:, 6] - out[:, 5]).mean():.0f}, bulk copy issue + read-out {(out[:, 4] - out[:, 6]).mean():.0f} cycles")
 col = buf[512 + 65536 * 3:512 + 65536 * 3 + 512].reshape(2, 64, 4)
 c0, cd = col[0], col[1]
 base = c0[0, 0]
