@@ -323,7 +323,7 @@ int64_t rbf_launch_count(void);
 int rbf_plan_halo(const int64_t *row_start, int64_t ncy, const int64_t *row_bounds, int32_t nranks,
                   int32_t rank, int32_t kh, int32_t rings, int64_t out[12]);
 
-/* Device memory.  Buffers from 256 MB up that a context frees are kept by the library
+/* Device memory.  Buffers from 16 MB up that a context frees are kept by the library
  * (with an event on the freeing stream) and handed to the next context that asks for
  * the same size, so repeated setups of one configuration do not go back to the memory
  * pool's fit rules (which stalled cudaMallocAsync for 0.1-1 s at random steps on cfg4).

@@ -66,7 +66,7 @@ int owned_cells(const rbf_ctx *c) { return (c->s.row_hi - c->s.row_lo) * c->g.nc
 // freed memory (release threshold = max), so repeated setup/solve cycles do not
 // return memory to the driver between steps.
 //
-// Buffers from 256 MB up (the X blocks, the neighbour list, the Krylov basis, ...) are
+// Buffers from 16 MB up (the X blocks, the neighbour list, the Krylov basis, ...) are
 // recycled by the library itself: a freed big buffer is kept with an event recorded on
 // the freeing stream, and a later request of the same size (within 1/8) takes it back
 // after waiting on that event.  The pool alone picks blocks by its own fit rules, and a
@@ -74,7 +74,7 @@ int owned_cells(const rbf_ctx *c) { return (c->s.row_hi - c->s.row_lo) * c->g.nc
 // had to map fresh memory for the next X -- 0.1-1 s stalls in cudaMallocAsync on cfg4,
 // at random steps (measured).  A failed allocation returns the cached
 // buffers to the pool and retries once; rbf_trim_memory() releases everything.
-constexpr size_t kCacheMin = 256ull << 20;
+constexpr size_t kCacheMin = 16ull << 20;
 constexpr size_t kCacheCap = 140ull << 30;  // bytes kept for reuse at most
 struct CachedBuf {
   void *p;
