@@ -133,6 +133,7 @@ __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const do
     }
   }
   int prev_row = 0, max_off = 0, max_step = 0;
+  uint4 grp = make_uint4(0, 0, 0, 0);  // MODE 1, 32-bit: the lane's current group of four
   for (int by = by0; by <= by1; ++by) {
     const int s0 = cell_start[by * g.ncx + bx0], s1 = cell_start[by * g.ncx + bx1 + 1];
     for (int s = s0; s < s1; ++s) {
@@ -150,10 +151,19 @@ __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const do
         max_off = max(max_off, off);
         max_step = max(max_step, step);
         const long long at = base + ((long long)(cnt >> 2) * 32 + lane) * 4 + (cnt & 3);
-        if (MODE == 1 && W16)
+        if (MODE == 1 && W16) {
           list16[at] = (unsigned short)((m >> 16) | ((unsigned)step << 11) | (unsigned)off);
-        else if (MODE == 1)
-          list[at] = (unsigned)(s - st.ext_lo) | m;
+        } else if (MODE == 1) {  // four entries per 16-byte store (full sectors)
+          const unsigned v = (unsigned)(s - st.ext_lo) | m;
+          const int q = cnt & 3;
+          if (q == 0) grp.x = v;
+          else if (q == 1) grp.y = v;
+          else if (q == 2) grp.z = v;
+          else {
+            grp.w = v;
+            *reinterpret_cast<uint4 *>(list + (at - 3)) = grp;
+          }
+        }
         ++cnt;
       }
     }
@@ -176,10 +186,19 @@ __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const do
   } else if (in_chunk) {  // padding: no mask bit (32-bit: the lane's first target; 16-bit:
                           // offset 0 of the current row, clamped into the ext range)
     const unsigned self = (unsigned)(own_off + (act[0] ? t[0] : 0));
-    for (int k = cnt; k < kmax; ++k) {
-      const long long at = base + ((long long)(k >> 2) * 32 + lane) * 4 + (k & 3);
-      if (W16) list16[at] = 0;
-      else list[at] = self;
+    if (W16) {
+      for (int k = cnt; k < kmax; ++k) list16[base + ((long long)(k >> 2) * 32 + lane) * 4 + (k & 3)] = 0;
+    } else {
+      for (int k = cnt; k < kmax; ++k) {
+        const int q = k & 3;
+        if (q == 0) grp.x = self;
+        else if (q == 1) grp.y = self;
+        else if (q == 2) grp.z = self;
+        else {
+          grp.w = self;
+          *reinterpret_cast<uint4 *>(list + base + ((long long)(k >> 2) * 32 + lane) * 4) = grp;
+        }
+      }
     }
   }
 }
