@@ -260,9 +260,24 @@ constexpr int kColCta = 20660;
   if ((threadIdx.x & 31) == 0 && blockIdx.x == kColCta && (j) < 64) g_col[a][j][k] = clock64();
 #define TRACE(i) \
   if (threadIdx.x == 0 && blockIdx.x < 65536) { g_trace[blockIdx.x][0] = smid(); g_trace[blockIdx.x][i] = gtimer(); }
+// LU path phase clocks per CTA (persistent grid <= 296 CTAs): 0 assembly, 1 panel copy +
+// factor, 2 panel write-back + L11, 3 U12 solve, 4 trailing update, 5 back substitution,
+// 6 X copy-out; [7] cells, [8] sum of n
+__device__ long long g_lu_acc[512][10];
+__device__ long long g_lu_t[512];
+#define LUP0() \
+  if (threadIdx.x == 0) g_lu_t[blockIdx.x] = clock64();
+#define LUP(p) \
+  if (threadIdx.x == 0) { \
+    const long long t_ = clock64(); \
+    g_lu_acc[blockIdx.x][p] += t_ - g_lu_t[blockIdx.x]; \
+    g_lu_t[blockIdx.x] = t_; \
+  }
 #define PROBE(i) /* 64 sampled CTAs spread over the grid (mostly interior cells) */ \
   if (threadIdx.x == 0 && blockIdx.x % 509 == 300 && blockIdx.x / 509 < 64) g_probe[blockIdx.x / 509][i] = clock64();
 #else
+#define LUP0()
+#define LUP(p)
 #define PROBE(i)
 #define TRACE(i)
 #define PCOL(a, j, k) {}
@@ -787,17 +802,16 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
 // Right-looking and blocked by kLuNb columns so that the trailing matrix is read
 // and written once per panel instead of once per column: (1) the panel is factored
 // in a transposed copy PT (kLuNb x n, coalesced column access), whole rows are
-// swapped eagerly in A; (2) one pass over the remaining columns does the unit-lower
-// solve U12 = L11^-1 A12 and the rank-kLuNb update A22 -= L21 U12 on the fp64 tensor
-// cores (DMMA.8x8x4, U12 blocks in shared memory, L21 fragments in registers).  The back
-// substitution is blocked the same way.  One CTA per cell; A (n x lda, lda = n +
+// swapped eagerly in A; (2) the unit-lower solve U12 = L11^-1 A12 over all remaining
+// columns, then the rank-kLuNb update A22 -= L21 U12 on the fp64 tensor cores
+// (lu_trailing_update: DMMA.8x8x4, L21 fragments in registers).  The back substitution
+// is blocked the same way.  One CTA per cell; A (n x lda, lda = n +
 // n_own) and PT live in a per-CTA slice of a global workspace (L2).
 // threads per LU CTA: 512 (one cell per SM) for subdomains beyond kLuBigN points, else
 // 256 (two cells in flight per SM: the panel's barrier and L2 latency hide better)
 constexpr int kLuBigN = 330;
 constexpr int kLuNb = 32;     // panel width
 constexpr int kLuRows = 64;   // rows staged in shared memory per back-substitution pass
-constexpr int kLuCb = 64;     // trailing-update column block (U12 block in shared memory)
 
 __device__ __forceinline__ void lu_argmax(double v, int i, double *red_v, int *red_i, int *out) {
   // CTA reduction: largest value, lowest index on ties; result in *out (shared)
@@ -822,6 +836,107 @@ __device__ __forceinline__ void lu_argmax(double v, int i, double *red_v, int *r
   __syncthreads();
 }
 
+// Trailing update of one panel step:
+// (1) U12 = L11^-1 A12 for every column right of the panel, one column per thread over
+//     all threads (the unit-lower L11 in shared memory), written back in place;
+// (2) A22 -= L21 U12 on DMMA.8x8x4: work items of 8 RT rows x 64 columns spread over
+//     the warps; a warp holds its item's L21 fragments (RT row tiles x k = 32) in
+//     registers and walks the 8 column tiles with the next tile's U12 fragments and C
+//     values loaded before the current tile's RT independent DMMA chains run.  (Round 1
+//     solved U12 in 64-column blocks on 64 threads, staged each block in shared memory
+//     behind a barrier and ran one 8-DMMA chain per load round trip: 9-16% slower.)
+template <int RT>
+__device__ __forceinline__ void lu_trailing_update(double *__restrict__ A, const double *__restrict__ PT,
+                                                   const double (*L11)[kLuNb + 1], int n, long long lda,
+                                                   int k0, int kb) {
+  const int tid = threadIdx.x, T = blockDim.x;
+  const int j0 = k0 + kb;
+  for (long long j = j0 + tid; j < lda; j += T) {
+    double u[kLuNb];
+#pragma unroll
+    for (int t = 0; t < kLuNb; ++t) u[t] = t < kb ? A[(long long)(k0 + t) * lda + j] : 0.0;
+#pragma unroll
+    for (int r = 1; r < kLuNb; ++r)
+#pragma unroll
+      for (int t = 0; t < r; ++t) u[r] = fma(-L11[r][t], u[t], u[r]);
+#pragma unroll
+    for (int t = 0; t < kLuNb; ++t)
+      if (t < kb) A[(long long)(k0 + t) * lda + j] = u[t];
+  }
+  __syncthreads();
+  LUP(3)
+  const int lane = tid & 31, warp = tid >> 5, nwarps = T >> 5, q = lane & 3, r8 = lane >> 2;
+  const int m = n - j0;
+  const long long w = lda - j0;
+  if (m <= 0 || w <= 0) return;
+  constexpr int RH = 8 * RT;  // rows per work item
+  const int ngr = (m + RH - 1) / RH, nch = (int)((w + 63) >> 6);
+  // 32-bit element offsets (n * lda < 2^31 on this path)
+  const int ldi = (int)lda;
+  for (int it = warp; it < ngr * nch; it += nwarps) {
+    const int gr = it / nch, ch = it - gr * nch;
+    const int ib = j0 + RH * gr;
+    const int jbi = j0 + 64 * ch;
+    const int ncol = ldi - jbi < 64 ? ldi - jbi : 64;
+    double af[RT][kLuNb / 4];
+    int coff[RT];
+    unsigned rowok = 0;
+#pragma unroll
+    for (int t = 0; t < RT; ++t) {
+      const int ia = ib + 8 * t + r8;
+      const bool ok = ia < n;
+#pragma unroll
+      for (int s4 = 0; s4 < kLuNb / 4; ++s4) {
+        const int k = 4 * s4 + q;
+        af[t][s4] = (k < kb && ok) ? PT[(long long)k * n + ia] : 0.0;
+      }
+      coff[t] = (ok ? ia : 0) * ldi + jbi + 2 * q;
+      rowok |= (ok ? 1u : 0u) << t;
+    }
+    // U12 fragment: row k0 + 4 s4 + q, column jbi + cj + r8
+    const int boff = (k0 + q) * ldi + jbi + r8;
+    const int kq = kb - q;  // fragment k = 4 s4 + q is valid while 4 s4 < kq
+    double bf[kLuNb / 4], c[RT][2];
+    auto load = [&](int cj, double *b, double (*cc)[2]) {
+      const bool okb = jbi + cj + r8 < ldi, ok0 = jbi + cj + 2 * q < ldi, ok1 = jbi + cj + 2 * q + 1 < ldi;
+#pragma unroll
+      for (int s4 = 0; s4 < kLuNb / 4; ++s4) b[s4] = (okb && 4 * s4 < kq) ? A[boff + 4 * s4 * ldi + cj] : 0.0;
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        const bool rk = (rowok >> t) & 1u;
+        cc[t][0] = (rk && ok0) ? A[coff[t] + cj] : 0.0;
+        cc[t][1] = (rk && ok1) ? A[coff[t] + cj + 1] : 0.0;
+      }
+    };
+    load(0, bf, c);
+#pragma unroll 1
+    for (int cj = 0; cj < ncol; cj += 8) {
+      double bn[kLuNb / 4], cn[RT][2];
+      if (cj + 8 < ncol) load(cj + 8, bn, cn);
+      double d[RT][2];
+#pragma unroll
+      for (int t = 0; t < RT; ++t) d[t][0] = d[t][1] = 0.0;
+#pragma unroll
+      for (int s4 = 0; s4 < kLuNb / 4; ++s4)
+#pragma unroll
+        for (int t = 0; t < RT; ++t) dmma(d[t][0], d[t][1], af[t][s4], bf[s4]);
+      const bool ok0 = jbi + cj + 2 * q < ldi, ok1 = jbi + cj + 2 * q + 1 < ldi;
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        const bool rk = (rowok >> t) & 1u;
+        if (rk && ok0) A[coff[t] + cj] = c[t][0] - d[t][0];
+        if (rk && ok1) A[coff[t] + cj + 1] = c[t][1] - d[t][1];
+      }
+#pragma unroll
+      for (int s4 = 0; s4 < kLuNb / 4; ++s4) bf[s4] = bn[s4];
+#pragma unroll
+      for (int t = 0; t < RT; ++t) { c[t][0] = cn[t][0]; c[t][1] = cn[t][1]; }
+    }
+  }
+  __syncthreads();
+  LUP(4)
+}
+
 // One cell of the LU path (the body of the persistent kernel below); A and PT live in
 // this CTA's workspace slice ws.
 // PIV = false: no row exchanges -- LU of an SPD matrix needs none (it is Cholesky with
@@ -839,20 +954,22 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
   __shared__ double red_v[kLuThreads / 32];
   __shared__ int red_i[kLuThreads / 32];
   __shared__ int s_piv;
-  // Ls (back substitution) and Ub (trailing update) are never live together: one buffer,
-  // so that the shared-memory panel leaves room for two CTAs per SM on larger cells
-  constexpr int kLsUb = (kLuRows * (kLuNb + 1) > kLuNb * (kLuCb + 1)) ? kLuRows * (kLuNb + 1)
-                                                                        : kLuNb * (kLuCb + 1);
-  __shared__ double LsUb[kLsUb];
+  __shared__ double LsUb[kLuRows * (kLuNb + 1)];
   double (*Ls)[kLuNb + 1] = reinterpret_cast<double (*)[kLuNb + 1]>(LsUb);  // staged U rows
-  double (*Ub)[kLuCb + 1] = reinterpret_cast<double (*)[kLuCb + 1]>(LsUb);  // U12 column block
   __shared__ double L11[kLuNb][kLuNb + 1];
   __shared__ double prow[kLuNb];
   const int tid = threadIdx.x, T = blockDim.x;
   const int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
+  LUP0()
   if (tid == 0) sub_runs(g, cell_start, ov, cl, cx, cy, R);
   __syncthreads();
   const int n = R.n_ov, n_own = R.n_own, n0 = n - n_own, own_nat = R.own_nat_lo;
+#ifdef RBF_PROBE
+  if (tid == 0) {
+    g_lu_acc[blockIdx.x][7] += 1;
+    g_lu_acc[blockIdx.x][8] += n;
+  }
+#endif
   // right-hand sides: E_own (RASM), or the identity in natural order (ASM, reading Q26)
   const int nrhs = g.asm_full ? n : n_own;
   const long long lda = n + nrhs;
@@ -880,6 +997,7 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
     A[t] = v;
   }
   __syncthreads();
+  LUP(0)
   bool singular = false;
   for (int k0 = 0; k0 < n && !singular; k0 += kLuNb) {
     const int kb = n - k0 < kLuNb ? n - k0 : kLuNb;
@@ -928,6 +1046,7 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
       }
       __syncthreads();
     }
+    LUP(1)
     if (singular) break;
     // write the factored panel back (L below the diagonal, U on and above it)
     for (long long t = tid; t < (long long)kb * (n - k0); t += T) {
@@ -941,54 +1060,11 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
       L11[r][c] = (c < r && r < kb) ? PT[(long long)c * n + k0 + r] : 0.0;
     }
     __syncthreads();
-    // ---- U12 = L11^-1 A12 (one column per thread, L11 in shared memory), then
-    //      A22 -= L21 U12 on the fp64 tensor cores: column blocks of kLuCb columns with
-    //      the U12 block staged in shared memory; each warp walks 8-row tiles holding
-    //      its L21 fragments (8 x 32) in registers, 8 DMMA.8x8x4 per 8x8 output tile.
-    const int j0 = k0 + kb;
-    for (long long jb = j0; jb < lda; jb += kLuCb) {
-      const int nc = (int)(lda - jb < kLuCb ? lda - jb : kLuCb);
-      if (tid < kLuCb) {
-        double u[kLuNb];
-        const long long j = jb + tid;
-        const bool act = tid < nc;
-#pragma unroll
-        for (int t = 0; t < kLuNb; ++t) u[t] = (act && t < kb) ? A[(long long)(k0 + t) * lda + j] : 0.0;
-#pragma unroll
-        for (int r = 1; r < kLuNb; ++r)
-#pragma unroll
-          for (int t = 0; t < r; ++t) u[r] = fma(-L11[r][t], u[t], u[r]);
-#pragma unroll
-        for (int t = 0; t < kLuNb; ++t) {
-          Ub[t][tid] = u[t];
-          if (act && t < kb) A[(long long)(k0 + t) * lda + j] = u[t];
-        }
-      }
-      __syncthreads();
-      const int lane = tid & 31, nwarps = T >> 5, q = lane & 3, r8 = lane >> 2;
-      for (int i0 = j0 + 8 * (tid >> 5); i0 < n; i0 += 8 * nwarps) {
-        double af[kLuNb / 4];
-        const int ia = i0 + r8;
-#pragma unroll
-        for (int s4 = 0; s4 < kLuNb / 4; ++s4) {
-          const int k = 4 * s4 + q;
-          af[s4] = (k < kb && ia < n) ? PT[(long long)k * n + ia] : 0.0;
-        }
-        for (int cj = 0; cj < nc; cj += 8) {
-          const long long jc = jb + cj + 2 * q;
-          double *crow = A + (long long)ia * lda + jc;
-          const bool ok0 = ia < n && jc < lda, ok1 = ia < n && jc + 1 < lda;
-          const double c0 = ok0 ? crow[0] : 0.0, c1 = ok1 ? crow[1] : 0.0;
-          double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-          for (int s4 = 0; s4 < kLuNb / 4; ++s4) dmma(d0, d1, af[s4], Ub[4 * s4 + q][cj + r8]);
-          if (ok0) crow[0] = c0 - d0;
-          if (ok1) crow[1] = c1 - d1;
-        }
-      }
-      __syncthreads();
-    }
+    LUP(2)
+    // ---- U12 = L11^-1 A12, then A22 -= L21 U12 on the fp64 tensor cores
+    lu_trailing_update<2>(A, PT, L11, n, lda, k0, kb);
   }
+  LUP(4)
   if (singular) {
     if (tid == 0) {
       if (PIV) atomicMin(fail_key, cy * g.ncx + cx);
@@ -1057,6 +1133,7 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
   }
   }
   __syncthreads();
+  LUP(5)
   const long long ld = (n + 1) & ~1;
   double *Xc = X + x_off[cl];
   for (long long t = tid; t < (long long)nrhs * ld; t += T) {  // row o: RHS column o
@@ -1071,6 +1148,8 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
     }
     Xc[t] = v;
   }
+  __syncthreads();
+  LUP(6)
 }
 
 // Persistent LU kernel: one CTA per SM takes the cells of glist (sorted largest first)
@@ -1283,6 +1362,7 @@ int probe_read(long long *out) {
   RBF_CUDA_TRY(cudaMemcpyFromSymbol(out + 64 * 8, g_trace, sizeof(long long) * 65536 * 3));
   RBF_CUDA_TRY(cudaMemcpyFromSymbol(out + 64 * 8 + 65536 * 3, g_col, sizeof(long long) * 512));
   RBF_CUDA_TRY(cudaMemcpyFromSymbol(out + 64 * 8 + 65536 * 3 + 512, g_wcol, sizeof(long long) * 128));
+  RBF_CUDA_TRY(cudaMemcpyFromSymbol(out + 64 * 8 + 65536 * 3 + 512 + 128, g_lu_acc, sizeof(long long) * 512 * 10));
   return RBF_OK;
 #else
   (void)out;
