@@ -811,7 +811,7 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
 // 256 (two cells in flight per SM: the panel's barrier and L2 latency hide better)
 constexpr int kLuBigN = 330;
 constexpr int kLuNb = 32;     // panel width
-constexpr int kLuRows = 64;   // rows staged in shared memory per back-substitution pass
+constexpr int kBsCols = 64;   // right-hand-side columns per back-substitution sweep
 
 __device__ __forceinline__ void lu_argmax(double v, int i, double *red_v, int *red_i, int *out) {
   // CTA reduction: largest value, lowest index on ties; result in *out (shared)
@@ -954,8 +954,7 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
   __shared__ double red_v[kLuThreads / 32];
   __shared__ int red_i[kLuThreads / 32];
   __shared__ int s_piv;
-  __shared__ double LsUb[kLuRows * (kLuNb + 1)];
-  double (*Ls)[kLuNb + 1] = reinterpret_cast<double (*)[kLuNb + 1]>(LsUb);  // staged U rows
+  __shared__ double Zs[kLuNb][kBsCols + 1];  // back substitution: the solved block Z_b
   __shared__ double L11[kLuNb][kLuNb + 1];
   __shared__ double prow[kLuNb];
   const int tid = threadIdx.x, T = blockDim.x;
@@ -1073,64 +1072,76 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
     return;
   }
   __syncthreads();
-  // ---- back substitution U Z = Y on the nrhs right-hand-side columns (A[:, n:]),
-  //      blocks of kLuNb rows from the bottom; threads = (column, row group); column
-  //      chunks of at most T columns (ASM has n of them)
-  for (int cb = 0; cb < nrhs; cb += T) {
-  const int nc = nrhs - cb < T ? nrhs - cb : T;
-  const int ngrp = T / nc;
-  for (int r0 = ((n - 1) / kLuNb) * kLuNb; r0 >= 0; r0 -= kLuNb) {
-    const int kb = n - r0 < kLuNb ? n - r0 : kLuNb;
-    __syncthreads();
-    for (int t = tid; t < kLuNb * kLuNb; t += T) {  // U block (upper incl. diagonal), zero beyond kb
-      const int r = t / kLuNb, c = t - r * kLuNb;
-      L11[r][c] = (c >= r && c < kb) ? A[(long long)(r0 + r) * lda + r0 + c] : 0.0;
-    }
-    __syncthreads();
-    if (tid < nc) {  // solve the diagonal block for this column
-      const long long j = n + cb + tid;
-      double z[kLuNb];
-#pragma unroll
-      for (int t = 0; t < kLuNb; ++t) z[t] = t < kb ? A[(long long)(r0 + t) * lda + j] : 0.0;
-#pragma unroll
-      for (int r = kLuNb - 1; r >= 0; --r) {
-        if (r < kb) {
-          double a = z[r];
-#pragma unroll
-          for (int t = r + 1; t < kLuNb; ++t) a = fma(-L11[r][t], z[t], a);
-          z[r] = a / L11[r][r];
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < kLuNb; ++t)
-        if (t < kb) A[(long long)(r0 + t) * lda + j] = z[t];
-    }
-    __syncthreads();
-    // rows above: Y[i] -= U[i, r0:r0+kb] z, columns x row groups
-    const int jc = tid % nc, grp = tid / nc;
-    const bool act = grp < ngrp;
-    const long long jcol = n + cb + jc;
-    double z[kLuNb];
-#pragma unroll
-    for (int t = 0; t < kLuNb; ++t) z[t] = (act && t < kb) ? A[(long long)(r0 + t) * lda + jcol] : 0.0;
-    for (int i0 = 0; i0 < r0; i0 += kLuRows) {
-      const int nr = r0 - i0 < kLuRows ? r0 - i0 : kLuRows;
+  // ---- back substitution U Z = Y on the nrhs right-hand-side columns (A[:, n:]), in
+  //      chunks of kBsCols columns, blocks of kLuNb rows from the bottom: the diagonal
+  //      block solved one column per thread (U block in shared memory), Z_b staged in
+  //      shared memory, then every row above updated at once, Y[0:r0] -= U[0:r0, b] Z_b,
+  //      on DMMA.8x8x4 (warps over 8-row tiles, U fragments in registers, the next
+  //      column tile's Y values loaded before the current one's chain): three barriers
+  //      per block instead of two per 64 rows above it
+  for (int cb = 0; cb < nrhs; cb += kBsCols) {
+    const int nc = nrhs - cb < kBsCols ? nrhs - cb : kBsCols;
+    for (int r0 = ((n - 1) / kLuNb) * kLuNb; r0 >= 0; r0 -= kLuNb) {
+      const int kb = n - r0 < kLuNb ? n - r0 : kLuNb;
       __syncthreads();
-      for (int t = tid; t < nr * kLuNb; t += T) {
+      for (int t = tid; t < kLuNb * kLuNb; t += T) {  // U block (upper incl. diagonal), zero beyond kb
         const int r = t / kLuNb, c = t - r * kLuNb;
-        Ls[r][c] = (c < kb) ? A[(long long)(i0 + r) * lda + r0 + c] : 0.0;
+        L11[r][c] = (c >= r && c < kb) ? A[(long long)(r0 + r) * lda + r0 + c] : 0.0;
       }
       __syncthreads();
-      if (act) {
-        for (int r = grp; r < nr; r += ngrp) {
-          double a = A[(long long)(i0 + r) * lda + jcol];
+      if (tid < kBsCols) {  // solve the diagonal block for this column; Z_b to shared memory
+        const long long j = n + cb + tid;
+        const bool act = tid < nc;
+        double z[kLuNb];
 #pragma unroll
-          for (int t = 0; t < kLuNb; ++t) a = fma(-Ls[r][t], z[t], a);
-          A[(long long)(i0 + r) * lda + jcol] = a;
+        for (int t = 0; t < kLuNb; ++t) z[t] = (act && t < kb) ? A[(long long)(r0 + t) * lda + j] : 0.0;
+#pragma unroll
+        for (int r = kLuNb - 1; r >= 0; --r) {
+          if (r < kb) {
+            double a = z[r];
+#pragma unroll
+            for (int t = r + 1; t < kLuNb; ++t) a = fma(-L11[r][t], z[t], a);
+            z[r] = a / L11[r][r];
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < kLuNb; ++t) {
+          Zs[t][tid] = z[t];  // 0 beyond kb and nc
+          if (act && t < kb) A[(long long)(r0 + t) * lda + j] = z[t];
+        }
+      }
+      __syncthreads();
+      const int lane = tid & 31, warp = tid >> 5, nwarps = T >> 5, q = lane & 3, r8 = lane >> 2;
+      for (int i0 = 8 * warp; i0 < r0; i0 += 8 * nwarps) {  // r0 is a multiple of 8
+        const int ia = i0 + r8;
+        double af[kLuNb / 4];
+#pragma unroll
+        for (int s4 = 0; s4 < kLuNb / 4; ++s4) {
+          const int k = 4 * s4 + q;
+          af[s4] = k < kb ? A[(long long)ia * lda + r0 + k] : 0.0;
+        }
+        double *yrow = A + (long long)ia * lda + n + cb;
+        auto ld = [&](int cj, double &c0, double &c1) {
+          const int jc = cj + 2 * q;
+          c0 = jc < nc ? yrow[jc] : 0.0;
+          c1 = jc + 1 < nc ? yrow[jc + 1] : 0.0;
+        };
+        double c0, c1;
+        ld(0, c0, c1);
+        for (int cj = 0; cj < nc; cj += 8) {
+          double n0 = 0.0, n1 = 0.0;
+          if (cj + 8 < nc) ld(cj + 8, n0, n1);
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int s4 = 0; s4 < kLuNb / 4; ++s4) dmma(d0, d1, af[s4], Zs[4 * s4 + q][cj + r8]);
+          const int jc = cj + 2 * q;
+          if (jc < nc) yrow[jc] = c0 - d0;
+          if (jc + 1 < nc) yrow[jc + 1] = c1 - d1;
+          c0 = n0;
+          c1 = n1;
         }
       }
     }
-  }
   }
   __syncthreads();
   LUP(5)
