@@ -937,6 +937,28 @@ __device__ __forceinline__ void lu_trailing_update(double *__restrict__ A, const
   LUP(4)
 }
 
+// Block-strided copy dst[d(t)] = src[s(t)] for t = threadIdx.x + k blockDim.x < count,
+// 8 loads issued before their 8 stores (source and destination share the workspace, so
+// the compiler would not move a load above an earlier store); idx(t) -> {s(t), d(t)}.
+template <class Idx>
+__device__ __forceinline__ void lu_copy_batched(long long count, const double *src, double *dst, Idx idx) {
+  const int T = blockDim.x;
+  for (long long t0 = threadIdx.x; t0 < count; t0 += 8LL * T) {
+    double v[8];
+    long long d[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const long long t = t0 + (long long)u * T;
+      const longlong2 sd = idx(t < count ? t : 0);
+      d[u] = sd.y;
+      v[u] = t < count ? src[sd.x] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (t0 + (long long)u * T < count) dst[d[u]] = v[u];
+  }
+}
+
 // One cell of the LU path (the body of the persistent kernel below); A and PT live in
 // this CTA's workspace slice ws.
 // PIV = false: no row exchanges -- LU of an SPD matrix needs none (it is Cholesky with
@@ -1000,11 +1022,12 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
   bool singular = false;
   for (int k0 = 0; k0 < n && !singular; k0 += kLuNb) {
     const int kb = n - k0 < kLuNb ? n - k0 : kLuNb;
-    // ---- panel: PT[c][i] = A[i][k0 + c], rows i >= k0
-    for (long long t = tid; t < (long long)kb * (n - k0); t += T) {
-      const int c = (int)(t / (n - k0)), i = k0 + (int)(t - (long long)c * (n - k0));
-      PT[(long long)c * n + i] = A[(long long)i * lda + k0 + c];
-    }
+    // ---- panel: PT[c][i] = A[i][k0 + c], rows i >= k0 (batched: A and PT share the
+    //      workspace, so loads are not moved above earlier stores by the compiler)
+    lu_copy_batched((long long)kb * (n - k0), A, PT, [&](long long t) {
+      const int c = (int)t / (n - k0), i = k0 + (int)t - c * (n - k0);  // kb (n - k0) < 2^31
+      return make_longlong2((long long)i * lda + k0 + c, (long long)c * n + i);
+    });
     __syncthreads();
     for (int c = 0; c < kb; ++c) {
       const int kk = k0 + c;
@@ -1039,19 +1062,29 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
       if (!PIV && !(prow[c] > 0.0)) { singular = true; break; }  // uniform: not SPD here
       const double inv = 1.0 / prow[c];
       for (int i = kk + 1 + tid; i < n; i += T) {
+        // the row's panel values in groups of 8 loaded together: PT shares the workspace
+        // with A, so the compiler would not move a load above the previous store (one L2
+        // round trip per group instead of one per element)
         const double l = PT[(long long)c * n + i] * inv;
         PT[(long long)c * n + i] = l;
-        for (int cc = c + 1; cc < kb; ++cc) PT[(long long)cc * n + i] = fma(-l, prow[cc], PT[(long long)cc * n + i]);
+        for (int c8 = c + 1; c8 < kb; c8 += 8) {
+          double rv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) rv[u] = c8 + u < kb ? PT[(long long)(c8 + u) * n + i] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (c8 + u < kb) PT[(long long)(c8 + u) * n + i] = fma(-l, prow[c8 + u], rv[u]);
+        }
       }
       __syncthreads();
     }
     LUP(1)
     if (singular) break;
     // write the factored panel back (L below the diagonal, U on and above it)
-    for (long long t = tid; t < (long long)kb * (n - k0); t += T) {
-      const int c = (int)(t / (n - k0)), i = k0 + (int)(t - (long long)c * (n - k0));
-      A[(long long)i * lda + k0 + c] = PT[(long long)c * n + i];
-    }
+    lu_copy_batched((long long)kb * (n - k0), PT, A, [&](long long t) {
+      const int c = (int)t / (n - k0), i = k0 + (int)t - c * (n - k0);
+      return make_longlong2((long long)c * n + i, (long long)i * lda + k0 + c);
+    });
     // L11 (unit lower) to shared memory, zero beyond kb: the unrolled solves below run
     // over all kLuNb rows and columns, and 0 * (stale shared memory) can be NaN
     for (int t = tid; t < kLuNb * kLuNb; t += T) {
