@@ -1049,11 +1049,24 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
           PT[(long long)cc * n + kk] = PT[(long long)cc * n + p];
           PT[(long long)cc * n + p] = t0;
         }
-        for (long long j = tid; j < lda; j += T) {
-          if (j >= k0 && j < k0 + kb) continue;
-          const double t0 = A[(long long)kk * lda + j];
-          A[(long long)kk * lda + j] = A[(long long)p * lda + j];
-          A[(long long)p * lda + j] = t0;
+        // right of the panel only (the L columns of earlier panels are never read
+        // again: the right-hand sides are carried in A); four column pairs per pass
+        for (long long j0s = k0 + kb + tid; j0s < lda; j0s += 4LL * T) {
+          double x0[4], x1[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const long long j = j0s + (long long)u * T;
+            x0[u] = j < lda ? A[(long long)kk * lda + j] : 0.0;
+            x1[u] = j < lda ? A[(long long)p * lda + j] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const long long j = j0s + (long long)u * T;
+            if (j < lda) {
+              A[(long long)kk * lda + j] = x1[u];
+              A[(long long)p * lda + j] = x0[u];
+            }
+          }
         }
       }
       __syncthreads();
