@@ -845,20 +845,29 @@ __device__ __forceinline__ void lu_argmax(double v, int i, double *red_v, int *r
 //     values loaded before the current tile's RT independent DMMA chains run.  (Round 1
 //     solved U12 in 64-column blocks on 64 threads, staged each block in shared memory
 //     behind a barrier and ran one 8-DMMA chain per load round trip: 9-16% slower.)
+__device__ __forceinline__ double lds_f64(unsigned addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
 template <int RT>
 __device__ __forceinline__ void lu_trailing_update(double *__restrict__ A, const double *__restrict__ PT,
                                                    const double (*L11)[kLuNb + 1], int n, long long lda,
                                                    int k0, int kb) {
   const int tid = threadIdx.x, T = blockDim.x;
   const int j0 = k0 + kb;
+  const unsigned l11 = (unsigned)__cvta_generic_to_shared(&L11[0][0]);
   for (long long j = j0 + tid; j < lda; j += T) {
     double u[kLuNb];
 #pragma unroll
     for (int t = 0; t < kLuNb; ++t) u[t] = t < kb ? A[(long long)(k0 + t) * lda + j] : 0.0;
+    // L11 read with volatile shared loads: the compiler would otherwise hoist all 496
+    // entries out of the column loop and spill them to local memory
 #pragma unroll
     for (int r = 1; r < kLuNb; ++r)
 #pragma unroll
-      for (int t = 0; t < r; ++t) u[r] = fma(-L11[r][t], u[t], u[r]);
+      for (int t = 0; t < r; ++t) u[r] = fma(-lds_f64(l11 + 8u * (unsigned)(r * (kLuNb + 1) + t)), u[t], u[r]);
 #pragma unroll
     for (int t = 0; t < kLuNb; ++t)
       if (t < kb) A[(long long)(k0 + t) * lda + j] = u[t];
