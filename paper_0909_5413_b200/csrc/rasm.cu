@@ -851,14 +851,15 @@ __device__ __forceinline__ double lds_f64(unsigned addr) {
   return v;
 }
 
-template <int RT>
+template <int RT, bool SYM>
 __device__ __forceinline__ void lu_trailing_update(double *__restrict__ A, const double *__restrict__ PT,
-                                                   const double (*L11)[kLuNb + 1], int n, long long lda,
-                                                   int k0, int kb) {
+                                                   const double (*L11)[kLuNb + 1], const double *dpiv, int n,
+                                                   long long lda, int k0, int kb) {
   const int tid = threadIdx.x, T = blockDim.x;
   const int j0 = k0 + kb;
   const unsigned l11 = (unsigned)__cvta_generic_to_shared(&L11[0][0]);
-  for (long long j = j0 + tid; j < lda; j += T) {
+  // SYM: U12 is solved for the right-hand-side columns only (left of n, U = D L^T)
+  for (long long j = (SYM ? n : j0) + tid; j < lda; j += T) {
     double u[kLuNb];
 #pragma unroll
     for (int t = 0; t < kLuNb; ++t) u[t] = t < kb ? A[(long long)(k0 + t) * lda + j] : 0.0;
@@ -879,14 +880,23 @@ __device__ __forceinline__ void lu_trailing_update(double *__restrict__ A, const
   const long long w = lda - j0;
   if (m <= 0 || w <= 0) return;
   constexpr int RH = 8 * RT;  // rows per work item
-  const int ngr = (m + RH - 1) / RH, nch = (int)((w + 63) >> 6);
   // 32-bit element offsets (n * lda < 2^31 on this path)
   const int ldi = (int)lda;
+  // column chunks of 64: SYM splits them at n (left: the lower triangle plus the strip up
+  // to the end of the row group's own 32-row panel block, so that every later diagonal
+  // block is complete; right: the right-hand sides), else one run over [j0, lda)
+  const int nchL = SYM ? (m + 63) >> 6 : (int)((w + 63) >> 6);
+  const int nchR = SYM ? (int)((lda - n + 63) >> 6) : 0;
+  const int nch = nchL + nchR;
+  const int ngr = (m + RH - 1) / RH;
   for (int it = warp; it < ngr * nch; it += nwarps) {
     const int gr = it / nch, ch = it - gr * nch;
     const int ib = j0 + RH * gr;
-    const int jbi = j0 + 64 * ch;
-    const int ncol = ldi - jbi < 64 ? ldi - jbi : 64;
+    const bool left = !SYM || ch < nchL;
+    const int jbi = left ? j0 + 64 * ch : n + 64 * (ch - nchL);
+    const int jend = !SYM ? ldi : (left ? n : ldi);
+    if (SYM && left && jbi >= (((ib - k0) >> 5) << 5) + k0 + kLuNb) continue;  // strictly upper: never read
+    const int ncol = jend - jbi < 64 ? jend - jbi : 64;
     double af[RT][kLuNb / 4];
     int coff[RT];
     unsigned rowok = 0;
@@ -897,19 +907,23 @@ __device__ __forceinline__ void lu_trailing_update(double *__restrict__ A, const
 #pragma unroll
       for (int s4 = 0; s4 < kLuNb / 4; ++s4) {
         const int k = 4 * s4 + q;
-        af[t][s4] = (k < kb && ok) ? PT[(long long)k * n + ia] : 0.0;
+        // SYM, left of n: C -= (L21 D) L^T, the pivots folded into the L21 fragments
+        const double v = (k < kb && ok) ? PT[(long long)k * n + ia] : 0.0;
+        af[t][s4] = (SYM && left) ? v * dpiv[k] : v;
       }
       coff[t] = (ok ? ia : 0) * ldi + jbi + 2 * q;
       rowok |= (ok ? 1u : 0u) << t;
     }
-    // U12 fragment: row k0 + 4 s4 + q, column jbi + cj + r8
-    const int boff = (k0 + q) * ldi + jbi + r8;
+    // B fragment (k = 4 s4 + q, column jbi + cj + r8): U12 from A, or (SYM, left of n)
+    // L^T from the transposed panel
+    const double *Bp = (SYM && left) ? PT + q * n + jbi + r8 : A + (k0 + q) * ldi + jbi + r8;
+    const int bst = (SYM && left) ? 4 * n : 4 * ldi;
     const int kq = kb - q;  // fragment k = 4 s4 + q is valid while 4 s4 < kq
     double bf[kLuNb / 4], c[RT][2];
     auto load = [&](int cj, double *b, double (*cc)[2]) {
-      const bool okb = jbi + cj + r8 < ldi, ok0 = jbi + cj + 2 * q < ldi, ok1 = jbi + cj + 2 * q + 1 < ldi;
+      const bool okb = jbi + cj + r8 < jend, ok0 = jbi + cj + 2 * q < jend, ok1 = jbi + cj + 2 * q + 1 < jend;
 #pragma unroll
-      for (int s4 = 0; s4 < kLuNb / 4; ++s4) b[s4] = (okb && 4 * s4 < kq) ? A[boff + 4 * s4 * ldi + cj] : 0.0;
+      for (int s4 = 0; s4 < kLuNb / 4; ++s4) b[s4] = (okb && 4 * s4 < kq) ? Bp[s4 * bst + cj] : 0.0;
 #pragma unroll
       for (int t = 0; t < RT; ++t) {
         const bool rk = (rowok >> t) & 1u;
@@ -929,7 +943,7 @@ __device__ __forceinline__ void lu_trailing_update(double *__restrict__ A, const
       for (int s4 = 0; s4 < kLuNb / 4; ++s4)
 #pragma unroll
         for (int t = 0; t < RT; ++t) dmma(d[t][0], d[t][1], af[t][s4], bf[s4]);
-      const bool ok0 = jbi + cj + 2 * q < ldi, ok1 = jbi + cj + 2 * q + 1 < ldi;
+      const bool ok0 = jbi + cj + 2 * q < jend, ok1 = jbi + cj + 2 * q + 1 < jend;
 #pragma unroll
       for (int t = 0; t < RT; ++t) {
         const bool rk = (rowok >> t) & 1u;
@@ -988,6 +1002,7 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
   __shared__ double Zs[kLuNb][kBsCols + 1];  // back substitution: the solved block Z_b
   __shared__ double L11[kLuNb][kLuNb + 1];
   __shared__ double prow[kLuNb];
+  __shared__ double dpiv[kLuNb];  // the panel's pivots U(kk, kk) (no-pivot pass: U = D L^T)
   const int tid = threadIdx.x, T = blockDim.x;
   const int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
   LUP0()
@@ -1113,10 +1128,11 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
       const int r = t / kLuNb, c = t - r * kLuNb;
       L11[r][c] = (c < r && r < kb) ? PT[(long long)c * n + k0 + r] : 0.0;
     }
+    if (tid < kLuNb) dpiv[tid] = tid < kb ? PT[(long long)tid * n + k0 + tid] : 0.0;
     __syncthreads();
     LUP(2)
     // ---- U12 = L11^-1 A12, then A22 -= L21 U12 on the fp64 tensor cores
-    lu_trailing_update<2>(A, PT, L11, n, lda, k0, kb);
+    lu_trailing_update<2, !PIV>(A, PT, L11, dpiv, n, lda, k0, kb);
   }
   LUP(4)
   if (singular) {
@@ -1170,10 +1186,13 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
       for (int i0 = 8 * warp; i0 < r0; i0 += 8 * nwarps) {  // r0 is a multiple of 8
         const int ia = i0 + r8;
         double af[kLuNb / 4];
+        // U(ia, r0 + k); no-pivot pass: U = D L^T, so D(ia) L(r0 + k, ia) (the strictly
+        // upper part left of the right-hand sides is not kept up to date there)
+        const double dia = PIV ? 1.0 : A[(long long)ia * lda + ia];
 #pragma unroll
         for (int s4 = 0; s4 < kLuNb / 4; ++s4) {
           const int k = 4 * s4 + q;
-          af[s4] = k < kb ? A[(long long)ia * lda + r0 + k] : 0.0;
+          af[s4] = k < kb ? (PIV ? A[(long long)ia * lda + r0 + k] : dia * A[(long long)(r0 + k) * lda + ia]) : 0.0;
         }
         double *yrow = A + (long long)ia * lda + n + cb;
         auto ld = [&](int cj, double &c0, double &c1) {
