@@ -344,7 +344,8 @@ int rbf_trim_memory(void);
  *   "mv_targets_per_lane" 2   matvec union lists of 1..3 targets per lane
  *   "mv_pair_targets"     1   matvec: nearest-neighbour target groups; 0: consecutive targets
  *   "mv_sort_lanes"       1   matvec: lanes sorted by list length within windows
- *   "mv_variant"          0   matvec kernel variant 0..4 (A/B measurements)
+ *   "mv_variant"          0   matvec kernel variant 0..5 (A/B measurements; 5: the
+ *                              sources of each CTA staged in shared memory by bulk copies)
  *   "solve_graph"         1   single-rank solve as one CUDA graph; 0: host-driven loop
  *   "fused_arnoldi"       1   single-rank fused cooperative Arnoldi kernel; 0: per-step kernels
  *   "mgs_pairs"           1   fused MGS: two projections per grid barrier (reading Q28)

@@ -31,7 +31,7 @@ struct OptDef {
 static const OptDef kOptDefs[OPT_COUNT] = {
     {"poison", 0, 0, 1},         {"lu_nopiv", 1, 0, 1},    {"lu_smem_panel", 1, 0, 1},
     {"mv_targets_per_lane", 2, 1, 3}, {"mv_pair_targets", 1, 0, 1}, {"mv_sort_lanes", 1, 0, 1},
-    {"mv_variant", 0, 0, 4},     {"solve_graph", 1, 0, 1}, {"fused_arnoldi", 1, 0, 1},
+    {"mv_variant", 0, 0, 5},     {"solve_graph", 1, 0, 1}, {"fused_arnoldi", 1, 0, 1},
     {"mgs_pairs", 1, 0, 1},      {"arnoldi_ctas_per_sm", 2, 1, 4},
     {"log_slow_alloc", 0, 0, 1000000}, {"mv_index16", 0, 0, 1},
 };
@@ -497,6 +497,7 @@ void rbf_destroy(rbf_ctx *c) {
   dfree(c->chunk_len, s);
   dfree(c->chunk_off, s);
   dfree(c->nlist, s);
+  dfree(c->mv_win, s);
   dfree(c->X, s);
   dfree(c->asm_toff, s);
   dfree(c->asm_t, s);

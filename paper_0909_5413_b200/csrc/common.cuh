@@ -263,6 +263,7 @@ struct rbf_ctx {
   void *nlist = nullptr;       // 32-bit: source index (ext-relative sorted order) | target mask bits;
                                // 16-bit (mv_w16): mask bits | row step | offset in the row's run
   int mv_w16 = 0;
+  int4 *mv_win = nullptr;      // matvec variant 5: per CTA, the staged source window (bx0, bx1, by0, by1; x < 0: none)
   long long nlist_entries = 0;  // ELL entries including padding
   long long nlist_union = 0;    // sum over lanes of the union-list lengths
   // workspaces

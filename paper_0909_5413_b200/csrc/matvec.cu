@@ -100,7 +100,8 @@ __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const do
                                                       const long long *__restrict__ chunk_off,
                                                       void *__restrict__ list_v,
                                                       unsigned long long *__restrict__ n_union,
-                                                      int *__restrict__ lane_len, int *__restrict__ fmt) {
+                                                      int *__restrict__ lane_len, int *__restrict__ fmt,
+                                                      const int4 *__restrict__ win = nullptr) {
   unsigned *list = reinterpret_cast<unsigned *>(list_v);
   unsigned short *list16 = reinterpret_cast<unsigned short *>(list_v);
   const long long lt = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // lane-group
@@ -134,8 +135,19 @@ __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const do
   }
   int prev_row = 0, max_off = 0, max_step = 0;
   uint4 grp = make_uint4(0, 0, 0, 0);  // MODE 1, 32-bit: the lane's current group of four
+  // matvec variant 5: entries are slots of the CTA's staged window (its rows' runs
+  // [cell_start(by, wbx0), cell_start(by, wbx1 + 1)) back to back) instead of indices
+  int4 wv = make_int4(-1, -1, 0, -1);
+  if (MODE == 1 && win && in_chunk) wv = win[lt / kMvThreads];
+  const bool staged = wv.x >= 0;
+  long long wslot = 0;  // slot of the first source of row wv.z + r, advanced row by row
+  if (staged)
+    for (int by = wv.z; by < by0; ++by)
+      wslot += cell_start[by * g.ncx + wv.y + 1] - cell_start[by * g.ncx + wv.x];
   for (int by = by0; by <= by1; ++by) {
     const int s0 = cell_start[by * g.ncx + bx0], s1 = cell_start[by * g.ncx + bx1 + 1];
+    const long long rs = staged ? wslot + (s0 - cell_start[by * g.ncx + wv.x]) : 0;
+    if (staged) wslot += cell_start[by * g.ncx + wv.y + 1] - cell_start[by * g.ncx + wv.x];
     for (int s = s0; s < s1; ++s) {
       const double2 o = xy[s - st.ext_lo];
       unsigned m = 0;
@@ -154,7 +166,7 @@ __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const do
         if (MODE == 1 && W16) {
           list16[at] = (unsigned short)((m >> 16) | ((unsigned)step << 11) | (unsigned)off);
         } else if (MODE == 1) {  // four entries per 16-byte store (full sectors)
-          const unsigned v = (unsigned)(s - st.ext_lo) | m;
+          const unsigned v = (unsigned)(staged ? rs + (s - s0) : s - st.ext_lo) | m;
           const int q = cnt & 3;
           if (q == 0) grp.x = v;
           else if (q == 1) grp.y = v;
@@ -185,7 +197,7 @@ __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const do
     if (lane == 0 && csum) atomicAdd(n_union, (unsigned long long)csum);
   } else if (in_chunk) {  // padding: no mask bit (32-bit: the lane's first target; 16-bit:
                           // offset 0 of the current row, clamped into the ext range)
-    const unsigned self = (unsigned)(own_off + (act[0] ? t[0] : 0));
+    const unsigned self = staged ? 0u : (unsigned)(own_off + (act[0] ? t[0] : 0));
     if (W16) {
       for (int k = cnt; k < kmax; ++k) list16[base + ((long long)(k >> 2) * 32 + lane) * 4 + (k & 3)] = 0;
     } else {
@@ -217,6 +229,143 @@ __global__ void k_init_rec(const double2 *__restrict__ xy, long long n, double4 
 __global__ void k_pack_w(const double *__restrict__ w, long long n, double4 *__restrict__ rec) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) reinterpret_cast<double *>(rec + i)[2] = w[i];
+}
+
+// ---------------------------------------------------------------------------
+// Matvec variant 5 (A/B measurement of the staged design, SURVEY §8.a2 / DESIGN.md §6):
+// each CTA's sources -- the union box of its lanes' stencils, 2kh+1 (or 2kh+2) cell
+// rows, each one contiguous run of the sorted records -- are copied into shared memory
+// by one 1-D bulk copy per row (cp.async.bulk, mbarrier completion) and the lanes gather
+// from there; list entries are window slots.  CTAs whose window exceeds kMvStageMax
+// records (targets spanning two cell rows, the cells' leftover singles) keep the global
+// gathers.
+// ---------------------------------------------------------------------------
+constexpr int kMvStageMax = 3400;  // records per CTA window (106 KB: two CTAs per SM)
+
+__global__ __launch_bounds__(kMvThreads) void k_mv_windows(Geom g, Strip st, const double2 *__restrict__ xy,
+                                                           const int *__restrict__ cell_start, long long nloc,
+                                                           const int4 *__restrict__ tgt, long long nlanes,
+                                                           int4 *__restrict__ win) {
+  __shared__ int sb[4];
+  if (threadIdx.x == 0) { sb[0] = g.ncx; sb[1] = -1; sb[2] = g.ncy; sb[3] = -1; }
+  __syncthreads();
+  const long long lt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int t[2];
+  lane_targets<2>(tgt, lt, nloc, nlanes, t);
+  const long long own_off = st.own_lo - st.ext_lo;
+  for (int j = 0; j < 2; ++j) {
+    if (t[j] < 0) continue;
+    int cx = 0, cy = 0;
+    target_cell(g, xy[own_off + t[j]], cx, cy);
+    atomicMin(&sb[0], max(cx - g.kh, 0));
+    atomicMax(&sb[1], min(cx + g.kh, g.ncx - 1));
+    atomicMin(&sb[2], max(cy - g.kh, 0));
+    atomicMax(&sb[3], min(cy + g.kh, g.ncy - 1));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long tot = 0;
+    for (int by = sb[2]; by <= sb[3]; ++by)
+      tot += cell_start[by * g.ncx + sb[1] + 1] - cell_start[by * g.ncx + sb[0]];
+    win[blockIdx.x] = (sb[1] >= sb[0] && tot <= kMvStageMax) ? make_int4(sb[0], sb[1], sb[2], sb[3])
+                                                             : make_int4(-1, -1, 0, -1);
+  }
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long *m, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(m)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *m, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(m)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *m, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(m);
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(done)
+                 : "r"(a), "r"(parity)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(m))
+               : "memory");
+}
+
+template <int DEG, int MINB>
+__global__ __launch_bounds__(kMvThreads, MINB) void k_matvec_st(
+    Geom g, Strip st, long long nloc, long long own_off, const double4 *__restrict__ rec,
+    const int *__restrict__ cell_start, const int4 *__restrict__ win, const int4 *__restrict__ tgt,
+    long long nlanes, const int *__restrict__ chunk_len, const long long *__restrict__ chunk_off,
+    const unsigned *__restrict__ list, double *__restrict__ y) {
+  extern __shared__ __align__(16) double4 srec[];
+  __shared__ __align__(8) unsigned long long mbar;
+  const int lane = threadIdx.x & 31;
+  const int4 wv = win[blockIdx.x];
+  const bool staged = wv.x >= 0;  // uniform per CTA
+  if (staged && threadIdx.x == 0) {
+    mbar_init(&mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    long long tot = 0;
+    for (int by = wv.z; by <= wv.w; ++by)
+      tot += cell_start[by * g.ncx + wv.y + 1] - cell_start[by * g.ncx + wv.x];
+    mbar_expect_tx(&mbar, (unsigned)(tot * sizeof(double4)));
+    long long slot = 0;
+    for (int by = wv.z; by <= wv.w; ++by) {
+      const int s0 = cell_start[by * g.ncx + wv.x], s1 = cell_start[by * g.ncx + wv.y + 1];
+      if (s1 > s0) bulk_g2s(srec + slot, rec + (s0 - st.ext_lo), (unsigned)((s1 - s0) * sizeof(double4)), &mbar);
+      slot += s1 - s0;
+    }
+  }
+  __syncthreads();
+  const long long lt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long ch = lt >> 5;
+  int t[2];
+  lane_targets<2>(tgt, lt, nloc, nlanes, t);
+  double2 me[2];
+  double acc[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const double4 r = rec[own_off + (t[j] >= 0 ? t[j] : 0)];
+    me[j] = make_double2(r.x, r.y);
+    acc[j] = 0.0;
+  }
+  if (staged) mbar_wait(&mbar, 0);
+  if ((ch << 5) < nlanes) {
+    const int K = chunk_len[ch];
+    const uint4 *lp = reinterpret_cast<const uint4 *>(list + chunk_off[ch]) + lane;
+    const double esc = g.esc;
+    uint4 nxt = (K > 0) ? __ldcs(lp) : make_uint4(0, 0, 0, 0);
+    for (int k = 0; k < K; k += 4) {
+      const uint4 ev = nxt;
+      if (k + 4 < K) nxt = __ldcs(lp + ((k >> 2) + 1) * 32);
+      const unsigned es[4] = {ev.x, ev.y, ev.z, ev.w};
+      double4 o[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const unsigned idx = es[u] & MvIdx<2>::kIdxMask;
+        o[u] = staged ? srec[idx] : ld_rec(rec + idx);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const double dx = me[j].x - o[u].x, dy = me[j].y - o[u].y;
+          const double e = gauss_exp2<DEG>(fma(dx, dx, dy * dy), esc);
+          if (es[u] & MvIdx<2>::bit(j)) acc[j] = fma(o[u].z, e, acc[j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      if (t[j] >= 0) y[t[j]] = acc[j] * g.norm;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -672,8 +821,20 @@ int build_nlist(rbf_ctx *c, cudaStream_t s) {
   c->nlist_union = (long long)hnu;
   dfree(nu, s);
   RBF_TRY(dalloc(c, (void **)&c->nlist, (c->mv_w16 ? 2 : 4) * (size_t)(total > 0 ? total : 1), s));
+  // variant 5 (staged sources, A/B only): one window per matvec CTA, single strip
+  const bool stage = c->mv_var == 5 && G == 2 && c->lane_tgt && c->mv_int_chunks == 0 && !c->mv_w16;
+  if (stage) {
+    RBF_TRY(dalloc(c, (void **)&c->mv_win, sizeof(int4) * (size_t)blocks, s));
+    k_mv_windows<<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, c->lane_tgt, lanes,
+                                               c->mv_win);
+    count_launch(1);
+    RBF_CUDA_TRY(cudaGetLastError());
+  }
   if (c->mv_w16) {
     RBF_NLIST(1, true, c->chunk_off, c->nlist);
+  } else if (stage) {
+    k_nlist<1, 2><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, c->lane_tgt, lanes,
+                                               c->chunk_len, c->chunk_off, c->nlist, nu, ll, fmt, c->mv_win);
   } else {
     RBF_NLIST(1, false, c->chunk_off, c->nlist);
   }
@@ -719,7 +880,14 @@ int launch_matvec(const rbf_ctx *c, const double *w_ext, double *y_loc, cudaStre
   // 2/4/5 CTAs per SM, L1 prefetch of the next group's records, G = 1 or 3, the
   // degree-10 exp: none faster than the default).
   (void)lanes;
-  if (c->mv_w16) {
+  if (c->mv_win) {
+    const size_t dyn = sizeof(double4) * kMvStageMax;
+    RBF_TRY(ensure_dyn_smem((const void *)k_matvec_st<kExpDeg, 2>, dyn));
+    k_matvec_st<kExpDeg, 2><<<blocks, kMvThreads, dyn, s>>>(c->g, c->s, nl, own_off, c->rec, c->cell_start,
+                                                           c->mv_win, c->lane_tgt, lane1, c->chunk_len,
+                                                           c->chunk_off, reinterpret_cast<const unsigned *>(c->nlist),
+                                                           y_loc);
+  } else if (c->mv_w16) {
     k_matvec16<kExpDeg, 3><<<blocks, kMvThreads, 0, s>>>(
         c->g, own_off, c->s.ext_lo, n_ext(c), c->cell_start, c->rec, c->lane_tgt, lane1, c->chunk_len,
         c->chunk_off, reinterpret_cast<const unsigned short *>(c->nlist), y_loc, lane0);

@@ -852,11 +852,13 @@ def test_paper_ratio_oracle_parity(paper_sweep, ratio):
 # ------------------------------------------------------------------ matvec variants
 
 @pytest.mark.parametrize("env", [{"mv_targets_per_lane": 1}, {"mv_targets_per_lane": 3},
-                                 {"mv_pair_targets": 0}, {"mv_variant": 1}, {"mv_index16": 1}],
-                         ids=["G1", "G3", "consecutive", "deg9", "index16"])
+                                 {"mv_pair_targets": 0}, {"mv_variant": 1}, {"mv_index16": 1},
+                                 {"mv_variant": 5}],
+                         ids=["G1", "G3", "consecutive", "deg9", "index16", "staged"])
 def test_matvec_variants_parity(env, lib_options):
-    """Every neighbour-list layout (targets per lane, pairing) and the degree-9 exp
-    give the oracle's matvec; the layouts (same exp) agree bitwise with the default."""
+    """Every neighbour-list layout (targets per lane, pairing), the staged-source variant
+    and the degree-9 exp give the oracle's matvec; the layouts (same exp) agree bitwise
+    with the default."""
     wl = SMALL[3]
     w = np.random.default_rng(41).standard_normal(wl.n)
     ref = O.matvec_brute(wl.xy, w, wl.sigma, wl.rc)
@@ -866,8 +868,22 @@ def test_matvec_variants_parity(env, lib_options):
     with ctx_for(wl, rings=0) as c:
         y = to_caller(c, c.matvec(c.to_local(torch.from_numpy(w).cuda())))
     assert rel(y, ref) <= 1e-12
-    if "mv_variant" not in env:
+    if env.get("mv_variant", 5) == 5:  # same exp: bitwise (staged: the same records from shared memory)
         assert np.array_equal(y, y0)
+
+
+def test_matvec_staged_variant_bitwise_on_lattice(lib_options):
+    """Variant 5 (sources staged in shared memory per CTA window) on a
+    jittered 256^2 lattice, where most CTAs' windows fit and the row-crossing and
+    leftover-single CTAs fall back to global gathers: bitwise equal to the default."""
+    wl = W.make_lattice(256, jitter_frac=0.1, seed=12)
+    w = torch.from_numpy(np.random.default_rng(43).standard_normal(wl.n)).cuda()
+    with ctx_for(wl, rings=0) as c:
+        y0 = to_caller(c, c.matvec(c.to_local(w)))
+    lib_options(mv_variant=5)
+    with ctx_for(wl, rings=0) as c:
+        y = to_caller(c, c.matvec(c.to_local(w)))
+    assert np.array_equal(y, y0)
 
 
 # ------------------------------------------------ T-box truncation (reading Q25, §8.f2)
