@@ -1027,19 +1027,22 @@ __device__ __forceinline__ void lu_cell(Geom g, Strip st, const double2 *__restr
     pos[p] = xy[nat_to_global(R, q) - st.ext_lo];
   }
   __syncthreads();
-  for (long long t = tid; t < (long long)n * lda; t += T) {
-    const int i = (int)(t / lda), j = (int)(t - (long long)i * lda);
-    double v;
-    if (j < n) {
-      const double dx = pos[i].x - pos[j].x, dy = pos[i].y - pos[j].y;
+  // row by row (no 64-bit index division); the no-pivot pass assembles only what its
+  // symmetric factorisation reads: the lower triangle and each row's diagonal block
+  for (int i = 0; i < n; ++i) {
+    const double2 pi = pos[i];
+    double *Ai = A + (long long)i * lda;
+    const int jn = PIV ? n : min(n, ((i >> 5) << 5) + kLuNb);
+    for (int j = tid; j < jn; j += T) {
+      const double dx = pi.x - pos[j].x, dy = pi.y - pos[j].y;
       const double r2 = fma(dx, dx, dy * dy);
-      v = (r2 < g.rc2) ? exp(r2 * g.neg_inv_2s2) * g.norm : 0.0;
-    } else {  // column j - n = e_{natural index}, in factor order (own points last)
-      const int q = g.asm_full ? (int)(j - n) : own_nat + (int)(j - n);
-      const int fq = q < own_nat ? q : (q < own_nat + n_own ? n0 + (q - own_nat) : q - n_own);
-      v = (i == fq) ? 1.0 : 0.0;
+      Ai[j] = (r2 < g.rc2) ? exp(r2 * g.neg_inv_2s2) * g.norm : 0.0;
     }
-    A[t] = v;
+    for (int j = n + tid; j < lda; j += T) {  // column j - n = e_{natural index}, in factor order
+      const int q = g.asm_full ? j - n : own_nat + (j - n);
+      const int fq = q < own_nat ? q : (q < own_nat + n_own ? n0 + (q - own_nat) : q - n_own);
+      Ai[j] = (i == fq) ? 1.0 : 0.0;
+    }
   }
   __syncthreads();
   LUP(0)
