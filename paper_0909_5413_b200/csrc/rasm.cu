@@ -1660,12 +1660,22 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
       RBF_CUDA_TRY(cudaMemcpyAsync(&hretry, nretry, sizeof(int), cudaMemcpyDeviceToHost, s));
       RBF_CUDA_TRY(cudaStreamSynchronize(s));
       rest_piv = 4 * hretry > probe;
-      if (rest > 0) RBF_TRY(pass(rest_piv, sorted + nbd + probe, rest, n_rest));
-      if (rest > 0 && !rest_piv) {
-        RBF_CUDA_TRY(cudaMemcpyAsync(&hretry, nretry, sizeof(int), cudaMemcpyDeviceToHost, s));
-        RBF_CUDA_TRY(cudaStreamSynchronize(s));
+      if (rest_piv) {
+        // one pivoting pass over the probe's failed cells (the largest) followed by the
+        // rest, so that the largest cells start first (longest-processing-time order)
+        // instead of forming a last wave of their own
+        if (rest > 0)
+          RBF_CUDA_TRY(cudaMemcpyAsync(retry + hretry, sorted + nbd + probe, sizeof(int) * (size_t)rest,
+                                       cudaMemcpyDeviceToDevice, s));
+        if (hretry + rest > 0) RBF_TRY(pass(true, retry, hretry + rest, hretry > 0 ? n_sz : n_rest));
+      } else {
+        if (rest > 0) RBF_TRY(pass(false, sorted + nbd + probe, rest, n_rest));
+        if (rest > 0) {
+          RBF_CUDA_TRY(cudaMemcpyAsync(&hretry, nretry, sizeof(int), cudaMemcpyDeviceToHost, s));
+          RBF_CUDA_TRY(cudaStreamSynchronize(s));
+        }
+        if (hretry > 0) RBF_TRY(pass(true, retry, hretry, n_sz));
       }
-      if (hretry > 0) RBF_TRY(pass(true, retry, hretry, n_sz));
     }
     c->n_lu_pivot = nbd + (nopiv ? hretry + (rest_piv ? rest : 0) : nsz);  // cells factored with partial pivoting
     count_launch(9);  // sizes, two sorts
