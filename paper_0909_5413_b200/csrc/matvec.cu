@@ -92,7 +92,7 @@ __device__ __forceinline__ void lane_targets(const int4 *__restrict__ tgt, long 
 // of the current row's run (cell_start[(by0 + row) ncx + bx0]); the lane's box corner key
 // by0 ncx + bx0 is kept in its lane_tgt .w.  MODE 0 reports the largest offset and row
 // step (fmt[0], fmt[1]) so the host picks 16-bit entries only when they fit.
-template <int MODE, int G, bool W16 = false>
+template <int MODE, int G, bool W16 = false, bool ST = false>
 __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const double2 *__restrict__ xy,
                                                       const int *__restrict__ cell_start, long long nloc,
                                                       int4 *__restrict__ tgt, long long nlanes,
@@ -138,8 +138,8 @@ __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const do
   // matvec variant 5: entries are slots of the CTA's staged window (its rows' runs
   // [cell_start(by, wbx0), cell_start(by, wbx1 + 1)) back to back) instead of indices
   int4 wv = make_int4(-1, -1, 0, -1);
-  if (MODE == 1 && win && in_chunk) wv = win[lt / kMvThreads];
-  const bool staged = wv.x >= 0;
+  if (ST && MODE == 1 && in_chunk) wv = win[lt / kMvThreads];
+  const bool staged = ST && wv.x >= 0;
   long long wslot = 0;  // slot of the first source of row wv.z + r, advanced row by row
   if (staged)
     for (int by = wv.z; by < by0; ++by)
@@ -833,7 +833,7 @@ int build_nlist(rbf_ctx *c, cudaStream_t s) {
   if (c->mv_w16) {
     RBF_NLIST(1, true, c->chunk_off, c->nlist);
   } else if (stage) {
-    k_nlist<1, 2><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, c->lane_tgt, lanes,
+    k_nlist<1, 2, false, true><<<blocks, kMvThreads, 0, s>>>(c->g, c->s, c->xy_ext, c->cell_start, nl, c->lane_tgt, lanes,
                                                c->chunk_len, c->chunk_off, c->nlist, nu, ll, fmt, c->mv_win);
   } else {
     RBF_NLIST(1, false, c->chunk_off, c->nlist);
