@@ -101,7 +101,11 @@ typedef struct {
   double trunc_width;
 } rbf_params;
 
-/* Domain decomposition into strips of cell rows.
+/* Domain decomposition into strips of cell rows.  The rows
+ * are cut by a work model computed identically on every rank (per cell: n_own (0.28 S +
+ * n_ov), S = points in the matvec stencil, n_ov = subdomain size -- matvec pairs plus
+ * RASM apply entries), so a dense cluster is split across strips; on uniform data this
+ * is the same as balancing points.
  *  rank, nranks   this process's strip and the strip count (1 <= nranks).
  *  comm           RBF_COMM_NCCL: halos/reductions go through an NCCL communicator
  *                 created from nccl_id (one process per GPU; the caller selects the

@@ -584,10 +584,17 @@ int rbf_setup(rbf_ctx **out, const double *xy, int64_t n, const rbf_params *p, c
   int st = build_cell_list(c, xy, s);
   cudaEventRecord(ev[1], s);
   if (st != RBF_OK) { rbf_destroy(c); return st; }
-  // strips of cell rows, balanced by point count; each strip >= halo depth rows
+  // strips of cell rows balanced by a work model (matvec pairs + RASM apply entries per
+  // row; on uniform data the same as balancing points); each strip >= halo
+  // depth rows
   const int depth = g.kh > g.rings ? g.kh : g.rings;
   std::vector<long long> counts(g.ncy), bounds(c->nranks + 1);
-  for (int r = 0; r < g.ncy; ++r) counts[r] = c->row_start[r + 1] - c->row_start[r];
+  if (c->nranks > 1) {
+    st = row_costs(c, s, counts);
+    if (st != RBF_OK) { rbf_destroy(c); return st; }
+  } else {
+    for (int r = 0; r < g.ncy; ++r) counts[r] = c->row_start[r + 1] - c->row_start[r];
+  }
   st = plan_strips(counts.data(), g.ncy, c->nranks, c->nranks > 1 ? depth : 1, bounds.data());
   if (st != RBF_OK) { rbf_destroy(c); return st; }
   plan_strip(c->row_start.data(), g.ncy, bounds.data(), c->nranks, c->rank, depth, g.kh, g.rings,

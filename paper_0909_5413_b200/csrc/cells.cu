@@ -260,4 +260,42 @@ int count_pairs(rbf_ctx *c, long long *out, cudaStream_t s) {
   return RBF_OK;
 }
 
+// Strip cost of each cell row (cfg5's cluster core must be split by work,
+// not by points): per cell, n_own (0.28 S + n_ov) scaled by 25 to integers, where S is
+// the number of points in the matvec stencil (about 0.28 S of them within rc: pairs) and
+// n_ov the subdomain size (the RASM apply streams n_own n_ov entries of X); one pair and
+// one X entry cost about the same (FP64-bound matvec vs HBM-bound apply).  Integer sums,
+// so every rank computes the same partition.
+__global__ void k_row_costs(Geom g, const int *__restrict__ cell_start, unsigned long long *__restrict__ cost) {
+  const long long cl = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (cl >= (long long)g.ncx * g.ncy) return;
+  const int cy = (int)(cl / g.ncx), cx = (int)(cl - (long long)cy * g.ncx);
+  const long long own = cell_start[cl + 1] - cell_start[cl];
+  if (own == 0) return;
+  auto box = [&](int k) {
+    long long n = 0;
+    const int x0 = max(cx - k, 0), x1 = min(cx + k, g.ncx - 1);
+    for (int y = max(cy - k, 0); y <= min(cy + k, g.ncy - 1); ++y)
+      n += cell_start[y * g.ncx + x1 + 1] - cell_start[y * g.ncx + x0];
+    return n;
+  };
+  atomicAdd(&cost[cy], (unsigned long long)(own * (7 * box(g.kh) + 25 * box(g.rings > 0 ? g.rings : 1))));
+}
+
+int row_costs(rbf_ctx *c, cudaStream_t s, std::vector<long long> &out) {
+  const Geom &g = c->g;
+  out.assign(g.ncy, 0);
+  unsigned long long *d = nullptr;
+  ScratchGuard sg(s);
+  RBF_TRY(sg.alloc(c, &d, sizeof(unsigned long long) * (size_t)g.ncy));
+  RBF_CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(unsigned long long) * (size_t)g.ncy, s));
+  const long long ncl = (long long)g.ncx * g.ncy;
+  k_row_costs<<<(int)((ncl + 255) / 256), 256, 0, s>>>(g, c->cell_start, d);
+  count_launch(1);
+  RBF_CUDA_TRY(cudaGetLastError());
+  RBF_CUDA_TRY(cudaMemcpyAsync(out.data(), d, sizeof(long long) * (size_t)g.ncy, cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  return RBF_OK;
+}
+
 }  // namespace rbf

@@ -332,6 +332,7 @@ struct ScratchGuard {
 
 // cells.cu
 int build_cell_list(rbf_ctx *c, const double *xy_caller, cudaStream_t s);
+int row_costs(rbf_ctx *c, cudaStream_t s, std::vector<long long> &out);  // strip cost per cell row
 int count_pairs(rbf_ctx *c, long long *out, cudaStream_t s);
 int launch_to_local(const rbf_ctx *c, const double *v_caller, double *v_loc, cudaStream_t s);
 int launch_from_local(const rbf_ctx *c, const double *v_loc, double *v_caller, cudaStream_t s);

@@ -216,3 +216,24 @@ def test_evaluate_pair_count_brute_force():
     # the kernel's fma(dx,dx,dy*dy) < rc^2 and numpy's sum differ only for pairs within
     # rounding of the cutoff (none in seeded uniform data at this size)
     assert n == int((d2 < wl.rc ** 2).sum())
+
+
+def test_threads_strips_cut_by_work_on_clustered_data():
+    """cfg5's cluster core is split by work, not by points.  cfg5 recipe at
+    65,536 points, 4 in-process strips: the per-strip work (in-cutoff matvec pairs + RASM
+    X entries) stays near the mean while the point counts differ widely."""
+    wl = W.make_clustered(65536, seed=5)
+    xy = torch.from_numpy(wl.xy).cuda()
+
+    def body(r, key, st):
+        with P.Context(xy, wl.sigma, wl.cell, wl.rc, 1, wl.box, rank=r, nranks=4,
+                       comm="threads", nccl_id=key, stream=st) as c:
+            return c.count_pairs(), c.info()["x_doubles"], c.n_local
+
+    res = _threads(4, body)
+    work = np.array([p + x for p, x, _ in res], dtype=float)
+    npts = np.array([n for *_, n in res])
+    print("work per strip", work / work.mean(), "points", npts)
+    assert npts.sum() == wl.n
+    assert work.max() <= 1.3 * work.mean()
+    assert npts.max() >= 1.5 * npts.min()  # a point-count cut would not have done this
