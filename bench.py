@@ -226,9 +226,29 @@ def run_reference(args, rank, world):
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": full.name, "N": full.n},
             "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "oracle",
-                             "sample": desc},
+                             "sample": desc, **host_info()},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def host_info():
+    """CPU model and host RAM of the box the oracle runs on (recorded with
+    the oracle timing)."""
+    model, ram = None, None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as fh:
+            for ln in fh:
+                if ln.startswith("MemTotal"):
+                    ram = round(int(ln.split()[1]) / 2**20, 1)
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "host_ram_gib": ram}
 
 
 # --------------------------------------------------------------------------- our arm
@@ -480,7 +500,7 @@ def run_ours(args, rank, world):
         cores = os.cpu_count() or 1
         os.environ["OMP_NUM_THREADS"] = str(cores)
         v, desc = oracle_estimate(args.config, None if weak else wl)
-        cpu = {"value": v, "unit": "s", "cores": cores, "kind": "oracle", "sample": desc}
+        cpu = {"value": v, "unit": "s", "cores": cores, "kind": "oracle", "sample": desc, **host_info()}
 
     if rank == 0:
         r0 = reps[0]
