@@ -419,11 +419,19 @@ class Context:
 
 def interpolate_host(xy: np.ndarray, f: np.ndarray, sigma, cell, rc, rings=1,
                      box=(-1.0, -1.0, 1.0, 1.0), restart=30, max_iters=1000, rtol=1e-13,
-                     atol=0.0, stream=None, overlap_width=0.0, orth="mgs", trunc_width=0.0):
-    """rbf_interpolate_host: host buffers in caller order -> weights lambda (host)."""
+                     atol=0.0, stream=None, overlap_width=0.0, orth="mgs", trunc_width=0.0,
+                     out=None):
+    """rbf_interpolate_host: host buffers in caller order -> weights lambda (host).  `out`:
+    optional float64 host array for lambda (e.g. pinned memory, reused across calls)."""
     xy = np.ascontiguousarray(xy, dtype=np.float64)
     f = np.ascontiguousarray(f, dtype=np.float64)
-    lam = np.empty_like(f)
+    if out is not None:
+        if (not isinstance(out, np.ndarray) or out.dtype != np.float64 or out.shape != f.shape
+                or not out.flags.c_contiguous):
+            raise ValueError("interpolate_host: out must be a contiguous float64 array shaped like f")
+        lam = out
+    else:
+        lam = np.empty_like(f)
     prm = make_params(sigma, cell, rc, rings, box, overlap_width, trunc_width)
     gp = GmresParams(int(restart), int(max_iters), float(rtol), float(atol), 0,
                      {"mgs": 0, "cgs2": 1, "dcgs2": 2}[orth])

@@ -224,6 +224,12 @@ def test_interpolate_host_matches_context(cfg1_oracle):
     lam, rep = P.interpolate_host(wl.xy, wl.f, wl.sigma, wl.cell, wl.rc, 1, wl.box, rtol=wl.tol)
     assert rep.converged and abs(rep.iterations - ref.iterations) <= 2
     assert rel(lam, ref.x) <= 1e-8
+    # the same into a caller-provided pinned buffer (what bench.py's e2e leg passes)
+    out = torch.empty(wl.n, dtype=torch.float64).pin_memory().numpy()
+    lam2, _ = P.interpolate_host(wl.xy, wl.f, wl.sigma, wl.cell, wl.rc, 1, wl.box, rtol=wl.tol, out=out)
+    assert lam2 is out and np.array_equal(lam2, lam)
+    with pytest.raises(ValueError):
+        P.interpolate_host(wl.xy, wl.f, wl.sigma, wl.cell, wl.rc, 1, wl.box, out=np.empty(3))
 
 
 def test_solve_parity_jittered_restarts():
