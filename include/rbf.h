@@ -69,8 +69,11 @@ enum {
  *                 sum_c R_c^T A_c^-1 R_c: every subdomain adds its whole local solution
  *                 (sums in ascending cell order, reading Q26).  Stores the full A_c^-1
  *                 (|Omega_c|^2 doubles per cell, ~9x the RASM blocks) and solves every
- *                 subdomain with the LU path; single-rank contexts only (EUNSUPPORTED
- *                 otherwise).
+ *                 subdomain with the LU path.  Across strips the t_c entries of the
+ *                 overlap_rings cell rows next to each strip edge are exchanged with the
+ *                 neighbours (rbf_rasm_apply; the sums stay in ascending cell order, so
+ *                 bitwise equal to one strip); needs overlap_width 0 there, and
+ *                 rbf_rasm_apply_ext returns EUNSUPPORTED for it.
  *  x0,y0,x1,y1    domain box; every point must satisfy x0 <= x <= x1, y0 <= y <= y1.
  *  overlap_width  >= 0.  0: Omega_c is the whole block (above).  > 0: the paper's box
  *                 overlap ("overlapping subdomains of size D"; reading Q24):
@@ -223,8 +226,9 @@ int rbf_from_local(const rbf_ctx *ctx, const double *v_loc_dev, double *v_caller
 int rbf_matvec(rbf_ctx *ctx, const double *w_loc_dev, double *y_loc_dev, void *stream);
 /* z = M^-1 r (PCApply / MatSolve, Eq.(10)-(11)): halo exchange of r
  * (overlap_rings rows), then z[own(c)] = (A_c^-1 R_c r)[own(c)] for every cell
- * (with RBF_SCHWARZ_ASM: t_c = A_c^-1 R_c r per cell, then z_i = sum of the t_c entries
- * of point i over the subdomains containing it, ascending cell order, Eq.(8)). */
+ * (with RBF_SCHWARZ_ASM: t_c = A_c^-1 R_c r per cell, the boundary rows' t_c exchanged
+ * with the neighbouring strips, then z_i = sum of the t_c entries of point i over the
+ * subdomains containing it, ascending cell order, Eq.(8)). */
 int rbf_rasm_apply(rbf_ctx *ctx, const double *r_loc_dev, double *z_loc_dev, void *stream);
 /* Same two operators with the halo supplied by the caller: w_ext_dev holds
  * rbf_ext_count() entries = global sorted entries [ext_lo, ext_hi). */

@@ -569,8 +569,8 @@ int rbf_setup(rbf_ctx **out, const double *xy, int64_t n, const rbf_params *p, c
   g.kh = (int)std::ceil(p->rc / p->cell * (1.0 + 1e-12));
   g.tw = p->trunc_width;
   g.asm_full = p->schwarz == RBF_SCHWARZ_ASM;
-  if (g.asm_full && c->nranks > 1) {
-    set_error("rbf_setup: RBF_SCHWARZ_ASM is single-rank only (the Eq.(8) sums cross strips)");
+  if (g.asm_full && c->nranks > 1 && p->overlap_width > 0.0) {
+    set_error("rbf_setup: RBF_SCHWARZ_ASM across strips needs whole-ring overlap (overlap_width 0)");
     rbf_destroy(c);
     return RBF_EUNSUPPORTED;
   }
@@ -685,6 +685,10 @@ int rbf_matvec_ext(rbf_ctx *c, const double *w_ext, double *y, void *stream) {
 
 int rbf_rasm_apply_ext(rbf_ctx *c, const double *r_ext, double *z, void *stream) {
   if (!c || !r_ext || !z) { set_error("NULL argument"); return RBF_EINVAL; }
+  if (c->g.asm_full && c->nranks > 1) {  // the Eq.(8) sums need the neighbours' t (rbf_rasm_apply)
+    set_error("rbf_rasm_apply_ext: RBF_SCHWARZ_ASM across strips needs rbf_rasm_apply (t exchange)");
+    return RBF_EUNSUPPORTED;
+  }
   return launch_rasm_apply(c, r_ext, z, (cudaStream_t)stream);
 }
 

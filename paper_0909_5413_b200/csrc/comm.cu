@@ -241,6 +241,22 @@ int dist_matvec(rbf_ctx *c, const double *w_loc, double *y_loc, cudaStream_t s) 
 // the interior cells while the halo (overlap_rings rows) is exchanged, then the cells
 // next to the strip edges.
 int dist_rasm_apply(rbf_ctx *c, const double *r_loc, double *z_loc, cudaStream_t s) {
+  if (c->g.asm_full) {
+    // Eq.(8) across strips: r's halo, the own cells' t_c, then the t of the rings rows
+    // next to each strip edge both ways (a point near the edge sums subdomains of both
+    // strips, in ascending cell order as on one strip: bitwise the same sums)
+    RBF_TRY(halo_exchange(c, r_loc, c->w_ext, false, s));
+    RBF_TRY(launch_asm_local(c, c->w_ext, s));
+    if (c->comm_mode == RBF_COMM_THREADS) {
+      RBF_TRY(halo_exchange_threads(c, c->asm_t + c->asm_sb, c->asm_t, c->halo_asm, s));
+    } else if (c->comm_mode == RBF_COMM_NCCL) {
+      RBF_TRY(nccl_halo(c, c->asm_t + c->asm_sb, c->asm_t, c->halo_asm, s));
+    } else {
+      set_error("virtual strip context (RBF_COMM_NONE) has no communicator: use the *_ext calls");
+      return RBF_EUNSUPPORTED;
+    }
+    return launch_asm_gather(c, z_loc, s);
+  }
   if (!c->overlap) {
     RBF_TRY(halo_exchange(c, r_loc, c->w_ext, false, s));
     return launch_rasm_apply(c, c->w_ext, z_loc, s);

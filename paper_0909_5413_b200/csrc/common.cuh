@@ -246,6 +246,9 @@ struct rbf_ctx {
   double *asm_t = nullptr;        // ASM: the local solutions t_c = A_c^-1 R_c u
   int *asm_map = nullptr;         // ASM: per point, the t entries that sum to z_i (cell order)
   long long *asm_poff = nullptr;  // ASM: CSR offsets of asm_map (n_loc + 1)
+  long long asm_sb = 0;           // ASM across strips: asm_t = [t of the rings rows below the strip
+                                  // (sb entries, from rank-1) | own cells' t | rows above (rank+1)]
+  rbf::Halo halo_asm[2]{};        // ASM: exchange of the boundary rows' t with the neighbours
   long long x_count = 0;
   int max_ov = 0, max_own = 0, nsub = 0, n_lu = 0;
   int n_lu_pivot = 0;          // LU-path subdomains that needed row exchanges
@@ -357,6 +360,8 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s);
 int probe_read(long long *out);  // RBF_PROBE builds only
 // part 0 = every cell, 1 = the interior cells, 2 = the cells within overlap_rings rows of
 // a strip edge with a neighbour rank (only these read the halo)
+int launch_asm_local(const rbf_ctx *c, const double *r_ext, cudaStream_t s);  // Eq.(8) t_c, own cells
+int launch_asm_gather(const rbf_ctx *c, double *z_loc, cudaStream_t s);      // Eq.(8) sums
 int launch_rasm_apply(const rbf_ctx *c, const double *r_ext, double *z_loc, cudaStream_t s, int part = 0);
 
 // comm.cu

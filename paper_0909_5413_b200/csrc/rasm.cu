@@ -1375,28 +1375,46 @@ __global__ __launch_bounds__(kRaThreads) void k_asm_local(
   }
 }
 
-// (point, t index) pairs in (cell, position) order, for the stable sort by point
-__global__ void k_asm_entries(Geom g, Strip st, const int *__restrict__ cell_start,
-                              const long long *__restrict__ t_off, int *__restrict__ key,
+// t sizes (n_ov, or 0 for an empty cell) of the cells of rows [row0, row0 + ncl_e / ncx):
+// the strip's own rows plus, across strips, the `rings` rows on each side whose
+// subdomains reach into the strip
+__global__ void k_asm_tsizes(Geom g, Strip st, const int *__restrict__ cell_start, int row0, int ncl_e,
+                             long long *__restrict__ tsizes, OvList ov) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e > ncl_e) return;
+  if (e == ncl_e) { tsizes[e] = 0; return; }
+  const int cy = row0 + e / g.ncx, cx = e % g.ncx;
+  Runs R;  // box-overlap lists exist for the own cells only (ASM across strips needs whole rings)
+  sub_runs(g, cell_start, ov, cy - st.row_lo >= 0 ? (cy - st.row_lo) * g.ncx + cx : 0, cx, cy, R);
+  tsizes[e] = R.n_own ? R.n_ov : 0;
+}
+
+// (point, t index) pairs in (cell, position) order, for the stable sort by point; cells of
+// rows [row0, ...) with t offsets t_off; points outside the strip get the key npts (sorted
+// last, not summed)
+__global__ void k_asm_entries(Geom g, Strip st, const int *__restrict__ cell_start, int row0,
+                              const long long *__restrict__ t_off, long long npts, int *__restrict__ key,
                               int *__restrict__ val, OvList ov) {
-  const int cl = blockIdx.x;
-  const int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
+  const int e = blockIdx.x;
+  const int cy = row0 + e / g.ncx, cx = e % g.ncx;
   Runs R;
-  sub_runs(g, cell_start, ov, cl, cx, cy, R);
+  sub_runs(g, cell_start, ov, cy - st.row_lo >= 0 ? (cy - st.row_lo) * g.ncx + cx : 0, cx, cy, R);
   if (R.n_own == 0) return;
-  const long long o = t_off[cl];
+  const long long o = t_off[e];
   for (int q = threadIdx.x; q < R.n_ov; q += blockDim.x) {
-    key[o + q] = nat_to_global(R, q) - (int)st.own_lo;
+    const long long k = nat_to_global(R, q) - st.own_lo;
+    key[o + q] = (int)(k >= 0 && k < npts ? k : npts);
     val[o + q] = (int)(o + q);
   }
 }
 
-// CSR offsets from the sorted keys: every point has >= 1 entry (its own cell)
+// CSR offsets from the sorted keys: every point has >= 1 entry (its own cell); the keys
+// npts (entries for other strips' points) are last and close the table
 __global__ void k_asm_offsets(const int *__restrict__ skey, long long total, long long npts,
                               long long *__restrict__ poff) {
   const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (k < total && (k == 0 || skey[k] != skey[k - 1])) poff[skey[k]] = k;
-  if (k == 0) poff[npts] = total;
+  if (k < total && (k == 0 || skey[k] != skey[k - 1]) && skey[k] <= npts) poff[skey[k]] = k;
+  if (k == 0 && (total == 0 || skey[total - 1] < npts)) poff[npts] = total;
 }
 
 __global__ void k_asm_gather(const long long *__restrict__ poff, const int *__restrict__ map,
@@ -1410,37 +1428,67 @@ __global__ void k_asm_gather(const long long *__restrict__ poff, const int *__re
 
 static OvList ov_of(const rbf_ctx *c) { return OvList{c->ov_idx, c->ov_off, c->ov_own}; }
 
-static int build_asm_map(rbf_ctx *c, int ncl, long long total, cudaStream_t s) {
+static int build_asm_map(rbf_ctx *c, int ncl, long long total_own, cudaStream_t s) {
   const long long np = n_loc(c);
+  const Geom &g = c->g;
+  // across strips: the rings rows on each side whose subdomains reach into this strip
+  const int nrows = c->s.row_hi - c->s.row_lo;
+  const int rb = (c->nranks > 1 && c->rank > 0) ? g.rings : 0;
+  const int ra = (c->nranks > 1 && c->rank < c->nranks - 1) ? g.rings : 0;
+  const int row0 = c->s.row_lo - rb, ncl_e = (nrows + rb + ra) * g.ncx;
+  ScratchGuard sg(s);
+  long long *tsz = nullptr, *toff = nullptr;
+  RBF_TRY(sg.alloc(c, &tsz, sizeof(long long) * (size_t)(ncl_e + 1)));
+  RBF_TRY(sg.alloc(c, &toff, sizeof(long long) * (size_t)(ncl_e + 1)));
+  k_asm_tsizes<<<(ncl_e + 256) / 256, 256, 0, s>>>(g, c->s, c->cell_start, row0, ncl_e, tsz, ov_of(c));
+  size_t tb0 = 0;
+  RBF_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb0, tsz, toff, ncl_e + 1, s));
+  void *tmp0 = nullptr;
+  RBF_TRY(sg.alloc(c, &tmp0, tb0));
+  RBF_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp0, tb0, tsz, toff, ncl_e + 1, s));
+  // block boundaries: below | own | above, and the boundary rows sent to the neighbours
+  long long hb[5] = {0, 0, 0, 0, 0};
+  const int idx[5] = {rb * g.ncx, (rb + rb) * g.ncx, (rb + nrows - ra) * g.ncx, (rb + nrows) * g.ncx, ncl_e};
+  for (int k = 0; k < 5; ++k)
+    RBF_CUDA_TRY(cudaMemcpyAsync(&hb[k], toff + idx[k], sizeof(long long), cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  const long long sb = hb[0], so = hb[3] - hb[0], total = hb[4];
+  if (so != total_own) {
+    set_error("rbf_setup: ASM local-solution sizes disagree (%lld vs %lld)", so, total_own);
+    return RBF_EINVAL;
+  }
   if (total >= (1LL << 31)) {
     set_error("rbf_setup: ASM needs %lld local-solution entries (limit 2^31)", total);
     return RBF_EUNSUPPORTED;
   }
+  c->asm_sb = sb;
+  // t exchange: to rank - 1 the own first rb rows' t, from it the rb rows below; to rank + 1
+  // the own last ra rows' t, from it the ra rows above (offsets: send in the own block,
+  // receive in the whole buffer)
+  c->halo_asm[0] = Halo{0, rb ? hb[1] - sb : 0, 0, sb};
+  c->halo_asm[1] = Halo{ra ? hb[2] - sb : 0, ra ? hb[3] - hb[2] : 0, hb[3], total - hb[3]};
   int *key = nullptr, *val = nullptr, *skey = nullptr;
-  RBF_TRY(dalloc(c, (void **)&key, sizeof(int) * (size_t)total, s));
-  RBF_TRY(dalloc(c, (void **)&val, sizeof(int) * (size_t)total, s));
-  RBF_TRY(dalloc(c, (void **)&skey, sizeof(int) * (size_t)total, s));
-  RBF_TRY(dalloc(c, (void **)&c->asm_map, sizeof(int) * (size_t)total, s));
+  RBF_TRY(sg.alloc(c, &key, sizeof(int) * (size_t)(total > 0 ? total : 1)));
+  RBF_TRY(sg.alloc(c, &val, sizeof(int) * (size_t)(total > 0 ? total : 1)));
+  RBF_TRY(sg.alloc(c, &skey, sizeof(int) * (size_t)(total > 0 ? total : 1)));
+  RBF_TRY(dalloc(c, (void **)&c->asm_map, sizeof(int) * (size_t)(total > 0 ? total : 1), s));
   RBF_TRY(dalloc(c, (void **)&c->asm_poff, sizeof(long long) * (size_t)(np + 1), s));
-  RBF_TRY(dalloc(c, (void **)&c->asm_t, sizeof(double) * (size_t)total, s));
-  k_asm_entries<<<ncl, 128, 0, s>>>(c->g, c->s, c->cell_start, c->asm_toff, key, val, ov_of(c));
+  RBF_TRY(dalloc(c, (void **)&c->asm_t, sizeof(double) * (size_t)(total > 0 ? total : 1), s));
+  k_asm_entries<<<ncl_e, 128, 0, s>>>(g, c->s, c->cell_start, row0, toff, np, key, val, ov_of(c));
   RBF_CUDA_TRY(cudaGetLastError());
   int end_bit = 1;
-  while ((1LL << end_bit) < np) ++end_bit;
+  while ((1LL << end_bit) <= np) ++end_bit;  // keys up to np (other strips' points)
   size_t tb = 0;
   RBF_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, key, skey, val, c->asm_map, (int)total, 0,
                                                end_bit, s));
   void *tmp = nullptr;
-  RBF_TRY(dalloc(c, &tmp, tb, s));
+  RBF_TRY(sg.alloc(c, &tmp, tb));
   RBF_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tb, key, skey, val, c->asm_map, (int)total, 0,
                                                end_bit, s));  // stable: cell order kept per point
-  k_asm_offsets<<<(int)((total + 255) / 256), 256, 0, s>>>(skey, total, np, c->asm_poff);
-  count_launch(3 + (end_bit + 7) / 8);
+  k_asm_offsets<<<(int)((total + 255) / 256) + 1, 256, 0, s>>>(skey, total, np, c->asm_poff);
+  count_launch(6 + (end_bit + 7) / 8);
   RBF_CUDA_TRY(cudaGetLastError());
-  dfree(tmp, s);
-  dfree(key, s);
-  dfree(val, s);
-  dfree(skey, s);
+  (void)ncl;
   return RBF_OK;
 }
 
@@ -1701,20 +1749,36 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
   return RBF_OK;
 }
 
+int launch_asm_local(const rbf_ctx *c, const double *r_ext, cudaStream_t s) {
+  const int ncl = owned_cells(c);
+  if (ncl <= 0 || c->nsub == 0) return RBF_OK;
+  const size_t smem = sizeof(double) * (size_t)(c->max_ov + 2);
+  RBF_TRY(ensure_dyn_smem((const void *)k_asm_local, smem));
+  k_asm_local<<<ncl, kRaThreads, smem, s>>>(c->g, c->s, c->cell_start, c->x_off, c->asm_toff, c->X, r_ext,
+                                            c->asm_t + c->asm_sb, ov_of(c));
+  count_launch(1);
+  RBF_CUDA_TRY(cudaGetLastError());
+  return RBF_OK;
+}
+
+int launch_asm_gather(const rbf_ctx *c, double *z_loc, cudaStream_t s) {
+  const long long np = n_loc(c);
+  if (np <= 0) return RBF_OK;
+  k_asm_gather<<<(int)((np + 255) / 256), 256, 0, s>>>(c->asm_poff, c->asm_map, c->asm_t, np, z_loc);
+  count_launch(1);
+  RBF_CUDA_TRY(cudaGetLastError());
+  return RBF_OK;
+}
+
 int launch_rasm_apply(const rbf_ctx *c, const double *r_ext, double *z_loc, cudaStream_t s, int part) {
   const int ncl = owned_cells(c);
   if (ncl <= 0 || c->nsub == 0) return RBF_OK;
   const size_t smem = sizeof(double) * (size_t)(c->max_ov + 2);
-  if (c->g.asm_full) {  // Eq.(8): local solutions, then the per-point sums (single rank)
+  if (c->g.asm_full) {  // Eq.(8): local solutions, then the per-point sums (one strip; across
+                        // strips dist_rasm_apply exchanges the boundary rows' t in between)
     if (part == 2) return RBF_OK;
-    RBF_TRY(ensure_dyn_smem((const void *)k_asm_local, smem));
-    k_asm_local<<<ncl, kRaThreads, smem, s>>>(c->g, c->s, c->cell_start, c->x_off, c->asm_toff, c->X,
-                                              r_ext, c->asm_t, ov_of(c));
-    const long long np = n_loc(c);
-    k_asm_gather<<<(int)((np + 255) / 256), 256, 0, s>>>(c->asm_poff, c->asm_map, c->asm_t, np, z_loc);
-    count_launch(2);
-    RBF_CUDA_TRY(cudaGetLastError());
-    return RBF_OK;
+    RBF_TRY(launch_asm_local(c, r_ext, s));
+    return launch_asm_gather(c, z_loc, s);
   }
   // cell rows next to a strip edge with a neighbour rank read the halo (rings rows)
   const int nrows = c->s.row_hi - c->s.row_lo, ncx = c->g.ncx;

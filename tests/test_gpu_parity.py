@@ -1009,11 +1009,49 @@ def test_asm_solve_parity(wl):
     assert rel(lam, ref.x) <= 1e-8
 
 
-def test_asm_multirank_unsupported():
+def test_asm_multirank_limits():
+    """Eq.(8) across strips exchanges whole cell rows of local solutions: the box overlap
+    (rows of partial cells) is refused, and so is the caller-supplied-halo apply of a
+    virtual strip (it has no neighbours to exchange the t entries with)."""
     wl = W.make_lattice(60, jitter_frac=0.1, seed=5)
     xy = torch.from_numpy(wl.xy).cuda()
     with pytest.raises(P.RbfError):
-        P.Context(xy, wl.sigma, wl.cell, wl.rc, 1, wl.box, rank=0, nranks=2, schwarz="asm")
+        P.Context(xy, wl.sigma, wl.cell, wl.rc, 1, wl.box, rank=0, nranks=2, schwarz="asm",
+                  overlap_width=0.5 * wl.cell)
+    with P.Context(xy, wl.sigma, wl.cell, wl.rc, 1, wl.box, rank=0, nranks=2, schwarz="asm") as c:
+        r_ext = torch.zeros(c.n_ext, dtype=torch.float64, device="cuda")
+        with pytest.raises(P.RbfError):
+            c.rasm_apply_ext(r_ext)
+
+
+@pytest.mark.parametrize("nranks,rings", [(2, 1), (3, 1), (2, 2)])
+def test_threads_asm_bitwise(nranks, rings):
+    """Eq.(8) across in-process strips: each strip's local solutions plus the neighbours'
+    boundary rows, summed per point in ascending cell order -- bitwise the one-strip apply;
+    the multi-strip ASM solve agrees with the one-strip solve."""
+    wl = W.make_lattice(48, jitter_frac=0.1, seed=6)
+    rng = np.random.default_rng(12)
+    w = torch.from_numpy(rng.standard_normal(wl.n)).cuda()
+    f = torch.from_numpy(wl.f).cuda()
+    xy = torch.from_numpy(wl.xy).cuda()
+    with ctx_for(wl, rings=rings, schwarz="asm") as c1:
+        z1 = c1.from_local(c1.rasm_apply(c1.to_local(w))).cpu().numpy()
+        lam1, rep1 = c1.solve(c1.to_local(f), rtol=1e-12)
+        lam1 = c1.from_local(lam1).cpu().numpy()
+
+    def body(r, key, st):
+        with P.Context(xy, wl.sigma, wl.cell, wl.rc, rings, wl.box, rank=r, nranks=nranks,
+                       comm="threads", nccl_id=key, stream=st, schwarz="asm") as c:
+            z = c.from_local(c.rasm_apply(c.to_local(w))).cpu().numpy()
+            lam, rep = c.solve(c.to_local(f), rtol=1e-12)
+            return z, c.from_local(lam).cpu().numpy(), rep
+
+    res = _run_threads(nranks, body)
+    assert np.array_equal(sum(r[0] for r in res), z1)
+    lam = sum(r[1] for r in res)
+    assert all(r[2].converged for r in res) and rep1.converged
+    assert all(abs(r[2].iterations - rep1.iterations) <= 1 for r in res)
+    assert rel(lam, lam1) <= 1e-9
 
 
 @pytest.mark.parametrize("orth", ["mgs", "dcgs2"])
