@@ -1,5 +1,6 @@
-"""Orthogonalisation phase time of a cfg2 solve for env-var variants; not part of the product.
-Usage: orth_ab.py VAR=val,VAR2=val ..."""
+"""Orthogonalisation phase time of a cfg2 solve for library-option variants (rbf_set_option,
+e.g. mgs_pairs=0,fused_arnoldi=1); not part of the product.
+Usage: orth_ab.py opt=val,opt2=val ..."""
 import os
 import sys
 
@@ -16,7 +17,7 @@ for spec in sys.argv[1:]:
     for kv in spec.split(","):
         if kv:
             k, v = kv.split("=")
-            os.environ[k] = v
+            P.set_option(k, int(v))
     res = []
     for rep in range(3):
         c = P.Context(xy, wl.sigma, wl.cell, wl.rc, wl.rings, wl.box)
