@@ -21,6 +21,9 @@
 #include <type_traits>
 #include <vector>
 #include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -265,6 +268,23 @@ constexpr int kColCta = 20660;
 // 6 X copy-out; [7] cells, [8] sum of n
 __device__ long long g_lu_acc[512][10];
 __device__ long long g_lu_t[512];
+// k_rasm_setup_tc2 phase clocks per CTA (warp 0 lane 0): 0 cells, 1 runs + positions,
+// 2 Cholesky, 3 W + S^-1, 4 X
+__device__ long long g_t2_acc[512][8];
+__device__ long long g_t2_col[32][8];  // one interior cell of CTA 7: per column j (see T2C)
+__device__ long long g_t2_w[32][8];    // the same cell's W phase: warp 0 per step jt
+#define T2W(k)                                                                   \
+  if (blockIdx.x == 7 && t2_cellno == 40 && (threadIdx.x & 31) == 0 && jt < 32) \
+    g_t2_w[jt][k] = clock64();
+#define T2C(k)                                                                  \
+  if (blockIdx.x == 7 && t2_cellno == 40 && (threadIdx.x & 31) == 0 && j < 32) \
+    g_t2_col[j][k] = clock64();
+#define T2P(p)                                             \
+  if (threadIdx.x == 0) {                                  \
+    const long long t_ = clock64();                        \
+    if ((p) > 0) g_t2_acc[blockIdx.x][p] += t_ - t2_last;  \
+    t2_last = t_;                                          \
+  }
 #define LUP0() \
   if (threadIdx.x == 0) g_lu_t[blockIdx.x] = clock64();
 #define LUP(p) \
@@ -278,6 +298,9 @@ __device__ long long g_lu_t[512];
 #else
 #define LUP0()
 #define LUP(p)
+#define T2P(p) {}
+#define T2C(k) {}
+#define T2W(k) {}
 #define PROBE(i)
 #define TRACE(i)
 #define PCOL(a, j, k) {}
@@ -325,8 +348,7 @@ __device__ __forceinline__ void acc_finish(const AccSet &A, double *sm, int it, 
 
 // 8x8 Cholesky of the diagonal tile j in place (lanes 0..7 = rows) plus its inverse:
 // lower part = L_d, upper part (r < c) = Linv[c][r], rdiag = 1 / diag(L_d).
-__device__ __forceinline__ bool diag_factor(double *sm, double *rdiag, int j, int lane) {
-  double *D = sm + toff(j, j);
+__device__ __forceinline__ bool diag_factor_t(double *D, double *rdiag, int j, int lane) {
   double a[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) a[c] = (lane < 8) ? D[swz(lane, c)] : 1.0;
@@ -361,6 +383,9 @@ __device__ __forceinline__ bool diag_factor(double *sm, double *rdiag, int j, in
     rdiag[j * 8 + lane] = rinv;
   }
   return bad;
+}
+__device__ __forceinline__ bool diag_factor(double *sm, double *rdiag, int j, int lane) {
+  return diag_factor_t(sm + toff(j, j), rdiag, j, lane);
 }
 
 // A_c = R_c A_rc R_c^T (reading Q10) entries of tile (it, jt) at this lane's
@@ -674,13 +699,13 @@ __device__ __forceinline__ void setup_post(double *sm, double *rdiag, double2 *p
 __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
     Geom g, Strip st, const double2 *__restrict__ xy, const int *__restrict__ cell_start,
     const long long *__restrict__ x_off, double *__restrict__ X, int *__restrict__ counts,
-    int *__restrict__ glist, OvList ov) {
+    int *__restrict__ glist, OvList ov, const int *__restrict__ list) {
   TRACE(1)
   extern __shared__ __align__(16) double sm[];
   __shared__ Runs R;
   __shared__ int s_fail;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int cl = blockIdx.x;
+  const int cl = list ? list[blockIdx.x] : blockIdx.x;  // list: the cells k_rasm_setup_tc2 left
   const int cy = st.row_lo + cl / g.ncx, cx = cl % g.ncx;
   if (tid == 0) {
     sub_runs(g, cell_start, ov, cl, cx, cy, R);
@@ -792,6 +817,542 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
   }
 
   setup_post(sm, rdiag, pos, S, R, g, X, x_off, cl, tid, lane, warp);
+}
+
+// ---------------------------------------------------------------------------
+// Two factorisations per SM: k_rasm_setup_tc2 (same arithmetic as k_rasm_setup_tc).
+//
+// The one-CTA-per-SM kernel above holds the whole tile-packed factor (223 KB for
+// n = 225) although the left-looking column loop only ever reads the rows at or
+// below the current column: a row of L11 is final, and no longer read by the
+// factorisation, once its own column has been formed.  Here each such row is
+// copied to a per-CTA global workspace (L2-resident, column-major so that a
+// column of L11 is contiguous) as soon as the loop is done with it, and its
+// tiles' shared-memory slots are reused by the next columns.  The live set is
+// then at most (T-1-j)(j+1) + 2 tiles at column j (212 tiles = 106 KB for T = 29
+// instead of 435), so two CTAs of 8 warps fit on an SM and two subdomains are
+// factored concurrently: one CTA's per-column barriers and serial 8x8 diagonal
+// chain overlap the other CTA's tensor-core accumulations.
+//
+// Tile (it, jt) lives in slot slot[it(it+1)/2 + jt]; the slot plan (lowest free
+// slot first, in the order the loop forms and retires tiles) is computed on the
+// host per tile shape (T, T1) -- see t2_plan in rasm_setup -- together with the
+// slots that are free after the factorisation (the W phase streams the columns
+// of L11 back through them).  After the factorisation:
+//   W = L21 L11^-1 by a backward sweep over the columns jt of L11 (one warp per own
+//       tile row; column jt of L11 arrives by cp.async three columns ahead),
+//   S^-1 = L22^-T L22^-1 concurrently on the other four warps (as above),
+//   X_c = S^-1 [-W, I] written straight to HBM.
+// Persistent: 2 CTAs per SM take the cells from an atomic counter.  Cells with
+// more than 4 own tile rows (n_own > 32) are left to k_rasm_setup_tc (list).
+// ---------------------------------------------------------------------------
+constexpr int kT2Threads = 256;
+constexpr int kT2Warps = kT2Threads / 32;
+constexpr int kT2Acc = kT2Warps - 2;  // accumulate warps; the last two alternate as diagonal warps
+constexpr int kT2M = (kTcMaxTiles - 1 + kT2Acc - 1) / kT2Acc;  // tiles per accumulate warp and column
+constexpr int kT2MaxT1 = 4;           // own tile rows (n_own <= 32)
+constexpr int kT2Cap = 212;           // tile slots: max_j (T-1-j)(j+1) + 2 at T = 29
+constexpr int kT2Rec = 1024;          // bytes per (T, T1) plan record (see rbf::t2_plan)
+constexpr int kT2RecFree = 512;       // record offset of the free-slot list
+constexpr int kT2RecPeak = 1016;      // int: slots used; int at 1020: free slots after the factorisation
+constexpr int kT2WsTiles = kTcMaxTiles * (kTcMaxTiles + 1) / 2;  // workspace tiles per CTA
+constexpr size_t kT2Smem = (size_t)kT2Cap * 512 + kTcMaxTiles * 8 * sizeof(double) +
+                           kTcMaxTiles * 8 * sizeof(double2) + 440;
+
+__device__ __forceinline__ int t2_gcol(int kt, int T0) { return kt * T0 - ((kt * (kt - 1)) >> 1); }
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+
+// Plan record of tile shape (T, T1): slot table, free list, peak (host-written).
+__host__ __device__ inline int t2_rec_index(int T, int T1) { return T * (kT2MaxT1 + 1) + T1; }
+constexpr int kT2Recs = (kTcMaxTiles + 1) * (kT2MaxT1 + 1);
+
+// acc[m] += sum_{kt < j} L(it0 + kT2Acc m, kt) L(j+1, kt)^T for m < NM (one chain per row;
+// the B fragments of row j+1 are shared by the NM rows)
+template <int NM>
+__device__ __forceinline__ void t2_acc_rows(double (&acc)[kT2M][2], const double *sm, const unsigned char *slot,
+                                            int j, int it0, int f0, int f1) {
+  const unsigned char *sj = slot + (((j + 1) * (j + 2)) >> 1);
+  const unsigned char *si[NM];
+#pragma unroll
+  for (int m = 0; m < NM; ++m) {
+    const int it = it0 + kT2Acc * m;
+    si[m] = slot + ((it * (it + 1)) >> 1);
+  }
+#pragma unroll 2
+  for (int kt = 0; kt < j; ++kt) {
+    const double *Bt = sm + (int)sj[kt] * 64;
+    const double *At[NM];
+#pragma unroll
+    for (int m = 0; m < NM; ++m) At[m] = sm + (int)si[m][kt] * 64;
+    const double b0 = Bt[f0], b1 = Bt[f1];
+    double a0[NM], a1[NM];
+#pragma unroll
+    for (int m = 0; m < NM; ++m) {
+      a0[m] = At[m][f0];
+      a1[m] = At[m][f1];
+    }
+#pragma unroll
+    for (int m = 0; m < NM; ++m) dmma(acc[m][0], acc[m][1], a0[m], b0);
+#pragma unroll
+    for (int m = 0; m < NM; ++m) dmma(acc[m][0], acc[m][1], a1[m], b1);
+  }
+}
+
+__global__ __launch_bounds__(kT2Threads, 2) void k_rasm_setup_tc2(
+    Geom g, Strip st, const double2 *__restrict__ xy, const int *__restrict__ cell_start,
+    const long long *__restrict__ x_off, double *__restrict__ X, int *__restrict__ counts,
+    int *__restrict__ glist, OvList ov, const unsigned char *__restrict__ plans, double *__restrict__ ws,
+    int *__restrict__ work, int *__restrict__ deferred, int ncl) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ Runs R;
+  __shared__ int s_cl, s_fail;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double *rdiag = sm + kT2Cap * 64;
+  double2 *pos = reinterpret_cast<double2 *>(rdiag + kTcMaxTiles * 8);
+  unsigned char *slot = reinterpret_cast<unsigned char *>(pos + kTcMaxTiles * 8);
+  double *wsl = ws + (size_t)blockIdx.x * kT2WsTiles * 64;
+  const int f0 = frag_rowk(lane, 0), f1 = frag_rowk(lane, 1);
+#ifdef RBF_PROBE
+  long long t2_last = 0;
+  int t2_cellno = 0;
+#endif
+  for (;;) {
+    __syncthreads();  // the previous cell is done with R and the shared tiles
+    T2P(0)
+    if (tid == 0) {
+      const int cl = atomicAdd(work, 1);
+      s_cl = cl;
+      s_fail = 0;
+      if (cl < ncl) sub_runs(g, cell_start, ov, cl, cl % g.ncx, st.row_lo + cl / g.ncx, R);
+    }
+    __syncthreads();
+    const int cl = s_cl;
+    if (cl >= ncl) return;
+    if (R.n_own == 0) continue;
+    const TileShape S(R.n_ov, R.n_own);
+    if (!S.fits_tc()) continue;  // handled by k_rasm_setup_lu
+    const unsigned char *plan = plans + (size_t)t2_rec_index(S.T, S.T1 <= kT2MaxT1 ? S.T1 : 0) * kT2Rec;
+    const int *pint = reinterpret_cast<const int *>(plan + kT2RecPeak);
+    if (S.T1 > kT2MaxT1 || pint[0] > kT2Cap || pint[1] < 3 * S.T0 + 4) {
+      if (tid == 0) deferred[atomicAdd(work + 1, 1)] = cl;  // left to k_rasm_setup_tc
+      continue;
+    }
+    const int T = S.T, N = S.N, T0 = S.T0, T1 = S.T1;
+    const int ntix = T * (T + 1) / 2;
+    for (int i = tid; i < (ntix + 3) / 4; i += kT2Threads)
+      reinterpret_cast<unsigned *>(slot)[i] = __ldg(reinterpret_cast<const unsigned *>(plan) + i);
+    for (int p = tid; p < N; p += kT2Threads) {
+      const int gi = fac_to_global(R, S, p);
+      pos[p] = (gi >= 0) ? xy[gi - st.ext_lo] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    T2P(1)
+#ifdef RBF_PROBE
+    if (tid == 0) g_t2_acc[blockIdx.x][0] += 1;
+    ++t2_cellno;
+#endif
+    auto tile = [&](int it, int jt) -> double * { return sm + (int)slot[((it * (it + 1)) >> 1) + jt] * 64; };
+
+    // ---- left-looking Cholesky over tile columns (as k_rasm_setup_tc), rows retired
+    // to the workspace.  Accumulate warp w handles the rows j+1+w+kT2Acc m of column j;
+    // with one row only, it runs two DMMA chains (even / odd kt) for it.
+    double acc[kT2M][2], accb[2];
+#pragma unroll
+    for (int m = 0; m < kT2M; ++m) acc[m][0] = acc[m][1] = 0.0;
+    accb[0] = accb[1] = 0.0;
+    // the A entries of column 0's tiles (accumulators start at -A: C = -acc at the end)
+    if (warp < kT2Acc) {
+#pragma unroll
+      for (int m = 0; m < kT2M; ++m) {
+        const int it = 1 + warp + kT2Acc * m;
+        if (it < T) {
+          double v0, v1;
+          a_entries(pos, S, g, it, 0, lane, v0, v1);
+          acc[m][0] = -v0;
+          acc[m][1] = -v1;
+        }
+      }
+    } else if (warp == kT2Acc) {
+      double v0, v1;
+      a_entries(pos, S, g, 0, 0, lane, v0, v1);
+      acc[0][0] = -v0;
+      acc[0][1] = -v1;
+    }
+    for (int j = 0; j < T; ++j) {
+      const int dw = kT2Acc + (j & 1);
+      if (warp == 0) T2C(0)
+      if (warp < kT2Acc) {
+        // rows of column j (step 1) = rows of column j+1's accumulation (step 2) shifted
+        const int nm1 = (T - (j + 1) - warp + kT2Acc - 1) / kT2Acc;  // it = j+1+warp+kT2Acc m < T
+        const int nm2 = (T - (j + 2) - warp + kT2Acc - 1) / kT2Acc;
+        // step 1: finish column j with the kt = j-1 term, store C = A - sum
+        if (nm1 > 0) {
+          const double *Bt = j >= 1 ? tile(j, j - 1) : sm;
+          const double b0 = Bt[f0], b1 = Bt[f1];
+#pragma unroll
+          for (int m = 0; m < kT2M; ++m)
+            if (m < nm1) {
+              const int it = j + 1 + warp + kT2Acc * m;
+              if (j >= 1) {
+                const double *At = tile(it, j - 1);
+                dmma(acc[m][0], acc[m][1], At[f0], b0);
+                dmma(acc[m][0], acc[m][1], At[f1], b1);
+              }
+              double c0 = acc[m][0], c1 = acc[m][1];
+              if (m == 0 && nm1 == 1) {
+                c0 += accb[0];
+                c1 += accb[1];
+              }
+              *reinterpret_cast<double2 *>(tile(it, j) + frag_acc(lane)) = make_double2(-c0, -c1);
+            }
+        }
+        if (warp == 0) T2C(1)
+        // step 2: accumulate column j+1 (rows it > j+1) over kt < j
+        accb[0] = accb[1] = 0.0;
+        if (nm2 > 0) {
+#pragma unroll
+          for (int m = 0; m < kT2M; ++m)
+            if (m < nm2) {
+              double v0, v1;
+              a_entries(pos, S, g, j + 2 + warp + kT2Acc * m, j + 1, lane, v0, v1);
+              acc[m][0] = -v0;
+              acc[m][1] = -v1;
+            }
+          const unsigned char *sj = slot + (((j + 1) * (j + 2)) >> 1);
+          if (nm2 == 1) {
+            const int it = j + 2 + warp;
+            const unsigned char *si = slot + ((it * (it + 1)) >> 1);
+            int kt = 0;
+            for (; kt + 1 < j; kt += 2) {
+              const double *B0 = sm + (int)sj[kt] * 64, *B1 = sm + (int)sj[kt + 1] * 64;
+              const double *A0 = sm + (int)si[kt] * 64, *A1 = sm + (int)si[kt + 1] * 64;
+              dmma(acc[0][0], acc[0][1], A0[f0], B0[f0]);
+              dmma(accb[0], accb[1], A1[f0], B1[f0]);
+              dmma(acc[0][0], acc[0][1], A0[f1], B0[f1]);
+              dmma(accb[0], accb[1], A1[f1], B1[f1]);
+            }
+            if (kt < j) {
+              const double *B0 = sm + (int)sj[kt] * 64, *A0 = sm + (int)si[kt] * 64;
+              dmma(acc[0][0], acc[0][1], A0[f0], B0[f0]);
+              dmma(acc[0][0], acc[0][1], A0[f1], B0[f1]);
+            }
+          } else {
+            switch (nm2) {  // straight-line code per tile count (no per-tile branches)
+              case 2: t2_acc_rows<2>(acc, sm, slot, j, j + 2 + warp, f0, f1); break;
+              case 3: t2_acc_rows<3>(acc, sm, slot, j, j + 2 + warp, f0, f1); break;
+              case 4: t2_acc_rows<4>(acc, sm, slot, j, j + 2 + warp, f0, f1); break;
+              default: t2_acc_rows<kT2M>(acc, sm, slot, j, j + 2 + warp, f0, f1); break;
+            }
+          }
+        }
+      } else if (warp == dw) {
+        // finish the diagonal tile (its sum over kt < j-1 was accumulated last column)
+        double *D = tile(j, j);
+        if (j >= 1) {
+          const double *Lt = tile(j, j - 1);
+          const double l0 = Lt[f0], l1 = Lt[f1];
+          dmma(acc[0][0], acc[0][1], l0, l0);
+          dmma(accb[0], accb[1], l1, l1);
+        }
+        *reinterpret_cast<double2 *>(D + frag_acc(lane)) =
+            make_double2(-(acc[0][0] + accb[0]), -(acc[0][1] + accb[1]));
+        __syncwarp();
+        T2C(5)
+        if (diag_factor_t(D, rdiag, j, lane) && lane == 0) s_fail = 1;
+        T2C(6)
+      } else if (j + 1 < T) {
+        // the other diagonal warp accumulates the next diagonal tile over kt < j
+        double v0, v1;
+        a_entries(pos, S, g, j + 1, j + 1, lane, v0, v1);
+        acc[0][0] = -v0;
+        acc[0][1] = -v1;
+        accb[0] = accb[1] = 0.0;
+        const unsigned char *sj = slot + (((j + 1) * (j + 2)) >> 1);
+        int kt = 0;
+        for (; kt + 1 < j; kt += 2) {
+          const double *L0 = sm + (int)sj[kt] * 64, *L1 = sm + (int)sj[kt + 1] * 64;
+          const double x0 = L0[f0], x1 = L0[f1], y0 = L1[f0], y1 = L1[f1];
+          dmma(acc[0][0], acc[0][1], x0, x0);
+          dmma(accb[0], accb[1], y0, y0);
+          dmma(acc[0][0], acc[0][1], x1, x1);
+          dmma(accb[0], accb[1], y1, y1);
+        }
+        if (kt < j) {
+          const double *L0 = sm + (int)sj[kt] * 64;
+          const double x0 = L0[f0], x1 = L0[f1];
+          dmma(acc[0][0], acc[0][1], x0, x0);
+          dmma(acc[0][0], acc[0][1], x1, x1);
+        }
+      }
+      if (warp == 0) T2C(2)
+      __syncthreads();
+      if (warp == 0) T2C(3)
+      if (s_fail) break;  // uniform
+      if (warp < kT2Acc) {
+        // panel L(it, j) = C(it, j) L_d^-T
+        const int nm1 = (T - (j + 1) - warp + kT2Acc - 1) / kT2Acc;
+        if (nm1 > 0) {
+          const double *D = tile(j, j);
+          double bv[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int k = 4 * h + (lane & 3), n = lane >> 2;
+            bv[h] = (n > k) ? D[swz(k, n)] : (n == k ? rdiag[j * 8 + k] : 0.0);
+          }
+#pragma unroll
+          for (int m = 0; m < kT2M; ++m)
+            if (m < nm1) {
+              double *Ct = tile(j + 1 + warp + kT2Acc * m, j);
+              double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+              for (int h = 0; h < 2; ++h) dmma(d0, d1, Ct[frag_rowk(lane, h)], bv[h]);
+              __syncwarp();
+              *reinterpret_cast<double2 *>(Ct + frag_acc(lane)) = make_double2(d0, d1);
+            }
+        }
+      } else {
+        // retire the rows the loop is done with (rows of L11 only): row j+1's tiles
+        // (j+1, kt < j) and row j's last two, (j, j-1) and (j, j); their slots are
+        // reused from the next column on (the plan frees them here)
+        const int t = tid - kT2Acc * 32;
+        const int na = (j + 1 < T0) ? j : 0;
+        const int nb = (j < T0) ? (j >= 1 ? 2 : 1) : 0;
+        for (int q = t; q < (na + nb) * 32; q += 64) {
+          const int e = q >> 5, p = q & 31;
+          int it, kt;
+          if (e < na) {
+            it = j + 1;
+            kt = e;
+          } else {
+            it = j;
+            kt = (e - na == nb - 1) ? j : j - 1;
+          }
+          const double2 v = *reinterpret_cast<const double2 *>(tile(it, kt) + 2 * p);
+          __stcg(reinterpret_cast<double2 *>(wsl + (size_t)(t2_gcol(kt, T0) + it - kt) * 64 + 2 * p), v);
+        }
+      }
+      if (warp == 0) T2C(4)
+      __syncthreads();
+    }
+    if (s_fail) {  // Cholesky broke down: redo this cell with LU (reading Q11)
+      if (tid == 0) glist[atomicAdd(&counts[3], 1)] = cl;
+      continue;
+    }
+
+    T2P(2)
+#ifdef RBF_PROBE
+    const long long t2_post0 = clock64();
+#endif
+    // ---- W = L21 L11^-1 (warps 0..3, one own tile row each) and S^-1 (warps 4..7)
+    const unsigned char *fl = plan + kT2RecFree;  // slots free after the factorisation
+    if (warp < 4) {
+      // W(r, jt) = (C(r, jt) - sum_{kt > jt} W(r, kt) L(kt, jt)) L_d(jt)^-1, jt = T0-1 .. 0;
+      // column jt of L11 (tiles (jt..T0-1, jt), contiguous in the workspace) in ring buffer jt % 3
+      // lane e holds the slot of tile e of each ring buffer (column jt of L11 is buffer
+      // jt % 3, its tile e = row jt + e) and the slot of this warp's W(r, e)
+      const int r = warp;
+      int flr[3] = {0, 0, 0};
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        if (lane < T0) flr[b] = __ldg(fl + b * T0 + lane);
+      const int wslot = (r < T1 && lane < T0) ? (int)slot[(((T0 + r) * (T0 + r + 1)) >> 1) + lane] : 0;
+      auto fetch = [&](int jt) {
+        const int nt = T0 - jt, b = jt % 3;
+        const int fb = b == 0 ? flr[0] : (b == 1 ? flr[1] : flr[2]);
+        const double *src = wsl + (size_t)t2_gcol(jt, T0) * 64;
+        for (int e = warp; e < nt; e += 4) {  // one tile per warp and pass
+          const int sl = __shfl_sync(0xffffffffu, fb, e);
+          cp_async16(sm + sl * 64 + 2 * lane, src + e * 64 + 2 * lane);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+      };
+      if (T0 >= 1) fetch(T0 - 1);
+      if (T0 >= 2) fetch(T0 - 2);
+      for (int jt = T0 - 1; jt >= 0; --jt) {
+        if (warp == 0) T2W(0)
+        if (jt >= 1) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        if (warp == 0) T2W(1)
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (warp == 0) T2W(2)
+        if (jt >= 2) fetch(jt - 2);
+        if (warp == 0) T2W(3)
+        if (r < T1) {
+          const int b = jt % 3;
+          const int fb = b == 0 ? flr[0] : (b == 1 ? flr[1] : flr[2]);
+          double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0;
+          int kt = jt + 1;
+#pragma unroll 2
+          for (; kt + 1 < T0; kt += 2) {
+            const double *W0 = sm + __shfl_sync(0xffffffffu, wslot, kt) * 64;
+            const double *W1 = sm + __shfl_sync(0xffffffffu, wslot, kt + 1) * 64;
+            const double *L0 = sm + __shfl_sync(0xffffffffu, fb, kt - jt) * 64;
+            const double *L1 = sm + __shfl_sync(0xffffffffu, fb, kt + 1 - jt) * 64;
+            dmma(a0, a1, W0[f0], L0[frag_colk(lane, 0)]);
+            dmma(c0, c1, W1[f0], L1[frag_colk(lane, 0)]);
+            dmma(a0, a1, W0[f1], L0[frag_colk(lane, 1)]);
+            dmma(c0, c1, W1[f1], L1[frag_colk(lane, 1)]);
+          }
+          if (kt < T0) {
+            const double *W0 = sm + __shfl_sync(0xffffffffu, wslot, kt) * 64;
+            const double *L0 = sm + __shfl_sync(0xffffffffu, fb, kt - jt) * 64;
+            dmma(a0, a1, W0[f0], L0[frag_colk(lane, 0)]);
+            dmma(a0, a1, W0[f1], L0[frag_colk(lane, 1)]);
+          }
+          if (warp == 0) T2W(4)
+          double *Ct = sm + __shfl_sync(0xffffffffu, wslot, jt) * 64;
+          double2 *cp = reinterpret_cast<double2 *>(Ct + frag_acc(lane));
+          double2 cv = *cp;
+          cv.x -= a0 + c0;
+          cv.y -= a1 + c1;
+          *cp = cv;
+          __syncwarp();
+          const double *D = sm + __shfl_sync(0xffffffffu, fb, 0) * 64;  // diagonal tile (jt, jt)
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int k = 4 * h + (lane & 3), n = lane >> 2;
+            const double bv = (k > n) ? D[swz(n, k)] : (k == n ? rdiag[jt * 8 + k] : 0.0);
+            dmma(d0, d1, Ct[frag_rowk(lane, h)], bv);
+          }
+          __syncwarp();
+          *cp = make_double2(d0, d1);
+          __syncwarp();
+          if (warp == 0) T2W(5)
+        }
+      }
+#ifdef RBF_PROBE
+      if (tid == 0) g_t2_acc[blockIdx.x][5] += clock64() - t2_post0;
+#endif
+    } else {
+      // S^-1 = L22^-T L22^-1 (as setup_post): M = L22^-1 by columns, one warp per column
+      const int sw = warp - 4;
+      double *Mt = reinterpret_cast<double *>(pos);
+      double *scr = sm + (int)__ldg(fl + 3 * T0 + sw) * 64;
+      auto mt = [&](int a, int b) { return Mt + ((a * (a - 1)) / 2 + b) * 64; };  // a > b only
+      const int m_ = lane >> 2, q_ = lane & 3;
+      auto linvA = [&](int a, int h) -> double {
+        const double *D = tile(T0 + a, T0 + a);
+        const int kk = 4 * h + q_;
+        return (m_ > kk) ? D[swz(kk, m_)] : (m_ == kk ? rdiag[(T0 + a) * 8 + m_] : 0.0);
+      };
+      auto linvB = [&](int a, int h) -> double {
+        const double *D = tile(T0 + a, T0 + a);
+        const int kk = 4 * h + q_;
+        return (kk > m_) ? D[swz(m_, kk)] : (kk == m_ ? rdiag[(T0 + a) * 8 + kk] : 0.0);
+      };
+      auto linvT = [&](int a, int h) -> double {
+        const double *D = tile(T0 + a, T0 + a);
+        const int kk = 4 * h + q_;
+        return (kk > m_) ? D[swz(m_, kk)] : (kk == m_ ? rdiag[(T0 + a) * 8 + m_] : 0.0);
+      };
+      for (int b = sw; b < T1 - 1; b += 4) {
+        for (int a = b + 1; a < T1; ++a) {
+          double d0 = 0.0, d1 = 0.0;
+          for (int k = b; k < a; ++k) {
+            const double *La = tile(T0 + a, T0 + k);
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              dmma(d0, d1, La[frag_rowk(lane, h)], k == b ? linvB(b, h) : mt(k, b)[frag_colk(lane, h)]);
+          }
+          *reinterpret_cast<double2 *>(scr + frag_acc(lane)) = make_double2(d0, d1);
+          __syncwarp();
+          double e0 = 0.0, e1 = 0.0;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) dmma(e0, e1, linvA(a, h), scr[frag_colk(lane, h)]);
+          __syncwarp();
+          *reinterpret_cast<double2 *>(mt(a, b) + frag_acc(lane)) = make_double2(-e0, -e1);
+          __syncwarp();
+        }
+      }
+      asm volatile("bar.sync 2, 128;" ::: "memory");  // M complete
+      constexpr int kSlots = (kT2MaxT1 * (kT2MaxT1 + 1) / 2 + 3) / 4;
+      double res[kSlots][2];
+      const int ntl = T1 * (T1 + 1) / 2;
+#pragma unroll
+      for (int sl = 0; sl < kSlots; ++sl) {
+        const int t = sw + sl * 4;
+        res[sl][0] = res[sl][1] = 0.0;
+        if (t < ntl) {
+          int a = 0;
+          while ((a + 1) * (a + 2) / 2 <= t) ++a;
+          const int bb = t - a * (a + 1) / 2;
+          for (int k = a; k < T1; ++k) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const double av = (k == a) ? linvT(a, h) : mt(k, a)[frag_colk(lane, h)];
+              const double bv = (k == bb) ? linvB(bb, h) : mt(k, bb)[frag_colk(lane, h)];
+              dmma(res[sl][0], res[sl][1], av, bv);
+            }
+          }
+        }
+      }
+      asm volatile("bar.sync 2, 128;" ::: "memory");  // L^-1 scratch read
+#pragma unroll
+      for (int sl = 0; sl < kSlots; ++sl) {
+        const int t = sw + sl * 4;
+        if (t < ntl) {
+          int a = 0;
+          while ((a + 1) * (a + 2) / 2 <= t) ++a;
+          const int bb = t - a * (a + 1) / 2;
+          *reinterpret_cast<double2 *>(tile(T0 + a, T0 + bb) + frag_acc(lane)) =
+              make_double2(res[sl][0], res[sl][1]);
+        }
+      }
+#ifdef RBF_PROBE
+      if (tid == 128) g_t2_acc[blockIdx.x][6] += clock64() - t2_post0;
+#endif
+    }
+    __syncthreads();
+    T2P(3)
+
+    // ---- X_c = S^-1 [-W, I] in natural column order (ld = n rounded up to even), to HBM
+    const int n = S.n;
+    const int ld = (n + 1) & ~1;
+    double *Xc = X + x_off[cl];
+    auto x_store = [&](int ot, int jt, double d0, double d1) {
+      const int o = ot * 8 + (lane >> 2);
+      const int p0 = jt * 8 + 2 * (lane & 3);
+      if (o < S.n1) {
+        if (p0 < S.n0) Xc[(size_t)o * ld + (p0 < R.own_nat_lo ? p0 : p0 + S.n1)] = -d0;
+        if (p0 + 1 < S.n0) Xc[(size_t)o * ld + (p0 + 1 < R.own_nat_lo ? p0 + 1 : p0 + 1 + S.n1)] = -d1;
+      }
+    };
+    auto sinv_frag = [&](int ot, int kt, int h) -> double {
+      const bool lower = kt <= ot;
+      const double *At = lower ? tile(T0 + ot, T0 + kt) : tile(T0 + kt, T0 + ot);
+      const int m = lane >> 2, k = 4 * h + (lane & 3);
+      return lower ? At[swz(m, k)] : At[swz(k, m)];
+    };
+    for (int task = warp; task < T1 * T0; task += kT2Warps) {
+      const int ot = task / T0, jt = task - ot * T0;
+      double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+      for (int kt = 0; kt < T1; ++kt) {
+        const double *Bt = tile(T0 + kt, jt);
+        if (kt & 1) {
+          dmma(e0, e1, sinv_frag(ot, kt, 0), Bt[frag_colk(lane, 0)]);
+          dmma(e0, e1, sinv_frag(ot, kt, 1), Bt[frag_colk(lane, 1)]);
+        } else {
+          dmma(d0, d1, sinv_frag(ot, kt, 0), Bt[frag_colk(lane, 0)]);
+          dmma(d0, d1, sinv_frag(ot, kt, 1), Bt[frag_colk(lane, 1)]);
+        }
+      }
+      x_store(ot, jt, d0 + e0, d1 + e1);
+    }
+    for (int t = tid; t < S.n1 * S.n1; t += kT2Threads) {
+      const int o = t / S.n1, jj = t - o * S.n1;
+      const int i1 = o >= jj ? o : jj, j1 = o >= jj ? jj : o;
+      Xc[(size_t)o * ld + R.own_nat_lo + jj] = tile(T0 + (i1 >> 3), T0 + (j1 >> 3))[swz(i1 & 7, j1 & 7)];
+    }
+    if (ld != n)
+      for (int o = tid; o < S.n1; o += kT2Threads) Xc[(size_t)o * ld + n] = 0.0;
+    T2P(4)
+  }
 }
 
 // Global-memory local solve for subdomains whose factor does not fit in shared
@@ -1499,6 +2060,9 @@ int probe_read(long long *out) {
   RBF_CUDA_TRY(cudaMemcpyFromSymbol(out + 64 * 8 + 65536 * 3, g_col, sizeof(long long) * 512));
   RBF_CUDA_TRY(cudaMemcpyFromSymbol(out + 64 * 8 + 65536 * 3 + 512, g_wcol, sizeof(long long) * 128));
   RBF_CUDA_TRY(cudaMemcpyFromSymbol(out + 64 * 8 + 65536 * 3 + 512 + 128, g_lu_acc, sizeof(long long) * 512 * 10));
+  RBF_CUDA_TRY(cudaMemcpyFromSymbol(out + 64 * 8 + 65536 * 3 + 512 + 128 + 5120, g_t2_acc, sizeof(long long) * 512 * 8));
+  RBF_CUDA_TRY(cudaMemcpyFromSymbol(out + 64 * 8 + 65536 * 3 + 512 + 128 + 5120 + 4096, g_t2_col, sizeof(long long) * 256));
+  RBF_CUDA_TRY(cudaMemcpyFromSymbol(out + 64 * 8 + 65536 * 3 + 512 + 128 + 5120 + 4096 + 256, g_t2_w, sizeof(long long) * 256));
   return RBF_OK;
 #else
   (void)out;
@@ -1537,6 +2101,60 @@ static int build_ov_lists(rbf_ctx *c, int ncl, cudaStream_t s) {
                                        c->ov_idx, c->ov_own);
   count_launch(3);  // count, scan, fill
   RBF_CUDA_TRY(cudaGetLastError());
+  return RBF_OK;
+}
+
+// Slot plans of k_rasm_setup_tc2 for every tile shape (T <= 29, T1 <= 4): the order in
+// which the column loop forms tiles (column j: (j..T-1, j)) and retires them (in column
+// j's panel step: row j+1's tiles (j+1, kt < j) and row j's (j, j-1), (j, j), rows of
+// L11 only), each new tile taking the lowest free slot.  Uploaded once per device.
+static void t2_plan(int T, int T1, unsigned char *rec) {
+  std::memset(rec, 0, kT2Rec);
+  if (T1 > T) return;
+  const int T0 = T - T1;
+  std::vector<int> slot(T * (T + 1) / 2, 0);
+  std::vector<char> used(512, 0);
+  int peak = 0;
+  auto tix = [](int it, int jt) { return it * (it + 1) / 2 + jt; };
+  for (int j = 0; j < T; ++j) {
+    for (int it = j; it < T; ++it) {
+      int sl = 0;
+      while (used[sl]) ++sl;
+      used[sl] = 1;
+      slot[tix(it, j)] = sl;
+      peak = std::max(peak, sl + 1);
+    }
+    if (j + 1 < T0)
+      for (int kt = 0; kt < j; ++kt) used[slot[tix(j + 1, kt)]] = 0;
+    if (j < T0) {
+      if (j >= 1) used[slot[tix(j, j - 1)]] = 0;
+      used[slot[tix(j, j)]] = 0;
+    }
+  }
+  for (size_t i = 0; i < slot.size(); ++i) rec[i] = (unsigned char)std::min(slot[i], 255);
+  int nfree = 0;
+  for (int sl = 0; sl < kT2Cap; ++sl)
+    if (!used[sl]) rec[kT2RecFree + nfree++] = (unsigned char)sl;
+  int *pi = reinterpret_cast<int *>(rec + kT2RecPeak);
+  pi[0] = peak;
+  pi[1] = nfree;
+}
+
+static int t2_plans(const unsigned char **out) {
+  static std::mutex mu;
+  static std::map<int, unsigned char *> per_dev;
+  int dev = 0;
+  RBF_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  unsigned char *&d = per_dev[dev];
+  if (!d) {
+    std::vector<unsigned char> h((size_t)kT2Recs * kT2Rec);
+    for (int T = 1; T <= kTcMaxTiles; ++T)
+      for (int T1 = 1; T1 <= kT2MaxT1; ++T1) t2_plan(T, T1, h.data() + (size_t)t2_rec_index(T, T1) * kT2Rec);
+    RBF_CUDA_TRY(cudaMalloc((void **)&d, h.size()));
+    RBF_CUDA_TRY(cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice));
+  }
+  *out = d;
   return RBF_OK;
 }
 
@@ -1589,15 +2207,60 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
   RBF_TRY(dalloc(c, (void **)&c->X, sizeof(double) * (size_t)(total > 0 ? total : 2), s));
   if (ncl > 0 && c->nsub > hc[3]) {
     const size_t smem = (size_t)hc[4];  // the largest per-cell layout of the tensor-core cells
-    RBF_TRY(ensure_dyn_smem((const void *)k_rasm_setup_tc, smem));
-    k_rasm_setup_tc<<<ncl, kTcThreads, smem, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off,
-                                                  c->X, cnt, glist, ov);
-    count_launch(1);
-    RBF_CUDA_TRY(cudaGetLastError());
-    // host work while the kernel runs: GMRES workspace and the solve graph (krylov.cu)
-    RBF_TRY(prebuild_solve(c, s));
-    RBF_CUDA_TRY(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
-    RBF_CUDA_TRY(cudaStreamSynchronize(s));
+    if (opt(OPT_SETUP_TC2)) {
+      // two factorisations per SM; the cells it cannot take (n_own > 32) are listed for
+      // the one-per-SM kernel
+      const unsigned char *plans = nullptr;
+      RBF_TRY(t2_plans(&plans));
+      int dev = 0, sms = 148, occ = 0;
+      RBF_CUDA_TRY(cudaGetDevice(&dev));
+      RBF_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      RBF_TRY(ensure_dyn_smem((const void *)k_rasm_setup_tc2, kT2Smem));
+      RBF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rasm_setup_tc2, kT2Threads, kT2Smem));
+      const int grid = std::max(1, std::min(ncl, std::max(occ, 1) * sms));
+#ifdef RBF_PROBE
+      fprintf(stderr, "[probe] k_rasm_setup_tc2: %d CTAs per SM, grid %d, %zu B dynamic shared memory\n", occ, grid,
+              kT2Smem);
+      {
+        static long long zero[512 * 8];
+        RBF_CUDA_TRY(cudaMemcpyToSymbolAsync(g_t2_acc, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, s));
+      }
+#endif
+      double *ws2 = nullptr;
+      int *w2 = nullptr;
+      RBF_TRY(dalloc(c, (void **)&ws2, sizeof(double) * 64 * (size_t)kT2WsTiles * grid, s));
+      RBF_TRY(dalloc(c, (void **)&w2, sizeof(int) * (2 + (size_t)ncl), s));
+      RBF_CUDA_TRY(cudaMemsetAsync(w2, 0, 2 * sizeof(int), s));
+      k_rasm_setup_tc2<<<grid, kT2Threads, kT2Smem, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off, c->X,
+                                                          cnt, glist, ov, plans, ws2, w2, w2 + 2, ncl);
+      count_launch(1);
+      RBF_CUDA_TRY(cudaGetLastError());
+      RBF_TRY(prebuild_solve(c, s));  // host work while the kernel runs (krylov.cu)
+      int nd = 0;
+      RBF_CUDA_TRY(cudaMemcpyAsync(&nd, w2 + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+      RBF_CUDA_TRY(cudaStreamSynchronize(s));
+      if (nd > 0) {
+        RBF_TRY(ensure_dyn_smem((const void *)k_rasm_setup_tc, smem));
+        k_rasm_setup_tc<<<nd, kTcThreads, smem, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off, c->X, cnt,
+                                                     glist, ov, w2 + 2);
+        count_launch(1);
+        RBF_CUDA_TRY(cudaGetLastError());
+      }
+      RBF_CUDA_TRY(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
+      RBF_CUDA_TRY(cudaStreamSynchronize(s));
+      dfree(w2, s);
+      dfree(ws2, s);
+    } else {
+      RBF_TRY(ensure_dyn_smem((const void *)k_rasm_setup_tc, smem));
+      k_rasm_setup_tc<<<ncl, kTcThreads, smem, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off,
+                                                    c->X, cnt, glist, ov, nullptr);
+      count_launch(1);
+      RBF_CUDA_TRY(cudaGetLastError());
+      // host work while the kernel runs: GMRES workspace and the solve graph (krylov.cu)
+      RBF_TRY(prebuild_solve(c, s));
+      RBF_CUDA_TRY(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
+      RBF_CUDA_TRY(cudaStreamSynchronize(s));
+    }
   }
   const int nglobal = hc[3];  // big cells + Cholesky breakdowns (ASM: every cell)
   if (ncl > 0 && c->nsub == nglobal) RBF_TRY(prebuild_solve(c, s));  // no tensor-core pass

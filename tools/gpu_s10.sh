@@ -1,0 +1,1 @@
+TC2=1 timeout 300 python tools/probe_setup.py 2 2>&1 | grep -v "^\[probe\]\|^{" | grep -A40 "W phase"

@@ -14,6 +14,7 @@ R.LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "probe", o
 L = R.lib()
 L.rbf_debug_probe.argtypes = [C.c_void_p]
 L.rbf_debug_probe.restype = C.c_int
+R.set_option("setup_tc2", int(os.environ.get("TC2", "1")))
 wl = W.config(int(sys.argv[1]) if len(sys.argv) > 1 else 2)
 xy = torch.from_numpy(wl.xy).cuda()
 for _ in range(2):
@@ -21,8 +22,32 @@ for _ in range(2):
     torch.cuda.synchronize()
     print(c.setup_times())
     c.close()
-buf = np.zeros(64 * 8 + 65536 * 3 + 512 + 128, dtype=np.int64)
+buf = np.zeros(64 * 8 + 65536 * 3 + 512 + 128 + 5120 + 4096 + 512, dtype=np.int64)
 assert L.rbf_debug_probe(buf.ctypes.data_as(C.c_void_p)) == 0
+t2 = buf[512 + 65536 * 3 + 512 + 128 + 5120:512 + 65536 * 3 + 512 + 128 + 5120 + 4096].reshape(512, 8)
+t2c = buf[512 + 65536 * 3 + 512 + 128 + 5120 + 4096:512 + 65536 * 3 + 512 + 128 + 5120 + 4096 + 256].reshape(32, 8)
+t2w = buf[512 + 65536 * 3 + 512 + 128 + 5120 + 4096 + 256:].reshape(32, 8)
+if t2[:, 0].sum() > 0:
+    sel = t2[:, 0] > 0
+    cells = t2[sel, 0].sum()
+    print(f"tc2: {sel.sum()} CTAs, {cells} cells; per cell (cycles of one CTA): runs+pos {t2[sel, 1].sum() / cells:.0f}, "
+          f"cholesky {t2[sel, 2].sum() / cells:.0f}, W+Sinv {t2[sel, 3].sum() / cells:.0f} (W warps {t2[sel, 5].sum() / cells:.0f}, "
+          f"Sinv warps {t2[sel, 6].sum() / cells:.0f}), X {t2[sel, 4].sum() / cells:.0f}")
+    print("per column (one interior cell, CTA 7): w0 step1, step2, wait b1, panel(w0), b2 wait(w0) | dw finish->factor start, factor | column")
+    for j in range(32):
+        c_ = t2c[j]
+        if c_[0] == 0:
+            continue
+        print(f"{j:2d}: {c_[1]-c_[0]:6d} {c_[2]-c_[1]:6d} {c_[3]-c_[2]:6d} {c_[4]-c_[3]:6d} | {c_[5]-c_[0]:6d} {c_[6]-c_[5]:6d} | "
+              f"{(t2c[j + 1][0] - c_[0]) if j + 1 < 32 and t2c[j + 1][0] else 0:6d}")
+    print("W phase per step jt (warp 0): wait_group, bar.sync, fetch issue, dot product, finish, to next step")
+    for jt in range(31, -1, -1):
+        c_ = t2w[jt]
+        if c_[0] == 0:
+            continue
+        nxt = t2w[jt - 1][0] if jt >= 1 and t2w[jt - 1][0] else c_[5]
+        print(f"{jt:2d}: {c_[1]-c_[0]:6d} {c_[2]-c_[1]:6d} {c_[3]-c_[2]:6d} {c_[4]-c_[3]:6d} {c_[5]-c_[4]:6d} {nxt-c_[5]:6d}")
+    sys.exit(0)
 out = buf[:512].reshape(64, 8)
 tr = buf[512:512 + 65536 * 3].reshape(65536, 3)[:42025]
 dur = (tr[:, 2] - tr[:, 1]) / 1e3
@@ -54,7 +79,16 @@ for j in range(30):
         break
     print(f"{j:2d} w0: {c0[j, 1] - c0[j, 0]:6d} {c0[j, 2] - c0[j, 1]:6d} {c0[j, 3] - c0[j, 2]:6d} | "
           f"dw: {cd[j, 1] - cd[j, 0]:6d} {cd[j, 2] - cd[j, 1]:6d} | col {c0[j, 3] - c0[j, 0]:6d}")
-wc = buf[512 + 65536 * 3 + 512:].reshape(32, 4)
+wc = buf[512 + 65536 * 3 + 512:512 + 65536 * 3 + 512 + 128].reshape(32, 4)
+t2 = buf[512 + 65536 * 3 + 512 + 128 + 5120:512 + 65536 * 3 + 512 + 128 + 5120 + 4096].reshape(512, 8)
+t2c = buf[512 + 65536 * 3 + 512 + 128 + 5120 + 4096:512 + 65536 * 3 + 512 + 128 + 5120 + 4096 + 256].reshape(32, 8)
+t2w = buf[512 + 65536 * 3 + 512 + 128 + 5120 + 4096 + 256:].reshape(32, 8)
+if t2[:, 0].sum() > 0:
+    sel = t2[:, 0] > 0
+    cells = t2[sel, 0].sum()
+    print(f"tc2: {sel.sum()} CTAs, {cells} cells; per cell (cycles, CTA-time): runs+pos {t2[sel, 1].sum() / cells:.0f}, "
+          f"cholesky {t2[sel, 2].sum() / cells:.0f}, W+Sinv {t2[sel, 3].sum() / cells:.0f} (W warps {t2[sel, 5].sum() / cells:.0f}, "
+          f"Sinv warps {t2[sel, 6].sum() / cells:.0f}), X {t2[sel, 4].sum() / cells:.0f}")
 print("W phase (right-looking), warp 0 per column kt: [wait at the step barrier, chain update + finish, other updates]; S^-1 warps total")
 for jt in range(31):
     if wc[jt, 0] == 0:
