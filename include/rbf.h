@@ -361,9 +361,12 @@ int rbf_trim_memory(void);
  *   "log_slow_alloc"      0   diagnostics: report device allocations slower than N ms (stderr)
  *   "mv_index16"          0   1: 16-bit neighbour-list entries when every row offset fits (half
  *                              the list bytes; measured 8-10% slower)
- *   "setup_tc2"           0   1: RASM setup with two subdomain factorisations per SM, the finished
- *                              rows of L11 retired to an L2 workspace (k_rasm_setup_tc2; measured
- *                              at parity with the one-per-SM kernel on cfg2-cfg5)
+ *   "setup_kernel"        0   RASM setup kernel for the tensor-core cells:
+ *                              0 k_rasm_setup_tc, one factorisation per SM;
+ *                              1 k_rasm_setup_tc2, two per SM, finished rows of L11 retired to
+ *                                an L2 workspace (measured at parity with 0);
+ *                              2 k_rasm_setup_tc3, factorisation of cell i and W / S^-1 / X of
+ *                                cell i-1 pipelined on one SM
  * EINVAL for an unknown name or a value out of range. */
 int rbf_set_option(const char *name, int64_t value);
 int rbf_get_option(const char *name, int64_t *value);

@@ -34,7 +34,7 @@ static const OptDef kOptDefs[OPT_COUNT] = {
     {"mv_variant", 0, 0, 5},     {"solve_graph", 1, 0, 1}, {"fused_arnoldi", 1, 0, 1},
     {"mgs_pairs", 1, 0, 1},      {"arnoldi_ctas_per_sm", 2, 1, 4},
     {"log_slow_alloc", 0, 0, 1000000}, {"mv_index16", 0, 0, 1},
-    {"setup_tc2", 0, 0, 1},
+    {"setup_kernel", 0, 0, 2},
 };
 static std::atomic<long long> g_opt[OPT_COUNT] = {};
 static std::once_flag g_opt_init;

@@ -52,7 +52,7 @@ enum Opt {
   OPT_ARNOLDI_PER_SM,    // fused Arnoldi: CTAs per SM (2)
   OPT_LOG_SLOW_ALLOC,    // diagnostics: log device allocations slower than this many ms (0 = off)
   OPT_MV_INDEX16,        // matvec: 16-bit neighbour-list entries when they fit (0: measured slower)
-  OPT_SETUP_TC2,         // RASM setup: two factorisations per SM with rows retired to L2 (0: measured at parity)
+  OPT_SETUP_KERNEL,      // RASM setup kernel: 0 one factorisation per SM, 1 two per SM, 2 pipelined post phase
   OPT_COUNT
 };
 long long opt(Opt o);

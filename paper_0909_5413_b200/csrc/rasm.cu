@@ -873,14 +873,14 @@ constexpr int kT2Recs = (kTcMaxTiles + 1) * (kT2MaxT1 + 1);
 
 // acc[m] += sum_{kt < j} L(it0 + kT2Acc m, kt) L(j+1, kt)^T for m < NM (one chain per row;
 // the B fragments of row j+1 are shared by the NM rows)
-template <int NM>
-__device__ __forceinline__ void t2_acc_rows(double (&acc)[kT2M][2], const double *sm, const unsigned char *slot,
+template <int NM, int ACC = kT2Acc, int MM = kT2M>
+__device__ __forceinline__ void t2_acc_rows(double (&acc)[MM][2], const double *sm, const unsigned char *slot,
                                             int j, int it0, int f0, int f1) {
   const unsigned char *sj = slot + (((j + 1) * (j + 2)) >> 1);
   const unsigned char *si[NM];
 #pragma unroll
   for (int m = 0; m < NM; ++m) {
-    const int it = it0 + kT2Acc * m;
+    const int it = it0 + ACC * m;
     si[m] = slot + ((it * (it + 1)) >> 1);
   }
 #pragma unroll 2
@@ -1353,6 +1353,488 @@ __global__ __launch_bounds__(kT2Threads, 2) void k_rasm_setup_tc2(
       for (int o = tid; o < S.n1; o += kT2Threads) Xc[(size_t)o * ld + n] = 0.0;
     T2P(4)
   }
+}
+
+// ---------------------------------------------------------------------------
+// Factorisation and post phase pipelined on one SM: k_rasm_setup_tc3 (option setup_tc = 3).
+//
+// One persistent CTA of 20 warps per SM (96 registers).  Warps 0..15 factor cell i (14
+// accumulate warps, two alternating diagonal warps; the row-retiring column loop of
+// k_rasm_setup_tc2 in its 212-slot region C), while warps 16..19 run the post phase of cell i-1 -- W = L21 L11^-1
+// from the retired L11 columns (cp.async ring), S^-1 = L22^-T L22^-1 and X_c = S^-1 [-W, I]
+// -- from a region P that holds that cell's own tile rows.  At the end of cell i's
+// factorisation the two groups meet (named barrier 3): the post warps are done with cell
+// i-1, the factor warps copy cell i's own rows and diagonal reciprocals into P and hand
+// over.  The retired rows alternate between two workspace slices per CTA, so that cell
+// i+1 can retire rows while the post warps read cell i's.  Measured: the
+// post phase is hidden (75k of the 155k cycles per cell), but the factorisation next to it
+// takes 155k cycles instead of the one-per-SM kernel's 125k, so the setup is at parity.
+// ---------------------------------------------------------------------------
+constexpr int kT3FacWarps = 16;              // factor warps 0..15
+constexpr int kT3Threads = (kT3FacWarps + 4) * 32;
+constexpr int kT3Acc = kT3FacWarps - 2;      // accumulate warps; the last two alternate as diagonal warps
+constexpr int kT3M = (kTcMaxTiles - 1 + kT3Acc - 1) / kT3Acc;  // rows per accumulate warp and column
+constexpr int kT3PostWarps = 4;              // the last four warps
+constexpr int kT3OwnTiles = kT2MaxT1 * kTcMaxTiles;   // P: own tile rows, row-major (r, jt)
+constexpr int kT3Ring = 3 * kTcMaxTiles;             // P: three L11 column buffers
+constexpr int kT3Scr = 4;                            // P: S^-1 product scratch, one per warp
+constexpr int kT3MTiles = kT2MaxT1 * (kT2MaxT1 - 1) / 2;  // P: M = L22^-1 strictly lower tiles
+constexpr size_t kT3SmemTiles = (size_t)kT2Cap + kT3OwnTiles + kT3Ring + kT3Scr + kT3MTiles;
+constexpr size_t kT3Smem = kT3SmemTiles * 512 + 2 * kTcMaxTiles * 8 * sizeof(double) +
+                           kTcMaxTiles * 8 * sizeof(double2) + 440;
+
+struct T3Post {  // the cell handed to the post warps
+  int cl, n, n0, n1, own_nat_lo, T0, T1, slice;
+};
+
+__global__ __launch_bounds__(kT3Threads, 1) void k_rasm_setup_tc3(
+    Geom g, Strip st, const double2 *__restrict__ xy, const int *__restrict__ cell_start,
+    const long long *__restrict__ x_off, double *__restrict__ X, int *__restrict__ counts,
+    int *__restrict__ glist, OvList ov, const unsigned char *__restrict__ plans, double *__restrict__ ws,
+    int *__restrict__ work, int *__restrict__ deferred, int ncl) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ Runs R;
+  __shared__ int s_cl, s_fail;
+  __shared__ T3Post s_post;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double *Pown = sm + (size_t)kT2Cap * 64;            // own tile (T0 + r, jt) at Pown + (r * 29 + jt) * 64
+  double *Pring = Pown + (size_t)kT3OwnTiles * 64;    // ring tile e of buffer b at Pring + (b * 29 + e) * 64
+  double *Pscr = Pring + (size_t)kT3Ring * 64;        // scratch of post warp w at Pscr + w * 64
+  double *Pm = Pscr + (size_t)kT3Scr * 64;            // M tiles
+  double *rdiag = Pm + (size_t)kT3MTiles * 64;        // factor side
+  double *rdiagP = rdiag + kTcMaxTiles * 8;           // post side
+  double2 *pos = reinterpret_cast<double2 *>(rdiagP + kTcMaxTiles * 8);
+  unsigned char *slot = reinterpret_cast<unsigned char *>(pos + kTcMaxTiles * 8);
+  const int f0 = frag_rowk(lane, 0), f1 = frag_rowk(lane, 1);
+#ifdef RBF_PROBE
+#define T3P(k, who)                                                   \
+  if (tid == (who)) {                                                 \
+    const long long t_ = clock64();                                   \
+    if ((k) > 0) g_t2_acc[blockIdx.x][k] += t_ - t3_last;             \
+    t3_last = t_;                                                     \
+  }
+  long long t3_last = 0;
+#else
+#define T3P(k, who) {}
+#endif
+
+  if (warp >= kT3FacWarps) {
+    // =================== post warps: W, S^-1, X of the handed-over cell ===================
+    const int pw = warp - kT3FacWarps, ptid = tid - kT3FacWarps * 32;
+    for (;;) {
+      asm volatile("bar.sync 3, %0;" ::"n"(kT3Threads) : "memory");  // done with the previous cell
+      asm volatile("bar.sync 3, %0;" ::"n"(kT3Threads) : "memory");  // the next cell is in P
+      const T3Post q = s_post;
+      if (q.cl < 0) return;
+      T3P(0, kT3FacWarps * 32)
+#ifdef RBF_T3_NOPOST
+      continue;  // timing diagnostic only: the factorisation without the post phase
+#endif
+      const int T0 = q.T0, T1 = q.T1;
+      const double *wsl = ws + ((size_t)blockIdx.x * 2 + q.slice) * kT2WsTiles * 64;
+      auto ptile = [&](int it, int jt) -> double * { return Pown + ((it - T0) * kTcMaxTiles + jt) * 64; };
+      // ---- W(r, jt) = (C(r, jt) - sum_{kt > jt} W(r, kt) L(kt, jt)) L_d(jt)^-1, jt = T0-1..0
+      auto fetch = [&](int jt) {
+        const int nt = T0 - jt, b = jt % 3;
+        const double2 *src = reinterpret_cast<const double2 *>(wsl + (size_t)t2_gcol(jt, T0) * 64);
+        double2 *dst = reinterpret_cast<double2 *>(Pring + (size_t)b * kTcMaxTiles * 64);
+        for (int q2 = ptid; q2 < nt * 32; q2 += kT3PostWarps * 32) cp_async16(dst + q2, src + q2);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+      };
+      if (T0 >= 1) fetch(T0 - 1);
+      if (T0 >= 2) fetch(T0 - 2);
+      const int r = pw;
+      for (int jt = T0 - 1; jt >= 0; --jt) {
+        if (jt >= 1) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        asm volatile("bar.sync 2, %0;" ::"n"(kT3PostWarps * 32) : "memory");
+        if (jt >= 2) fetch(jt - 2);
+        if (r < T1) {
+          const double *col = Pring + (size_t)(jt % 3) * kTcMaxTiles * 64;  // tile e = L(jt + e, jt)
+          const int g0 = frag_colk(lane, 0), g1 = frag_colk(lane, 1);
+          double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0;
+          const double *Wr = ptile(T0 + r, 0);
+          int kt = jt + 1;
+#pragma unroll 2
+          for (; kt + 1 < T0; kt += 2) {
+            const double *W0 = Wr + kt * 64, *W1 = W0 + 64;
+            const double *L0 = col + (kt - jt) * 64, *L1 = L0 + 64;
+            dmma(a0, a1, W0[f0], L0[g0]);
+            dmma(c0, c1, W1[f0], L1[g0]);
+            dmma(a0, a1, W0[f1], L0[g1]);
+            dmma(c0, c1, W1[f1], L1[g1]);
+          }
+          if (kt < T0) {
+            const double *W0 = Wr + kt * 64, *L0 = col + (kt - jt) * 64;
+            dmma(a0, a1, W0[f0], L0[g0]);
+            dmma(a0, a1, W0[f1], L0[g1]);
+          }
+          double *Ct = ptile(T0 + r, jt);
+          double2 *cp = reinterpret_cast<double2 *>(Ct + frag_acc(lane));
+          double2 cv = *cp;
+          cv.x -= a0 + c0;
+          cv.y -= a1 + c1;
+          *cp = cv;
+          __syncwarp();
+          const double *D = col;  // diagonal tile (jt, jt)
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int k = 4 * h + (lane & 3), n = lane >> 2;
+            const double bv = (k > n) ? D[swz(n, k)] : (k == n ? rdiagP[jt * 8 + k] : 0.0);
+            dmma(d0, d1, Ct[frag_rowk(lane, h)], bv);
+          }
+          __syncwarp();
+          *cp = make_double2(d0, d1);
+          __syncwarp();
+        }
+      }
+      T3P(5, kT3FacWarps * 32)
+      // ---- S^-1 = L22^-T L22^-1 (M = L22^-1 by columns, one warp per column)
+      {
+        const int sw = pw;
+        double *scr = Pscr + sw * 64;
+        auto mt = [&](int a, int b) { return Pm + ((a * (a - 1)) / 2 + b) * 64; };  // a > b only
+        const int m_ = lane >> 2, q_ = lane & 3;
+        auto linvA = [&](int a, int h) -> double {
+          const double *D = ptile(T0 + a, T0 + a);
+          const int kk = 4 * h + q_;
+          return (m_ > kk) ? D[swz(kk, m_)] : (m_ == kk ? rdiagP[(T0 + a) * 8 + m_] : 0.0);
+        };
+        auto linvB = [&](int a, int h) -> double {
+          const double *D = ptile(T0 + a, T0 + a);
+          const int kk = 4 * h + q_;
+          return (kk > m_) ? D[swz(m_, kk)] : (kk == m_ ? rdiagP[(T0 + a) * 8 + kk] : 0.0);
+        };
+        auto linvT = [&](int a, int h) -> double {
+          const double *D = ptile(T0 + a, T0 + a);
+          const int kk = 4 * h + q_;
+          return (kk > m_) ? D[swz(m_, kk)] : (kk == m_ ? rdiagP[(T0 + a) * 8 + m_] : 0.0);
+        };
+        for (int b = sw; b < T1 - 1; b += kT3PostWarps) {
+          for (int a = b + 1; a < T1; ++a) {
+            double d0 = 0.0, d1 = 0.0;
+            for (int k = b; k < a; ++k) {
+              const double *La = ptile(T0 + a, T0 + k);
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+                dmma(d0, d1, La[frag_rowk(lane, h)], k == b ? linvB(b, h) : mt(k, b)[frag_colk(lane, h)]);
+            }
+            *reinterpret_cast<double2 *>(scr + frag_acc(lane)) = make_double2(d0, d1);
+            __syncwarp();
+            double e0 = 0.0, e1 = 0.0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) dmma(e0, e1, linvA(a, h), scr[frag_colk(lane, h)]);
+            __syncwarp();
+            *reinterpret_cast<double2 *>(mt(a, b) + frag_acc(lane)) = make_double2(-e0, -e1);
+            __syncwarp();
+          }
+        }
+        asm volatile("bar.sync 2, %0;" ::"n"(kT3PostWarps * 32) : "memory");  // M complete
+        constexpr int kSlots = (kT2MaxT1 * (kT2MaxT1 + 1) / 2 + kT3PostWarps - 1) / kT3PostWarps;
+        double res[kSlots][2];
+        const int ntl = T1 * (T1 + 1) / 2;
+#pragma unroll
+        for (int sl = 0; sl < kSlots; ++sl) {
+          const int t = sw + sl * kT3PostWarps;
+          res[sl][0] = res[sl][1] = 0.0;
+          if (t < ntl) {
+            int a = 0;
+            while ((a + 1) * (a + 2) / 2 <= t) ++a;
+            const int bb = t - a * (a + 1) / 2;
+            for (int k = a; k < T1; ++k) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const double av = (k == a) ? linvT(a, h) : mt(k, a)[frag_colk(lane, h)];
+                const double bv = (k == bb) ? linvB(bb, h) : mt(k, bb)[frag_colk(lane, h)];
+                dmma(res[sl][0], res[sl][1], av, bv);
+              }
+            }
+          }
+        }
+        asm volatile("bar.sync 2, %0;" ::"n"(kT3PostWarps * 32) : "memory");  // L^-1 scratch read
+#pragma unroll
+        for (int sl = 0; sl < kSlots; ++sl) {
+          const int t = sw + sl * kT3PostWarps;
+          if (t < ntl) {
+            int a = 0;
+            while ((a + 1) * (a + 2) / 2 <= t) ++a;
+            const int bb = t - a * (a + 1) / 2;
+            *reinterpret_cast<double2 *>(ptile(T0 + a, T0 + bb) + frag_acc(lane)) =
+                make_double2(res[sl][0], res[sl][1]);
+          }
+        }
+        asm volatile("bar.sync 2, %0;" ::"n"(kT3PostWarps * 32) : "memory");  // S^-1 final
+      }
+      T3P(6, kT3FacWarps * 32)
+      // ---- X_c = S^-1 [-W, I] in natural column order (ld = n rounded up to even), to HBM
+      {
+        const int n = q.n, n0 = q.n0, n1 = q.n1, onl = q.own_nat_lo;
+        const int ld = (n + 1) & ~1;
+        double *Xc = X + x_off[q.cl];
+        auto sinv_frag = [&](int ot, int kt, int h) -> double {
+          const bool lower = kt <= ot;
+          const double *At = lower ? ptile(T0 + ot, T0 + kt) : ptile(T0 + kt, T0 + ot);
+          const int m = lane >> 2, k = 4 * h + (lane & 3);
+          return lower ? At[swz(m, k)] : At[swz(k, m)];
+        };
+        for (int task = pw; task < T1 * T0; task += kT3PostWarps) {
+          const int ot = task / T0, jt = task - ot * T0;
+          double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+          for (int kt = 0; kt < T1; ++kt) {
+            const double *Bt = ptile(T0 + kt, jt);
+            if (kt & 1) {
+              dmma(e0, e1, sinv_frag(ot, kt, 0), Bt[frag_colk(lane, 0)]);
+              dmma(e0, e1, sinv_frag(ot, kt, 1), Bt[frag_colk(lane, 1)]);
+            } else {
+              dmma(d0, d1, sinv_frag(ot, kt, 0), Bt[frag_colk(lane, 0)]);
+              dmma(d0, d1, sinv_frag(ot, kt, 1), Bt[frag_colk(lane, 1)]);
+            }
+          }
+          const int o = ot * 8 + (lane >> 2);
+          const int p0 = jt * 8 + 2 * (lane & 3);
+          if (o < n1) {
+            if (p0 < n0) Xc[(size_t)o * ld + (p0 < onl ? p0 : p0 + n1)] = -(d0 + e0);
+            if (p0 + 1 < n0) Xc[(size_t)o * ld + (p0 + 1 < onl ? p0 + 1 : p0 + 1 + n1)] = -(d1 + e1);
+          }
+        }
+        for (int t = ptid; t < n1 * n1; t += kT3PostWarps * 32) {
+          const int o = t / n1, jj = t - o * n1;
+          const int i1 = o >= jj ? o : jj, j1 = o >= jj ? jj : o;
+          Xc[(size_t)o * ld + onl + jj] = ptile(T0 + (i1 >> 3), T0 + (j1 >> 3))[swz(i1 & 7, j1 & 7)];
+        }
+        if (ld != n)
+          for (int o = ptid; o < n1; o += kT3PostWarps * 32) Xc[(size_t)o * ld + n] = 0.0;
+      }
+      T3P(7, kT3FacWarps * 32)
+    }
+  }
+
+  // =================== factor warps 0..11 ===================
+  int ncell = 0;
+  for (;;) {
+    asm volatile("bar.sync 1, %0;" ::"n"(kT3FacWarps * 32) : "memory");  // done with R and region C
+    T3P(0, 0)
+    if (tid == 0) {
+      const int cl = atomicAdd(work, 1);
+      s_cl = cl;
+      s_fail = 0;
+      if (cl < ncl) sub_runs(g, cell_start, ov, cl, cl % g.ncx, st.row_lo + cl / g.ncx, R);
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kT3FacWarps * 32) : "memory");
+    const int cl = s_cl;
+    if (cl >= ncl) break;
+    if (R.n_own == 0) continue;
+    const TileShape S(R.n_ov, R.n_own);
+    if (!S.fits_tc()) continue;  // handled by k_rasm_setup_lu
+    const unsigned char *plan = plans + (size_t)t2_rec_index(S.T, S.T1 <= kT2MaxT1 ? S.T1 : 0) * kT2Rec;
+    const int *pint = reinterpret_cast<const int *>(plan + kT2RecPeak);
+    if (S.T1 > kT2MaxT1 || pint[0] > kT2Cap) {
+      if (tid == 0) deferred[atomicAdd(work + 1, 1)] = cl;  // left to k_rasm_setup_tc
+      continue;
+    }
+    const int T = S.T, N = S.N, T0 = S.T0, T1 = S.T1;
+    const int slice = ncell & 1;
+    double *wsl = ws + ((size_t)blockIdx.x * 2 + slice) * kT2WsTiles * 64;
+    const int ntix = T * (T + 1) / 2;
+    for (int i = tid; i < (ntix + 3) / 4; i += kT3FacWarps * 32)
+      reinterpret_cast<unsigned *>(slot)[i] = __ldg(reinterpret_cast<const unsigned *>(plan) + i);
+    for (int p = tid; p < N; p += kT3FacWarps * 32) {
+      const int gi = fac_to_global(R, S, p);
+      pos[p] = (gi >= 0) ? xy[gi - st.ext_lo] : make_double2(0.0, 0.0);
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kT3FacWarps * 32) : "memory");
+    auto tile = [&](int it, int jt) -> double * { return sm + (int)slot[((it * (it + 1)) >> 1) + jt] * 64; };
+    T3P(1, 0)
+#ifdef RBF_PROBE
+    if (tid == 0) g_t2_acc[blockIdx.x][0] += 1;
+#endif
+
+    double acc[kT3M][2], accb[2];
+#pragma unroll
+    for (int m = 0; m < kT3M; ++m) acc[m][0] = acc[m][1] = 0.0;
+    accb[0] = accb[1] = 0.0;
+    if (warp < kT3Acc) {
+#pragma unroll
+      for (int m = 0; m < kT3M; ++m) {
+        const int it = 1 + warp + kT3Acc * m;
+        if (it < T) {
+          double v0, v1;
+          a_entries(pos, S, g, it, 0, lane, v0, v1);
+          acc[m][0] = -v0;
+          acc[m][1] = -v1;
+        }
+      }
+    } else if (warp == kT3Acc) {
+      double v0, v1;
+      a_entries(pos, S, g, 0, 0, lane, v0, v1);
+      acc[0][0] = -v0;
+      acc[0][1] = -v1;
+    }
+    for (int j = 0; j < T; ++j) {
+      const int dw = kT3Acc + (j & 1);
+      if (warp < kT3Acc) {
+        const int nm1 = (T - (j + 1) - warp + kT3Acc - 1) / kT3Acc;
+        const int nm2 = (T - (j + 2) - warp + kT3Acc - 1) / kT3Acc;
+        if (nm1 > 0) {
+          const double *Bt = j >= 1 ? tile(j, j - 1) : sm;
+          const double b0 = Bt[f0], b1 = Bt[f1];
+#pragma unroll
+          for (int m = 0; m < kT3M; ++m)
+            if (m < nm1) {
+              const int it = j + 1 + warp + kT3Acc * m;
+              if (j >= 1) {
+                const double *At = tile(it, j - 1);
+                dmma(acc[m][0], acc[m][1], At[f0], b0);
+                dmma(acc[m][0], acc[m][1], At[f1], b1);
+              }
+              double c0 = acc[m][0], c1 = acc[m][1];
+              if (m == 0 && nm1 == 1) {
+                c0 += accb[0];
+                c1 += accb[1];
+              }
+              *reinterpret_cast<double2 *>(tile(it, j) + frag_acc(lane)) = make_double2(-c0, -c1);
+            }
+        }
+        accb[0] = accb[1] = 0.0;
+        if (nm2 > 0) {
+#pragma unroll
+          for (int m = 0; m < kT3M; ++m)
+            if (m < nm2) {
+              double v0, v1;
+              a_entries(pos, S, g, j + 2 + warp + kT3Acc * m, j + 1, lane, v0, v1);
+              acc[m][0] = -v0;
+              acc[m][1] = -v1;
+            }
+          if (nm2 == 1) {
+            const unsigned char *sj = slot + (((j + 1) * (j + 2)) >> 1);
+            const int it = j + 2 + warp;
+            const unsigned char *si = slot + ((it * (it + 1)) >> 1);
+            int kt = 0;
+            for (; kt + 1 < j; kt += 2) {
+              const double *B0 = sm + (int)sj[kt] * 64, *B1 = sm + (int)sj[kt + 1] * 64;
+              const double *A0 = sm + (int)si[kt] * 64, *A1 = sm + (int)si[kt + 1] * 64;
+              dmma(acc[0][0], acc[0][1], A0[f0], B0[f0]);
+              dmma(accb[0], accb[1], A1[f0], B1[f0]);
+              dmma(acc[0][0], acc[0][1], A0[f1], B0[f1]);
+              dmma(accb[0], accb[1], A1[f1], B1[f1]);
+            }
+            if (kt < j) {
+              const double *B0 = sm + (int)sj[kt] * 64, *A0 = sm + (int)si[kt] * 64;
+              dmma(acc[0][0], acc[0][1], A0[f0], B0[f0]);
+              dmma(acc[0][0], acc[0][1], A0[f1], B0[f1]);
+            }
+          } else if (nm2 == 2) {
+            t2_acc_rows<2, kT3Acc, kT3M>(acc, sm, slot, j, j + 2 + warp, f0, f1);
+          } else {
+            t2_acc_rows<kT3M, kT3Acc, kT3M>(acc, sm, slot, j, j + 2 + warp, f0, f1);
+          }
+        }
+      } else if (warp == dw) {
+        double *D = tile(j, j);
+        if (j >= 1) {
+          const double *Lt = tile(j, j - 1);
+          const double l0 = Lt[f0], l1 = Lt[f1];
+          dmma(acc[0][0], acc[0][1], l0, l0);
+          dmma(accb[0], accb[1], l1, l1);
+        }
+        *reinterpret_cast<double2 *>(D + frag_acc(lane)) =
+            make_double2(-(acc[0][0] + accb[0]), -(acc[0][1] + accb[1]));
+        __syncwarp();
+        if (diag_factor_t(D, rdiag, j, lane) && lane == 0) s_fail = 1;
+      } else if (j + 1 < T) {
+        double v0, v1;
+        a_entries(pos, S, g, j + 1, j + 1, lane, v0, v1);
+        acc[0][0] = -v0;
+        acc[0][1] = -v1;
+        accb[0] = accb[1] = 0.0;
+        const unsigned char *sj = slot + (((j + 1) * (j + 2)) >> 1);
+        int kt = 0;
+        for (; kt + 1 < j; kt += 2) {
+          const double *L0 = sm + (int)sj[kt] * 64, *L1 = sm + (int)sj[kt + 1] * 64;
+          const double x0 = L0[f0], x1 = L0[f1], y0 = L1[f0], y1 = L1[f1];
+          dmma(acc[0][0], acc[0][1], x0, x0);
+          dmma(accb[0], accb[1], y0, y0);
+          dmma(acc[0][0], acc[0][1], x1, x1);
+          dmma(accb[0], accb[1], y1, y1);
+        }
+        if (kt < j) {
+          const double *L0 = sm + (int)sj[kt] * 64;
+          const double x0 = L0[f0], x1 = L0[f1];
+          dmma(acc[0][0], acc[0][1], x0, x0);
+          dmma(acc[0][0], acc[0][1], x1, x1);
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kT3FacWarps * 32) : "memory");
+      if (s_fail) break;  // uniform
+      if (warp < kT3Acc) {
+        const int nm1 = (T - (j + 1) - warp + kT3Acc - 1) / kT3Acc;
+        if (nm1 > 0) {
+          const double *D = tile(j, j);
+          double bv[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int k = 4 * h + (lane & 3), n = lane >> 2;
+            bv[h] = (n > k) ? D[swz(k, n)] : (n == k ? rdiag[j * 8 + k] : 0.0);
+          }
+#pragma unroll
+          for (int m = 0; m < kT3M; ++m)
+            if (m < nm1) {
+              double *Ct = tile(j + 1 + warp + kT3Acc * m, j);
+              double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+              for (int h = 0; h < 2; ++h) dmma(d0, d1, Ct[frag_rowk(lane, h)], bv[h]);
+              __syncwarp();
+              *reinterpret_cast<double2 *>(Ct + frag_acc(lane)) = make_double2(d0, d1);
+            }
+        }
+      } else {
+        // retire row j+1's tiles (j+1, kt < j) and row j's (j, j-1), (j, j) (rows of L11)
+        const int t = tid - kT3Acc * 32;
+        const int na = (j + 1 < T0) ? j : 0;
+        const int nb = (j < T0) ? (j >= 1 ? 2 : 1) : 0;
+        for (int q2 = t; q2 < (na + nb) * 32; q2 += 64) {
+          const int e = q2 >> 5, p = q2 & 31;
+          int it, kt;
+          if (e < na) {
+            it = j + 1;
+            kt = e;
+          } else {
+            it = j;
+            kt = (e - na == nb - 1) ? j : j - 1;
+          }
+          const double2 v = *reinterpret_cast<const double2 *>(tile(it, kt) + 2 * p);
+          __stcg(reinterpret_cast<double2 *>(wsl + (size_t)(t2_gcol(kt, T0) + it - kt) * 64 + 2 * p), v);
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kT3FacWarps * 32) : "memory");
+    }
+    if (s_fail) {  // Cholesky broke down: redo this cell with LU (reading Q11)
+      if (tid == 0) glist[atomicAdd(&counts[3], 1)] = cl;
+      continue;
+    }
+    T3P(2, 0)
+    // ---- hand the cell over: wait for the post warps, copy the own rows into P
+    asm volatile("bar.sync 3, %0;" ::"n"(kT3Threads) : "memory");
+    T3P(3, 0)
+    for (int q2 = tid; q2 < T1 * T * 32; q2 += kT3FacWarps * 32) {
+      const int e = q2 >> 5, p = q2 & 31;
+      const int r = e / T, jt = e - r * T;
+      if (jt <= T0 + r) {
+        const double2 v = *reinterpret_cast<const double2 *>(tile(T0 + r, jt) + 2 * p);
+        *reinterpret_cast<double2 *>(Pown + ((size_t)r * kTcMaxTiles + jt) * 64 + 2 * p) = v;
+      }
+    }
+    for (int i = tid; i < T * 8; i += kT3FacWarps * 32) rdiagP[i] = rdiag[i];
+    if (tid == 0) s_post = T3Post{cl, S.n, S.n0, S.n1, R.own_nat_lo, T0, T1, slice};
+    asm volatile("bar.sync 3, %0;" ::"n"(kT3Threads) : "memory");
+    T3P(4, 0)
+    ++ncell;
+  }
+  // no cells left: release the post warps
+  asm volatile("bar.sync 3, %0;" ::"n"(kT3Threads) : "memory");
+  if (tid == 0) s_post.cl = -1;
+  asm volatile("bar.sync 3, %0;" ::"n"(kT3Threads) : "memory");
 }
 
 // Global-memory local solve for subdomains whose factor does not fit in shared
@@ -2207,19 +2689,25 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
   RBF_TRY(dalloc(c, (void **)&c->X, sizeof(double) * (size_t)(total > 0 ? total : 2), s));
   if (ncl > 0 && c->nsub > hc[3]) {
     const size_t smem = (size_t)hc[4];  // the largest per-cell layout of the tensor-core cells
-    if (opt(OPT_SETUP_TC2)) {
-      // two factorisations per SM; the cells it cannot take (n_own > 32) are listed for
-      // the one-per-SM kernel
+    const int skern = (int)opt(OPT_SETUP_KERNEL);
+    if (skern == 1 || skern == 2) {
+      // 1: two factorisations per SM; 2: factorisation and post phase pipelined on one SM.
+      // The cells they cannot take (n_own > 32) are listed for the one-per-SM kernel.
       const unsigned char *plans = nullptr;
       RBF_TRY(t2_plans(&plans));
       int dev = 0, sms = 148, occ = 0;
       RBF_CUDA_TRY(cudaGetDevice(&dev));
       RBF_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      RBF_TRY(ensure_dyn_smem((const void *)k_rasm_setup_tc2, kT2Smem));
-      RBF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rasm_setup_tc2, kT2Threads, kT2Smem));
+      if (skern == 1) {
+        RBF_TRY(ensure_dyn_smem((const void *)k_rasm_setup_tc2, kT2Smem));
+        RBF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rasm_setup_tc2, kT2Threads, kT2Smem));
+      } else {
+        RBF_TRY(ensure_dyn_smem((const void *)k_rasm_setup_tc3, kT3Smem));
+        RBF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rasm_setup_tc3, kT3Threads, kT3Smem));
+      }
       const int grid = std::max(1, std::min(ncl, std::max(occ, 1) * sms));
 #ifdef RBF_PROBE
-      fprintf(stderr, "[probe] k_rasm_setup_tc2: %d CTAs per SM, grid %d, %zu B dynamic shared memory\n", occ, grid,
+      fprintf(stderr, "[probe] k_rasm_setup_tc2/3: %d CTAs per SM, grid %d, %zu B dynamic shared memory\n", occ, grid,
               kT2Smem);
       {
         static long long zero[512 * 8];
@@ -2228,11 +2716,15 @@ int rasm_setup(rbf_ctx *c, cudaStream_t s) {
 #endif
       double *ws2 = nullptr;
       int *w2 = nullptr;
-      RBF_TRY(dalloc(c, (void **)&ws2, sizeof(double) * 64 * (size_t)kT2WsTiles * grid, s));
+      RBF_TRY(dalloc(c, (void **)&ws2, sizeof(double) * 64 * (size_t)kT2WsTiles * grid * (skern == 2 ? 2 : 1), s));
       RBF_TRY(dalloc(c, (void **)&w2, sizeof(int) * (2 + (size_t)ncl), s));
       RBF_CUDA_TRY(cudaMemsetAsync(w2, 0, 2 * sizeof(int), s));
-      k_rasm_setup_tc2<<<grid, kT2Threads, kT2Smem, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off, c->X,
-                                                          cnt, glist, ov, plans, ws2, w2, w2 + 2, ncl);
+      if (skern == 1)
+        k_rasm_setup_tc2<<<grid, kT2Threads, kT2Smem, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off, c->X,
+                                                            cnt, glist, ov, plans, ws2, w2, w2 + 2, ncl);
+      else
+        k_rasm_setup_tc3<<<grid, kT3Threads, kT3Smem, s>>>(c->g, c->s, c->xy_ext, c->cell_start, c->x_off, c->X,
+                                                            cnt, glist, ov, plans, ws2, w2, w2 + 2, ncl);
       count_launch(1);
       RBF_CUDA_TRY(cudaGetLastError());
       RBF_TRY(prebuild_solve(c, s));  // host work while the kernel runs (krylov.cu)

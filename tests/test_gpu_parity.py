@@ -84,9 +84,10 @@ def test_rasm_apply_parity(wl):
     assert rel(z, ref) <= 1e-10
 
 
+@pytest.mark.parametrize("kern", [1, 2], ids=["two-per-sm", "pipelined"])
 @pytest.mark.parametrize("wl", SMALL[:4], ids=IDS[:4])
-def test_rasm_apply_parity_two_per_sm(wl, lib_options):
-    """Option setup_tc2 = 1: the setup kernel with two factorisations per SM (finished
+def test_rasm_apply_parity_two_per_sm(wl, kern, lib_options):
+    """Option setup_kernel = 1: the setup kernel with two factorisations per SM (finished
     rows of L11 retired to an L2 workspace, W from the rows streamed back) is held to the
     oracle like the default kernel, and to the default kernel itself within rounding
     (the two sum the same products in different orders)."""
@@ -96,19 +97,20 @@ def test_rasm_apply_parity_two_per_sm(wl, lib_options):
     ref = Pc.apply(r)
     Pc.close()
     z = {}
-    for v in (0, 1):
-        lib_options(setup_tc2=v)
+    for v in (0, kern):
+        lib_options(setup_kernel=v)
         with ctx_for(wl) as c:
             z[v] = to_caller(c, c.rasm_apply(c.to_local(torch.from_numpy(r).cuda())))
-    assert rel(z[1], ref) <= 1e-10
-    assert rel(z[1], z[0]) <= 1e-10
+    assert rel(z[kern], ref) <= 1e-10
+    assert rel(z[kern], z[0]) <= 1e-10
 
 
-def test_two_per_sm_defers_large_own_cells_and_solves(lib_options):
+@pytest.mark.parametrize("kern", [1, 2], ids=["two-per-sm", "pipelined"])
+def test_two_per_sm_defers_large_own_cells_and_solves(kern, lib_options):
     """Cells with more than 32 own points are left by k_rasm_setup_tc2 to the one-per-SM
     kernel (the paper's B = 5 sigma at h/sigma = 0.9 with box overlap D = 1.5 B: 33..64
     own points); apply and solve stay at oracle parity."""
-    lib_options(setup_tc2=1)
+    lib_options(setup_kernel=kern)
     wl = W.make_paper_lattice(61, 0.9, b_over_sigma=5.0, d_over_b=1.5)
     r = np.random.default_rng(61).standard_normal(wl.n)
     Pc = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, wl.rings, overlap_width=wl.overlap_width)

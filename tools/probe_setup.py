@@ -14,7 +14,7 @@ R.LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "probe", o
 L = R.lib()
 L.rbf_debug_probe.argtypes = [C.c_void_p]
 L.rbf_debug_probe.restype = C.c_int
-R.set_option("setup_tc2", int(os.environ.get("TC2", "1")))
+R.set_option("setup_kernel", int(os.environ.get("TC2", "1")))
 wl = W.config(int(sys.argv[1]) if len(sys.argv) > 1 else 2)
 xy = torch.from_numpy(wl.xy).cuda()
 for _ in range(2):
@@ -27,6 +27,13 @@ assert L.rbf_debug_probe(buf.ctypes.data_as(C.c_void_p)) == 0
 t2 = buf[512 + 65536 * 3 + 512 + 128 + 5120:512 + 65536 * 3 + 512 + 128 + 5120 + 4096].reshape(512, 8)
 t2c = buf[512 + 65536 * 3 + 512 + 128 + 5120 + 4096:512 + 65536 * 3 + 512 + 128 + 5120 + 4096 + 256].reshape(32, 8)
 t2w = buf[512 + 65536 * 3 + 512 + 128 + 5120 + 4096 + 256:].reshape(32, 8)
+if t2[:, 0].sum() > 0 and os.environ.get("TC2") == "2":
+    sel = t2[:, 0] > 0
+    cells = t2[sel, 0].sum()
+    print(f"tc3: {sel.sum()} CTAs, {cells} cells; per cell (cycles): factor warps: runs+pos {t2[sel, 1].sum() / cells:.0f}, "
+          f"cholesky {t2[sel, 2].sum() / cells:.0f}, wait for post {t2[sel, 3].sum() / cells:.0f}, copy {t2[sel, 4].sum() / cells:.0f}; "
+          f"post warps: W {t2[sel, 5].sum() / cells:.0f}, Sinv {t2[sel, 6].sum() / cells:.0f}, X {t2[sel, 7].sum() / cells:.0f}")
+    sys.exit(0)
 if t2[:, 0].sum() > 0:
     sel = t2[:, 0] > 0
     cells = t2[sel, 0].sum()
@@ -83,6 +90,13 @@ wc = buf[512 + 65536 * 3 + 512:512 + 65536 * 3 + 512 + 128].reshape(32, 4)
 t2 = buf[512 + 65536 * 3 + 512 + 128 + 5120:512 + 65536 * 3 + 512 + 128 + 5120 + 4096].reshape(512, 8)
 t2c = buf[512 + 65536 * 3 + 512 + 128 + 5120 + 4096:512 + 65536 * 3 + 512 + 128 + 5120 + 4096 + 256].reshape(32, 8)
 t2w = buf[512 + 65536 * 3 + 512 + 128 + 5120 + 4096 + 256:].reshape(32, 8)
+if t2[:, 0].sum() > 0 and os.environ.get("TC2") == "2":
+    sel = t2[:, 0] > 0
+    cells = t2[sel, 0].sum()
+    print(f"tc3: {sel.sum()} CTAs, {cells} cells; per cell (cycles): factor warps: runs+pos {t2[sel, 1].sum() / cells:.0f}, "
+          f"cholesky {t2[sel, 2].sum() / cells:.0f}, wait for post {t2[sel, 3].sum() / cells:.0f}, copy {t2[sel, 4].sum() / cells:.0f}; "
+          f"post warps: W {t2[sel, 5].sum() / cells:.0f}, Sinv {t2[sel, 6].sum() / cells:.0f}, X {t2[sel, 7].sum() / cells:.0f}")
+    sys.exit(0)
 if t2[:, 0].sum() > 0:
     sel = t2[:, 0] > 0
     cells = t2[sel, 0].sum()

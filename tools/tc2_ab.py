@@ -1,4 +1,4 @@
-"""A/B of the RASM setup kernels: option setup_tc2 = 0 (one factorisation per SM) vs 1
+"""A/B of the RASM setup kernels: option setup_kernel = 0 (one factorisation per SM) vs 1
 (two per SM, rows retired to L2).  Per config: setup time (median of 3), the apply
 difference between the two on a random vector, and one solve's iterations.
 Not part of the product.  Usage: tc2_ab.py CFG [CFG ...]"""
@@ -16,8 +16,8 @@ for cfg in [int(a) for a in sys.argv[1:]] or [2]:
     wl = W.config(cfg)
     xy = torch.from_numpy(wl.xy).cuda()
     z = {}
-    for v in (0, 1):
-        with P.options(setup_tc2=v):
+    for v in [int(k) for k in os.environ.get("KERNELS", "0,1").split(",")]:
+        with P.options(setup_kernel=v):
             su = []
             for r in range(3):
                 c = P.Context(xy, wl.sigma, wl.cell, wl.rc, wl.rings, wl.box)
@@ -34,7 +34,9 @@ for cfg in [int(a) for a in sys.argv[1:]] or [2]:
                 it = rep.iterations
             c.close()
             torch.cuda.synchronize()
-        print(f"cfg{cfg} setup_tc2={v}: rasm setup {statistics.median(su):.2f} ms (all {[round(x, 2) for x in su]}), "
+        print(f"cfg{cfg} setup_kernel={v}: rasm setup {statistics.median(su):.2f} ms (all {[round(x, 2) for x in su]}), "
               f"solve iterations {it}", flush=True)
-    d = (z[0] - z[1]).norm().item() / z[0].norm().item()
-    print(f"cfg{cfg}: apply relative difference tc2 vs tc {d:.3e}", flush=True)
+    ks = sorted(z)
+    for k in ks[1:]:
+        d = (z[ks[0]] - z[k]).norm().item() / z[ks[0]].norm().item()
+        print(f"cfg{cfg}: apply relative difference kernel {k} vs {ks[0]}: {d:.3e}", flush=True)
