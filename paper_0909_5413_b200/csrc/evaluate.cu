@@ -65,8 +65,23 @@ __global__ __launch_bounds__(256) void k_evaluate(Geom g, Strip st, const double
   const bool tbox = g.tw > 0.0;
   double acc = 0.0;
   unsigned long long cnt = 0;
+  // radial cutoff: per cell row, only the cells the disc |q - x| < rc reaches in x (the
+  // row's distance from q, less a margin, bounds |dy| from below); the skipped sources
+  // all fail the exact test, so the sum (same sources, same order) is unchanged
+  const double mg = 1e-9 * g.cell;
   for (int by = by0; by <= by1; ++by) {
-    const int s0 = cell_start[by * g.ncx + bx0], s1 = cell_start[by * g.ncx + bx1 + 1];
+    int xa = bx0, xb = bx1;
+    if (!tbox) {
+      const double lo = g.y0 + by * g.cell, hi = lo + g.cell;
+      const double dy = fmax(fmax(fmax(lo - qy, qy - hi), 0.0) - mg, 0.0);
+      const double w2 = g.rc2 - dy * dy;
+      if (!(w2 > 0.0)) continue;
+      const double wx = sqrt(w2) + mg;
+      xa = max(bx0, (int)floor((qx - wx - g.x0) / g.cell));
+      xb = min(bx1, (int)floor((qx + wx - g.x0) / g.cell));
+      if (xa > xb) continue;
+    }
+    const int s0 = cell_start[by * g.ncx + xa], s1 = cell_start[by * g.ncx + xb + 1];
     for (int j = s0; j < s1; ++j) {
       const double4 o = ld_rec(rec + (j - st.ext_lo));
       const double dx = qx - o.x, dy = qy - o.y;

@@ -144,11 +144,38 @@ __global__ __launch_bounds__(kMvThreads) void k_nlist(Geom g, Strip st, const do
   if (staged)
     for (int by = wv.z; by < by0; ++by)
       wslot += cell_start[by * g.ncx + wv.y + 1] - cell_start[by * g.ncx + wv.x];
+  const double mg = 1e-9 * g.cell;
   for (int by = by0; by <= by1; ++by) {
-    const int s0 = cell_start[by * g.ncx + bx0], s1 = cell_start[by * g.ncx + bx1 + 1];
+    const int s0 = cell_start[by * g.ncx + bx0];
     const long long rs = staged ? wslot + (s0 - cell_start[by * g.ncx + wv.x]) : 0;
     if (staged) wslot += cell_start[by * g.ncx + wv.y + 1] - cell_start[by * g.ncx + wv.x];
-    for (int s = s0; s < s1; ++s) {
+    // radial cutoff: only the cells of this row that the targets' discs reach in x (the
+    // row's distance from a target, less a margin, bounds |dy| from below); the skipped
+    // sources carry no mask bit, so the list (entries, order, offsets from s0) is unchanged
+    int xa = bx0, xb = bx1;
+    if (!tbox) {
+      const double lo = g.y0 + by * g.cell, hi = lo + g.cell;
+      double wl = 1e300, wh = -1e300;
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const double dy = fmax(fmax(fmax(lo - p[j].y, p[j].y - hi), 0.0) - mg, 0.0);
+        const double w2 = g.rc2 - dy * dy;
+        if (act[j] && w2 > 0.0) {
+          const double wx = sqrt(w2) + mg;
+          wl = fmin(wl, p[j].x - wx);
+          wh = fmax(wh, p[j].x + wx);
+        }
+      }
+      if (wl <= wh) {
+        xa = max(bx0, (int)floor((wl - g.x0) / g.cell));
+        xb = min(bx1, (int)floor((wh - g.x0) / g.cell));
+      } else {
+        xb = xa - 1;
+      }
+    }
+    const int s_lo = xa <= xb ? cell_start[by * g.ncx + xa] : 0;
+    const int s1 = xa <= xb ? cell_start[by * g.ncx + xb + 1] : 0;
+    for (int s = s_lo; s < s1; ++s) {
       const double2 o = xy[s - st.ext_lo];
       unsigned m = 0;
 #pragma unroll
