@@ -422,7 +422,7 @@ __device__ __forceinline__ void a_entries(const double2 *pos, const TileShape &S
 __device__ __forceinline__ void setup_post(double *sm, double *rdiag, double2 *pos, const TileShape &S,
                                            const Runs &R, const Geom &g, double *__restrict__ X,
                                            const long long *__restrict__ x_off, int cl, int tid,
-                                           int lane, int warp) {
+                                           int lane, int warp, int *s_fail) {
   const int T = S.T, T0 = S.T0, T1 = S.T1;
   (void)T;
   PROBE(2)
@@ -522,6 +522,42 @@ __device__ __forceinline__ void setup_post(double *sm, double *rdiag, double2 *p
     // M (strictly lower tiles) lives in the positions buffer (dead after the factorisation),
     // each warp's product scratch tile in the (former) W partials area.
     const int sw = warp - kWWarps;
+    // L22: Cholesky of the Schur complement S (formed in place by all warps), right-looking
+    // over the T1 own tile columns, while warps 0..11 run the W phase (which reads L11 and
+    // L21 only)
+    for (int a = 0; a < T1; ++a) {
+      if (sw == 0 && diag_factor(sm, rdiag, T0 + a, lane) && lane == 0) *s_fail = 1;
+      asm volatile("bar.sync 2, %0;" ::"n"((kTcWarps - kWWarps) * 32) : "memory");
+      // panel L(T0+b, T0+a) = C L_d^-T, b > a
+      const double *D = sm + toff(T0 + a, T0 + a);
+      double bv[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int k = 4 * h + (lane & 3), n = lane >> 2;
+        bv[h] = (n > k) ? D[swz(k, n)] : (n == k ? rdiag[(T0 + a) * 8 + k] : 0.0);
+      }
+      for (int b = a + 1 + sw; b < T1; b += kTcWarps - kWWarps) {
+        double *Ct = sm + toff(T0 + b, T0 + a);
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) dmma(d0, d1, Ct[frag_rowk(lane, h)], bv[h]);
+        __syncwarp();
+        *reinterpret_cast<double2 *>(Ct + frag_acc(lane)) = make_double2(d0, d1);
+      }
+      asm volatile("bar.sync 2, %0;" ::"n"((kTcWarps - kWWarps) * 32) : "memory");
+      // trailing update C(T0+b, T0+c) -= L(T0+b, T0+a) L(T0+c, T0+a)^T, a < c <= b
+      const int nr = T1 - 1 - a, nt = nr * (nr + 1) / 2;
+      for (int t = sw; t < nt; t += kTcWarps - kWWarps) {
+        int bb = 0;
+        while ((bb + 1) * (bb + 2) / 2 <= t) ++bb;
+        const int cc = t - bb * (bb + 1) / 2;
+        AccSet A;
+        A.zero();
+        acc_range(A, sm, T0 + a + 1 + bb, T0 + a + 1 + cc, T0 + a, T0 + a + 1, lane);
+        acc_finish_rmw(A, sm, T0 + a + 1 + bb, T0 + a + 1 + cc, lane);
+      }
+      asm volatile("bar.sync 2, %0;" ::"n"((kTcWarps - kWWarps) * 32) : "memory");
+    }
     double *Mt = reinterpret_cast<double *>(pos);
     double *scr = rdiag + T * 8 + sw * 64;
     auto mt = [&](int a, int b) { return Mt + ((a * (a - 1)) / 2 + b) * 64; };  // a > b only
@@ -599,7 +635,16 @@ __device__ __forceinline__ void setup_post(double *sm, double *rdiag, double2 *p
     if (warp == kWWarps) PW(31, 1)
   }
   __syncthreads();
+}
 
+__device__ __forceinline__ void setup_x(double *sm, double *rdiag, double2 *pos, const TileShape &S,
+                                        const Runs &R, const Geom &g, double *__restrict__ X,
+                                        const long long *__restrict__ x_off, int cl, int tid, int lane,
+                                        int warp) {
+  const int T0 = S.T0, T1 = S.T1;
+  (void)rdiag;
+  (void)pos;
+  (void)g;
   PROBE(3)
   // ---- X_c = S^-1 [-W, I] in natural column order, ld = n rounded up to even, staged
   // in shared memory (the L11 tiles are dead) as the contiguous n_own x ld block and
@@ -743,7 +788,10 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
   } else if (warp == kAccWarps) {
     a_entries(pos, S, g, 0, 0, lane, acc[0].v0, acc[0].v1);
   }
-  for (int j = 0; j < T; ++j) {
+  // the loop factors the columns of L11 (and L21); the Schur complement block L22 is
+  // formed and factored after it (see below), concurrently with the W phase
+  const int T0 = S.T0;
+  for (int j = 0; j < T0; ++j) {
     const int dw = kAccWarps + (j & 1);  // diagonal warp of column j
     if (warp == 0) PCOL(0, j, 0)
     if (warp == dw) PCOL(1, j, 0)
@@ -762,7 +810,7 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
       for (int m = 0; m < 2; ++m) {
         const int it = j + 2 + warp + kAccWarps * m;
         acc[m].zero();
-        if (it < T && j + 1 < T) {
+        if (it < T && j + 1 < T0) {
           a_entries(pos, S, g, it, j + 1, lane, acc[m].v0, acc[m].v1);
           acc_range(acc[m], sm, it, j + 1, 0, j, lane);
         }
@@ -775,7 +823,7 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
       PCOL(1, j, 1)
       if (diag_factor(sm, rdiag, j, lane) && lane == 0) s_fail = 1;
       PCOL(1, j, 2)
-    } else if (j + 1 < T) {
+    } else if (j + 1 < T0) {
       // the other diagonal warp accumulates the next diagonal tile over kt < j
       acc[0].zero();
       a_entries(pos, S, g, j + 1, j + 1, lane, acc[0].v0, acc[0].v1);
@@ -815,8 +863,30 @@ __global__ __launch_bounds__(kTcThreads, 1) void k_rasm_setup_tc(
     if (tid == 0) glist[atomicAdd(&counts[3], 1)] = cl;
     return;
   }
+  // ---- the Schur complement S = A22 - L21 L21^T on the own tile rows, all warps: tile
+  // (T0 + a, T0 + b), b <= a, summed over the T0 columns of L21 (two DMMA chains)
+  {
+    const int T1 = S.T1;
+    const int ntl = T1 * (T1 + 1) / 2;
+    for (int t = warp; t < ntl; t += kTcWarps) {
+      int a = 0;
+      while ((a + 1) * (a + 2) / 2 <= t) ++a;
+      const int b = t - a * (a + 1) / 2;
+      AccSet A;
+      A.zero();
+      a_entries(pos, S, g, T0 + a, T0 + b, lane, A.v0, A.v1);
+      acc_range(A, sm, T0 + a, T0 + b, 0, T0, lane);
+      acc_finish(A, sm, T0 + a, T0 + b, lane);
+    }
+  }
+  __syncthreads();
 
-  setup_post(sm, rdiag, pos, S, R, g, X, x_off, cl, tid, lane, warp);
+  setup_post(sm, rdiag, pos, S, R, g, X, x_off, cl, tid, lane, warp, &s_fail);
+  if (s_fail) {  // the Schur complement's Cholesky broke down (LU, reading Q11)
+    if (tid == 0) glist[atomicAdd(&counts[3], 1)] = cl;
+    return;
+  }
+  setup_x(sm, rdiag, pos, S, R, g, X, x_off, cl, tid, lane, warp);
 }
 
 // ---------------------------------------------------------------------------
