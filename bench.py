@@ -112,7 +112,18 @@ class Clocks:
 
     def mark(self):
         """Start of the timed window (the sampler is started earlier, so its start-up
-        does not fall into the timed steps)."""
+        does not fall into the timed steps).  nvidia-smi's first query (NVML start-up)
+        stalls this process's CUDA calls for tens of ms: wait for its first samples so
+        that the stall falls before the timed steps on short configs."""
+        if self.p is not None:
+            t_end = time.time() + 10.0
+            while time.time() < t_end:
+                try:
+                    if sum(1 for _ in open(self.path)) >= 2:
+                        break
+                except OSError:
+                    pass
+                time.sleep(0.05)
         self.t0 = time.time()
 
     def stop(self):
