@@ -574,7 +574,7 @@ def main():
                     help="strong: one BASELINE config on all GPUs (default); weak: one cfg2-sized "
                          "block per GPU (rbf_workloads.weak)")
     ap.add_argument("--orth", choices=["mgs", "cgs2", "dcgs2"], default=None,
-                    help="GMRES orthogonalisation (default: mgs on 1 GPU, dcgs2 across GPUs)")
+                    help="GMRES orthogonalisation (default: mgs for every GPU count, BJ:5)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # one process per GPU: re-launch this script under torch.distributed.run
