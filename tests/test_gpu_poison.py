@@ -72,6 +72,24 @@ def test_rasm_apply_poisoned(name, wl, rings, kw):
     assert rel(z, ref) <= 1e-10
 
 
+@pytest.mark.parametrize("kern", [1, 2], ids=["two-per-sm", "pipelined"])
+@pytest.mark.parametrize("wl", [W.make_lattice(24), W.make_lattice(37, jitter_frac=0.3, seed=3)],
+                         ids=["ragged24", "jitter37"])
+def test_rasm_apply_poisoned_other_setup_kernels(wl, kern, lib_options):
+    """The two-per-SM and pipelined setup kernels (option setup_kernel) with NaN-filled
+    shared memory, workspace and buffers: every tile, retired row and ring slot they read
+    was written first."""
+    lib_options(setup_kernel=kern)
+    r = np.random.default_rng(7).standard_normal(wl.n)
+    Pc = O.Rasm(wl.xy, wl.sigma, wl.rc, wl.box, wl.cell, 1)
+    ref = Pc.apply(r)
+    Pc.close()
+    with ctx_for(wl) as c:
+        z = to_caller(c, c.rasm_apply(c.to_local(torch.from_numpy(r).cuda())))
+    assert np.all(np.isfinite(z))
+    assert rel(z, ref) <= 1e-10
+
+
 @pytest.mark.parametrize("wl", [W.config(1), W.make_lattice(37, jitter_frac=0.3, seed=3)],
                          ids=["cfg1", "jitter37"])
 def test_matvec_poisoned(wl):
